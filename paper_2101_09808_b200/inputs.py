@@ -1,0 +1,94 @@
+"""Seeded synthetic inputs shared by the tests, the bench and the oracle.
+
+This module holds NO arithmetic of the method; it
+only draws tensors.  Everything is generated on the CPU with a
+``torch.Generator`` so that the oracle, every GPU and every shard see the same
+bits, independent of device.
+
+* ``kind="real"``: In, then Ker, i.i.d. uniform[-1, 1) as
+  ``torch.rand(shape) * 2 - 1`` (fp32), the value distribution BASELINE.json's
+  configs state.
+* ``kind="int"``: the integer twin, values in {-2,...,2}
+  (``torch.randint(-2, 3, shape)`` cast to fp32).  Every value is exact in
+  bf16/tf32 and every partial sum (|.| <= 4*C*R*S < 2^24) is exact in fp32, so
+  all paths must reproduce Eq. 1 bit-for-bit.
+
+Layouts follow PAPER.md:425 (NCHW In/Out, KCRS Ker).  H, W are OUTPUT extents
+(reading R1); In is [N, C, H+R-1, W+S-1].
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+
+@dataclass(frozen=True)
+class Shape:
+    N: int
+    K: int
+    C: int
+    H: int
+    W: int
+    R: int
+    S: int
+
+    @property
+    def Hin(self) -> int:
+        return self.H + self.R - 1
+
+    @property
+    def Win(self) -> int:
+        return self.W + self.S - 1
+
+    @property
+    def in_shape(self):
+        return (self.N, self.C, self.Hin, self.Win)
+
+    @property
+    def ker_shape(self):
+        return (self.K, self.C, self.R, self.S)
+
+    @property
+    def out_shape(self):
+        return (self.N, self.K, self.H, self.W)
+
+    @property
+    def flops(self) -> int:
+        """2*N*K*H*W*C*R*S (BASELINE.json metric; H, W output extents)."""
+        return 2 * self.N * self.K * self.H * self.W * self.C * self.R * self.S
+
+    @property
+    def compulsory_bytes(self) -> int:
+        """fp32 bytes of In + Ker + Out, each touched once."""
+        n_in = self.N * self.C * self.Hin * self.Win
+        n_ker = self.K * self.C * self.R * self.S
+        n_out = self.N * self.K * self.H * self.W
+        return 4 * (n_in + n_ker + n_out)
+
+    def as_tuple(self):
+        return (self.N, self.K, self.C, self.H, self.W, self.R, self.S)
+
+
+# BASELINE.json "configs", in order.  Names are used by tests and bench.
+CONFIGS = {
+    "tiny": Shape(N=1, K=16, C=16, H=8, W=8, R=3, S=3),
+    "r2": Shape(N=1, K=64, C=64, H=56, W=56, R=3, S=3),
+    "pw": Shape(N=1, K=256, C=64, H=56, W=56, R=1, S=1),
+    "det": Shape(N=1, K=64, C=32, H=136, W=136, R=3, S=3),
+    "batched": Shape(N=256, K=256, C=256, H=14, W=14, R=3, S=3),
+}
+
+
+def make_inputs(shape: Shape, seed: int = 0, kind: str = "real"):
+    """Return (In, Ker) as contiguous CPU fp32 tensors, In drawn first."""
+    g = torch.Generator().manual_seed(int(seed))
+    if kind == "real":
+        inp = torch.rand(shape.in_shape, generator=g, dtype=torch.float32) * 2 - 1
+        ker = torch.rand(shape.ker_shape, generator=g, dtype=torch.float32) * 2 - 1
+    elif kind == "int":
+        inp = torch.randint(-2, 3, shape.in_shape, generator=g).to(torch.float32)
+        ker = torch.randint(-2, 3, shape.ker_shape, generator=g).to(torch.float32)
+    else:
+        raise ValueError(f"unknown input kind {kind!r}")
+    return inp.contiguous(), ker.contiguous()

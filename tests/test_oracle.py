@@ -1,0 +1,226 @@
+"""Pins for the CPU oracle, CPU only.
+
+Each test pins ``oracle.conv_eq1`` (Eq. 1, Listing 2 order
+PAPER.md:150-158) to something other than itself: hand-worked values
+(tests/golden), closed forms, an independent algorithm (integral images),
+textbook/library routines (float64 matmul, torch conv2d) and brute force.
+A dropped term, a wrong sign or index, a flipped kernel or a transposed
+operand fails at least one of them (see the docstrings).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2101_09808_b200.inputs import CONFIGS, Shape, make_inputs
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", ["eq1_hand_2x2.json", "eq1_hand_2ch.json"])
+def test_hand_worked_golden(name):
+    """Hand-worked Eq. 1 values (catches kernel flip, c/k transposition)."""
+    g = _golden(name)
+    inp = np.array(g["In"], dtype=np.float32)
+    ker = np.array(g["Ker"], dtype=np.float32)
+    out = oracle.conv_eq1(inp, ker)
+    np.testing.assert_array_equal(out, np.array(g["Out"], dtype=np.float64))
+
+
+def test_p1_identity_1x1():
+    """P1: K=C, R=S=1, Ker=delta_kc => Out == In exactly."""
+    sh = Shape(N=2, K=5, C=5, H=7, W=9, R=1, S=1)
+    inp, _ = make_inputs(sh, seed=3)
+    ker = np.eye(5, dtype=np.float32).reshape(5, 5, 1, 1)
+    out = oracle.conv_eq1(inp.numpy(), ker)
+    np.testing.assert_array_equal(out, inp.numpy().astype(np.float64))
+
+
+@pytest.mark.parametrize("r0,s0", [(r, s) for r in range(2) for s in range(3)])
+def test_p2_shifted_delta(r0, s0):
+    """P2: Ker = delta_kc delta_{r r0} delta_{s s0} => Out[n,k,h,w] =
+    In[n,k,h+r0,w+s0].  R != S and H != W, so a flipped kernel, swapped r/s
+    or h/w, or an off-by-one at the last row/column fails."""
+    sh = Shape(N=2, K=3, C=3, H=5, W=6, R=2, S=3)
+    inp, _ = make_inputs(sh, seed=4)
+    ker = np.zeros(sh.ker_shape, dtype=np.float32)
+    for k in range(3):
+        ker[k, k, r0, s0] = 1.0
+    out = oracle.conv_eq1(inp.numpy(), ker)
+    exp = inp.numpy()[:, :, r0:r0 + sh.H, s0:s0 + sh.W].astype(np.float64)
+    np.testing.assert_array_equal(out, exp)
+
+
+def test_p3_all_ones_input():
+    """P3: In == 1 => Out[n,k,:,:] = sum_{c,r,s} Ker[k,c,r,s] (per-k constant)."""
+    sh = Shape(N=2, K=4, C=3, H=4, W=5, R=3, S=2)
+    _, ker = make_inputs(sh, seed=5)
+    inp = np.ones(sh.in_shape, dtype=np.float32)
+    out = oracle.conv_eq1(inp, ker.numpy())
+    for k in range(sh.K):
+        exp = math.fsum(ker.numpy()[k].astype(np.float64).ravel().tolist())
+        np.testing.assert_allclose(out[:, k], exp, rtol=1e-14, atol=1e-14)
+
+
+def test_p4_all_ones_kernel_box_sum():
+    """P4: Ker == 1 => Out = R x S x C box sum of In, identical for all k.
+    Expected values come from integral images (summed-area tables) -- a
+    different algorithm from the loop nest."""
+    sh = Shape(N=2, K=3, C=4, H=6, W=5, R=3, S=2)
+    inp, _ = make_inputs(sh, seed=6, kind="int")
+    x = inp.numpy().astype(np.float64).sum(axis=1)          # [N, Hin, Win]
+    sat = np.zeros((sh.N, sh.Hin + 1, sh.Win + 1))
+    sat[:, 1:, 1:] = x.cumsum(1).cumsum(2)
+    box = (sat[:, sh.R:, sh.S:] - sat[:, :-sh.R, sh.S:]
+           - sat[:, sh.R:, :-sh.S] + sat[:, :-sh.R, :-sh.S])
+    out = oracle.conv_eq1(inp.numpy(), np.ones(sh.ker_shape, dtype=np.float32))
+    for k in range(sh.K):
+        np.testing.assert_array_equal(out[:, k], box)
+
+
+def test_p5_linearity_exact_on_integers():
+    """P5: conv(a*In1 + b*In2, Ker) = a*conv(In1) + b*conv(In2) and likewise
+    in Ker; exact on small-integer data with small-integer a, b."""
+    sh = Shape(N=2, K=3, C=4, H=5, W=4, R=2, S=3)
+    i1, k1 = make_inputs(sh, seed=7, kind="int")
+    i2, k2 = make_inputs(sh, seed=8, kind="int")
+    a, b = 3.0, -2.0
+    i1, i2, k1, k2 = (t.numpy() for t in (i1, i2, k1, k2))
+    lhs = oracle.conv_eq1((a * i1 + b * i2).astype(np.float32), k1)
+    rhs = a * oracle.conv_eq1(i1, k1) + b * oracle.conv_eq1(i2, k1)
+    np.testing.assert_array_equal(lhs, rhs)
+    lhs = oracle.conv_eq1(i1, (a * k1 + b * k2).astype(np.float32))
+    rhs = a * oracle.conv_eq1(i1, k1) + b * oracle.conv_eq1(i1, k2)
+    np.testing.assert_array_equal(lhs, rhs)
+
+
+def test_p6_integer_twin_exact_integers():
+    """P6: integer-twin inputs give integer outputs with |Out| <= 4*C*R*S,
+    equal to torch's float64 conv2d bit-for-bit."""
+    sh = CONFIGS["tiny"]
+    inp, ker = make_inputs(sh, seed=1, kind="int")
+    out = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert np.all(out == np.round(out))
+    assert np.abs(out).max() <= 4 * sh.C * sh.R * sh.S
+    ref = torch.nn.functional.conv2d(inp.double(), ker.double()).numpy()
+    np.testing.assert_array_equal(out, ref)
+
+
+def test_p7_pointwise_is_a_gemm():
+    """P7: R=S=1 => Out[n] = Ker[:,:,0,0] @ In[n].reshape(C, H*W) (float64
+    matmul, a textbook routine; pw config shape)."""
+    sh = Shape(N=2, K=32, C=16, H=9, W=11, R=1, S=1)
+    inp, ker = make_inputs(sh, seed=9)
+    out = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    k2 = ker.numpy()[:, :, 0, 0].astype(np.float64)
+    for n in range(sh.N):
+        exp = k2 @ inp.numpy()[n].reshape(sh.C, -1).astype(np.float64)
+        np.testing.assert_allclose(out[n].reshape(sh.K, -1), exp, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["tiny", "r2"])
+def test_p8_torch_conv2d_float64(name):
+    """P8: torch.nn.functional.conv2d (cross-correlation) in float64 on the
+    CPU, test-only library cross-check."""
+    sh = CONFIGS[name]
+    inp, ker = make_inputs(sh, seed=0)
+    out = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    ref = torch.nn.functional.conv2d(inp.double(), ker.double()).numpy()
+    err = np.abs(out - ref).max()
+    assert err <= 1e-12 * max(1.0, np.abs(ref).max()), err
+
+
+def test_p8_odd_shape():
+    sh = Shape(N=2, K=5, C=3, H=7, W=9, R=3, S=2)
+    inp, ker = make_inputs(sh, seed=2)
+    out = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    ref = torch.nn.functional.conv2d(inp.double(), ker.double()).numpy()
+    np.testing.assert_allclose(out, ref, rtol=0, atol=1e-13)
+
+
+def test_p9_brute_force_points():
+    """P9: random output points equal the correctly rounded (fsum) sum of
+    their C*R*S exact products, within the double-summation bound."""
+    sh = CONFIGS["r2"]
+    inp, ker = make_inputs(sh, seed=0)
+    x, w = inp.numpy(), ker.numpy()
+    out = oracle.conv_eq1(x, w)
+    rng = np.random.default_rng(0)
+    crs = sh.C * sh.R * sh.S
+    for _ in range(200):
+        n, k = rng.integers(sh.N), rng.integers(sh.K)
+        h, ww = rng.integers(sh.H), rng.integers(sh.W)
+        exact = oracle.conv_eq1_point(x, w, n, k, h, ww)
+        absum = float(np.abs(x[n, :, h:h + sh.R, ww:ww + sh.S].astype(np.float64)
+                             * w[k].astype(np.float64)).sum())
+        assert abs(out[n, k, h, ww] - exact) <= crs * 2.0 ** -53 * absum + 1e-300
+
+
+def test_point_matches_closed_form():
+    """conv_eq1_point on the P2 shifted-delta kernel returns In exactly."""
+    sh = Shape(N=1, K=2, C=2, H=3, W=4, R=2, S=3)
+    inp, _ = make_inputs(sh, seed=11)
+    ker = np.zeros(sh.ker_shape, dtype=np.float32)
+    ker[1, 0, 1, 2] = 1.0
+    x = inp.numpy()
+    for h in range(sh.H):
+        for w in range(sh.W):
+            assert oracle.conv_eq1_point(x, ker, 0, 1, h, w) == float(x[0, 0, h + 1, w + 2])
+
+
+def test_thread_count_invariance():
+    """Planes are summed serially, so 1 and many threads agree bit-for-bit."""
+    sh = Shape(N=2, K=6, C=5, H=7, W=6, R=3, S=3)
+    inp, ker = make_inputs(sh, seed=12)
+    a = oracle.conv_eq1(inp.numpy(), ker.numpy(), nthreads=1)
+    b = oracle.conv_eq1(inp.numpy(), ker.numpy(), nthreads=8)
+    assert np.array_equal(a, b)
+
+
+def test_rejects_bad_shapes():
+    with pytest.raises(ValueError):
+        oracle.conv_eq1(np.zeros((1, 2, 3, 3), np.float32), np.zeros((1, 3, 1, 1), np.float32))
+    with pytest.raises(ValueError):
+        oracle.conv_eq1(np.zeros((1, 1, 2, 2), np.float32), np.zeros((1, 1, 3, 3), np.float32))
+
+
+# ---- rounding helpers (reading R5) --------------------------------
+
+def test_bf16_rne_matches_torch_cast():
+    """round_bf16_rne == torch's CPU fp32->bf16 cast (round-to-nearest-even)."""
+    g = torch.Generator().manual_seed(0)
+    x = torch.cat([torch.rand(100000, generator=g) * 2 - 1,
+                   torch.randn(100000, generator=g) * 1e3,
+                   torch.tensor([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -(1.0 + 2 ** -8), 0.0, -0.0])])
+    ref = x.to(torch.bfloat16).to(torch.float32).numpy()
+    got = oracle.round_bf16_rne(x.numpy())
+    np.testing.assert_array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+def test_tf32_rna_ties_and_bound():
+    """TF32 keeps 10 mantissa bits; ulp(1) = 2^-10.  Ties round away from 0."""
+    f = np.float32
+    cases = {
+        1.0 + 2 ** -11: 1.0 + 2 ** -10,            # exact tie -> away from zero
+        -(1.0 + 2 ** -11): -(1.0 + 2 ** -10),
+        1.0 + 2 ** -12: 1.0,                       # below half ulp -> down
+        1.0 + 3 * 2 ** -11: 1.0 + 2 * 2 ** -10,    # tie at odd -> away (up)
+        1.0 + 2 ** -10: 1.0 + 2 ** -10,            # representable -> unchanged
+    }
+    for x, exp in cases.items():
+        assert oracle.round_tf32_rna(np.array([x], f))[0] == f(exp)
+    g = np.random.default_rng(1)
+    x = (g.random(100000, dtype=np.float32) * 2 - 1) * f(37.0)
+    r = oracle.round_tf32_rna(x)
+    assert np.all((r.view(np.uint32) & 0x1FFF) == 0)
+    ulp = np.ldexp(1.0, np.frexp(np.abs(x).astype(np.float64))[1] - 11)
+    assert np.all(np.abs(r.astype(np.float64) - x) <= ulp / 2)
