@@ -1,0 +1,168 @@
+/*
+ * conv.h -- C ABI of the B200-native direct-convolution library (libconv.so).
+ *
+ * Operation (Sec. 1, Eq. 1 of Li et al., ASPLOS'21):
+ *
+ *     Out[n,k,h,w] = sum_{c<C, r<R, s<S} In[n,c,h+r,w+s] * Ker[k,c,r,s]
+ *
+ * stride 1, no padding, fp32 tensors, In/Out NCHW and Ker KCRS
+ * (Sec. 9: "All input and output tensors were stored in NCHW
+ * layout and all kernel tensors were stored in KCRS layout").  H and W are the
+ * OUTPUT extents (the loop extents N_h, N_w of Listing 2);
+ * the input is (H+R-1) x (W+S-1) (Sec. 3.1).  conv_run
+ * OVERWRITES Out (Eq. 1 is "=", reading R4).  Internal layout
+ * transforms are part of every conv_run, as the paper counts them
+ * (PAPER.md:371).
+ *
+ * Conventions (all functions):
+ *   - Plain C types only.  Device pointers are CUDA device pointers on the
+ *     device that was current when the plan was created.  `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every conv_status-returning call returns CONV_OK (0) or an error code;
+ *     conv_last_error() then returns a thread-local, NUL-terminated message
+ *     (static storage, valid until the next failing call on that thread).
+ *   - Error classes follow SPEC.md:552's exit-code classes: 1 = invalid
+ *     argument / usage, 2 = infeasible request; 3, 4 add CUDA and device
+ *     failures.  There is no CPU fallback: on a machine without an sm_100
+ *     device, conv_plan_create fails with CONV_ERR_UNSUPPORTED_DEVICE.
+ *   - Thread safety: a plan is immutable after create / set_path / set_tile.
+ *     conv_run may be called concurrently on one plan from several host
+ *     threads / streams if each call has its own workspace.
+ */
+#ifndef CONV_H_
+#define CONV_H_
+
+#include <stddef.h>
+
+#if defined(__GNUC__)
+#define CONV_API __attribute__((visibility("default")))
+#else
+#define CONV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct conv_plan conv_plan; /* opaque, owned by the library */
+
+typedef enum {
+    CONV_OK = 0,
+    CONV_ERR_INVALID_ARGUMENT = 1,  /* extent < 1, size overflow, NULL/misaligned pointer */
+    CONV_ERR_INFEASIBLE = 2,        /* no tile fits the hardware limits for the requested path */
+    CONV_ERR_CUDA = 3,              /* a CUDA runtime/driver call or launch failed */
+    CONV_ERR_UNSUPPORTED_DEVICE = 4 /* no device, or the current device is not sm_100 */
+} conv_status;
+
+typedef enum {
+    CONV_PATH_AUTO = 0,      /* selector picks among the three below */
+    CONV_PATH_FP32_SIMT = 1, /* FP32 FFMA direct convolution on native NCHW (no repack) */
+    CONV_PATH_TF32 = 2,      /* tcgen05 implicit GEMM, inputs rounded to TF32 (RNA), fp32 accumulate */
+    CONV_PATH_BF16 = 3       /* tcgen05 implicit GEMM, inputs rounded to BF16 (RNE), fp32 accumulate */
+} conv_path;
+
+/* ---- plans ------------------------------------------------------------- */
+
+/* Create a plan for Eq. 1 with batch N, output channels K, input channels C,
+ * OUTPUT extents H x W and kernel R x S (In is N x C x (H+R-1) x (W+S-1)).
+ * Binds to the current CUDA device, queries its attributes and runs the tile
+ * selector (Sec. 5 min-max,
+ * PAPER.md:383-419 Alg. 1).  Returns NULL on error (conv_last_error()):
+ * INVALID_ARGUMENT if an extent is < 1 ("all extents >= 1") or a
+ * tensor has >= 2^31 elements; UNSUPPORTED_DEVICE without an sm_100 device. */
+CONV_API conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R, int S);
+
+/* Force a path (default AUTO) and re-run the selector for it.
+ * INFEASIBLE if no candidate of that path fits (e.g. R or S > 128 on the
+ * tensor paths: TMA im2col offsets are limited to [-128, 127]). */
+CONV_API conv_status conv_plan_set_path(conv_plan* plan, conv_path path);
+
+/* Force a tiling (tests / the selector-validation study).  `spec` is a
+ * comma-separated key=value list; keys for the tensor paths: bn, stages;
+ * for the SIMT path: tk, tw, kg, pw, tn, th, bc.  Unspecified keys keep the
+ * selector's choice.  NULL or "" restores the selector's choice.
+ * INVALID_ARGUMENT on a malformed spec, INFEASIBLE if the tile exceeds
+ * SMEM/TMEM/register capacity (Eq. 4, per level). */
+CONV_API conv_status conv_plan_set_tile(conv_plan* plan, const char* spec);
+
+/* Bytes of device workspace conv_run needs (NHWC / KRSC repack buffers of the
+ * tensor paths; 0 for the SIMT path).  Caller allocates, 256-B aligned. */
+CONV_API size_t conv_plan_workspace_bytes(const conv_plan* plan);
+
+/* Number of kernels one conv_run launches (repacks + main). */
+CONV_API int conv_plan_num_kernels(const conv_plan* plan);
+
+/* Path the plan will run (never AUTO after create). */
+CONV_API conv_path conv_plan_path(const conv_plan* plan);
+
+/* Write a JSON description (path, tiles, modeled data volume per level and
+ * bandwidth-scaled costs, roofline) into buf (NUL-terminated, truncated to
+ * cap).  Returns the number of bytes needed excluding the NUL, or -1. */
+CONV_API int conv_plan_describe(const conv_plan* plan, char* buf, size_t cap);
+
+/* NULL-safe. */
+CONV_API void conv_plan_destroy(conv_plan* plan);
+
+/* ---- execution ---------------------------------------------------------- */
+
+/* Out = Eq. 1 (In, Ker), asynchronously on `stream`.
+ *   in:  N*C*(H+R-1)*(W+S-1) fp32, NCHW, contiguous, 16-B aligned
+ *   ker: K*C*R*S fp32, KCRS, contiguous, 16-B aligned
+ *   out: N*K*H*W fp32, NCHW, contiguous, 16-B aligned; overwritten; must not
+ *        alias in, ker or workspace
+ *   workspace: >= conv_plan_workspace_bytes(plan) bytes, 256-B aligned
+ *        (may be NULL when that is 0).
+ * Returns INVALID_ARGUMENT on NULL/misaligned pointers, CUDA on a launch
+ * error.  Asynchronous faults surface at the caller's next synchronisation. */
+CONV_API conv_status conv_run(const conv_plan* plan, const float* in, const float* ker,
+                     float* out, void* workspace, void* stream);
+
+/* As conv_run, and records caller-created cudaEvent_t handles (passed as
+ * void*) on `stream` around each kernel: events[0] before the first kernel,
+ * events[i] after kernel i (i = 1..num_kernels).  n_events must be
+ * conv_plan_num_kernels(plan) + 1.  Used by bench.py to time the dominant
+ * kernel on the stream it is launched on. */
+CONV_API conv_status conv_run_events(const conv_plan* plan, const float* in, const float* ker,
+                            float* out, void* workspace, void* stream,
+                            void* const* events, int n_events);
+
+/* Device bytes conv_run_host needs: In + Ker + Out device copies + workspace. */
+CONV_API size_t conv_plan_host_run_bytes(const conv_plan* plan);
+
+/* End-to-end call with HOST buffers (pinned for overlap; pageable works but
+ * synchronises): copies in/ker host->device into `device_buffer`
+ * (>= conv_plan_host_run_bytes, 256-B aligned), runs conv_run, copies Out
+ * device->host, all on `stream` with one cudaMemcpyAsync per tensor.  The
+ * call is asynchronous: out_host is valid after the stream synchronises. */
+CONV_API conv_status conv_run_host(const conv_plan* plan, const float* in_host, const float* ker_host,
+                          float* out_host, void* device_buffer, void* stream);
+
+/* Thread-local message for the last failing call on this thread ("" if none). */
+CONV_API const char* conv_last_error(void);
+
+/* Library version string, e.g. "0.1.0 sm_100a". */
+CONV_API const char* conv_version(void);
+
+/* ---- the tile selector's data-movement model (host only, no device) ------ */
+
+/* Sec. 3.2's data volume for single-level tiling of Eq. 1
+ * with tile-loop permutation perm[0..6] (outermost first; iterator ids
+ * n=0,k=1,c=2,r=3,s=4,h=5,w=6), problem extents Nx[7] and tile sizes T[7]
+ * (same id order; 1 <= T <= N; trip counts ceil(N/T)).  Writes the In, Ker,
+ * Out volumes (words) to dv[0..2] and returns their sum; Out carries the
+ * paper's factor 2 (read + write).  Returns -1 on bad input. */
+CONV_API double conv_model_dv(const int perm[7], const double Nx[7], const double T[7], double dv[3]);
+
+/* Sec. 2.2's matmul model (Eq. 3): C[i][j] += A[i][k]*B[k][j]
+ * tiled by T[3] with tile-loop permutation perm[0..2] (ids i=0,j=1,k=2).
+ * Returns the total data volume (C counted twice), -1 on bad input. */
+CONV_API double conv_model_dv_matmul(const int perm[3], const double Nx[3], const double T[3]);
+
+/* Eq. 4 left-hand side: the tile footprint of In + Ker + Out. */
+CONV_API double conv_model_footprint(const double T[7]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CONV_H_ */

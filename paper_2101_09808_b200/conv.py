@@ -1,0 +1,275 @@
+"""Python binding of libconv.so (include/conv.h) -- argument marshalling only.
+
+Every step of a convolution runs in the library's sm_100a kernels; this module
+passes tensor pointers, sizes and the caller's CUDA stream through ctypes.
+PyTorch is used only for device memory and streams.  There is no CPU
+fallback: if ``libconv.so`` is missing or no sm_100 device is present the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import threading
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libconv.so")
+
+CONV_OK = 0
+CONV_ERR_INVALID_ARGUMENT = 1
+CONV_ERR_INFEASIBLE = 2
+CONV_ERR_CUDA = 3
+CONV_ERR_UNSUPPORTED_DEVICE = 4
+
+PATHS = {"auto": 0, "fp32_simt": 1, "tf32": 2, "bf16": 3}
+PATH_NAMES = {v: k for k, v in PATHS.items()}
+
+# Every symbol include/conv.h declares (tests check the library exports them).
+EXPORTED = (
+    "conv_plan_create", "conv_plan_set_path", "conv_plan_set_tile", "conv_plan_workspace_bytes",
+    "conv_plan_num_kernels", "conv_plan_path", "conv_plan_describe", "conv_plan_destroy",
+    "conv_run", "conv_run_events", "conv_plan_host_run_bytes", "conv_run_host",
+    "conv_last_error", "conv_version", "conv_model_dv", "conv_model_dv_matmul",
+    "conv_model_footprint",
+)
+
+
+class ConvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[conv status {status}] {msg}")
+        self.status = status
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libconv.so (raises if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(
+                f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        vp, sz, i, d = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_double
+        sig = {
+            "conv_plan_create": (vp, [i] * 7),
+            "conv_plan_set_path": (i, [vp, i]),
+            "conv_plan_set_tile": (i, [vp, ctypes.c_char_p]),
+            "conv_plan_workspace_bytes": (sz, [vp]),
+            "conv_plan_num_kernels": (i, [vp]),
+            "conv_plan_path": (i, [vp]),
+            "conv_plan_describe": (i, [vp, ctypes.c_char_p, sz]),
+            "conv_plan_destroy": (None, [vp]),
+            "conv_run": (i, [vp, vp, vp, vp, vp, vp]),
+            "conv_run_events": (i, [vp, vp, vp, vp, vp, vp, ctypes.POINTER(vp), i]),
+            "conv_plan_host_run_bytes": (sz, [vp]),
+            "conv_run_host": (i, [vp, vp, vp, vp, vp, vp]),
+            "conv_last_error": (ctypes.c_char_p, []),
+            "conv_version": (ctypes.c_char_p, []),
+            "conv_model_dv": (d, [ctypes.POINTER(i), ctypes.POINTER(d), ctypes.POINTER(d), ctypes.POINTER(d)]),
+            "conv_model_dv_matmul": (d, [ctypes.POINTER(i), ctypes.POINTER(d), ctypes.POINTER(d)]),
+            "conv_model_footprint": (d, [ctypes.POINTER(d)]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    return load_library().conv_last_error().decode()
+
+
+def version() -> str:
+    return load_library().conv_version().decode()
+
+
+def _check(status: int):
+    if status != CONV_OK:
+        raise ConvError(status, last_error())
+
+
+def _stream_handle(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class ConvPlan:
+    """A plan for Eq. 1 with OUTPUT extents H x W."""
+
+    def __init__(self, N: int, K: int, C: int, H: int, W: int, R: int, S: int,
+                 path: str = "auto", tile: Optional[str] = None):
+        lib = load_library()
+        self._lib = lib
+        self.shape = (N, K, C, H, W, R, S)
+        h = lib.conv_plan_create(N, K, C, H, W, R, S)
+        if not h:
+            raise ConvError(CONV_ERR_INVALID_ARGUMENT, last_error())
+        self._h = ctypes.c_void_p(h)
+        if path != "auto":
+            self.set_path(path)
+        if tile:
+            self.set_tile(tile)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.conv_plan_destroy(h)
+            self._h = None
+
+    def set_path(self, path: str):
+        if path not in PATHS:
+            raise ValueError(f"unknown path {path!r}")
+        _check(self._lib.conv_plan_set_path(self._h, PATHS[path]))
+
+    def set_tile(self, spec: Optional[str]):
+        _check(self._lib.conv_plan_set_tile(self._h, (spec or "").encode()))
+
+    @property
+    def path(self) -> str:
+        return PATH_NAMES[self._lib.conv_plan_path(self._h)]
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(self._lib.conv_plan_workspace_bytes(self._h))
+
+    @property
+    def num_kernels(self) -> int:
+        return int(self._lib.conv_plan_num_kernels(self._h))
+
+    @property
+    def host_run_bytes(self) -> int:
+        return int(self._lib.conv_plan_host_run_bytes(self._h))
+
+    def describe(self) -> dict:
+        n = self._lib.conv_plan_describe(self._h, None, 0)
+        buf = ctypes.create_string_buffer(n + 1)
+        self._lib.conv_plan_describe(self._h, buf, n + 1)
+        return json.loads(buf.value.decode())
+
+    # -- execution -----------------------------------------------------------
+    def _shapes(self):
+        N, K, C, H, W, R, S = self.shape
+        return (N, C, H + R - 1, W + S - 1), (K, C, R, S), (N, K, H, W)
+
+    def _check_tensors(self, inp, ker, out):
+        import torch
+        si, sk, so = self._shapes()
+        for t, s, name in ((inp, si, "in"), (ker, sk, "ker"), (out, so, "out")):
+            if not isinstance(t, torch.Tensor) or not t.is_cuda:
+                raise ValueError(f"{name} must be a CUDA tensor")
+            if t.dtype != torch.float32 or tuple(t.shape) != s or not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous float32 of shape {s}, got {t.dtype} {tuple(t.shape)}")
+
+    def new_workspace(self, device=None):
+        import torch
+        n = self.workspace_bytes
+        return torch.empty(max(n, 1), dtype=torch.uint8, device=device or "cuda")
+
+    def new_output(self, device=None):
+        import torch
+        return torch.empty(self._shapes()[2], dtype=torch.float32, device=device or "cuda")
+
+    def run(self, inp, ker, out=None, workspace=None, stream=None):
+        """Out = Eq. 1 (In, Ker), asynchronous on ``stream`` (default: torch's
+        current stream).  Returns ``out``."""
+        if out is None:
+            out = self.new_output(inp.device)
+        self._check_tensors(inp, ker, out)
+        if workspace is None and self.workspace_bytes:
+            workspace = self.new_workspace(inp.device)
+        ws = workspace.data_ptr() if workspace is not None and self.workspace_bytes else None
+        _check(self._lib.conv_run(self._h, inp.data_ptr(), ker.data_ptr(), out.data_ptr(), ws,
+                                  _stream_handle(stream)))
+        return out
+
+    def run_events(self, inp, ker, out, workspace, events: Sequence, stream=None):
+        """conv_run recording ``events`` (torch.cuda.Event, enable_timing) around
+        each kernel on ``stream``."""
+        self._check_tensors(inp, ker, out)
+        n = len(events)
+        arr = (ctypes.c_void_p * n)(*[e.cuda_event for e in events])
+        ws = workspace.data_ptr() if workspace is not None and self.workspace_bytes else None
+        _check(self._lib.conv_run_events(self._h, inp.data_ptr(), ker.data_ptr(), out.data_ptr(), ws,
+                                         _stream_handle(stream), arr, n))
+
+    def run_host(self, in_host, ker_host, out_host, device_buffer, stream=None):
+        """End-to-end call with (pinned) host tensors: H2D, conv, D2H on one
+        stream inside the library.  Asynchronous."""
+        import torch
+        si, sk, so = self._shapes()
+        for t, s, name in ((in_host, si, "in"), (ker_host, sk, "ker"), (out_host, so, "out")):
+            if t.is_cuda or t.dtype != torch.float32 or tuple(t.shape) != s or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float32 host tensor of shape {s}")
+        if device_buffer.numel() * device_buffer.element_size() < self.host_run_bytes:
+            raise ValueError("device_buffer too small")
+        _check(self._lib.conv_run_host(self._h, in_host.data_ptr(), ker_host.data_ptr(),
+                                       out_host.data_ptr(), device_buffer.data_ptr(),
+                                       _stream_handle(stream)))
+
+
+_plan_cache = {}
+
+
+def conv2d(inp, ker, path: str = "auto", out=None, stream=None):
+    """Eq. 1 on CUDA tensors (In NCHW [N,C,H+R-1,W+S-1], Ker KCRS) with a
+    cached plan per (shape, path, device)."""
+    N, C, Hin, Win = inp.shape
+    K, C2, R, S = ker.shape
+    if C2 != C:
+        raise ValueError("channel mismatch between In and Ker")
+    key = (N, K, C, Hin - R + 1, Win - S + 1, R, S, path, inp.device.index)
+    plan = _plan_cache.get(key)
+    if plan is None:
+        plan = ConvPlan(*key[:7], path=path)
+        _plan_cache[key] = plan
+    return plan.run(inp, ker, out=out, stream=stream)
+
+
+# -- the selector's data-movement model (host only; no device needed) ---------
+ITER = {"n": 0, "k": 1, "c": 2, "r": 3, "s": 4, "h": 5, "w": 6}
+
+
+def model_dv(perm: Sequence[str], Nx: dict, T: dict):
+    """Sec. 3.2 data volume for tile-loop order ``perm``
+    (outermost first, iterator names n,k,c,r,s,h,w).  Returns (In, Ker, Out)."""
+    lib = load_library()
+    p = (ctypes.c_int * 7)(*[ITER[x] for x in perm])
+    order = ["n", "k", "c", "r", "s", "h", "w"]
+    n = (ctypes.c_double * 7)(*[float(Nx[x]) for x in order])
+    t = (ctypes.c_double * 7)(*[float(T[x]) for x in order])
+    dv = (ctypes.c_double * 3)()
+    tot = lib.conv_model_dv(p, n, t, dv)
+    if tot < 0:
+        raise ValueError("invalid model arguments")
+    return dv[0], dv[1], dv[2]
+
+
+def model_dv_matmul(perm: Sequence[str], Nx: dict, T: dict) -> float:
+    """Sec. 2.2 matmul model (Eq. 3); iterators i, j, k."""
+    lib = load_library()
+    ids = {"i": 0, "j": 1, "k": 2}
+    p = (ctypes.c_int * 3)(*[ids[x] for x in perm])
+    n = (ctypes.c_double * 3)(*[float(Nx[x]) for x in "ijk"])
+    t = (ctypes.c_double * 3)(*[float(T[x]) for x in "ijk"])
+    tot = lib.conv_model_dv_matmul(p, n, t)
+    if tot < 0:
+        raise ValueError("invalid model arguments")
+    return tot
+
+
+def model_footprint(T: dict) -> float:
+    """Eq. 4 left-hand side."""
+    lib = load_library()
+    t = (ctypes.c_double * 7)(*[float(T[x]) for x in ["n", "k", "c", "r", "s", "h", "w"]])
+    return lib.conv_model_footprint(t)

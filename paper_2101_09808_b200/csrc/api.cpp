@@ -1,0 +1,382 @@
+// api.cpp -- the C ABI (include/conv.h): plan objects, argument validation,
+// path/tile selection, describe JSON, and run dispatch.  No computation of
+// Eq. 1 happens on the host; every step of conv_run is a kernel of this
+// library, and there is no CPU fallback.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+
+#include "../../include/conv.h"
+#include "internal.h"
+#include "model.h"
+
+namespace conv {
+PFN_encodeTiled g_encode_tiled = nullptr;
+PFN_encodeIm2col g_encode_im2col = nullptr;
+
+bool driver_init(std::string& err) {
+    static std::once_flag once;
+    static std::string init_err;
+    std::call_once(once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn) {
+            init_err = "cannot resolve cuTensorMapEncodeTiled";
+            return;
+        }
+        g_encode_tiled = reinterpret_cast<PFN_encodeTiled>(fn);
+        fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn) {
+            init_err = "cannot resolve cuTensorMapEncodeIm2col";
+            return;
+        }
+        g_encode_im2col = reinterpret_cast<PFN_encodeIm2col>(fn);
+    });
+    err = init_err;
+    return init_err.empty();
+}
+}  // namespace conv
+
+using namespace conv;
+
+struct conv_plan {
+    Problem pb;
+    Device dev;
+    conv_path requested = CONV_PATH_AUTO;
+    conv_path path = CONV_PATH_AUTO;
+    TcTile tc;
+    TcLayout tcl;
+    SimtTile simt;
+    ModelResult model;
+    // forced tile (conv_plan_set_tile)
+    int force_bn = 0, force_stages = 0;
+    SimtTile force_simt;
+    unsigned force_simt_mask = 0;
+};
+
+static thread_local std::string g_err;
+
+static conv_status fail(conv_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+extern "C" const char* conv_last_error(void) { return g_err.c_str(); }
+extern "C" const char* conv_version(void) { return "0.1.0 sm_100a"; }
+
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+static size_t ws_bytes(const conv_plan* p) {
+    if (p->path == CONV_PATH_FP32_SIMT) return align256(simt_ws_bytes(p->pb, p->simt));
+    return align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes);
+}
+
+// Re-run the selector for the requested path (Alg. 1:
+// every candidate evaluated, minimum modeled cost wins).
+static conv_status select(conv_plan* p) {
+    std::string why;
+    const Problem& pb = p->pb;
+    TcTile tt;
+    ModelResult rt;
+    SimtTile st;
+    ModelResult rs;
+    const SimtTile* fs = p->force_simt_mask ? &p->force_simt : nullptr;
+    switch (p->requested) {
+        case CONV_PATH_FP32_SIMT:
+            if (!select_simt(pb, p->dev, st, rs, fs, p->force_simt_mask, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            p->simt = st; p->model = rs; p->path = CONV_PATH_FP32_SIMT;
+            break;
+        case CONV_PATH_TF32:
+        case CONV_PATH_BF16: {
+            const bool bf16 = p->requested == CONV_PATH_BF16;
+            if (!select_tc(pb, p->dev, bf16, tt, rt, p->force_bn, p->force_stages, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            p->tc = tt; p->model = rt; p->path = p->requested; p->tcl = tc_layout(pb, bf16);
+            break;
+        }
+        case CONV_PATH_AUTO:
+        default: {
+            // AUTO keeps fp32 inputs or TF32 products (the precision of the
+            // paper's fp32 method); BF16 only when requested.
+            const bool ok_s = select_simt(pb, p->dev, st, rs, fs, p->force_simt_mask, why);
+            const bool ok_t = select_tc(pb, p->dev, false, tt, rt, p->force_bn, p->force_stages, why);
+            if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            if (ok_t && (!ok_s || rt.model_us < rs.model_us)) {
+                p->tc = tt; p->model = rt; p->path = CONV_PATH_TF32; p->tcl = tc_layout(pb, false);
+            } else {
+                p->simt = st; p->model = rs; p->path = CONV_PATH_FP32_SIMT;
+            }
+        }
+    }
+    return CONV_OK;
+}
+
+extern "C" conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R, int S) {
+    if (N < 1 || K < 1 || C < 1 || H < 1 || W < 1 || R < 1 || S < 1) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "extent must be >= 1 (N=%d K=%d C=%d H=%d W=%d R=%d S=%d)", N, K, C, H, W, R, S);
+        return nullptr;
+    }
+    Problem pb{N, K, C, H, W, R, S};
+    const int64_t lim = (int64_t)1 << 31;
+    if (pb.in_elems() >= lim || pb.ker_elems() >= lim || pb.out_elems() >= lim || pb.Hin() >= lim || pb.Win() >= lim) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "tensor with >= 2^31 elements is not supported");
+        return nullptr;
+    }
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(CONV_ERR_UNSUPPORTED_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+        return nullptr;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+        fail(CONV_ERR_UNSUPPORTED_DEVICE, "cudaGetDeviceProperties failed");
+        return nullptr;
+    }
+    if (prop.major != 10 || prop.minor != 0) {
+        fail(CONV_ERR_UNSUPPORTED_DEVICE, "device %s is sm_%d%d; this library is built for sm_100a only",
+             prop.name, prop.major, prop.minor);
+        return nullptr;
+    }
+    std::string err;
+    if (!driver_init(err)) {
+        fail(CONV_ERR_UNSUPPORTED_DEVICE, "%s", err.c_str());
+        return nullptr;
+    }
+    conv_plan* p = new conv_plan();
+    p->pb = pb;
+    p->dev.ordinal = dev;
+    p->dev.sms = prop.multiProcessorCount;
+    p->dev.cc_major = prop.major;
+    p->dev.cc_minor = prop.minor;
+    p->dev.smem_optin = prop.sharedMemPerBlockOptin;
+    p->dev.l2_bytes = prop.l2CacheSize;
+    if (select(p) != CONV_OK) {
+        delete p;
+        return nullptr;
+    }
+    return p;
+}
+
+extern "C" conv_status conv_plan_set_path(conv_plan* p, conv_path path) {
+    if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (path < CONV_PATH_AUTO || path > CONV_PATH_BF16) return fail(CONV_ERR_INVALID_ARGUMENT, "unknown path %d", (int)path);
+    const conv_path old = p->requested;
+    p->requested = path;
+    conv_status s = select(p);
+    if (s != CONV_OK) {
+        p->requested = old;
+        select(p);
+    }
+    return s;
+}
+
+extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
+    if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
+    int fbn = 0, fst = 0;
+    SimtTile fs;
+    unsigned mask = 0;
+    if (spec && *spec) {
+        std::string s(spec);
+        size_t pos = 0;
+        while (pos < s.size()) {
+            size_t comma = s.find(',', pos);
+            if (comma == std::string::npos) comma = s.size();
+            std::string kv = s.substr(pos, comma - pos);
+            pos = comma + 1;
+            if (kv.empty()) continue;
+            size_t eq = kv.find('=');
+            if (eq == std::string::npos) return fail(CONV_ERR_INVALID_ARGUMENT, "malformed tile spec item '%s'", kv.c_str());
+            std::string key = kv.substr(0, eq);
+            char* end = nullptr;
+            long v = strtol(kv.c_str() + eq + 1, &end, 10);
+            if (!end || *end || v < 1 || v > 4096) return fail(CONV_ERR_INVALID_ARGUMENT, "bad value in '%s'", kv.c_str());
+            if (key == "bn") fbn = (int)v;
+            else if (key == "stages") fst = (int)v;
+            else if (key == "tk") { fs.tk = (int)v; mask |= 1; }
+            else if (key == "tw") { fs.tw = (int)v; mask |= 2; }
+            else if (key == "kg") { fs.kg = (int)v; mask |= 4; }
+            else if (key == "pw") { fs.pw = (int)v; mask |= 8; }
+            else if (key == "tn") { fs.tn = (int)v; mask |= 16; }
+            else if (key == "th") { fs.th = (int)v; mask |= 32; }
+            else if (key == "bc") { fs.bc = (int)v; mask |= 64; }
+            else return fail(CONV_ERR_INVALID_ARGUMENT, "unknown tile key '%s'", key.c_str());
+        }
+        if (fbn && (fbn % 32 != 0 || fbn > 256)) return fail(CONV_ERR_INFEASIBLE, "bn must be a multiple of 32 in [32, 256]");
+    }
+    const int obn = p->force_bn, ost = p->force_stages;
+    const SimtTile ofs = p->force_simt;
+    const unsigned omask = p->force_simt_mask;
+    p->force_bn = fbn; p->force_stages = fst; p->force_simt = fs; p->force_simt_mask = mask;
+    conv_status s = select(p);
+    if (s != CONV_OK) {
+        p->force_bn = obn; p->force_stages = ost; p->force_simt = ofs; p->force_simt_mask = omask;
+        select(p);
+    }
+    return s;
+}
+
+extern "C" size_t conv_plan_workspace_bytes(const conv_plan* p) { return p ? ws_bytes(p) : 0; }
+
+extern "C" int conv_plan_num_kernels(const conv_plan* p) {
+    if (!p) return -1;
+    return p->path == CONV_PATH_FP32_SIMT ? 2 : 3;
+}
+
+extern "C" conv_path conv_plan_path(const conv_plan* p) { return p ? p->path : CONV_PATH_AUTO; }
+
+extern "C" void conv_plan_destroy(conv_plan* p) { delete p; }
+
+static const char* path_name(conv_path p) {
+    switch (p) {
+        case CONV_PATH_FP32_SIMT: return "fp32_simt";
+        case CONV_PATH_TF32: return "tf32";
+        case CONV_PATH_BF16: return "bf16";
+        default: return "auto";
+    }
+}
+
+extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
+    if (!p) return -1;
+    const Problem& pb = p->pb;
+    const ModelResult& m = p->model;
+    const double peak = p->path == CONV_PATH_FP32_SIMT ? p->dev.peak_fp32
+                        : (p->path == CONV_PATH_BF16 ? p->dev.peak_bf16 : p->dev.peak_tf32);
+    const double comp_bytes = 4.0 * (pb.in_elems() + pb.ker_elems() + pb.out_elems());
+    const double roof_us = std::max(pb.flops() / peak, comp_bytes / p->dev.bw_hbm) * 1e6;
+    std::string tile;
+    char t[256];
+    if (p->path == CONV_PATH_FP32_SIMT) {
+        snprintf(t, sizeof t, "{\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"threads\":%d}",
+                 p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
+                 32 * p->simt.kg * p->simt.pw);
+    } else {
+        snprintf(t, sizeof t, "{\"bm\":128,\"bn\":%d,\"stages\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
+                 p->tc.bn, p->tc.stages, p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
+    }
+    tile = t;
+    char out[2048];
+    int n = snprintf(out, sizeof out,
+        "{\"problem\":{\"N\":%d,\"K\":%d,\"C\":%d,\"H\":%d,\"W\":%d,\"R\":%d,\"S\":%d},"
+        "\"path\":\"%s\",\"tile\":%s,\"workspace_bytes\":%zu,\"kernels\":%d,"
+        "\"model\":{\"tiles\":%ld,\"ctas\":%ld,\"wave_eff\":%.4f,\"smem_bytes\":%zu,"
+        "\"levels\":{\"l2_smem\":{\"dv_bytes\":%.6g,\"bw\":%.6g,\"us\":%.4f},"
+        "\"hbm\":{\"dv_bytes\":%.6g,\"bw\":%.6g,\"us\":%.4f},"
+        "\"compute\":{\"flops_issued_us\":%.4f,\"peak\":%.6g}},\"model_us\":%.4f},"
+        "\"roofline\":{\"flops\":%.6g,\"compulsory_bytes\":%.6g,\"roofline_us\":%.4f},"
+        "\"device\":{\"ordinal\":%d,\"sms\":%d,\"smem_optin\":%zu,\"l2_bytes\":%zu}}",
+        pb.N, pb.K, pb.C, pb.H, pb.W, pb.R, pb.S, path_name(p->path), tile.c_str(), ws_bytes(p),
+        conv_plan_num_kernels(p), m.tiles, m.ctas, m.wave_eff, m.smem,
+        m.dv_l2_smem, p->dev.bw_l2, m.t_l2_us, m.dv_hbm, p->dev.bw_hbm, m.t_hbm_us, m.t_comp_us, peak,
+        m.model_us, pb.flops(), comp_bytes, roof_us, p->dev.ordinal, p->dev.sms, p->dev.smem_optin,
+        p->dev.l2_bytes);
+    if (n < 0) return -1;
+    if (buf && cap) {
+        size_t c = std::min((size_t)n, cap - 1);
+        memcpy(buf, out, c);
+        buf[c] = 0;
+    }
+    return n;
+}
+
+static conv_status check_ptr(const void* ptr, const char* name, size_t align) {
+    if (!ptr) return fail(CONV_ERR_INVALID_ARGUMENT, "%s is NULL", name);
+    if (reinterpret_cast<uintptr_t>(ptr) % align) return fail(CONV_ERR_INVALID_ARGUMENT, "%s is not %zu-B aligned", name, align);
+    return CONV_OK;
+}
+
+static conv_status run_impl(const conv_plan* p, const float* in, const float* ker, float* out, void* ws,
+                            void* stream, void* const* events, int n_events) {
+    if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
+    conv_status s;
+    if ((s = check_ptr(in, "in", 16)) != CONV_OK) return s;
+    if ((s = check_ptr(ker, "ker", 16)) != CONV_OK) return s;
+    if ((s = check_ptr(out, "out", 16)) != CONV_OK) return s;
+    const size_t need = ws_bytes(p);
+    if (need && (s = check_ptr(ws, "workspace", 256)) != CONV_OK) return s;
+    const int nk = conv_plan_num_kernels(p);
+    if (events && n_events != nk + 1) return fail(CONV_ERR_INVALID_ARGUMENT, "n_events must be %d", nk + 1);
+    // Out must not alias the inputs or the workspace.
+    const char* o0 = reinterpret_cast<const char*>(out);
+    const char* o1 = o0 + 4 * p->pb.out_elems();
+    auto overlaps = [&](const void* b, size_t bytes) {
+        const char* a0 = static_cast<const char*>(b);
+        return a0 < o1 && o0 < a0 + bytes;
+    };
+    if (overlaps(in, 4 * p->pb.in_elems()) || overlaps(ker, 4 * p->pb.ker_elems()) || (need && overlaps(ws, need)))
+        return fail(CONV_ERR_INVALID_ARGUMENT, "out aliases in, ker or workspace");
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev != p->dev.ordinal)
+        return fail(CONV_ERR_INVALID_ARGUMENT, "current device %d is not the plan's device %d", dev, p->dev.ordinal);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev[4];
+    cudaEvent_t* evp = nullptr;
+    if (events) {
+        for (int i = 0; i <= nk; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
+        evp = ev;
+    }
+    std::string err;
+    cudaError_t e;
+    if (p->path == CONV_PATH_FP32_SIMT)
+        e = simt_run(p->pb, p->simt, in, ker, out, ws, st, evp, err);
+    else
+        e = tc_run(p->pb, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, ws, st, p->dev.sms, evp, err);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CONV_ERR_CUDA, "%s%s%s", err.c_str(), err.empty() ? "" : ": ", cudaGetErrorString(e));
+    }
+    return CONV_OK;
+}
+
+extern "C" conv_status conv_run(const conv_plan* p, const float* in, const float* ker, float* out, void* ws,
+                                void* stream) {
+    return run_impl(p, in, ker, out, ws, stream, nullptr, 0);
+}
+
+extern "C" conv_status conv_run_events(const conv_plan* p, const float* in, const float* ker, float* out,
+                                       void* ws, void* stream, void* const* events, int n_events) {
+    if (!events) return fail(CONV_ERR_INVALID_ARGUMENT, "events is NULL");
+    return run_impl(p, in, ker, out, ws, stream, events, n_events);
+}
+
+extern "C" size_t conv_plan_host_run_bytes(const conv_plan* p) {
+    if (!p) return 0;
+    return align256(4 * p->pb.in_elems()) + align256(4 * p->pb.ker_elems()) + align256(4 * p->pb.out_elems()) +
+           ws_bytes(p);
+}
+
+extern "C" conv_status conv_run_host(const conv_plan* p, const float* in_host, const float* ker_host,
+                                     float* out_host, void* dbuf, void* stream) {
+    if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (!in_host || !ker_host || !out_host) return fail(CONV_ERR_INVALID_ARGUMENT, "host pointer is NULL");
+    conv_status s;
+    if ((s = check_ptr(dbuf, "device_buffer", 256)) != CONV_OK) return s;
+    const size_t bi = 4 * p->pb.in_elems(), bk = 4 * p->pb.ker_elems(), bo = 4 * p->pb.out_elems();
+    char* d = static_cast<char*>(dbuf);
+    float* din = reinterpret_cast<float*>(d);
+    float* dker = reinterpret_cast<float*>(d + align256(bi));
+    float* dout = reinterpret_cast<float*>(d + align256(bi) + align256(bk));
+    void* dws = d + align256(bi) + align256(bk) + align256(bo);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(din, in_host, bi, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dker, ker_host, bk, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(CONV_ERR_CUDA, "H2D copy failed: %s", cudaGetErrorString(e)); }
+    s = run_impl(p, din, dker, dout, dws, stream, nullptr, 0);
+    if (s != CONV_OK) return s;
+    e = cudaMemcpyAsync(out_host, dout, bo, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(CONV_ERR_CUDA, "D2H copy failed: %s", cudaGetErrorString(e)); }
+    return CONV_OK;
+}

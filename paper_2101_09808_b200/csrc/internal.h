@@ -1,0 +1,98 @@
+// internal.h -- library-internal declarations shared by the host plan code
+// and the kernel launchers.  Not part of the ABI (see include/conv.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <string>
+
+namespace conv {
+
+// Problem of Eq. 1: H, W are OUTPUT extents.
+struct Problem {
+    int N, K, C, H, W, R, S;
+    int64_t Hin() const { return (int64_t)H + R - 1; }
+    int64_t Win() const { return (int64_t)W + S - 1; }
+    int64_t M() const { return (int64_t)N * H * W; }  // implicit-GEMM M
+    int64_t in_elems() const { return (int64_t)N * C * Hin() * Win(); }
+    int64_t ker_elems() const { return (int64_t)K * C * R * S; }
+    int64_t out_elems() const { return (int64_t)N * K * H * W; }
+    double flops() const { return 2.0 * (double)N * K * H * W * (double)C * R * S; }
+};
+
+// Device facts the selector uses (queried at plan creation).
+struct Device {
+    int ordinal = 0;
+    int sms = 148;
+    int cc_major = 10, cc_minor = 0;
+    size_t smem_optin = 232448;   // max dynamic smem per block (opt-in)
+    size_t l2_bytes = 126u << 20;
+    // Bandwidths (bytes/s) and peaks (flop/s) used by the model.  HBM and the
+    // bf16 tensor peak default to MEASURED_PEAKS.json's values; the L2->SMEM
+    // figure and the FFMA peak are defaults to be replaced by the probes.
+    double bw_hbm = 6544.7e9;
+    double bw_l2 = 12.0e12;
+    double peak_bf16 = 1651.8e12;
+    double peak_tf32 = 825.9e12;
+    double peak_fp32 = 74.4e12;
+};
+
+// ---- tensor-core path (K3) ------------------------------------------------
+struct TcTile {
+    int bn = 128;        // GEMM-N tile (output channels), multiple of 32, <= 256
+    int stages = 4;      // smem ring depth
+};
+
+struct TcLayout {        // derived from Problem + element size
+    int elem;            // bytes per element in the workspace (4 tf32, 2 bf16)
+    int Cp;              // channels padded so that Cp*elem is 32, 64 or a multiple of 128
+    int sw;              // swizzle span in bytes = BKc*elem (32, 64 or 128)
+    int bkc;             // channels per k-block
+    int n_cblk;          // Cp / bkc
+    size_t in_ws_bytes;  // NHWC workspace
+    size_t ker_ws_bytes; // KRSC workspace
+};
+
+TcLayout tc_layout(const Problem& p, bool bf16);
+size_t tc_smem_bytes(const TcLayout& L, const TcTile& t);
+
+// Launch K1 (ker repack), K2 (in repack) and K3 (tcgen05 implicit GEMM).
+// events (optional, n_events == 4) are recorded around each kernel.
+cudaError_t tc_run(const Problem& p, const TcLayout& L, const TcTile& t, bool bf16,
+                   const float* in, const float* ker, float* out, void* ws,
+                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err);
+
+// ---- FP32 SIMT path (K4) ----------------------------------------------------
+struct SimtTile {
+    int tk = 8;   // output channels per thread (register tile)
+    int tw = 4;   // output pixels per thread (stride-32 within a warp)
+    int kg = 4;   // channel groups (warps along k) per CTA
+    int pw = 2;   // pixel warps per CTA
+    int tn = 1;   // images per CTA tile
+    int th = 8;   // output rows per image per CTA tile
+    int bc = 8;   // input channels per smem stage
+};
+size_t simt_smem_bytes(const Problem& p, const SimtTile& t);
+size_t simt_ws_bytes(const Problem& p, const SimtTile& t);   // packed Ker
+bool simt_tile_supported(const SimtTile& t);
+// Launch the Ker packing kernel and K4.  events (optional, 3) around each.
+cudaError_t simt_run(const Problem& p, const SimtTile& t, const float* in, const float* ker,
+                     float* out, void* ws, cudaStream_t st, cudaEvent_t* ev, std::string& err);
+
+// Driver entry points resolved through the runtime (no -lcuda link).
+bool driver_init(std::string& err);
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*PFN_encodeIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                     const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                     cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                     CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+extern PFN_encodeTiled g_encode_tiled;
+extern PFN_encodeIm2col g_encode_im2col;
+
+}  // namespace conv

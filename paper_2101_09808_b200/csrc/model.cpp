@@ -1,0 +1,304 @@
+// model.cpp -- the tile selector.
+//
+// The paper's method (MOpt, Sec. 5 and Alg. 1
+// PAPER.md:383-419) picks the tiling that minimises the bottleneck level's
+// bandwidth-scaled data movement, max_l DV^l / BW^l, subject to per-level
+// capacity constraints (Eq. 4).  On a B200 the levels are
+// registers/TMEM, shared memory, L2 and HBM; the tile space of each kernel is
+// small and discrete, so instead of Ipopt + FloorToInteger + LoadBalancer the
+// selector enumerates every feasible candidate and evaluates
+//
+//   T(cand) = max( FLOPs_issued / peak,  DV_{L2->SMEM} / BW_L2 ) / wave_eff
+//             + DV_HBM / BW_HBM (the part not overlapped) + fixed launch costs
+//
+// where DV_{L2->SMEM} comes from the paper's single-level model (Sec. 3.2,
+// conv_model_dv below) instantiated with the CTA tile and the kernel's
+// tile-loop order, wave_eff = tiles / (ceil(tiles / slots) * slots) is Sec. 7's
+// "prod T/PT == num_cores" load-balance term and DV_HBM counts
+// the compulsory traffic plus the layout transforms.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/conv.h"
+#include "internal.h"
+#include "model.h"
+
+// ---------------------------------------------------------------------------
+// Sec. 3 / Sec. 2.2 data-movement model (exported: conv_model_*)
+
+namespace {
+enum { IN_ = 0, KER_ = 1, OUT_ = 2 };
+enum { I_N = 0, I_K = 1, I_C = 2, I_R = 3, I_S = 4, I_H = 5, I_W = 6 };
+
+// Which of the 7 iterators index each tensor (Sec. 4:
+// "each of the seven loop indices is present in exactly two of the three
+// tensors").
+const bool kPresent[3][7] = {
+    /* In  [n,c,h+r,w+s] */ {true, false, true, true, true, true, true},
+    /* Ker [k,c,r,s]     */ {false, true, true, true, true, false, false},
+    /* Out [n,k,h,w]     */ {true, true, false, false, false, true, true},
+};
+
+double footprint(int t, const double* T) {
+    switch (t) {
+        case IN_: return T[I_N] * T[I_C] * (T[I_H] + T[I_R] - 1) * (T[I_W] + T[I_S] - 1);
+        case KER_: return T[I_K] * T[I_C] * T[I_R] * T[I_S];
+        default: return T[I_N] * T[I_K] * T[I_H] * T[I_W];
+    }
+}
+}  // namespace
+
+extern "C" double conv_model_footprint(const double T[7]) {
+    if (!T) return -1;
+    return footprint(IN_, T) + footprint(KER_, T) + footprint(OUT_, T);
+}
+
+extern "C" double conv_model_dv(const int perm[7], const double Nx[7], const double T[7], double dv[3]) {
+    if (!perm || !Nx || !T) return -1;
+    bool seen[7] = {false};
+    for (int i = 0; i < 7; ++i) {
+        if (perm[i] < 0 || perm[i] > 6 || seen[perm[i]]) return -1;
+        seen[perm[i]] = true;
+        if (!(T[i] >= 1) || !(Nx[i] >= 1) || T[i] > Nx[i]) return -1;
+    }
+    double trip[7];
+    for (int d = 0; d < 7; ++d) trip[d] = ceil(Nx[d] / T[d]);
+    double out[3];
+    for (int t = 0; t < 3; ++t) {
+        // R_A: innermost tile loop whose iterator indexes A (perm[6] is innermost).
+        int ra = -1;
+        for (int i = 6; i >= 0; --i)
+            if (kPresent[t][perm[i]]) { ra = i; break; }
+        const int it = perm[ra];
+        if (t == IN_ && (it == I_W || it == I_H || it == I_S || it == I_R)) {
+            // Case 2: partial reuse along the innermost
+            // present iterator; loops strictly outside it multiply.
+            double outer = 1;
+            for (int i = 0; i < ra; ++i) outer *= trip[perm[i]];
+            double partial;
+            const double spanh = T[I_H] + T[I_R] - 1, spanw = T[I_W] + T[I_S] - 1;
+            const double base = T[I_N] * T[I_C];
+            switch (it) {
+                case I_W: partial = base * spanh * T[I_W] * (trip[I_W] - 1); break;
+                case I_S: partial = base * spanh * T[I_S] * (trip[I_S] - 1); break;
+                case I_H: partial = base * T[I_H] * (trip[I_H] - 1) * spanw; break;
+                default:  partial = base * T[I_R] * (trip[I_R] - 1) * spanw; break;
+            }
+            out[t] = outer * (footprint(IN_, T) + partial);
+        } else {
+            // Case 1: a fresh slice every time the
+            // iterator at R_A (or any loop outside it) changes.
+            double cnt = 1;
+            for (int i = 0; i <= ra; ++i) cnt *= trip[perm[i]];
+            out[t] = cnt * footprint(t, T) * (t == OUT_ ? 2.0 : 1.0);
+        }
+    }
+    if (dv) { dv[0] = out[0]; dv[1] = out[1]; dv[2] = out[2]; }
+    return out[0] + out[1] + out[2];
+}
+
+extern "C" double conv_model_dv_matmul(const int perm[3], const double Nx[3], const double T[3]) {
+    // Sec. 2.2: C[i][j] += A[i][k] * B[k][j]; same two-case
+    // rule with index sets A{i,k}, B{k,j}, C{i,j} (C read + written: x2).
+    if (!perm || !Nx || !T) return -1;
+    static const bool pres[3][3] = {{true, false, true}, {false, true, true}, {true, true, false}};
+    bool seen[3] = {false};
+    for (int i = 0; i < 3; ++i) {
+        if (perm[i] < 0 || perm[i] > 2 || seen[perm[i]]) return -1;
+        seen[perm[i]] = true;
+        if (!(T[i] >= 1) || T[i] > Nx[i]) return -1;
+    }
+    double trip[3];
+    for (int d = 0; d < 3; ++d) trip[d] = ceil(Nx[d] / T[d]);
+    const double fp[3] = {T[0] * T[2], T[2] * T[1], T[0] * T[1]};
+    double total = 0;
+    for (int a = 0; a < 3; ++a) {
+        int ra = -1;
+        for (int i = 2; i >= 0; --i)
+            if (pres[a][perm[i]]) { ra = i; break; }
+        double cnt = 1;
+        for (int i = 0; i <= ra; ++i) cnt *= trip[perm[i]];
+        total += cnt * fp[a] * (a == 2 ? 2.0 : 1.0);
+    }
+    return total;
+}
+
+// ---------------------------------------------------------------------------
+// Selector
+
+namespace conv {
+
+static const double kLaunchUs = 2.0;      // per-kernel launch + ramp
+static const double kTileOverheadUs = 0.25;  // per wave: pipeline fill + epilogue drain
+
+static double wave_eff(long tiles, long slots) {
+    if (tiles <= 0 || slots <= 0) return 1.0;
+    const long waves = (tiles + slots - 1) / slots;
+    return (double)tiles / (double)(waves * slots);
+}
+
+// GPU instantiation of the Sec. 3.2 model for the implicit GEMM's CTA tile:
+// pixels are one flattened dimension (T_w = 128 of N_w = M), T_k = BN,
+// T_c = BKc, T_r = T_s = 1; tile-loop order (outer -> inner) = pixel tile,
+// k tile, r, s, c-block.  In and Ker are case 1 (innermost ct), i.e. the
+// im2col replay; Out leaves the SM from TMEM straight to global, so only
+// In + Ker cross L2 -> SMEM.
+static double tc_dv_l2_smem_bytes(const Problem& pb, const TcLayout& L, int bn) {
+    const int perm[7] = {I_N, I_H, I_W, I_K, I_R, I_S, I_C};
+    const double Nx[7] = {1, (double)pb.K, (double)L.Cp, (double)pb.R, (double)pb.S, 1, (double)pb.M()};
+    const double T[7] = {1, (double)std::min(bn, pb.K), (double)L.bkc, 1, 1, 1, (double)std::min<int64_t>(128, pb.M())};
+    double dv[3];
+    conv_model_dv(perm, Nx, T, dv);
+    // Trip counts are ceil(N/T): partial tiles are charged as full tiles
+    // (TMA moves whole boxes; out-of-bounds rows are zero-filled, not read).
+    return (dv[IN_] + dv[KER_]) * L.elem;
+}
+
+ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t) {
+    ModelResult r;
+    const TcLayout L = tc_layout(pb, bf16);
+    const long mt = (long)((pb.M() + 127) / 128), nt = (pb.K + t.bn - 1) / t.bn;
+    r.tiles = mt * nt;
+    r.ctas = std::min<long>(r.tiles, dev.sms);
+    r.wave_eff = wave_eff(r.tiles, dev.sms);
+    const double peak = bf16 ? dev.peak_bf16 : dev.peak_tf32;
+    const double flops_issued = 2.0 * (double)mt * 128 * (double)nt * t.bn * (double)pb.R * pb.S * L.Cp;
+    r.t_comp_us = flops_issued / peak * 1e6;
+    r.dv_l2_smem = tc_dv_l2_smem_bytes(pb, L, t.bn);
+    r.t_l2_us = r.dv_l2_smem / dev.bw_l2 * 1e6;
+    // HBM: repacks (read fp32 In/Ker, write workspace) + main kernel (read
+    // workspace once -- the 9x im2col replay and the k-tile re-reads hit L2 --
+    // and write fp32 Out once).
+    const double repack = 4.0 * pb.in_elems() + (double)L.in_ws_bytes + 4.0 * pb.ker_elems() + (double)L.ker_ws_bytes;
+    const double main_hbm = (double)L.in_ws_bytes + (double)L.ker_ws_bytes + 4.0 * pb.out_elems();
+    r.dv_hbm = repack + main_hbm;
+    r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
+    const double waves = ceil((double)r.tiles / dev.sms);
+    const double t_main = std::max({r.t_comp_us / r.wave_eff, r.t_l2_us / r.wave_eff, main_hbm / dev.bw_hbm * 1e6})
+                          + waves * kTileOverheadUs + kLaunchUs;
+    const double t_rep = repack / (0.7 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
+    r.model_us = t_main + t_rep;
+    r.smem = tc_smem_bytes(L, t);
+    return r;
+}
+
+static int tc_max_stages(const Device& dev, const TcLayout& L, int bn) {
+    for (int s = 8; s >= 2; --s) {
+        TcTile t;
+        t.bn = bn;
+        t.stages = s;
+        if (tc_smem_bytes(L, t) <= dev.smem_optin) return s;
+    }
+    return 0;
+}
+
+bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& best_r,
+               int force_bn, int force_stages, std::string& why) {
+    const TcLayout L = tc_layout(pb, bf16);
+    if (pb.R > 128 || pb.S > 128) { why = "R, S > 128: TMA im2col offsets are limited to [-128, 127]"; return false; }
+    if (pb.M() + 128 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
+    bool found = false;
+    for (int bn = 32; bn <= 256; bn += 32) {
+        if (force_bn && bn != force_bn) continue;
+        if (!force_bn && bn > ((pb.K + 31) / 32) * 32) continue;
+        const int smax = tc_max_stages(dev, L, bn);
+        if (smax < 2) continue;
+        TcTile t;
+        t.bn = bn;
+        t.stages = force_stages ? force_stages : smax;
+        if (t.stages < 2 || t.stages > smax) continue;
+        ModelResult r = model_tc(pb, dev, bf16, t);
+        if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+    }
+    if (!found) why = "no tensor-path tile fits shared memory / TMEM for this request";
+    return found;
+}
+
+// ---- SIMT -------------------------------------------------------------------
+ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) {
+    ModelResult r;
+    const int bko = t.kg * t.tk;
+    const long ntile = (pb.N + t.tn - 1) / t.tn, htile = (pb.H + t.th - 1) / t.th, ktile = (pb.K + bko - 1) / bko;
+    r.tiles = ntile * htile * ktile;
+    const int threads = 32 * t.kg * t.pw;
+    const size_t smem = simt_smem_bytes(pb, t);
+    r.smem = smem;
+    // Register level (Sec. 6 microkernel analog): TK*TW accumulators + TW + TK
+    // operands per thread; ~24 registers of addressing.
+    const int regs = t.tk * t.tw + t.tk + 3 * t.tw + 28;
+    const int by_regs = 65536 / (std::max(regs, 32) * threads);
+    const int by_smem = (int)(228 * 1024 / (smem + 1024));
+    const int by_thr = 2048 / threads;
+    int per_sm = std::min({by_regs, by_smem, by_thr, 32});
+    if (per_sm < 1) { r.model_us = 1e30; return r; }
+    r.ctas = std::min<long>(r.tiles, (long)per_sm * dev.sms);
+    r.wave_eff = wave_eff(r.tiles, (long)per_sm * dev.sms);
+    // Issued FFMA lanes (idle pixel slots included) plus the LDS the register
+    // tile needs per (c,r,s): TW scalar + TK/4 vector loads per TK*TW FFMA.
+    const double slots = 32.0 * t.tw * t.pw;
+    const double lanes_fma = (double)r.tiles * slots * bko * (double)pb.C * pb.R * pb.S;
+    const double issue_factor = 1.0 + (t.tw + t.tk / 4.0 + 1.0) / (t.tk * t.tw);
+    r.t_comp_us = 2.0 * lanes_fma * issue_factor / dev.peak_fp32 * 1e6;
+    // Latency hiding: fewer than 8 warps per SM cannot keep 4 SMSPs busy.
+    const int warps_sm = per_sm * threads / 32;
+    if (warps_sm < 8) r.t_comp_us *= 8.0 / warps_sm;
+    // L2 -> SMEM: per CTA, every c-chunk loads the In halo tile and Ker slab
+    // (Eq. 4's In and Ker footprints).
+    const double in_stage = (double)t.bc * t.tn * (t.th + pb.R - 1) * pb.Win();
+    const double ker_stage = (double)t.bc * pb.R * pb.S * bko;
+    const double chunks = ceil((double)pb.C / t.bc);
+    r.dv_l2_smem = (double)r.tiles * chunks * (in_stage + ker_stage) * 4.0;
+    r.t_l2_us = r.dv_l2_smem / dev.bw_l2 * 1e6;
+    r.dv_hbm = 4.0 * (pb.in_elems() + 2.0 * pb.ker_elems() + pb.out_elems());
+    r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
+    r.model_us = std::max({r.t_comp_us, r.t_l2_us}) / r.wave_eff + r.t_hbm_us * 0.2 + 2 * kLaunchUs;
+    return r;
+}
+
+bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResult& best_r,
+                 const SimtTile* forced, unsigned forced_mask, std::string& why) {
+    bool found = false;
+    const int tks[2] = {4, 8};
+    const int kgs[4] = {1, 2, 4, 8};
+    const int bcs[3] = {4, 8, 16};
+    const int tn_max = std::min(pb.N, 16);
+    for (int tk : tks)
+    for (int tw = 1; tw <= 8; ++tw)
+    for (int kg : kgs)
+    for (int pw = 1; pw * kg <= 16; ++pw)
+    for (int tn = 1; tn <= tn_max; tn = (tn < 4 ? tn + 1 : tn * 2))
+    for (int bc : bcs) {
+        SimtTile t;
+        t.tk = tk; t.tw = tw; t.kg = kg; t.pw = pw; t.tn = tn; t.bc = bc;
+        if (forced) {
+            if ((forced_mask & 1) && t.tk != forced->tk) continue;
+            if ((forced_mask & 2) && t.tw != forced->tw) continue;
+            if ((forced_mask & 4) && t.kg != forced->kg) continue;
+            if ((forced_mask & 8) && t.pw != forced->pw) continue;
+            if ((forced_mask & 16) && t.tn != forced->tn) continue;
+            if ((forced_mask & 64) && t.bc != forced->bc) continue;
+        }
+        if (!simt_tile_supported(t)) continue;
+        // rows per tile: as many as the pixel slots allow
+        const long slots = 32L * tw * pw;
+        int th = (int)std::min<long>(pb.H, slots / ((long)tn * pb.W));
+        if (forced && (forced_mask & 32)) th = forced->th;
+        if (th < 1) continue;
+        if ((long)tn * th * pb.W > slots) continue;
+        // slot utilisation >= 50%
+        if (2L * tn * th * pb.W < slots && !(forced && (forced_mask & 32))) continue;
+        t.th = th;
+        if (simt_smem_bytes(pb, t) > dev.smem_optin) continue;
+        if (t.kg * t.tk > ((pb.K + 3) / 4) * 4 * 2 && !forced) continue;  // mostly-empty k tile
+        ModelResult r = model_simt(pb, dev, t);
+        if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+    }
+    if (!found) why = "no SIMT tile fits shared memory for this request";
+    return found;
+}
+
+}  // namespace conv

@@ -1,0 +1,30 @@
+// model.h -- selector internals (not part of the ABI).
+#pragma once
+#include <string>
+
+#include "internal.h"
+
+namespace conv {
+
+struct ModelResult {
+    long tiles = 0;          // CTA tiles
+    long ctas = 0;           // CTAs resident in the first wave
+    double wave_eff = 1.0;   // tiles / (waves * slots)
+    double t_comp_us = 0;    // issued FLOPs / path peak
+    double dv_l2_smem = 0;   // bytes L2 -> SMEM (Sec. 3.2 model, CTA tile)
+    double t_l2_us = 0;
+    double dv_hbm = 0;       // bytes HBM (compulsory + layout transforms)
+    double t_hbm_us = 0;
+    double model_us = 0;     // modeled conv_run time
+    size_t smem = 0;         // dynamic shared memory per CTA
+};
+
+ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t);
+bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& r,
+               int force_bn, int force_stages, std::string& why);
+ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t);
+// forced_mask bits: 1 tk, 2 tw, 4 kg, 8 pw, 16 tn, 32 th, 64 bc
+bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResult& r,
+                 const SimtTile* forced, unsigned forced_mask, std::string& why);
+
+}  // namespace conv

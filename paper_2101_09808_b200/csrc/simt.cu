@@ -1,0 +1,270 @@
+// simt.cu -- K4: FP32 SIMT direct convolution.
+//
+// Eq. 1 on native NCHW In with fp32 FFMA, no tensor cores.
+// The structure follows the paper's own CPU design, re-targeted to an SM:
+//   * packing (Sec. 6): Ker [K,C,R,S] -> [K/BKo, C, R, S, BKo]
+//     so that a CTA's kernel slab is contiguous and a thread's TK output
+//     channels are adjacent (vector loads, warp broadcast) -- the paper's
+//     [K/VecLen, C, R, S, VecLen] with VecLen = BKo;
+//   * outer-product register tile (Fig. 4 / Listing 4): each
+//     thread holds TK output channels x TW output pixels of accumulators; per
+//     (c, r, s) it loads TK kernel values (float4, broadcast) and TW input
+//     values (one per pixel, conflict-free: the TW pixels of a thread are 32
+//     apart, so a warp's loads are 32 consecutive pixels);
+//   * shared-memory tile = Eq. 4's In + Ker footprints:
+//     bc channels x tn images x (th+R-1) input rows x Win, plus
+//     bc x R x S x BKo kernel values, double-buffered with cp.async;
+//   * parallelism over non-reduction dims only: grid over
+//     (image tile x row tile, k tile); the c,r,s reduction stays inside a
+//     thread in a fixed order (c ascending, then r, then s).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace conv {
+
+struct SimtParams {
+    int N, K, C, H, W, R, S;
+    int Hin, Win, HW, RS;
+    int tn, th, bc, kg;
+    int bko;          // kg * TK
+    int rows_in;      // th + R - 1
+    int plane;        // tn * rows_in * Win  (floats per channel in smem)
+    int n_htiles;     // ceil(H / th)
+    int nchunks;      // ceil(C / bc)
+    int bp;           // tn * th * W (real pixels per CTA tile)
+    int vec4_in;      // Win % 4 == 0
+};
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Packing kernel: Ker KCRS -> [ceil(K/bko)][C][R][S][bko], k >= K zero.
+__global__ void __launch_bounds__(256) pack_ker_simt(const float* __restrict__ ker, float* __restrict__ out,
+                                                     int K, int C, int RS, int bko, int64_t total) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int kk = (int)(i % bko);
+        const int64_t t = i / bko;            // (kb*C + c)*RS + rs
+        const int rs = (int)(t % RS);
+        const int64_t t2 = t / RS;             // kb*C + c
+        const int c = (int)(t2 % C);
+        const int64_t kb = t2 / C;
+        const int64_t k = kb * bko + kk;
+        out[i] = k < K ? __ldg(ker + (k * C + c) * RS + rs) : 0.0f;
+    }
+}
+
+template <int TK, int TW>
+__global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict__ in,
+                                                         const float* __restrict__ kerp,
+                                                         float* __restrict__ out, const SimtParams p) {
+    extern __shared__ __align__(16) float sm[];
+    const int in_stage = p.bc * p.plane;
+    const int ker_stage = p.bc * p.RS * p.bko;
+    const int stage_floats = in_stage + ker_stage;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int kgi = warp % p.kg;
+    const int pwi = warp / p.kg;
+
+    const int nt = blockIdx.x / p.n_htiles;
+    const int ht = blockIdx.x - nt * p.n_htiles;
+    const int n0 = nt * p.tn;
+    const int h0 = ht * p.th;
+    const int kb = blockIdx.y;
+    const int k0 = kb * p.bko;
+
+    // Per-slot pixel offsets into the smem In tile.
+    int off[TW];
+    int pix_img[TW], pix_h[TW], pix_w[TW];
+    bool valid[TW];
+    const int thw = p.th * p.W;
+#pragma unroll
+    for (int j = 0; j < TW; ++j) {
+        const int q = pwi * 32 * TW + lane + 32 * j;
+        const int img = q / thw;
+        const int rem = q - img * thw;
+        const int h = rem / p.W;
+        const int w = rem - h * p.W;
+        valid[j] = q < p.bp && (n0 + img) < p.N && (h0 + h) < p.H;
+        off[j] = valid[j] ? (img * p.rows_in + h) * p.Win + w : 0;
+        pix_img[j] = img;
+        pix_h[j] = h;
+        pix_w[j] = w;
+    }
+
+    float acc[TK][TW];
+#pragma unroll
+    for (int i = 0; i < TK; ++i)
+#pragma unroll
+        for (int j = 0; j < TW; ++j) acc[i][j] = 0.0f;
+
+    auto load_stage = [&](int buf, int chunk) {
+        float* in_s = sm + buf * stage_floats;
+        float* ker_s = in_s + in_stage;
+        const int c0 = chunk * p.bc;
+        // In: bc*tn segments of rows_in*Win contiguous floats.
+        const int seg_len = p.rows_in * p.Win;
+        for (int seg = 0; seg < p.bc * p.tn; ++seg) {
+            const int cc = seg / p.tn;
+            const int img = seg - cc * p.tn;
+            const int c = c0 + cc;
+            const int n = n0 + img;
+            const bool seg_ok = c < p.C && n < p.N;
+            const float* g = in + (((int64_t)n * p.C + c) * p.Hin + h0) * p.Win;
+            float* s = in_s + cc * p.plane + img * seg_len;
+            // valid elements: rows < Hin - h0
+            const int rows_ok = p.Hin - h0 < p.rows_in ? p.Hin - h0 : p.rows_in;
+            const int len_ok = seg_ok ? rows_ok * p.Win : 0;
+            if (p.vec4_in) {
+                for (int e = threadIdx.x * 4; e < seg_len; e += blockDim.x * 4)
+                    cp_async16(s + e, e < len_ok ? g + e : in, e < len_ok);
+            } else {
+                for (int e = threadIdx.x; e < seg_len; e += blockDim.x)
+                    cp_async4(s + e, e < len_ok ? g + e : in, e < len_ok);
+            }
+        }
+        // Ker: contiguous slab of the packed tensor, channels >= C zero.
+        const int cvalid = p.C - c0 < p.bc ? p.C - c0 : p.bc;
+        const int len_ok = cvalid * p.RS * p.bko;
+        const float* g = kerp + (((int64_t)kb * p.C + c0) * p.RS) * p.bko;
+        for (int e = threadIdx.x * 4; e < ker_stage; e += blockDim.x * 4)
+            cp_async16(ker_s + e, e < len_ok ? g + e : kerp, e < len_ok);
+    };
+
+    load_stage(0, 0);
+    cp_async_commit();
+    for (int chunk = 0; chunk < p.nchunks; ++chunk) {
+        const int buf = chunk & 1;
+        if (chunk + 1 < p.nchunks) load_stage(buf ^ 1, chunk + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const float* in_s = sm + buf * stage_floats;
+        const float* ker_s = in_s + in_stage;
+        const int cc_end = p.C - chunk * p.bc < p.bc ? p.C - chunk * p.bc : p.bc;
+        for (int cc = 0; cc < cc_end; ++cc) {
+            for (int r = 0; r < p.R; ++r) {
+                const float* ip = in_s + cc * p.plane + r * p.Win;
+                const float* kp = ker_s + ((cc * p.R + r) * p.S) * p.bko + kgi * TK;
+                for (int s = 0; s < p.S; ++s) {
+                    float iv[TW];
+#pragma unroll
+                    for (int j = 0; j < TW; ++j) iv[j] = ip[off[j] + s];
+                    float kv[TK];
+#pragma unroll
+                    for (int i = 0; i < TK; i += 4) {
+                        const float4 k4 = *reinterpret_cast<const float4*>(kp + s * p.bko + i);
+                        kv[i] = k4.x; kv[i + 1] = k4.y; kv[i + 2] = k4.z; kv[i + 3] = k4.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < TK; ++i)
+#pragma unroll
+                        for (int j = 0; j < TW; ++j) acc[i][j] = fmaf(kv[i], iv[j], acc[i][j]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+#pragma unroll
+    for (int i = 0; i < TK; ++i) {
+        const int k = k0 + kgi * TK + i;
+        if (k >= p.K) break;
+#pragma unroll
+        for (int j = 0; j < TW; ++j) {
+            if (valid[j]) {
+                const int64_t o = (((int64_t)(n0 + pix_img[j]) * p.K + k) * p.H + (h0 + pix_h[j])) * p.W + pix_w[j];
+                out[o] = acc[i][j];
+            }
+        }
+    }
+}
+
+bool simt_tile_supported(const SimtTile& t) {
+    if (t.tk != 4 && t.tk != 8) return false;
+    if (t.tw < 1 || t.tw > 8) return false;
+    const int threads = 32 * t.kg * t.pw;
+    return t.kg >= 1 && t.pw >= 1 && threads <= 512 && t.tn >= 1 && t.th >= 1 && t.bc >= 1;
+}
+
+size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
+    const size_t plane = (size_t)t.tn * (t.th + pb.R - 1) * pb.Win();
+    const size_t in_stage = (size_t)t.bc * plane;
+    const size_t ker_stage = (size_t)t.bc * pb.R * pb.S * t.kg * t.tk;
+    return 2 * (in_stage + ker_stage) * sizeof(float);
+}
+
+template <int TK, int TW>
+static cudaError_t launch_simt_t(const float* in, const float* kerp, float* out, const SimtParams& p,
+                                 dim3 grid, int threads, size_t smem, cudaStream_t st) {
+    auto kfn = conv_direct_simt<TK, TW>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, threads, smem, st>>>(in, kerp, out, p);
+    return cudaGetLastError();
+}
+
+#define SIMT_CASE(TK_, TW_) \
+    if (t.tk == TK_ && t.tw == TW_) return launch_simt_t<TK_, TW_>(in, kerp, out, p, grid, threads, smem, st);
+
+static cudaError_t dispatch_simt(const SimtTile& t, const float* in, const float* kerp, float* out,
+                                 const SimtParams& p, dim3 grid, int threads, size_t smem, cudaStream_t st) {
+    SIMT_CASE(4, 1) SIMT_CASE(4, 2) SIMT_CASE(4, 3) SIMT_CASE(4, 4)
+    SIMT_CASE(4, 5) SIMT_CASE(4, 6) SIMT_CASE(4, 7) SIMT_CASE(4, 8)
+    SIMT_CASE(8, 1) SIMT_CASE(8, 2) SIMT_CASE(8, 3) SIMT_CASE(8, 4)
+    SIMT_CASE(8, 5) SIMT_CASE(8, 6) SIMT_CASE(8, 7) SIMT_CASE(8, 8)
+    return cudaErrorInvalidValue;
+}
+
+size_t simt_ws_bytes(const Problem& pb, const SimtTile& t) {
+    const int bko = t.kg * t.tk;
+    const size_t kb = (size_t)(pb.K + bko - 1) / bko;
+    return kb * bko * (size_t)pb.C * pb.R * pb.S * sizeof(float);
+}
+
+cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, const float* ker,
+                     float* out, void* ws, cudaStream_t st, cudaEvent_t* ev, std::string& err) {
+    SimtParams p;
+    p.N = pb.N; p.K = pb.K; p.C = pb.C; p.H = pb.H; p.W = pb.W; p.R = pb.R; p.S = pb.S;
+    p.Hin = (int)pb.Hin(); p.Win = (int)pb.Win(); p.HW = pb.H * pb.W; p.RS = pb.R * pb.S;
+    p.tn = t.tn; p.th = t.th; p.bc = t.bc; p.kg = t.kg;
+    p.bko = t.kg * t.tk;
+    p.rows_in = t.th + pb.R - 1;
+    p.plane = t.tn * p.rows_in * p.Win;
+    p.n_htiles = (pb.H + t.th - 1) / t.th;
+    p.nchunks = (pb.C + t.bc - 1) / t.bc;
+    p.bp = t.tn * t.th * pb.W;
+    p.vec4_in = (p.Win % 4 == 0) ? 1 : 0;
+    if (p.bp > t.pw * 32 * t.tw) { err = "SIMT tile: pixel slots < tn*th*W"; return cudaErrorInvalidValue; }
+
+    float* kerp = static_cast<float*>(ws);
+    const int64_t total = (int64_t)((pb.K + p.bko - 1) / p.bko) * p.bko * pb.C * p.RS;
+    const int pblocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    if (ev) cudaEventRecord(ev[0], st);
+    pack_ker_simt<<<pblocks, 256, 0, st>>>(ker, kerp, pb.K, pb.C, p.RS, p.bko, total);
+    if (ev) cudaEventRecord(ev[1], st);
+
+    const int n_ntiles = (pb.N + t.tn - 1) / t.tn;
+    dim3 grid((unsigned)(n_ntiles * p.n_htiles), (unsigned)((pb.K + p.bko - 1) / p.bko));
+    const int threads = 32 * t.kg * t.pw;
+    const size_t smem = simt_smem_bytes(pb, t);
+    cudaError_t e = dispatch_simt(t, in, kerp, out, p, grid, threads, smem, st);
+    if (e != cudaSuccess) { err = std::string("SIMT kernel launch failed: ") + cudaGetErrorString(e); return e; }
+    if (ev) cudaEventRecord(ev[2], st);
+    return cudaSuccess;
+}
+
+}  // namespace conv

@@ -1,0 +1,338 @@
+// tc.cu -- K3: tcgen05 implicit-GEMM convolution.
+//
+// Eq. 1 as a GEMM: M = N*H*W output pixels, N_gemm = K output
+// channels, K_gemm = R*S*C taps.  A[m, (r,s,c)] = In_NHWC[n, h+r, w+s, c] is
+// loaded per (r, s, c-block) by TMA in im2col mode (the traversal walks BM
+// consecutive output pixels, the filter-tap offsets (s, r) are added to every
+// pixel); B[k, (r,s,c)] = Ker_KRSC[k, r, s, c] by a tiled TMA load.  Both
+// operands are K-major with the 32/64/128-B swizzle matching the k-block's
+// byte width.  tcgen05.mma (M = 128, N = BN) accumulates fp32 in TMEM.
+//
+// Warp roles (256 threads, one CTA per SM, persistent over tiles):
+//   warp 0  TMA producer (one lane)       -> full[stage]  (mbarrier, tx bytes)
+//   warp 1  MMA issuer   (one lane)       -> empty[stage] (tcgen05.commit)
+//                                          -> tmem_full[acc]
+//   warp 2  TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4-7 epilogue: tcgen05.ld 32x32b (warp w%4 owns TMEM lanes 32(w%4)..)
+//             -> coalesced st.global into NCHW Out (consecutive TMEM lanes are
+//             consecutive pixels of one (n,k) plane)   -> tmem_empty[acc]
+//
+// Accumulation order per output element is fixed by the k-loop (r, s, c-block
+// ascending) and does not depend on the tile shape or on the grid, so results
+// are bit-identical across BN choices and batch shards.
+// Parallelism is over the non-reduction dims only (Sec. 7).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace conv {
+
+using namespace sm100;
+
+static constexpr int kBM = 128;
+static constexpr int kThreads = 256;
+
+struct TcParams {
+    float* out;
+    int M;            // N*H*W
+    int HW;           // H*W
+    int W;            // output width
+    int K;            // output channels
+    int R, S;
+    int Cp, bkc, n_cblk;
+    int k_iters;      // R*S*n_cblk
+    int num_n_tiles;
+    int num_tiles;
+    int stages;
+    uint32_t sw;              // 32 / 64 / 128 (bytes per operand row per k-block)
+    uint32_t a_stage_bytes;   // 128 * sw
+    uint32_t b_stage_bytes;   // bn * sw
+};
+
+template <int BN, bool BF16>
+__global__ void __launch_bounds__(kThreads, 1)
+conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
+                   const __grid_constant__ CUtensorMap tmap_b, const TcParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for the 128-B swizzle atoms.
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + (size_t)p.stages * p.a_stage_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_b + (size_t)p.stages * p.b_stage_bytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + p.stages;
+    uint64_t* tmem_full = bars + 2 * p.stages;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                   : (2 * BN <= 256) ? 256 : 512;
+
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+        for (int i = 0; i < p.stages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            const uint64_t pol_a = policy_evict_normal();
+            const uint64_t pol_b = policy_evict_last();   // Ker is re-read by every M tile
+            const uint32_t tx_bytes = p.a_stage_bytes + p.b_stage_bytes;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                const int m_tile = tile / p.num_n_tiles;
+                const int n_tile = tile - m_tile * p.num_n_tiles;
+                const int m0 = m_tile * kBM;
+                const int img = m0 / p.HW;
+                const int pix = m0 - img * p.HW;
+                const int h0 = pix / p.W;
+                const int w0 = pix - h0 * p.W;
+                const int k0 = n_tile * BN;
+                for (int r = 0; r < p.R; ++r) {
+                    for (int s = 0; s < p.S; ++s) {
+                        for (int cb = 0; cb < p.n_cblk; ++cb) {
+                            mbar_wait(&empty[stage], phase ^ 1);
+                            mbar_arrive_expect_tx(&full[stage], tx_bytes);
+                            tma_load_im2col_4d(smem_a + (size_t)stage * p.a_stage_bytes, &tmap_a, &full[stage],
+                                               cb * p.bkc, w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
+                            tma_load_2d(smem_b + (size_t)stage * p.b_stage_bytes, &tmap_b, &full[stage],
+                                        (r * p.S + s) * p.Cp + cb * p.bkc, k0, pol_b);
+                            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc(BF16 ? 1u : 2u, kBM, BN);
+            const uint32_t layout = umma_layout_for_swizzle(p.sw);
+            const uint32_t sbo = 8 * p.sw;
+            const int k_steps = (int)(p.sw / 32);   // 32 B of K per MMA (8 tf32 / 16 bf16)
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+                for (int it = 0; it < p.k_iters; ++it) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(smem_a + (size_t)stage * p.a_stage_bytes);
+                    const uint32_t b_addr = smem_u32(smem_b + (size_t)stage * p.b_stage_bytes);
+                    for (int kk = 0; kk < k_steps; ++kk) {
+                        const uint64_t ad = make_sdesc(a_addr + kk * 32, sbo, layout);
+                        const uint64_t bd = make_sdesc(b_addr + kk * 32, sbo, layout);
+                        const uint32_t accum = (it > 0 || kk > 0) ? 1u : 0u;
+                        if (BF16) mma_bf16(d_tmem, ad, bd, idesc, accum);
+                        else      mma_tf32(d_tmem, ad, bd, idesc, accum);
+                    }
+                    tc_commit(&empty[stage]);          // frees the smem slot when the MMAs retire
+                    if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                }
+                tc_commit(&tmem_full[acc]);            // accumulator ready for the epilogue
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue: TMEM -> registers -> NCHW Out =====
+        const int q = warp & 3;                       // TMEM lane quadrant of this warp
+        const int row = q * 32 + (int)lane;           // accumulator row = pixel within the tile
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            const int m_tile = tile / p.num_n_tiles;
+            const int n_tile = tile - m_tile * p.num_n_tiles;
+            const int m = m_tile * kBM + row;
+            const int k0 = n_tile * BN;
+            const bool valid_m = m < p.M;
+            const int img = valid_m ? m / p.HW : 0;
+            const int pix = valid_m ? m - img * p.HW : 0;
+            float* obase = p.out + ((int64_t)img * p.K) * p.HW + pix;
+
+            mbar_wait(&tmem_full[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+            for (int j0 = 0; j0 < BN; j0 += 32) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(t0 + (uint32_t)j0, v);
+                tmem_ld_wait();
+                const int kbase = k0 + j0;
+                if (valid_m) {
+                    if (kbase + 32 <= p.K) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            __stcs(obase + (int64_t)(kbase + j) * p.HW, __uint_as_float(v[j]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (kbase + j < p.K) __stcs(obase + (int64_t)(kbase + j) * p.HW, __uint_as_float(v[j]));
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tmem_empty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+TcLayout tc_layout(const Problem& pb, bool bf16) {
+    TcLayout L;
+    L.elem = bf16 ? 2 : 4;
+    const int cbytes = pb.C * L.elem;
+    int cp_bytes;
+    if (cbytes <= 32) cp_bytes = 32;
+    else if (cbytes <= 64) cp_bytes = 64;
+    else cp_bytes = (cbytes + 127) / 128 * 128;
+    L.Cp = cp_bytes / L.elem;
+    L.sw = cp_bytes >= 128 ? 128 : cp_bytes;
+    L.bkc = L.sw / L.elem;
+    L.n_cblk = L.Cp / L.bkc;
+    L.in_ws_bytes = (size_t)pb.N * pb.Hin() * pb.Win() * L.Cp * L.elem;
+    L.ker_ws_bytes = (size_t)pb.K * pb.R * pb.S * L.Cp * L.elem;
+    return L;
+}
+
+size_t tc_smem_bytes(const TcLayout& L, const TcTile& t) {
+    const size_t a = (size_t)kBM * L.sw, b = (size_t)t.bn * L.sw;
+    return 1024 /*align slack*/ + (size_t)t.stages * (a + b) + (2 * t.stages + 4) * 8 + 16;
+}
+
+cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
+                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev);
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+template <int BN, bool BF16>
+static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& prm,
+                             size_t smem, int grid, cudaStream_t st) {
+    auto kfn = conv_igemm_tcgen05<BN, BF16>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, kThreads, smem, st>>>(ta, tb, prm);
+    return cudaGetLastError();
+}
+
+template <bool BF16>
+static cudaError_t launch_tc_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                                const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
+    switch (bn) {
+        case 32: return launch_tc<32, BF16>(ta, tb, prm, smem, grid, st);
+        case 64: return launch_tc<64, BF16>(ta, tb, prm, smem, grid, st);
+        case 96: return launch_tc<96, BF16>(ta, tb, prm, smem, grid, st);
+        case 128: return launch_tc<128, BF16>(ta, tb, prm, smem, grid, st);
+        case 160: return launch_tc<160, BF16>(ta, tb, prm, smem, grid, st);
+        case 192: return launch_tc<192, BF16>(ta, tb, prm, smem, grid, st);
+        case 224: return launch_tc<224, BF16>(ta, tb, prm, smem, grid, st);
+        case 256: return launch_tc<256, BF16>(ta, tb, prm, smem, grid, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool bf16,
+                   const float* in, const float* ker, float* out, void* ws,
+                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err) {
+    uint8_t* wsb = static_cast<uint8_t*>(ws);
+    void* in_ws = wsb;
+    void* ker_ws = wsb + align_up(L.in_ws_bytes, 256);
+
+    // Tensor maps are encoded per call (the workspace address is only known
+    // here); encoding is a host-only call of ~1 us.
+    const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUtensorMapSwizzle swz = L.sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                   : (L.sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    CUtensorMap ta, tb;
+    {
+        // In NHWC: dims (C, W, H, N) innermost first.
+        cuuint64_t dims[4] = {(cuuint64_t)L.Cp, (cuuint64_t)pb.Win(), (cuuint64_t)pb.Hin(), (cuuint64_t)pb.N};
+        cuuint64_t strides[3] = {(cuuint64_t)L.Cp * L.elem, (cuuint64_t)L.Cp * L.elem * pb.Win(),
+                                 (cuuint64_t)L.Cp * L.elem * pb.Win() * pb.Hin()};
+        // Bounding box per image: w in [0, Win-1-(S-1)], h in [0, Hin-1-(R-1)]:
+        // the traversal visits exactly the output pixels of valid conv.
+        int lower[2] = {0, 0};
+        int upper[2] = {-(pb.S - 1), -(pb.R - 1)};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = g_encode_im2col(&ta, dt, 4, in_ws, dims, strides, lower, upper, (cuuint32_t)L.bkc,
+                                     (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
+    }
+    {
+        // Ker KRSC as 2-D [K rows][R*S*Cp cols].
+        cuuint64_t dims[2] = {(cuuint64_t)pb.R * pb.S * L.Cp, (cuuint64_t)pb.K};
+        cuuint64_t strides[1] = {(cuuint64_t)pb.R * pb.S * L.Cp * L.elem};
+        cuuint32_t box[2] = {(cuuint32_t)L.bkc, (cuuint32_t)t.bn};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = g_encode_tiled(&tb, dt, 2, ker_ws, dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
+    }
+
+    cudaError_t e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev);
+    if (e != cudaSuccess) { err = "repack launch failed"; return e; }
+
+    TcParams prm;
+    prm.out = out;
+    prm.M = (int)pb.M();
+    prm.HW = pb.H * pb.W;
+    prm.W = pb.W;
+    prm.K = pb.K;
+    prm.R = pb.R;
+    prm.S = pb.S;
+    prm.Cp = L.Cp;
+    prm.bkc = L.bkc;
+    prm.n_cblk = L.n_cblk;
+    prm.k_iters = pb.R * pb.S * L.n_cblk;
+    prm.num_n_tiles = (pb.K + t.bn - 1) / t.bn;
+    const int num_m_tiles = (int)((pb.M() + kBM - 1) / kBM);
+    prm.num_tiles = num_m_tiles * prm.num_n_tiles;
+    prm.stages = t.stages;
+    prm.sw = (uint32_t)L.sw;
+    prm.a_stage_bytes = (uint32_t)(kBM * L.sw);
+    prm.b_stage_bytes = (uint32_t)(t.bn * L.sw);
+    const int grid = prm.num_tiles < num_sms ? prm.num_tiles : num_sms;
+    const size_t smem = tc_smem_bytes(L, t);
+    e = bf16 ? launch_tc_bn<true>(t.bn, ta, tb, prm, smem, grid, st)
+             : launch_tc_bn<false>(t.bn, ta, tb, prm, smem, grid, st);
+    if (e != cudaSuccess) { err = std::string("tcgen05 kernel launch failed: ") + cudaGetErrorString(e); return e; }
+    if (ev) cudaEventRecord(ev[3], st);
+    return cudaSuccess;
+}
+
+}  // namespace conv

@@ -1,0 +1,138 @@
+"""CPU-only checks of the C ABI: the library loads, exports every symbol
+include/conv.h declares, refuses to plan without an sm_100 device (no CPU
+fallback), and its data-movement model reproduces the paper's worked numbers.
+"""
+import itertools
+import os
+import re
+
+import pytest
+import torch
+
+from paper_2101_09808_b200 import conv
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2101_09808_b200 import build
+    build.build()
+    return conv.load_library()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "conv.h")).read()
+    return sorted(set(re.findall(r"CONV_API[^;(]*?\b(conv_\w+)\s*\(", src)))
+
+
+def test_header_declares_what_binding_lists():
+    assert declared_symbols() == sorted(conv.EXPORTED)
+
+
+def test_exports_every_declared_symbol(lib):
+    out = os.popen(f"nm -D --defined-only {conv.LIB_PATH}").read()
+    exported = set(re.findall(r" T (conv_\w+)", out))
+    for s in declared_symbols():
+        assert s in exported, s
+        assert hasattr(lib, s)
+
+
+def test_version(lib):
+    assert "sm_100a" in conv.version()
+
+
+def test_library_has_no_cpu_fallback(lib):
+    """Without an sm_100 device conv_plan_create fails loudly."""
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(conv.ConvError) as e:
+        conv.ConvPlan(1, 16, 16, 8, 8, 3, 3)
+    assert e.value.status in (conv.CONV_ERR_UNSUPPORTED_DEVICE, conv.CONV_ERR_INVALID_ARGUMENT)
+
+
+def test_invalid_extents_rejected_before_device(lib):
+    h = lib.conv_plan_create(1, 1, 1, 0, 1, 1, 1)
+    assert not h
+    assert "extent must be >= 1" in conv.last_error()
+    h = lib.conv_plan_create(70000, 70000, 1, 1, 1, 1, 1)
+    assert not h
+    assert "2^31" in conv.last_error()
+
+
+def test_null_plan_calls_are_safe(lib):
+    lib.conv_plan_destroy(None)
+    assert lib.conv_plan_workspace_bytes(None) == 0
+    assert lib.conv_plan_num_kernels(None) == -1
+    assert lib.conv_run(None, None, None, None, None, None) == conv.CONV_ERR_INVALID_ARGUMENT
+
+
+# ---- the selector's model: worked numbers -----------------
+
+def test_eq5_worked_example(lib):
+    """Eq. 5 at N=(n1,k4,c2,r1,s1,h4,w4), T=(1,2,2,1,1,2,2):
+    substituting into the printed formula gives
+    2*[4 + 1*2*(2*2*8 + 1*2*2*4)] = 200 = Out 128 + In 64 + Ker 8."""
+    Nx = dict(n=1, k=4, c=2, r=1, s=1, h=4, w=4)
+    T = dict(n=1, k=2, c=2, r=1, s=1, h=2, w=2)
+    dv_in, dv_ker, dv_out = conv.model_dv(["k", "c", "r", "s", "n", "h", "w"], Nx, T)
+    assert (dv_in, dv_ker, dv_out) == (64.0, 8.0, 128.0)
+
+
+def eq5(Nx, T):
+    """Eq. 5 exactly as printed."""
+    n, k, c, r, s, h, w = (Nx[x] for x in "nkcrshw")
+    tn, tk, tc, tr, ts, th, tw = (T[x] for x in "nkcrshw")
+    return (k / tk) * (c / tc) * (r / tr) * (s / ts) * (
+        tk * tc * tr * ts + (n / tn) * (h / th) * (2 * (w / tw) * tn * tk * th * tw + tn * tc * (th + tr - 1) * (w + ts - 1)))
+
+
+def test_eq5_class_members_equal_printed_formula(lib):
+    """Every permutation in the class <{kt,ct,rt,st},{nt,ht},wt> (4!*2! = 48
+    members) gives Eq. 5's value at random divisible tiles."""
+    import random
+    rng = random.Random(0)
+    for _ in range(20):
+        Nx, T = {}, {}
+        for x in "nkcrshw":
+            t = rng.choice([1, 2, 3])
+            T[x] = t
+            Nx[x] = t * rng.choice([1, 2, 4])
+        expected = eq5(Nx, T)
+        for outer in itertools.permutations("kcrs"):
+            for mid in itertools.permutations("nh"):
+                tot = sum(conv.model_dv(list(outer) + list(mid) + ["w"], Nx, T))
+                assert abs(tot - expected) <= 1e-9 * expected
+
+
+def test_eq3_matmul(lib):
+    """Eq. 3: N=4, T=2 => 64*(1/2+1/2+2/4) = 96."""
+    Nx = dict(i=4, j=4, k=4)
+    T = dict(i=2, j=2, k=2)
+    assert conv.model_dv_matmul(["i", "j", "k"], Nx, T) == 96.0
+    for Ni, Nj, Nk, Ti, Tj in [(8, 6, 10, 2, 3), (16, 16, 4, 4, 8)]:
+        got = conv.model_dv_matmul(["i", "j", "k"], dict(i=Ni, j=Nj, k=Nk), dict(i=Ti, j=Tj, k=2))
+        assert abs(got - Ni * Nj * Nk * (1 / Ti + 1 / Tj + 2 / Nk)) < 1e-9
+
+
+def test_footprints(lib):
+    """Eq. 4 LHS: T=(n1,k2,c2,r1,s1,h2,w2) -> 8 + 4 + 8 = 20;
+    In footprint with T=(n1,c3,h2,w2,r3,s3) is 1*3*4*4 = 48."""
+    assert conv.model_footprint(dict(n=1, k=2, c=2, r=1, s=1, h=2, w=2)) == 20.0
+    fp = conv.model_footprint(dict(n=1, k=1, c=3, r=3, s=3, h=2, w=2))
+    assert fp == 48 + 1 * 3 * 3 * 3 + 1 * 1 * 2 * 2
+
+
+def test_single_tile_permutation_invariance(lib):
+    """T = N: every permutation moves each tensor exactly once (Out twice)."""
+    Nx = dict(n=2, k=3, c=4, r=3, s=2, h=5, w=6)
+    exp = (2 * 4 * (5 + 3 - 1) * (6 + 2 - 1), 3 * 4 * 3 * 2, 2 * 2 * 3 * 5 * 6)
+    for perm in list(itertools.permutations("nkcrshw"))[::97]:
+        assert conv.model_dv(list(perm), Nx, Nx) == exp
+
+
+def test_model_rejects_bad_input(lib):
+    with pytest.raises(ValueError):
+        conv.model_dv(list("nkcrshw"), dict(n=1, k=1, c=1, r=1, s=1, h=1, w=1), dict(n=2, k=1, c=1, r=1, s=1, h=1, w=1))
+    with pytest.raises(KeyError):
+        conv.model_dv(list("nkcrshx"), dict(n=1, k=1, c=1, r=1, s=1, h=1, w=1), dict(n=1, k=1, c=1, r=1, s=1, h=1, w=1))

@@ -1,0 +1,220 @@
+"""GPU parity: every path of libconv.so against the CPU oracle (Eq. 1,
+PAPER.md:54), through the C ABI.  Tolerances are north_star's (BASELINE.json):
+relative L2 <= 1e-5 (FP32 SIMT), <= 5e-3 (TF32, BF16); bit-exact on the
+integer twin.  Tensor paths are additionally checked against the oracle run on
+the path's rounded inputs (reading R5), which isolates the
+accumulation error (fp32, <= 1e-5 relative) from the input rounding.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2101_09808_b200 import conv
+from paper_2101_09808_b200.inputs import CONFIGS, Shape, make_inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32_simt": 1e-5, "tf32": 5e-3, "bf16": 5e-3}
+ROUND = {"fp32_simt": lambda x: x, "tf32": oracle.round_tf32_rna, "bf16": oracle.round_bf16_rne}
+PATHS = ["fp32_simt", "tf32", "bf16"]
+
+
+def rel_l2(got, ref):
+    d = np.linalg.norm((got.astype(np.float64) - ref).ravel())
+    n = np.linalg.norm(ref.ravel())
+    return d / n if n else d
+
+
+def run(shape, inp, ker, path, tile=None):
+    plan = conv.ConvPlan(*shape.as_tuple(), path=path, tile=tile)
+    out = plan.run(inp.cuda(), ker.cuda())
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), plan
+
+
+ODD = [
+    Shape(N=1, K=5, C=3, H=7, W=9, R=3, S=3),
+    Shape(N=2, K=7, C=5, H=6, W=5, R=2, S=3),
+    Shape(N=3, K=33, C=17, H=11, W=13, R=3, S=1),
+    Shape(N=1, K=1, C=1, H=1, W=1, R=1, S=1),
+    Shape(N=2, K=40, C=70, H=9, W=10, R=1, S=1),
+    Shape(N=1, K=130, C=36, H=5, W=37, R=5, S=4),
+    Shape(N=5, K=64, C=40, H=3, W=3, R=3, S=3),
+    Shape(N=1, K=300, C=8, H=20, W=3, R=1, S=3),
+]
+SMALL = [CONFIGS["tiny"], CONFIGS["r2"], CONFIGS["pw"], CONFIGS["det"]]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("shape", SMALL + ODD, ids=lambda s: "x".join(map(str, s.as_tuple())))
+def test_real_inputs(path, shape):
+    inp, ker = make_inputs(shape, seed=0)
+    got, _ = run(shape, inp, ker, path)
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert rel_l2(got, ref) <= TOL[path]
+    # Against the oracle on the path's rounded inputs: only fp32 accumulation
+    # differs, whatever the precision of the products.
+    ref_r = oracle.conv_eq1(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()))
+    assert rel_l2(got, ref_r) <= 1e-5
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("shape", SMALL + ODD, ids=lambda s: "x".join(map(str, s.as_tuple())))
+def test_integer_twin_bit_exact(path, shape):
+    inp, ker = make_inputs(shape, seed=1, kind="int")
+    got, _ = run(shape, inp, ker, path)
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert np.array_equal(got.astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_p1_identity(path):
+    """P1: 1x1 identity kernel reproduces round_path(In) exactly."""
+    sh = Shape(N=2, K=48, C=48, H=9, W=13, R=1, S=1)
+    inp, _ = make_inputs(sh, seed=5)
+    ker = torch.eye(48).reshape(48, 48, 1, 1).contiguous()
+    got, _ = run(sh, inp, ker, path)
+    assert np.array_equal(got, ROUND[path](inp.numpy()))
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("r0,s0", [(0, 0), (1, 2), (2, 1), (2, 2)])
+def test_p2_shifted_delta(path, r0, s0):
+    """P2: Ker = delta_kc delta_{r r0} delta_{s s0} => Out = shifted In (no
+    kernel flip, correct h+r / w+s indexing incl. the last row/column)."""
+    sh = Shape(N=2, K=16, C=16, H=10, W=12, R=3, S=3)
+    inp, _ = make_inputs(sh, seed=6)
+    ker = torch.zeros(sh.ker_shape)
+    for k in range(16):
+        ker[k, k, r0, s0] = 1.0
+    got, _ = run(sh, inp, ker, path)
+    exp = ROUND[path](inp.numpy())[:, :, r0:r0 + sh.H, s0:s0 + sh.W]
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_p10_tile_invariance_tensor(path):
+    """P10: the k-loop order does not depend on BN, so every BN gives
+    bit-identical results."""
+    sh = Shape(N=2, K=256, C=64, H=12, W=12, R=3, S=3)
+    inp, ker = make_inputs(sh, seed=7)
+    outs = []
+    for bn in (32, 64, 128, 256):
+        got, plan = run(sh, inp, ker, path, tile=f"bn={bn}")
+        assert plan.describe()["tile"]["bn"] == bn
+        outs.append(got)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+def test_p10_tile_invariance_simt():
+    sh = Shape(N=2, K=32, C=24, H=12, W=12, R=3, S=3)
+    inp, ker = make_inputs(sh, seed=8)
+    outs = []
+    for spec in ("tk=4,tw=4,kg=2,pw=2", "tk=8,tw=8,kg=4,pw=1,bc=4", "tk=8,tw=2,kg=1,pw=4,bc=16"):
+        got, _ = run(sh, inp, ker, "fp32_simt", tile=spec)
+        outs.append(got)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_p10_batch_shards_bit_identical(path):
+    """Shards over n equal the slices of the full result."""
+    sh = Shape(N=8, K=64, C=32, H=14, W=14, R=3, S=3)
+    inp, ker = make_inputs(sh, seed=9)
+    full, _ = run(sh, inp, ker, path)
+    for p in (2, 4):
+        step = sh.N // p
+        for r in range(p):
+            sub = Shape(N=step, K=sh.K, C=sh.C, H=sh.H, W=sh.W, R=sh.R, S=sh.S)
+            got, _ = run(sub, inp[r * step:(r + 1) * step].contiguous(), ker, path)
+            assert np.array_equal(got, full[r * step:(r + 1) * step])
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_batched_full_size_sampled(path):
+    """BASELINE configs[4] at full size, in the bench's launch configuration:
+    two whole images against the oracle, 256 sampled points against the
+    correctly rounded brute-force sum, and the integer twin exact everywhere
+    the oracle is cheap (first image) plus all-integer everywhere."""
+    sh = CONFIGS["batched"]
+    inp, ker = make_inputs(sh, seed=0)
+    got, plan = run(sh, inp, ker, path)
+    x, w = inp.numpy(), ker.numpy()
+    ref2 = oracle.conv_eq1(x[:2], w)
+    assert rel_l2(got[:2], ref2) <= TOL[path]
+    rng = np.random.default_rng(0)
+    pts = [(rng.integers(sh.N), rng.integers(sh.K), rng.integers(sh.H), rng.integers(sh.W)) for _ in range(256)]
+    ref_pts = np.array([oracle.conv_eq1_point(x, w, *p) for p in pts])
+    got_pts = np.array([got[p] for p in pts], dtype=np.float64)
+    assert np.linalg.norm(got_pts - ref_pts) / np.linalg.norm(ref_pts) <= TOL[path]
+    # integer twin
+    xi, wi = make_inputs(sh, seed=1, kind="int")
+    goti, _ = run(sh, xi, wi, path)
+    assert np.all(goti == np.round(goti))
+    refi = oracle.conv_eq1(xi.numpy()[:1], wi.numpy())
+    assert np.array_equal(goti[:1].astype(np.float64), refi)
+    for p in pts[:64]:
+        assert goti[p] == oracle.conv_eq1_point(xi.numpy(), wi.numpy(), *p)
+
+
+def test_auto_path_and_describe():
+    for name, sh in CONFIGS.items():
+        plan = conv.ConvPlan(*sh.as_tuple())
+        d = plan.describe()
+        assert d["path"] in ("fp32_simt", "tf32")
+        assert d["problem"]["N"] == sh.N and d["problem"]["W"] == sh.W
+        assert d["model"]["model_us"] > 0
+        assert d["kernels"] == plan.num_kernels
+
+
+def test_argument_errors():
+    sh = CONFIGS["tiny"]
+    plan = conv.ConvPlan(*sh.as_tuple(), path="tf32")
+    inp, ker = make_inputs(sh, seed=0)
+    i, k = inp.cuda(), ker.cuda()
+    out = plan.new_output()
+    ws = plan.new_workspace()
+    lib = conv.load_library()
+    st = torch.cuda.current_stream().cuda_stream
+    # misaligned input pointer
+    assert lib.conv_run(plan._h, i.data_ptr() + 4, k.data_ptr(), out.data_ptr(), ws.data_ptr(), st) == 1
+    # NULL output
+    assert lib.conv_run(plan._h, i.data_ptr(), k.data_ptr(), None, ws.data_ptr(), st) == 1
+    # out aliases in
+    assert lib.conv_run(plan._h, i.data_ptr(), k.data_ptr(), i.data_ptr(), ws.data_ptr(), st) == 1
+    # missing workspace on a tensor path
+    assert lib.conv_run(plan._h, i.data_ptr(), k.data_ptr(), out.data_ptr(), None, st) == 1
+    assert "NULL" in conv.last_error()
+    with pytest.raises(conv.ConvError):
+        conv.ConvPlan(1, 1, 1, 0, 1, 1, 1)
+    with pytest.raises(conv.ConvError) as e:
+        conv.ConvPlan(1, 4, 4, 4, 4, 130, 1, path="tf32")
+    assert e.value.status == conv.CONV_ERR_INFEASIBLE
+
+
+def test_run_host_end_to_end():
+    sh = CONFIGS["r2"]
+    inp, ker = make_inputs(sh, seed=0)
+    plan = conv.ConvPlan(*sh.as_tuple(), path="tf32")
+    dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device="cuda")
+    out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+    plan.run_host(inp.pin_memory(), ker.pin_memory(), out_h, dbuf)
+    torch.cuda.synchronize()
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert rel_l2(out_h.numpy(), ref) <= TOL["tf32"]
+
+
+def test_run_events_records_each_kernel():
+    sh = CONFIGS["det"]
+    inp, ker = make_inputs(sh, seed=0)
+    for path in PATHS:
+        plan = conv.ConvPlan(*sh.as_tuple(), path=path)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(plan.num_kernels + 1)]
+        out = plan.new_output()
+        plan.run_events(inp.cuda(), ker.cuda(), out, plan.new_workspace(), ev)
+        torch.cuda.synchronize()
+        ts = [ev[i].elapsed_time(ev[i + 1]) for i in range(plan.num_kernels)]
+        assert all(t >= 0 for t in ts)
