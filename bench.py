@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""bench.py -- conv TFLOP/s of Eq. 1 on B200, BASELINE.json's
+metric: 2*N*K*H*W*C*R*S / time, plus % of roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--path tf32|bf16|fp32_simt|auto]
+                    [--config batched] [--scaling weak|strong] [--gather] [--impl ours|reference]
+
+A "step" is one conv_run over the workload (all of its kernels: the layout
+transforms and the main kernel, PAPER.md:371/425/624 count them).  Timing
+follows the paper's protocol: each run is timed individually
+on the device with CUDA events on the launching stream, with an L2 flush
+(a write of a buffer >= 2x L2) before every run, outside the event pair.
+The K timed runs are bracketed by a barrier + synchronize on both sides and
+the reported time is the max over ranks.
+
+Multi-GPU (torchrun, one process per GPU, NCCL): the batched layer shards by
+batch n (only non-reduction dims are parallelised).  Default
+"weak": every rank convolves its own batch of 256 images (independent units,
+no data-path collective); "strong": the 256 images are split across ranks.
+--gather runs NCCL all_gather_into_tensor of the Out slabs after the timed
+region and reports its time separately.
+
+--impl reference times the CPU oracle (oracle/, plain C, double) as it stands
+on the host cores, on bounded samples of the same workload, same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2101_09808_b200.inputs import CONFIGS, Shape, make_inputs  # noqa: E402
+
+METRIC = "conv TFLOP/s (2*N*K*H*W*C*R*S / time)"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def path_peak(path, peaks):
+    """Peak for the dominant kernel's arithmetic (TFLOP/s) and its bound."""
+    if path == "bf16":
+        return peaks["bf16_tflops"], "tensor", "measured cuBLAS bf16 burst (MEASURED_PEAKS.json)"
+    if path == "tf32":
+        # kind::tf32 issues at half the kind::f16 rate (nominal 1.1 vs 2.25 PF dense)
+        return peaks["bf16_tflops"] * 0.5, "tensor", "measured bf16 burst x 0.5 (nominal tf32/bf16 ratio)"
+    # FP32 SIMT: 148 SMs x 128 FFMA lanes x 2 flop x max SM clock
+    return 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, "alu", \
+        "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (derived)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+        self._t = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self._proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(s[0]) for s in self.samples if num(s[0])]
+        mx = [num(s[1]) for s in self.samples if num(s[1])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(args, world):
+    base = CONFIGS[args.config]
+    if args.scaling == "strong" and world > 1:
+        if base.N % world:
+            raise SystemExit(f"N={base.N} not divisible by {world}")
+        return base, Shape(base.N // world, base.K, base.C, base.H, base.W, base.R, base.S)
+    return base, base
+
+
+def bench_ours(args):
+    import torch.distributed as dist
+
+    from paper_2101_09808_b200 import conv
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    full, sh = workload(args, world)
+
+    # inputs: seeded on the CPU; weak scaling gives every rank its own batch
+    if args.scaling == "strong" and world > 1:
+        inp_all, ker = make_inputs(full, seed=0)
+        inp = inp_all[rank * sh.N:(rank + 1) * sh.N].contiguous()
+    else:
+        inp, ker = make_inputs(sh, seed=rank)
+    inp_h, ker_h = inp.pin_memory(), ker.pin_memory()
+    d_in, d_ker = inp_h.to(dev), ker_h.to(dev)
+    plan = conv.ConvPlan(*sh.as_tuple(), path=args.path)
+    desc = plan.describe()
+    d_out = plan.new_output(dev)
+    ws = plan.new_workspace(dev)
+    props = torch.cuda.get_device_properties(dev)
+    l2 = getattr(props, "L2_cache_size", 126 << 20)
+    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    nk = plan.num_kernels
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    for _ in range(args.warmup):
+        flush.zero_()
+        plan.run(d_in, d_ker, d_out, ws)
+    torch.cuda.synchronize(dev)
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        flush.zero_()                                   # L2 flush, outside the event pair
+        plan.run_events(d_in, d_ker, d_out, ws, evs[i])
+    torch.cuda.synchronize(dev)
+    barrier()
+    clocks.stop()
+    per_kernel = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(nk)] for e in evs])  # ms
+    step_ms = per_kernel.sum(axis=1)
+    ms = float(step_ms.mean())
+    main_ms = float(per_kernel[:, -1].mean())
+
+    # end-to-end through the C ABI with pinned host buffers (H2D + conv + D2H)
+    dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device=dev)
+    out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+    for _ in range(max(1, args.warmup)):
+        plan.run_host(inp_h, ker_h, out_h, dbuf)
+    torch.cuda.synchronize(dev)
+    e2e_ms = []
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        plan.run_host(inp_h, ker_h, out_h, dbuf)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    torch.cuda.synchronize(dev)
+    e2e = float(np.mean(e2e_ms))
+
+    gather = None
+    if args.gather and world > 1:
+        full_out = torch.empty((world,) + tuple(d_out.shape), dtype=torch.float32, device=dev)
+        dist.all_gather_into_tensor(full_out, d_out)      # warm-up
+        torch.cuda.synchronize(dev)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            dist.all_gather_into_tensor(full_out, d_out)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        g_ms = a.elapsed_time(b) / args.steps
+        gather = {"ms": g_ms, "bytes_recv_per_gpu": (world - 1) * d_out.numel() * 4}
+
+    # max over ranks
+    vals = torch.tensor([ms, main_ms, e2e, gather["ms"] if gather else 0.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, main_ms, e2e, g_ms = vals.tolist()
+    if gather:
+        gather["ms"] = g_ms
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        peak, bound, peak_note = path_peak(plan.path, peaks)
+        flops_rank = sh.flops
+        total_flops = flops_rank * world
+        value = total_flops / (ms * 1e-3) / 1e12
+        achieved = flops_rank / (main_ms * 1e-3) / 1e12
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get(f"{args.config}:{plan.path}")
+        roof_us = max(sh.flops / (peak * 1e12), sh.compulsory_bytes / (peaks["hbm_gbs"] * 1e9)) * 1e6
+        line = {
+            "metric": METRIC,
+            "value": round(value, 3),
+            "unit": "TFLOP/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 5),
+            "higher_is_better": True,
+            "scaling": "weak" if (args.scaling == "weak" or world == 1) else "strong",
+            "vs_baseline": None,
+            "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32_simt": "f32"}[plan.path],
+            "data": "synthetic (seeded uniform[-1,1), BASELINE.json configs)",
+            "config": {
+                "workload": f"{args.config}: N={sh.N} K={sh.K} C={sh.C} out {sh.H}x{sh.W} R={sh.R} S={sh.S} "
+                            f"(stride 1, no pad, fp32 NCHW/KCRS){' per rank' if world > 1 else ''}",
+                "path": plan.path,
+                "tile": desc["tile"],
+                "l2": "flushed before every timed step (write of 2x L2), outside the event pair",
+                "parallelism": f"n-shard x{world}" if world > 1 else "single GPU",
+                "kernels_per_step": nk,
+            },
+            "roofline": {
+                "bound": bound,
+                "achieved": round(achieved, 2),
+                "peak": round(peak, 1),
+                "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4),
+                "traffic": traffic,
+                "kernel": "conv_igemm_tcgen05" if plan.path != "fp32_simt" else "conv_direct_simt",
+                "kernel_ms": round(main_ms, 5),
+                "peak_source": f"{peak_note}; {peak_src}",
+                "step_roofline_us": round(roof_us, 3),
+                "step_frac": round(roof_us / (ms * 1e3), 4),
+                "kernel_share_of_step": round(main_ms / ms, 4),
+            },
+            "e2e": {
+                "value": round(total_flops / (e2e * 1e-3) / 1e12, 3),
+                "unit": "TFLOP/s",
+                "ms_per_step": round(e2e, 4),
+                "h2d_bytes_per_step": 4 * (sh.N * sh.C * sh.Hin * sh.Win + sh.K * sh.C * sh.R * sh.S),
+                "d2h_bytes_per_step": 4 * sh.N * sh.K * sh.H * sh.W,
+                "api": "conv_run_host (C ABI, pinned host buffers)",
+            },
+            "gpu_launches": nk * args.steps,
+            "clocks": clocks.summary(),
+        }
+        if gather:
+            line["gather"] = gather
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(full, args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def oracle_sample_time(sh: Shape, n_img: int, threads: int):
+    import oracle
+    inp, ker = make_inputs(Shape(n_img, sh.K, sh.C, sh.H, sh.W, sh.R, sh.S), seed=0)
+    x, w = inp.numpy(), ker.numpy()
+    t0 = time.perf_counter()
+    oracle.conv_eq1(x, w, nthreads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(sh: Shape, args, target_s: float = 10.0):
+    """The oracle as it stands, on the host cores, on a bounded sample of the
+    workload (the first n images of the batch, sized for ~target_s)."""
+    import oracle
+    threads = oracle.host_threads()
+    used = oracle.num_threads(threads)
+    t1 = oracle_sample_time(sh, 1, threads)
+    n = int(max(1, min(sh.N, target_s / max(t1, 1e-6))))
+    t = oracle_sample_time(sh, n, threads) if n > 1 else t1
+    flops = 2.0 * n * sh.K * sh.H * sh.W * sh.C * sh.R * sh.S
+    return {"value": round(flops / t / 1e12, 6), "unit": "TFLOP/s", "cores": used, "kind": "oracle",
+            "sample": f"first {n} of {sh.N} images of the {args.config} layer ({t:.1f} s, double accumulation, "
+                      f"OpenMP over (n,k) planes)"}
+
+
+def bench_reference(args):
+    """--impl reference: the oracle on the host cores, same metric."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    sh = CONFIGS[args.config]
+    threads = oracle.host_threads()
+    used = oracle.num_threads(threads)
+    t1 = oracle_sample_time(sh, 1, threads)
+    # each step: a bounded sample so that warmup+steps finish in a few minutes
+    n = int(max(1, min(sh.N, 8.0 / max(t1, 1e-6))))
+    for _ in range(args.warmup):
+        oracle_sample_time(sh, 1, threads)
+    ts = [oracle_sample_time(sh, n, threads) for _ in range(args.steps)]
+    ms = float(np.mean(ts)) * 1e3
+    flops = 2.0 * n * sh.K * sh.H * sh.W * sh.C * sh.R * sh.S
+    value = flops / (ms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform[-1,1), BASELINE.json configs)",
+        "config": {"workload": f"{args.config}: N={sh.N} K={sh.K} C={sh.C} out {sh.H}x{sh.W} R={sh.R} S={sh.S}",
+                   "sample_images_per_step": n},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": used, "kind": "oracle",
+                         "sample": f"first {n} of {sh.N} images per step"},
+        "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--path", default="bf16", choices=["auto", "fp32_simt", "tf32", "bf16"])
+    ap.add_argument("--config", default="batched", choices=list(CONFIGS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--gather", action="store_true")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -97,6 +97,11 @@ def _check(status: int):
         raise ConvError(status, last_error())
 
 
+def torch_current_stream(device=None):
+    import torch
+    return torch.cuda.current_stream(device)
+
+
 def _stream_handle(stream) -> Optional[int]:
     import torch
     if stream is None:
@@ -198,6 +203,10 @@ class ConvPlan:
         each kernel on ``stream``."""
         self._check_tensors(inp, ker, out)
         n = len(events)
+        s = stream if stream is not None else torch_current_stream(inp.device)
+        for e in events:
+            if not e.cuda_event:          # torch creates the cudaEvent_t lazily, on first record
+                e.record(s)
         arr = (ctypes.c_void_p * n)(*[e.cuda_event for e in events])
         ws = workspace.data_ptr() if workspace is not None and self.workspace_bytes else None
         _check(self._lib.conv_run_events(self._h, inp.data_ptr(), ker.data_ptr(), out.data_ptr(), ws,

@@ -325,7 +325,14 @@ static conv_status run_impl(const conv_plan* p, const float* in, const float* ke
     cudaEvent_t ev[4];
     cudaEvent_t* evp = nullptr;
     if (events) {
-        for (int i = 0; i <= nk; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
+        for (int i = 0; i <= nk; ++i) {
+            ev[i] = static_cast<cudaEvent_t>(events[i]);
+            const cudaError_t q = ev[i] ? cudaEventQuery(ev[i]) : cudaErrorInvalidResourceHandle;
+            if (q != cudaSuccess && q != cudaErrorNotReady) {
+                cudaGetLastError();
+                return fail(CONV_ERR_INVALID_ARGUMENT, "events[%d] is not a valid cudaEvent_t", i);
+            }
+        }
         evp = ev;
     }
     std::string err;
