@@ -43,6 +43,7 @@ struct Device {
 struct TcTile {
     int bn = 128;        // GEMM-N tile (output channels), multiple of 32, <= 256
     int stages = 4;      // smem ring depth
+    int cg = 1;          // CTAs per MMA: 1 (M = 128) or 2 (CTA pair, M = 256)
 };
 
 struct TcLayout {        // derived from Problem + element size

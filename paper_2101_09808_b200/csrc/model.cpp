@@ -147,10 +147,11 @@ static double wave_eff(long tiles, long slots) {
 // k tile, r, s, c-block.  In and Ker are case 1 (innermost ct), i.e. the
 // im2col replay; Out leaves the SM from TMEM straight to global, so only
 // In + Ker cross L2 -> SMEM.
-static double tc_dv_l2_smem_bytes(const Problem& pb, const TcLayout& L, int bn) {
+static double tc_dv_l2_smem_bytes(const Problem& pb, const TcLayout& L, int bn, int cg) {
     const int perm[7] = {I_N, I_H, I_W, I_K, I_R, I_S, I_C};
     const double Nx[7] = {1, (double)pb.K, (double)L.Cp, (double)pb.R, (double)pb.S, 1, (double)pb.M()};
-    const double T[7] = {1, (double)std::min(bn, pb.K), (double)L.bkc, 1, 1, 1, (double)std::min<int64_t>(128, pb.M())};
+    const double T[7] = {1, (double)std::min(bn, pb.K), (double)L.bkc, 1, 1, 1,
+                         (double)std::min<int64_t>(128 * cg, pb.M())};
     double dv[3];
     conv_model_dv(perm, Nx, T, dv);
     // Trip counts are ceil(N/T): partial tiles are charged as full tiles
@@ -158,18 +159,29 @@ static double tc_dv_l2_smem_bytes(const Problem& pb, const TcLayout& L, int bn) 
     return (dv[IN_] + dv[KER_]) * L.elem;
 }
 
+// Shared-memory port of one SM (128 B/clk): the TMA writes every operand byte
+// once and the tensor core reads it once.  The pair's B half is read by its
+// own SM only, so per SM per k-block: 2 * (128 + BN/cg) * sw bytes.
+static const double kSmemBytesPerClk = 128.0;
+static const double kClockHz = 1.75e9;   // SM clock seen under this load (ncu, r01)
+
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t) {
     ModelResult r;
     const TcLayout L = tc_layout(pb, bf16);
-    const long mt = (long)((pb.M() + 127) / 128), nt = (pb.K + t.bn - 1) / t.bn;
+    const long tm = 128L * t.cg;
+    const long mt = (long)((pb.M() + tm - 1) / tm), nt = (pb.K + t.bn - 1) / t.bn;
+    const long units = dev.sms / t.cg;
     r.tiles = mt * nt;
-    r.ctas = std::min<long>(r.tiles, dev.sms);
-    r.wave_eff = wave_eff(r.tiles, dev.sms);
+    r.ctas = std::min<long>(r.tiles, units) * t.cg;
+    r.wave_eff = wave_eff(r.tiles, units);
     const double peak = bf16 ? dev.peak_bf16 : dev.peak_tf32;
-    const double flops_issued = 2.0 * (double)mt * 128 * (double)nt * t.bn * (double)pb.R * pb.S * L.Cp;
+    const double flops_issued = 2.0 * (double)mt * tm * (double)nt * t.bn * (double)pb.R * pb.S * L.Cp;
     r.t_comp_us = flops_issued / peak * 1e6;
-    r.dv_l2_smem = tc_dv_l2_smem_bytes(pb, L, t.bn);
+    r.dv_l2_smem = tc_dv_l2_smem_bytes(pb, L, t.bn, t.cg);
     r.t_l2_us = r.dv_l2_smem / dev.bw_l2 * 1e6;
+    const double kblocks_per_sm = (double)r.tiles * pb.R * pb.S * L.n_cblk / units;
+    const double t_smem_us = kblocks_per_sm * 2.0 * (128.0 + (double)t.bn / t.cg) * L.sw /
+                             kSmemBytesPerClk / kClockHz * 1e6;
     // HBM: repacks (read fp32 In/Ker, write workspace) + main kernel (read
     // workspace once -- the 9x im2col replay and the k-tile re-reads hit L2 --
     // and write fp32 Out once).
@@ -177,42 +189,48 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     const double main_hbm = (double)L.in_ws_bytes + (double)L.ker_ws_bytes + 4.0 * pb.out_elems();
     r.dv_hbm = repack + main_hbm;
     r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
-    const double waves = ceil((double)r.tiles / dev.sms);
-    const double t_main = std::max({r.t_comp_us / r.wave_eff, r.t_l2_us / r.wave_eff, main_hbm / dev.bw_hbm * 1e6})
+    const double waves = ceil((double)r.tiles / units);
+    const double t_main = std::max({r.t_comp_us / r.wave_eff, r.t_l2_us / r.wave_eff, t_smem_us / r.wave_eff,
+                                    main_hbm / dev.bw_hbm * 1e6})
                           + waves * kTileOverheadUs + kLaunchUs;
-    const double t_rep = repack / (0.7 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
+    const double t_rep = repack / (0.8 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
     r.model_us = t_main + t_rep;
     r.smem = tc_smem_bytes(L, t);
     return r;
 }
 
-static int tc_max_stages(const Device& dev, const TcLayout& L, int bn) {
+static int tc_max_stages(const Device& dev, const TcLayout& L, int bn, int cg) {
     for (int s = 8; s >= 2; --s) {
         TcTile t;
         t.bn = bn;
         t.stages = s;
+        t.cg = cg;
         if (tc_smem_bytes(L, t) <= dev.smem_optin) return s;
     }
     return 0;
 }
 
 bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& best_r,
-               int force_bn, int force_stages, std::string& why) {
+               int force_bn, int force_stages, int force_cg, std::string& why) {
     const TcLayout L = tc_layout(pb, bf16);
     if (pb.R > 128 || pb.S > 128) { why = "R, S > 128: TMA im2col offsets are limited to [-128, 127]"; return false; }
-    if (pb.M() + 128 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
+    if (pb.M() + 256 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
     bool found = false;
-    for (int bn = 32; bn <= 256; bn += 32) {
-        if (force_bn && bn != force_bn) continue;
-        if (!force_bn && bn > ((pb.K + 31) / 32) * 32) continue;
-        const int smax = tc_max_stages(dev, L, bn);
-        if (smax < 2) continue;
-        TcTile t;
-        t.bn = bn;
-        t.stages = force_stages ? force_stages : smax;
-        if (t.stages < 2 || t.stages > smax) continue;
-        ModelResult r = model_tc(pb, dev, bf16, t);
-        if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+    for (int cg = 1; cg <= 2; ++cg) {
+        if (force_cg && cg != force_cg) continue;
+        for (int bn = 32; bn <= 256; bn += 32) {
+            if (force_bn && bn != force_bn) continue;
+            if (!force_bn && bn > ((pb.K + 31) / 32) * 32) continue;
+            const int smax = tc_max_stages(dev, L, bn, cg);
+            if (smax < 2) continue;
+            TcTile t;
+            t.bn = bn;
+            t.cg = cg;
+            t.stages = force_stages ? force_stages : smax;
+            if (t.stages < 2 || t.stages > smax) continue;
+            ModelResult r = model_tc(pb, dev, bf16, t);
+            if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+        }
     }
     if (!found) why = "no tensor-path tile fits shared memory / TMEM for this request";
     return found;
@@ -228,24 +246,29 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const size_t smem = simt_smem_bytes(pb, t);
     r.smem = smem;
     // Register level (Sec. 6 microkernel analog): TK*TW accumulators + TW + TK
-    // operands per thread; ~24 registers of addressing.
-    const int regs = t.tk * t.tw + t.tk + 3 * t.tw + 28;
-    const int by_regs = 65536 / (std::max(regs, 32) * threads);
+    // operands per thread plus addressing; ptxas caps at 128 (launch bounds 512).
+    const int regs = std::min(128, t.tk * t.tw + t.tk + 3 * t.tw + 32);
+    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * threads);
     const int by_smem = (int)(228 * 1024 / (smem + 1024));
     const int by_thr = 2048 / threads;
-    int per_sm = std::min({by_regs, by_smem, by_thr, 32});
+    const int per_sm = std::min({by_regs, by_smem, by_thr, 32});
     if (per_sm < 1) { r.model_us = 1e30; return r; }
+    // CTAs land round-robin on the SMs: the busiest SM runs ceil(tiles/SMs)
+    // of them, `conc` at a time.
+    const long per_sm_total = (r.tiles + dev.sms - 1) / dev.sms;
+    const long conc = std::min<long>(per_sm, per_sm_total);
+    const long waves = (per_sm_total + conc - 1) / conc;
     r.ctas = std::min<long>(r.tiles, (long)per_sm * dev.sms);
-    r.wave_eff = wave_eff(r.tiles, (long)per_sm * dev.sms);
-    // Issued FFMA lanes (idle pixel slots included) plus the LDS the register
-    // tile needs per (c,r,s): TW scalar + TK/4 vector loads per TK*TW FFMA.
-    const double slots = 32.0 * t.tw * t.pw;
-    const double lanes_fma = (double)r.tiles * slots * bko * (double)pb.C * pb.R * pb.S;
+    r.wave_eff = (double)r.tiles / ((double)dev.sms * per_sm_total);
+    // FFMA issue: 128 lanes/clk/SM at >= 8 resident warps (2 per SMSP hide
+    // the LDS latency), proportionally less below; the register tile costs
+    // TW scalar + TK/4 vector loads + ~1 address op per TK*TW FFMA.
+    const double warps = (double)conc * threads / 32.0;
+    const double eff = std::min(1.0, warps / 8.0);
     const double issue_factor = 1.0 + (t.tw + t.tk / 4.0 + 1.0) / (t.tk * t.tw);
-    r.t_comp_us = 2.0 * lanes_fma * issue_factor / dev.peak_fp32 * 1e6;
-    // Latency hiding: fewer than 8 warps per SM cannot keep 4 SMSPs busy.
-    const int warps_sm = per_sm * threads / 32;
-    if (warps_sm < 8) r.t_comp_us *= 8.0 / warps_sm;
+    const double lane_fma_cta = (double)threads * t.tk * t.tw * (double)pb.C * pb.R * pb.S * issue_factor;
+    const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
+    r.t_comp_us = waves * conc * lane_fma_cta / (128.0 * eff * clk) * 1e6;
     // L2 -> SMEM: per CTA, every c-chunk loads the In halo tile and Ker slab
     // (Eq. 4's In and Ker footprints).
     const double in_stage = (double)t.bc * t.tn * (t.th + pb.R - 1) * pb.Win();
@@ -255,7 +278,7 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     r.t_l2_us = r.dv_l2_smem / dev.bw_l2 * 1e6;
     r.dv_hbm = 4.0 * (pb.in_elems() + 2.0 * pb.ker_elems() + pb.out_elems());
     r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
-    r.model_us = std::max({r.t_comp_us, r.t_l2_us}) / r.wave_eff + r.t_hbm_us * 0.2 + 2 * kLaunchUs;
+    r.model_us = std::max({r.t_comp_us, r.t_l2_us / r.wave_eff, r.t_hbm_us}) + 2 * kLaunchUs;
     return r;
 }
 
@@ -289,11 +312,12 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         if (forced && (forced_mask & 32)) th = forced->th;
         if (th < 1) continue;
         if ((long)tn * th * pb.W > slots) continue;
-        // slot utilisation >= 50%
-        if (2L * tn * th * pb.W < slots && !(forced && (forced_mask & 32))) continue;
+        // slot utilisation >= 50% unless the tile already covers all pixels
+        const bool whole = th >= pb.H && tn >= pb.N;
+        if (2L * tn * th * pb.W < slots && !whole && !(forced && (forced_mask & 32))) continue;
         t.th = th;
         if (simt_smem_bytes(pb, t) > dev.smem_optin) continue;
-        if (t.kg * t.tk > ((pb.K + 3) / 4) * 4 * 2 && !forced) continue;  // mostly-empty k tile
+        if (t.kg > 1 && t.kg * t.tk >= 2 * pb.K && !forced) continue;  // mostly-empty k tile
         ModelResult r = model_simt(pb, dev, t);
         if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
     }

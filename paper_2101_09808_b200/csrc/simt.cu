@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "internal.h"
 
 namespace conv {
@@ -211,8 +213,15 @@ template <int TK, int TW>
 static cudaError_t launch_simt_t(const float* in, const float* kerp, float* out, const SimtParams& p,
                                  dim3 grid, int threads, size_t smem, cudaStream_t st) {
     auto kfn = conv_direct_simt<TK, TW>;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    static std::atomic<int> smem_set{0};
+    if (smem_set.load(std::memory_order_acquire) < (int)smem) {
+        int optin = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        if (e != cudaSuccess) return e;
+        smem_set.store(optin, std::memory_order_release);
+    }
     kfn<<<grid, threads, smem, st>>>(in, kerp, out, p);
     return cudaGetLastError();
 }

@@ -24,6 +24,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -52,7 +56,14 @@ struct TcParams {
     uint32_t b_stage_bytes;   // bn * sw
 };
 
-template <int BN, bool BF16>
+// CG = 1: one CTA per 128-pixel tile (tcgen05 cta_group::1, M = 128).
+// CG = 2: a CTA pair (cluster of 2 on one TPC) per 256-pixel tile
+//   (cta_group::2, M = 256): each CTA loads its own 128 A rows and HALF of
+//   the BN B rows; the leader CTA issues the MMAs, which read both CTAs'
+//   shared memory, and each CTA's TMEM receives its own 128 accumulator rows.
+//   Per SM this halves the B operand traffic (L2 -> SMEM and SMEM -> tensor
+//   core), which is what bounds the 1-CTA kernel on wide tiles.
+template <int BN, bool BF16, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const TcParams p) {
@@ -72,6 +83,10 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     const uint32_t lane = threadIdx.x & 31;
     constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;       // position in the pair
+    const bool leader = rank == 0;
+    const int unit = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;   // pair / CTA index
+    const int nunits = CG == 2 ? (int)nclusters_x() : (int)gridDim.x;
 
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmap_a);
@@ -82,42 +97,54 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
-            mbar_init(&tmem_empty[i], 128);
+            mbar_init(&tmem_empty[i], 4 * CG);    // one arrive per epilogue warp of the pair
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 2) {
+        if (CG == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
+        else tmem_alloc(tmem_slot, kTmemCols);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===== TMA producer =====
+        // ===== TMA producer (both CTAs of a pair) =====
         if (lane == 0) {
             const uint64_t pol_a = policy_evict_normal();
             const uint64_t pol_b = policy_evict_last();   // Ker is re-read by every M tile
-            const uint32_t tx_bytes = p.a_stage_bytes + p.b_stage_bytes;
+            const uint32_t tx_bytes = CG * (p.a_stage_bytes + p.b_stage_bytes);
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            for (int tile = unit; tile < p.num_tiles; tile += nunits) {
                 const int m_tile = tile / p.num_n_tiles;
                 const int n_tile = tile - m_tile * p.num_n_tiles;
-                const int m0 = m_tile * kBM;
+                const int m0 = m_tile * (kBM * CG) + (int)rank * kBM;
                 const int img = m0 / p.HW;
                 const int pix = m0 - img * p.HW;
                 const int h0 = pix / p.W;
                 const int w0 = pix - h0 * p.W;
-                const int k0 = n_tile * BN;
+                const int kb0 = n_tile * BN + (int)rank * (BN / CG);   // this CTA's B rows
                 for (int r = 0; r < p.R; ++r) {
                     for (int s = 0; s < p.S; ++s) {
                         for (int cb = 0; cb < p.n_cblk; ++cb) {
                             mbar_wait(&empty[stage], phase ^ 1);
-                            mbar_arrive_expect_tx(&full[stage], tx_bytes);
-                            tma_load_im2col_4d(smem_a + (size_t)stage * p.a_stage_bytes, &tmap_a, &full[stage],
-                                               cb * p.bkc, w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
-                            tma_load_2d(smem_b + (size_t)stage * p.b_stage_bytes, &tmap_b, &full[stage],
-                                        (r * p.S + s) * p.Cp + cb * p.bkc, k0, pol_b);
+                            uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
+                            uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
+                            const int bx = (r * p.S + s) * p.Cp + cb * p.bkc;
+                            if (CG == 2) {
+                                if (leader) mbar_arrive_expect_tx(&full[stage], tx_bytes);
+                                tma_load_im2col_4d_pair(a_dst, &tmap_a, &full[stage], cb * p.bkc, w0, h0, img,
+                                                        (uint16_t)s, (uint16_t)r, pol_a);
+                                tma_load_2d_pair(b_dst, &tmap_b, &full[stage], bx, kb0, pol_b);
+                            } else {
+                                mbar_arrive_expect_tx(&full[stage], tx_bytes);
+                                tma_load_im2col_4d(a_dst, &tmap_a, &full[stage], cb * p.bkc, w0, h0, img,
+                                                   (uint16_t)s, (uint16_t)r, pol_a);
+                                tma_load_2d(b_dst, &tmap_b, &full[stage], bx, kb0, pol_b);
+                            }
                             if (++stage == p.stages) { stage = 0; phase ^= 1; }
                         }
                     }
@@ -125,9 +152,9 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer =====
-        if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(BF16 ? 1u : 2u, kBM, BN);
+        // ===== MMA issuer (leader CTA only) =====
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = make_idesc(BF16 ? 1u : 2u, kBM * CG, BN);
             const uint32_t layout = umma_layout_for_swizzle(p.sw);
             const uint32_t sbo = 8 * p.sw;
             const int k_steps = (int)(p.sw / 32);   // 32 B of K per MMA (8 tf32 / 16 bf16)
@@ -135,7 +162,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            for (int tile = unit; tile < p.num_tiles; tile += nunits) {
                 mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -148,26 +175,35 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                         const uint64_t ad = make_sdesc(a_addr + kk * 32, sbo, layout);
                         const uint64_t bd = make_sdesc(b_addr + kk * 32, sbo, layout);
                         const uint32_t accum = (it > 0 || kk > 0) ? 1u : 0u;
-                        if (BF16) mma_bf16(d_tmem, ad, bd, idesc, accum);
-                        else      mma_tf32(d_tmem, ad, bd, idesc, accum);
+                        if (CG == 2) {
+                            if (BF16) mma_bf16_pair(d_tmem, ad, bd, idesc, accum);
+                            else      mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
+                        } else {
+                            if (BF16) mma_bf16(d_tmem, ad, bd, idesc, accum);
+                            else      mma_tf32(d_tmem, ad, bd, idesc, accum);
+                        }
                     }
-                    tc_commit(&empty[stage]);          // frees the smem slot when the MMAs retire
+                    // frees the smem slot (in both CTAs) when the MMAs retire
+                    if (CG == 2) tc_commit_pair_mc(&empty[stage], 0x3);
+                    else tc_commit(&empty[stage]);
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
                 }
-                tc_commit(&tmem_full[acc]);            // accumulator ready for the epilogue
+                // accumulator ready for the epilogue (of both CTAs)
+                if (CG == 2) tc_commit_pair_mc(&tmem_full[acc], 0x3);
+                else tc_commit(&tmem_full[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> NCHW Out =====
         const int q = warp & 3;                       // TMEM lane quadrant of this warp
-        const int row = q * 32 + (int)lane;           // accumulator row = pixel within the tile
+        const int row = q * 32 + (int)lane;           // accumulator row = pixel within the CTA's tile
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (int tile = unit; tile < p.num_tiles; tile += nunits) {
             const int m_tile = tile / p.num_n_tiles;
             const int n_tile = tile - m_tile * p.num_n_tiles;
-            const int m = m_tile * kBM + row;
+            const int m = m_tile * (kBM * CG) + (int)rank * kBM + row;
             const int k0 = n_tile * BN;
             const bool valid_m = m < p.M;
             const int img = valid_m ? m / p.HW : 0;
@@ -196,15 +232,23 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tmem_empty[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_leader(&tmem_empty[acc]);
+                else mbar_arrive(&tmem_empty[acc]);
+            }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
 
-    __syncthreads();
+    // Teardown: every MMA has retired (the epilogues consumed every
+    // accumulator) before the TMEM is released.
+    tc_fence_before();
+    if (CG == 2) cluster_sync_all(); else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, kTmemCols);
+        if (CG == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
+        else tmem_dealloc(tmem_base, kTmemCols);
     }
 }
 
@@ -229,7 +273,7 @@ TcLayout tc_layout(const Problem& pb, bool bf16) {
 }
 
 size_t tc_smem_bytes(const TcLayout& L, const TcTile& t) {
-    const size_t a = (size_t)kBM * L.sw, b = (size_t)t.bn * L.sw;
+    const size_t a = (size_t)kBM * L.sw, b = (size_t)(t.bn / t.cg) * L.sw;
     return 1024 /*align slack*/ + (size_t)t.stages * (a + b) + (2 * t.stages + 4) * 8 + 16;
 }
 
@@ -238,28 +282,47 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-template <int BN, bool BF16>
+template <int BN, bool BF16, int CG>
 static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& prm,
                              size_t smem, int grid, cudaStream_t st) {
-    auto kfn = conv_igemm_tcgen05<BN, BF16>;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kfn<<<grid, kThreads, smem, st>>>(ta, tb, prm);
-    return cudaGetLastError();
+    auto kfn = conv_igemm_tcgen05<BN, BF16, CG>;
+    // Opt in to the largest dynamic smem once per instantiation (per process).
+    static std::atomic<int> smem_set{0};
+    if (smem_set.load(std::memory_order_acquire) < (int)smem) {
+        int optin = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        if (e != cudaSuccess) return e;
+        smem_set.store(optin, std::memory_order_release);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, ta, tb, prm);
 }
 
-template <bool BF16>
+template <bool BF16, int CG>
 static cudaError_t launch_tc_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                                 const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
     switch (bn) {
-        case 32: return launch_tc<32, BF16>(ta, tb, prm, smem, grid, st);
-        case 64: return launch_tc<64, BF16>(ta, tb, prm, smem, grid, st);
-        case 96: return launch_tc<96, BF16>(ta, tb, prm, smem, grid, st);
-        case 128: return launch_tc<128, BF16>(ta, tb, prm, smem, grid, st);
-        case 160: return launch_tc<160, BF16>(ta, tb, prm, smem, grid, st);
-        case 192: return launch_tc<192, BF16>(ta, tb, prm, smem, grid, st);
-        case 224: return launch_tc<224, BF16>(ta, tb, prm, smem, grid, st);
-        case 256: return launch_tc<256, BF16>(ta, tb, prm, smem, grid, st);
+        case 32: return launch_tc<32, BF16, CG>(ta, tb, prm, smem, grid, st);
+        case 64: return launch_tc<64, BF16, CG>(ta, tb, prm, smem, grid, st);
+        case 96: return launch_tc<96, BF16, CG>(ta, tb, prm, smem, grid, st);
+        case 128: return launch_tc<128, BF16, CG>(ta, tb, prm, smem, grid, st);
+        case 160: return launch_tc<160, BF16, CG>(ta, tb, prm, smem, grid, st);
+        case 192: return launch_tc<192, BF16, CG>(ta, tb, prm, smem, grid, st);
+        case 224: return launch_tc<224, BF16, CG>(ta, tb, prm, smem, grid, st);
+        case 256: return launch_tc<256, BF16, CG>(ta, tb, prm, smem, grid, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -271,12 +334,33 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     void* in_ws = wsb;
     void* ker_ws = wsb + align_up(L.in_ws_bytes, 256);
 
-    // Tensor maps are encoded per call (the workspace address is only known
-    // here); encoding is a host-only call of ~1 us.
+    // Tensor maps depend on the workspace address, known only here; they are
+    // encoded on first use and cached per (workspace, problem, tile).
+    struct Key {
+        const void* ws; Problem pb; int bn; int cg; int bf16; int dev;
+    };
+    struct Entry { Key k; CUtensorMap ta, tb; };
+    static std::mutex mu;
+    static Entry cache[16];
+    static int n_cached = 0, next_slot = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const Key key{ws, pb, t.bn, t.cg, bf16 ? 1 : 0, dev};
+    auto same = [&](const Key& a) {
+        return a.ws == key.ws && memcmp(&a.pb, &key.pb, sizeof(Problem)) == 0 && a.bn == key.bn && a.cg == key.cg &&
+               a.bf16 == key.bf16 && a.dev == key.dev;
+    };
+    CUtensorMap ta, tb;
+    bool hit = false;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (int i = 0; i < n_cached; ++i)
+            if (same(cache[i].k)) { ta = cache[i].ta; tb = cache[i].tb; hit = true; break; }
+    }
+    if (!hit) {
     const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const CUtensorMapSwizzle swz = L.sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                    : (L.sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
-    CUtensorMap ta, tb;
     {
         // In NHWC: dims (C, W, H, N) innermost first.
         cuuint64_t dims[4] = {(cuuint64_t)L.Cp, (cuuint64_t)pb.Win(), (cuuint64_t)pb.Hin(), (cuuint64_t)pb.N};
@@ -296,12 +380,17 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         // Ker KRSC as 2-D [K rows][R*S*Cp cols].
         cuuint64_t dims[2] = {(cuuint64_t)pb.R * pb.S * L.Cp, (cuuint64_t)pb.K};
         cuuint64_t strides[1] = {(cuuint64_t)pb.R * pb.S * L.Cp * L.elem};
-        cuuint32_t box[2] = {(cuuint32_t)L.bkc, (cuuint32_t)t.bn};
+        cuuint32_t box[2] = {(cuuint32_t)L.bkc, (cuuint32_t)(t.bn / t.cg)};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = g_encode_tiled(&tb, dt, 2, ker_ws, dims, strides, box, estr,
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
+    }
+    std::lock_guard<std::mutex> g(mu);
+    cache[next_slot] = Entry{key, ta, tb};
+    next_slot = (next_slot + 1) % 16;
+    if (n_cached < 16) ++n_cached;
     }
 
     cudaError_t e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev);
@@ -320,16 +409,22 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     prm.n_cblk = L.n_cblk;
     prm.k_iters = pb.R * pb.S * L.n_cblk;
     prm.num_n_tiles = (pb.K + t.bn - 1) / t.bn;
-    const int num_m_tiles = (int)((pb.M() + kBM - 1) / kBM);
+    const int tile_m = kBM * t.cg;
+    const int num_m_tiles = (int)((pb.M() + tile_m - 1) / tile_m);
     prm.num_tiles = num_m_tiles * prm.num_n_tiles;
     prm.stages = t.stages;
     prm.sw = (uint32_t)L.sw;
     prm.a_stage_bytes = (uint32_t)(kBM * L.sw);
-    prm.b_stage_bytes = (uint32_t)(t.bn * L.sw);
-    const int grid = prm.num_tiles < num_sms ? prm.num_tiles : num_sms;
+    prm.b_stage_bytes = (uint32_t)((t.bn / t.cg) * L.sw);
+    const int units = num_sms / t.cg;
+    const int grid = (prm.num_tiles < units ? prm.num_tiles : units) * t.cg;
     const size_t smem = tc_smem_bytes(L, t);
-    e = bf16 ? launch_tc_bn<true>(t.bn, ta, tb, prm, smem, grid, st)
-             : launch_tc_bn<false>(t.bn, ta, tb, prm, smem, grid, st);
+    if (t.cg == 2)
+        e = bf16 ? launch_tc_bn<true, 2>(t.bn, ta, tb, prm, smem, grid, st)
+                 : launch_tc_bn<false, 2>(t.bn, ta, tb, prm, smem, grid, st);
+    else
+        e = bf16 ? launch_tc_bn<true, 1>(t.bn, ta, tb, prm, smem, grid, st)
+                 : launch_tc_bn<false, 1>(t.bn, ta, tb, prm, smem, grid, st);
     if (e != cudaSuccess) { err = std::string("tcgen05 kernel launch failed: ") + cudaGetErrorString(e); return e; }
     if (ev) cudaEventRecord(ev[3], st);
     return cudaSuccess;

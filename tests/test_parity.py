@@ -68,6 +68,22 @@ def test_integer_twin_bit_exact(path, shape):
     assert np.array_equal(got.astype(np.float64), ref)
 
 
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("shape", SMALL + ODD[:4], ids=lambda s: "x".join(map(str, s.as_tuple())))
+def test_tensor_cta_group_variants(path, cg, shape):
+    """Both the 1-CTA (M=128) and the CTA-pair (M=256) kernels, forced."""
+    inp, ker = make_inputs(shape, seed=1, kind="int")
+    got, plan = run(shape, inp, ker, path, tile=f"cg={cg}")
+    assert plan.describe()["tile"]["cg"] == cg
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert np.array_equal(got.astype(np.float64), ref)
+    inp, ker = make_inputs(shape, seed=0)
+    got, _ = run(shape, inp, ker, path, tile=f"cg={cg}")
+    ref = oracle.conv_eq1(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()))
+    assert rel_l2(got, ref) <= 1e-5
+
+
 @pytest.mark.parametrize("path", PATHS)
 def test_p1_identity(path):
     """P1: 1x1 identity kernel reproduces round_path(In) exactly."""
@@ -100,10 +116,11 @@ def test_p10_tile_invariance_tensor(path):
     sh = Shape(N=2, K=256, C=64, H=12, W=12, R=3, S=3)
     inp, ker = make_inputs(sh, seed=7)
     outs = []
-    for bn in (32, 64, 128, 256):
-        got, plan = run(sh, inp, ker, path, tile=f"bn={bn}")
-        assert plan.describe()["tile"]["bn"] == bn
-        outs.append(got)
+    for cg in (1, 2):
+        for bn in (32, 64, 128, 256):
+            got, plan = run(sh, inp, ker, path, tile=f"bn={bn},cg={cg}")
+            assert plan.describe()["tile"]["bn"] == bn and plan.describe()["tile"]["cg"] == cg
+            outs.append(got)
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
 
