@@ -72,6 +72,14 @@ typedef enum {
  * tensor has >= 2^31 elements; UNSUPPORTED_DEVICE without an sm_100 device. */
 CONV_API conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R, int S);
 
+/* A plan for a described (not present) device: `sms` SMs, `smem_optin` bytes
+ * of opt-in shared memory per block, `l2_bytes` of L2.  Runs the same
+ * selector; the plan can be described but not run (conv_run returns
+ * CONV_ERR_UNSUPPORTED_DEVICE).  For the selector's CPU tests and offline
+ * studies.  NULL on invalid arguments. */
+CONV_API conv_plan* conv_plan_create_offline(int N, int K, int C, int H, int W, int R, int S,
+                                             int sms, size_t smem_optin, size_t l2_bytes);
+
 /* Force a path (default AUTO) and re-run the selector for it.
  * INFEASIBLE if no candidate of that path fits (e.g. R or S > 128 on the
  * tensor paths: TMA im2col offsets are limited to [-128, 127]). */

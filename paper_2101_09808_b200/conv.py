@@ -28,7 +28,7 @@ PATH_NAMES = {v: k for k, v in PATHS.items()}
 
 # Every symbol include/conv.h declares (tests check the library exports them).
 EXPORTED = (
-    "conv_plan_create", "conv_plan_set_path", "conv_plan_set_tile", "conv_plan_workspace_bytes",
+    "conv_plan_create", "conv_plan_create_offline", "conv_plan_set_path", "conv_plan_set_tile", "conv_plan_workspace_bytes",
     "conv_plan_num_kernels", "conv_plan_path", "conv_plan_describe", "conv_plan_destroy",
     "conv_run", "conv_run_events", "conv_plan_host_run_bytes", "conv_run_host",
     "conv_last_error", "conv_version", "conv_model_dv", "conv_model_dv_matmul",
@@ -59,6 +59,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         vp, sz, i, d = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_double
         sig = {
             "conv_plan_create": (vp, [i] * 7),
+            "conv_plan_create_offline": (vp, [i] * 8 + [sz, sz]),
             "conv_plan_set_path": (i, [vp, i]),
             "conv_plan_set_tile": (i, [vp, ctypes.c_char_p]),
             "conv_plan_workspace_bytes": (sz, [vp]),
@@ -113,13 +114,24 @@ class ConvPlan:
     """A plan for Eq. 1 with OUTPUT extents H x W."""
 
     def __init__(self, N: int, K: int, C: int, H: int, W: int, R: int, S: int,
-                 path: str = "auto", tile: Optional[str] = None):
+                 path: str = "auto", tile: Optional[str] = None, offline_device: Optional[dict] = None):
+        """``offline_device`` = dict(sms=, smem_optin=, l2_bytes=) plans for a
+        described device without touching CUDA (describe-only plan)."""
         lib = load_library()
         self._lib = lib
         self.shape = (N, K, C, H, W, R, S)
-        h = lib.conv_plan_create(N, K, C, H, W, R, S)
+        if offline_device is not None:
+            d = offline_device
+            h = lib.conv_plan_create_offline(N, K, C, H, W, R, S, int(d["sms"]), int(d["smem_optin"]),
+                                             int(d["l2_bytes"]))
+        else:
+            h = lib.conv_plan_create(N, K, C, H, W, R, S)
         if not h:
-            raise ConvError(CONV_ERR_INVALID_ARGUMENT, last_error())
+            msg = last_error()
+            status = CONV_ERR_UNSUPPORTED_DEVICE if ("device" in msg and "extent" not in msg) else CONV_ERR_INVALID_ARGUMENT
+            if "no " in msg and "tile" in msg:
+                status = CONV_ERR_INFEASIBLE
+            raise ConvError(status, msg)
         self._h = ctypes.c_void_p(h)
         if path != "auto":
             self.set_path(path)
@@ -282,3 +294,7 @@ def model_footprint(T: dict) -> float:
     lib = load_library()
     t = (ctypes.c_double * 7)(*[float(T[x]) for x in ["n", "k", "c", "r", "s", "h", "w"]])
     return lib.conv_model_footprint(t)
+
+
+# B200 as the selector sees it (for offline plans in CPU tests / studies).
+B200 = dict(sms=148, smem_optin=232448, l2_bytes=132120576)

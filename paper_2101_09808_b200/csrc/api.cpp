@@ -171,6 +171,35 @@ extern "C" conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R,
     return p;
 }
 
+extern "C" conv_plan* conv_plan_create_offline(int N, int K, int C, int H, int W, int R, int S, int sms,
+                                                size_t smem_optin, size_t l2_bytes) {
+    if (N < 1 || K < 1 || C < 1 || H < 1 || W < 1 || R < 1 || S < 1) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "extent must be >= 1 (N=%d K=%d C=%d H=%d W=%d R=%d S=%d)", N, K, C, H, W, R, S);
+        return nullptr;
+    }
+    if (sms < 2 || smem_optin < 16384 || l2_bytes == 0) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "device description out of range");
+        return nullptr;
+    }
+    Problem pb{N, K, C, H, W, R, S};
+    const int64_t lim = (int64_t)1 << 31;
+    if (pb.in_elems() >= lim || pb.ker_elems() >= lim || pb.out_elems() >= lim) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "tensor with >= 2^31 elements is not supported");
+        return nullptr;
+    }
+    conv_plan* p = new conv_plan();
+    p->pb = pb;
+    p->dev.ordinal = -1;                 // not bound to a device: cannot run
+    p->dev.sms = sms;
+    p->dev.smem_optin = smem_optin;
+    p->dev.l2_bytes = l2_bytes;
+    if (select(p) != CONV_OK) {
+        delete p;
+        return nullptr;
+    }
+    return p;
+}
+
 extern "C" conv_status conv_plan_set_path(conv_plan* p, conv_path path) {
     if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
     if (path < CONV_PATH_AUTO || path > CONV_PATH_BF16) return fail(CONV_ERR_INVALID_ARGUMENT, "unknown path %d", (int)path);
@@ -320,6 +349,7 @@ static conv_status run_impl(const conv_plan* p, const float* in, const float* ke
     };
     if (overlaps(in, 4 * p->pb.in_elems()) || overlaps(ker, 4 * p->pb.ker_elems()) || (need && overlaps(ws, need)))
         return fail(CONV_ERR_INVALID_ARGUMENT, "out aliases in, ker or workspace");
+    if (p->dev.ordinal < 0) return fail(CONV_ERR_UNSUPPORTED_DEVICE, "offline plan: not bound to a device");
     int dev = -1;
     if (cudaGetDevice(&dev) != cudaSuccess || dev != p->dev.ordinal)
         return fail(CONV_ERR_INVALID_ARGUMENT, "current device %d is not the plan's device %d", dev, p->dev.ordinal);

@@ -50,10 +50,16 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait(a, parity)) return;
-    const uint64_t t0 = globaltimer_ns();
+#ifdef CONV_NO_WATCHDOG
     while (!mbar_try_wait(a, parity)) {
-        if (globaltimer_ns() - t0 > 4000000000ull) __trap();
     }
+#else
+    // SM-clock watchdog (cheap CS2R read): ~8e9 cycles is > 4 s at any clock.
+    const long long t0 = clock64();
+    while (!mbar_try_wait(a, parity)) {
+        if (clock64() - t0 > 8000000000ll) __trap();
+    }
+#endif
 }
 
 // ---- TMA ------------------------------------------------------------------

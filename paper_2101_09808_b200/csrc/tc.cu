@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -54,6 +55,7 @@ struct TcParams {
     uint32_t sw;              // 32 / 64 / 128 (bytes per operand row per k-block)
     uint32_t a_stage_bytes;   // 128 * sw
     uint32_t b_stage_bytes;   // bn * sw
+    uint32_t debug;           // experiments only (env CONV_DEBUG_MODE): 1 no MMA, 2 no TMA, 4 no stores
 };
 
 // CG = 1: one CTA per 128-pixel tile (tcgen05 cta_group::1, M = 128).
@@ -134,7 +136,9 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                             uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
                             uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
                             const int bx = (r * p.S + s) * p.Cp + cb * p.bkc;
-                            if (CG == 2) {
+                            if (p.debug & 2) {
+                                if (leader) mbar_arrive(&full[stage]);
+                            } else if (CG == 2) {
                                 if (leader) mbar_arrive_expect_tx(&full[stage], tx_bytes);
                                 tma_load_im2col_4d_pair(a_dst, &tmap_a, &full[stage], cb * p.bkc, w0, h0, img,
                                                         (uint16_t)s, (uint16_t)r, pol_a);
@@ -171,7 +175,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(smem_a + (size_t)stage * p.a_stage_bytes);
                     const uint32_t b_addr = smem_u32(smem_b + (size_t)stage * p.b_stage_bytes);
-                    for (int kk = 0; kk < k_steps; ++kk) {
+                    for (int kk = 0; kk < ((p.debug & 1) ? 0 : k_steps); ++kk) {
                         const uint64_t ad = make_sdesc(a_addr + kk * 32, sbo, layout);
                         const uint64_t bd = make_sdesc(b_addr + kk * 32, sbo, layout);
                         const uint32_t accum = (it > 0 || kk > 0) ? 1u : 0u;
@@ -219,7 +223,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 tmem_ld_32x32b_x32(t0 + (uint32_t)j0, v);
                 tmem_ld_wait();
                 const int kbase = k0 + j0;
-                if (valid_m) {
+                if (valid_m && !(p.debug & 4)) {
                     if (kbase + 32 <= p.K) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
@@ -409,6 +413,11 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     prm.n_cblk = L.n_cblk;
     prm.k_iters = pb.R * pb.S * L.n_cblk;
     prm.num_n_tiles = (pb.K + t.bn - 1) / t.bn;
+    static const uint32_t debug_mode = [] {
+        const char* e = getenv("CONV_DEBUG_MODE");
+        return e ? (uint32_t)atoi(e) : 0u;
+    }();
+    prm.debug = debug_mode;
     const int tile_m = kBM * t.cg;
     const int num_m_tiles = (int)((pb.M() + tile_m - 1) / tile_m);
     prm.num_tiles = num_m_tiles * prm.num_n_tiles;
