@@ -66,60 +66,64 @@ def path_peak(path, peaks):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled through NVML every ~1 ms from a
+    background thread while the timed region runs (nvidia-smi's 100-ms floor
+    is longer than a 50-step timed region)."""
 
-    def __init__(self, index: int):
-        self.index = index
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device_index: int):
         self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
         self._stop = threading.Event()
-        self._proc = None
         self._t = None
+        self._h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            props = torch.cuda.get_device_properties(device_index)
+            try:
+                bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self._err = repr(e)
 
     def start(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except (OSError, FileNotFoundError):
-            self._proc = None
+        if self._h is None:
             return
-        self._t = threading.Thread(target=self._read, daemon=True)
+        self._stop.clear()
+        self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
+    def _run(self):
+        nv = self._nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_reasons(self._h))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def stop(self):
-        if self._proc:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=2)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
+        self._stop.set()
         if self._t:
             self._t.join(timeout=2)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-        sm = [num(s[0]) for s in self.samples if num(s[0])]
-        mx = [num(s[1]) for s in self.samples if num(s[1])]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        reasons = sorted(n for bit, n in self.REASONS.items() if self.reasons & bit)
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "sm_mhz_min": min(self.samples)}
 
 
 def dist_env():
@@ -172,15 +176,22 @@ def bench_ours(args):
         if world > 1:
             dist.barrier()
 
-    # warm-up
+    # warm-up: W steps, then the same step until >= 1 s has passed so that the
+    # clocks settle under this load (the clock sampler runs from here on)
     for _ in range(args.warmup):
         flush.zero_()
         plan.run(d_in, d_ker, d_out, ws)
     torch.cuda.synchronize(dev)
-
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
     clocks = ClockSampler(local)
     clocks.start()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < args.soak:
+        for _ in range(20):
+            flush.zero_()
+            plan.run(d_in, d_ker, d_out, ws)
+        torch.cuda.synchronize(dev)
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize(dev)
     for i in range(args.steps):
@@ -268,6 +279,7 @@ def bench_ours(args):
                 "path": plan.path,
                 "tile": desc["tile"],
                 "l2": "flushed before every timed step (write of 2x L2), outside the event pair",
+                "clocks_window": "NVML samples every ~1 ms over the >= 1 s warm-up soak and the timed region",
                 "parallelism": f"n-shard x{world}" if world > 1 else "single GPU",
                 "kernels_per_step": nk,
             },
@@ -374,6 +386,7 @@ def main():
     ap.add_argument("--gather", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--soak", type=float, default=1.0, help="seconds of extra warm-up steps before timing")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -56,7 +56,7 @@ typedef enum {
 
 typedef enum {
     CONV_PATH_AUTO = 0,      /* selector picks among the three below */
-    CONV_PATH_FP32_SIMT = 1, /* FP32 FFMA direct convolution on native NCHW (no repack) */
+    CONV_PATH_FP32_SIMT = 1, /* FP32 FFMA direct convolution on native NCHW In (Ker packed) */
     CONV_PATH_TF32 = 2,      /* tcgen05 implicit GEMM, inputs rounded to TF32 (RNA), fp32 accumulate */
     CONV_PATH_BF16 = 3       /* tcgen05 implicit GEMM, inputs rounded to BF16 (RNE), fp32 accumulate */
 } conv_path;
@@ -93,11 +93,13 @@ CONV_API conv_status conv_plan_set_path(conv_plan* plan, conv_path path);
  * SMEM/TMEM/register capacity (Eq. 4, per level). */
 CONV_API conv_status conv_plan_set_tile(conv_plan* plan, const char* spec);
 
-/* Bytes of device workspace conv_run needs (NHWC / KRSC repack buffers of the
- * tensor paths; 0 for the SIMT path).  Caller allocates, 256-B aligned. */
+/* Bytes of device workspace conv_run needs: the NHWC In / KRSC Ker buffers of
+ * the tensor paths, the packed [K/BKo][C][R][S][BKo] Ker of the SIMT path.
+ * Caller allocates, 256-B aligned. */
 CONV_API size_t conv_plan_workspace_bytes(const conv_plan* plan);
 
-/* Number of kernels one conv_run launches (repacks + main). */
+/* Number of kernels one conv_run launches: 2 on every path (one layout
+ * transform launch + the main kernel). */
 CONV_API int conv_plan_num_kernels(const conv_plan* plan);
 
 /* Path the plan will run (never AUTO after create). */

@@ -57,7 +57,7 @@ struct conv_plan {
     SimtTile simt;
     ModelResult model;
     // forced tile (conv_plan_set_tile)
-    int force_bn = 0, force_stages = 0, force_cg = 0;
+    int force_bn = 0, force_stages = 0, force_cg = 0, force_kbs = 0;
     SimtTile force_simt;
     unsigned force_simt_mask = 0;
 };
@@ -102,7 +102,7 @@ static conv_status select(conv_plan* p) {
         case CONV_PATH_TF32:
         case CONV_PATH_BF16: {
             const bool bf16 = p->requested == CONV_PATH_BF16;
-            if (!select_tc(pb, p->dev, bf16, tt, rt, p->force_bn, p->force_stages, p->force_cg, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            if (!select_tc(pb, p->dev, bf16, tt, rt, p->force_bn, p->force_stages, p->force_cg, p->force_kbs, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             p->tc = tt; p->model = rt; p->path = p->requested; p->tcl = tc_layout(pb, bf16);
             break;
         }
@@ -111,7 +111,7 @@ static conv_status select(conv_plan* p) {
             // AUTO keeps fp32 inputs or TF32 products (the precision of the
             // paper's fp32 method); BF16 only when requested.
             const bool ok_s = select_simt(pb, p->dev, st, rs, fs, p->force_simt_mask, why);
-            const bool ok_t = select_tc(pb, p->dev, false, tt, rt, p->force_bn, p->force_stages, p->force_cg, why);
+            const bool ok_t = select_tc(pb, p->dev, false, tt, rt, p->force_bn, p->force_stages, p->force_cg, p->force_kbs, why);
             if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             if (ok_t && (!ok_s || rt.model_us < rs.model_us)) {
                 p->tc = tt; p->model = rt; p->path = CONV_PATH_TF32; p->tcl = tc_layout(pb, false);
@@ -215,7 +215,7 @@ extern "C" conv_status conv_plan_set_path(conv_plan* p, conv_path path) {
 
 extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
     if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
-    int fbn = 0, fst = 0, fcg = 0;
+    int fbn = 0, fst = 0, fcg = 0, fkbs = 0;
     SimtTile fs;
     unsigned mask = 0;
     if (spec && *spec) {
@@ -236,6 +236,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             if (key == "bn") fbn = (int)v;
             else if (key == "stages") fst = (int)v;
             else if (key == "cg") fcg = (int)v;
+            else if (key == "kbs") fkbs = (int)v;
             else if (key == "tk") { fs.tk = (int)v; mask |= 1; }
             else if (key == "tw") { fs.tw = (int)v; mask |= 2; }
             else if (key == "kg") { fs.kg = (int)v; mask |= 4; }
@@ -245,16 +246,18 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "bc") { fs.bc = (int)v; mask |= 64; }
             else return fail(CONV_ERR_INVALID_ARGUMENT, "unknown tile key '%s'", key.c_str());
         }
-        if (fbn && (fbn % 32 != 0 || fbn > 256)) return fail(CONV_ERR_INFEASIBLE, "bn must be a multiple of 32 in [32, 256]");
+        if (fbn && fbn != 32 && fbn != 64 && fbn != 128 && fbn != 192 && fbn != 256)
+            return fail(CONV_ERR_INFEASIBLE, "bn must be one of 32, 64, 128, 192, 256");
+        if (fkbs && fkbs != 1 && fkbs != 2 && fkbs != 4) return fail(CONV_ERR_INFEASIBLE, "kbs must be 1, 2 or 4");
         if (fcg && fcg != 1 && fcg != 2) return fail(CONV_ERR_INFEASIBLE, "cg must be 1 or 2");
     }
-    const int obn = p->force_bn, ost = p->force_stages, ocg = p->force_cg;
+    const int obn = p->force_bn, ost = p->force_stages, ocg = p->force_cg, okbs = p->force_kbs;
     const SimtTile ofs = p->force_simt;
     const unsigned omask = p->force_simt_mask;
-    p->force_bn = fbn; p->force_stages = fst; p->force_cg = fcg; p->force_simt = fs; p->force_simt_mask = mask;
+    p->force_bn = fbn; p->force_stages = fst; p->force_cg = fcg; p->force_kbs = fkbs; p->force_simt = fs; p->force_simt_mask = mask;
     conv_status s = select(p);
     if (s != CONV_OK) {
-        p->force_bn = obn; p->force_stages = ost; p->force_cg = ocg; p->force_simt = ofs; p->force_simt_mask = omask;
+        p->force_bn = obn; p->force_stages = ost; p->force_cg = ocg; p->force_kbs = okbs; p->force_simt = ofs; p->force_simt_mask = omask;
         select(p);
     }
     return s;
@@ -264,7 +267,7 @@ extern "C" size_t conv_plan_workspace_bytes(const conv_plan* p) { return p ? ws_
 
 extern "C" int conv_plan_num_kernels(const conv_plan* p) {
     if (!p) return -1;
-    return p->path == CONV_PATH_FP32_SIMT ? 2 : 3;
+    return 2;   // tensor paths: repack (K1+K2 in one launch) + main; SIMT: pack + main
 }
 
 extern "C" conv_path conv_plan_path(const conv_plan* p) { return p ? p->path : CONV_PATH_AUTO; }
@@ -295,8 +298,8 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
                  p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
                  32 * p->simt.kg * p->simt.pw);
     } else {
-        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"stages\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
-                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.stages, p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
+        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
+                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
     }
     tile = t;
     char out[2048];
@@ -304,8 +307,8 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
         "{\"problem\":{\"N\":%d,\"K\":%d,\"C\":%d,\"H\":%d,\"W\":%d,\"R\":%d,\"S\":%d},"
         "\"path\":\"%s\",\"tile\":%s,\"workspace_bytes\":%zu,\"kernels\":%d,"
         "\"model\":{\"tiles\":%ld,\"ctas\":%ld,\"wave_eff\":%.4f,\"smem_bytes\":%zu,"
-        "\"levels\":{\"l2_smem\":{\"dv_bytes\":%.6g,\"bw\":%.6g,\"us\":%.4f},"
-        "\"hbm\":{\"dv_bytes\":%.6g,\"bw\":%.6g,\"us\":%.4f},"
+        "\"levels\":{\"l2_smem\":{\"dv_bytes\":%.12g,\"bw\":%.6g,\"us\":%.4f},"
+        "\"hbm\":{\"dv_bytes\":%.12g,\"bw\":%.6g,\"us\":%.4f},"
         "\"compute\":{\"flops_issued_us\":%.4f,\"peak\":%.6g}},\"model_us\":%.4f},"
         "\"roofline\":{\"flops\":%.6g,\"compulsory_bytes\":%.6g,\"roofline_us\":%.4f},"
         "\"device\":{\"ordinal\":%d,\"sms\":%d,\"smem_optin\":%zu,\"l2_bytes\":%zu}}",
@@ -332,6 +335,7 @@ static conv_status check_ptr(const void* ptr, const char* name, size_t align) {
 static conv_status run_impl(const conv_plan* p, const float* in, const float* ker, float* out, void* ws,
                             void* stream, void* const* events, int n_events) {
     if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (p->dev.ordinal < 0) return fail(CONV_ERR_UNSUPPORTED_DEVICE, "offline plan: not bound to a device");
     conv_status s;
     if ((s = check_ptr(in, "in", 16)) != CONV_OK) return s;
     if ((s = check_ptr(ker, "ker", 16)) != CONV_OK) return s;
@@ -349,12 +353,11 @@ static conv_status run_impl(const conv_plan* p, const float* in, const float* ke
     };
     if (overlaps(in, 4 * p->pb.in_elems()) || overlaps(ker, 4 * p->pb.ker_elems()) || (need && overlaps(ws, need)))
         return fail(CONV_ERR_INVALID_ARGUMENT, "out aliases in, ker or workspace");
-    if (p->dev.ordinal < 0) return fail(CONV_ERR_UNSUPPORTED_DEVICE, "offline plan: not bound to a device");
     int dev = -1;
     if (cudaGetDevice(&dev) != cudaSuccess || dev != p->dev.ordinal)
         return fail(CONV_ERR_INVALID_ARGUMENT, "current device %d is not the plan's device %d", dev, p->dev.ordinal);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaEvent_t ev[4];
+    cudaEvent_t ev[3];
     cudaEvent_t* evp = nullptr;
     if (events) {
         for (int i = 0; i <= nk; ++i) {

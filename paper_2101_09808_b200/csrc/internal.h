@@ -33,7 +33,8 @@ struct Device {
     // bf16 tensor peak default to MEASURED_PEAKS.json's values; the L2->SMEM
     // figure and the FFMA peak are defaults to be replaced by the probes.
     double bw_hbm = 6544.7e9;
-    double bw_l2 = 12.0e12;
+    double bw_l2 = 20.0e12;       // L2 -> SMEM via TMA: >= 23 TB/s sustained in the r01
+                                  // TMA-only experiment (693 MB in 30 us); 20 TB/s used
     double peak_bf16 = 1651.8e12;
     double peak_tf32 = 825.9e12;
     double peak_fp32 = 74.4e12;
@@ -44,6 +45,7 @@ struct TcTile {
     int bn = 128;        // GEMM-N tile (output channels), multiple of 32, <= 256
     int stages = 4;      // smem ring depth
     int cg = 1;          // CTAs per MMA: 1 (M = 128) or 2 (CTA pair, M = 256)
+    int kbs = 1;         // k-blocks (one TMA box of A and of B each) per pipeline stage
 };
 
 struct TcLayout {        // derived from Problem + element size
@@ -59,8 +61,8 @@ struct TcLayout {        // derived from Problem + element size
 TcLayout tc_layout(const Problem& p, bool bf16);
 size_t tc_smem_bytes(const TcLayout& L, const TcTile& t);
 
-// Launch K1 (ker repack), K2 (in repack) and K3 (tcgen05 implicit GEMM).
-// events (optional, n_events == 4) are recorded around each kernel.
+// Launch the repack (K1 + K2, one launch) and K3 (tcgen05 implicit GEMM).
+// events (optional, n_events == 3) are recorded around each kernel.
 cudaError_t tc_run(const Problem& p, const TcLayout& L, const TcTile& t, bool bf16,
                    const float* in, const float* ker, float* out, void* ws,
                    cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err);

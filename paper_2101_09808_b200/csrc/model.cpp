@@ -163,7 +163,12 @@ static double tc_dv_l2_smem_bytes(const Problem& pb, const TcLayout& L, int bn, 
 // once and the tensor core reads it once.  The pair's B half is read by its
 // own SM only, so per SM per k-block: 2 * (128 + BN/cg) * sw bytes.
 static const double kSmemBytesPerClk = 128.0;
-static const double kClockHz = 1.75e9;   // SM clock seen under this load (ncu, r01)
+static const double kClockHz = 1.84e9;   // SM clock measured under tcgen05 load (scripts/probe_mma.cu)
+// tcgen05.mma issue model (measured, scripts/probe_mma.cu and the r01
+// timeline trace): one 128 x N x 32-byte-K MMA takes max(N/2, 48) cycles on
+// an SM; every pipeline stage adds ~150 cycles of barrier / commit bubble.
+static const double kStageBubbleClk = 150.0;
+static const double kEpiStoreBW = 5.0e12;  // bytes/s the whole chip's epilogues drain at
 
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t) {
     ModelResult r;
@@ -179,9 +184,18 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     r.t_comp_us = flops_issued / peak * 1e6;
     r.dv_l2_smem = tc_dv_l2_smem_bytes(pb, L, t.bn, t.cg);
     r.t_l2_us = r.dv_l2_smem / dev.bw_l2 * 1e6;
+    // tensor pipe of the busiest unit: ceil(tiles/units) tiles, each
+    // R*S*n_cblk/kbs stages of kbs*(sw/32) MMAs.
+    const double tiles_per_unit = ceil((double)r.tiles / units);
+    const double stages_per_tile = (double)pb.R * pb.S * L.n_cblk / t.kbs;
+    const double mma_clk = std::max(t.bn / 2.0, 48.0);
+    const double stage_clk = t.kbs * (L.sw / 32.0) * mma_clk + kStageBubbleClk;
+    const double t_pipe_us = tiles_per_unit * stages_per_tile * stage_clk / kClockHz * 1e6;
     const double kblocks_per_sm = (double)r.tiles * pb.R * pb.S * L.n_cblk / units;
     const double t_smem_us = kblocks_per_sm * 2.0 * (128.0 + (double)t.bn / t.cg) * L.sw /
                              kSmemBytesPerClk / kClockHz * 1e6;
+    // last tile's epilogue is not overlapped: every CTA stores 128 x BN fp32
+    const double t_tail_us = std::min<double>(r.tiles * t.cg, dev.sms) * 128.0 * std::min(t.bn, pb.K) * 4.0 / kEpiStoreBW * 1e6;
     // HBM: repacks (read fp32 In/Ker, write workspace) + main kernel (read
     // workspace once -- the 9x im2col replay and the k-tile re-reads hit L2 --
     // and write fp32 Out once).
@@ -189,47 +203,56 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     const double main_hbm = (double)L.in_ws_bytes + (double)L.ker_ws_bytes + 4.0 * pb.out_elems();
     r.dv_hbm = repack + main_hbm;
     r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
-    const double waves = ceil((double)r.tiles / units);
-    const double t_main = std::max({r.t_comp_us / r.wave_eff, r.t_l2_us / r.wave_eff, t_smem_us / r.wave_eff,
-                                    main_hbm / dev.bw_hbm * 1e6})
-                          + waves * kTileOverheadUs + kLaunchUs;
+    // (t_comp_us, at the MEASURED_PEAKS cuBLAS rate, is reported only: the
+    // tensor pipe term t_pipe uses the measured per-MMA cycle counts.)
+    const double t_main = std::max({t_pipe_us, r.t_l2_us / r.wave_eff,
+                                    t_smem_us / r.wave_eff, main_hbm / dev.bw_hbm * 1e6})
+                          + t_tail_us + kLaunchUs;
     const double t_rep = repack / (0.8 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
     r.model_us = t_main + t_rep;
     r.smem = tc_smem_bytes(L, t);
     return r;
 }
 
-static int tc_max_stages(const Device& dev, const TcLayout& L, int bn, int cg) {
+static int tc_max_stages(const Device& dev, const TcLayout& L, int bn, int cg, int kbs) {
     for (int s = 8; s >= 2; --s) {
         TcTile t;
         t.bn = bn;
         t.stages = s;
         t.cg = cg;
+        t.kbs = kbs;
         if (tc_smem_bytes(L, t) <= dev.smem_optin) return s;
     }
     return 0;
 }
 
 bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& best_r,
-               int force_bn, int force_stages, int force_cg, std::string& why) {
+               int force_bn, int force_stages, int force_cg, int force_kbs, std::string& why) {
     const TcLayout L = tc_layout(pb, bf16);
     if (pb.R > 128 || pb.S > 128) { why = "R, S > 128: TMA im2col offsets are limited to [-128, 127]"; return false; }
     if (pb.M() + 256 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
+    static const int kBNs[] = {32, 64, 128, 192, 256};
     bool found = false;
     for (int cg = 1; cg <= 2; ++cg) {
         if (force_cg && cg != force_cg) continue;
-        for (int bn = 32; bn <= 256; bn += 32) {
-            if (force_bn && bn != force_bn) continue;
-            if (!force_bn && bn > ((pb.K + 31) / 32) * 32) continue;
-            const int smax = tc_max_stages(dev, L, bn, cg);
-            if (smax < 2) continue;
-            TcTile t;
-            t.bn = bn;
-            t.cg = cg;
-            t.stages = force_stages ? force_stages : smax;
-            if (t.stages < 2 || t.stages > smax) continue;
-            ModelResult r = model_tc(pb, dev, bf16, t);
-            if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+        for (int kbs = 1; kbs <= 4; kbs *= 2) {
+            if (force_kbs && kbs != force_kbs) continue;
+            if (L.n_cblk % kbs) continue;
+            for (int bn : kBNs) {
+                if (force_bn && bn != force_bn) continue;
+                if (!force_bn && bn > 32 && bn / 2 >= pb.K) continue;   // mostly padding
+                const int smax = tc_max_stages(dev, L, bn, cg, kbs);
+                // at least 3 stages unless forced (2 cannot overlap load and MMA well)
+                if (smax < (force_stages || force_kbs ? 2 : 3)) continue;
+                TcTile t;
+                t.bn = bn;
+                t.cg = cg;
+                t.kbs = kbs;
+                t.stages = force_stages ? force_stages : smax;
+                if (t.stages < 2 || t.stages > smax) continue;
+                ModelResult r = model_tc(pb, dev, bf16, t);
+                if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+            }
         }
     }
     if (!found) why = "no tensor-path tile fits shared memory / TMEM for this request";

@@ -7,12 +7,15 @@
 //           the im2col A operand), channels C..Cp-1 zero.
 //   K2 in : NCHW fp32 -> [N][Hin][Win][Cp] (NHWC; TMA im2col needs channels
 //           innermost and 16-B aligned pixel strides), channels C..Cp-1 zero.
+// Both run in ONE launch (repack_all).
 //
 // Element conversion: TF32 path rounds to nearest, ties away (cvt.rna.tf32),
 // BF16 path rounds to nearest even (cvt.rn.bf16x2).  Both are memory-bound
 // (roofline: bytes / HBM bandwidth).
 #include <cuda_bf16.h>
 #include <stdint.h>
+
+#include <algorithm>
 
 #include "internal.h"
 
@@ -37,58 +40,60 @@ struct Elem<true> {
     __device__ static T cvt(float x) { return __float2bfloat16_rn(x); }
 };
 
-// K1 (generic): one thread per output element (K*R*S*Cp <= 2^31).
-template <bool BF16>
-__global__ void __launch_bounds__(256) repack_ker_krsc(const float* __restrict__ ker,
-                                                       typename Elem<BF16>::T* __restrict__ out,
-                                                       int K, int C, int RS, int Cp) {
-    const int64_t total = (int64_t)K * RS * Cp;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i % Cp);
-        const int64_t krs = i / Cp;
-        const int rs = (int)(krs % RS);
-        const int64_t k = krs / RS;
-        const float v = c < C ? __ldg(ker + (k * C + c) * RS + rs) : 0.0f;
-        out[i] = Elem<BF16>::cvt(v);
-    }
-}
+// One launch performs both layout transforms (PAPER.md:371 packing; the
+// two are independent, so merging them removes a kernel boundary):
+//   CTAs [0, n_ker)          K1: Ker KCRS fp32 -> [K][R][S][Cp], one CTA per
+//                            (k, chunk of `cc` channels): the chunk's cc*R*S
+//                            contiguous floats are staged in shared memory with
+//                            coalesced loads, then written c-innermost with
+//                            coalesced stores; channels C..Cp-1 are zero.
+//   CTAs [n_ker, n_ker+n_in) K2: NCHW fp32 -> NHWC, one CTA per (image,
+//                            64-channel block, 64-pixel block) through a padded
+//                            64x65 tile: float4 loads along pixels (scalar when
+//                            the pixel count is not a multiple of 4), 16-B
+//                            stores of 8 bf16 / 4 fp32 consecutive channels.
+struct RepackGeom {
+    int C, Cp, RS, cc, ker_chunks;   // K1
+    int64_t P;                       // K2: pixels per image
+    int ptiles, ctiles;              // K2 tile grid per image
+    int n_ker;                       // number of K1 CTAs
+};
 
-// K1 (fast): one CTA per output channel k.  The k-th filter (C*R*S
-// contiguous floats) is staged in shared memory with coalesced loads, then
-// written c-innermost with coalesced stores.  Used when C*R*S*4 <= 48 KB.
 template <bool BF16>
-__global__ void __launch_bounds__(256) repack_ker_krsc_smem(const float* __restrict__ ker,
-                                                            typename Elem<BF16>::T* __restrict__ out,
-                                                            int C, int RS, int Cp) {
-    extern __shared__ float filt[];
-    const int64_t k = blockIdx.x;
-    const int crs = C * RS;
-    const float* src = ker + k * crs;
-    for (int i = threadIdx.x; i < crs; i += blockDim.x) filt[i] = __ldg(src + i);
-    __syncthreads();
-    typename Elem<BF16>::T* dst = out + k * (int64_t)RS * Cp;
-    for (int i = threadIdx.x; i < RS * Cp; i += blockDim.x) {
-        const int rs = i / Cp;
-        const int c = i - rs * Cp;
-        dst[i] = Elem<BF16>::cvt(c < C ? filt[c * RS + rs] : 0.0f);
-    }
-}
-
-// K2: tiled transpose per image, 64 channels x 64 pixels per CTA through a
-// padded shared-memory tile.  Loads are float4 along pixels (when the pixel
-// count P is a multiple of 4; scalar otherwise), stores are 16-B vectors of
-// 8 bf16 / 4 fp32 consecutive channels of one pixel, so both sides move
-// full 128-B lines.  grid = (ceil(P/64), ceil(Cp/64), N), block = 256.
-template <bool BF16>
-__global__ void __launch_bounds__(256) repack_in_nhwc(const float* __restrict__ in,
-                                                      typename Elem<BF16>::T* __restrict__ out,
-                                                      int C, int64_t P, int Cp) {
-    __shared__ float tile[64][65];
+__global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, const float* __restrict__ ker,
+                                                  typename Elem<BF16>::T* __restrict__ in_ws,
+                                                  typename Elem<BF16>::T* __restrict__ ker_ws, const RepackGeom g) {
+    extern __shared__ float sm[];
     const int tid = threadIdx.x;
-    const int64_t p0 = (int64_t)blockIdx.x * 64;
-    const int c0 = blockIdx.y * 64;
-    const int64_t n = blockIdx.z;
+    if ((int)blockIdx.x < g.n_ker) {
+        // ---- K1 ----
+        const int64_t k = blockIdx.x / g.ker_chunks;
+        const int c0 = (blockIdx.x % g.ker_chunks) * g.cc;
+        const int c1 = min(c0 + g.cc, g.Cp);
+        const int cload = max(0, min(c1, g.C) - c0);
+        const float* src = ker + (k * g.C + c0) * g.RS;
+        for (int i = tid; i < cload * g.RS; i += 256) sm[i] = __ldg(src + i);
+        __syncthreads();
+        typename Elem<BF16>::T* dst = ker_ws + k * (int64_t)g.RS * g.Cp;
+        const int width = c1 - c0;
+        for (int i = tid; i < g.RS * width; i += 256) {
+            const int rs = i / width;
+            const int c = c0 + (i - rs * width);
+            dst[(int64_t)rs * g.Cp + c] = Elem<BF16>::cvt(c < g.C ? sm[(c - c0) * g.RS + rs] : 0.0f);
+        }
+        return;
+    }
+    // ---- K2 ----
+    float (*tile)[65] = reinterpret_cast<float (*)[65]>(sm);
+    int b = blockIdx.x - g.n_ker;
+    const int pt = b % g.ptiles;
+    b /= g.ptiles;
+    const int ct = b % g.ctiles;
+    const int64_t n = b / g.ctiles;
+    const int64_t P = g.P;
+    const int C = g.C, Cp = g.Cp;
+    const int64_t p0 = (int64_t)pt * 64;
+    const int c0 = ct * 64;
     const float* src = in + n * C * P;
     if ((P & 3) == 0) {
 #pragma unroll
@@ -112,7 +117,7 @@ __global__ void __launch_bounds__(256) repack_in_nhwc(const float* __restrict__ 
         }
     }
     __syncthreads();
-    typename Elem<BF16>::T* dst = out + n * P * Cp;
+    typename Elem<BF16>::T* dst = in_ws + n * P * Cp;
     constexpr int kVec = BF16 ? 8 : 4;               // channels per 16-B store
     constexpr int kChunks = 64 / kVec;               // 16-B chunks per pixel row of the tile
 #pragma unroll
@@ -126,8 +131,8 @@ __global__ void __launch_bounds__(256) repack_in_nhwc(const float* __restrict__ 
                 uint32_t w[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const __nv_bfloat162 b = __floats2bfloat162_rn(tile[cq + 2 * j][pl], tile[cq + 2 * j + 1][pl]);
-                    w[j] = *reinterpret_cast<const uint32_t*>(&b);
+                    const __nv_bfloat162 bb = __floats2bfloat162_rn(tile[cq + 2 * j][pl], tile[cq + 2 * j + 1][pl]);
+                    w[j] = *reinterpret_cast<const uint32_t*>(&bb);
                 }
                 *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + p * Cp + c) = make_uint4(w[0], w[1], w[2], w[3]);
             } else {
@@ -144,30 +149,32 @@ __global__ void __launch_bounds__(256) repack_in_nhwc(const float* __restrict__ 
 
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
                           void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev) {
-    const int RS = pb.R * pb.S;
-    const int64_t P = pb.Hin() * pb.Win();
-    if (ev) cudaEventRecord(ev[0], st);
-    const size_t filt_bytes = (size_t)pb.C * RS * sizeof(float);
-    if (filt_bytes <= 48 * 1024) {
-        if (bf16)
-            repack_ker_krsc_smem<true><<<pb.K, 256, filt_bytes, st>>>(ker, (__nv_bfloat16*)ker_ws, pb.C, RS, Cp);
-        else
-            repack_ker_krsc_smem<false><<<pb.K, 256, filt_bytes, st>>>(ker, (float*)ker_ws, pb.C, RS, Cp);
-    } else {
-        const int64_t ktotal = (int64_t)pb.K * RS * Cp;
-        const int kblocks = (int)((ktotal + 255) / 256 < 4096 ? (ktotal + 255) / 256 : 4096);
-        if (bf16)
-            repack_ker_krsc<true><<<kblocks, 256, 0, st>>>(ker, (__nv_bfloat16*)ker_ws, pb.K, pb.C, RS, Cp);
-        else
-            repack_ker_krsc<false><<<kblocks, 256, 0, st>>>(ker, (float*)ker_ws, pb.K, pb.C, RS, Cp);
+    RepackGeom g;
+    g.C = pb.C;
+    g.Cp = Cp;
+    g.RS = pb.R * pb.S;
+    // channels per K1 CTA so that the staged slice is <= 32 KB (at least 1)
+    g.cc = std::max(1, std::min(Cp, (int)(32768 / (4 * g.RS))));
+    g.ker_chunks = (Cp + g.cc - 1) / g.cc;
+    g.n_ker = pb.K * g.ker_chunks;
+    g.P = pb.Hin() * pb.Win();
+    g.ptiles = (int)((g.P + 63) / 64);
+    g.ctiles = (Cp + 63) / 64;
+    const int64_t n_in = (int64_t)g.ptiles * g.ctiles * pb.N;
+    const int64_t grid = g.n_ker + n_in;
+    if (grid >= (1ll << 31)) return cudaErrorInvalidValue;
+    const size_t smem = std::max<size_t>(64 * 65 * sizeof(float), (size_t)g.cc * g.RS * sizeof(float));
+    if (smem > 48 * 1024) {   // very large R*S: one channel per K1 CTA still needs > 48 KB
+        cudaError_t e = bf16 ? cudaFuncSetAttribute(repack_all<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                             : cudaFuncSetAttribute(repack_all<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
     }
-    if (ev) cudaEventRecord(ev[1], st);
-    dim3 tgrid((unsigned)((P + 63) / 64), (unsigned)((Cp + 63) / 64), (unsigned)pb.N);
+    if (ev) cudaEventRecord(ev[0], st);
     if (bf16)
-        repack_in_nhwc<true><<<tgrid, 256, 0, st>>>(in, (__nv_bfloat16*)in_ws, pb.C, P, Cp);
+        repack_all<true><<<(unsigned)grid, 256, smem, st>>>(in, ker, (__nv_bfloat16*)in_ws, (__nv_bfloat16*)ker_ws, g);
     else
-        repack_in_nhwc<false><<<tgrid, 256, 0, st>>>(in, (float*)in_ws, pb.C, P, Cp);
-    if (ev) cudaEventRecord(ev[2], st);
+        repack_all<false><<<(unsigned)grid, 256, smem, st>>>(in, ker, (float*)in_ws, (float*)ker_ws, g);
+    if (ev) cudaEventRecord(ev[1], st);
     return cudaGetLastError();
 }
 

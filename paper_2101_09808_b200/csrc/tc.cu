@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -52,10 +53,12 @@ struct TcParams {
     int num_n_tiles;
     int num_tiles;
     int stages;
+    int kbs;                  // k-blocks per pipeline stage (1, 2 or 4)
     uint32_t sw;              // 32 / 64 / 128 (bytes per operand row per k-block)
-    uint32_t a_stage_bytes;   // 128 * sw
-    uint32_t b_stage_bytes;   // bn * sw
+    uint32_t a_stage_bytes;   // kbs * 128 * sw
+    uint32_t b_stage_bytes;   // kbs * (bn / cg) * sw
     uint32_t debug;           // experiments only (env CONV_DEBUG_MODE): 1 no MMA, 2 no TMA, 4 no stores
+    unsigned long long* trace;  // experiments only (env CONV_TRACE): per-CTA timeline, 64 slots
 };
 
 // CG = 1: one CTA per 128-pixel tile (tcgen05 cta_group::1, M = 128).
@@ -65,7 +68,7 @@ struct TcParams {
 //   shared memory, and each CTA's TMEM receives its own 128 accumulator rows.
 //   Per SM this halves the B operand traffic (L2 -> SMEM and SMEM -> tensor
 //   core), which is what bounds the 1-CTA kernel on wide tiles.
-template <int BN, bool BF16, int CG>
+template <int BN, bool BF16, int CG, int KSTEPS>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const TcParams p) {
@@ -111,13 +114,17 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     if (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t wflavor = (p.debug >> 3) & 3;
 
     if (warp == 0) {
-        // ===== TMA producer (both CTAs of a pair) =====
-        if (lane == 0) {
+        // ===== TMA producer (both CTAs of a pair): the whole warp runs the
+        // loop (warp-uniform control flow keeps the operands in uniform
+        // registers), one elected lane issues =====
+        {
             const uint64_t pol_a = policy_evict_normal();
             const uint64_t pol_b = policy_evict_last();   // Ker is re-read by every M tile
             const uint32_t tx_bytes = CG * (p.a_stage_bytes + p.b_stage_bytes);
+            long long prod_wait = 0;
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = unit; tile < p.num_tiles; tile += nunits) {
@@ -129,72 +136,118 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 const int h0 = pix / p.W;
                 const int w0 = pix - h0 * p.W;
                 const int kb0 = n_tile * BN + (int)rank * (BN / CG);   // this CTA's B rows
+                const uint32_t a_blk = kBM * p.sw, b_blk = (BN / CG) * p.sw;
                 for (int r = 0; r < p.R; ++r) {
                     for (int s = 0; s < p.S; ++s) {
-                        for (int cb = 0; cb < p.n_cblk; ++cb) {
-                            mbar_wait(&empty[stage], phase ^ 1);
+                        for (int cb0 = 0; cb0 < p.n_cblk; cb0 += p.kbs) {
+                            const long long pw0 = p.trace ? clock64() : 0;
+                            mbar_wait_flavor(&empty[stage], phase ^ 1, wflavor);
+                            if (p.trace) prod_wait += clock64() - pw0;
                             uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
                             uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
-                            const int bx = (r * p.S + s) * p.Cp + cb * p.bkc;
-                            if (p.debug & 2) {
+                            if (!elect_one_sync()) {
+                            } else if (p.debug & 2) {
                                 if (leader) mbar_arrive(&full[stage]);
-                            } else if (CG == 2) {
-                                if (leader) mbar_arrive_expect_tx(&full[stage], tx_bytes);
-                                tma_load_im2col_4d_pair(a_dst, &tmap_a, &full[stage], cb * p.bkc, w0, h0, img,
-                                                        (uint16_t)s, (uint16_t)r, pol_a);
-                                tma_load_2d_pair(b_dst, &tmap_b, &full[stage], bx, kb0, pol_b);
                             } else {
-                                mbar_arrive_expect_tx(&full[stage], tx_bytes);
-                                tma_load_im2col_4d(a_dst, &tmap_a, &full[stage], cb * p.bkc, w0, h0, img,
-                                                   (uint16_t)s, (uint16_t)r, pol_a);
-                                tma_load_2d(b_dst, &tmap_b, &full[stage], bx, kb0, pol_b);
+                                if (leader) mbar_arrive_expect_tx(&full[stage], tx_bytes);
+                                for (int kb = 0; kb < p.kbs; ++kb) {
+                                    const int cb = cb0 + kb;
+                                    const int bx = (r * p.S + s) * p.Cp + cb * p.bkc;
+                                    if (CG == 2) {
+                                        tma_load_im2col_4d_pair(a_dst + kb * a_blk, &tmap_a, &full[stage], cb * p.bkc,
+                                                                w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
+                                        tma_load_2d_pair(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
+                                    } else {
+                                        tma_load_im2col_4d(a_dst + kb * a_blk, &tmap_a, &full[stage], cb * p.bkc,
+                                                           w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
+                                        tma_load_2d(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
+                                    }
+                                }
                             }
+                            __syncwarp();
                             if (++stage == p.stages) { stage = 0; phase ^= 1; }
                         }
                     }
                 }
             }
+            if (p.trace && lane == 0) {
+                p.trace[(size_t)blockIdx.x * 64 + 60] = (unsigned long long)prod_wait;
+                p.trace[(size_t)blockIdx.x * 64 + 61] = globaltimer_ns();
+            }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer (leader CTA only) =====
-        if (lane == 0 && leader) {
+        // ===== MMA issuer (leader CTA only): whole warp loops, one elected
+        // lane issues the tcgen05 instructions =====
+        if (leader) {
             constexpr uint32_t idesc = make_idesc(BF16 ? 1u : 2u, kBM * CG, BN);
-            const uint32_t layout = umma_layout_for_swizzle(p.sw);
-            const uint32_t sbo = 8 * p.sw;
-            const int k_steps = (int)(p.sw / 32);   // 32 B of K per MMA (8 tf32 / 16 bf16)
+            constexpr uint32_t kSw = KSTEPS * 32;            // swizzle span = k-block row bytes
+            constexpr uint32_t layout = umma_layout_for_swizzle(kSw);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = unit; tile < p.num_tiles; tile += nunits) {
-                mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+            // Descriptors: the stage-0 descriptor plus (byte offset >> 4) in
+            // the start-address field; one k step of 32 B adds 2.
+            const uint64_t a_desc0 = make_sdesc(smem_u32(smem_a), 8 * kSw, layout);
+            const uint64_t b_desc0 = make_sdesc(smem_u32(smem_b), 8 * kSw, layout);
+            const uint32_t a_step = p.a_stage_bytes >> 4, b_step = p.b_stage_bytes >> 4;
+            constexpr uint32_t a_blk = (kBM * kSw) >> 4, b_blk = ((BN / CG) * kSw) >> 4;
+            const bool no_mma = (p.debug & 1) != 0;
+            const int kbs = p.kbs;
+            const int iters = p.k_iters / kbs;
+            unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
+            int ti = 0;
+            if (tr && lane == 0) tr[0] = globaltimer_ns();
+            for (int tile = unit; tile < p.num_tiles; tile += nunits, ++ti) {
+                mbar_wait_flavor(&tmem_empty[acc], acc_phase ^ 1, wflavor);
                 tc_fence_after();
+                if (tr && lane == 0 && ti < 8) tr[1 + 4 * ti] = globaltimer_ns();
+                long long wait_cyc = 0;
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-                for (int it = 0; it < p.k_iters; ++it) {
-                    mbar_wait(&full[stage], phase);
+                uint32_t accum = 0;                      // first MMA of the tile overwrites D
+                for (int it = 0; it < iters; ++it) {
+                    const long long w0 = tr ? clock64() : 0;
+                    mbar_wait_flavor(&full[stage], phase, wflavor);
+                    if (tr) wait_cyc += clock64() - w0;
                     tc_fence_after();
-                    const uint32_t a_addr = smem_u32(smem_a + (size_t)stage * p.a_stage_bytes);
-                    const uint32_t b_addr = smem_u32(smem_b + (size_t)stage * p.b_stage_bytes);
-                    for (int kk = 0; kk < ((p.debug & 1) ? 0 : k_steps); ++kk) {
-                        const uint64_t ad = make_sdesc(a_addr + kk * 32, sbo, layout);
-                        const uint64_t bd = make_sdesc(b_addr + kk * 32, sbo, layout);
-                        const uint32_t accum = (it > 0 || kk > 0) ? 1u : 0u;
-                        if (CG == 2) {
-                            if (BF16) mma_bf16_pair(d_tmem, ad, bd, idesc, accum);
-                            else      mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
-                        } else {
-                            if (BF16) mma_bf16(d_tmem, ad, bd, idesc, accum);
-                            else      mma_tf32(d_tmem, ad, bd, idesc, accum);
+                    if (elect_one_sync()) {
+                        const uint64_t ad0 = a_desc0 + (uint64_t)(stage * a_step);
+                        const uint64_t bd0 = b_desc0 + (uint64_t)(stage * b_step);
+                        if (!no_mma) {
+                            for (int kb = 0; kb < kbs; ++kb) {
+#pragma unroll
+                                for (int kk = 0; kk < KSTEPS; ++kk) {
+                                    const uint64_t ad = ad0 + (uint64_t)(kb * a_blk + 2 * kk);
+                                    const uint64_t bd = bd0 + (uint64_t)(kb * b_blk + 2 * kk);
+                                    if (CG == 2) {
+                                        if (BF16) mma_bf16_pair(d_tmem, ad, bd, idesc, accum);
+                                        else      mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
+                                    } else {
+                                        if (BF16) mma_bf16(d_tmem, ad, bd, idesc, accum);
+                                        else      mma_tf32(d_tmem, ad, bd, idesc, accum);
+                                    }
+                                    accum = 1;
+                                }
+                            }
                         }
+                        // frees the smem slot (in both CTAs) when the MMAs retire
+                        if (CG == 2) tc_commit_pair_mc(&empty[stage], 0x3);
+                        else tc_commit(&empty[stage]);
                     }
-                    // frees the smem slot (in both CTAs) when the MMAs retire
-                    if (CG == 2) tc_commit_pair_mc(&empty[stage], 0x3);
-                    else tc_commit(&empty[stage]);
+                    __syncwarp();
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
                 }
                 // accumulator ready for the epilogue (of both CTAs)
-                if (CG == 2) tc_commit_pair_mc(&tmem_full[acc], 0x3);
-                else tc_commit(&tmem_full[acc]);
+                if (elect_one_sync()) {
+                    if (CG == 2) tc_commit_pair_mc(&tmem_full[acc], 0x3);
+                    else tc_commit(&tmem_full[acc]);
+                }
+                __syncwarp();
+                if (tr && lane == 0 && ti < 8) {
+                    tr[1 + 4 * ti + 1] = (unsigned long long)wait_cyc;
+                    tr[1 + 4 * ti + 2] = globaltimer_ns();
+                    tr[1 + 4 * ti + 3] = (unsigned long long)clock64();
+                }
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
@@ -214,8 +267,10 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             const int pix = valid_m ? m - img * p.HW : 0;
             float* obase = p.out + ((int64_t)img * p.K) * p.HW + pix;
 
-            mbar_wait(&tmem_full[acc], acc_phase);
+            mbar_wait_sleep(&tmem_full[acc], acc_phase, 256);
             tc_fence_after();
+            const int ti_e = (tile - unit) / nunits;
+            if (p.trace && warp == 4 && lane == 0 && ti_e < 8) p.trace[(size_t)blockIdx.x * 64 + 40 + 2 * ti_e] = globaltimer_ns();
             const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
             for (int j0 = 0; j0 < BN; j0 += 32) {
@@ -237,6 +292,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             }
             tc_fence_before();
             __syncwarp();
+            if (p.trace && warp == 4 && lane == 0 && ti_e < 8) p.trace[(size_t)blockIdx.x * 64 + 41 + 2 * ti_e] = globaltimer_ns();
             if (lane == 0) {
                 if (CG == 2) mbar_arrive_leader(&tmem_empty[acc]);
                 else mbar_arrive(&tmem_empty[acc]);
@@ -277,7 +333,7 @@ TcLayout tc_layout(const Problem& pb, bool bf16) {
 }
 
 size_t tc_smem_bytes(const TcLayout& L, const TcTile& t) {
-    const size_t a = (size_t)kBM * L.sw, b = (size_t)(t.bn / t.cg) * L.sw;
+    const size_t a = (size_t)t.kbs * kBM * L.sw, b = (size_t)t.kbs * (t.bn / t.cg) * L.sw;
     return 1024 /*align slack*/ + (size_t)t.stages * (a + b) + (2 * t.stages + 4) * 8 + 16;
 }
 
@@ -286,10 +342,10 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-template <int BN, bool BF16, int CG>
+template <int BN, bool BF16, int CG, int KSTEPS>
 static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& prm,
                              size_t smem, int grid, cudaStream_t st) {
-    auto kfn = conv_igemm_tcgen05<BN, BF16, CG>;
+    auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS>;
     // Opt in to the largest dynamic smem once per instantiation (per process).
     static std::atomic<int> smem_set{0};
     if (smem_set.load(std::memory_order_acquire) < (int)smem) {
@@ -315,18 +371,26 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const
     return cudaLaunchKernelEx(&cfg, kfn, ta, tb, prm);
 }
 
-template <bool BF16, int CG>
+template <bool BF16, int CG, int KSTEPS>
 static cudaError_t launch_tc_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                                 const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
     switch (bn) {
-        case 32: return launch_tc<32, BF16, CG>(ta, tb, prm, smem, grid, st);
-        case 64: return launch_tc<64, BF16, CG>(ta, tb, prm, smem, grid, st);
-        case 96: return launch_tc<96, BF16, CG>(ta, tb, prm, smem, grid, st);
-        case 128: return launch_tc<128, BF16, CG>(ta, tb, prm, smem, grid, st);
-        case 160: return launch_tc<160, BF16, CG>(ta, tb, prm, smem, grid, st);
-        case 192: return launch_tc<192, BF16, CG>(ta, tb, prm, smem, grid, st);
-        case 224: return launch_tc<224, BF16, CG>(ta, tb, prm, smem, grid, st);
-        case 256: return launch_tc<256, BF16, CG>(ta, tb, prm, smem, grid, st);
+        case 32: return launch_tc<32, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
+        case 64: return launch_tc<64, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
+        case 128: return launch_tc<128, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
+        case 192: return launch_tc<192, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
+        case 256: return launch_tc<256, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <bool BF16, int CG>
+static cudaError_t launch_tc_sw(int sw, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                                const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
+    switch (sw) {
+        case 128: return launch_tc_bn<BF16, CG, 4>(bn, ta, tb, prm, smem, grid, st);
+        case 64: return launch_tc_bn<BF16, CG, 2>(bn, ta, tb, prm, smem, grid, st);
+        case 32: return launch_tc_bn<BF16, CG, 1>(bn, ta, tb, prm, smem, grid, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -341,7 +405,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     // Tensor maps depend on the workspace address, known only here; they are
     // encoded on first use and cached per (workspace, problem, tile).
     struct Key {
-        const void* ws; Problem pb; int bn; int cg; int bf16; int dev;
+        const void* ws; Problem pb; int bn; int cg; int kbs; int bf16; int dev;
     };
     struct Entry { Key k; CUtensorMap ta, tb; };
     static std::mutex mu;
@@ -349,9 +413,9 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     static int n_cached = 0, next_slot = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    const Key key{ws, pb, t.bn, t.cg, bf16 ? 1 : 0, dev};
+    const Key key{ws, pb, t.bn, t.cg, t.kbs, bf16 ? 1 : 0, dev};
     auto same = [&](const Key& a) {
-        return a.ws == key.ws && memcmp(&a.pb, &key.pb, sizeof(Problem)) == 0 && a.bn == key.bn && a.cg == key.cg &&
+        return a.ws == key.ws && memcmp(&a.pb, &key.pb, sizeof(Problem)) == 0 && a.bn == key.bn && a.cg == key.cg && a.kbs == key.kbs &&
                a.bf16 == key.bf16 && a.dev == key.dev;
     };
     CUtensorMap ta, tb;
@@ -418,24 +482,43 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         return e ? (uint32_t)atoi(e) : 0u;
     }();
     prm.debug = debug_mode;
+    static const char* trace_path = getenv("CONV_TRACE");
+    static unsigned long long* trace_buf = nullptr;
+    prm.trace = nullptr;
+    if (trace_path) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 1024 * 64 * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, 1024 * 64 * sizeof(unsigned long long), st);
+        prm.trace = trace_buf;
+    }
     const int tile_m = kBM * t.cg;
     const int num_m_tiles = (int)((pb.M() + tile_m - 1) / tile_m);
     prm.num_tiles = num_m_tiles * prm.num_n_tiles;
     prm.stages = t.stages;
+    prm.kbs = t.kbs;
     prm.sw = (uint32_t)L.sw;
-    prm.a_stage_bytes = (uint32_t)(kBM * L.sw);
-    prm.b_stage_bytes = (uint32_t)((t.bn / t.cg) * L.sw);
+    prm.a_stage_bytes = (uint32_t)(t.kbs * kBM * L.sw);
+    prm.b_stage_bytes = (uint32_t)(t.kbs * (t.bn / t.cg) * L.sw);
     const int units = num_sms / t.cg;
     const int grid = (prm.num_tiles < units ? prm.num_tiles : units) * t.cg;
     const size_t smem = tc_smem_bytes(L, t);
+    if (L.n_cblk % t.kbs != 0) { err = "k-blocks per stage must divide the c-block count"; return cudaErrorInvalidValue; }
     if (t.cg == 2)
-        e = bf16 ? launch_tc_bn<true, 2>(t.bn, ta, tb, prm, smem, grid, st)
-                 : launch_tc_bn<false, 2>(t.bn, ta, tb, prm, smem, grid, st);
+        e = bf16 ? launch_tc_sw<true, 2>(L.sw, t.bn, ta, tb, prm, smem, grid, st)
+                 : launch_tc_sw<false, 2>(L.sw, t.bn, ta, tb, prm, smem, grid, st);
     else
-        e = bf16 ? launch_tc_bn<true, 1>(t.bn, ta, tb, prm, smem, grid, st)
-                 : launch_tc_bn<false, 1>(t.bn, ta, tb, prm, smem, grid, st);
+        e = bf16 ? launch_tc_sw<true, 1>(L.sw, t.bn, ta, tb, prm, smem, grid, st)
+                 : launch_tc_sw<false, 1>(L.sw, t.bn, ta, tb, prm, smem, grid, st);
     if (e != cudaSuccess) { err = std::string("tcgen05 kernel launch failed: ") + cudaGetErrorString(e); return e; }
-    if (ev) cudaEventRecord(ev[3], st);
+    if (ev) cudaEventRecord(ev[2], st);
+    if (prm.trace) {
+        static unsigned long long host[1024 * 64];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(host, prm.trace, sizeof(host), cudaMemcpyDeviceToHost);
+        if (FILE* f = fopen(trace_path, "wb")) {
+            fwrite(host, sizeof(unsigned long long), (size_t)grid * 64, f);
+            fclose(f);
+        }
+    }
     return cudaSuccess;
 }
 

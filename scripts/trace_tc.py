@@ -1,0 +1,42 @@
+"""Run the tensor kernel once with CONV_TRACE and summarise the per-CTA timeline."""
+import os, sys, subprocess
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+path, cfg, tile = sys.argv[1], sys.argv[2], (sys.argv[3] if len(sys.argv) > 3 else "")
+out = f"/tmp/trace_{path}_{cfg}_{tile.replace(',', '_').replace('=', '')}.bin"
+env = dict(os.environ, CONV_TRACE=out)
+code = f"""
+import torch
+from paper_2101_09808_b200 import conv
+from paper_2101_09808_b200.inputs import CONFIGS, make_inputs
+sh = CONFIGS['{cfg}']
+p = conv.ConvPlan(*sh.as_tuple(), path='{path}', tile='{tile}' or None)
+i, k = make_inputs(sh)
+i, k = i.cuda(), k.cuda(); o = p.new_output(); ws = p.new_workspace()
+for _ in range(3): p.run(i, k, o, ws)
+torch.cuda.synchronize()
+print(p.describe()['tile'])
+"""
+subprocess.run([sys.executable, "-c", code], env=env, check=True)
+t = np.fromfile(out, dtype=np.uint64).reshape(-1, 64).astype(np.int64)
+t = t[t[:, 0] > 0]
+t0 = t[:, 0].min()
+print(f"CTAs traced: {len(t)}")
+ntiles = [(t[c, 1:33].reshape(8, 4)[:, 0] > 0).sum() for c in range(len(t))]
+print("tiles per CTA:", np.bincount(ntiles))
+for ti in range(max(ntiles)):
+    beg = t[:, 1 + 4 * ti] - t0; end = t[:, 3 + 4 * ti] - t0; wc = t[:, 2 + 4 * ti]
+    ok = t[:, 1 + 4 * ti] > 0
+    es, ee = t[:, 40 + 2 * ti] - t0, t[:, 41 + 2 * ti] - t0
+    print(f"tile {ti}: mma begin {np.median(beg[ok])/1e3:7.2f}us  end {np.median(end[ok])/1e3:7.2f}us "
+          f"(dur med {np.median((end-beg)[ok])/1e3:6.2f}us)  full-wait {np.median(wc[ok])/1e3:7.1f}kcyc  "
+          f"epi {np.median(es[ok])/1e3:7.2f}->{np.median(ee[ok])/1e3:7.2f}us")
+ends_ns = np.stack([t[:, 3 + 4 * i] for i in range(max(ntiles))], 1)
+ends_clk = np.stack([t[:, 4 + 4 * i] for i in range(max(ntiles))], 1)
+ok = (ends_ns[:, 0] > 0) & (ends_ns[:, -1] > 0)
+mhz = (ends_clk[ok, -1] - ends_clk[ok, 0]) / (ends_ns[ok, -1] - ends_ns[ok, 0]) * 1e3
+print(f"effective SM clock between first and last tile end: median {np.median(mhz):.0f} MHz (min {mhz.min():.0f}, max {mhz.max():.0f})")
+print(f"producer empty-wait med {np.median(t[:,60])/1e3:.1f}kcyc, producer end med {np.median(t[:,61]-t0)/1e3:.2f}us")
+n = max(ntiles)
+last = np.max(t[:, 41 + 2 * (n - 1)] - t0)
+print(f"last epilogue end {last/1e3:.2f}us; first start spread {(t[:,0].max()-t0)/1e3:.2f}us")

@@ -136,3 +136,75 @@ def test_model_rejects_bad_input(lib):
         conv.model_dv(list("nkcrshw"), dict(n=1, k=1, c=1, r=1, s=1, h=1, w=1), dict(n=2, k=1, c=1, r=1, s=1, h=1, w=1))
     with pytest.raises(KeyError):
         conv.model_dv(list("nkcrshx"), dict(n=1, k=1, c=1, r=1, s=1, h=1, w=1), dict(n=1, k=1, c=1, r=1, s=1, h=1, w=1))
+
+
+# ---- the selector on a described B200 (offline plans, no device) -------------
+
+def _offline(shape, path, tile=None):
+    return conv.ConvPlan(*shape.as_tuple(), path=path, tile=tile, offline_device=conv.B200)
+
+
+@pytest.mark.parametrize("path", ["fp32_simt", "tf32", "bf16"])
+def test_selector_respects_capacity(lib, path):
+    """Every emitted tile satisfies the per-level capacity constraints (Eq. 4
+    per level): shared memory per CTA <= opt-in, TMEM 2*BN <= 512."""
+    from paper_2101_09808_b200.inputs import CONFIGS, Shape
+    shapes = list(CONFIGS.values()) + [Shape(1, 5, 3, 7, 9, 3, 3), Shape(2, 300, 700, 9, 10, 1, 1),
+                                       Shape(1, 64, 4096, 3, 3, 3, 3), Shape(1, 8, 8, 2, 3000, 1, 5)]
+    for sh in shapes:
+        d = _offline(sh, path).describe()
+        assert d["path"] == path
+        assert d["model"]["smem_bytes"] <= conv.B200["smem_optin"]
+        if path != "fp32_simt":
+            assert 2 * d["tile"]["bn"] <= 512 and d["tile"]["cg"] in (1, 2)
+            assert d["tile"]["cp"] >= sh.C and (d["tile"]["cp"] * (2 if path == "bf16" else 4)) % 32 == 0
+        else:
+            t = d["tile"]
+            assert t["threads"] <= 512 and t["tn"] * t["th"] * sh.W <= t["threads"] // 32 // t["kg"] * 32 * t["tw"]
+
+
+def test_selector_forced_tiles(lib):
+    from paper_2101_09808_b200.inputs import CONFIGS
+    sh = CONFIGS["batched"]
+    for cg in (1, 2):
+        for bn in (32, 128, 256):
+            d = _offline(sh, "bf16", tile=f"bn={bn},cg={cg}").describe()
+            assert (d["tile"]["bn"], d["tile"]["cg"]) == (bn, cg)
+    with pytest.raises(conv.ConvError) as e:
+        _offline(sh, "bf16", tile="bn=48")
+    assert e.value.status == conv.CONV_ERR_INFEASIBLE
+    with pytest.raises(conv.ConvError) as e:
+        _offline(sh, "bf16", tile="bogus=1")
+    assert e.value.status == conv.CONV_ERR_INVALID_ARGUMENT
+
+
+def test_selector_model_levels_consistent(lib):
+    """The reported model time is at least every level's bandwidth-scaled
+    cost (Sec. 5 min-max: cost = max over levels)."""
+    from paper_2101_09808_b200.inputs import CONFIGS
+    for sh in CONFIGS.values():
+        for path in ("tf32", "bf16", "fp32_simt"):
+            m = _offline(sh, path).describe()["model"]
+            lv = m["levels"]
+            assert m["model_us"] >= lv["l2_smem"]["us"] * 0.999
+            assert m["model_us"] >= lv["compute"]["flops_issued_us"] * 0.999
+            assert lv["l2_smem"]["us"] == pytest.approx(lv["l2_smem"]["dv_bytes"] / lv["l2_smem"]["bw"] * 1e6, rel=1e-3, abs=1e-3)
+
+
+def test_offline_plan_cannot_run(lib):
+    from paper_2101_09808_b200.inputs import CONFIGS
+    p = _offline(CONFIGS["tiny"], "tf32")
+    assert lib.conv_run(p._h, 16, 16, 16, 256, None) == conv.CONV_ERR_UNSUPPORTED_DEVICE
+
+
+def test_tensor_l2_volume_matches_im2col_replay(lib):
+    """DV_{L2->SMEM} of the tensor path = (A im2col replay + B re-reads) from
+    the Sec. 3.2 evaluator = ceil(M/BM)*BM*R*S*Cp*e + ceil(M/BM)*K*R*S*Cp*e."""
+    from paper_2101_09808_b200.inputs import CONFIGS
+    sh = CONFIGS["batched"]
+    for cg in (1, 2):
+        d = _offline(sh, "bf16", tile=f"bn=256,cg={cg}").describe()
+        bm = 128 * cg
+        mt = -(-sh.N * sh.H * sh.W // bm)
+        exp = mt * bm * 9 * 256 * 2 + mt * 256 * 9 * 256 * 2
+        assert d["model"]["levels"]["l2_smem"]["dv_bytes"] == pytest.approx(exp, rel=1e-9)
