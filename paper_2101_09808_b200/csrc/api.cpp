@@ -244,6 +244,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "tn") { fs.tn = (int)v; mask |= 16; }
             else if (key == "th") { fs.th = (int)v; mask |= 32; }
             else if (key == "bc") { fs.bc = (int)v; mask |= 64; }
+            else if (key == "ver") { fs.ver = (int)v; mask |= 128; }
             else return fail(CONV_ERR_INVALID_ARGUMENT, "unknown tile key '%s'", key.c_str());
         }
         if (fbn && fbn != 32 && fbn != 64 && fbn != 128 && fbn != 192 && fbn != 256)
@@ -294,8 +295,8 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     std::string tile;
     char t[256];
     if (p->path == CONV_PATH_FP32_SIMT) {
-        snprintf(t, sizeof t, "{\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"threads\":%d}",
-                 p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
+        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"threads\":%d}",
+                 p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
                  32 * p->simt.kg * p->simt.pw);
     } else {
         snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",

@@ -268,9 +268,10 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const int threads = 32 * t.kg * t.pw;
     const size_t smem = simt_smem_bytes(pb, t);
     r.smem = smem;
-    // Register level (Sec. 6 microkernel analog): TK*TW accumulators + TW + TK
-    // operands per thread plus addressing; ptxas caps at 128 (launch bounds 512).
-    const int regs = std::min(128, t.tk * t.tw + t.tk + 3 * t.tw + 32);
+    // Register level (Sec. 6 microkernel analog): TK*TW accumulators + the
+    // input window + TK kernel values + addressing; ptxas caps at 128.
+    const int win = t.ver == 2 ? (t.tw + pb.S - 1 + 3) / 4 * 4 : t.tw;
+    const int regs = std::min(128, t.tk * t.tw + t.tk + win + (t.ver == 2 ? 24 : 2 * t.tw + 28));
     const int by_regs = 65536 / (((regs + 7) / 8 * 8) * threads);
     const int by_smem = (int)(228 * 1024 / (smem + 1024));
     const int by_thr = 2048 / threads;
@@ -284,20 +285,27 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     r.ctas = std::min<long>(r.tiles, (long)per_sm * dev.sms);
     r.wave_eff = (double)r.tiles / ((double)dev.sms * per_sm_total);
     // FFMA issue: 128 lanes/clk/SM at >= 8 resident warps (2 per SMSP hide
-    // the LDS latency), proportionally less below; the register tile costs
-    // TW scalar + TK/4 vector loads + ~1 address op per TK*TW FFMA.
+    // the LDS latency), proportionally less below.  Per (c, r) the register
+    // tile costs: v1 S*(TW + TK/4 + 1) loads/address ops, v2 WIN/4 + S*TK/4 + 3.
     const double warps = (double)conc * threads / 32.0;
     const double eff = std::min(1.0, warps / 8.0);
-    const double issue_factor = 1.0 + (t.tw + t.tk / 4.0 + 1.0) / (t.tk * t.tw);
-    const double lane_fma_cta = (double)threads * t.tk * t.tw * (double)pb.C * pb.R * pb.S * issue_factor;
+    const double fma_cr = (double)pb.S * t.tk * t.tw;
+    const double over_cr = t.ver == 2 ? win / 4.0 + pb.S * t.tk / 4.0 + 3.0
+                                      : pb.S * (t.tw + t.tk / 4.0 + 1.0);
+    const double issue_factor = 1.0 + over_cr / fma_cr;
+    const double chunks = ceil((double)pb.C / t.bc);
+    // one chunk: every thread's FFMAs, plus the cp.async copies (one per 4-B
+    // element in v1/v2 In rows, ~6 instructions each, spread over the CTA)
+    const double fma_chunk_cta = (double)threads * t.tk * t.tw * t.bc * pb.R * pb.S * issue_factor;
+    const double in_elems_chunk = (double)t.bc * t.tn * (t.th + pb.R - 1) * pb.Win();
+    const double copy_chunk_cta = in_elems_chunk * 6.0 + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
-    r.t_comp_us = waves * conc * lane_fma_cta / (128.0 * eff * clk) * 1e6;
+    const double chunk_cyc = std::max((double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff), 1200.0);
+    r.t_comp_us = waves * chunks * chunk_cyc / clk * 1e6;
     // L2 -> SMEM: per CTA, every c-chunk loads the In halo tile and Ker slab
     // (Eq. 4's In and Ker footprints).
-    const double in_stage = (double)t.bc * t.tn * (t.th + pb.R - 1) * pb.Win();
     const double ker_stage = (double)t.bc * pb.R * pb.S * bko;
-    const double chunks = ceil((double)pb.C / t.bc);
-    r.dv_l2_smem = (double)r.tiles * chunks * (in_stage + ker_stage) * 4.0;
+    r.dv_l2_smem = (double)r.tiles * chunks * (in_elems_chunk + ker_stage) * 4.0;
     r.t_l2_us = r.dv_l2_smem / dev.bw_l2 * 1e6;
     r.dv_hbm = 4.0 * (pb.in_elems() + 2.0 * pb.ker_elems() + pb.out_elems());
     r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
@@ -312,6 +320,9 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     const int kgs[4] = {1, 2, 4, 8};
     const int bcs[3] = {4, 8, 16};
     const int tn_max = std::min(pb.N, 16);
+    for (int ver = 1; ver <= 2; ++ver) {
+    if (ver == 2 && !simt_v2_ok(pb)) continue;
+    if (forced && (forced_mask & 128) && ver != forced->ver) continue;
     for (int tk : tks)
     for (int tw = 1; tw <= 8; ++tw)
     for (int kg : kgs)
@@ -319,7 +330,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     for (int tn = 1; tn <= tn_max; tn = (tn < 4 ? tn + 1 : tn * 2))
     for (int bc : bcs) {
         SimtTile t;
-        t.tk = tk; t.tw = tw; t.kg = kg; t.pw = pw; t.tn = tn; t.bc = bc;
+        t.tk = tk; t.tw = tw; t.kg = kg; t.pw = pw; t.tn = tn; t.bc = bc; t.ver = ver;
         if (forced) {
             if ((forced_mask & 1) && t.tk != forced->tk) continue;
             if ((forced_mask & 2) && t.tw != forced->tw) continue;
@@ -330,19 +341,22 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         }
         if (!simt_tile_supported(t)) continue;
         // rows per tile: as many as the pixel slots allow
-        const long slots = 32L * tw * pw;
-        int th = (int)std::min<long>(pb.H, slots / ((long)tn * pb.W));
+        const long slots = 32L * pw;                                   // lanes per k-group
+        const long per_row = ver == 2 ? (pb.W + tw - 1) / tw : pb.W;   // slots one output row needs
+        const long cap = ver == 2 ? slots : slots * tw;
+        int th = (int)std::min<long>(pb.H, cap / ((long)tn * per_row));
         if (forced && (forced_mask & 32)) th = forced->th;
         if (th < 1) continue;
-        if ((long)tn * th * pb.W > slots) continue;
+        if ((long)tn * th * per_row > cap) continue;
         // slot utilisation >= 50% unless the tile already covers all pixels
         const bool whole = th >= pb.H && tn >= pb.N;
-        if (2L * tn * th * pb.W < slots && !whole && !(forced && (forced_mask & 32))) continue;
+        if (2L * tn * th * per_row < cap && !whole && !(forced && (forced_mask & 32))) continue;
         t.th = th;
         if (simt_smem_bytes(pb, t) > dev.smem_optin) continue;
         if (t.kg > 1 && t.kg * t.tk >= 2 * pb.K && !forced) continue;  // mostly-empty k tile
         ModelResult r = model_simt(pb, dev, t);
         if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+    }
     }
     if (!found) why = "no SIMT tile fits shared memory for this request";
     return found;

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "internal.h"
@@ -195,18 +196,204 @@ __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict_
     }
 }
 
+// ---------------------------------------------------------------------------
+// K4 v2: the paper's microkernel (Fig. 4) on an SM.  A thread
+// owns TK output channels x TW CONSECUTIVE output pixels of one row; per (c, r)
+// it loads the TW+S-1 input values of its window once (vector LDS from a
+// row-padded shared-memory tile) and reuses them across the S taps in
+// registers; per (c, r, s) the TK kernel values are a broadcast float4 load.
+// FFMA : LDS = S*TK*TW : (ceil((TW+S-1)/4) + S*TK/4)  (96 : 8 at TK=8,TW=4,S=3).
+struct Simt2Params {
+    int N, K, C, H, W, R, S;
+    int Hin, Win;
+    int tn, th, bc, kg;
+    int bko;          // kg * TK
+    int rows_in;      // th + R - 1
+    int pitch;        // floats per smem row (>= groups*TW + S - 1, multiple of 4)
+    int plane;        // tn * rows_in * pitch (floats per channel in smem)
+    int groups;       // ceil(W / TW): pixel groups per output row
+    int n_htiles;
+    int nchunks;
+    int slots;        // tn * th * groups (valid pixel-group slots per CTA)
+};
+
+template <int TK, int TW, int KS>
+__global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict__ in,
+                                                          const float* __restrict__ kerp,
+                                                          float* __restrict__ out, const Simt2Params p) {
+    extern __shared__ __align__(16) float sm[];
+    const int in_stage = p.bc * p.plane;
+    const int ker_stage = p.bc * p.R * KS * p.bko;
+    const int stage_floats = in_stage + ker_stage;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int kgi = warp % p.kg;
+    const int pwi = warp / p.kg;
+
+    const int nt = blockIdx.x / p.n_htiles;
+    const int ht = blockIdx.x - nt * p.n_htiles;
+    const int n0 = nt * p.tn;
+    const int h0 = ht * p.th;
+    const int kb = blockIdx.y;
+    const int k0 = kb * p.bko;
+
+    // this thread's pixel group: (img, row, g) -> pixels w0 .. w0+TW-1 of one row
+    const int q = pwi * 32 + lane;
+    const int per_img = p.th * p.groups;
+    const int img = q / per_img;
+    const int rem = q - img * per_img;
+    const int row = rem / p.groups;
+    const int g = rem - row * p.groups;
+    const int w0 = g * TW;
+    const bool valid = q < p.slots && (n0 + img) < p.N && (h0 + row) < p.H;
+    const int off = valid ? (img * p.rows_in + row) * p.pitch + w0 : 0;
+
+    float acc[TK][TW];
+#pragma unroll
+    for (int i = 0; i < TK; ++i)
+#pragma unroll
+        for (int j = 0; j < TW; ++j) acc[i][j] = 0.0f;
+
+    auto load_stage = [&](int buf, int chunk) {
+        float* in_s = sm + buf * stage_floats;
+        float* ker_s = in_s + in_stage;
+        const int c0 = chunk * p.bc;
+        // In: per (channel, image, input row) one row of Win floats into a
+        // pitch-padded smem row (the pad columns are never read for valid
+        // outputs; they hold stale data for the junk pixels of the last group).
+        const int nrows = p.bc * p.tn * p.rows_in;
+        const int rows_ok = p.Hin - h0 < p.rows_in ? p.Hin - h0 : p.rows_in;
+        const int nwarps = blockDim.x >> 5;
+        for (int rr = warp; rr < nrows; rr += nwarps) {            // one warp per input row
+            const int ir = rr % p.rows_in;
+            const int t2 = rr / p.rows_in;
+            const int im = t2 % p.tn;
+            const int cc = t2 / p.tn;
+            const int c = c0 + cc, n = n0 + im;
+            const bool ok = c < p.C && n < p.N && ir < rows_ok;
+            const float* src = in + (((int64_t)n * p.C + c) * p.Hin + h0 + ir) * p.Win;
+            float* dst = in_s + cc * p.plane + (im * p.rows_in + ir) * p.pitch;
+            for (int col = lane; col < p.Win; col += 32) cp_async4(dst + col, ok ? src + col : in, ok);
+        }
+        // Ker: contiguous slab of the packed tensor, channels >= C zero.
+        const int cvalid = p.C - c0 < p.bc ? p.C - c0 : p.bc;
+        const int len_ok = cvalid * p.R * KS * p.bko;
+        const float* gk = kerp + (((int64_t)kb * p.C + c0) * p.R * KS) * p.bko;
+        for (int e = threadIdx.x * 4; e < ker_stage; e += blockDim.x * 4)
+            cp_async16(ker_s + e, e < len_ok ? gk + e : kerp, e < len_ok);
+    };
+
+    constexpr int WIN = TW + KS - 1;
+    constexpr int WIN4 = (WIN + 3) / 4 * 4;
+    load_stage(0, 0);
+    cp_async_commit();
+    for (int chunk = 0; chunk < p.nchunks; ++chunk) {
+        const int buf = chunk & 1;
+        if (chunk + 1 < p.nchunks) load_stage(buf ^ 1, chunk + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const float* in_s = sm + buf * stage_floats;
+        const float* ker_s = in_s + in_stage;
+        const int cc_end = p.C - chunk * p.bc < p.bc ? p.C - chunk * p.bc : p.bc;
+        for (int cc = 0; cc < cc_end; ++cc) {
+            const float* ip = in_s + cc * p.plane + off;
+            const float* kp = ker_s + cc * p.R * KS * p.bko + kgi * TK;
+            for (int r = 0; r < p.R; ++r) {
+                float win[WIN4];
+#pragma unroll
+                for (int j = 0; j < WIN4; j += 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(ip + r * p.pitch + j);
+                    win[j] = v.x; win[j + 1] = v.y; win[j + 2] = v.z; win[j + 3] = v.w;
+                }
+#pragma unroll
+                for (int s = 0; s < KS; ++s) {
+                    float kv[TK];
+#pragma unroll
+                    for (int i = 0; i < TK; i += 4) {
+                        const float4 k4 = *reinterpret_cast<const float4*>(kp + (r * KS + s) * p.bko + i);
+                        kv[i] = k4.x; kv[i + 1] = k4.y; kv[i + 2] = k4.z; kv[i + 3] = k4.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < TK; ++i)
+#pragma unroll
+                        for (int j = 0; j < TW; ++j) acc[i][j] = fmaf(kv[i], win[j + s], acc[i][j]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    if (!valid) return;
+    const int h = h0 + row;
+#pragma unroll
+    for (int i = 0; i < TK; ++i) {
+        const int k = k0 + kgi * TK + i;
+        if (k >= p.K) break;
+        float* o = out + (((int64_t)(n0 + img) * p.K + k) * p.H + h) * p.W + w0;
+#pragma unroll
+        for (int j = 0; j < TW; ++j)
+            if (w0 + j < p.W) o[j] = acc[i][j];
+    }
+}
+
 bool simt_tile_supported(const SimtTile& t) {
     if (t.tk != 4 && t.tk != 8) return false;
     if (t.tw < 1 || t.tw > 8) return false;
+    if (t.ver == 2 && t.tw != 4 && t.tw != 8) return false;
     const int threads = 32 * t.kg * t.pw;
     return t.kg >= 1 && t.pw >= 1 && threads <= 512 && t.tn >= 1 && t.th >= 1 && t.bc >= 1;
 }
 
+bool simt_v2_ok(const Problem& pb) { return pb.S == 1 || pb.S == 3; }
+
+// v2 smem row pitch: the last group's window (WIN rounded up to 4) must fit;
+// multiple of 4 floats; rows of <= 16 floats of groups are offset by 16 mod 32
+// floats so that a quarter-warp's 128-bit window loads hit distinct banks.
+int simt2_pitch(const Problem& pb, const SimtTile& t) {
+    const int groups = (pb.W + t.tw - 1) / t.tw;
+    const int win4 = (t.tw + pb.S - 1 + 3) / 4 * 4;
+    int pitch = std::max((int)pb.Win(), (groups - 1) * t.tw + win4);
+    pitch = (pitch + 3) / 4 * 4;
+    if (groups * t.tw <= 16) { while (pitch % 32 != 16) pitch += 4; }
+    else if (pitch % 32 != 0 && pitch > 32) { pitch = (pitch + 31) / 32 * 32; }
+    return pitch;
+}
+
 size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
-    const size_t plane = (size_t)t.tn * (t.th + pb.R - 1) * pb.Win();
+    const size_t row = t.ver == 2 ? (size_t)simt2_pitch(pb, t) : (size_t)pb.Win();
+    const size_t plane = (size_t)t.tn * (t.th + pb.R - 1) * row;
     const size_t in_stage = (size_t)t.bc * plane;
     const size_t ker_stage = (size_t)t.bc * pb.R * pb.S * t.kg * t.tk;
     return 2 * (in_stage + ker_stage) * sizeof(float);
+}
+
+template <int TK, int TW, int KS>
+static cudaError_t launch_simt2_t(const float* in, const float* kerp, float* out, const Simt2Params& p,
+                                  dim3 grid, int threads, size_t smem, cudaStream_t st) {
+    auto kfn = conv_direct_simt2<TK, TW, KS>;
+    static std::atomic<int> smem_set{0};
+    if (smem_set.load(std::memory_order_acquire) < (int)smem) {
+        int optin = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        if (e != cudaSuccess) return e;
+        smem_set.store(optin, std::memory_order_release);
+    }
+    kfn<<<grid, threads, smem, st>>>(in, kerp, out, p);
+    return cudaGetLastError();
+}
+
+static cudaError_t dispatch_simt2(const SimtTile& t, int S, const float* in, const float* kerp, float* out,
+                                  const Simt2Params& p, dim3 grid, int threads, size_t smem, cudaStream_t st) {
+#define SIMT2_CASE(TK_, TW_, S_) \
+    if (t.tk == TK_ && t.tw == TW_ && S == S_) return launch_simt2_t<TK_, TW_, S_>(in, kerp, out, p, grid, threads, smem, st);
+    SIMT2_CASE(4, 4, 1) SIMT2_CASE(4, 8, 1) SIMT2_CASE(8, 4, 1) SIMT2_CASE(8, 8, 1)
+    SIMT2_CASE(4, 4, 3) SIMT2_CASE(4, 8, 3) SIMT2_CASE(8, 4, 3) SIMT2_CASE(8, 8, 3)
+#undef SIMT2_CASE
+    return cudaErrorInvalidValue;
 }
 
 template <int TK, int TW>
@@ -257,7 +444,7 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
     p.nchunks = (pb.C + t.bc - 1) / t.bc;
     p.bp = t.tn * t.th * pb.W;
     p.vec4_in = (p.Win % 4 == 0) ? 1 : 0;
-    if (p.bp > t.pw * 32 * t.tw) { err = "SIMT tile: pixel slots < tn*th*W"; return cudaErrorInvalidValue; }
+    if (t.ver != 2 && p.bp > t.pw * 32 * t.tw) { err = "SIMT tile: pixel slots < tn*th*W"; return cudaErrorInvalidValue; }
 
     float* kerp = static_cast<float*>(ws);
     const int64_t total = (int64_t)((pb.K + p.bko - 1) / p.bko) * p.bko * pb.C * p.RS;
@@ -270,7 +457,24 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
     dim3 grid((unsigned)(n_ntiles * p.n_htiles), (unsigned)((pb.K + p.bko - 1) / p.bko));
     const int threads = 32 * t.kg * t.pw;
     const size_t smem = simt_smem_bytes(pb, t);
-    cudaError_t e = dispatch_simt(t, in, kerp, out, p, grid, threads, smem, st);
+    cudaError_t e;
+    if (t.ver == 2) {
+        Simt2Params q;
+        q.N = pb.N; q.K = pb.K; q.C = pb.C; q.H = pb.H; q.W = pb.W; q.R = pb.R; q.S = pb.S;
+        q.Hin = (int)pb.Hin(); q.Win = (int)pb.Win();
+        q.tn = t.tn; q.th = t.th; q.bc = t.bc; q.kg = t.kg; q.bko = p.bko;
+        q.rows_in = p.rows_in;
+        q.pitch = simt2_pitch(pb, t);
+        q.plane = t.tn * q.rows_in * q.pitch;
+        q.groups = (pb.W + t.tw - 1) / t.tw;
+        q.n_htiles = p.n_htiles;
+        q.nchunks = p.nchunks;
+        q.slots = t.tn * t.th * q.groups;
+        if (q.slots > t.pw * 32) { err = "SIMT v2 tile: pixel-group slots > pw*32"; return cudaErrorInvalidValue; }
+        e = dispatch_simt2(t, pb.S, in, kerp, out, q, grid, threads, smem, st);
+    } else {
+        e = dispatch_simt(t, in, kerp, out, p, grid, threads, smem, st);
+    }
     if (e != cudaSuccess) { err = std::string("SIMT kernel launch failed: ") + cudaGetErrorString(e); return e; }
     if (ev) cudaEventRecord(ev[2], st);
     return cudaSuccess;
