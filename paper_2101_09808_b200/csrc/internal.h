@@ -46,6 +46,7 @@ struct TcTile {
     int stages = 4;      // smem ring depth
     int cg = 1;          // CTAs per MMA: 1 (M = 128) or 2 (CTA pair, M = 256)
     int kbs = 1;         // k-blocks (one TMA box of A and of B each) per pipeline stage
+    int fuse = 0;        // 1: the NCHW->NHWC In transform runs inside the main kernel
 };
 
 struct TcLayout {        // derived from Problem + element size

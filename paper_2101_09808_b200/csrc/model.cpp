@@ -169,6 +169,7 @@ static const double kClockHz = 1.84e9;   // SM clock measured under tcgen05 load
 // an SM; every pipeline stage adds ~150 cycles of barrier / commit bubble.
 static const double kStageBubbleClk = 150.0;
 static const double kEpiStoreBW = 5.0e12;  // bytes/s the whole chip's epilogues drain at
+static const double kTransformBW = 30.0e9; // bytes/s one CTA's 4 transform warps move (read+write)
 
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t) {
     ModelResult r;
@@ -187,7 +188,7 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     // tensor pipe of the busiest unit: ceil(tiles/units) tiles, each
     // R*S*n_cblk/kbs stages of kbs*(sw/32) MMAs.
     const double tiles_per_unit = ceil((double)r.tiles / units);
-    const double stages_per_tile = (double)pb.R * pb.S * L.n_cblk / t.kbs;
+    const double stages_per_tile = (double)pb.R * pb.S * L.n_cblk / t.kbs;   // k_iters / kbs
     const double mma_clk = std::max(t.bn / 2.0, 48.0);
     const double stage_clk = t.kbs * (L.sw / 32.0) * mma_clk + kStageBubbleClk;
     const double t_pipe_us = tiles_per_unit * stages_per_tile * stage_clk / kClockHz * 1e6;
@@ -208,8 +209,21 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     const double t_main = std::max({t_pipe_us, r.t_l2_us / r.wave_eff,
                                     t_smem_us / r.wave_eff, main_hbm / dev.bw_hbm * 1e6})
                           + t_tail_us + kLaunchUs;
-    const double t_rep = repack / (0.8 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
-    r.model_us = t_main + t_rep;
+    double t_rep = repack / (0.8 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
+    double t_main_f = t_main;
+    if (t.fuse) {
+        // In transform inside the main kernel: 4 warps per CTA transform the
+        // input rows of each tile (about (128/W + R - 1 + 1) rows x Win x Cp)
+        // at kTransformBW per CTA, overlapped with the tile's MMAs; the first
+        // tile's transform is exposed.  The repack launch keeps only Ker.
+        const double rows = std::min<double>(128.0 / pb.W + pb.R, (double)pb.Hin() * pb.N);
+        const double bytes_tile = rows * pb.Win() * L.Cp * (4.0 + L.elem);
+        const double t_tr_tile = bytes_tile / kTransformBW * 1e6;
+        const double t_tile = t_pipe_us / std::max(1.0, tiles_per_unit);
+        t_main_f = std::max(t_main, tiles_per_unit * std::max(t_tile, t_tr_tile) + t_tail_us + kLaunchUs) + t_tr_tile;
+        t_rep = (4.0 * pb.ker_elems() + (double)L.ker_ws_bytes) / (0.5 * dev.bw_hbm) * 1e6 + kLaunchUs;
+    }
+    r.model_us = t_main_f + t_rep;
     r.smem = tc_smem_bytes(L, t);
     return r;
 }
@@ -227,7 +241,7 @@ static int tc_max_stages(const Device& dev, const TcLayout& L, int bn, int cg, i
 }
 
 bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& best_r,
-               int force_bn, int force_stages, int force_cg, int force_kbs, std::string& why) {
+               int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, std::string& why) {
     const TcLayout L = tc_layout(pb, bf16);
     if (pb.R > 128 || pb.S > 128) { why = "R, S > 128: TMA im2col offsets are limited to [-128, 127]"; return false; }
     if (pb.M() + 256 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
@@ -237,21 +251,27 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
         if (force_cg && cg != force_cg) continue;
         for (int kbs = 1; kbs <= 4; kbs *= 2) {
             if (force_kbs && kbs != force_kbs) continue;
-            if (L.n_cblk % kbs) continue;
+            if ((pb.R * pb.S * L.n_cblk) % kbs) continue;
             for (int bn : kBNs) {
                 if (force_bn && bn != force_bn) continue;
                 if (!force_bn && bn > 32 && bn / 2 >= pb.K) continue;   // mostly padding
                 const int smax = tc_max_stages(dev, L, bn, cg, kbs);
                 // at least 3 stages unless forced (2 cannot overlap load and MMA well)
                 if (smax < (force_stages || force_kbs ? 2 : 3)) continue;
-                TcTile t;
-                t.bn = bn;
-                t.cg = cg;
-                t.kbs = kbs;
-                t.stages = force_stages ? force_stages : smax;
-                if (t.stages < 2 || t.stages > smax) continue;
-                ModelResult r = model_tc(pb, dev, bf16, t);
-                if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+                // fuse = 1 is only taken when forced: measured slower on every r01
+                // config (the in-kernel transform competes for issue slots).
+                for (int fuse = 0; fuse <= 1; ++fuse) {
+                    if (force_fuse >= 0 ? fuse != force_fuse : fuse != 0) continue;
+                    TcTile t;
+                    t.bn = bn;
+                    t.cg = cg;
+                    t.kbs = kbs;
+                    t.fuse = fuse;
+                    t.stages = force_stages ? force_stages : smax;
+                    if (t.stages < 2 || t.stages > smax) continue;
+                    ModelResult r = model_tc(pb, dev, bf16, t);
+                    if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+                }
             }
         }
     }
@@ -287,8 +307,10 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // FFMA issue: 128 lanes/clk/SM at >= 8 resident warps (2 per SMSP hide
     // the LDS latency), proportionally less below.  Per (c, r) the register
     // tile costs: v1 S*(TW + TK/4 + 1) loads/address ops, v2 WIN/4 + S*TK/4 + 3.
+    // ncu r01: 8 resident warps/SM issue on only ~54% of cycles; ~16 are
+    // needed to cover the LDS/FFMA dependency latencies.
     const double warps = (double)conc * threads / 32.0;
-    const double eff = std::min(1.0, warps / 8.0);
+    const double eff = std::min(1.0, warps / 16.0);
     const double fma_cr = (double)pb.S * t.tk * t.tw;
     const double over_cr = t.ver == 2 ? win / 4.0 + pb.S * t.tk / 4.0 + 3.0
                                       : pb.S * (t.tw + t.tk / 4.0 + 1.0);

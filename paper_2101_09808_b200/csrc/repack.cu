@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
 }
 
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
-                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev) {
+                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in) {
     RepackGeom g;
     g.C = pb.C;
     g.Cp = Cp;
@@ -160,7 +160,7 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
     g.P = pb.Hin() * pb.Win();
     g.ptiles = (int)((g.P + 63) / 64);
     g.ctiles = (Cp + 63) / 64;
-    const int64_t n_in = (int64_t)g.ptiles * g.ctiles * pb.N;
+    const int64_t n_in = with_in ? (int64_t)g.ptiles * g.ctiles * pb.N : 0;   // fused: Ker only
     const int64_t grid = g.n_ker + n_in;
     if (grid >= (1ll << 31)) return cudaErrorInvalidValue;
     const size_t smem = std::max<size_t>(64 * 65 * sizeof(float), (size_t)g.cc * g.RS * sizeof(float));

@@ -215,9 +215,10 @@ struct Simt2Params {
     int n_htiles;
     int nchunks;
     int slots;        // tn * th * groups (valid pixel-group slots per CTA)
+    int vec4;         // Win % 4 == 0: 16-B copies of input rows
 };
 
-template <int TK, int TW, int KS>
+template <int TK, int TW, int KR, int KS>   // KR = 0: runtime R
 __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict__ in,
                                                           const float* __restrict__ kerp,
                                                           float* __restrict__ out, const Simt2Params p) {
@@ -255,26 +256,64 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
 #pragma unroll
         for (int j = 0; j < TW; ++j) acc[i][j] = 0.0f;
 
+    // Copy plan of the In tile, computed once: a unit is 16 B (4 floats) of
+    // one input row when Win % 4 == 0 (rows are then 16-B aligned in NCHW and
+    // in smem), else 4 B.  Each thread owns up to kSlots units; per chunk the
+    // source only advances by bc channel planes.  Falls back to a row loop
+    // when the tile has more units than kSlots * threads.
+    constexpr int kSlots = 4;
+    const int nrows = p.bc * p.tn * p.rows_in;
+    const int upr = p.vec4 ? p.Win / 4 : p.Win;           // units per row
+    const int units = nrows * upr;
+    const bool slotted = units <= kSlots * (int)blockDim.x;
+    const int rows_ok = p.Hin - h0 < p.rows_in ? p.Hin - h0 : p.rows_in;
+    int64_t s_src[kSlots];
+    int s_dst[kSlots], s_cc[kSlots];
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) {
+        const int u = threadIdx.x + k * blockDim.x;
+        s_cc[k] = -1; s_dst[k] = 0; s_src[k] = 0;
+        if (slotted && u < units) {
+            const int rr = u / upr, col = (u - rr * upr) * (p.vec4 ? 4 : 1);
+            const int ir = rr % p.rows_in, t2 = rr / p.rows_in;
+            const int im = t2 % p.tn, cc = t2 / p.tn;
+            const int n = n0 + im;
+            s_dst[k] = cc * p.plane + (im * p.rows_in + ir) * p.pitch + col;
+            if (n < p.N && ir < rows_ok) {
+                s_cc[k] = cc;
+                s_src[k] = (((int64_t)n * p.C + cc) * p.Hin + h0 + ir) * p.Win + col;
+            } else {
+                s_cc[k] = -2;                              // zero-fill
+            }
+        }
+    }
     auto load_stage = [&](int buf, int chunk) {
         float* in_s = sm + buf * stage_floats;
         float* ker_s = in_s + in_stage;
         const int c0 = chunk * p.bc;
-        // In: per (channel, image, input row) one row of Win floats into a
-        // pitch-padded smem row (the pad columns are never read for valid
-        // outputs; they hold stale data for the junk pixels of the last group).
-        const int nrows = p.bc * p.tn * p.rows_in;
-        const int rows_ok = p.Hin - h0 < p.rows_in ? p.Hin - h0 : p.rows_in;
-        const int nwarps = blockDim.x >> 5;
-        for (int rr = warp; rr < nrows; rr += nwarps) {            // one warp per input row
-            const int ir = rr % p.rows_in;
-            const int t2 = rr / p.rows_in;
-            const int im = t2 % p.tn;
-            const int cc = t2 / p.tn;
-            const int c = c0 + cc, n = n0 + im;
-            const bool ok = c < p.C && n < p.N && ir < rows_ok;
-            const float* src = in + (((int64_t)n * p.C + c) * p.Hin + h0 + ir) * p.Win;
-            float* dst = in_s + cc * p.plane + (im * p.rows_in + ir) * p.pitch;
-            for (int col = lane; col < p.Win; col += 32) cp_async4(dst + col, ok ? src + col : in, ok);
+        if (slotted) {
+            const int64_t adv = (int64_t)c0 * p.Hin * p.Win;
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k) {
+                if (s_cc[k] == -1) continue;
+                const bool ok = s_cc[k] >= 0 && c0 + s_cc[k] < p.C;
+                const float* src = ok ? in + s_src[k] + adv : in;
+                if (p.vec4) cp_async16(in_s + s_dst[k], src, ok);
+                else cp_async4(in_s + s_dst[k], src, ok);
+            }
+        } else {
+            const int nwarps = blockDim.x >> 5;
+            for (int rr = warp; rr < nrows; rr += nwarps) {            // one warp per input row
+                const int ir = rr % p.rows_in;
+                const int t2 = rr / p.rows_in;
+                const int im = t2 % p.tn;
+                const int cc = t2 / p.tn;
+                const int c = c0 + cc, n = n0 + im;
+                const bool ok = c < p.C && n < p.N && ir < rows_ok;
+                const float* src = in + (((int64_t)n * p.C + c) * p.Hin + h0 + ir) * p.Win;
+                float* dst = in_s + cc * p.plane + (im * p.rows_in + ir) * p.pitch;
+                for (int col = lane; col < p.Win; col += 32) cp_async4(dst + col, ok ? src + col : in, ok);
+            }
         }
         // Ker: contiguous slab of the packed tensor, channels >= C zero.
         const int cvalid = p.C - c0 < p.bc ? p.C - c0 : p.bc;
@@ -297,10 +336,12 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
         const float* in_s = sm + buf * stage_floats;
         const float* ker_s = in_s + in_stage;
         const int cc_end = p.C - chunk * p.bc < p.bc ? p.C - chunk * p.bc : p.bc;
+        const int R = KR ? KR : p.R;
         for (int cc = 0; cc < cc_end; ++cc) {
             const float* ip = in_s + cc * p.plane + off;
-            const float* kp = ker_s + cc * p.R * KS * p.bko + kgi * TK;
-            for (int r = 0; r < p.R; ++r) {
+            const float* kp = ker_s + cc * R * KS * p.bko + kgi * TK;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
                 float win[WIN4];
 #pragma unroll
                 for (int j = 0; j < WIN4; j += 4) {
@@ -356,8 +397,7 @@ int simt2_pitch(const Problem& pb, const SimtTile& t) {
     const int win4 = (t.tw + pb.S - 1 + 3) / 4 * 4;
     int pitch = std::max((int)pb.Win(), (groups - 1) * t.tw + win4);
     pitch = (pitch + 3) / 4 * 4;
-    if (groups * t.tw <= 16) { while (pitch % 32 != 16) pitch += 4; }
-    else if (pitch % 32 != 0 && pitch > 32) { pitch = (pitch + 31) / 32 * 32; }
+    if (pitch % 32 == 0) pitch += 4;      // rows 128 B apart would put every row's window on the same banks
     return pitch;
 }
 
@@ -369,10 +409,10 @@ size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
     return 2 * (in_stage + ker_stage) * sizeof(float);
 }
 
-template <int TK, int TW, int KS>
+template <int TK, int TW, int KR, int KS>
 static cudaError_t launch_simt2_t(const float* in, const float* kerp, float* out, const Simt2Params& p,
                                   dim3 grid, int threads, size_t smem, cudaStream_t st) {
-    auto kfn = conv_direct_simt2<TK, TW, KS>;
+    auto kfn = conv_direct_simt2<TK, TW, KR, KS>;
     static std::atomic<int> smem_set{0};
     if (smem_set.load(std::memory_order_acquire) < (int)smem) {
         int optin = 0, dev = 0;
@@ -386,12 +426,15 @@ static cudaError_t launch_simt2_t(const float* in, const float* kerp, float* out
     return cudaGetLastError();
 }
 
-static cudaError_t dispatch_simt2(const SimtTile& t, int S, const float* in, const float* kerp, float* out,
+static cudaError_t dispatch_simt2(const SimtTile& t, int R, int S, const float* in, const float* kerp, float* out,
                                   const Simt2Params& p, dim3 grid, int threads, size_t smem, cudaStream_t st) {
-#define SIMT2_CASE(TK_, TW_, S_) \
-    if (t.tk == TK_ && t.tw == TW_ && S == S_) return launch_simt2_t<TK_, TW_, S_>(in, kerp, out, p, grid, threads, smem, st);
-    SIMT2_CASE(4, 4, 1) SIMT2_CASE(4, 8, 1) SIMT2_CASE(8, 4, 1) SIMT2_CASE(8, 8, 1)
-    SIMT2_CASE(4, 4, 3) SIMT2_CASE(4, 8, 3) SIMT2_CASE(8, 4, 3) SIMT2_CASE(8, 8, 3)
+#define SIMT2_CASE(TK_, TW_, R_, S_) \
+    if (t.tk == TK_ && t.tw == TW_ && (R_ == 0 || R == R_) && S == S_) \
+        return launch_simt2_t<TK_, TW_, R_, S_>(in, kerp, out, p, grid, threads, smem, st);
+    SIMT2_CASE(4, 4, 1, 1) SIMT2_CASE(4, 8, 1, 1) SIMT2_CASE(8, 4, 1, 1) SIMT2_CASE(8, 8, 1, 1)
+    SIMT2_CASE(4, 4, 3, 3) SIMT2_CASE(4, 8, 3, 3) SIMT2_CASE(8, 4, 3, 3) SIMT2_CASE(8, 8, 3, 3)
+    SIMT2_CASE(4, 4, 0, 1) SIMT2_CASE(4, 8, 0, 1) SIMT2_CASE(8, 4, 0, 1) SIMT2_CASE(8, 8, 0, 1)
+    SIMT2_CASE(4, 4, 0, 3) SIMT2_CASE(4, 8, 0, 3) SIMT2_CASE(8, 4, 0, 3) SIMT2_CASE(8, 8, 0, 3)
 #undef SIMT2_CASE
     return cudaErrorInvalidValue;
 }
@@ -471,7 +514,8 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
         q.nchunks = p.nchunks;
         q.slots = t.tn * t.th * q.groups;
         if (q.slots > t.pw * 32) { err = "SIMT v2 tile: pixel-group slots > pw*32"; return cudaErrorInvalidValue; }
-        e = dispatch_simt2(t, pb.S, in, kerp, out, q, grid, threads, smem, st);
+        q.vec4 = (q.Win % 4 == 0) ? 1 : 0;
+        e = dispatch_simt2(t, pb.R, pb.S, in, kerp, out, q, grid, threads, smem, st);
     } else {
         e = dispatch_simt(t, in, kerp, out, p, grid, threads, smem, st);
     }

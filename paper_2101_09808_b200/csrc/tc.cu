@@ -8,14 +8,20 @@
 // operands are K-major with the 32/64/128-B swizzle matching the k-block's
 // byte width.  tcgen05.mma (M = 128, N = BN) accumulates fp32 in TMEM.
 //
-// Warp roles (256 threads, one CTA per SM, persistent over tiles):
-//   warp 0  TMA producer (one lane)       -> full[stage]  (mbarrier, tx bytes)
-//   warp 1  MMA issuer   (one lane)       -> empty[stage] (tcgen05.commit)
+// Warp roles (384 threads, one CTA per SM, persistent over tiles).  The
+// warp arbiter favours higher warp ids, so the latency-critical issuers get
+// the highest ones:
+//   warp 11   MMA issuer (elected lane)   -> empty[stage] (tcgen05.commit)
 //                                          -> tmem_full[acc]
-//   warp 2  TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warp 10   TMA producer (elected lane) -> full[stage]  (mbarrier, tx bytes)
+//   warp 8    TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
 //   warps 4-7 epilogue: tcgen05.ld 32x32b (warp w%4 owns TMEM lanes 32(w%4)..)
 //             -> coalesced st.global into NCHW Out (consecutive TMEM lanes are
 //             consecutive pixels of one (n,k) plane)   -> tmem_empty[acc]
+//   warps 0-3 (fuse = 1) In transform: NCHW fp32 -> NHWC rows of the next
+//             channel block, one block ahead of the producer -> in_full[]
+// k-loop order: c-block outermost, then r, then s; a pipeline stage holds
+// kbs consecutive iterations of that order.
 //
 // Accumulation order per output element is fixed by the k-loop (r, s, c-block
 // ascending) and does not depend on the tile shape or on the grid, so results
@@ -39,7 +45,7 @@ namespace conv {
 using namespace sm100;
 
 static constexpr int kBM = 128;
-static constexpr int kThreads = 256;
+static constexpr int kThreads = 384;        // 12 warps: TMA, MMA, alloc, -, 4 epilogue, 4 In-transform
 
 struct TcParams {
     float* out;
@@ -59,7 +65,97 @@ struct TcParams {
     uint32_t b_stage_bytes;   // kbs * (bn / cg) * sw
     uint32_t debug;           // experiments only (env CONV_DEBUG_MODE): 1 no MMA, 2 no TMA, 4 no stores
     unsigned long long* trace;  // experiments only (env CONV_TRACE): per-CTA timeline, 64 slots
+    // fused In transform (a-3 inside the main kernel): NCHW fp32 -> NHWC workspace
+    int fuse;                 // 1: warps 8-11 write the NHWC rows each tile needs; 0: workspace pre-filled
+    const float* in;          // NCHW fp32 In
+    void* in_ws;              // NHWC workspace (tf32-in-fp32 or bf16), [N][Hin][Win][Cp]
+    int C, Hin, Win;
 };
+
+// ---- fused NCHW -> NHWC transform of the input rows one tile needs ----------
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// The rows of In (image n, input row h_in, all Win pixels, all Cp channels)
+// read by the im2col loads of output pixels [m0, m0 + 128): for every image
+// the tile touches, output rows h_lo..h_hi need input rows h_lo..h_hi+R-1.
+// Work item = (row, VEC channels, 4 pixels) when the NCHW rows allow float4
+// loads (Win % 4 == 0), else (row, VEC channels, 1 pixel); one 16-B store
+// per pixel of VEC converted channels.  nthr threads starting at tid.
+template <bool BF16>
+__device__ void transform_tile_rows(const TcParams& p, int m0, int cbeg, int cend, int tid, int nthr) {
+    constexpr int VEC = BF16 ? 8 : 4;
+    constexpr int ES = BF16 ? 2 : 4;
+    const int m1 = min(m0 + 128, p.M) - 1;
+    if (m1 < m0) return;
+    const int n_a = m0 / p.HW, n_b = m1 / p.HW;
+    const bool vec4 = (p.Win & 3) == 0;
+    const int pg = vec4 ? 4 : 1;
+    const int groups = p.Win / pg;                 // pixel groups per row
+    const int cvecs = (cend - cbeg) / VEC;
+    const int per_row = groups * cvecs;
+    const int64_t P = (int64_t)p.Hin * p.Win;
+    for (int i0 = tid; i0 < per_row; i0 += nthr) {  // usually one (cv, g) per thread
+        const int cv = i0 / groups;
+        const int g = i0 - cv * groups;
+        const int w0 = g * pg;
+        const int c0 = cbeg + cv * VEC;
+        for (int n = n_a; n <= n_b; ++n) {
+            const int p_lo = n == n_a ? m0 - n * p.HW : 0;
+            const int p_hi = n == n_b ? m1 - n * p.HW : p.HW - 1;
+            const int h_lo = p_lo / p.W;
+            const int h_hi = min(p_hi / p.W + p.R - 1, p.Hin - 1);
+            const float* src = p.in + ((int64_t)n * p.C + c0) * P + (int64_t)h_lo * p.Win + w0;
+            uint8_t* dst = reinterpret_cast<uint8_t*>(p.in_ws) +
+                           ((((int64_t)n * p.Hin + h_lo) * p.Win + w0) * p.Cp + c0) * ES;
+            const int64_t dst_row = (int64_t)p.Win * p.Cp * ES;
+            for (int h = h_lo; h <= h_hi; ++h, src += p.Win, dst += dst_row) {
+                float v[VEC][4];
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) {
+                    if (c0 + j < p.C) {
+                        const float* s = src + (int64_t)j * P;
+                        if (vec4) {
+                            const float4 x = __ldg(reinterpret_cast<const float4*>(s));
+                            v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
+                        } else {
+                            v[j][0] = __ldg(s);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) v[j][q] = 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (q < pg) {
+                        uint4 o;
+                        if (BF16) {
+                            o.x = pack_bf16x2(v[0][q], v[1][q]);
+                            o.y = pack_bf16x2(v[2][q], v[3][q]);
+                            o.z = pack_bf16x2(v[4 % VEC][q], v[5 % VEC][q]);
+                            o.w = pack_bf16x2(v[6 % VEC][q], v[7 % VEC][q]);
+                        } else {
+                            o.x = __float_as_uint(tf32_rna(v[0][q]));
+                            o.y = __float_as_uint(tf32_rna(v[1][q]));
+                            o.z = __float_as_uint(tf32_rna(v[2][q]));
+                            o.w = __float_as_uint(tf32_rna(v[3][q]));
+                        }
+                        *reinterpret_cast<uint4*>(dst + (int64_t)q * p.Cp * ES) = o;
+                    }
+                }
+            }
+        }
+    }
+}
 
 // CG = 1: one CTA per 128-pixel tile (tcgen05 cta_group::1, M = 128).
 // CG = 2: a CTA pair (cluster of 2 on one TPC) per 256-pixel tile
@@ -82,7 +178,9 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     uint64_t* empty = bars + p.stages;
     uint64_t* tmem_full = bars + 2 * p.stages;
     uint64_t* tmem_empty = tmem_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    uint64_t* in_full = tmem_empty + 2;           // fused In transform -> producer
+    uint64_t* in_empty = in_full + 2;             // producer -> In transform (bounds run-ahead)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(in_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -103,10 +201,12 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
             mbar_init(&tmem_empty[i], 4 * CG);    // one arrive per epilogue warp of the pair
+            mbar_init(&in_full[i], 4);            // one arrive per transform warp
+            mbar_init(&in_empty[i], 1);
         }
         fence_barrier_init();
     }
-    if (warp == 2) {
+    if (warp == 8) {
         if (CG == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
         else tmem_alloc(tmem_slot, kTmemCols);
     }
@@ -116,7 +216,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t wflavor = (p.debug >> 3) & 3;
 
-    if (warp == 0) {
+    if (warp == 10) {
         // ===== TMA producer (both CTAs of a pair): the whole warp runs the
         // loop (warp-uniform control flow keeps the operands in uniform
         // registers), one elected lane issues =====
@@ -127,6 +227,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             long long prod_wait = 0;
             int stage = 0;
             uint32_t phase = 0;
+            int u = 0;                                    // (tile, channel group) units
             for (int tile = unit; tile < p.num_tiles; tile += nunits) {
                 const int m_tile = tile / p.num_n_tiles;
                 const int n_tile = tile - m_tile * p.num_n_tiles;
@@ -137,37 +238,43 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 const int w0 = pix - h0 * p.W;
                 const int kb0 = n_tile * BN + (int)rank * (BN / CG);   // this CTA's B rows
                 const uint32_t a_blk = kBM * p.sw, b_blk = (BN / CG) * p.sw;
-                for (int r = 0; r < p.R; ++r) {
-                    for (int s = 0; s < p.S; ++s) {
-                        for (int cb0 = 0; cb0 < p.n_cblk; cb0 += p.kbs) {
-                            const long long pw0 = p.trace ? clock64() : 0;
-                            mbar_wait_flavor(&empty[stage], phase ^ 1, wflavor);
-                            if (p.trace) prod_wait += clock64() - pw0;
-                            uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
-                            uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
-                            if (!elect_one_sync()) {
-                            } else if (p.debug & 2) {
-                                if (leader) mbar_arrive(&full[stage]);
+                const int RS = p.R * p.S;
+                // k iterations in the fixed order (cb, r, s); a stage holds kbs
+                // consecutive iterations, so the order does not depend on kbs.
+                for (int it0 = 0; it0 < p.k_iters; it0 += p.kbs) {
+                    const long long pw0 = p.trace ? clock64() : 0;
+                    mbar_wait_flavor(&empty[stage], phase ^ 1, wflavor);
+                    if (p.trace) prod_wait += clock64() - pw0;
+                    uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
+                    uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
+                    for (int kb = 0; kb < p.kbs; ++kb) {
+                        const int it = it0 + kb;
+                        const int cb = it / RS;
+                        const int rs = it - cb * RS;
+                        const int r = rs / p.S, s = rs - r * p.S;
+                        if (p.fuse && rs == 0) mbar_wait(&in_full[u & 1], (u >> 1) & 1);   // channel block written
+                        if (elect_one_sync()) {
+                            if (p.debug & 2) {
+                                if (leader && kb == 0) mbar_arrive(&full[stage]);
                             } else {
-                                if (leader) mbar_arrive_expect_tx(&full[stage], tx_bytes);
-                                for (int kb = 0; kb < p.kbs; ++kb) {
-                                    const int cb = cb0 + kb;
-                                    const int bx = (r * p.S + s) * p.Cp + cb * p.bkc;
-                                    if (CG == 2) {
-                                        tma_load_im2col_4d_pair(a_dst + kb * a_blk, &tmap_a, &full[stage], cb * p.bkc,
-                                                                w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
-                                        tma_load_2d_pair(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
-                                    } else {
-                                        tma_load_im2col_4d(a_dst + kb * a_blk, &tmap_a, &full[stage], cb * p.bkc,
-                                                           w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
-                                        tma_load_2d(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
-                                    }
+                                if (leader && kb == 0) mbar_arrive_expect_tx(&full[stage], tx_bytes);
+                                const int bx = (r * p.S + s) * p.Cp + cb * p.bkc;
+                                if (CG == 2) {
+                                    tma_load_im2col_4d_pair(a_dst + kb * a_blk, &tmap_a, &full[stage], cb * p.bkc,
+                                                            w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
+                                    tma_load_2d_pair(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
+                                } else {
+                                    tma_load_im2col_4d(a_dst + kb * a_blk, &tmap_a, &full[stage], cb * p.bkc,
+                                                       w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
+                                    tma_load_2d(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
                                 }
                             }
-                            __syncwarp();
-                            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                            if (p.fuse && rs == RS - 1) mbar_arrive(&in_empty[u & 1]);
                         }
+                        __syncwarp();
+                        if (p.fuse && rs == RS - 1) ++u;
                     }
+                    if (++stage == p.stages) { stage = 0; phase ^= 1; }
                 }
             }
             if (p.trace && lane == 0) {
@@ -175,7 +282,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 p.trace[(size_t)blockIdx.x * 64 + 61] = globaltimer_ns();
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 11) {
         // ===== MMA issuer (leader CTA only): whole warp loops, one elected
         // lane issues the tcgen05 instructions =====
         if (leader) {
@@ -251,7 +358,28 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp < 4) {
+        // ===== fused In transform: NCHW fp32 -> NHWC rows, one channel group
+        // ahead of the producer =====
+        if (p.fuse) {
+            const int tid = threadIdx.x;
+            int u = 0;
+            for (int tile = unit; tile < p.num_tiles; tile += nunits) {
+                const int m_tile = tile / p.num_n_tiles;
+                // Every CTA writes the rows its own tiles read (tiles of other
+                // CTAs may rewrite the same rows with the same values): the
+                // only ordering needed is CTA-local.
+                for (int cb = 0; cb < p.n_cblk; ++cb, ++u) {
+                    mbar_wait_sleep(&in_empty[u & 1], ((u >> 1) & 1) ^ 1, 64);
+                    transform_tile_rows<BF16>(p, m_tile * (kBM * CG) + (int)rank * kBM, cb * p.bkc,
+                                              (cb + 1) * p.bkc, tid, 128);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&in_full[u & 1]);
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
         // ===== epilogue: TMEM -> registers -> NCHW Out =====
         const int q = warp & 3;                       // TMEM lane quadrant of this warp
         const int row = q * 32 + (int)lane;           // accumulator row = pixel within the CTA's tile
@@ -305,7 +433,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     // accumulator) before the TMEM is released.
     tc_fence_before();
     if (CG == 2) cluster_sync_all(); else __syncthreads();
-    if (warp == 2) {
+    if (warp == 8) {
         tc_fence_after();
         if (CG == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
         else tmem_dealloc(tmem_base, kTmemCols);
@@ -334,11 +462,11 @@ TcLayout tc_layout(const Problem& pb, bool bf16) {
 
 size_t tc_smem_bytes(const TcLayout& L, const TcTile& t) {
     const size_t a = (size_t)t.kbs * kBM * L.sw, b = (size_t)t.kbs * (t.bn / t.cg) * L.sw;
-    return 1024 /*align slack*/ + (size_t)t.stages * (a + b) + (2 * t.stages + 4) * 8 + 16;
+    return 1024 /*align slack*/ + (size_t)t.stages * (a + b) + (2 * t.stages + 8) * 8 + 16;
 }
 
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
-                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev);
+                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in);
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -405,7 +533,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     // Tensor maps depend on the workspace address, known only here; they are
     // encoded on first use and cached per (workspace, problem, tile).
     struct Key {
-        const void* ws; Problem pb; int bn; int cg; int kbs; int bf16; int dev;
+        const void* ws; Problem pb; int bn; int cg; int kbs; int bf16; int dev;  // (fuse does not change the maps)
     };
     struct Entry { Key k; CUtensorMap ta, tb; };
     static std::mutex mu;
@@ -461,7 +589,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     if (n_cached < 16) ++n_cached;
     }
 
-    cudaError_t e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev);
+    cudaError_t e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse);
     if (e != cudaSuccess) { err = "repack launch failed"; return e; }
 
     TcParams prm;
@@ -482,6 +610,12 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         return e ? (uint32_t)atoi(e) : 0u;
     }();
     prm.debug = debug_mode;
+    prm.fuse = t.fuse;
+    prm.in = in;
+    prm.in_ws = in_ws;
+    prm.C = pb.C;
+    prm.Hin = (int)pb.Hin();
+    prm.Win = (int)pb.Win();
     static const char* trace_path = getenv("CONV_TRACE");
     static unsigned long long* trace_buf = nullptr;
     prm.trace = nullptr;
@@ -501,7 +635,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     const int units = num_sms / t.cg;
     const int grid = (prm.num_tiles < units ? prm.num_tiles : units) * t.cg;
     const size_t smem = tc_smem_bytes(L, t);
-    if (L.n_cblk % t.kbs != 0) { err = "k-blocks per stage must divide the c-block count"; return cudaErrorInvalidValue; }
+    if (prm.k_iters % t.kbs != 0) { err = "k-blocks per stage must divide R*S*c-blocks"; return cudaErrorInvalidValue; }
     if (t.cg == 2)
         e = bf16 ? launch_tc_sw<true, 2>(L.sw, t.bn, ta, tb, prm, smem, grid, st)
                  : launch_tc_sw<false, 2>(L.sw, t.bn, ta, tb, prm, smem, grid, st);

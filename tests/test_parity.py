@@ -70,16 +70,19 @@ def test_integer_twin_bit_exact(path, shape):
 
 @pytest.mark.parametrize("path", ["tf32", "bf16"])
 @pytest.mark.parametrize("cg", [1, 2])
-@pytest.mark.parametrize("shape", SMALL + ODD[:4], ids=lambda s: "x".join(map(str, s.as_tuple())))
-def test_tensor_cta_group_variants(path, cg, shape):
-    """Both the 1-CTA (M=128) and the CTA-pair (M=256) kernels, forced."""
+@pytest.mark.parametrize("fuse", [0, 1])
+@pytest.mark.parametrize("shape", SMALL + ODD, ids=lambda s: "x".join(map(str, s.as_tuple())))
+def test_tensor_cta_group_variants(path, cg, fuse, shape):
+    """Both the 1-CTA (M=128) and the CTA-pair (M=256) kernels, with the In
+    transform as a separate launch (fuse=0) or inside the kernel (fuse=1)."""
+    spec = f"cg={cg},fuse={fuse}"
     inp, ker = make_inputs(shape, seed=1, kind="int")
-    got, plan = run(shape, inp, ker, path, tile=f"cg={cg}")
-    assert plan.describe()["tile"]["cg"] == cg
+    got, plan = run(shape, inp, ker, path, tile=spec)
+    assert plan.describe()["tile"]["cg"] == cg and plan.describe()["tile"]["fuse"] == fuse
     ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
     assert np.array_equal(got.astype(np.float64), ref)
     inp, ker = make_inputs(shape, seed=0)
-    got, _ = run(shape, inp, ker, path, tile=f"cg={cg}")
+    got, _ = run(shape, inp, ker, path, tile=spec)
     ref = oracle.conv_eq1(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()))
     assert rel_l2(got, ref) <= 1e-5
 
@@ -117,9 +120,9 @@ def test_p10_tile_invariance_tensor(path):
     inp, ker = make_inputs(sh, seed=7)
     outs = []
     for cg in (1, 2):
-        for bn, kbs in ((32, 1), (64, 2), (128, 4), (192, 1), (256, 2)):
+        for bn, kbs, fuse in ((32, 1, 0), (64, 2, 1), (128, 4, 0), (192, 1, 1), (256, 2, 1)):
             try:
-                got, plan = run(sh, inp, ker, path, tile=f"bn={bn},cg={cg},kbs={kbs}")
+                got, plan = run(sh, inp, ker, path, tile=f"bn={bn},cg={cg},kbs={kbs},fuse={fuse}")
             except conv.ConvError as e:           # e.g. kbs=4 stages do not fit smem
                 assert e.status == conv.CONV_ERR_INFEASIBLE
                 continue
