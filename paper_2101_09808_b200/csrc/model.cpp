@@ -314,7 +314,9 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const double fma_cr = (double)pb.S * t.tk * t.tw;
     const double over_cr = t.ver == 2 ? win / 4.0 + pb.S * t.tk / 4.0 + 3.0
                                       : pb.S * (t.tw + t.tk / 4.0 + 1.0);
-    const double issue_factor = 1.0 + over_cr / fma_cr;
+    // v1's strided scalar loads and per-tap address math measured ~1.5-2.5x
+    // slower than v2 on every r01 config (scripts/simt_sweep.py).
+    const double issue_factor = (1.0 + over_cr / fma_cr) * (t.ver == 2 ? 1.0 : 1.6);
     const double chunks = ceil((double)pb.C / t.bc);
     // one chunk: every thread's FFMAs, plus the cp.async copies (one per 4-B
     // element in v1/v2 In rows, ~6 instructions each, spread over the CTA)
@@ -322,7 +324,8 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const double in_elems_chunk = (double)t.bc * t.tn * (t.th + pb.R - 1) * pb.Win();
     const double copy_chunk_cta = in_elems_chunk * 6.0 + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
-    const double chunk_cyc = std::max((double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff), 1200.0);
+    // a chunk cannot take less than one L2 round trip + two barriers
+    const double chunk_cyc = std::max((double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff), 2000.0);
     r.t_comp_us = waves * chunks * chunk_cyc / clk * 1e6;
     // L2 -> SMEM: per CTA, every c-chunk loads the In halo tile and Ker slab
     // (Eq. 4's In and Ker footprints).

@@ -65,6 +65,10 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
                                                   typename Elem<BF16>::T* __restrict__ ker_ws, const RepackGeom g) {
     extern __shared__ float sm[];
     const int tid = threadIdx.x;
+    // let the dependent main kernel (launched with programmatic stream
+    // serialization) start its prologue as SMs free up; it waits for this
+    // grid's completion (griddepcontrol.wait) before reading the workspace
+    asm volatile("griddepcontrol.launch_dependents;");
     if ((int)blockIdx.x < g.n_ker) {
         // ---- K1 ----
         const int64_t k = blockIdx.x / g.ker_chunks;

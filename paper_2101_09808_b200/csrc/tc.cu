@@ -215,6 +215,10 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t wflavor = (p.debug >> 3) & 3;
+    // Programmatic dependent launch: everything above overlapped the tail of
+    // the repack launch; from here on the repacked workspace is read (and Out
+    // written), so wait for the preceding grid to complete and flush.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 10) {
         // ===== TMA producer (both CTAs of a pair): the whole warp runs the
@@ -489,13 +493,15 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL after the repack
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kfn, ta, tb, prm);
 }
 

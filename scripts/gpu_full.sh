@@ -1,5 +1,5 @@
 #!/bin/bash
-# GPU round: tests, smoke, bench (tensor paths), ncu launch list + full capture.
+# GPU round: tests, smoke, bench (all paths), ncu launch list + full captures.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -3
@@ -18,7 +18,8 @@ if [ -n "$NCU" ]; then
   $CMD > gpurun_out/plain2.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_igemm -s 3 -c 1 -o gpurun_out/prof_bf16 $CMD > gpurun_out/ncu_full.log 2>&1
   echo "ncu full rc=$?"
-  $CMD > gpurun_out/plain3.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:repack -s 3 -c 1 -o gpurun_out/prof_repack_bf16 $CMD > gpurun_out/ncu_full_repack.log 2>&1
-  echo "ncu repack rc=$?"
+  C2="python scripts/run_once.py fp32_simt batched"
+  $C2 > gpurun_out/plain3.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_direct -s 1 -c 1 -o gpurun_out/prof_simt $C2 > gpurun_out/ncu_simt.log 2>&1
+  echo "ncu simt rc=$?"
 fi
