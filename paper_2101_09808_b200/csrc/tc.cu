@@ -70,6 +70,7 @@ struct TcParams {
     const float* in;          // NCHW fp32 In
     void* in_ws;              // NHWC workspace (tf32-in-fp32 or bf16), [N][Hin][Win][Cp]
     int C, Hin, Win;
+    int tap_outer;            // k order: 1 = (r, s, cb) [not with fuse], 0 = (cb, r, s)
 };
 
 // ---- fused NCHW -> NHWC transform of the input rows one tile needs ----------
@@ -231,7 +232,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             long long prod_wait = 0;
             int stage = 0;
             uint32_t phase = 0;
-            int u = 0;                                    // (tile, channel group) units
+            int u = 0, ue = 0;                            // (tile, channel block) units: waited / released
             for (int tile = unit; tile < p.num_tiles; tile += nunits) {
                 const int m_tile = tile / p.num_n_tiles;
                 const int n_tile = tile - m_tile * p.num_n_tiles;
@@ -242,41 +243,71 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 const int w0 = pix - h0 * p.W;
                 const int kb0 = n_tile * BN + (int)rank * (BN / CG);   // this CTA's B rows
                 const uint32_t a_blk = kBM * p.sw, b_blk = (BN / CG) * p.sw;
-                const int RS = p.R * p.S;
-                // k iterations in the fixed order (cb, r, s); a stage holds kbs
+                // k iterations in a fixed order -- (cb, r, s) or (r, s, cb) --
+                // tracked by counters (no divisions); a stage holds kbs
                 // consecutive iterations, so the order does not depend on kbs.
+                int cb = 0, r = 0, s = 0;
                 for (int it0 = 0; it0 < p.k_iters; it0 += p.kbs) {
+                    if (p.fuse) {   // channel blocks that start inside this stage must be written
+                        int c2 = cb, r2 = r, s2 = s;
+                        for (int kb = 0; kb < p.kbs; ++kb) {
+                            if (r2 == 0 && s2 == 0) { mbar_wait(&in_full[u & 1], (u >> 1) & 1); ++u; }
+                            if (++s2 == p.S) { s2 = 0; if (++r2 == p.R) { r2 = 0; ++c2; } }
+                        }
+                    }
                     const long long pw0 = p.trace ? clock64() : 0;
                     mbar_wait_flavor(&empty[stage], phase ^ 1, wflavor);
                     if (p.trace) prod_wait += clock64() - pw0;
                     uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
                     uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
+                    const int cb_s = cb, r_s = r, s_s = s;
+                    // advance the counters past this stage (all lanes, uniform)
                     for (int kb = 0; kb < p.kbs; ++kb) {
-                        const int it = it0 + kb;
-                        const int cb = it / RS;
-                        const int rs = it - cb * RS;
-                        const int r = rs / p.S, s = rs - r * p.S;
-                        if (p.fuse && rs == 0) mbar_wait(&in_full[u & 1], (u >> 1) & 1);   // channel block written
-                        if (elect_one_sync()) {
-                            if (p.debug & 2) {
-                                if (leader && kb == 0) mbar_arrive(&full[stage]);
-                            } else {
-                                if (leader && kb == 0) mbar_arrive_expect_tx(&full[stage], tx_bytes);
-                                const int bx = (r * p.S + s) * p.Cp + cb * p.bkc;
+                        if (p.tap_outer) {
+                            if (++cb == p.n_cblk) { cb = 0; if (++s == p.S) { s = 0; ++r; } }
+                        } else {
+                            if (++s == p.S) { s = 0; if (++r == p.R) { r = 0; ++cb; } }
+                        }
+                    }
+                    if (elect_one_sync()) {
+                        if (p.debug & 2) {
+                            if (leader) mbar_arrive(&full[stage]);
+                        } else {
+                            if (leader) mbar_arrive_expect_tx(&full[stage], tx_bytes);
+                            int c1 = cb_s, r1 = r_s, s1 = s_s;
+                            for (int kb = 0; kb < p.kbs; ++kb) {
+                                const int bx = (r1 * p.S + s1) * p.Cp + c1 * p.bkc;
                                 if (CG == 2) {
-                                    tma_load_im2col_4d_pair(a_dst + kb * a_blk, &tmap_a, &full[stage], cb * p.bkc,
-                                                            w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
+                                    tma_load_im2col_4d_pair(a_dst + kb * a_blk, &tmap_a, &full[stage], c1 * p.bkc,
+                                                            w0, h0, img, (uint16_t)s1, (uint16_t)r1, pol_a);
                                     tma_load_2d_pair(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
                                 } else {
-                                    tma_load_im2col_4d(a_dst + kb * a_blk, &tmap_a, &full[stage], cb * p.bkc,
-                                                       w0, h0, img, (uint16_t)s, (uint16_t)r, pol_a);
+                                    tma_load_im2col_4d(a_dst + kb * a_blk, &tmap_a, &full[stage], c1 * p.bkc,
+                                                       w0, h0, img, (uint16_t)s1, (uint16_t)r1, pol_a);
                                     tma_load_2d(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
                                 }
+                                if (p.tap_outer) {
+                                    if (++c1 == p.n_cblk) { c1 = 0; if (++s1 == p.S) { s1 = 0; ++r1; } }
+                                } else {
+                                    if (++s1 == p.S) { s1 = 0; if (++r1 == p.R) { r1 = 0; ++c1; } }
+                                }
                             }
-                            if (p.fuse && rs == RS - 1) mbar_arrive(&in_empty[u & 1]);
                         }
-                        __syncwarp();
-                        if (p.fuse && rs == RS - 1) ++u;
+                        if (p.fuse) {   // channel blocks that end inside this stage are consumed
+                            int r2 = r_s, s2 = s_s, e2 = ue;
+                            for (int kb = 0; kb < p.kbs; ++kb) {
+                                if (r2 == p.R - 1 && s2 == p.S - 1) mbar_arrive(&in_empty[(e2++) & 1]);
+                                if (++s2 == p.S) { s2 = 0; if (++r2 == p.R) r2 = 0; }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (p.fuse) {   // same count in every lane (uniform)
+                        int r2 = r_s, s2 = s_s;
+                        for (int kb = 0; kb < p.kbs; ++kb) {
+                            if (r2 == p.R - 1 && s2 == p.S - 1) ++ue;
+                            if (++s2 == p.S) { s2 = 0; if (++r2 == p.R) r2 = 0; }
+                        }
                     }
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
                 }
@@ -498,8 +529,9 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    static const int no_pdl = getenv("CONV_NO_PDL") ? 1 : 0;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL after the repack
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kfn, ta, tb, prm);
@@ -617,6 +649,10 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     }();
     prm.debug = debug_mode;
     prm.fuse = t.fuse;
+    static const int env_order = [] { const char* e = getenv("CONV_KORDER"); return e ? atoi(e) : -1; }();
+    // One order for every configuration (fused or not), so results are
+    // bit-identical across tilings (P10); env CONV_KORDER=1 is for experiments.
+    prm.tap_outer = t.fuse ? 0 : (env_order >= 0 ? env_order : 0);
     prm.in = in;
     prm.in_ws = in_ws;
     prm.C = pb.C;
