@@ -169,6 +169,15 @@ def bench_ours(args):
     props = torch.cuda.get_device_properties(dev)
     l2 = getattr(props, "L2_cache_size", 126 << 20)
     flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    flush_rd = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    flush_out = torch.empty(1, dtype=torch.float32, device=dev)
+
+    def l2_flush():
+        # write a buffer > L2 (evicts every line), then read another one so
+        # the dirty lines of the first pass are written back here, outside
+        # the timed events: each step starts with a cold, clean L2
+        flush.zero_()
+        torch.sum(flush_rd, dim=0, out=flush_out)
     stream = torch.cuda.current_stream(dev)
     nk = plan.num_kernels
 
@@ -179,7 +188,7 @@ def bench_ours(args):
     # warm-up: W steps, then the same step until >= 1 s has passed so that the
     # clocks settle under this load (the clock sampler runs from here on)
     for _ in range(args.warmup):
-        flush.zero_()
+        l2_flush()
         plan.run(d_in, d_ker, d_out, ws)
     torch.cuda.synchronize(dev)
     clocks = ClockSampler(local)
@@ -187,20 +196,41 @@ def bench_ours(args):
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < args.soak:
         for _ in range(20):
-            flush.zero_()
+            l2_flush()
             plan.run(d_in, d_ker, d_out, ws)
         torch.cuda.synchronize(dev)
 
-    # (1) headline: K steps, each conv_run bracketed by its own event pair
-    #     (kernels back to back, so the main kernel's programmatic-dependent
-    #     launch overlaps the repack tail as in production)
+    # (1) headline: K steps, each conv_run bracketed by its own event pair.
+    #     conv_run is replayed from a CUDA graph (its kernels back to back on
+    #     the device, the main kernel's programmatic dependent launch kept),
+    #     so host launch latency never shows up in the device timing.
+    graph = None
+    if not args.no_graph:
+        try:
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                plan.run(d_in, d_ker, d_out, ws)
+            cap.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cap):
+                plan.run(d_in, d_ker, d_out, ws, stream=cap)
+            torch.cuda.synchronize(dev)
+            graph.replay()
+            torch.cuda.synchronize(dev)
+        except Exception as e:  # pragma: no cover - fall back to stream launches
+            print(f"warning: CUDA graph capture failed ({e}); timing stream launches", file=sys.stderr)
+            graph = None
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize(dev)
     for i in range(args.steps):
-        flush.zero_()                                   # L2 flush, outside the event pair
+        l2_flush()                                      # L2 flush, outside the event pair
         step_ev[i][0].record(stream)
-        plan.run(d_in, d_ker, d_out, ws)
+        if graph is not None:
+            graph.replay()
+        else:
+            plan.run(d_in, d_ker, d_out, ws)
         step_ev[i][1].record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -213,7 +243,7 @@ def bench_ours(args):
     barrier()
     torch.cuda.synchronize(dev)
     for i in range(args.steps):
-        flush.zero_()
+        l2_flush()
         plan.run_events(d_in, d_ker, d_out, ws, evs[i])
     torch.cuda.synchronize(dev)
     barrier()
@@ -231,7 +261,7 @@ def bench_ours(args):
     e2e_ms = []
     barrier()
     for _ in range(args.steps):
-        flush.zero_()
+        l2_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         plan.run_host(inp_h, ker_h, out_h, dbuf)
@@ -295,10 +325,12 @@ def bench_ours(args):
                             f"(stride 1, no pad, fp32 NCHW/KCRS){' per rank' if world > 1 else ''}",
                 "path": plan.path,
                 "tile": desc["tile"],
-                "l2": "flushed before every timed step (write of 2x L2), outside the event pair",
+                "l2": "flushed before every timed step, outside the event pair: write of a 2x-L2 buffer, then a read "
+                      "of another 2x-L2 buffer (dirty lines written back before the step: cold, clean L2)",
                 "clocks_window": "NVML samples every ~1 ms over the >= 1 s warm-up soak and both timed passes",
                 "parallelism": f"n-shard x{world}" if world > 1 else "single GPU",
                 "kernels_per_step": nk,
+                "launch": "cuda_graph replay of conv_run" if graph is not None else "stream launches",
             },
             "roofline": {
                 "bound": bound,
@@ -406,6 +438,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of extra warm-up steps before timing")
+    ap.add_argument("--no-graph", action="store_true", help="time plain stream launches instead of a CUDA graph replay")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

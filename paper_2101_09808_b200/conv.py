@@ -133,6 +133,7 @@ class ConvPlan:
                 status = CONV_ERR_INFEASIBLE
             raise ConvError(status, msg)
         self._h = ctypes.c_void_p(h)
+        self._shapes_cache = tuple(self._shapes_sizes())
         if path != "auto":
             self.set_path(path)
         if tile:
@@ -179,14 +180,16 @@ class ConvPlan:
         N, K, C, H, W, R, S = self.shape
         return (N, C, H + R - 1, W + S - 1), (K, C, R, S), (N, K, H, W)
 
-    def _check_tensors(self, inp, ker, out):
+    def _shapes_sizes(self):
         import torch
-        si, sk, so = self._shapes()
+        return [torch.Size(s) for s in self._shapes()]
+
+    def _check_tensors(self, inp, ker, out):
+        si, sk, so = self._shapes_cache
         for t, s, name in ((inp, si, "in"), (ker, sk, "ker"), (out, so, "out")):
-            if not isinstance(t, torch.Tensor) or not t.is_cuda:
-                raise ValueError(f"{name} must be a CUDA tensor")
-            if t.dtype != torch.float32 or tuple(t.shape) != s or not t.is_contiguous():
-                raise ValueError(f"{name} must be contiguous float32 of shape {s}, got {t.dtype} {tuple(t.shape)}")
+            if not (t.is_cuda and t.dtype is _f32() and t.shape == s and t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous float32 CUDA tensor of shape {tuple(s)}, "
+                                 f"got {t.dtype} {tuple(t.shape)} on {t.device}")
 
     def new_workspace(self, device=None):
         import torch
@@ -237,6 +240,11 @@ class ConvPlan:
         _check(self._lib.conv_run_host(self._h, in_host.data_ptr(), ker_host.data_ptr(),
                                        out_host.data_ptr(), device_buffer.data_ptr(),
                                        _stream_handle(stream)))
+
+
+def _f32():
+    import torch
+    return torch.float32
 
 
 _plan_cache = {}

@@ -14,10 +14,12 @@
 // (roofline: bytes / HBM bandwidth).
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace conv {
 
@@ -25,6 +27,13 @@ __device__ __forceinline__ float to_tf32_rna(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
+}
+
+// RNE pack of two fp32 into bf16x2 (lo in the low half)
+__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
+    uint32_t v;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(v) : "f"(hi), "f"(lo));
+    return v;
 }
 
 template <bool BF16>
@@ -57,6 +66,9 @@ struct RepackGeom {
     int64_t P;                       // K2: pixels per image
     int ptiles, ctiles;              // K2 tile grid per image
     int n_ker;                       // number of K1 CTAs
+    int N;                           // images
+    int64_t n_tiles;                 // K2 tiles (TMA variant)
+    int pdl_from;                    // first block that triggers the dependent launch
 };
 
 template <bool BF16>
@@ -65,10 +77,12 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
                                                   typename Elem<BF16>::T* __restrict__ ker_ws, const RepackGeom g) {
     extern __shared__ float sm[];
     const int tid = threadIdx.x;
-    // let the dependent main kernel (launched with programmatic stream
-    // serialization) start its prologue as SMs free up; it waits for this
-    // grid's completion (griddepcontrol.wait) before reading the workspace
-    asm volatile("griddepcontrol.launch_dependents;");
+    // Programmatic dependent launch: the main kernel (one 200-KB CTA per SM)
+    // may start its prologue once every CTA of this grid has triggered or
+    // exited.  Only the last wave triggers, so the main kernel does not take
+    // SMs away from the bulk of the repack; it waits for this grid's
+    // completion (griddepcontrol.wait) before reading the workspace.
+    if ((int)blockIdx.x >= g.pdl_from) asm volatile("griddepcontrol.launch_dependents;");
     if ((int)blockIdx.x < g.n_ker) {
         // ---- K1 ----
         const int64_t k = blockIdx.x / g.ker_chunks;
@@ -151,6 +165,122 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
     }
 }
 
+// K2 with TMA (used when the NCHW pixel stride P*4 is a multiple of 16 B):
+// persistent CTAs of 128 threads loop over (image, 64-channel, 64-pixel)
+// tiles.  A 3-D TMA load brings the [64 ch][64 px] fp32 box of NCHW into
+// shared memory (channels >= C are zero-filled by the TMA: that is the Cp
+// padding); the threads convert it into the 128B-swizzled [64 px][64 ch] box
+// (bf16: one 128-B row per pixel; tf32: two 32-channel boxes) and one thread
+// TMA-stores it into the NHWC workspace.  Loads and stores are double-
+// buffered, so each SM keeps two 16-KB loads in flight with few instructions.
+// CTAs [0, n_ker) run K1 exactly as in repack_all.
+template <bool BF16>
+__global__ void __launch_bounds__(128) repack_tma(const float* __restrict__ ker,
+                                                  typename Elem<BF16>::T* __restrict__ ker_ws,
+                                                  const __grid_constant__ CUtensorMap src_map,
+                                                  const __grid_constant__ CUtensorMap dst_map, const RepackGeom g) {
+    using namespace sm100;
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    const int tid = threadIdx.x;
+    if ((int)blockIdx.x >= g.pdl_from) asm volatile("griddepcontrol.launch_dependents;");
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    if ((int)blockIdx.x < g.n_ker) {
+        float* filt = reinterpret_cast<float*>(sm);
+        const int64_t k = blockIdx.x / g.ker_chunks;
+        const int c0 = (blockIdx.x % g.ker_chunks) * g.cc;
+        const int c1 = min(c0 + g.cc, g.Cp);
+        const int cload = max(0, min(c1, g.C) - c0);
+        const float* src = ker + (k * g.C + c0) * g.RS;
+        for (int i = tid; i < cload * g.RS; i += 128) filt[i] = __ldg(src + i);
+        __syncthreads();
+        typename Elem<BF16>::T* dst = ker_ws + k * (int64_t)g.RS * g.Cp;
+        const int width = c1 - c0;
+        for (int i = tid; i < g.RS * width; i += 128) {
+            const int rs = i / width;
+            const int c = c0 + (i - rs * width);
+            dst[(int64_t)rs * g.Cp + c] = Elem<BF16>::cvt(c < g.C ? filt[(c - c0) * g.RS + rs] : 0.0f);
+        }
+        return;
+    }
+    float* in_buf[2] = {reinterpret_cast<float*>(sm), reinterpret_cast<float*>(sm + 16384)};
+    uint8_t* out_buf[2] = {sm + 32768, sm + 49152};
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + 65536);
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int64_t first = blockIdx.x - g.n_ker;
+    const int64_t stride = gridDim.x - g.n_ker;
+    auto coords = [&](int64_t tile, int& px, int& cx, int& n) {
+        px = (int)(tile % g.ptiles) * 64;
+        const int64_t t2 = tile / g.ptiles;
+        cx = (int)(t2 % g.ctiles) * 64;
+        n = (int)(t2 / g.ctiles);
+    };
+    if (tid == 0 && first < g.n_tiles) {
+        int px, cx, n;
+        coords(first, px, cx, n);
+        mbar_arrive_expect_tx(&full[0], 16384);
+        tma_load_3d(in_buf[0], &src_map, &full[0], px, cx, n);
+    }
+    int i = 0;
+    for (int64_t tile = first; tile < g.n_tiles; tile += stride, ++i) {
+        const int b = i & 1;
+        const int64_t next = tile + stride;
+        if (tid == 0 && next < g.n_tiles) {       // prefetch into the other buffer (released at barrier B)
+            int px, cx, n;
+            coords(next, px, cx, n);
+            mbar_arrive_expect_tx(&full[b ^ 1], 16384);
+            tma_load_3d(in_buf[b ^ 1], &src_map, &full[b ^ 1], px, cx, n);
+        }
+        mbar_wait(&full[b], (i >> 1) & 1);
+        if (tid == 0) bulk_wait_read<1>();        // the store of tile i-2 has read out_buf[b]
+        __syncthreads();                          // (A)
+        const int p = tid & 63, half = tid >> 6;  // pixel, channel half
+        const float* src = in_buf[b] + (half * 32) * 64 + p;
+        if (BF16) {
+            // row p = 64 channels x 2 B = 128 B; 16-B chunk j holds channels 8j..8j+7
+            uint8_t* row = out_buf[b] + p * 128;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = half * 4 + q;
+                uint4 o;
+                const float* s = src + (q * 8) * 64;
+                o.x = pack2_bf16(s[0], s[64]);
+                o.y = pack2_bf16(s[128], s[192]);
+                o.z = pack2_bf16(s[256], s[320]);
+                o.w = pack2_bf16(s[384], s[448]);
+                *reinterpret_cast<uint4*>(row + ((j ^ (p & 7)) << 4)) = o;
+            }
+        } else {
+            // box `half` (32 channels x 4 B = 128 B per pixel row); chunk j = 4 channels
+            uint8_t* row = out_buf[b] + half * 8192 + p * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float* s = src + (j * 4) * 64;
+                float4 o;
+                o.x = to_tf32_rna(s[0]);
+                o.y = to_tf32_rna(s[64]);
+                o.z = to_tf32_rna(s[128]);
+                o.w = to_tf32_rna(s[192]);
+                *reinterpret_cast<float4*>(row + ((j ^ (p & 7)) << 4)) = o;
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();                          // (B) out_buf[b] written, in_buf[b] consumed
+        if (tid == 0) {
+            int px, cx, n;
+            coords(tile, px, cx, n);
+            tma_store_3d(&dst_map, out_buf[b], cx, px, n);
+            if (!BF16) tma_store_3d(&dst_map, out_buf[b] + 8192, cx + 32, px, n);
+            bulk_commit();
+        }
+    }
+    if (tid == 0) bulk_wait<0>();
+}
+
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
                           void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in) {
     RepackGeom g;
@@ -164,9 +294,70 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
     g.P = pb.Hin() * pb.Win();
     g.ptiles = (int)((g.P + 63) / 64);
     g.ctiles = (Cp + 63) / 64;
+    g.N = pb.N;
+    g.n_tiles = (int64_t)g.ptiles * g.ctiles * pb.N;
+    // The TMA variant measured slower than repack_all in r01 (27.5 vs 23.7 us,
+    // batched bf16); kept for study behind CONV_TMA_REPACK=1.
+    static const bool want_tma = getenv("CONV_TMA_REPACK") != nullptr;
+    const bool use_tma = with_in && want_tma && (g.P % 4 == 0) && g.cc * g.RS * 4 <= 32768 &&
+                         g.n_tiles < (1ll << 31) && g.P < (1ll << 31);
+    if (use_tma) {
+        CUtensorMap src_map, dst_map;
+        {
+            cuuint64_t dims[3] = {(cuuint64_t)g.P, (cuuint64_t)pb.C, (cuuint64_t)pb.N};
+            cuuint64_t strides[2] = {(cuuint64_t)g.P * 4, (cuuint64_t)g.P * 4 * pb.C};
+            cuuint32_t box[3] = {64, 64, 1};
+            cuuint32_t es[3] = {1, 1, 1};
+            if (g_encode_tiled(&src_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return cudaErrorInvalidValue;
+        }
+        {
+            const int es_b = bf16 ? 2 : 4;
+            // 3-D {Cp, P, N}: boxes that run past the image's last pixel are
+            // clipped at the image, never spill into the next one
+            cuuint64_t dims[3] = {(cuuint64_t)Cp, (cuuint64_t)g.P, (cuuint64_t)pb.N};
+            cuuint64_t strides[2] = {(cuuint64_t)Cp * es_b, (cuuint64_t)Cp * es_b * g.P};
+            cuuint32_t box[3] = {(cuuint32_t)(bf16 ? 64 : 32), 64, 1};
+            cuuint32_t es[3] = {1, 1, 1};
+            if (g_encode_tiled(&dst_map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                               in_ws, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return cudaErrorInvalidValue;
+        }
+        int sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t persist = std::min<int64_t>(g.n_tiles, (int64_t)sms * 3);
+        const size_t smem = 1024 + 65536 + 64;
+        static bool attr_set[2] = {false, false};
+        if (!attr_set[bf16]) {
+            cudaError_t e = bf16 ? cudaFuncSetAttribute(repack_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                                 : cudaFuncSetAttribute(repack_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            attr_set[bf16] = true;
+        }
+        if (ev) cudaEventRecord(ev[0], st);
+        const unsigned grid = (unsigned)(g.n_ker + persist);
+        g.pdl_from = (int)std::max<int64_t>(0, (int64_t)grid - (int64_t)sms * 3);
+        if (bf16)
+            repack_tma<true><<<grid, 128, smem, st>>>(ker, (__nv_bfloat16*)ker_ws, src_map, dst_map, g);
+        else
+            repack_tma<false><<<grid, 128, smem, st>>>(ker, (float*)ker_ws, src_map, dst_map, g);
+        if (ev) cudaEventRecord(ev[1], st);
+        return cudaGetLastError();
+    }
     const int64_t n_in = with_in ? (int64_t)g.ptiles * g.ctiles * pb.N : 0;   // fused: Ker only
     const int64_t grid = g.n_ker + n_in;
     if (grid >= (1ll << 31)) return cudaErrorInvalidValue;
+    {
+        int sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g.pdl_from = (int)std::max<int64_t>(0, grid - (int64_t)sms * 8);   // ~ the last resident wave
+    }
     const size_t smem = std::max<size_t>(64 * 65 * sizeof(float), (size_t)g.cc * g.RS * sizeof(float));
     if (smem > 48 * 1024) {   // very large R*S: one channel per K1 CTA still needs > 48 KB
         cudaError_t e = bf16 ? cudaFuncSetAttribute(repack_all<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)

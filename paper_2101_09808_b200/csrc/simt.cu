@@ -27,6 +27,24 @@
 
 namespace conv {
 
+// Launch with programmatic stream serialization: the kernel's prologue
+// overlaps the tail of the Ker packing grid; it calls griddepcontrol.wait
+// before reading the packed kernel.
+template <typename Kern, typename... Args>
+static cudaError_t launch_pdl(Kern kfn, dim3 grid, int threads, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kfn, args...);
+}
+
 struct SimtParams {
     int N, K, C, H, W, R, S;
     int Hin, Win, HW, RS;
@@ -55,6 +73,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Packing kernel: Ker KCRS -> [ceil(K/bko)][C][R][S][bko], k >= K zero.
 __global__ void __launch_bounds__(256) pack_ker_simt(const float* __restrict__ ker, float* __restrict__ out,
                                                      int K, int C, int RS, int bko, int64_t total) {
+    asm volatile("griddepcontrol.launch_dependents;");   // small grid: one wave
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int kk = (int)(i % bko);
@@ -147,6 +166,7 @@ __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict_
             cp_async16(ker_s + e, e < len_ok ? g + e : kerp, e < len_ok);
     };
 
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // packed Ker written by the previous grid
     load_stage(0, 0);
     cp_async_commit();
     for (int chunk = 0; chunk < p.nchunks; ++chunk) {
@@ -325,6 +345,7 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
 
     constexpr int WIN = TW + KS - 1;
     constexpr int WIN4 = (WIN + 3) / 4 * 4;
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // packed Ker written by the previous grid
     load_stage(0, 0);
     cp_async_commit();
     for (int chunk = 0; chunk < p.nchunks; ++chunk) {
@@ -422,8 +443,7 @@ static cudaError_t launch_simt2_t(const float* in, const float* kerp, float* out
         if (e != cudaSuccess) return e;
         smem_set.store(optin, std::memory_order_release);
     }
-    kfn<<<grid, threads, smem, st>>>(in, kerp, out, p);
-    return cudaGetLastError();
+    return launch_pdl(kfn, grid, threads, smem, st, in, kerp, out, p);
 }
 
 static cudaError_t dispatch_simt2(const SimtTile& t, int R, int S, const float* in, const float* kerp, float* out,
@@ -452,8 +472,7 @@ static cudaError_t launch_simt_t(const float* in, const float* kerp, float* out,
         if (e != cudaSuccess) return e;
         smem_set.store(optin, std::memory_order_release);
     }
-    kfn<<<grid, threads, smem, st>>>(in, kerp, out, p);
-    return cudaGetLastError();
+    return launch_pdl(kfn, grid, threads, smem, st, in, kerp, out, p);
 }
 
 #define SIMT_CASE(TK_, TW_) \
