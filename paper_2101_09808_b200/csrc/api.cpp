@@ -60,6 +60,19 @@ struct conv_plan {
     int force_bn = 0, force_stages = 0, force_cg = 0, force_kbs = 0, force_fuse = -1;
     SimtTile force_simt;
     unsigned force_simt_mask = 0;
+    // conv_run_host pipeline (created on first use, guarded by host_mu)
+    std::mutex host_mu;
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    static constexpr int kMaxChunks = 8;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {};
+    ~conv_plan() {
+        for (cudaStream_t s : {h2d, comp, d2h}) if (s) cudaStreamDestroy(s);
+        for (cudaEvent_t e : {ev_start, ev_end}) if (e) cudaEventDestroy(e);
+        for (int i = 0; i < kMaxChunks; ++i) {
+            if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
+            if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
+        }
+    }
 };
 
 static thread_local std::string g_err;
@@ -335,6 +348,30 @@ static conv_status check_ptr(const void* ptr, const char* name, size_t align) {
     return CONV_OK;
 }
 
+// Launch the plan's kernels for images [n0, n0 + sub.N) of the plan's problem
+// (sub = the plan's problem with N replaced).  The tensor paths' NHWC
+// workspace slice of those images and the shared Ker workspace are addressed
+// inside the plan's full workspace, so chunks never overlap.
+static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0, const float* in, const float* ker,
+                                  float* out, void* ws, cudaStream_t st, cudaEvent_t* evp) {
+    std::string err;
+    cudaError_t e;
+    if (p->path == CONV_PATH_FP32_SIMT) {
+        e = simt_run(sub, p->simt, in, ker, out, ws, st, evp, err);
+    } else {
+        uint8_t* wsb = static_cast<uint8_t*>(ws);
+        const size_t per_img = p->tcl.in_ws_bytes / (size_t)p->pb.N;
+        void* in_ws = wsb + per_img * (size_t)n0;
+        void* ker_ws = wsb + align256(p->tcl.in_ws_bytes);
+        e = tc_run(sub, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, in_ws, ker_ws, st, p->dev.sms, evp, err);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CONV_ERR_CUDA, "%s%s%s", err.c_str(), err.empty() ? "" : ": ", cudaGetErrorString(e));
+    }
+    return CONV_OK;
+}
+
 static conv_status run_impl(const conv_plan* p, const float* in, const float* ker, float* out, void* ws,
                             void* stream, void* const* events, int n_events) {
     if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
@@ -373,17 +410,7 @@ static conv_status run_impl(const conv_plan* p, const float* in, const float* ke
         }
         evp = ev;
     }
-    std::string err;
-    cudaError_t e;
-    if (p->path == CONV_PATH_FP32_SIMT)
-        e = simt_run(p->pb, p->simt, in, ker, out, ws, st, evp, err);
-    else
-        e = tc_run(p->pb, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, ws, st, p->dev.sms, evp, err);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(CONV_ERR_CUDA, "%s%s%s", err.c_str(), err.empty() ? "" : ": ", cudaGetErrorString(e));
-    }
-    return CONV_OK;
+    return launch_kernels(p, p->pb, 0, in, ker, out, ws, st, evp);
 }
 
 extern "C" conv_status conv_run(const conv_plan* p, const float* in, const float* ker, float* out, void* ws,
@@ -403,25 +430,68 @@ extern "C" size_t conv_plan_host_run_bytes(const conv_plan* p) {
            ws_bytes(p);
 }
 
-extern "C" conv_status conv_run_host(const conv_plan* p, const float* in_host, const float* ker_host,
+extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, const float* ker_host,
                                      float* out_host, void* dbuf, void* stream) {
-    if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (!cp) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
+    conv_plan* p = const_cast<conv_plan*>(cp);   // only the pipeline resources are mutated
     if (!in_host || !ker_host || !out_host) return fail(CONV_ERR_INVALID_ARGUMENT, "host pointer is NULL");
     conv_status s;
     if ((s = check_ptr(dbuf, "device_buffer", 256)) != CONV_OK) return s;
-    const size_t bi = 4 * p->pb.in_elems(), bk = 4 * p->pb.ker_elems(), bo = 4 * p->pb.out_elems();
+    if (p->dev.ordinal < 0) return fail(CONV_ERR_UNSUPPORTED_DEVICE, "offline plan: not bound to a device");
+    const Problem& pb = p->pb;
+    const size_t bi = 4 * pb.in_elems(), bk = 4 * pb.ker_elems(), bo = 4 * pb.out_elems();
     char* d = static_cast<char*>(dbuf);
     float* din = reinterpret_cast<float*>(d);
     float* dker = reinterpret_cast<float*>(d + align256(bi));
     float* dout = reinterpret_cast<float*>(d + align256(bi) + align256(bk));
     void* dws = d + align256(bi) + align256(bk) + align256(bo);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaMemcpyAsync(din, in_host, bi, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dker, ker_host, bk, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) { cudaGetLastError(); return fail(CONV_ERR_CUDA, "H2D copy failed: %s", cudaGetErrorString(e)); }
-    s = run_impl(p, din, dker, dout, dws, stream, nullptr, 0);
-    if (s != CONV_OK) return s;
-    e = cudaMemcpyAsync(out_host, dout, bo, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) { cudaGetLastError(); return fail(CONV_ERR_CUDA, "D2H copy failed: %s", cudaGetErrorString(e)); }
+    // Pipeline over image chunks on three internal streams: the upload of
+    // chunk j+1, the convolution of chunk j and the download of chunk j-1
+    // overlap (PCIe is full duplex).  One chunk for small inputs.
+    const int nch = (bi >= (8u << 20)) ? std::min(pb.N, (int)conv_plan::kMaxChunks) : 1;
+    std::lock_guard<std::mutex> g(p->host_mu);
+    cudaError_t e = cudaSuccess;
+    auto ok = [&](cudaError_t r) { if (r != cudaSuccess && e == cudaSuccess) e = r; };
+    if (!p->h2d) {
+        ok(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
+        ok(cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking));
+        ok(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+        ok(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
+        ok(cudaEventCreateWithFlags(&p->ev_end, cudaEventDisableTiming));
+        for (int i = 0; i < conv_plan::kMaxChunks; ++i) {
+            ok(cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming));
+            ok(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming));
+        }
+        if (e != cudaSuccess) { cudaGetLastError(); return fail(CONV_ERR_CUDA, "pipeline setup failed: %s", cudaGetErrorString(e)); }
+    }
+    // everything after the caller's prior work on `stream`
+    ok(cudaEventRecord(p->ev_start, st));
+    ok(cudaStreamWaitEvent(p->h2d, p->ev_start, 0));
+    ok(cudaStreamWaitEvent(p->comp, p->ev_start, 0));
+    ok(cudaStreamWaitEvent(p->d2h, p->ev_start, 0));
+    ok(cudaMemcpyAsync(dker, ker_host, bk, cudaMemcpyHostToDevice, p->h2d));
+    const int64_t img_in = (int64_t)pb.C * pb.Hin() * pb.Win(), img_out = (int64_t)pb.K * pb.H * pb.W;
+    int n0 = 0;
+    for (int j = 0; j < nch && e == cudaSuccess; ++j) {
+        const int n1 = (int)((int64_t)pb.N * (j + 1) / nch);
+        Problem sub = pb;
+        sub.N = n1 - n0;
+        ok(cudaMemcpyAsync(din + n0 * img_in, in_host + n0 * img_in, 4 * sub.N * img_in, cudaMemcpyHostToDevice, p->h2d));
+        ok(cudaEventRecord(p->ev_h2d[j], p->h2d));
+        ok(cudaStreamWaitEvent(p->comp, p->ev_h2d[j], 0));
+        if (e != cudaSuccess) break;
+        s = launch_kernels(p, sub, n0, din + n0 * img_in, dker, dout + n0 * img_out, dws, p->comp, nullptr);
+        if (s != CONV_OK) return s;
+        ok(cudaEventRecord(p->ev_comp[j], p->comp));
+        ok(cudaStreamWaitEvent(p->d2h, p->ev_comp[j], 0));
+        ok(cudaMemcpyAsync(out_host + n0 * img_out, dout + n0 * img_out, 4 * sub.N * img_out, cudaMemcpyDeviceToHost, p->d2h));
+        n0 = n1;
+    }
+    // the caller's stream continues after the last download (and everything
+    // else, which the download depends on)
+    ok(cudaEventRecord(p->ev_end, p->d2h));
+    ok(cudaStreamWaitEvent(st, p->ev_end, 0));
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(CONV_ERR_CUDA, "host pipeline failed: %s", cudaGetErrorString(e)); }
     return CONV_OK;
 }

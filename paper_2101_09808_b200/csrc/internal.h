@@ -65,7 +65,7 @@ size_t tc_smem_bytes(const TcLayout& L, const TcTile& t);
 // Launch the repack (K1 + K2, one launch) and K3 (tcgen05 implicit GEMM).
 // events (optional, n_events == 3) are recorded around each kernel.
 cudaError_t tc_run(const Problem& p, const TcLayout& L, const TcTile& t, bool bf16,
-                   const float* in, const float* ker, float* out, void* ws,
+                   const float* in, const float* ker, float* out, void* in_ws, void* ker_ws,
                    cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err);
 
 // ---- FP32 SIMT path (K4) ----------------------------------------------------

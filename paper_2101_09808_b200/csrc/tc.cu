@@ -503,7 +503,6 @@ size_t tc_smem_bytes(const TcLayout& L, const TcTile& t) {
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
                           void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in);
 
-static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 template <int BN, bool BF16, int CG, int KSTEPS>
 static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& prm,
@@ -562,16 +561,14 @@ static cudaError_t launch_tc_sw(int sw, int bn, const CUtensorMap& ta, const CUt
 }
 
 cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool bf16,
-                   const float* in, const float* ker, float* out, void* ws,
+                   const float* in, const float* ker, float* out, void* in_ws, void* ker_ws,
                    cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err) {
-    uint8_t* wsb = static_cast<uint8_t*>(ws);
-    void* in_ws = wsb;
-    void* ker_ws = wsb + align_up(L.in_ws_bytes, 256);
+    const void* ws = in_ws;   // tensor-map cache key
 
     // Tensor maps depend on the workspace address, known only here; they are
     // encoded on first use and cached per (workspace, problem, tile).
     struct Key {
-        const void* ws; Problem pb; int bn; int cg; int kbs; int bf16; int dev;  // (fuse does not change the maps)
+        const void* ws; const void* kws; Problem pb; int bn; int cg; int kbs; int bf16; int dev;  // (fuse does not change the maps)
     };
     struct Entry { Key k; CUtensorMap ta, tb; };
     static std::mutex mu;
@@ -579,9 +576,9 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     static int n_cached = 0, next_slot = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    const Key key{ws, pb, t.bn, t.cg, t.kbs, bf16 ? 1 : 0, dev};
+    const Key key{ws, ker_ws, pb, t.bn, t.cg, t.kbs, bf16 ? 1 : 0, dev};
     auto same = [&](const Key& a) {
-        return a.ws == key.ws && memcmp(&a.pb, &key.pb, sizeof(Problem)) == 0 && a.bn == key.bn && a.cg == key.cg && a.kbs == key.kbs &&
+        return a.ws == key.ws && a.kws == key.kws && memcmp(&a.pb, &key.pb, sizeof(Problem)) == 0 && a.bn == key.bn && a.cg == key.cg && a.kbs == key.kbs &&
                a.bf16 == key.bf16 && a.dev == key.dev;
     };
     CUtensorMap ta, tb;
