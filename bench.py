@@ -162,7 +162,7 @@ def bench_ours(args):
         inp, ker = make_inputs(sh, seed=rank)
     inp_h, ker_h = inp.pin_memory(), ker.pin_memory()
     d_in, d_ker = inp_h.to(dev), ker_h.to(dev)
-    plan = conv.ConvPlan(*sh.as_tuple(), path=args.path)
+    plan = conv.ConvPlan(*sh.as_tuple(), path=args.path, tile=args.tile)
     desc = plan.describe()
     d_out = plan.new_output(dev)
     ws = plan.new_workspace(dev)
@@ -170,7 +170,7 @@ def bench_ours(args):
     l2 = getattr(props, "L2_cache_size", 126 << 20)
     flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
     flush_rd = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
-    flush_out = torch.empty(1, dtype=torch.float32, device=dev)
+    flush_out = torch.empty((), dtype=torch.float32, device=dev)
 
     def l2_flush():
         # write a buffer > L2 (evicts every line), then read another one so
@@ -439,6 +439,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of extra warm-up steps before timing")
     ap.add_argument("--no-graph", action="store_true", help="time plain stream launches instead of a CUDA graph replay")
+    ap.add_argument("--tile", default=None, help="force a tile (conv_plan_set_tile spec, e.g. 'fuse=0,bn=128'); experiments")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -94,7 +94,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 static size_t ws_bytes(const conv_plan* p) {
     if (p->path == CONV_PATH_FP32_SIMT) return align256(simt_ws_bytes(p->pb, p->simt));
-    return align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes);
+    return align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes) + (p->tc.fuse ? align256(p->tcl.flag_bytes) : 0);
 }
 
 // Re-run the selector for the requested path (Alg. 1:
@@ -314,8 +314,9 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
                  32 * p->simt.kg * p->simt.pw);
     } else {
-        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"fuse\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
-                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.fuse, p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
+        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"fuse\":%d,\"tnb\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
+                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
+                 p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
     }
     tile = t;
     char out[2048];
@@ -363,7 +364,9 @@ static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0
         const size_t per_img = p->tcl.in_ws_bytes / (size_t)p->pb.N;
         void* in_ws = wsb + per_img * (size_t)n0;
         void* ker_ws = wsb + align256(p->tcl.in_ws_bytes);
-        e = tc_run(sub, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, in_ws, ker_ws, st, p->dev.sms, evp, err);
+        void* flag_ws = p->tc.fuse ? wsb + align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes) : nullptr;
+        e = tc_run(sub, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, in_ws, ker_ws, flag_ws, st, p->dev.sms,
+                   evp, err);
     }
     if (e != cudaSuccess) {
         cudaGetLastError();

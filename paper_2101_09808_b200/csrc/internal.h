@@ -47,6 +47,8 @@ struct TcTile {
     int cg = 1;          // CTAs per MMA: 1 (M = 128) or 2 (CTA pair, M = 256)
     int kbs = 1;         // k-blocks (one TMA box of A and of B each) per pipeline stage
     int fuse = 0;        // 1: the NCHW->NHWC In transform runs inside the main kernel
+                         //    (cooperative chunk transform, warps 0-3 of every CTA)
+    int tnb = 2;         // fuse: input staging buffers of the transform (2..4)
 };
 
 struct TcLayout {        // derived from Problem + element size
@@ -57,15 +59,24 @@ struct TcLayout {        // derived from Problem + element size
     int n_cblk;          // Cp / bkc
     size_t in_ws_bytes;  // NHWC workspace
     size_t ker_ws_bytes; // KRSC workspace
+    // cooperative in-kernel transform (fuse = 1): chunks of 64 pixels x cc channels
+    int cc;              // channels per chunk: min(32, bkc)
+    int nch;             // Cp / cc
+    int hh;              // chunks per k-block: bkc / cc
+    int64_t npch;        // 64-pixel chunks per input plane
+    bool coop_ok;        // TMA-legal NCHW plane (Hin*Win*4 a multiple of 16 B)
+    size_t flag_bytes;   // 128 B reserved + one int ready flag per chunk
 };
+size_t tc_transform_smem_bytes(const TcLayout& L, int tnb);
 
 TcLayout tc_layout(const Problem& p, bool bf16);
 size_t tc_smem_bytes(const TcLayout& L, const TcTile& t);
 
 // Launch the repack (K1 + K2, one launch) and K3 (tcgen05 implicit GEMM).
 // events (optional, n_events == 3) are recorded around each kernel.
+// flag_ws: L.flag_bytes of workspace for the fused transform (unused if !t.fuse).
 cudaError_t tc_run(const Problem& p, const TcLayout& L, const TcTile& t, bool bf16,
-                   const float* in, const float* ker, float* out, void* in_ws, void* ker_ws,
+                   const float* in, const float* ker, float* out, void* in_ws, void* ker_ws, void* flag_ws,
                    cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err);
 
 // ---- FP32 SIMT path (K4) ----------------------------------------------------

@@ -169,7 +169,7 @@ static const double kClockHz = 1.84e9;   // SM clock measured under tcgen05 load
 // an SM; every pipeline stage adds ~150 cycles of barrier / commit bubble.
 static const double kStageBubbleClk = 150.0;
 static const double kEpiStoreBW = 5.0e12;  // bytes/s the whole chip's epilogues drain at
-static const double kTransformBW = 30.0e9; // bytes/s one CTA's 4 transform warps move (read+write)
+static const double kTransformLatUs = 2.0; // fused transform: one chunk's load -> convert -> store -> flag round trip
 
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t) {
     ModelResult r;
@@ -212,29 +212,35 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     double t_rep = repack / (0.8 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
     double t_main_f = t_main;
     if (t.fuse) {
-        // In transform inside the main kernel: 4 warps per CTA transform the
-        // input rows of each tile (about (128/W + R - 1 + 1) rows x Win x Cp)
-        // at kTransformBW per CTA, overlapped with the tile's MMAs; the first
-        // tile's transform is exposed.  The repack launch keeps only Ker.
-        const double rows = std::min<double>(128.0 / pb.W + pb.R, (double)pb.Hin() * pb.N);
-        const double bytes_tile = rows * pb.Win() * L.Cp * (4.0 + L.elem);
-        const double t_tr_tile = bytes_tile / kTransformBW * 1e6;
-        const double t_tile = t_pipe_us / std::max(1.0, tiles_per_unit);
-        t_main_f = std::max(t_main, tiles_per_unit * std::max(t_tile, t_tr_tile) + t_tail_us + kLaunchUs) + t_tr_tile;
+        // Cooperative In transform inside the main kernel: every CTA's 4
+        // transform warps keep tnb chunk loads of cc x 64 fp32 in flight
+        // (Little's law with ~kTransformLatUs per chunk round trip), capped at
+        // the HBM rate; it overlaps the MMAs, and the first tiles wait about
+        // one chunk round trip for their first channel block.  The separate
+        // launch keeps only the Ker repack (and clears the chunk flags).
+        const double in_rd = 4.0 * pb.in_elems();
+        const double rate = std::min(0.8 * dev.bw_hbm, (double)dev.sms * t.tnb * L.cc * 256.0 / (kTransformLatUs * 1e-6));
+        const double t_tr = in_rd / rate * 1e6;
+        const double hbm_f = (in_rd + (double)L.in_ws_bytes + (double)L.ker_ws_bytes + 4.0 * pb.out_elems()) / dev.bw_hbm * 1e6;
+        t_main_f = std::max({t_main - kLaunchUs - t_tail_us, t_tr, hbm_f}) + t_tail_us + kLaunchUs + kTransformLatUs;
         t_rep = (4.0 * pb.ker_elems() + (double)L.ker_ws_bytes) / (0.5 * dev.bw_hbm) * 1e6 + kLaunchUs;
+        r.dv_hbm = in_rd + (double)L.in_ws_bytes + 4.0 * pb.ker_elems() + 2.0 * (double)L.ker_ws_bytes + 4.0 * pb.out_elems();
+        r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
     }
     r.model_us = t_main_f + t_rep;
     r.smem = tc_smem_bytes(L, t);
     return r;
 }
 
-static int tc_max_stages(const Device& dev, const TcLayout& L, int bn, int cg, int kbs) {
+static int tc_max_stages(const Device& dev, const TcLayout& L, int bn, int cg, int kbs, int fuse) {
     for (int s = 8; s >= 2; --s) {
         TcTile t;
         t.bn = bn;
         t.stages = s;
         t.cg = cg;
         t.kbs = kbs;
+        t.fuse = fuse;
+        t.tnb = 2;
         if (tc_smem_bytes(L, t) <= dev.smem_optin) return s;
     }
     return 0;
@@ -245,6 +251,10 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
     const TcLayout L = tc_layout(pb, bf16);
     if (pb.R > 128 || pb.S > 128) { why = "R, S > 128: TMA im2col offsets are limited to [-128, 127]"; return false; }
     if (pb.M() + 256 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
+    if (force_fuse == 1 && !L.coop_ok) {
+        why = "fuse=1 needs (H+R-1)*(W+S-1) % 4 == 0 (TMA-legal NCHW plane)";
+        return false;
+    }
     static const int kBNs[] = {32, 64, 128, 192, 256};
     bool found = false;
     for (int cg = 1; cg <= 2; ++cg) {
@@ -255,13 +265,16 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
             for (int bn : kBNs) {
                 if (force_bn && bn != force_bn) continue;
                 if (!force_bn && bn > 32 && bn / 2 >= pb.K) continue;   // mostly padding
-                const int smax = tc_max_stages(dev, L, bn, cg, kbs);
-                // at least 3 stages unless forced (2 cannot overlap load and MMA well)
-                if (smax < (force_stages || force_kbs ? 2 : 3)) continue;
-                // fuse = 1 is only taken when forced: measured slower on every r01
-                // config (the in-kernel transform competes for issue slots).
+                // fuse = 1 (cooperative in-kernel In transform) is taken only
+                // when forced: measured r01b, it ties the separate repack on the
+                // batched layer (tf32 108.2 vs 108.6 us, bf16 72.2 vs 69.2 us)
+                // and loses on the small ones (startup latency of the chunk
+                // pipeline; profiles/r01b/fuse_sweep.log)
                 for (int fuse = 0; fuse <= 1; ++fuse) {
                     if (force_fuse >= 0 ? fuse != force_fuse : fuse != 0) continue;
+                    const int smax = tc_max_stages(dev, L, bn, cg, kbs, fuse);
+                    // at least 3 stages unless forced (2 cannot overlap load and MMA well)
+                    if (smax < (force_stages || force_kbs ? 2 : 3)) continue;
                     TcTile t;
                     t.bn = bn;
                     t.cg = cg;
@@ -269,6 +282,14 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
                     t.fuse = fuse;
                     t.stages = force_stages ? force_stages : smax;
                     if (t.stages < 2 || t.stages > smax) continue;
+                    if (fuse) {   // as many transform chunk buffers as fit (2..6)
+                        t.tnb = 2;
+                        for (int nb = 6; nb > 2; --nb) {
+                            TcTile u = t;
+                            u.tnb = nb;
+                            if (tc_smem_bytes(L, u) <= dev.smem_optin) { t.tnb = nb; break; }
+                        }
+                    }
                     ModelResult r = model_tc(pb, dev, bf16, t);
                     if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
                 }

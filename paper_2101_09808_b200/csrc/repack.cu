@@ -69,6 +69,8 @@ struct RepackGeom {
     int N;                           // images
     int64_t n_tiles;                 // K2 tiles (TMA variant)
     int pdl_from;                    // first block that triggers the dependent launch
+    int* zero_ptr;                   // fused main kernel: claim counter + chunk flags to clear
+    int zero_n;                      //   (ints; spread over the K1 CTAs)
 };
 
 template <bool BF16>
@@ -85,6 +87,11 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
     if ((int)blockIdx.x >= g.pdl_from) asm volatile("griddepcontrol.launch_dependents;");
     if ((int)blockIdx.x < g.n_ker) {
         // ---- K1 ----
+        if (g.zero_n) {   // clear the fused transform's claim counter and chunk flags
+            const int per = (g.zero_n + g.n_ker - 1) / g.n_ker;
+            const int z0 = blockIdx.x * per, z1 = min(z0 + per, g.zero_n);
+            for (int i = z0 + tid; i < z1; i += 256) g.zero_ptr[i] = 0;
+        }
         const int64_t k = blockIdx.x / g.ker_chunks;
         const int c0 = (blockIdx.x % g.ker_chunks) * g.cc;
         const int c1 = min(c0 + g.cc, g.Cp);
@@ -282,8 +289,11 @@ __global__ void __launch_bounds__(128) repack_tma(const float* __restrict__ ker,
 }
 
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
-                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in) {
+                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in,
+                          int* zero_ptr, int zero_n) {
     RepackGeom g;
+    g.zero_ptr = zero_ptr;
+    g.zero_n = zero_n;
     g.C = pb.C;
     g.Cp = Cp;
     g.RS = pb.R * pb.S;
@@ -299,7 +309,7 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
     // The TMA variant measured slower than repack_all in r01 (27.5 vs 23.7 us,
     // batched bf16); kept for study behind CONV_TMA_REPACK=1.
     static const bool want_tma = getenv("CONV_TMA_REPACK") != nullptr;
-    const bool use_tma = with_in && want_tma && (g.P % 4 == 0) && g.cc * g.RS * 4 <= 32768 &&
+    const bool use_tma = with_in && zero_n == 0 && want_tma && (g.P % 4 == 0) && g.cc * g.RS * 4 <= 32768 &&
                          g.n_tiles < (1ll << 31) && g.P < (1ll << 31);
     if (use_tma) {
         CUtensorMap src_map, dst_map;

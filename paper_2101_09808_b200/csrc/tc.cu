@@ -18,8 +18,13 @@
 //   warps 4-7 epilogue: tcgen05.ld 32x32b (warp w%4 owns TMEM lanes 32(w%4)..)
 //             -> coalesced st.global into NCHW Out (consecutive TMEM lanes are
 //             consecutive pixels of one (n,k) plane)   -> tmem_empty[acc]
-//   warps 0-3 (fuse = 1) In transform: NCHW fp32 -> NHWC rows of the next
-//             channel block, one block ahead of the producer -> in_full[]
+//   warp 9    (fuse = 1) watcher: acquires the flags of the chunks each of
+//             the CTA's (tile, channel block) units reads -> ready_ctr (smem)
+//   warp 8    TMEM allocator; (fuse = 1) flag publisher: releases the flags
+//             of the chunks this CTA's converters stored
+//   warps 0-3 (fuse = 1) cooperative In transform: cp.async of NCHW fp32
+//             chunks, RNE bf16 / RNA tf32 conversion, stores into the NHWC
+//             workspace; then half of the CTA's last accumulator
 // k-loop order: c-block outermost, then r, then s; a pipeline stage holds
 // kbs consecutive iterations of that order.
 //
@@ -34,6 +39,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 
@@ -45,7 +51,15 @@ namespace conv {
 using namespace sm100;
 
 static constexpr int kBM = 128;
-static constexpr int kThreads = 384;        // 12 warps: TMA, MMA, alloc, -, 4 epilogue, 4 In-transform
+static constexpr int kThreads = 384;
+static constexpr int kRing = 64;            // fused transform: decoded-chunk ring entries
+static constexpr int kDecode = 16;          //   decoded per block, one block ahead
+static constexpr int kMaxTnb = 6;           //   chunk buffers at most
+// The CTA's last tile is stored by 8 warps (4-7 and 0-3) when BN allows two
+// 32-column halves (CONV_DEBUG_MODE bit 32 disables it, experiments only).
+#ifndef CONV_SPLIT_LAST
+#define CONV_SPLIT_LAST 1
+#endif        // 12 warps: 4 In-transform, 4 epilogue, alloc, watcher, TMA, MMA
 
 struct TcParams {
     float* out;
@@ -65,15 +79,37 @@ struct TcParams {
     uint32_t b_stage_bytes;   // kbs * (bn / cg) * sw
     uint32_t debug;           // experiments only (env CONV_DEBUG_MODE): 1 no MMA, 2 no TMA, 4 no stores
     unsigned long long* trace;  // experiments only (env CONV_TRACE): per-CTA timeline, 64 slots
-    // fused In transform (a-3 inside the main kernel): NCHW fp32 -> NHWC workspace
-    int fuse;                 // 1: warps 8-11 write the NHWC rows each tile needs; 0: workspace pre-filled
-    const float* in;          // NCHW fp32 In
-    void* in_ws;              // NHWC workspace (tf32-in-fp32 or bf16), [N][Hin][Win][Cp]
-    int C, Hin, Win;
     int tap_outer;            // k order: 1 = (r, s, cb) [not with fuse], 0 = (cb, r, s)
+    // ---- cooperative In transform (a-3 inside the main kernel, fuse = 1) ----
+    int fuse;                 // 1: warps 0-3 of every CTA convert NCHW fp32 chunks into the NHWC workspace
+    int* flags;               // [Q][nch] chunk-ready flags (zeroed by the Ker repack launch)
+    const float* in;          // In, NCHW fp32
+    void* in_ws;              // NHWC workspace
+    int C;                    // input channels
+    int P, Win;               // pixels per input image (Hin*Win), input width
+    int npch;                 // 64-pixel chunks per image plane: ceil(P / 64)
+    int cc;                   // channels per chunk (min(32, bkc))
+    int nch;                  // channel chunks: Cp / cc
+    int hh;                   // channel chunks per k-block: bkc / cc
+    int total_chunks;         // N * npch * nch
+    int hh_log2;              // log2(hh)
+    int n_groups;             // chunk groups (waves of the schedule, merged to <= 32)
+    int gend[32];             // group g covers chunk-pixel indices q in [gend[g-1], gend[g])
+    int tnb;                  // input staging buffers (2..4)
+    uint32_t tr_off;          // byte offset of the transform smem region (1024-aligned)
 };
 
-// ---- fused NCHW -> NHWC transform of the input rows one tile needs ----------
+// ---- cooperative NCHW -> NHWC transform (row a-3 inside K3) ----------------
+// The input is cut into chunks (image n, 64-pixel run pch of the NCHW plane,
+// cc channels), ordered by when the persistent schedule first needs them:
+// waves of tiles, then channel block, then pixel.  CTA w of W transforms
+// sequence entries w, w + W, ... (all CTAs are co-resident: one per SM, and
+// the launch is cooperative).  A chunk is TMA-loaded as [cc][64] fp32,
+// converted (RNA tf32 / RNE bf16) and transposed in place into a [64 px][cc]
+// row-swizzled tile, TMA-stored into the NHWC workspace and published with
+// a release flag.  Each CTA's watcher acquires the flags of the chunks its
+// next (tile, channel block) im2col loads read and hands them to the TMA
+// producer through a shared counter.
 __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -84,75 +120,136 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta_smem(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta_smem(int* p, int v) {
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
-// The rows of In (image n, input row h_in, all Win pixels, all Cp channels)
-// read by the im2col loads of output pixels [m0, m0 + 128): for every image
-// the tile touches, output rows h_lo..h_hi need input rows h_lo..h_hi+R-1.
-// Work item = (row, VEC channels, 4 pixels) when the NCHW rows allow float4
-// loads (Win % 4 == 0), else (row, VEC channels, 1 pixel); one 16-B store
-// per pixel of VEC converted channels.  nthr threads starting at tid.
+// Chunk j of the sequence -> {flag index q*nch + ch, image n, first pixel,
+// first channel}.  Group g = the q range [gend[g-1], gend[g]) first read by
+// wave g of the persistent schedule (host-computed, see tc_run), so group g
+// starts at sequence index gend[g-1]*nch; inside a group the order is
+// (channel block, q, channel chunk within the block).
+__device__ __forceinline__ int4 chunk_decode(const TcParams& p, int j) {
+    int g = 0;
+    while (g < p.n_groups - 1 && p.gend[g] * p.nch <= j) ++g;
+    const int e_prev = g > 0 ? p.gend[g - 1] : 0;
+    const int l = j - e_prev * p.nch;
+    const int per_cb = (p.gend[g] - e_prev) << p.hh_log2;
+    const int cb = l / per_cb;
+    const int rem = l - cb * per_cb;
+    const int q = e_prev + (rem >> p.hh_log2);
+    const int ch = (cb << p.hh_log2) + (rem & ((1 << p.hh_log2) - 1));
+    const int n = q / p.npch;
+    return make_int4(q * p.nch + ch, n, (q - n * p.npch) * 64, ch * p.cc);
+}
+
+// Thread t of the 128 converters: pixel t & 63 of the chunk, channel half
+// t >> 6 (cc/2 channels).  Reads its values from the [cc][64] fp32 smem
+// copy of the chunk (conflict-free: consecutive lanes, consecutive pixels).
+__device__ __forceinline__ void chunk_read(const float* tin, int cc, int tid, float (&v)[16]) {
+    const int px = tid & 63, half = tid >> 6, ch = cc / 2;
+    const float* s = tin + (half * ch) * 64 + px;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        if (j < ch) v[j] = s[j * 64];
+}
+// In place: [cc][64] fp32 -> [64 px][cc] rows of cc*elem bytes, 16-B
+// pieces swizzled as the destination map's SWIZZLE_{32,64,128}B expects
+// (piece k of row r at k ^ ((r * row_bytes >> 7) & (row_bytes/16 - 1))).
+// All threads read (chunk_read) before any thread writes.
 template <bool BF16>
-__device__ void transform_tile_rows(const TcParams& p, int m0, int cbeg, int cend, int tid, int nthr) {
-    constexpr int VEC = BF16 ? 8 : 4;
-    constexpr int ES = BF16 ? 2 : 4;
-    const int m1 = min(m0 + 128, p.M) - 1;
-    if (m1 < m0) return;
-    const int n_a = m0 / p.HW, n_b = m1 / p.HW;
-    const bool vec4 = (p.Win & 3) == 0;
-    const int pg = vec4 ? 4 : 1;
-    const int groups = p.Win / pg;                 // pixel groups per row
-    const int cvecs = (cend - cbeg) / VEC;
-    const int per_row = groups * cvecs;
-    const int64_t P = (int64_t)p.Hin * p.Win;
-    for (int i0 = tid; i0 < per_row; i0 += nthr) {  // usually one (cv, g) per thread
-        const int cv = i0 / groups;
-        const int g = i0 - cv * groups;
-        const int w0 = g * pg;
-        const int c0 = cbeg + cv * VEC;
-        for (int n = n_a; n <= n_b; ++n) {
-            const int p_lo = n == n_a ? m0 - n * p.HW : 0;
-            const int p_hi = n == n_b ? m1 - n * p.HW : p.HW - 1;
-            const int h_lo = p_lo / p.W;
-            const int h_hi = min(p_hi / p.W + p.R - 1, p.Hin - 1);
-            const float* src = p.in + ((int64_t)n * p.C + c0) * P + (int64_t)h_lo * p.Win + w0;
-            uint8_t* dst = reinterpret_cast<uint8_t*>(p.in_ws) +
-                           ((((int64_t)n * p.Hin + h_lo) * p.Win + w0) * p.Cp + c0) * ES;
-            const int64_t dst_row = (int64_t)p.Win * p.Cp * ES;
-            for (int h = h_lo; h <= h_hi; ++h, src += p.Win, dst += dst_row) {
-                float v[VEC][4];
+__device__ __forceinline__ void chunk_write(uint8_t* tout, int cc, int tid, const float (&v)[16]) {
+    const int px = tid & 63, half = tid >> 6, ch = cc / 2;
+    const int row_bytes = cc * (BF16 ? 2 : 4);
+    const int sw = ((px * row_bytes) >> 7) & (row_bytes / 16 - 1);
+    uint8_t* row = tout + px * row_bytes;
+    if (BF16) {   // ch in {8, 16}: 8 channels per 16-B piece
+        const int nk = ch / 8;
 #pragma unroll
-                for (int j = 0; j < VEC; ++j) {
-                    if (c0 + j < p.C) {
-                        const float* s = src + (int64_t)j * P;
-                        if (vec4) {
-                            const float4 x = __ldg(reinterpret_cast<const float4*>(s));
-                            v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
-                        } else {
-                            v[j][0] = __ldg(s);
-                        }
-                    } else {
+        for (int kk = 0; kk < 2; ++kk) {
+            if (kk < nk) {
+                uint4 o;
+                o.x = pack_bf16x2(v[8 * kk + 0], v[8 * kk + 1]);
+                o.y = pack_bf16x2(v[8 * kk + 2], v[8 * kk + 3]);
+                o.z = pack_bf16x2(v[8 * kk + 4], v[8 * kk + 5]);
+                o.w = pack_bf16x2(v[8 * kk + 6], v[8 * kk + 7]);
+                const int k = half * nk + kk;
+                *reinterpret_cast<uint4*>(row + ((k ^ sw) << 4)) = o;
+            }
+        }
+    } else {      // ch in {4, 8, 16}: 4 channels per 16-B piece
+        const int nk = ch / 4;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) v[j][q] = 0.0f;
-                    }
-                }
+        for (int kk = 0; kk < 4; ++kk) {
+            if (kk < nk) {
+                float4 o;
+                o.x = tf32_rna(v[4 * kk + 0]);
+                o.y = tf32_rna(v[4 * kk + 1]);
+                o.z = tf32_rna(v[4 * kk + 2]);
+                o.w = tf32_rna(v[4 * kk + 3]);
+                const int k = half * nk + kk;
+                *reinterpret_cast<float4*>(row + ((k ^ sw) << 4)) = o;
+            }
+        }
+    }
+}
+
+// TMEM accumulator columns [j_lo, j_hi) of one tile -> NCHW Out.  Warp
+// quadrant q owns TMEM lanes 32q..32q+31 = the tile's pixels 32q + lane;
+// each 32x32b load gives a thread 32 consecutive output channels of its
+// pixel, stored as 32 coalesced 128-B runs (one per channel) by the warp.
+template <int BN, int CG>
+__device__ __forceinline__ void store_accumulator(const TcParams& p, uint32_t tmem_base, int tile, int acc,
+                                                  uint32_t rank, int q, uint32_t lane, int j_lo, int j_hi) {
+    const int m_tile = tile / p.num_n_tiles;
+    const int n_tile = tile - m_tile * p.num_n_tiles;
+    const int m = m_tile * (kBM * CG) + (int)rank * kBM + q * 32 + (int)lane;
+    const int k0 = n_tile * BN;
+    const bool valid_m = m < p.M;
+    const int img = valid_m ? m / p.HW : 0;
+    const int pix = valid_m ? m - img * p.HW : 0;
+    float* obase = p.out + ((int64_t)img * p.K) * p.HW + pix;
+    const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+    for (int j0 = j_lo; j0 < j_hi; j0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t0 + (uint32_t)j0, v);
+        tmem_ld_wait();
+        const int kbase = k0 + j0;
+        if (valid_m && !(p.debug & 4)) {
+            if (kbase + 32 <= p.K) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (q < pg) {
-                        uint4 o;
-                        if (BF16) {
-                            o.x = pack_bf16x2(v[0][q], v[1][q]);
-                            o.y = pack_bf16x2(v[2][q], v[3][q]);
-                            o.z = pack_bf16x2(v[4 % VEC][q], v[5 % VEC][q]);
-                            o.w = pack_bf16x2(v[6 % VEC][q], v[7 % VEC][q]);
-                        } else {
-                            o.x = __float_as_uint(tf32_rna(v[0][q]));
-                            o.y = __float_as_uint(tf32_rna(v[1][q]));
-                            o.z = __float_as_uint(tf32_rna(v[2][q]));
-                            o.w = __float_as_uint(tf32_rna(v[3][q]));
-                        }
-                        *reinterpret_cast<uint4*>(dst + (int64_t)q * p.Cp * ES) = o;
-                    }
-                }
+                for (int j = 0; j < 32; ++j)
+                    __stcs(obase + (int64_t)(kbase + j) * p.HW, __uint_as_float(v[j]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (kbase + j < p.K) __stcs(obase + (int64_t)(kbase + j) * p.HW, __uint_as_float(v[j]));
             }
         }
     }
@@ -168,7 +265,10 @@ __device__ void transform_tile_rows(const TcParams& p, int m0, int cbeg, int cen
 template <int BN, bool BF16, int CG, int KSTEPS>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
-                   const __grid_constant__ CUtensorMap tmap_b, const TcParams p) {
+                   const __grid_constant__ CUtensorMap tmap_b,
+                   const __grid_constant__ CUtensorMap tmap_src,    // fuse: In NCHW fp32 {P, C, N}
+                   const __grid_constant__ CUtensorMap tmap_dst,    // fuse: workspace NHWC {Cp, P, N}
+                   const TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the 128-B swizzle atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -179,9 +279,22 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     uint64_t* empty = bars + p.stages;
     uint64_t* tmem_full = bars + 2 * p.stages;
     uint64_t* tmem_empty = tmem_full + 2;
-    uint64_t* in_full = tmem_empty + 2;           // fused In transform -> producer
-    uint64_t* in_empty = in_full + 2;             // producer -> In transform (bounds run-ahead)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(in_empty + 2);
+    int* ready_ctr = reinterpret_cast<int*>(tmem_empty + 2);     // fuse: (tile, cb) units confirmed
+    uint64_t* last_full = tmem_empty + 3;                        // the CTA's last accumulator is ready
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 4);
+    int* done_ctr = reinterpret_cast<int*>(tmem_empty + 5);      // fuse: chunks stored so far
+    int* pub_ctr = done_ctr + 1;                                 // fuse: chunks whose flags are published
+    // fuse: per chunk buffer a "loaded" (TMA tx) and a "converted" (4 warps)
+    // mbarrier, then the decoded-chunk counter, after the pipeline barriers
+    uint64_t* tfull = tmem_empty + 6;
+    uint64_t* tconv = tfull + kMaxTnb;
+    int* dec_ctr = reinterpret_cast<int*>(tconv + kMaxTnb);      // fuse: ring entries decoded so far
+    // transform region (fuse): tnb chunk buffers of [cc][64] fp32 and a
+    // kRing-entry ring of decoded chunks
+    uint8_t* tbuf = smem + p.tr_off;
+    int4* cring = reinterpret_cast<int4*>(tbuf + (size_t)p.tnb * p.cc * 256);
+    // static chunk assignment: CTA w of W takes sequence indices w, w + W, ...
+    const int n_my = p.fuse ? (p.total_chunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -195,6 +308,17 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
+        if (p.fuse) {
+            prefetch_tmap(&tmap_src);
+            prefetch_tmap(&tmap_dst);
+            for (int i = 0; i < p.tnb; ++i) {
+                mbar_init(&tfull[i], 1);
+                mbar_init(&tconv[i], 4);                          // one arrive per converter warp
+            }
+            *done_ctr = 0;
+            *pub_ctr = 0;
+            *dec_ctr = 0;
+        }
         for (int i = 0; i < p.stages; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
@@ -202,9 +326,9 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
             mbar_init(&tmem_empty[i], 4 * CG);    // one arrive per epilogue warp of the pair
-            mbar_init(&in_full[i], 4);            // one arrive per transform warp
-            mbar_init(&in_empty[i], 1);
         }
+        mbar_init(last_full, 1);
+        *ready_ctr = 0;
         fence_barrier_init();
     }
     if (warp == 8) {
@@ -216,9 +340,11 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t wflavor = (p.debug >> 3) & 3;
+    const bool kSplitLast = CONV_SPLIT_LAST && BN >= 64 && !(p.debug & 32);
     // Programmatic dependent launch: everything above overlapped the tail of
-    // the repack launch; from here on the repacked workspace is read (and Out
-    // written), so wait for the preceding grid to complete and flush.
+    // the repack launch; from here on the repacked workspace (and, fused, the
+    // zeroed chunk flags) is read and Out written, so wait for the preceding
+    // grid to complete and flush.
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 10) {
@@ -232,8 +358,10 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             long long prod_wait = 0;
             int stage = 0;
             uint32_t phase = 0;
-            int u = 0, ue = 0;                            // (tile, channel block) units: waited / released
-            for (int tile = unit; tile < p.num_tiles; tile += nunits) {
+            int tiles_done = 0;                           // fuse: tiles of this CTA so far
+            int ready_seen = 0;                           // fuse: last value read from ready_ctr
+            long long ready_wait = 0;
+            for (int tile = unit; tile < p.num_tiles; tile += nunits, ++tiles_done) {
                 const int m_tile = tile / p.num_n_tiles;
                 const int n_tile = tile - m_tile * p.num_n_tiles;
                 const int m0 = m_tile * (kBM * CG) + (int)rank * kBM;
@@ -248,11 +376,29 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 // consecutive iterations, so the order does not depend on kbs.
                 int cb = 0, r = 0, s = 0;
                 for (int it0 = 0; it0 < p.k_iters; it0 += p.kbs) {
-                    if (p.fuse) {   // channel blocks that start inside this stage must be written
-                        int c2 = cb, r2 = r, s2 = s;
-                        for (int kb = 0; kb < p.kbs; ++kb) {
-                            if (r2 == 0 && s2 == 0) { mbar_wait(&in_full[u & 1], (u >> 1) & 1); ++u; }
-                            if (++s2 == p.S) { s2 = 0; if (++r2 == p.R) { r2 = 0; ++c2; } }
+                    const int cb_s = cb, r_s = r, s_s = s;
+                    // advance the counters past this stage (all lanes, uniform)
+                    int cb_last = cb;
+                    for (int kb = 0; kb < p.kbs; ++kb) {
+                        cb_last = cb;
+                        if (p.tap_outer) {
+                            if (++cb == p.n_cblk) { cb = 0; if (++s == p.S) { s = 0; ++r; } }
+                        } else {
+                            if (++s == p.S) { s = 0; if (++r == p.R) { r = 0; ++cb; } }
+                        }
+                    }
+                    if (p.fuse) {
+                        // the watcher has confirmed (tile, channel block) units in
+                        // order; this stage reads channel blocks up to cb_last
+                        const int need = tiles_done * p.n_cblk + cb_last + 1;
+                        if (ready_seen < need) {
+                            const long long t0 = clock64();
+                            while ((ready_seen = ld_acquire_cta_smem(ready_ctr)) < need) {
+                                __nanosleep(128);         // do not steal issue slots from the converters
+                                if (clock64() - t0 > 8000000000ll) __trap();
+                            }
+                            fence_proxy_async_global();   // flags observed -> TMA reads of the workspace
+                            if (p.trace) ready_wait += clock64() - t0;
                         }
                     }
                     const long long pw0 = p.trace ? clock64() : 0;
@@ -260,15 +406,6 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     if (p.trace) prod_wait += clock64() - pw0;
                     uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
                     uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
-                    const int cb_s = cb, r_s = r, s_s = s;
-                    // advance the counters past this stage (all lanes, uniform)
-                    for (int kb = 0; kb < p.kbs; ++kb) {
-                        if (p.tap_outer) {
-                            if (++cb == p.n_cblk) { cb = 0; if (++s == p.S) { s = 0; ++r; } }
-                        } else {
-                            if (++s == p.S) { s = 0; if (++r == p.R) { r = 0; ++cb; } }
-                        }
-                    }
                     if (elect_one_sync()) {
                         if (p.debug & 2) {
                             if (leader) mbar_arrive(&full[stage]);
@@ -293,28 +430,15 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                                 }
                             }
                         }
-                        if (p.fuse) {   // channel blocks that end inside this stage are consumed
-                            int r2 = r_s, s2 = s_s, e2 = ue;
-                            for (int kb = 0; kb < p.kbs; ++kb) {
-                                if (r2 == p.R - 1 && s2 == p.S - 1) mbar_arrive(&in_empty[(e2++) & 1]);
-                                if (++s2 == p.S) { s2 = 0; if (++r2 == p.R) r2 = 0; }
-                            }
-                        }
                     }
                     __syncwarp();
-                    if (p.fuse) {   // same count in every lane (uniform)
-                        int r2 = r_s, s2 = s_s;
-                        for (int kb = 0; kb < p.kbs; ++kb) {
-                            if (r2 == p.R - 1 && s2 == p.S - 1) ++ue;
-                            if (++s2 == p.S) { s2 = 0; if (++r2 == p.R) r2 = 0; }
-                        }
-                    }
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
                 }
             }
             if (p.trace && lane == 0) {
                 p.trace[(size_t)blockIdx.x * 64 + 60] = (unsigned long long)prod_wait;
                 p.trace[(size_t)blockIdx.x * 64 + 61] = globaltimer_ns();
+                p.trace[(size_t)blockIdx.x * 64 + 57] = (unsigned long long)ready_wait;
             }
         }
     } else if (warp == 11) {
@@ -379,10 +503,15 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     __syncwarp();
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
                 }
-                // accumulator ready for the epilogue (of both CTAs)
+                // accumulator ready for the epilogue (of both CTAs); the last
+                // tile's also signals warps 0-3, which store half of it
                 if (elect_one_sync()) {
                     if (CG == 2) tc_commit_pair_mc(&tmem_full[acc], 0x3);
                     else tc_commit(&tmem_full[acc]);
+                    if (kSplitLast && tile + nunits >= p.num_tiles) {
+                        if (CG == 2) tc_commit_pair_mc(last_full, 0x3);
+                        else tc_commit(last_full);
+                    }
                 }
                 __syncwarp();
                 if (tr && lane == 0 && ti < 8) {
@@ -393,66 +522,207 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else if (warp < 4) {
-        // ===== fused In transform: NCHW fp32 -> NHWC rows, one channel group
-        // ahead of the producer =====
+    } else if (warp == 9) {
+        // ===== watcher + publisher (fuse).  Each pass: (1) release the flags
+        // of chunks whose stores the storer reports landed (done_ctr), up to
+        // 32 per warp instruction, one GPU-scope fence per batch; (2) check
+        // the next (tile, channel block) unit of this CTA -- relaxed reads of
+        // the flags of every chunk its im2col loads read -- and, once all are
+        // set, acquire them and hand the unit count to the TMA producer. =====
         if (p.fuse) {
-            const int tid = threadIdx.x;
-            int u = 0;
-            for (int tile = unit; tile < p.num_tiles; tile += nunits) {
+            int u = 0, pub = 0;
+            const int n_units = ((p.num_tiles - unit + nunits - 1) / nunits) * p.n_cblk;
+            int tile = unit, cb = 0, q_lo = 0, cnt = 0;
+            auto tile_range = [&]() {
                 const int m_tile = tile / p.num_n_tiles;
-                // Every CTA writes the rows its own tiles read (tiles of other
-                // CTAs may rewrite the same rows with the same values): the
-                // only ordering needed is CTA-local.
-                for (int cb = 0; cb < p.n_cblk; ++cb, ++u) {
-                    mbar_wait_sleep(&in_empty[u & 1], ((u >> 1) & 1) ^ 1, 64);
-                    transform_tile_rows<BF16>(p, m_tile * (kBM * CG) + (int)rank * kBM, cb * p.bkc,
-                                              (cb + 1) * p.bkc, tid, 128);
-                    asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&in_full[u & 1]);
+                const int m0 = m_tile * (kBM * CG) + (int)rank * kBM;
+                q_lo = 0;
+                int q_hi = -1;                            // empty if the rows are all past M
+                if (m0 < p.M) {
+                    const int m1 = min(m0 + kBM, p.M) - 1;
+                    const int na = m0 / p.HW, nb = m1 / p.HW;
+                    const int ha = (m0 - na * p.HW) / p.W, hb = (m1 - nb * p.HW) / p.W;
+                    q_lo = na * p.npch + (ha * p.Win) / 64;
+                    q_hi = nb * p.npch + ((hb + p.R - 1) * p.Win + p.Win - 1) / 64;
                 }
+                cnt = (q_hi - q_lo + 1) * p.hh;
+            };
+            if (n_units > 0) tile_range();
+            long long w_spin = 0;
+            const long long t_start = clock64();
+            while (u < n_units || pub < n_my) {
+                if (clock64() - t_start > 8000000000ll) __trap();
+                bool progress = false;
+                const int done = ld_acquire_cta_smem(done_ctr);
+                if (pub < done) {
+                    const int batch = min(32, done - pub);
+                    if ((int)lane < batch) st_release_gpu(p.flags + cring[(pub + (int)lane) & (kRing - 1)].x, 1);
+                    if (p.trace && lane == 0 && pub == 0) p.trace[(size_t)(512 + blockIdx.x) * 64 + 2] = globaltimer_ns();
+                    pub += batch;
+                    __syncwarp();
+                    if (lane == 0) st_release_cta_smem(pub_ctr, pub);
+                    progress = true;
+                }
+                if (u < n_units) {
+                    bool ok = true;
+                    for (int i = (int)lane; i < cnt; i += 32) {
+                        const int q = q_lo + i / p.hh;
+                        const int ch = cb * p.hh + (i - (i / p.hh) * p.hh);
+                        if (ld_relaxed_gpu(p.flags + (size_t)q * p.nch + ch) == 0) ok = false;
+                    }
+                    if (__all_sync(0xffffffffu, ok)) {
+                        fence_acq_rel_gpu();              // the flags read above -> acquire
+                        fence_proxy_async_global();       // -> the producer's TMA reads
+                        ++u;
+                        if (lane == 0) st_release_cta_smem(ready_ctr, u);
+                        if (p.trace && lane == 0 && u == 1) p.trace[(size_t)blockIdx.x * 64 + 56] = globaltimer_ns();
+                        if (++cb == p.n_cblk) {
+                            cb = 0;
+                            tile += nunits;
+                            if (u < n_units) tile_range();
+                        }
+                        progress = true;
+                    }
+                }
+                if (!progress) {
+                    const long long t0 = p.trace ? clock64() : 0;
+                    __nanosleep(128);
+                    if (p.trace) w_spin += clock64() - t0;
+                }
+            }
+            if (p.trace && lane == 0) p.trace[(size_t)blockIdx.x * 64 + 39] = (unsigned long long)w_spin;
+        }
+    } else if (warp == 8) {
+        // ===== chunk loader / storer (fuse, lane 0): TMA-loads this CTA's
+        // chunks ([cc][64] fp32 boxes of NCHW) into tnb buffers, TMA-stores
+        // each converted [64][cc] tile into the NHWC workspace, refills a
+        // buffer once its store has read it, and reports landed stores
+        // (kPubLag behind) to the publisher.  Chunk coordinates come
+        // pre-decoded from the ring (no divisions on this thread). =====
+        if (p.fuse && lane == 0 && n_my > 0) {
+            constexpr int kPubLag = 1;
+            const uint32_t buf_bytes = (uint32_t)p.cc * 256;
+            unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
+            long long c_conv = 0, c_rd = 0, c_pub = 0, c_dec = 0;
+            if (tr) tr[58] = globaltimer_ns();
+            const long long t_start = clock64();
+            auto entry = [&](int k) -> int4 {          // waits until the converters decoded chunk k
+                if (ld_acquire_cta_smem(dec_ctr) <= k) {
+                    const long long t0 = clock64();
+                    while (ld_acquire_cta_smem(dec_ctr) <= k) {
+                        if (clock64() - t_start > 8000000000ll) __trap();
+                    }
+                    if (tr) c_dec += clock64() - t0;
+                }
+                return cring[k & (kRing - 1)];
+            };
+            auto load = [&](int k) {
+                const int4 e = entry(k);
+                const int b = k % p.tnb;
+                mbar_arrive_expect_tx(&tfull[b], buf_bytes);
+                tma_load_3d(tbuf + (size_t)b * buf_bytes, &tmap_src, &tfull[b], e.z, e.w, e.y);
+            };
+            unsigned long long* t2 = p.trace ? p.trace + (size_t)(512 + blockIdx.x) * 64 : nullptr;
+            for (int k = 0; k < p.tnb && k < n_my; ++k) {
+                load(k);
+                if (t2 && k == 0) t2[4] = globaltimer_ns();
+            }
+            for (int k = 0; k < n_my; ++k) {
+                const int b = k % p.tnb;
+                const long long t0 = tr ? clock64() : 0;
+                mbar_wait(&tconv[b], (uint32_t)(k / p.tnb) & 1);
+                if (t2 && k == 0) t2[0] = globaltimer_ns();
+                if (tr) c_conv += clock64() - t0;
+                const int4 e = cring[k & (kRing - 1)];
+                tma_store_3d(&tmap_dst, tbuf + (size_t)b * buf_bytes, e.w, e.z, e.y);
+                bulk_commit();
+                const int kn = k - 1 + p.tnb;             // refill chunk k-1's buffer with chunk k-1+tnb
+                if (k >= 1 && kn < n_my) {
+                    const long long t1 = tr ? clock64() : 0;
+                    bulk_wait_read<1>();
+                    if (tr) c_rd += clock64() - t1;
+                    load(kn);
+                }
+                const long long t3 = tr ? clock64() : 0;
+                bulk_wait<kPubLag>();                     // all but the newest kPubLag stores have landed
+                if (tr) c_pub += clock64() - t3;
+                if (k >= kPubLag) {
+                    fence_proxy_async_global();           // async-proxy writes -> generic flag release
+                    st_release_cta_smem(done_ctr, k - kPubLag + 1);
+                    if (t2 && k == kPubLag) t2[1] = globaltimer_ns();
+                }
+            }
+            bulk_wait<0>();
+            fence_proxy_async_global();
+            st_release_cta_smem(done_ctr, n_my);
+            if (tr) {
+                tr[33] = (unsigned long long)n_my;
+                tr[34] = (unsigned long long)c_conv;
+                tr[35] = (unsigned long long)c_rd;
+                tr[36] = (unsigned long long)c_pub;
+                tr[37] = (unsigned long long)c_dec;
+                tr[38] = globaltimer_ns();
+            }
+        }
+        __syncwarp();
+    } else if (warp < 4) {
+        // ===== chunk converters + decoders (fuse): decode the chunk ring
+        // one block ahead (parallel binary searches, no divisions on the
+        // storer), then convert + transpose every loaded chunk in place
+        // (RNE bf16 / RNA tf32) into the row-swizzled staging tile the
+        // storer's TMA store expects. =====
+        if (p.fuse && n_my > 0) {
+            const int tid = threadIdx.x;                  // 0..127
+            const int w = (int)blockIdx.x, W = (int)gridDim.x;
+            const uint32_t buf_bytes = (uint32_t)p.cc * 256;
+            auto decode_block = [&](int k0) {             // chunks [k0, k0 + kDecode) -> ring
+                if (tid < kDecode && k0 + tid < n_my)
+                    cring[(k0 + tid) & (kRing - 1)] = chunk_decode(p, w + (k0 + tid) * W);
+                named_bar_sync(1, 128);
+                if (tid == 0) st_release_cta_smem(dec_ctr, min(k0 + kDecode, n_my));
+            };
+            decode_block(0);
+            if (kDecode < n_my) decode_block(kDecode);
+            if (p.trace && tid == 0) p.trace[(size_t)(512 + blockIdx.x) * 64 + 3] = globaltimer_ns();
+            for (int k = 0; k < n_my; ++k) {
+                const int b = k % p.tnb;
+                // one block ahead: decode chunks [k + 2 kDecode, ...) once the
+                // publisher is past the ring slots they reuse
+                if ((k % kDecode) == 0 && k + 2 * kDecode < n_my) {
+                    const int k0 = k + 2 * kDecode;
+                    if (tid == 0) {
+                        const long long t0 = clock64();
+                        while (ld_acquire_cta_smem(pub_ctr) < k0 + kDecode - kRing) {
+                            __nanosleep(64);
+                            if (clock64() - t0 > 8000000000ll) __trap();
+                        }
+                    }
+                    named_bar_sync(1, 128);
+                    decode_block(k0);
+                }
+                mbar_wait_sleep(&tfull[b], (uint32_t)(k / p.tnb) & 1, 32);
+                uint8_t* buf = tbuf + (size_t)b * buf_bytes;
+                float v[16];
+                chunk_read(reinterpret_cast<const float*>(buf), p.cc, tid, v);
+                named_bar_sync(1, 128);                   // every read of buf done
+                chunk_write<BF16>(buf, p.cc, tid, v);
+                fence_proxy_async_smem();                 // generic smem writes -> TMA store
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tconv[b]);
             }
         }
     } else if (warp >= 4 && warp < 8) {
         // ===== epilogue: TMEM -> registers -> NCHW Out =====
-        const int q = warp & 3;                       // TMEM lane quadrant of this warp
-        const int row = q * 32 + (int)lane;           // accumulator row = pixel within the CTA's tile
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = unit; tile < p.num_tiles; tile += nunits) {
-            const int m_tile = tile / p.num_n_tiles;
-            const int n_tile = tile - m_tile * p.num_n_tiles;
-            const int m = m_tile * (kBM * CG) + (int)rank * kBM + row;
-            const int k0 = n_tile * BN;
-            const bool valid_m = m < p.M;
-            const int img = valid_m ? m / p.HW : 0;
-            const int pix = valid_m ? m - img * p.HW : 0;
-            float* obase = p.out + ((int64_t)img * p.K) * p.HW + pix;
-
             mbar_wait_sleep(&tmem_full[acc], acc_phase, 256);
             tc_fence_after();
             const int ti_e = (tile - unit) / nunits;
             if (p.trace && warp == 4 && lane == 0 && ti_e < 8) p.trace[(size_t)blockIdx.x * 64 + 40 + 2 * ti_e] = globaltimer_ns();
-            const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-#pragma unroll 1
-            for (int j0 = 0; j0 < BN; j0 += 32) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(t0 + (uint32_t)j0, v);
-                tmem_ld_wait();
-                const int kbase = k0 + j0;
-                if (valid_m && !(p.debug & 4)) {
-                    if (kbase + 32 <= p.K) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            __stcs(obase + (int64_t)(kbase + j) * p.HW, __uint_as_float(v[j]));
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (kbase + j < p.K) __stcs(obase + (int64_t)(kbase + j) * p.HW, __uint_as_float(v[j]));
-                    }
-                }
-            }
+            // the CTA's last tile is split: warps 0-3 store columns [BN/2, BN)
+            const bool last = kSplitLast && tile + nunits >= p.num_tiles;
+            store_accumulator<BN, CG>(p, tmem_base, tile, acc, rank, warp & 3, lane, 0, last ? BN / 2 : BN);
             tc_fence_before();
             __syncwarp();
             if (p.trace && warp == 4 && lane == 0 && ti_e < 8) p.trace[(size_t)blockIdx.x * 64 + 41 + 2 * ti_e] = globaltimer_ns();
@@ -462,6 +732,16 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+    }
+
+    // Warps 0-3 (after the transform, if any): the second half of the last
+    // accumulator, so the exposed tail of the kernel is half an epilogue.
+    if (kSplitLast && warp < 4 && unit < p.num_tiles) {
+        const int n_my = (p.num_tiles - unit + nunits - 1) / nunits;
+        const int ti = n_my - 1;
+        mbar_wait_sleep(last_full, 0, 256);
+        tc_fence_after();
+        store_accumulator<BN, CG>(p, tmem_base, unit + ti * nunits, ti & 1, rank, warp & 3, lane, BN / 2, BN);
     }
 
     // Teardown: every MMA has retired (the epilogues consumed every
@@ -492,21 +772,45 @@ TcLayout tc_layout(const Problem& pb, bool bf16) {
     L.n_cblk = L.Cp / L.bkc;
     L.in_ws_bytes = (size_t)pb.N * pb.Hin() * pb.Win() * L.Cp * L.elem;
     L.ker_ws_bytes = (size_t)pb.K * pb.R * pb.S * L.Cp * L.elem;
+    L.cc = L.bkc < 32 ? L.bkc : 32;
+    L.nch = L.Cp / L.cc;
+    L.hh = L.bkc / L.cc;
+    const int64_t P = pb.Hin() * pb.Win();
+    L.npch = (P + 63) / 64;
+    L.coop_ok = (P % 4) == 0 && (int64_t)pb.N * L.npch * L.nch < (1ll << 30);
+    L.flag_bytes = L.coop_ok ? 128 + (size_t)pb.N * L.npch * L.nch * sizeof(int) : 0;
     return L;
 }
 
-size_t tc_smem_bytes(const TcLayout& L, const TcTile& t) {
+// pipeline ring + barrier block, then (fuse) the transform region at a
+// 1024-B boundary: tnb fp32 [cc][64] chunk buffers (converted in place),
+// tnb mbarriers and tnb chunk slots.
+static size_t tc_pipe_bytes(const TcLayout& L, const TcTile& t) {
     const size_t a = (size_t)t.kbs * kBM * L.sw, b = (size_t)t.kbs * (t.bn / t.cg) * L.sw;
-    return 1024 /*align slack*/ + (size_t)t.stages * (a + b) + (2 * t.stages + 8) * 8 + 16;
+    // barriers: full/empty per stage, 2+2 accumulator, ready/last/slot/counters,
+    // and the fused transform's 2 x kMaxTnb chunk barriers + decode counter
+    return (size_t)t.stages * (a + b) + (2 * t.stages + 8 + 2 * kMaxTnb + 1) * 8 + 16;
+}
+size_t tc_transform_smem_bytes(const TcLayout& L, int tnb) {
+    return (size_t)tnb * L.cc * 256 + kRing * 16;
+}
+size_t tc_smem_bytes(const TcLayout& L, const TcTile& t) {
+    size_t s = tc_pipe_bytes(L, t);
+    if (t.fuse) s = (s + 1023) / 1024 * 1024 + tc_transform_smem_bytes(L, t.tnb);
+    return 1024 /*align slack*/ + s;
 }
 
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
-                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in);
+                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in,
+                          int* zero_ptr, int zero_n);
 
+
+struct TcMaps {
+    CUtensorMap a, b, src, dst;   // src/dst only with fuse (copies of a/b otherwise)
+};
 
 template <int BN, bool BF16, int CG, int KSTEPS>
-static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& prm,
-                             size_t smem, int grid, cudaStream_t st) {
+static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
     auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS>;
     // Opt in to the largest dynamic smem once per instantiation (per process).
     static std::atomic<int> smem_set{0};
@@ -523,7 +827,7 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
@@ -531,67 +835,48 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const
     static const int no_pdl = getenv("CONV_NO_PDL") ? 1 : 0;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL after the repack
     attr[1].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    // The fused transform's CTAs wait on chunks other CTAs convert: all of
+    // them must be resident at once, which a cooperative launch guarantees
+    // (or refuses to launch).
+    attr[2].id = cudaLaunchAttributeCooperative;
+    attr[2].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kfn, ta, tb, prm);
+    static const int no_coop = getenv("CONV_NO_COOP") ? 1 : 0;   // experiments only
+    cfg.numAttrs = (prm.fuse && !no_coop) ? 3 : 2;
+    return cudaLaunchKernelEx(&cfg, kfn, m.a, m.b, m.src, m.dst, prm);
 }
 
 template <bool BF16, int CG, int KSTEPS>
-static cudaError_t launch_tc_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                                const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
+static cudaError_t launch_tc_bn(int bn, const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
     switch (bn) {
-        case 32: return launch_tc<32, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
-        case 64: return launch_tc<64, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
-        case 128: return launch_tc<128, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
-        case 192: return launch_tc<192, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
-        case 256: return launch_tc<256, BF16, CG, KSTEPS>(ta, tb, prm, smem, grid, st);
+        case 32: return launch_tc<32, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
+        case 64: return launch_tc<64, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
+        case 128: return launch_tc<128, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
+        case 192: return launch_tc<192, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
+        case 256: return launch_tc<256, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
 template <bool BF16, int CG>
-static cudaError_t launch_tc_sw(int sw, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                                const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
+static cudaError_t launch_tc_sw(int sw, int bn, const TcMaps& m, const TcParams& prm, size_t smem, int grid,
+                                cudaStream_t st) {
     switch (sw) {
-        case 128: return launch_tc_bn<BF16, CG, 4>(bn, ta, tb, prm, smem, grid, st);
-        case 64: return launch_tc_bn<BF16, CG, 2>(bn, ta, tb, prm, smem, grid, st);
-        case 32: return launch_tc_bn<BF16, CG, 1>(bn, ta, tb, prm, smem, grid, st);
+        case 128: return launch_tc_bn<BF16, CG, 4>(bn, m, prm, smem, grid, st);
+        case 64: return launch_tc_bn<BF16, CG, 2>(bn, m, prm, smem, grid, st);
+        case 32: return launch_tc_bn<BF16, CG, 1>(bn, m, prm, smem, grid, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool bf16,
-                   const float* in, const float* ker, float* out, void* in_ws, void* ker_ws,
-                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err) {
-    const void* ws = in_ws;   // tensor-map cache key
+static CUtensorMapSwizzle swizzle_for(int bytes) {
+    return bytes >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
 
-    // Tensor maps depend on the workspace address, known only here; they are
-    // encoded on first use and cached per (workspace, problem, tile).
-    struct Key {
-        const void* ws; const void* kws; Problem pb; int bn; int cg; int kbs; int bf16; int dev;  // (fuse does not change the maps)
-    };
-    struct Entry { Key k; CUtensorMap ta, tb; };
-    static std::mutex mu;
-    static Entry cache[16];
-    static int n_cached = 0, next_slot = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const Key key{ws, ker_ws, pb, t.bn, t.cg, t.kbs, bf16 ? 1 : 0, dev};
-    auto same = [&](const Key& a) {
-        return a.ws == key.ws && a.kws == key.kws && memcmp(&a.pb, &key.pb, sizeof(Problem)) == 0 && a.bn == key.bn && a.cg == key.cg && a.kbs == key.kbs &&
-               a.bf16 == key.bf16 && a.dev == key.dev;
-    };
-    CUtensorMap ta, tb;
-    bool hit = false;
-    {
-        std::lock_guard<std::mutex> g(mu);
-        for (int i = 0; i < n_cached; ++i)
-            if (same(cache[i].k)) { ta = cache[i].ta; tb = cache[i].tb; hit = true; break; }
-    }
-    if (!hit) {
+static cudaError_t encode_maps(const Problem& pb, const TcLayout& L, const TcTile& t, bool bf16, const float* in,
+                               void* in_ws, void* ker_ws, TcMaps& m, std::string& err) {
     const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    const CUtensorMapSwizzle swz = L.sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                   : (L.sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    const CUtensorMapSwizzle swz = swizzle_for(L.sw);
     {
         // In NHWC: dims (C, W, H, N) innermost first.
         cuuint64_t dims[4] = {(cuuint64_t)L.Cp, (cuuint64_t)pb.Win(), (cuuint64_t)pb.Hin(), (cuuint64_t)pb.N};
@@ -602,7 +887,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         int lower[2] = {0, 0};
         int upper[2] = {-(pb.S - 1), -(pb.R - 1)};
         cuuint32_t estr[4] = {1, 1, 1, 1};
-        CUresult r = g_encode_im2col(&ta, dt, 4, in_ws, dims, strides, lower, upper, (cuuint32_t)L.bkc,
+        CUresult r = g_encode_im2col(&m.a, dt, 4, in_ws, dims, strides, lower, upper, (cuuint32_t)L.bkc,
                                      (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
@@ -613,21 +898,90 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         cuuint64_t strides[1] = {(cuuint64_t)pb.R * pb.S * L.Cp * L.elem};
         cuuint32_t box[2] = {(cuuint32_t)L.bkc, (cuuint32_t)(t.bn / t.cg)};
         cuuint32_t estr[2] = {1, 1};
-        CUresult r = g_encode_tiled(&tb, dt, 2, ker_ws, dims, strides, box, estr,
+        CUresult r = g_encode_tiled(&m.b, dt, 2, ker_ws, dims, strides, box, estr,
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
     }
-    std::lock_guard<std::mutex> g(mu);
-    cache[next_slot] = Entry{key, ta, tb};
-    next_slot = (next_slot + 1) % 16;
-    if (n_cached < 16) ++n_cached;
+    if (!t.fuse) {
+        m.src = m.a;
+        m.dst = m.b;
+        return cudaSuccess;
+    }
+    const int64_t P = pb.Hin() * pb.Win();
+    {
+        // In NCHW fp32 as {P, C, N}; box = 64 pixels x cc channels; channels
+        // >= C and pixels >= P are zero-filled (that is the Cp padding).
+        cuuint64_t dims[3] = {(cuuint64_t)P, (cuuint64_t)pb.C, (cuuint64_t)pb.N};
+        cuuint64_t strides[2] = {(cuuint64_t)P * 4, (cuuint64_t)P * 4 * pb.C};
+        cuuint32_t box[3] = {64, (cuuint32_t)L.cc, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = g_encode_tiled(&m.src, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeTiled (In NCHW) failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
+    }
+    {
+        // workspace NHWC as {Cp, P, N}; box = cc channels x 64 pixels, swizzled
+        // like the staging tile; stores past the image's last pixel are clipped
+        cuuint64_t dims[3] = {(cuuint64_t)L.Cp, (cuuint64_t)P, (cuuint64_t)pb.N};
+        cuuint64_t strides[2] = {(cuuint64_t)L.Cp * L.elem, (cuuint64_t)L.Cp * L.elem * P};
+        cuuint32_t box[3] = {(cuuint32_t)L.cc, 64, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        CUresult r = g_encode_tiled(&m.dst, dt, 3, in_ws, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    swizzle_for(L.cc * L.elem), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeTiled (NHWC store) failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
+    }
+    return cudaSuccess;
+}
+
+cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool bf16,
+                   const float* in, const float* ker, float* out, void* in_ws, void* ker_ws, void* flag_ws,
+                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err) {
+    if (t.fuse && (!L.coop_ok || !flag_ws)) { err = "fused transform needs a TMA-legal NCHW plane and flag workspace"; return cudaErrorInvalidValue; }
+    // Tensor maps depend on the workspace (and, fused, In) addresses, known
+    // only here; they are encoded on first use and cached.
+    struct Key {
+        const void* ws; const void* kws; const void* in; Problem pb; int bn; int cg; int kbs; int bf16; int fuse; int dev;
+    };
+    struct Entry { Key k; TcMaps m; };
+    static std::mutex mu;
+    static Entry cache[32];
+    static int n_cached = 0, next_slot = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const Key key{in_ws, ker_ws, t.fuse ? (const void*)in : nullptr, pb, t.bn, t.cg, t.kbs, bf16 ? 1 : 0, t.fuse, dev};
+    auto same = [&](const Key& a) {
+        return a.ws == key.ws && a.kws == key.kws && a.in == key.in && memcmp(&a.pb, &key.pb, sizeof(Problem)) == 0 &&
+               a.bn == key.bn && a.cg == key.cg && a.kbs == key.kbs && a.bf16 == key.bf16 && a.fuse == key.fuse &&
+               a.dev == key.dev;
+    };
+    TcMaps maps;
+    bool hit = false;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (int i = 0; i < n_cached; ++i)
+            if (same(cache[i].k)) { maps = cache[i].m; hit = true; break; }
+    }
+    if (!hit) {
+        cudaError_t e = encode_maps(pb, L, t, bf16, in, in_ws, ker_ws, maps, err);
+        if (e != cudaSuccess) return e;
+        std::lock_guard<std::mutex> g(mu);
+        cache[next_slot] = Entry{key, maps};
+        next_slot = (next_slot + 1) % 32;
+        if (n_cached < 32) ++n_cached;
     }
 
-    cudaError_t e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse);
+    int* flags = t.fuse ? static_cast<int*>(flag_ws) + 32 : nullptr;
+    const int n_flags = t.fuse ? (int)(pb.N * L.npch * L.nch) : 0;
+    cudaError_t e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse,
+                                  t.fuse ? static_cast<int*>(flag_ws) : nullptr, t.fuse ? 32 + n_flags : 0);
     if (e != cudaSuccess) { err = "repack launch failed"; return e; }
 
     TcParams prm;
+    memset(&prm, 0, sizeof(prm));
     prm.out = out;
     prm.M = (int)pb.M();
     prm.HW = pb.H * pb.W;
@@ -645,16 +999,10 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         return e ? (uint32_t)atoi(e) : 0u;
     }();
     prm.debug = debug_mode;
-    prm.fuse = t.fuse;
     static const int env_order = [] { const char* e = getenv("CONV_KORDER"); return e ? atoi(e) : -1; }();
     // One order for every configuration (fused or not), so results are
     // bit-identical across tilings (P10); env CONV_KORDER=1 is for experiments.
     prm.tap_outer = t.fuse ? 0 : (env_order >= 0 ? env_order : 0);
-    prm.in = in;
-    prm.in_ws = in_ws;
-    prm.C = pb.C;
-    prm.Hin = (int)pb.Hin();
-    prm.Win = (int)pb.Win();
     static const char* trace_path = getenv("CONV_TRACE");
     static unsigned long long* trace_buf = nullptr;
     prm.trace = nullptr;
@@ -674,13 +1022,49 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     const int units = num_sms / t.cg;
     const int grid = (prm.num_tiles < units ? prm.num_tiles : units) * t.cg;
     const size_t smem = tc_smem_bytes(L, t);
+    prm.fuse = t.fuse;
+    if (t.fuse) {
+        prm.flags = flags;
+        prm.in = in;
+        prm.in_ws = in_ws;
+        prm.C = pb.C;
+        prm.P = (int)(pb.Hin() * pb.Win());
+        prm.Win = (int)pb.Win();
+        prm.npch = (int)L.npch;
+        prm.cc = L.cc;
+        prm.nch = L.nch;
+        prm.hh = L.hh;
+        const int nunits = grid / t.cg;
+        const int n_waves = (prm.num_tiles + nunits - 1) / nunits;
+        prm.total_chunks = n_flags;
+        prm.hh_log2 = L.hh == 2 ? 1 : 0;
+        // group boundaries: the end (+1) of the input chunk-pixel range the
+        // tiles of waves 0..w read; with more than 32 waves, consecutive
+        // waves are merged (the order is a schedule heuristic only)
+        const int per = (n_waves + 31) / 32;
+        prm.n_groups = 0;
+        for (int w = per - 1;; w += per) {
+            const int wl = w < n_waves ? w : n_waves - 1;
+            const int last_tile = std::min((wl + 1) * nunits, prm.num_tiles) - 1;
+            const int m_tile = last_tile / prm.num_n_tiles;
+            const int m1 = (int)std::min<int64_t>((int64_t)(m_tile + 1) * tile_m, pb.M()) - 1;
+            const int n = m1 / prm.HW;
+            const int h = (m1 - n * prm.HW) / prm.W;
+            int e = n * (int)L.npch + (int)(((h + pb.R - 1) * pb.Win() + pb.Win() - 1) / 64) + 1;
+            if (prm.n_groups > 0 && e < prm.gend[prm.n_groups - 1]) e = prm.gend[prm.n_groups - 1];
+            prm.gend[prm.n_groups++] = e;
+            if (wl == n_waves - 1) break;
+        }
+        prm.tnb = t.tnb;
+        prm.tr_off = (uint32_t)((tc_pipe_bytes(L, t) + 1023) / 1024 * 1024);
+    }
     if (prm.k_iters % t.kbs != 0) { err = "k-blocks per stage must divide R*S*c-blocks"; return cudaErrorInvalidValue; }
     if (t.cg == 2)
-        e = bf16 ? launch_tc_sw<true, 2>(L.sw, t.bn, ta, tb, prm, smem, grid, st)
-                 : launch_tc_sw<false, 2>(L.sw, t.bn, ta, tb, prm, smem, grid, st);
+        e = bf16 ? launch_tc_sw<true, 2>(L.sw, t.bn, maps, prm, smem, grid, st)
+                 : launch_tc_sw<false, 2>(L.sw, t.bn, maps, prm, smem, grid, st);
     else
-        e = bf16 ? launch_tc_sw<true, 1>(L.sw, t.bn, ta, tb, prm, smem, grid, st)
-                 : launch_tc_sw<false, 1>(L.sw, t.bn, ta, tb, prm, smem, grid, st);
+        e = bf16 ? launch_tc_sw<true, 1>(L.sw, t.bn, maps, prm, smem, grid, st)
+                 : launch_tc_sw<false, 1>(L.sw, t.bn, maps, prm, smem, grid, st);
     if (e != cudaSuccess) { err = std::string("tcgen05 kernel launch failed: ") + cudaGetErrorString(e); return e; }
     if (ev) cudaEventRecord(ev[2], st);
     if (prm.trace) {
@@ -688,7 +1072,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         cudaStreamSynchronize(st);
         cudaMemcpy(host, prm.trace, sizeof(host), cudaMemcpyDeviceToHost);
         if (FILE* f = fopen(trace_path, "wb")) {
-            fwrite(host, sizeof(unsigned long long), (size_t)grid * 64, f);
+            fwrite(host, sizeof(unsigned long long), (size_t)1024 * 64, f);   // rows 512+: transform detail
             fclose(f);
         }
     }

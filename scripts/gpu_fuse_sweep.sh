@@ -1,0 +1,7 @@
+#!/bin/bash
+# fused vs separate In transform on every BASELINE config (step time, graph replay, cold L2)
+cd "$(dirname "$0")/.."
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -3
+for c in r2 pw det batched; do for p in bf16 tf32; do for t in fuse=0 fuse=1; do
+  timeout 300 python bench.py --config $c --path $p --tile $t --steps 30 --warmup 5 --soak 0.2 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c $p $t', 'step_us', round(d['ms_per_step']*1e3,2), 'kernels_us', [round(x*1e3,2) for x in d['roofline']['kernel_ms_each']], d['config']['tile'])" || echo "$c $p $t FAILED"
+done; done; done

@@ -19,6 +19,8 @@ print(p.describe()['tile'])
 """
 subprocess.run([sys.executable, "-c", code], env=env, check=True)
 t = np.fromfile(out, dtype=np.uint64).reshape(-1, 64).astype(np.int64)
+t2all = t[512:]
+t = t[:512]
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 print(f"CTAs traced: {len(t)}")
@@ -40,3 +42,18 @@ print(f"producer empty-wait med {np.median(t[:,60])/1e3:.1f}kcyc, producer end m
 n = max(ntiles)
 last = np.max(t[:, 41 + 2 * (n - 1)] - t0)
 print(f"last epilogue end {last/1e3:.2f}us; first start spread {(t[:,0].max()-t0)/1e3:.2f}us")
+# fused transform (all CTAs, both ranks of a pair): slots 33-39, 56-58
+a = np.fromfile(out, dtype=np.uint64).reshape(-1, 64).astype(np.int64)[:512]
+f = a[a[:, 58] > 0]
+f2 = t2all[:len(a)][a[:, 58] > 0]
+if len(f):
+    print(f"transform CTAs {len(f)}: chunks/CTA med {np.median(f[:,33]):.0f} (min {f[:,33].min()}, max {f[:,33].max()})")
+    print(f"  start spread {(f[:,58].max()-f[:,58].min())/1e3:.2f}us, end med {np.median(f[:,38]-t0)/1e3:.2f}us max {np.max(f[:,38]-t0)/1e3:.2f}us")
+    for k, name in ((34, "storer: wait converted"), (35, "storer: wait_read"), (36, "storer: bulk_wait lag"), (37, "storer: wait decoded")):
+        print(f"  {name:30s} med {np.median(f[:,k])/1e3:8.1f} kcyc  max {f[:,k].max()/1e3:8.1f} kcyc")
+    f2 = t2all[:len(a)][a[:, 58] > 0]
+    for k, name in ((3, "decode 0,1 done"), (4, "first load issued"), (0, "chunk 0 converted"), (1, "first done report"), (2, "first publish")):
+        print(f"  {name:26s} med {np.median(f2[:,k]-t0)/1e3:8.2f} us  max {np.max(f2[:,k]-t0)/1e3:8.2f} us")
+    g = a[a[:, 56] > 0]
+    print(f"  watcher sleep med {np.median(g[:,39])/1e3:.1f} kcyc, first unit ready med {np.median(g[:,56]-t0)/1e3:.2f}us")
+    print(f"  producer ready-wait med {np.median(g[:,57])/1e3:.1f} kcyc max {g[:,57].max()/1e3:.1f}")

@@ -26,6 +26,12 @@ def rel_l2(got, ref):
     return d / n if n else d
 
 
+def coop_ok(sh):
+    """The fused (cooperative) In transform TMA-loads NCHW planes: their byte
+    size must be a multiple of 16."""
+    return ((sh.H + sh.R - 1) * (sh.W + sh.S - 1)) % 4 == 0
+
+
 def run(shape, inp, ker, path, tile=None):
     plan = conv.ConvPlan(*shape.as_tuple(), path=path, tile=tile)
     out = plan.run(inp.cuda(), ker.cuda())
@@ -74,9 +80,15 @@ def test_integer_twin_bit_exact(path, shape):
 @pytest.mark.parametrize("shape", SMALL + ODD, ids=lambda s: "x".join(map(str, s.as_tuple())))
 def test_tensor_cta_group_variants(path, cg, fuse, shape):
     """Both the 1-CTA (M=128) and the CTA-pair (M=256) kernels, with the In
-    transform as a separate launch (fuse=0) or inside the kernel (fuse=1)."""
+    transform as a separate launch (fuse=0) or inside the kernel (fuse=1,
+    cooperative chunk transform; needs a TMA-legal NCHW plane)."""
     spec = f"cg={cg},fuse={fuse}"
     inp, ker = make_inputs(shape, seed=1, kind="int")
+    if fuse and not coop_ok(shape):
+        with pytest.raises(conv.ConvError) as e:
+            run(shape, inp, ker, path, tile=spec)
+        assert e.value.status == conv.CONV_ERR_INFEASIBLE
+        return
     got, plan = run(shape, inp, ker, path, tile=spec)
     assert plan.describe()["tile"]["cg"] == cg and plan.describe()["tile"]["fuse"] == fuse
     ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
@@ -263,3 +275,61 @@ def test_run_host_pipelined_chunks_bit_identical(path):
         assert np.array_equal(out_h.numpy(), dev_out.cpu().numpy())
     ref = oracle.conv_eq1(inp.numpy()[:2], ker.numpy())
     assert rel_l2(out_h.numpy()[:2], ref) <= TOL[path]
+
+
+FUSE_SHAPES = [CONFIGS["tiny"], CONFIGS["r2"], CONFIGS["pw"], CONFIGS["det"],
+               Shape(N=5, K=64, C=40, H=6, W=2, R=3, S=3), Shape(N=2, K=40, C=70, H=8, W=10, R=1, S=1),
+               Shape(N=7, K=96, C=200, H=10, W=14, R=3, S=3), Shape(N=3, K=32, C=16, H=62, W=30, R=3, S=3)]
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", FUSE_SHAPES, ids=lambda s: "x".join(map(str, s.as_tuple())))
+def test_fused_transform_bit_identical_to_separate(path, shape):
+    """The cooperative in-kernel transform produces the same workspace values
+    (same rounding) and the main kernel the same k-order, so fuse=1 equals
+    fuse=0 bit for bit; repeated runs of one plan (flags cleared by the Ker
+    launch each time) keep matching when the inputs change."""
+    assert coop_ok(shape), shape
+    for cg in (1, 2):
+        fused = conv.ConvPlan(*shape.as_tuple(), path=path, tile=f"cg={cg},fuse=1")
+        assert fused.describe()["tile"]["fuse"] == 1
+        sep = conv.ConvPlan(*shape.as_tuple(), path=path, tile=f"cg={cg},fuse=0")
+        out = fused.new_output()
+        ws = fused.new_workspace()
+        for seed in (21, 22, 23):
+            inp, ker = make_inputs(shape, seed=seed)
+            i, k = inp.cuda(), ker.cuda()
+            fused.run(i, k, out, ws)
+            ref = sep.run(i, k)
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref)
+        ref64 = oracle.conv_eq1(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()))
+        assert rel_l2(out.cpu().numpy(), ref64) <= 1e-5
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_fused_transform_cuda_graph_replay(path):
+    """The bench replays conv_run from a CUDA graph: the chunk flags must be
+    re-cleared inside the graph (by the Ker launch), so a replay with new
+    input values recomputes everything."""
+    sh = Shape(N=6, K=128, C=128, H=14, W=14, R=3, S=3)
+    plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=1")
+    inp, ker = make_inputs(sh, seed=31)
+    i, k = inp.cuda(), ker.cuda()
+    out, ws = plan.new_output(), plan.new_workspace()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.run(i, k, out, ws)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.run(i, k, out, ws, stream=s)
+    for seed in (32, 33):
+        inp2, ker2 = make_inputs(sh, seed=seed)
+        i.copy_(inp2)
+        k.copy_(ker2)
+        g.replay()
+        torch.cuda.synchronize()
+        ref = oracle.conv_eq1(ROUND[path](inp2.numpy()), ROUND[path](ker2.numpy()))
+        assert rel_l2(out.cpu().numpy(), ref) <= 1e-5
