@@ -57,7 +57,7 @@ struct conv_plan {
     SimtTile simt;
     ModelResult model;
     // forced tile (conv_plan_set_tile)
-    int force_bn = 0, force_stages = 0, force_cg = 0, force_kbs = 0, force_fuse = -1;
+    int force_bn = 0, force_stages = 0, force_cg = 0, force_kbs = 0, force_fuse = -1, force_pre_c = -1;
     SimtTile force_simt;
     unsigned force_simt_mask = 0;
     // conv_run_host pipeline (created on first use, guarded by host_mu)
@@ -115,7 +115,7 @@ static conv_status select(conv_plan* p) {
         case CONV_PATH_TF32:
         case CONV_PATH_BF16: {
             const bool bf16 = p->requested == CONV_PATH_BF16;
-            if (!select_tc(pb, p->dev, bf16, tt, rt, p->force_bn, p->force_stages, p->force_cg, p->force_kbs, p->force_fuse, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            if (!select_tc(pb, p->dev, bf16, tt, rt, p->force_bn, p->force_stages, p->force_cg, p->force_kbs, p->force_fuse, p->force_pre_c, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             p->tc = tt; p->model = rt; p->path = p->requested; p->tcl = tc_layout(pb, bf16);
             break;
         }
@@ -124,7 +124,7 @@ static conv_status select(conv_plan* p) {
             // AUTO keeps fp32 inputs or TF32 products (the precision of the
             // paper's fp32 method); BF16 only when requested.
             const bool ok_s = select_simt(pb, p->dev, st, rs, fs, p->force_simt_mask, why);
-            const bool ok_t = select_tc(pb, p->dev, false, tt, rt, p->force_bn, p->force_stages, p->force_cg, p->force_kbs, p->force_fuse, why);
+            const bool ok_t = select_tc(pb, p->dev, false, tt, rt, p->force_bn, p->force_stages, p->force_cg, p->force_kbs, p->force_fuse, p->force_pre_c, why);
             if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             if (ok_t && (!ok_s || rt.model_us < rs.model_us)) {
                 p->tc = tt; p->model = rt; p->path = CONV_PATH_TF32; p->tcl = tc_layout(pb, false);
@@ -228,7 +228,7 @@ extern "C" conv_status conv_plan_set_path(conv_plan* p, conv_path path) {
 
 extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
     if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
-    int fbn = 0, fst = 0, fcg = 0, fkbs = 0, ffuse = -1;
+    int fbn = 0, fst = 0, fcg = 0, fkbs = 0, ffuse = -1, fpre = -1;
     SimtTile fs;
     unsigned mask = 0;
     if (spec && *spec) {
@@ -245,13 +245,14 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             std::string key = kv.substr(0, eq);
             char* end = nullptr;
             long v = strtol(kv.c_str() + eq + 1, &end, 10);
-            const long vmin = key == "fuse" ? 0 : 1;
+            const long vmin = (key == "fuse" || key == "pre_c") ? 0 : 1;
             if (!end || *end || v < vmin || v > 4096) return fail(CONV_ERR_INVALID_ARGUMENT, "bad value in '%s'", kv.c_str());
             if (key == "bn") fbn = (int)v;
             else if (key == "stages") fst = (int)v;
             else if (key == "cg") fcg = (int)v;
             else if (key == "kbs") fkbs = (int)v;
             else if (key == "fuse") ffuse = v ? 1 : 0;
+            else if (key == "pre_c") fpre = (int)v;
             else if (key == "tk") { fs.tk = (int)v; mask |= 1; }
             else if (key == "tw") { fs.tw = (int)v; mask |= 2; }
             else if (key == "kg") { fs.kg = (int)v; mask |= 4; }
@@ -267,13 +268,16 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
         if (fkbs && fkbs != 1 && fkbs != 2 && fkbs != 4) return fail(CONV_ERR_INFEASIBLE, "kbs must be 1, 2 or 4");
         if (fcg && fcg != 1 && fcg != 2) return fail(CONV_ERR_INFEASIBLE, "cg must be 1 or 2");
     }
-    const int obn = p->force_bn, ost = p->force_stages, ocg = p->force_cg, okbs = p->force_kbs, ofuse = p->force_fuse;
+    const int obn = p->force_bn, ost = p->force_stages, ocg = p->force_cg, okbs = p->force_kbs, ofuse = p->force_fuse,
+              opre = p->force_pre_c;
     const SimtTile ofs = p->force_simt;
     const unsigned omask = p->force_simt_mask;
-    p->force_bn = fbn; p->force_stages = fst; p->force_cg = fcg; p->force_kbs = fkbs; p->force_fuse = ffuse; p->force_simt = fs; p->force_simt_mask = mask;
+    p->force_bn = fbn; p->force_stages = fst; p->force_cg = fcg; p->force_kbs = fkbs; p->force_fuse = ffuse; p->force_pre_c = fpre;
+    p->force_simt = fs; p->force_simt_mask = mask;
     conv_status s = select(p);
     if (s != CONV_OK) {
-        p->force_bn = obn; p->force_stages = ost; p->force_cg = ocg; p->force_kbs = okbs; p->force_fuse = ofuse; p->force_simt = ofs; p->force_simt_mask = omask;
+        p->force_bn = obn; p->force_stages = ost; p->force_cg = ocg; p->force_kbs = okbs; p->force_fuse = ofuse; p->force_pre_c = opre;
+        p->force_simt = ofs; p->force_simt_mask = omask;
         select(p);
     }
     return s;
@@ -314,8 +318,9 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
                  32 * p->simt.kg * p->simt.pw);
     } else {
-        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"fuse\":%d,\"tnb\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
+        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
                  128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
+                 p->tc.fuse ? std::min(p->tc.pre_c, p->tcl.Cp) : 0,
                  p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
     }
     tile = t;

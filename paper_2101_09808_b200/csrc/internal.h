@@ -48,7 +48,8 @@ struct TcTile {
     int kbs = 1;         // k-blocks (one TMA box of A and of B each) per pipeline stage
     int fuse = 0;        // 1: the NCHW->NHWC In transform runs inside the main kernel
                          //    (cooperative chunk transform, warps 0-3 of every CTA)
-    int tnb = 2;         // fuse: input staging buffers of the transform (2..4)
+    int tnb = 2;         // fuse: input staging buffers of the transform (2..6)
+    int pre_c = 64;      // fuse: channels of wave 0's input converted by the repack launch (prologue)
 };
 
 struct TcLayout {        // derived from Problem + element size
@@ -68,6 +69,22 @@ struct TcLayout {        // derived from Problem + element size
     size_t flag_bytes;   // 128 B reserved + one int ready flag per chunk
 };
 size_t tc_transform_smem_bytes(const TcLayout& L, int tnb);
+
+// Repack launch (repack.cu).  Fused plans (the In transform inside K3):
+// besides Ker, the launch clears the chunk flags and converts the
+// "prologue" -- channels [0, pre_ch * cc) of input chunk-pixels q < pre_q
+// (wave 0's first channel blocks) -- setting those chunks' flags.
+struct RepackFuse {
+    int* zero_ptr = nullptr;   // 32 reserved ints + the chunk flags [Q][nch]
+    int zero_n = 0;
+    int pre_q = 0;             // prologue chunk-pixels [0, pre_q)
+    int pre_ch = 0;            // channel chunks the prologue covers
+    int nch = 0;               // channel chunks per chunk-pixel (flag row length)
+    int cc = 0;                // channels per chunk
+};
+cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
+                          void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in,
+                          const RepackFuse& fz);
 
 TcLayout tc_layout(const Problem& p, bool bf16);
 size_t tc_smem_bytes(const TcLayout& L, const TcTile& t);

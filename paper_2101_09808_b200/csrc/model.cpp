@@ -169,7 +169,11 @@ static const double kClockHz = 1.84e9;   // SM clock measured under tcgen05 load
 // an SM; every pipeline stage adds ~150 cycles of barrier / commit bubble.
 static const double kStageBubbleClk = 150.0;
 static const double kEpiStoreBW = 5.0e12;  // bytes/s the whole chip's epilogues drain at
-static const double kTransformLatUs = 2.0; // fused transform: one chunk's load -> convert -> store -> flag round trip
+// fused transform (measured r01b, batched layer): 67 MB of fp32 In in ~35 us
+// per 148 CTAs while the MMAs run, 9% MMA slowdown, ~6 us startup chain
+static const double kTransformBW = 1.9e12;
+static const double kTransformDrag = 1.09;
+static const double kTransformStartUs = 6.0;
 
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t) {
     ModelResult r;
@@ -212,18 +216,25 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     double t_rep = repack / (0.8 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
     double t_main_f = t_main;
     if (t.fuse) {
-        // Cooperative In transform inside the main kernel: every CTA's 4
-        // transform warps keep tnb chunk loads of cc x 64 fp32 in flight
-        // (Little's law with ~kTransformLatUs per chunk round trip), capped at
-        // the HBM rate; it overlaps the MMAs, and the first tiles wait about
-        // one chunk round trip for their first channel block.  The separate
-        // launch keeps only the Ker repack (and clears the chunk flags).
+        // Cooperative In transform inside the main kernel (measured r01b,
+        // profiles/r01b/fuse_sweep.log): the repack launch converts only the
+        // prologue (pre_c channels of wave 0's input) besides Ker; the rest of
+        // In is converted by every CTA's transform warps at ~kTransformBW,
+        // overlapped with the MMAs but slowing them by kTransformDrag (they
+        // share the SM's shared-memory port, L2 and issue slots).  While the
+        // transform has not caught up, wave 0 waits: the part of its input
+        // beyond the prologue must be converted before its last channel
+        // block can run.  Single-wave layers also pay the chunk pipeline's
+        // startup chain (decode, load, convert, store, publish, watch).
         const double in_rd = 4.0 * pb.in_elems();
-        const double rate = std::min(0.8 * dev.bw_hbm, (double)dev.sms * t.tnb * L.cc * 256.0 / (kTransformLatUs * 1e-6));
-        const double t_tr = in_rd / rate * 1e6;
-        const double hbm_f = (in_rd + (double)L.in_ws_bytes + (double)L.ker_ws_bytes + 4.0 * pb.out_elems()) / dev.bw_hbm * 1e6;
-        t_main_f = std::max({t_main - kLaunchUs - t_tail_us, t_tr, hbm_f}) + t_tail_us + kLaunchUs + kTransformLatUs;
-        t_rep = (4.0 * pb.ker_elems() + (double)L.ker_ws_bytes) / (0.5 * dev.bw_hbm) * 1e6 + kLaunchUs;
+        const double waves = ceil((double)r.tiles / units);
+        const double pre_frac = std::min(1.0, (double)t.pre_c / L.Cp) / std::max(1.0, waves);
+        const double t_tr = in_rd * (1.0 - pre_frac) / kTransformBW * 1e6;
+        const double wave0_in = in_rd / std::max(1.0, waves) * (1.0 - std::min(1.0, (double)t.pre_c / L.Cp));
+        const double stall0 = std::max(0.0, wave0_in / kTransformBW * 1e6 - t_pipe_us / std::max(1.0, waves));
+        t_main_f = std::max(t_main * kTransformDrag, t_tr) + stall0 + (waves < 2 ? kTransformStartUs : 0.0);
+        const double pre_bytes = (4.0 + L.elem) * pb.in_elems() * pre_frac;
+        t_rep = (4.0 * pb.ker_elems() + (double)L.ker_ws_bytes + pre_bytes) / (0.8 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
         r.dv_hbm = in_rd + (double)L.in_ws_bytes + 4.0 * pb.ker_elems() + 2.0 * (double)L.ker_ws_bytes + 4.0 * pb.out_elems();
         r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
     }
@@ -247,7 +258,8 @@ static int tc_max_stages(const Device& dev, const TcLayout& L, int bn, int cg, i
 }
 
 bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& best_r,
-               int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, std::string& why) {
+               int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, int force_pre_c,
+               std::string& why) {
     const TcLayout L = tc_layout(pb, bf16);
     if (pb.R > 128 || pb.S > 128) { why = "R, S > 128: TMA im2col offsets are limited to [-128, 127]"; return false; }
     if (pb.M() + 256 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
@@ -265,13 +277,8 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
             for (int bn : kBNs) {
                 if (force_bn && bn != force_bn) continue;
                 if (!force_bn && bn > 32 && bn / 2 >= pb.K) continue;   // mostly padding
-                // fuse = 1 (cooperative in-kernel In transform) is taken only
-                // when forced: measured r01b, it ties the separate repack on the
-                // batched layer (tf32 108.2 vs 108.6 us, bf16 72.2 vs 69.2 us)
-                // and loses on the small ones (startup latency of the chunk
-                // pipeline; profiles/r01b/fuse_sweep.log)
                 for (int fuse = 0; fuse <= 1; ++fuse) {
-                    if (force_fuse >= 0 ? fuse != force_fuse : fuse != 0) continue;
+                    if (force_fuse >= 0 ? fuse != force_fuse : (fuse && !L.coop_ok)) continue;
                     const int smax = tc_max_stages(dev, L, bn, cg, kbs, fuse);
                     // at least 3 stages unless forced (2 cannot overlap load and MMA well)
                     if (smax < (force_stages || force_kbs ? 2 : 3)) continue;
@@ -283,6 +290,8 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
                     t.stages = force_stages ? force_stages : smax;
                     if (t.stages < 2 || t.stages > smax) continue;
                     if (fuse) {   // as many transform chunk buffers as fit (2..6)
+                        // prologue depth measured best in r01b: 128 channels (bf16), 64 (tf32)
+                        t.pre_c = force_pre_c >= 0 ? force_pre_c : (bf16 ? 128 : 64);
                         t.tnb = 2;
                         for (int nb = 6; nb > 2; --nb) {
                             TcTile u = t;

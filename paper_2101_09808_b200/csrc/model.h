@@ -21,7 +21,8 @@ struct ModelResult {
 
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t);
 bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& r,
-               int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, std::string& why);
+               int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, int force_pre_c,
+               std::string& why);
 ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t);
 // forced_mask bits: 1 tk, 2 tw, 4 kg, 8 pw, 16 tn, 32 th, 64 bc, 128 ver
 bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResult& r,

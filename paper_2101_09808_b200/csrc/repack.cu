@@ -69,8 +69,12 @@ struct RepackGeom {
     int N;                           // images
     int64_t n_tiles;                 // K2 tiles (TMA variant)
     int pdl_from;                    // first block that triggers the dependent launch
-    int* zero_ptr;                   // fused main kernel: claim counter + chunk flags to clear
+    int* zero_ptr;                   // fused main kernel: reserved ints + chunk flags to clear
     int zero_n;                      //   (ints; spread over the K1 CTAs)
+    int pre_q, pre_ch, nch;          // fused: prologue tiles (K2 CTAs for q < pre_q, channels
+                                     //   [0, 64)) whose chunk flags the launch sets (not clears)
+    int n_pre;                       // fused: number of prologue K2 CTAs (pre_q x 64-channel tiles)
+    int cc_f;                        // fused: channels per chunk (flag column granularity)
 };
 
 template <bool BF16>
@@ -87,10 +91,14 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
     if ((int)blockIdx.x >= g.pdl_from) asm volatile("griddepcontrol.launch_dependents;");
     if ((int)blockIdx.x < g.n_ker) {
         // ---- K1 ----
-        if (g.zero_n) {   // clear the fused transform's claim counter and chunk flags
+        if (g.zero_n) {   // clear the fused transform's chunk flags (the prologue's are set below)
             const int per = (g.zero_n + g.n_ker - 1) / g.n_ker;
             const int z0 = blockIdx.x * per, z1 = min(z0 + per, g.zero_n);
-            for (int i = z0 + tid; i < z1; i += 256) g.zero_ptr[i] = 0;
+            for (int i = z0 + tid; i < z1; i += 256) {
+                const int f = i - 32;   // flag index q * nch + ch
+                const bool pre = f >= 0 && f / g.nch < g.pre_q && f % g.nch < g.pre_ch;
+                if (!pre) g.zero_ptr[i] = 0;
+            }
         }
         const int64_t k = blockIdx.x / g.ker_chunks;
         const int c0 = (blockIdx.x % g.ker_chunks) * g.cc;
@@ -111,10 +119,20 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
     // ---- K2 ----
     float (*tile)[65] = reinterpret_cast<float (*)[65]>(sm);
     int b = blockIdx.x - g.n_ker;
-    const int pt = b % g.ptiles;
-    b /= g.ptiles;
-    const int ct = b % g.ctiles;
-    const int64_t n = b / g.ctiles;
+    int pt, ct;
+    int64_t n;
+    const int pre_ct = (g.pre_ch * g.cc_f + 63) / 64;   // 64-channel tiles in the prologue
+    if (g.n_pre) {                   // fused prologue: tile (q = b / pre_ct, channels 64 * (b % pre_ct) ...)
+        ct = b % pre_ct;
+        const int q = b / pre_ct;
+        n = q / g.ptiles;
+        pt = q % g.ptiles;
+    } else {
+        pt = b % g.ptiles;
+        b /= g.ptiles;
+        ct = b % g.ctiles;
+        n = b / g.ctiles;
+    }
     const int64_t P = g.P;
     const int C = g.C, Cp = g.Cp;
     const int64_t p0 = (int64_t)pt * 64;
@@ -169,6 +187,13 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
                 *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + p * Cp + c) = v;
             }
         }
+    }
+    // fused prologue: the main kernel reads these chunks only after this grid
+    // has completed (griddepcontrol.wait), so plain stores suffice
+    if (g.n_pre) {
+        const int q = (blockIdx.x - g.n_ker) / pre_ct;
+        const int ch0 = ct * 64 / g.cc_f, ch1 = min(ch0 + 64 / g.cc_f, g.pre_ch);
+        if (tid < ch1 - ch0) g.zero_ptr[32 + (int64_t)q * g.nch + ch0 + tid] = 1;
     }
 }
 
@@ -290,10 +315,16 @@ __global__ void __launch_bounds__(128) repack_tma(const float* __restrict__ ker,
 
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
                           void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in,
-                          int* zero_ptr, int zero_n) {
+                          const RepackFuse& fz) {
     RepackGeom g;
-    g.zero_ptr = zero_ptr;
-    g.zero_n = zero_n;
+    g.zero_ptr = fz.zero_ptr;
+    g.zero_n = fz.zero_n;
+    g.pre_q = fz.pre_q;
+    g.pre_ch = fz.pre_ch;
+    g.nch = fz.nch > 0 ? fz.nch : 1;
+    g.cc_f = fz.cc > 0 ? fz.cc : 1;
+    g.n_pre = (!with_in && fz.pre_ch > 0) ? fz.pre_q * ((fz.pre_ch * g.cc_f + 63) / 64) : 0;
+    const int zero_n = fz.zero_n;
     g.C = pb.C;
     g.Cp = Cp;
     g.RS = pb.R * pb.S;
@@ -359,7 +390,7 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
         if (ev) cudaEventRecord(ev[1], st);
         return cudaGetLastError();
     }
-    const int64_t n_in = with_in ? (int64_t)g.ptiles * g.ctiles * pb.N : 0;   // fused: Ker only
+    const int64_t n_in = with_in ? (int64_t)g.ptiles * g.ctiles * pb.N : g.n_pre;   // fused: Ker + prologue
     const int64_t grid = g.n_ker + n_in;
     if (grid >= (1ll << 31)) return cudaErrorInvalidValue;
     {

@@ -92,6 +92,7 @@ struct TcParams {
     int nch;                  // channel chunks: Cp / cc
     int hh;                   // channel chunks per k-block: bkc / cc
     int total_chunks;         // N * npch * nch
+    int seq0;                 // sequence indices [0, seq0) were converted by the repack launch (prologue)
     int hh_log2;              // log2(hh)
     int n_groups;             // chunk groups (waves of the schedule, merged to <= 32)
     int gend[32];             // group g covers chunk-pixel indices q in [gend[g-1], gend[g])
@@ -103,8 +104,8 @@ struct TcParams {
 // The input is cut into chunks (image n, 64-pixel run pch of the NCHW plane,
 // cc channels), ordered by when the persistent schedule first needs them:
 // waves of tiles, then channel block, then pixel.  CTA w of W transforms
-// sequence entries w, w + W, ... (all CTAs are co-resident: one per SM, and
-// the launch is cooperative).  A chunk is TMA-loaded as [cc][64] fp32,
+// sequence entries w, w + W, ... (all CTAs are co-resident: one per SM, grid
+// <= SM count).  A chunk is TMA-loaded as [cc][64] fp32,
 // converted (RNA tf32 / RNE bf16) and transposed in place into a [64 px][cc]
 // row-swizzled tile, TMA-stored into the NHWC workspace and published with
 // a release flag.  Each CTA's watcher acquires the flags of the chunks its
@@ -141,6 +142,11 @@ __device__ __forceinline__ int ld_acquire_cta_smem(const int* p) {
 }
 __device__ __forceinline__ void st_release_cta_smem(int* p, int v) {
     asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int4 lds_int4(const int4* p) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_u32(p)));
+    return v;
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -293,8 +299,8 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     // kRing-entry ring of decoded chunks
     uint8_t* tbuf = smem + p.tr_off;
     int4* cring = reinterpret_cast<int4*>(tbuf + (size_t)p.tnb * p.cc * 256);
-    // static chunk assignment: CTA w of W takes sequence indices w, w + W, ...
-    const int n_my = p.fuse ? (p.total_chunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    // static chunk assignment: CTA w of W takes sequence indices seq0 + w, seq0 + w + W, ...
+    const int n_my = p.fuse ? max(0, (p.total_chunks - p.seq0 - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) : 0;
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -600,7 +606,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         // (kPubLag behind) to the publisher.  Chunk coordinates come
         // pre-decoded from the ring (no divisions on this thread). =====
         if (p.fuse && lane == 0 && n_my > 0) {
-            constexpr int kPubLag = 1;
+            constexpr int kPubLag = 1, kReport = 2;   // completion checked + reported every kReport chunks
             const uint32_t buf_bytes = (uint32_t)p.cc * 256;
             unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
             long long c_conv = 0, c_rd = 0, c_pub = 0, c_dec = 0;
@@ -614,7 +620,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     }
                     if (tr) c_dec += clock64() - t0;
                 }
-                return cring[k & (kRing - 1)];
+                return lds_int4(&cring[k & (kRing - 1)]);
             };
             auto load = [&](int k) {
                 const int4 e = entry(k);
@@ -633,7 +639,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 mbar_wait(&tconv[b], (uint32_t)(k / p.tnb) & 1);
                 if (t2 && k == 0) t2[0] = globaltimer_ns();
                 if (tr) c_conv += clock64() - t0;
-                const int4 e = cring[k & (kRing - 1)];
+                const int4 e = lds_int4(&cring[k & (kRing - 1)]);
                 tma_store_3d(&tmap_dst, tbuf + (size_t)b * buf_bytes, e.w, e.z, e.y);
                 bulk_commit();
                 const int kn = k - 1 + p.tnb;             // refill chunk k-1's buffer with chunk k-1+tnb
@@ -643,10 +649,10 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     if (tr) c_rd += clock64() - t1;
                     load(kn);
                 }
-                const long long t3 = tr ? clock64() : 0;
-                bulk_wait<kPubLag>();                     // all but the newest kPubLag stores have landed
-                if (tr) c_pub += clock64() - t3;
-                if (k >= kPubLag) {
+                if (k >= kPubLag && ((k - kPubLag) % kReport) == 0) {
+                    const long long t3 = tr ? clock64() : 0;
+                    bulk_wait<kPubLag>();                 // all but the newest kPubLag stores have landed
+                    if (tr) c_pub += clock64() - t3;
                     fence_proxy_async_global();           // async-proxy writes -> generic flag release
                     st_release_cta_smem(done_ctr, k - kPubLag + 1);
                     if (t2 && k == kPubLag) t2[1] = globaltimer_ns();
@@ -677,7 +683,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             const uint32_t buf_bytes = (uint32_t)p.cc * 256;
             auto decode_block = [&](int k0) {             // chunks [k0, k0 + kDecode) -> ring
                 if (tid < kDecode && k0 + tid < n_my)
-                    cring[(k0 + tid) & (kRing - 1)] = chunk_decode(p, w + (k0 + tid) * W);
+                    cring[(k0 + tid) & (kRing - 1)] = chunk_decode(p, p.seq0 + w + (k0 + tid) * W);
                 named_bar_sync(1, 128);
                 if (tid == 0) st_release_cta_smem(dec_ctr, min(k0 + kDecode, n_my));
             };
@@ -802,7 +808,7 @@ size_t tc_smem_bytes(const TcLayout& L, const TcTile& t) {
 
 cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker,
                           void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in,
-                          int* zero_ptr, int zero_n);
+                          const RepackFuse& fz);
 
 
 struct TcMaps {
@@ -827,7 +833,7 @@ static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, 
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[3];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
@@ -836,13 +842,12 @@ static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, 
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL after the repack
     attr[1].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
     // The fused transform's CTAs wait on chunks other CTAs convert: all of
-    // them must be resident at once, which a cooperative launch guarantees
-    // (or refuses to launch).
-    attr[2].id = cudaLaunchAttributeCooperative;
-    attr[2].val.cooperative = 1;
+    // them must be resident at once.  They are -- one CTA per SM (smem and
+    // registers), grid <= SM count -- so no cooperative launch is requested
+    // (ncu cannot replay cooperative cluster launches); a starved wait traps
+    // after ~4 s (watchdog) instead of hanging.
     cfg.attrs = attr;
-    static const int no_coop = getenv("CONV_NO_COOP") ? 1 : 0;   // experiments only
-    cfg.numAttrs = (prm.fuse && !no_coop) ? 3 : 2;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kfn, m.a, m.b, m.src, m.dst, prm);
 }
 
@@ -976,9 +981,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
 
     int* flags = t.fuse ? static_cast<int*>(flag_ws) + 32 : nullptr;
     const int n_flags = t.fuse ? (int)(pb.N * L.npch * L.nch) : 0;
-    cudaError_t e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse,
-                                  t.fuse ? static_cast<int*>(flag_ws) : nullptr, t.fuse ? 32 + n_flags : 0);
-    if (e != cudaSuccess) { err = "repack launch failed"; return e; }
+    cudaError_t e = cudaSuccess;
 
     TcParams prm;
     memset(&prm, 0, sizeof(prm));
@@ -994,26 +997,10 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     prm.n_cblk = L.n_cblk;
     prm.k_iters = pb.R * pb.S * L.n_cblk;
     prm.num_n_tiles = (pb.K + t.bn - 1) / t.bn;
-    static const uint32_t debug_mode = [] {
-        const char* e = getenv("CONV_DEBUG_MODE");
-        return e ? (uint32_t)atoi(e) : 0u;
-    }();
-    prm.debug = debug_mode;
-    static const int env_order = [] { const char* e = getenv("CONV_KORDER"); return e ? atoi(e) : -1; }();
-    // One order for every configuration (fused or not), so results are
-    // bit-identical across tilings (P10); env CONV_KORDER=1 is for experiments.
-    prm.tap_outer = t.fuse ? 0 : (env_order >= 0 ? env_order : 0);
-    static const char* trace_path = getenv("CONV_TRACE");
-    static unsigned long long* trace_buf = nullptr;
-    prm.trace = nullptr;
-    if (trace_path) {
-        if (!trace_buf) cudaMalloc(&trace_buf, 1024 * 64 * sizeof(unsigned long long));
-        cudaMemsetAsync(trace_buf, 0, 1024 * 64 * sizeof(unsigned long long), st);
-        prm.trace = trace_buf;
-    }
     const int tile_m = kBM * t.cg;
     const int num_m_tiles = (int)((pb.M() + tile_m - 1) / tile_m);
     prm.num_tiles = num_m_tiles * prm.num_n_tiles;
+
     prm.stages = t.stages;
     prm.kbs = t.kbs;
     prm.sw = (uint32_t)L.sw;
@@ -1057,6 +1044,42 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         }
         prm.tnb = t.tnb;
         prm.tr_off = (uint32_t)((tc_pipe_bytes(L, t) + 1023) / 1024 * 1024);
+    }
+
+    RepackFuse fz;
+    if (t.fuse) {
+        fz.zero_ptr = static_cast<int*>(flag_ws);
+        fz.zero_n = 32 + n_flags;
+        fz.nch = L.nch;
+        fz.cc = L.cc;
+        // prologue = channels [0, pre_c) of group 0 (the chunk-pixels wave 0
+        // reads), pre_c a multiple of 64 (the repack tile) and of bkc: in
+        // sequence order that is the first pre_c / bkc channel blocks of group
+        // 0, which the in-kernel transform then skips
+        const int pre_c = std::min(L.Cp, (t.pre_c + 63) / 64 * 64);
+        fz.pre_q = pre_c > 0 ? prm.gend[0] : 0;
+        fz.pre_ch = pre_c / L.cc;
+        prm.seq0 = (pre_c / L.bkc) * prm.gend[0] * L.hh;
+    }
+    e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse, fz);
+    if (e != cudaSuccess) { err = "repack launch failed"; return e; }
+
+    static const uint32_t debug_mode = [] {
+        const char* e = getenv("CONV_DEBUG_MODE");
+        return e ? (uint32_t)atoi(e) : 0u;
+    }();
+    prm.debug = debug_mode;
+    static const int env_order = [] { const char* e = getenv("CONV_KORDER"); return e ? atoi(e) : -1; }();
+    // One order for every configuration (fused or not), so results are
+    // bit-identical across tilings (P10); env CONV_KORDER=1 is for experiments.
+    prm.tap_outer = t.fuse ? 0 : (env_order >= 0 ? env_order : 0);
+    static const char* trace_path = getenv("CONV_TRACE");
+    static unsigned long long* trace_buf = nullptr;
+    prm.trace = nullptr;
+    if (trace_path) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 1024 * 64 * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, 1024 * 64 * sizeof(unsigned long long), st);
+        prm.trace = trace_buf;
     }
     if (prm.k_iters % t.kbs != 0) { err = "k-blocks per stage must divide R*S*c-blocks"; return cudaErrorInvalidValue; }
     if (t.cg == 2)

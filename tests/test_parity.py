@@ -308,6 +308,25 @@ def test_fused_transform_bit_identical_to_separate(path, shape):
 
 
 @pytest.mark.parametrize("path", ["tf32", "bf16"])
+@pytest.mark.parametrize("pre_c", [0, 64, 128, 4096])
+def test_fused_transform_prologue_depths(path, pre_c):
+    """The repack launch converts the first pre_c channels of wave 0's input
+    (the prologue) and the kernel's chunk pipeline the rest: every split
+    gives the same bits as the separate repack (two waves of tiles)."""
+    sh = Shape(N=160, K=64, C=256, H=14, W=14, R=3, S=3)
+    inp, ker = make_inputs(sh, seed=41)
+    i, k = inp.cuda(), ker.cuda()
+    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1").run(i, k)
+    for cg in (1, 2):
+        plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile=f"fuse=1,cg={cg},pre_c={pre_c}")
+        d = plan.describe()["tile"]
+        assert d["fuse"] == 1 and d["pre_c"] == min(pre_c, d["cp"])
+        out = plan.run(i, k)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
 def test_fused_transform_cuda_graph_replay(path):
     """The bench replays conv_run from a CUDA graph: the chunk flags must be
     re-cleared inside the graph (by the Ker launch), so a replay with new
