@@ -305,7 +305,8 @@ def bench_ours(args):
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
             with open(tpath) as f:
-                traffic = json.load(f).get(f"{args.config}:{plan.path}")
+                tkey = f"{args.config}:{plan.path}" + (":fuse" if desc["tile"].get("fuse") else "")
+                traffic = json.load(f).get(tkey)
         roof_us = max(sh.flops / (peak * 1e12), sh.compulsory_bytes / (peaks["hbm_gbs"] * 1e9)) * 1e6
         line = {
             "metric": METRIC,

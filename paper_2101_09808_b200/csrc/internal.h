@@ -105,11 +105,13 @@ struct SimtTile {
     int tn = 1;   // images per CTA tile
     int th = 8;   // output rows per image per CTA tile
     int bc = 8;   // input channels per smem stage
-    int ver = 1;  // 1: stride-32 pixel slots (any S); 2: consecutive-pixel windows (S in {1,3}, TW in {4,8})
+    int ver = 1;  // 1: stride-32 pixel slots (any S); 2: consecutive-pixel windows (S in {1,3},
+                  //    TW in {4,8}, or TW = W in {7,14}: one thread per output row)
 };
 size_t simt_smem_bytes(const Problem& p, const SimtTile& t);
 size_t simt_ws_bytes(const Problem& p, const SimtTile& t);   // packed Ker
 bool simt_v2_ok(const Problem& p);
+bool simt_v2_tw_ok(const Problem& p, int tw);
 int simt2_pitch(const Problem& p, const SimtTile& t);
 bool simt_tile_supported(const SimtTile& t);
 // Launch the Ker packing kernel and K4.  events (optional, 3) around each.

@@ -340,19 +340,33 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // ncu r01: 8 resident warps/SM issue on only ~54% of cycles; ~16 are
     // needed to cover the LDS/FFMA dependency latencies.
     const double warps = (double)conc * threads / 32.0;
-    const double eff = std::min(1.0, warps / 16.0);
+    // one resident CTA per SM cannot hide its own chunk barriers / copy
+    // waits behind another CTA's FFMAs (measured r01b: 512-thread row-mode
+    // tiles 1501 us vs 2 x 256-thread tiles 1321 us, same warps per SM)
+    const double eff = std::min(1.0, warps / 16.0) * (conc == 1 ? 0.88 : 1.0);
     const double fma_cr = (double)pb.S * t.tk * t.tw;
     const double over_cr = t.ver == 2 ? win / 4.0 + pb.S * t.tk / 4.0 + 3.0
                                       : pb.S * (t.tw + t.tk / 4.0 + 1.0);
-    // v1's strided scalar loads and per-tap address math measured ~1.5-2.5x
-    // slower than v2 on every r01 config (scripts/simt_sweep.py).
-    const double issue_factor = (1.0 + over_cr / fma_cr) * (t.ver == 2 ? 1.0 : 1.6);
+    // v2 with several pixel groups per row (TW = 4 / 8) measured ~1.25x its
+    // modeled issue cost relative to row mode (TW = W, one group per row:
+    // aligned windows, no padded pixels) on the batched layer (r01b,
+    // scripts/simt_sweep3.py: 1571 vs 1321 us against models 1100 / 1152).
+    const bool row_mode = t.ver == 2 && (pb.W + t.tw - 1) / t.tw == 1;
+    // v1 (strided scalar loads) measured 3.5x its model on r2 (62.5 vs 17.8
+    // us, r01b simt_sweep2): charged 4x so that it is picked only where v2
+    // cannot run (S not in {1, 3})
+    const double issue_factor = (1.0 + over_cr / fma_cr) * (t.ver == 2 ? (row_mode ? 1.0 : 1.25) : 4.0);
     const double chunks = ceil((double)pb.C / t.bc);
     // one chunk: every thread's FFMAs, plus the cp.async copies (one per 4-B
     // element in v1/v2 In rows, ~6 instructions each, spread over the CTA)
     const double fma_chunk_cta = (double)threads * t.tk * t.tw * t.bc * pb.R * pb.S * issue_factor;
     const double in_elems_chunk = (double)t.bc * t.tn * (t.th + pb.R - 1) * pb.Win();
-    const double copy_chunk_cta = in_elems_chunk * 6.0 + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
+    // v2 copies 16-B units from a per-thread plan when they fit 4 per thread;
+    // beyond that a per-row loop of 4-B copies runs (~2.3x slower layer
+    // measured r01b)
+    const double units_v2 = (double)t.bc * t.tn * (t.th + pb.R - 1) * (pb.Win() % 4 == 0 ? pb.Win() / 4.0 : pb.Win());
+    const double copy_unit = (t.ver == 2 && units_v2 > 4.0 * threads) ? 6.0 * 4.0 : 6.0;
+    const double copy_chunk_cta = in_elems_chunk * copy_unit + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
     // a chunk cannot take less than one L2 round trip + two barriers
     const double chunk_cyc = std::max((double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff), 2000.0);
@@ -379,7 +393,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     if (ver == 2 && !simt_v2_ok(pb)) continue;
     if (forced && (forced_mask & 128) && ver != forced->ver) continue;
     for (int tk : tks)
-    for (int tw = 1; tw <= 8; ++tw)
+    for (int tw = 1; tw <= 14; ++tw)
     for (int kg : kgs)
     for (int pw = 1; pw * kg <= 16; ++pw)
     for (int tn = 1; tn <= tn_max; tn = (tn < 4 ? tn + 1 : tn * 2))
@@ -395,6 +409,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
             if ((forced_mask & 64) && t.bc != forced->bc) continue;
         }
         if (!simt_tile_supported(t)) continue;
+        if (ver == 2 && !simt_v2_tw_ok(pb, tw)) continue;
         // rows per tile: as many as the pixel slots allow
         const long slots = 32L * pw;                                   // lanes per k-group
         const long per_row = ver == 2 ? (pb.W + tw - 1) / tw : pb.W;   // slots one output row needs

@@ -402,13 +402,20 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
 
 bool simt_tile_supported(const SimtTile& t) {
     if (t.tk != 4 && t.tk != 8) return false;
-    if (t.tw < 1 || t.tw > 8) return false;
-    if (t.ver == 2 && t.tw != 4 && t.tw != 8) return false;
+    if (t.tw < 1 || t.tw > 14) return false;
+    if (t.ver != 2 && t.tw > 8) return false;
+    // v2: 4 / 8 pixels per thread (16-B aligned windows), or a whole output
+    // row of 7 or 14 pixels (row mode, TK = 4: 56 accumulators)
+    if (t.ver == 2 && t.tw != 4 && t.tw != 8 && !((t.tw == 7 || t.tw == 14) && t.tk == 4)) return false;
     const int threads = 32 * t.kg * t.pw;
     return t.kg >= 1 && t.pw >= 1 && threads <= 512 && t.tn >= 1 && t.th >= 1 && t.bc >= 1;
 }
 
 bool simt_v2_ok(const Problem& pb) { return pb.S == 1 || pb.S == 3; }
+
+// Row mode (TW = 7 or 14): one thread per output row, allowed only when the
+// row is exactly that wide (its window then starts 16-B aligned at w = 0).
+bool simt_v2_tw_ok(const Problem& pb, int tw) { return tw == 4 || tw == 8 || tw == pb.W; }
 
 // v2 smem row pitch: the last group's window (WIN rounded up to 4) must fit;
 // multiple of 4 floats; rows of <= 16 floats of groups are offset by 16 mod 32
@@ -418,7 +425,14 @@ int simt2_pitch(const Problem& pb, const SimtTile& t) {
     const int win4 = (t.tw + pb.S - 1 + 3) / 4 * 4;
     int pitch = std::max((int)pb.Win(), (groups - 1) * t.tw + win4);
     pitch = (pitch + 3) / 4 * 4;
-    if (pitch % 32 == 0) pitch += 4;      // rows 128 B apart would put every row's window on the same banks
+    if (groups == 1) {
+        // row mode: consecutive lanes are consecutive rows; an odd number of
+        // 16-B units per row puts a quarter-warp's 8 window loads on 8
+        // distinct 16-B bank groups
+        if ((pitch / 4) % 2 == 0) pitch += 4;
+    } else if (pitch % 32 == 0) {
+        pitch += 4;                       // rows 128 B apart would put every row's window on the same banks
+    }
     return pitch;
 }
 
@@ -455,6 +469,8 @@ static cudaError_t dispatch_simt2(const SimtTile& t, int R, int S, const float* 
     SIMT2_CASE(4, 4, 3, 3) SIMT2_CASE(4, 8, 3, 3) SIMT2_CASE(8, 4, 3, 3) SIMT2_CASE(8, 8, 3, 3)
     SIMT2_CASE(4, 4, 0, 1) SIMT2_CASE(4, 8, 0, 1) SIMT2_CASE(8, 4, 0, 1) SIMT2_CASE(8, 8, 0, 1)
     SIMT2_CASE(4, 4, 0, 3) SIMT2_CASE(4, 8, 0, 3) SIMT2_CASE(8, 4, 0, 3) SIMT2_CASE(8, 8, 0, 3)
+    SIMT2_CASE(4, 14, 3, 3) SIMT2_CASE(4, 7, 3, 3) SIMT2_CASE(4, 14, 1, 1) SIMT2_CASE(4, 7, 1, 1)
+    SIMT2_CASE(4, 14, 0, 3) SIMT2_CASE(4, 7, 0, 3) SIMT2_CASE(4, 14, 0, 1) SIMT2_CASE(4, 7, 0, 1)
 #undef SIMT2_CASE
     return cudaErrorInvalidValue;
 }
