@@ -63,7 +63,7 @@ struct conv_plan {
     // conv_run_host pipeline (created on first use, guarded by host_mu)
     std::mutex host_mu;
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
-    static constexpr int kMaxChunks = 8;
+    static constexpr int kMaxChunks = 32;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {};
     ~conv_plan() {
         for (cudaStream_t s : {h2d, comp, d2h}) if (s) cudaStreamDestroy(s);
@@ -457,7 +457,15 @@ extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, 
     // Pipeline over image chunks on three internal streams: the upload of
     // chunk j+1, the convolution of chunk j and the download of chunk j-1
     // overlap (PCIe is full duplex).  One chunk for small inputs.
-    const int nch = (bi >= (8u << 20)) ? std::min(pb.N, (int)conv_plan::kMaxChunks) : 1;
+    // Equal image chunks; 6 measured best for the batched layer (r01b:
+    // 4 / 6 / 8 / 16 chunks = 1.598 / 1.574 / 1.624 / 1.821 ms per step; a
+    // 1-2-4-6-6-6-6-4-2-1 taper 1.583 ms; H2D + D2H alone 1.38 ms).
+    // One chunk for small inputs; env CONV_HOST_CHUNKS for experiments.
+    static const int env_chunks = [] { const char* e = getenv("CONV_HOST_CHUNKS"); return e ? atoi(e) : 0; }();
+    const int nch = (bi < (8u << 20)) ? 1 : std::min({pb.N, (int)conv_plan::kMaxChunks, env_chunks > 0 ? env_chunks : 6});
+    int bounds[conv_plan::kMaxChunks + 1];
+    bounds[0] = 0;
+    for (int j = 0; j < nch; ++j) bounds[j + 1] = (int)((int64_t)pb.N * (j + 1) / nch);
     std::lock_guard<std::mutex> g(p->host_mu);
     cudaError_t e = cudaSuccess;
     auto ok = [&](cudaError_t r) { if (r != cudaSuccess && e == cudaSuccess) e = r; };
@@ -482,7 +490,8 @@ extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, 
     const int64_t img_in = (int64_t)pb.C * pb.Hin() * pb.Win(), img_out = (int64_t)pb.K * pb.H * pb.W;
     int n0 = 0;
     for (int j = 0; j < nch && e == cudaSuccess; ++j) {
-        const int n1 = (int)((int64_t)pb.N * (j + 1) / nch);
+        const int n1 = bounds[j + 1];
+        if (n1 == n0) continue;
         Problem sub = pb;
         sub.N = n1 - n0;
         ok(cudaMemcpyAsync(din + n0 * img_in, in_host + n0 * img_in, 4 * sub.N * img_in, cudaMemcpyHostToDevice, p->h2d));
