@@ -12,6 +12,13 @@ Functions and the passage each follows:
                          (PAPER.md:150-158), double accumulation, plain C
                          (``conv_oracle.c``).  Pinned by tests/test_oracle.py
                          (P1-P9 of SURVEY.md Sec. 8(c)).
+* ``conv_eq1_strided`` -- Eq. 1 with stride U (PAPER.md:201 footnote; Table 1,
+                         PAPER.md:439, stride-2 layers): In[n,c,U*h+r,U*w+s],
+                         explicit input extents, floor output extents; plain C.
+                         Pinned by tests/test_oracle.py: U = 1 equals conv_eq1,
+                         stride-U output = stride-1 output subsampled (exact),
+                         torch conv2d f64 with stride, a hand-worked golden,
+                         brute-force points.
 * ``conv_eq1_point``  -- one output element of Eq. 1 as the correctly rounded
                          sum (``math.fsum``) of its C*R*S exact products; used
                          for sampled parity at full sizes.  Pinned against
@@ -60,6 +67,9 @@ def _load():
             lib.oracle_conv_eq1.restype = ctypes.c_int
             lib.oracle_conv_eq1.argtypes = [ctypes.c_int] * 7 + [
                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+            lib.oracle_conv_eq1_strided.restype = ctypes.c_int
+            lib.oracle_conv_eq1_strided.argtypes = [ctypes.c_int] * 8 + [
+                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
             lib.oracle_num_threads.restype = ctypes.c_int
             lib.oracle_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
@@ -99,11 +109,33 @@ def conv_eq1(inp: np.ndarray, ker: np.ndarray, nthreads: int = 0) -> np.ndarray:
     return out
 
 
-def conv_eq1_point(inp: np.ndarray, ker: np.ndarray, n: int, k: int, h: int, w: int) -> float:
-    """Out[n,k,h,w] of Eq. 1 as the correctly rounded sum of its exact
-    products (each fp32*fp32 product is exact in float64)."""
+def conv_eq1_strided(inp: np.ndarray, ker: np.ndarray, stride: int, nthreads: int = 0) -> np.ndarray:
+    """Eq. 1 with stride U = ``stride``, no padding.  ``inp``: fp32
+    [N,C,Hin,Win]; ``ker``: fp32 [K,C,R,S].  Returns float64 [N,K,H,W] with
+    H = (Hin-R)//U + 1, W = (Win-S)//U + 1."""
+    inp = np.ascontiguousarray(inp, dtype=np.float32)
+    ker = np.ascontiguousarray(ker, dtype=np.float32)
+    if inp.ndim != 4 or ker.ndim != 4 or inp.shape[1] != ker.shape[1]:
+        raise ValueError("expected In [N,C,Hin,Win] and Ker [K,C,R,S] with equal C")
+    N, C, Hin, Win = inp.shape
+    K, _, R, S = ker.shape
+    if stride < 1 or Hin < R or Win < S:
+        raise ValueError("bad stride or input smaller than the kernel")
+    H, W = (Hin - R) // stride + 1, (Win - S) // stride + 1
+    out = np.empty((N, K, H, W), dtype=np.float64)
+    rc = _load().oracle_conv_eq1_strided(N, K, C, Hin, Win, R, S, stride,
+                                         inp.ctypes.data, ker.ctypes.data, out.ctypes.data,
+                                         nthreads or host_threads())
+    if rc != 0:
+        raise ValueError("oracle_conv_eq1_strided rejected its arguments")
+    return out
+
+
+def conv_eq1_point(inp: np.ndarray, ker: np.ndarray, n: int, k: int, h: int, w: int, stride: int = 1) -> float:
+    """Out[n,k,h,w] of Eq. 1 (stride U) as the correctly rounded sum of its
+    exact products (each fp32*fp32 product is exact in float64)."""
     R, S = ker.shape[2], ker.shape[3]
-    window = inp[n, :, h:h + R, w:w + S].astype(np.float64)
+    window = inp[n, :, stride * h:stride * h + R, stride * w:stride * w + S].astype(np.float64)
     prods = window * ker[k].astype(np.float64)
     return math.fsum(prods.ravel().tolist())
 

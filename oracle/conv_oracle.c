@@ -66,6 +66,52 @@ int oracle_conv_eq1(int N, int K, int C, int H, int W, int R, int S,
     return 0;
 }
 
+/*
+ * Strided Eq. 1 (the paper's footnote: "we do not show
+ * stride/dilation, but the methodology is applicable to the general case";
+ * Table 1, marks the stride-2 layers with *):
+ *
+ *     Out[n,k,h,w] = sum_{c,r,s} In[n,c,U*h+r,U*w+s] * Ker[k,c,r,s]
+ *
+ * In [N][C][Hin][Win] with explicit INPUT extents (Table 1 lists input
+ * sizes), Out [N][K][H][W] with H = (Hin-R)/U + 1, W = (Win-S)/U + 1 (floor:
+ * input rows/columns past the last full window are not read).  Same
+ * Listing-2 loop order, double accumulation and (n,k)-plane parallelism as
+ * oracle_conv_eq1.  Returns 0, or 1 on a bad extent / NULL pointer.
+ */
+int oracle_conv_eq1_strided(int N, int K, int C, int Hin, int Win, int R, int S, int U,
+                            const float* in, const float* ker, double* out, int nthreads)
+{
+    if (N < 1 || K < 1 || C < 1 || R < 1 || S < 1 || U < 1 || Hin < R || Win < S) return 1;
+    if (!in || !ker || !out) return 1;
+    const int64_t H = ((int64_t)Hin - R) / U + 1;
+    const int64_t W = ((int64_t)Win - S) / U + 1;
+    const int64_t planes = (int64_t)N * K;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t nk = 0; nk < planes; ++nk) {
+        const int64_t n = nk / K;
+        const int64_t k = nk % K;
+        double* acc = out + nk * H * W;                    /* Out[n][k][:][:] */
+        for (int64_t i = 0; i < H * W; ++i) acc[i] = 0.0;
+        for (int64_t c = 0; c < C; ++c)
+            for (int64_t r = 0; r < R; ++r)
+                for (int64_t s = 0; s < S; ++s) {
+                    const double kv = (double)ker[((k * C + c) * R + r) * S + s];
+                    const float* in_rs = in + ((n * C + c) * (int64_t)Hin + r) * Win + s;
+                    for (int64_t h = 0; h < H; ++h)
+                        for (int64_t w = 0; w < W; ++w)
+                            acc[h * W + w] += (double)in_rs[(U * h) * (int64_t)Win + U * w] * kv;
+                }
+    }
+    return 0;
+}
+
 /* Number of OpenMP threads a parallel region would use (for reporting). */
 int oracle_num_threads(int nthreads)
 {

@@ -224,3 +224,61 @@ def test_tf32_rna_ties_and_bound():
     assert np.all((r.view(np.uint32) & 0x1FFF) == 0)
     ulp = np.ldexp(1.0, np.frexp(np.abs(x).astype(np.float64))[1] - 11)
     assert np.all(np.abs(r.astype(np.float64) - x) <= ulp / 2)
+
+
+# ---- strided Eq. 1 (PAPER.md:201 footnote; Table 1 stride-2 layers)
+
+def test_strided_hand_worked_golden():
+    """Hand-worked stride-2 values (tests/golden/eq1_stride2_hand.json):
+    catches U*(h+r) instead of U*h+r, a stride on one axis only, and reading
+    past the last full window."""
+    g = _golden("eq1_stride2_hand.json")
+    out = oracle.conv_eq1_strided(np.array(g["In"], dtype=np.float32), np.array(g["Ker"], dtype=np.float32),
+                                  g["stride"])
+    np.testing.assert_array_equal(out, np.array(g["Out"], dtype=np.float64))
+
+
+def test_strided_unit_stride_is_eq1():
+    """U = 1 reduces to the (pinned) stride-1 oracle, bit for bit."""
+    sh = Shape(N=2, K=4, C=3, H=6, W=7, R=3, S=2)
+    inp, ker = make_inputs(sh, seed=51)
+    np.testing.assert_array_equal(oracle.conv_eq1_strided(inp.numpy(), ker.numpy(), 1),
+                                  oracle.conv_eq1(inp.numpy(), ker.numpy()))
+
+
+@pytest.mark.parametrize("U", [2, 3])
+def test_strided_is_subsampled_unit_stride(U):
+    """Out_U[h, w] = Out_1[U h, U w] exactly (same products, same summation
+    order); input extents with (Hin - R) % U != 0 check the floor."""
+    inp = torch.rand(2, 3, 12, 11, generator=torch.Generator().manual_seed(52)) * 2 - 1
+    ker = torch.rand(5, 3, 3, 2, generator=torch.Generator().manual_seed(53)) * 2 - 1
+    full = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    got = oracle.conv_eq1_strided(inp.numpy(), ker.numpy(), U)
+    assert got.shape == (2, 5, (12 - 3) // U + 1, (11 - 2) // U + 1)
+    np.testing.assert_array_equal(got, full[:, :, ::U, ::U])
+
+
+@pytest.mark.parametrize("U", [2, 3])
+def test_strided_vs_torch_conv2d(U):
+    """Library cross-check: torch conv2d (float64, stride U, no padding)."""
+    inp = torch.rand(2, 4, 15, 13, generator=torch.Generator().manual_seed(54)) * 2 - 1
+    ker = torch.rand(3, 4, 3, 3, generator=torch.Generator().manual_seed(55)) * 2 - 1
+    got = oracle.conv_eq1_strided(inp.numpy(), ker.numpy(), U)
+    ref = torch.nn.functional.conv2d(inp.double(), ker.double(), stride=U).numpy()
+    np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13)
+    xi = torch.randint(-2, 3, (1, 4, 15, 13), generator=torch.Generator().manual_seed(56)).float()
+    wi = torch.randint(-2, 3, (3, 4, 3, 3), generator=torch.Generator().manual_seed(57)).float()
+    np.testing.assert_array_equal(oracle.conv_eq1_strided(xi.numpy(), wi.numpy(), U),
+                                  torch.nn.functional.conv2d(xi.double(), wi.double(), stride=U).numpy())
+
+
+def test_strided_points_brute_force():
+    """Sampled outputs of the strided oracle vs the correctly rounded sum."""
+    inp = torch.rand(2, 8, 21, 17, generator=torch.Generator().manual_seed(58)) * 2 - 1
+    ker = torch.rand(6, 8, 7, 7, generator=torch.Generator().manual_seed(59)) * 2 - 1
+    x, w = inp.numpy(), ker.numpy()
+    out = oracle.conv_eq1_strided(x, w, 2)
+    rng = np.random.default_rng(60)
+    for _ in range(50):
+        p = (rng.integers(2), rng.integers(6), rng.integers(out.shape[2]), rng.integers(out.shape[3]))
+        assert abs(out[p] - oracle.conv_eq1_point(x, w, *p, stride=2)) <= 1e-13 * (1 + abs(out[p]))
