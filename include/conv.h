@@ -5,12 +5,20 @@
  *
  *     Out[n,k,h,w] = sum_{c<C, r<R, s<S} In[n,c,h+r,w+s] * Ker[k,c,r,s]
  *
- * stride 1, no padding, fp32 tensors, In/Out NCHW and Ker KCRS
+ * no padding, fp32 tensors, In/Out NCHW and Ker KCRS
  * (Sec. 9: "All input and output tensors were stored in NCHW
  * layout and all kernel tensors were stored in KCRS layout").  H and W are the
  * OUTPUT extents (the loop extents N_h, N_w of Listing 2);
  * the input is (H+R-1) x (W+S-1) (Sec. 3.1).  conv_run
- * OVERWRITES Out (Eq. 1 is "=", reading R4).  Internal layout
+ * OVERWRITES Out (Eq. 1 is "=", reading R4).  Plans made with
+ * conv_plan_create_strided use stride U (PAPER.md:201 footnote 1: the method
+ * "is applicable to the general case" of strided convolution; Table 1,
+ * PAPER.md:439, marks the stride-2 layers with *):
+ *
+ *     Out[n,k,h,w] = sum_{c,r,s} In[n,c,U*h+r,U*w+s] * Ker[k,c,r,s]
+ *
+ * with explicit INPUT extents Hin x Win and H = (Hin-R)/U + 1 (floor).
+ * Internal layout
  * transforms are part of every conv_run, as the paper counts them
  * (PAPER.md:371).
  *
@@ -72,6 +80,16 @@ typedef enum {
  * tensor has >= 2^31 elements; UNSUPPORTED_DEVICE without an sm_100 device. */
 CONV_API conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R, int S);
 
+/* Strided plan: input extents Hin x Win (as PAPER.md:439 Table 1 lists them),
+ * kernel R x S, stride U >= 1 on both axes; output H = (Hin-R)/U + 1,
+ * W = (Win-S)/U + 1 (input rows/columns past the last full window are not
+ * read).  In is N x C x Hin x Win.  With U = 1 and Hin = H+R-1 it is the
+ * same plan as conv_plan_create.  Paths: the tensor-core paths (TMA im2col
+ * traversal stride U, U <= 8) and FP32 SIMT v1; SIMT v2 needs U = 1.
+ * Errors as conv_plan_create, plus INVALID_ARGUMENT if U < 1 or the input is
+ * smaller than the kernel. */
+CONV_API conv_plan* conv_plan_create_strided(int N, int K, int C, int Hin, int Win, int R, int S, int U);
+
 /* A plan for a described (not present) device: `sms` SMs, `smem_optin` bytes
  * of opt-in shared memory per block, `l2_bytes` of L2.  Runs the same
  * selector; the plan can be described but not run (conv_run returns
@@ -79,6 +97,9 @@ CONV_API conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R, i
  * studies.  NULL on invalid arguments. */
 CONV_API conv_plan* conv_plan_create_offline(int N, int K, int C, int H, int W, int R, int S,
                                              int sms, size_t smem_optin, size_t l2_bytes);
+/* Offline variant of conv_plan_create_strided (same arguments as above). */
+CONV_API conv_plan* conv_plan_create_strided_offline(int N, int K, int C, int Hin, int Win, int R, int S, int U,
+                                                     int sms, size_t smem_optin, size_t l2_bytes);
 
 /* Force a path (default AUTO) and re-run the selector for it.
  * INFEASIBLE if no candidate of that path fits (e.g. R or S > 128 on the

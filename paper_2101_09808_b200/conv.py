@@ -28,7 +28,8 @@ PATH_NAMES = {v: k for k, v in PATHS.items()}
 
 # Every symbol include/conv.h declares (tests check the library exports them).
 EXPORTED = (
-    "conv_plan_create", "conv_plan_create_offline", "conv_plan_set_path", "conv_plan_set_tile", "conv_plan_workspace_bytes",
+    "conv_plan_create", "conv_plan_create_offline", "conv_plan_create_strided", "conv_plan_create_strided_offline",
+    "conv_plan_set_path", "conv_plan_set_tile", "conv_plan_workspace_bytes",
     "conv_plan_num_kernels", "conv_plan_path", "conv_plan_describe", "conv_plan_destroy",
     "conv_run", "conv_run_events", "conv_plan_host_run_bytes", "conv_run_host",
     "conv_last_error", "conv_version", "conv_model_dv", "conv_model_dv_matmul",
@@ -60,6 +61,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         sig = {
             "conv_plan_create": (vp, [i] * 7),
             "conv_plan_create_offline": (vp, [i] * 8 + [sz, sz]),
+            "conv_plan_create_strided": (vp, [i] * 8),
+            "conv_plan_create_strided_offline": (vp, [i] * 9 + [sz, sz]),
             "conv_plan_set_path": (i, [vp, i]),
             "conv_plan_set_tile": (i, [vp, ctypes.c_char_p]),
             "conv_plan_workspace_bytes": (sz, [vp]),
@@ -111,21 +114,38 @@ def _stream_handle(stream) -> Optional[int]:
 
 
 class ConvPlan:
-    """A plan for Eq. 1 with OUTPUT extents H x W."""
+    """A plan for Eq. 1 with OUTPUT extents H x W; with
+    ``stride`` U > 1 (or explicit ``in_hw``) the strided form
+    Out[n,k,h,w] = sum In[n,c,U*h+r,U*w+s] Ker[k,c,r,s] (conv_plan_create_strided)."""
 
     def __init__(self, N: int, K: int, C: int, H: int, W: int, R: int, S: int,
-                 path: str = "auto", tile: Optional[str] = None, offline_device: Optional[dict] = None):
+                 path: str = "auto", tile: Optional[str] = None, offline_device: Optional[dict] = None,
+                 stride: int = 1, in_hw: Optional[tuple] = None):
         """``offline_device`` = dict(sms=, smem_optin=, l2_bytes=) plans for a
-        described device without touching CUDA (describe-only plan)."""
+        described device without touching CUDA (describe-only plan).
+        ``in_hw`` = (Hin, Win) input extents of a strided plan (default the
+        minimal ((H-1)*U+R, (W-1)*U+S)); H, W must equal the floor output
+        extents (Hin-R)//U+1, (Win-S)//U+1."""
         lib = load_library()
         self._lib = lib
+        strided = stride != 1 or in_hw is not None
+        if strided:
+            Hin, Win = in_hw if in_hw is not None else ((H - 1) * stride + R, (W - 1) * stride + S)
+            if stride >= 1 and Hin >= R and Win >= S and ((Hin - R) // stride + 1, (Win - S) // stride + 1) != (H, W):
+                raise ValueError(f"output {H}x{W} does not match input {Hin}x{Win}, kernel {R}x{S}, stride {stride}")
+        else:
+            Hin, Win = H + R - 1, W + S - 1
         self.shape = (N, K, C, H, W, R, S)
+        self.stride = stride
+        self.in_hw = (Hin, Win)
         if offline_device is not None:
             d = offline_device
-            h = lib.conv_plan_create_offline(N, K, C, H, W, R, S, int(d["sms"]), int(d["smem_optin"]),
-                                             int(d["l2_bytes"]))
+            dev = (int(d["sms"]), int(d["smem_optin"]), int(d["l2_bytes"]))
+            h = (lib.conv_plan_create_strided_offline(N, K, C, Hin, Win, R, S, stride, *dev) if strided
+                 else lib.conv_plan_create_offline(N, K, C, H, W, R, S, *dev))
         else:
-            h = lib.conv_plan_create(N, K, C, H, W, R, S)
+            h = (lib.conv_plan_create_strided(N, K, C, Hin, Win, R, S, stride) if strided
+                 else lib.conv_plan_create(N, K, C, H, W, R, S))
         if not h:
             msg = last_error()
             status = CONV_ERR_UNSUPPORTED_DEVICE if ("device" in msg and "extent" not in msg) else CONV_ERR_INVALID_ARGUMENT
@@ -178,7 +198,7 @@ class ConvPlan:
     # -- execution -----------------------------------------------------------
     def _shapes(self):
         N, K, C, H, W, R, S = self.shape
-        return (N, C, H + R - 1, W + S - 1), (K, C, R, S), (N, K, H, W)
+        return (N, C) + tuple(self.in_hw), (K, C, R, S), (N, K, H, W)
 
     def _shapes_sizes(self):
         import torch

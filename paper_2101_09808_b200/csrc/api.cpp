@@ -136,52 +136,100 @@ static conv_status select(conv_plan* p) {
     return CONV_OK;
 }
 
-extern "C" conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R, int S) {
-    if (N < 1 || K < 1 || C < 1 || H < 1 || W < 1 || R < 1 || S < 1) {
-        fail(CONV_ERR_INVALID_ARGUMENT, "extent must be >= 1 (N=%d K=%d C=%d H=%d W=%d R=%d S=%d)", N, K, C, H, W, R, S);
-        return nullptr;
-    }
-    Problem pb{N, K, C, H, W, R, S};
+// Plan creation shared by the public constructors: validates the problem,
+// binds the current device (or the described offline one) and runs the
+// selector.
+static conv_plan* create_impl(const Problem& pb, const Device* offline) {
     const int64_t lim = (int64_t)1 << 31;
     if (pb.in_elems() >= lim || pb.ker_elems() >= lim || pb.out_elems() >= lim || pb.Hin() >= lim || pb.Win() >= lim) {
         fail(CONV_ERR_INVALID_ARGUMENT, "tensor with >= 2^31 elements is not supported");
         return nullptr;
     }
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        fail(CONV_ERR_UNSUPPORTED_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
-        return nullptr;
-    }
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
-        fail(CONV_ERR_UNSUPPORTED_DEVICE, "cudaGetDeviceProperties failed");
-        return nullptr;
-    }
-    if (prop.major != 10 || prop.minor != 0) {
-        fail(CONV_ERR_UNSUPPORTED_DEVICE, "device %s is sm_%d%d; this library is built for sm_100a only",
-             prop.name, prop.major, prop.minor);
-        return nullptr;
-    }
-    std::string err;
-    if (!driver_init(err)) {
-        fail(CONV_ERR_UNSUPPORTED_DEVICE, "%s", err.c_str());
-        return nullptr;
-    }
     conv_plan* p = new conv_plan();
     p->pb = pb;
-    p->dev.ordinal = dev;
-    p->dev.sms = prop.multiProcessorCount;
-    p->dev.cc_major = prop.major;
-    p->dev.cc_minor = prop.minor;
-    p->dev.smem_optin = prop.sharedMemPerBlockOptin;
-    p->dev.l2_bytes = prop.l2CacheSize;
+    if (offline) {
+        p->dev = *offline;
+        p->dev.ordinal = -1;                 // not bound to a device: cannot run
+    } else {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            delete p;
+            fail(CONV_ERR_UNSUPPORTED_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+            return nullptr;
+        }
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+            delete p;
+            fail(CONV_ERR_UNSUPPORTED_DEVICE, "cudaGetDeviceProperties failed");
+            return nullptr;
+        }
+        if (prop.major != 10 || prop.minor != 0) {
+            delete p;
+            fail(CONV_ERR_UNSUPPORTED_DEVICE, "device %s is sm_%d%d; this library is built for sm_100a only",
+                 prop.name, prop.major, prop.minor);
+            return nullptr;
+        }
+        std::string err;
+        if (!driver_init(err)) {
+            delete p;
+            fail(CONV_ERR_UNSUPPORTED_DEVICE, "%s", err.c_str());
+            return nullptr;
+        }
+        p->dev.ordinal = dev;
+        p->dev.sms = prop.multiProcessorCount;
+        p->dev.cc_major = prop.major;
+        p->dev.cc_minor = prop.minor;
+        p->dev.smem_optin = prop.sharedMemPerBlockOptin;
+        p->dev.l2_bytes = prop.l2CacheSize;
+    }
     if (select(p) != CONV_OK) {
         delete p;
         return nullptr;
     }
     return p;
+}
+
+static bool strided_problem(int N, int K, int C, int Hin, int Win, int R, int S, int U, Problem& pb) {
+    if (N < 1 || K < 1 || C < 1 || R < 1 || S < 1 || U < 1) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "extent must be >= 1 (N=%d K=%d C=%d R=%d S=%d U=%d)", N, K, C, R, S, U);
+        return false;
+    }
+    if (Hin < R || Win < S) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "input %dx%d smaller than the kernel %dx%d", Hin, Win, R, S);
+        return false;
+    }
+    pb = Problem{N, K, C, (Hin - R) / U + 1, (Win - S) / U + 1, R, S};
+    pb.U = U;
+    pb.hin = Hin;
+    pb.win = Win;
+    return true;
+}
+
+extern "C" conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R, int S) {
+    if (N < 1 || K < 1 || C < 1 || H < 1 || W < 1 || R < 1 || S < 1) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "extent must be >= 1 (N=%d K=%d C=%d H=%d W=%d R=%d S=%d)", N, K, C, H, W, R, S);
+        return nullptr;
+    }
+    return create_impl(Problem{N, K, C, H, W, R, S}, nullptr);
+}
+
+extern "C" conv_plan* conv_plan_create_strided(int N, int K, int C, int Hin, int Win, int R, int S, int U) {
+    Problem pb;
+    if (!strided_problem(N, K, C, Hin, Win, R, S, U, pb)) return nullptr;
+    return create_impl(pb, nullptr);
+}
+
+static bool offline_device(int sms, size_t smem_optin, size_t l2_bytes, Device& d) {
+    if (sms < 2 || smem_optin < 16384 || l2_bytes == 0) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "device description out of range");
+        return false;
+    }
+    d.sms = sms;
+    d.smem_optin = smem_optin;
+    d.l2_bytes = l2_bytes;
+    return true;
 }
 
 extern "C" conv_plan* conv_plan_create_offline(int N, int K, int C, int H, int W, int R, int S, int sms,
@@ -190,27 +238,18 @@ extern "C" conv_plan* conv_plan_create_offline(int N, int K, int C, int H, int W
         fail(CONV_ERR_INVALID_ARGUMENT, "extent must be >= 1 (N=%d K=%d C=%d H=%d W=%d R=%d S=%d)", N, K, C, H, W, R, S);
         return nullptr;
     }
-    if (sms < 2 || smem_optin < 16384 || l2_bytes == 0) {
-        fail(CONV_ERR_INVALID_ARGUMENT, "device description out of range");
-        return nullptr;
-    }
-    Problem pb{N, K, C, H, W, R, S};
-    const int64_t lim = (int64_t)1 << 31;
-    if (pb.in_elems() >= lim || pb.ker_elems() >= lim || pb.out_elems() >= lim) {
-        fail(CONV_ERR_INVALID_ARGUMENT, "tensor with >= 2^31 elements is not supported");
-        return nullptr;
-    }
-    conv_plan* p = new conv_plan();
-    p->pb = pb;
-    p->dev.ordinal = -1;                 // not bound to a device: cannot run
-    p->dev.sms = sms;
-    p->dev.smem_optin = smem_optin;
-    p->dev.l2_bytes = l2_bytes;
-    if (select(p) != CONV_OK) {
-        delete p;
-        return nullptr;
-    }
-    return p;
+    Device d;
+    if (!offline_device(sms, smem_optin, l2_bytes, d)) return nullptr;
+    return create_impl(Problem{N, K, C, H, W, R, S}, &d);
+}
+
+extern "C" conv_plan* conv_plan_create_strided_offline(int N, int K, int C, int Hin, int Win, int R, int S, int U,
+                                                        int sms, size_t smem_optin, size_t l2_bytes) {
+    Problem pb;
+    if (!strided_problem(N, K, C, Hin, Win, R, S, U, pb)) return nullptr;
+    Device d;
+    if (!offline_device(sms, smem_optin, l2_bytes, d)) return nullptr;
+    return create_impl(pb, &d);
 }
 
 extern "C" conv_status conv_plan_set_path(conv_plan* p, conv_path path) {
@@ -326,7 +365,7 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     tile = t;
     char out[2048];
     int n = snprintf(out, sizeof out,
-        "{\"problem\":{\"N\":%d,\"K\":%d,\"C\":%d,\"H\":%d,\"W\":%d,\"R\":%d,\"S\":%d},"
+        "{\"problem\":{\"N\":%d,\"K\":%d,\"C\":%d,\"H\":%d,\"W\":%d,\"R\":%d,\"S\":%d,\"U\":%d,\"Hin\":%lld,\"Win\":%lld},"
         "\"path\":\"%s\",\"tile\":%s,\"workspace_bytes\":%zu,\"kernels\":%d,"
         "\"model\":{\"tiles\":%ld,\"ctas\":%ld,\"wave_eff\":%.4f,\"smem_bytes\":%zu,"
         "\"levels\":{\"l2_smem\":{\"dv_bytes\":%.12g,\"bw\":%.6g,\"us\":%.4f},"
@@ -334,7 +373,7 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
         "\"compute\":{\"flops_issued_us\":%.4f,\"peak\":%.6g}},\"model_us\":%.4f},"
         "\"roofline\":{\"flops\":%.6g,\"compulsory_bytes\":%.6g,\"roofline_us\":%.4f},"
         "\"device\":{\"ordinal\":%d,\"sms\":%d,\"smem_optin\":%zu,\"l2_bytes\":%zu}}",
-        pb.N, pb.K, pb.C, pb.H, pb.W, pb.R, pb.S, path_name(p->path), tile.c_str(), ws_bytes(p),
+        pb.N, pb.K, pb.C, pb.H, pb.W, pb.R, pb.S, pb.U, (long long)pb.Hin(), (long long)pb.Win(), path_name(p->path), tile.c_str(), ws_bytes(p),
         conv_plan_num_kernels(p), m.tiles, m.ctas, m.wave_eff, m.smem,
         m.dv_l2_smem, p->dev.bw_l2, m.t_l2_us, m.dv_hbm, p->dev.bw_hbm, m.t_hbm_us, m.t_comp_us, peak,
         m.model_us, pb.flops(), comp_bytes, roof_us, p->dev.ordinal, p->dev.sms, p->dev.smem_optin,

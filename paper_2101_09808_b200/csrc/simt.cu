@@ -47,10 +47,11 @@ static cudaError_t launch_pdl(Kern kfn, dim3 grid, int threads, size_t smem, cud
 
 struct SimtParams {
     int N, K, C, H, W, R, S;
+    int U;            // stride (v1 only): output (h, w) reads input rows U*h + r, columns U*w + s
     int Hin, Win, HW, RS;
     int tn, th, bc, kg;
     int bko;          // kg * TK
-    int rows_in;      // th + R - 1
+    int rows_in;      // (th - 1) * U + R
     int plane;        // tn * rows_in * Win  (floats per channel in smem)
     int n_htiles;     // ceil(H / th)
     int nchunks;      // ceil(C / bc)
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict_
         const int h = rem / p.W;
         const int w = rem - h * p.W;
         valid[j] = q < p.bp && (n0 + img) < p.N && (h0 + h) < p.H;
-        off[j] = valid[j] ? (img * p.rows_in + h) * p.Win + w : 0;
+        off[j] = valid[j] ? (img * p.rows_in + h * p.U) * p.Win + w * p.U : 0;
         pix_img[j] = img;
         pix_h[j] = h;
         pix_w[j] = w;
@@ -145,10 +146,11 @@ __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict_
             const int c = c0 + cc;
             const int n = n0 + img;
             const bool seg_ok = c < p.C && n < p.N;
-            const float* g = in + (((int64_t)n * p.C + c) * p.Hin + h0) * p.Win;
+            const int hin0 = h0 * p.U;            // first input row of the tile
+            const float* g = in + (((int64_t)n * p.C + c) * p.Hin + hin0) * p.Win;
             float* s = in_s + cc * p.plane + img * seg_len;
-            // valid elements: rows < Hin - h0
-            const int rows_ok = p.Hin - h0 < p.rows_in ? p.Hin - h0 : p.rows_in;
+            // valid elements: rows < Hin - hin0
+            const int rows_ok = p.Hin - hin0 < p.rows_in ? p.Hin - hin0 : p.rows_in;
             const int len_ok = seg_ok ? rows_ok * p.Win : 0;
             if (p.vec4_in) {
                 for (int e = threadIdx.x * 4; e < seg_len; e += blockDim.x * 4)
@@ -411,7 +413,7 @@ bool simt_tile_supported(const SimtTile& t) {
     return t.kg >= 1 && t.pw >= 1 && threads <= 512 && t.tn >= 1 && t.th >= 1 && t.bc >= 1;
 }
 
-bool simt_v2_ok(const Problem& pb) { return pb.S == 1 || pb.S == 3; }
+bool simt_v2_ok(const Problem& pb) { return pb.U == 1 && (pb.S == 1 || pb.S == 3); }
 
 // Row mode (TW = 7 or 14): one thread per output row, allowed only when the
 // row is exactly that wide (its window then starts 16-B aligned at w = 0).
@@ -438,7 +440,7 @@ int simt2_pitch(const Problem& pb, const SimtTile& t) {
 
 size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
     const size_t row = t.ver == 2 ? (size_t)simt2_pitch(pb, t) : (size_t)pb.Win();
-    const size_t plane = (size_t)t.tn * (t.th + pb.R - 1) * row;
+    const size_t plane = (size_t)t.tn * ((t.th - 1) * pb.U + pb.R) * row;
     const size_t in_stage = (size_t)t.bc * plane;
     const size_t ker_stage = (size_t)t.bc * pb.R * pb.S * t.kg * t.tk;
     return 2 * (in_stage + ker_stage) * sizeof(float);
@@ -512,17 +514,18 @@ size_t simt_ws_bytes(const Problem& pb, const SimtTile& t) {
 cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, const float* ker,
                      float* out, void* ws, cudaStream_t st, cudaEvent_t* ev, std::string& err) {
     SimtParams p;
-    p.N = pb.N; p.K = pb.K; p.C = pb.C; p.H = pb.H; p.W = pb.W; p.R = pb.R; p.S = pb.S;
+    p.N = pb.N; p.K = pb.K; p.C = pb.C; p.H = pb.H; p.W = pb.W; p.R = pb.R; p.S = pb.S; p.U = pb.U;
     p.Hin = (int)pb.Hin(); p.Win = (int)pb.Win(); p.HW = pb.H * pb.W; p.RS = pb.R * pb.S;
     p.tn = t.tn; p.th = t.th; p.bc = t.bc; p.kg = t.kg;
     p.bko = t.kg * t.tk;
-    p.rows_in = t.th + pb.R - 1;
+    p.rows_in = (t.th - 1) * pb.U + pb.R;
     p.plane = t.tn * p.rows_in * p.Win;
     p.n_htiles = (pb.H + t.th - 1) / t.th;
     p.nchunks = (pb.C + t.bc - 1) / t.bc;
     p.bp = t.tn * t.th * pb.W;
     p.vec4_in = (p.Win % 4 == 0) ? 1 : 0;
     if (t.ver != 2 && p.bp > t.pw * 32 * t.tw) { err = "SIMT tile: pixel slots < tn*th*W"; return cudaErrorInvalidValue; }
+    if (t.ver == 2 && pb.U != 1) { err = "SIMT v2 needs stride 1"; return cudaErrorInvalidValue; }
 
     float* kerp = static_cast<float*>(ws);
     const int64_t total = (int64_t)((pb.K + p.bko - 1) / p.bko) * p.bko * pb.C * p.RS;

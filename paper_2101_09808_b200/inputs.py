@@ -25,6 +25,10 @@ import torch
 
 @dataclass(frozen=True)
 class Shape:
+    """H, W are OUTPUT extents.  U is the stride (PAPER.md:201 footnote;
+    Table 1's * layers); hin/win are explicit input extents of a strided
+    layer (0: the minimal (H-1)*U + R).  Use ``Shape.strided`` to build one
+    from input extents as Table 1 lists them."""
     N: int
     K: int
     C: int
@@ -32,14 +36,27 @@ class Shape:
     W: int
     R: int
     S: int
+    U: int = 1
+    hin: int = 0
+    win: int = 0
+
+    @classmethod
+    def strided(cls, N, K, C, Hin, Win, R, S, U) -> "Shape":
+        return cls(N, K, C, (Hin - R) // U + 1, (Win - S) // U + 1, R, S, U, Hin, Win)
 
     @property
     def Hin(self) -> int:
-        return self.H + self.R - 1
+        return self.hin or (self.H - 1) * self.U + self.R
 
     @property
     def Win(self) -> int:
-        return self.W + self.S - 1
+        return self.win or (self.W - 1) * self.U + self.S
+
+    def plan_kwargs(self) -> dict:
+        """Keyword arguments of ConvPlan for this shape (stride, input extents)."""
+        if self.U == 1 and not self.hin and not self.win:
+            return {}
+        return {"stride": self.U, "in_hw": (self.Hin, self.Win)}
 
     @property
     def in_shape(self):

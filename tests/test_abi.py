@@ -208,3 +208,26 @@ def test_tensor_l2_volume_matches_im2col_replay(lib):
         mt = -(-sh.N * sh.H * sh.W // bm)
         exp = mt * bm * 9 * 256 * 2 + mt * 256 * 9 * 256 * 2
         assert d["model"]["levels"]["l2_smem"]["dv_bytes"] == pytest.approx(exp, rel=1e-9)
+
+
+def test_strided_plans_offline(lib):
+    """conv_plan_create_strided(_offline): output extents (Hin-R)/U + 1 (floor),
+    describe() reports U and the input extents; SIMT picks v1 for U > 1 (v2
+    needs U = 1); bad strides / tiny inputs are rejected before any device."""
+    sh = dict(sms=148, smem_optin=232448, l2_bytes=132120576)
+    for (Hin, R, U) in ((56, 3, 2), (224, 7, 2), (13, 3, 2), (16, 5, 3)):
+        H = (Hin - R) // U + 1
+        p = conv.ConvPlan(1, 64, 32, H, H, R, R, stride=U, in_hw=(Hin, Hin), offline_device=sh)
+        d = p.describe()["problem"]
+        assert (d["U"], d["Hin"], d["Win"], d["H"], d["W"]) == (U, Hin, Hin, H, H)
+        ps = conv.ConvPlan(1, 64, 32, H, H, R, R, stride=U, in_hw=(Hin, Hin), offline_device=sh, path="fp32_simt")
+        assert ps.describe()["tile"]["ver"] == 1
+    assert not lib.conv_plan_create_strided(1, 1, 1, 8, 8, 3, 3, 0)
+    assert "extent must be >= 1" in conv.last_error()
+    assert not lib.conv_plan_create_strided(1, 1, 1, 2, 8, 3, 3, 1)
+    assert "smaller than the kernel" in conv.last_error()
+    with pytest.raises(conv.ConvError) as e:
+        conv.ConvPlan(1, 8, 8, 3, 3, 3, 3, stride=9, in_hw=(21, 21), offline_device=sh, path="bf16")
+    assert e.value.status == conv.CONV_ERR_INFEASIBLE
+    with pytest.raises(ValueError):   # H, W inconsistent with the input extents
+        conv.ConvPlan(1, 8, 8, 5, 5, 3, 3, stride=2, in_hw=(21, 21), offline_device=sh)

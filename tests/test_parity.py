@@ -33,7 +33,7 @@ def coop_ok(sh):
 
 
 def run(shape, inp, ker, path, tile=None):
-    plan = conv.ConvPlan(*shape.as_tuple(), path=path, tile=tile)
+    plan = conv.ConvPlan(*shape.as_tuple(), path=path, tile=tile, **shape.plan_kwargs())
     out = plan.run(inp.cuda(), ker.cuda())
     torch.cuda.synchronize()
     return out.cpu().numpy(), plan
@@ -352,3 +352,50 @@ def test_fused_transform_cuda_graph_replay(path):
         torch.cuda.synchronize()
         ref = oracle.conv_eq1(ROUND[path](inp2.numpy()), ROUND[path](ker2.numpy()))
         assert rel_l2(out.cpu().numpy(), ref) <= 1e-5
+
+
+# ---- stride (PAPER.md:201 footnote; Table 1's * layers) ------
+STRIDED = [
+    Shape.strided(1, 128, 64, 56, 56, 3, 3, 2),     # R4*
+    Shape.strided(1, 128, 64, 56, 56, 1, 1, 2),     # R5*
+    Shape.strided(1, 64, 3, 224, 224, 7, 7, 2),     # R1*
+    Shape.strided(1, 256, 128, 28, 28, 3, 3, 2),    # R7*
+    Shape.strided(2, 40, 17, 13, 11, 3, 2, 2),      # odd extents, (Hin - R) % U != 0
+    Shape.strided(3, 24, 8, 16, 15, 5, 3, 3),       # stride 3
+]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("shape", STRIDED, ids=lambda s: f"{s.N}x{s.K}x{s.C}x{s.Hin}x{s.Win}x{s.R}x{s.S}s{s.U}")
+def test_strided_parity(path, shape):
+    """Strided Eq. 1 on every path against the strided oracle: tolerance on
+    real inputs (and 1e-5 against the oracle on the path's rounded inputs),
+    bit-exact on the integer twin."""
+    inp, ker = make_inputs(shape, seed=61)
+    got, plan = run(shape, inp, ker, path)
+    d = plan.describe()["problem"]
+    assert (d["U"], d["Hin"], d["Win"], d["H"], d["W"]) == (shape.U, shape.Hin, shape.Win, shape.H, shape.W)
+    ref = oracle.conv_eq1_strided(inp.numpy(), ker.numpy(), shape.U)
+    assert got.shape == ref.shape
+    assert rel_l2(got, ref) <= TOL[path]
+    ref_r = oracle.conv_eq1_strided(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), shape.U)
+    assert rel_l2(got, ref_r) <= 1e-5
+    xi, wi = make_inputs(shape, seed=62, kind="int")
+    goti, _ = run(shape, xi, wi, path)
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1_strided(xi.numpy(), wi.numpy(), shape.U))
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_strided_fused_and_cta_groups_bit_identical(path):
+    """A multi-wave strided layer: the fused in-kernel transform and both
+    CTA-group sizes give the same bits as the separate repack."""
+    sh = Shape.strided(160, 128, 64, 28, 28, 3, 3, 2)
+    inp, ker = make_inputs(sh, seed=63)
+    i, k = inp.cuda(), ker.cuda()
+    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1", **sh.plan_kwargs()).run(i, k)
+    for spec in ("fuse=0,cg=2", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0"):
+        out = conv.ConvPlan(*sh.as_tuple(), path=path, tile=spec, **sh.plan_kwargs()).run(i, k)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), spec
+    ref64 = oracle.conv_eq1_strided(ROUND[path](inp.numpy()[:2]), ROUND[path](ker.numpy()), 2)
+    assert rel_l2(ref[:2].cpu().numpy(), ref64) <= 1e-5
