@@ -39,7 +39,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2101_09808_b200.inputs import CONFIGS, Shape, make_inputs  # noqa: E402
+from paper_2101_09808_b200.inputs import CONFIGS, TABLE1, Shape, make_inputs  # noqa: E402
 
 METRIC = "conv TFLOP/s (2*N*K*H*W*C*R*S / time)"
 
@@ -427,12 +427,66 @@ def bench_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def bench_table1(args):
+    """--sweep table1: every conv2d layer of PAPER.md:439 Table 1 (batch 1,
+    stride 1 or 2, Table 1's input extents), one JSON line per layer and
+    path, timed like the headline (CUDA-graph replay of conv_run, L2 flushed
+    before every step outside the event pair, CUDA events, after warm-up).
+    A NEXT-4 study, not the driver's bench line."""
+    from paper_2101_09808_b200 import conv
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    peaks, peak_src = load_peaks()
+    l2 = getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 << 20)
+    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    flush_rd = torch.ones_like(flush)
+    flush_out = torch.empty((), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    paths = [args.path] if args.path != "all" else ["bf16", "tf32", "fp32_simt"]
+    names = [n for n in TABLE1 if not args.layers or n in args.layers.split(",")]
+    for name in names:
+        sh = TABLE1[name]
+        inp, ker = make_inputs(sh, seed=0)
+        d_in, d_ker = inp.to(dev), ker.to(dev)
+        for path in paths:
+            plan = conv.ConvPlan(*sh.as_tuple(), path=path, **sh.plan_kwargs())
+            out, ws = plan.new_output(dev), plan.new_workspace(dev)
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                for _ in range(max(3, args.warmup)):
+                    plan.run(d_in, d_ker, out, ws, stream=cap)
+            cap.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                plan.run(d_in, d_ker, out, ws, stream=cap)
+            torch.cuda.synchronize(dev)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            for i in range(args.steps):
+                flush.zero_()
+                torch.sum(flush_rd, dim=0, out=flush_out)
+                ev[i][0].record(stream)
+                g.replay()
+                ev[i][1].record(stream)
+            torch.cuda.synchronize(dev)
+            ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+            peak, bound, _ = path_peak(plan.path, peaks)
+            roof_us = max(sh.flops / (peak * 1e12), 4.0 * (sh.N * sh.C * sh.Hin * sh.Win + sh.K * sh.C * sh.R * sh.S +
+                                                           sh.N * sh.K * sh.H * sh.W) / (peaks["hbm_gbs"] * 1e9)) * 1e6
+            d = plan.describe()
+            print(json.dumps({
+                "layer": name, "path": plan.path, "K": sh.K, "C": sh.C, "Hin": sh.Hin, "R": sh.R, "U": sh.U,
+                "out": [sh.H, sh.W], "gflop": round(sh.flops / 1e9, 4), "step_us": round(ms * 1e3, 2),
+                "tflops": round(sh.flops / (ms * 1e-3) / 1e12, 3), "roofline_us": round(roof_us, 3),
+                "frac": round(roof_us / (ms * 1e3), 4), "tile": d["tile"], "peak_source": peak_src}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--path", default="bf16", choices=["auto", "fp32_simt", "tf32", "bf16"])
+    ap.add_argument("--path", default="bf16", choices=["auto", "fp32_simt", "tf32", "bf16", "all"])
     ap.add_argument("--config", default="batched", choices=list(CONFIGS))
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--gather", action="store_true")
@@ -441,12 +495,18 @@ def main():
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of extra warm-up steps before timing")
     ap.add_argument("--no-graph", action="store_true", help="time plain stream launches instead of a CUDA graph replay")
     ap.add_argument("--tile", default=None, help="force a tile (conv_plan_set_tile spec, e.g. 'fuse=0,bn=128'); experiments")
+    ap.add_argument("--sweep", default=None, choices=["table1"], help="study mode: every Table-1 layer (one JSON line each)")
+    ap.add_argument("--layers", default=None, help="--sweep: comma-separated layer names (default all)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
-    if args.impl == "reference":
+    if args.sweep:
+        bench_table1(args)
+    elif args.impl == "reference":
         bench_reference(args)
     else:
+        if args.path == "all":
+            raise SystemExit("--path all is for --sweep")
         bench_ours(args)
 
 

@@ -278,6 +278,11 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
             for (int bn : kBNs) {
                 if (force_bn && bn != force_bn) continue;
                 if (!force_bn && bn > 32 && bn / 2 >= pb.K) continue;   // mostly padding
+                // CTA pairs halve the B operand traffic, which is negligible at
+                // BN = 32, while their cluster synchronisation lengthens a
+                // latency-bound k-loop: measured r01b on Table-1 M9 (M = 25,
+                // C*R*S = 9216) 92 us paired vs 53 us single at BN = 32
+                if (cg == 2 && bn < 64 && !force_cg) continue;
                 for (int fuse = 0; fuse <= 1; ++fuse) {
                     if (force_fuse >= 0 ? fuse != force_fuse : (fuse && !L.coop_ok)) continue;
                     const int smax = tc_max_stages(dev, L, bn, cg, kbs, fuse);

@@ -97,6 +97,26 @@ CONFIGS = {
 }
 
 
+# PAPER.md:439-477, Table 1: the 32 conv2d layers of Yolo-9000, ResNet-18 and
+# MobileNet, batch 1, H/W = INPUT extents, stride 2 for the layers marked *.
+# (name, K, C, H/W, R/S, stride).  The MobileNet rows are run as the dense
+# convolutions Table 1 lists (reading R7).
+TABLE1_ROWS = [
+    ("Y0", 32, 3, 544, 3, 1), ("Y2", 64, 32, 272, 3, 1), ("Y4", 128, 64, 136, 3, 1),
+    ("Y5", 64, 128, 136, 1, 1), ("Y8", 256, 128, 68, 3, 1), ("Y9", 128, 256, 68, 1, 1),
+    ("Y12", 512, 256, 34, 3, 1), ("Y13", 256, 512, 34, 1, 1), ("Y18", 1024, 512, 17, 3, 1),
+    ("Y19", 512, 1024, 17, 1, 1), ("Y23", 28269, 1024, 17, 1, 1),
+    ("R1", 64, 3, 224, 7, 2), ("R2", 64, 64, 56, 3, 1), ("R3", 64, 64, 56, 1, 1),
+    ("R4", 128, 64, 56, 3, 2), ("R5", 128, 64, 56, 1, 2), ("R6", 128, 128, 28, 3, 1),
+    ("R7", 256, 128, 28, 3, 2), ("R8", 256, 128, 28, 3, 1), ("R9", 256, 256, 14, 3, 1),
+    ("R10", 512, 256, 14, 3, 2), ("R11", 512, 256, 14, 1, 2), ("R12", 512, 512, 7, 3, 1),
+    ("M1", 32, 32, 112, 3, 1), ("M2", 64, 64, 112, 3, 2), ("M3", 128, 128, 56, 3, 1),
+    ("M4", 128, 128, 56, 3, 2), ("M5", 256, 256, 28, 3, 1), ("M6", 256, 256, 28, 3, 2),
+    ("M7", 512, 512, 14, 3, 1), ("M8", 512, 512, 14, 3, 2), ("M9", 1024, 1024, 7, 3, 1),
+]
+TABLE1 = {name: Shape.strided(1, K, C, HW, HW, R, R, U) for name, K, C, HW, R, U in TABLE1_ROWS}
+
+
 def make_inputs(shape: Shape, seed: int = 0, kind: str = "real"):
     """Return (In, Ker) as contiguous CPU fp32 tensors, In drawn first."""
     g = torch.Generator().manual_seed(int(seed))

@@ -399,3 +399,24 @@ def test_strided_fused_and_cta_groups_bit_identical(path):
         assert torch.equal(out, ref), spec
     ref64 = oracle.conv_eq1_strided(ROUND[path](inp.numpy()[:2]), ROUND[path](ker.numpy()), 2)
     assert rel_l2(ref[:2].cpu().numpy(), ref64) <= 1e-5
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_table1_layers(path):
+    """Every conv2d layer of PAPER.md:439 Table 1 (batch 1, stride 1/2, input
+    extents as listed) on each path against the (strided) oracle: the whole
+    output for layers <= 0.3 GFLOP, 64 sampled points for the larger ones."""
+    from paper_2101_09808_b200.inputs import TABLE1
+    rng = np.random.default_rng(70)
+    for name, sh in TABLE1.items():
+        inp, ker = make_inputs(sh, seed=71)
+        got, _ = run(sh, inp, ker, path)
+        x, w = inp.numpy(), ker.numpy()
+        if sh.flops <= 3e8:
+            ref = oracle.conv_eq1_strided(x, w, sh.U)
+            assert rel_l2(got, ref) <= TOL[path], name
+        else:
+            pts = [(0, rng.integers(sh.K), rng.integers(sh.H), rng.integers(sh.W)) for _ in range(64)]
+            ref = np.array([oracle.conv_eq1_point(x, w, *p, stride=sh.U) for p in pts])
+            g = np.array([got[p] for p in pts], dtype=np.float64)
+            assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= TOL[path], name
