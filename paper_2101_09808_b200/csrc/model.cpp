@@ -168,6 +168,7 @@ static const double kClockHz = 1.84e9;   // SM clock measured under tcgen05 load
 // timeline trace): one 128 x N x 32-byte-K MMA takes max(N/2, 48) cycles on
 // an SM; every pipeline stage adds ~150 cycles of barrier / commit bubble.
 static const double kStageBubbleClk = 150.0;
+static const double kStageLatClk = 800.0;
 static const double kEpiStoreBW = 5.0e12;  // bytes/s the whole chip's epilogues drain at
 // fused transform (measured r01b, batched layer): 67 MB of fp32 In in ~35 us
 // per 148 CTAs while the MMAs run, 9% MMA slowdown, ~6 us startup chain
@@ -194,7 +195,10 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     const double tiles_per_unit = ceil((double)r.tiles / units);
     const double stages_per_tile = (double)pb.R * pb.S * L.n_cblk / t.kbs;   // k_iters / kbs
     const double mma_clk = std::max(t.bn / 2.0, 48.0);
-    const double stage_clk = t.kbs * (L.sw / 32.0) * mma_clk + kStageBubbleClk;
+    // a stage also cannot turn over faster than the producer -> TMA -> MMA
+    // -> commit round trip allows (kStageLatClk, r01b selector study: on
+    // long-K few-tile layers time scales with the number of stages)
+    const double stage_clk = std::max(t.kbs * (L.sw / 32.0) * mma_clk + kStageBubbleClk, kStageLatClk);
     const double t_pipe_us = tiles_per_unit * stages_per_tile * stage_clk / kClockHz * 1e6;
     const double kblocks_per_sm = (double)r.tiles * pb.R * pb.S * L.n_cblk / units;
     const double t_smem_us = kblocks_per_sm * 2.0 * (128.0 + (double)t.bn / t.cg) * L.sw /
@@ -286,8 +290,11 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
                 for (int fuse = 0; fuse <= 1; ++fuse) {
                     if (force_fuse >= 0 ? fuse != force_fuse : (fuse && !L.coop_ok)) continue;
                     const int smax = tc_max_stages(dev, L, bn, cg, kbs, fuse);
-                    // at least 3 stages unless forced (2 cannot overlap load and MMA well)
-                    if (smax < (force_stages || force_kbs ? 2 : 3)) continue;
+                    // at least 4 k-blocks in flight (3 stages of 1-2 k-blocks, 2 of
+                    // 4) unless forced: fewer cannot overlap loads and MMAs well.
+                    // (r01b selector study: kbs = 4 x 2 stages is the measured
+                    // best on the tiny-M Table-1 layers M7, M9, R12, Y12.)
+                    if (smax < (force_stages || force_kbs ? 2 : (kbs >= 4 ? 2 : 3))) continue;
                     TcTile t;
                     t.bn = bn;
                     t.cg = cg;
