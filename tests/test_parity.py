@@ -420,3 +420,65 @@ def test_table1_layers(path):
             ref = np.array([oracle.conv_eq1_point(x, w, *p, stride=sh.U) for p in pts])
             g = np.array([got[p] for p in pts], dtype=np.float64)
             assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= TOL[path], name
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_run_host_fused_chunks_bit_identical(path):
+    """conv_run_host splits the batch into image chunks; with a fused plan each
+    chunk is a fused sub-problem whose flags the chunk's Ker launch clears on
+    the shared flag region: results equal the device run bit for bit, twice."""
+    sh = Shape(N=24, K=96, C=128, H=14, W=14, R=3, S=3)
+    inp, ker = make_inputs(sh, seed=81)
+    plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=1")
+    assert plan.describe()["tile"]["fuse"] == 1
+    dev_out = plan.run(inp.cuda(), ker.cuda())
+    sep = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0").run(inp.cuda(), ker.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(dev_out, sep)
+    dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device="cuda")
+    out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        out_h.zero_()
+        plan.run_host(inp.pin_memory(), ker.pin_memory(), out_h, dbuf)
+        torch.cuda.synchronize()
+        assert np.array_equal(out_h.numpy(), dev_out.cpu().numpy())
+
+
+FUSE_EDGE = [
+    Shape(N=1, K=40, C=72, H=120, W=60, R=3, S=3),      # one image, several waves, C % 64 != 0, K tail
+    Shape(N=9, K=200, C=24, H=18, W=22, R=5, S=1),      # small C (sub-128-B k-blocks), R != S
+    Shape.strided(12, 64, 96, 30, 30, 3, 3, 2),         # strided + fused
+]
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", FUSE_EDGE, ids=lambda s: f"{s.N}x{s.K}x{s.C}x{s.Hin}x{s.Win}x{s.R}x{s.S}s{s.U}")
+def test_fused_edge_shapes_and_graph_replay(path, shape):
+    """Fused transform on awkward shapes, replayed from a CUDA graph with new
+    input values: equal to the separate repack bit for bit, and to the oracle
+    on the rounded inputs."""
+    assert coop_ok(Shape(shape.N, shape.K, shape.C, shape.Hin - shape.R + 1, shape.Win - shape.S + 1, shape.R, shape.S))
+    kw = shape.plan_kwargs()
+    plan = conv.ConvPlan(*shape.as_tuple(), path=path, tile="fuse=1", **kw)
+    sep = conv.ConvPlan(*shape.as_tuple(), path=path, tile="fuse=0", **kw)
+    inp, ker = make_inputs(shape, seed=82)
+    i, k = inp.cuda(), ker.cuda()
+    out, ws = plan.new_output(), plan.new_workspace()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.run(i, k, out, ws, stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.run(i, k, out, ws, stream=s)
+    for seed in (83, 84):
+        inp2, ker2 = make_inputs(shape, seed=seed)
+        i.copy_(inp2)
+        k.copy_(ker2)
+        g.replay()
+        ref = sep.run(i, k)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+    ref64 = oracle.conv_eq1_strided(ROUND[path](inp2.numpy()), ROUND[path](ker2.numpy()), shape.U)
+    assert rel_l2(out.cpu().numpy(), ref64) <= 1e-5
