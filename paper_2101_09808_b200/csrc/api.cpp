@@ -304,7 +304,8 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
         }
         if (fbn && fbn != 32 && fbn != 64 && fbn != 128 && fbn != 192 && fbn != 256)
             return fail(CONV_ERR_INFEASIBLE, "bn must be one of 32, 64, 128, 192, 256");
-        if (fkbs && fkbs != 1 && fkbs != 2 && fkbs != 4) return fail(CONV_ERR_INFEASIBLE, "kbs must be 1, 2 or 4");
+        if (fkbs && fkbs != 1 && fkbs != 2 && fkbs != 3 && fkbs != 4 && fkbs != 6)
+            return fail(CONV_ERR_INFEASIBLE, "kbs must be 1, 2, 3, 4 or 6");
         if (fcg && fcg != 1 && fcg != 2) return fail(CONV_ERR_INFEASIBLE, "cg must be 1 or 2");
     }
     const int obn = p->force_bn, ost = p->force_stages, ocg = p->force_cg, okbs = p->force_kbs, ofuse = p->force_fuse,

@@ -276,7 +276,7 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
     bool found = false;
     for (int cg = 1; cg <= 2; ++cg) {
         if (force_cg && cg != force_cg) continue;
-        for (int kbs = 1; kbs <= 4; kbs *= 2) {
+        for (int kbs : {1, 2, 3, 4, 6}) {               // k-blocks per stage; must divide the k loop
             if (force_kbs && kbs != force_kbs) continue;
             if ((pb.R * pb.S * L.n_cblk) % kbs) continue;
             for (int bn : kBNs) {

@@ -132,7 +132,7 @@ def test_p10_tile_invariance_tensor(path):
     inp, ker = make_inputs(sh, seed=7)
     outs = []
     for cg in (1, 2):
-        for bn, kbs, fuse in ((32, 1, 0), (64, 2, 1), (128, 4, 0), (192, 1, 1), (256, 2, 1)):
+        for bn, kbs, fuse in ((32, 1, 0), (64, 2, 1), (128, 4, 0), (192, 1, 1), (256, 2, 1), (64, 3, 0), (128, 6, 1)):
             try:
                 got, plan = run(sh, inp, ker, path, tile=f"bn={bn},cg={cg},kbs={kbs},fuse={fuse}")
             except conv.ConvError as e:           # e.g. kbs=4 stages do not fit smem
