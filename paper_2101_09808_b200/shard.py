@@ -18,7 +18,7 @@ runs in libconv.so.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 from .inputs import Shape
 
@@ -47,14 +47,14 @@ def shard(shape: Shape, world: int, rank: int, dim: str = "auto") -> ShardSpec:
         if shape.N % world:
             raise ValueError(f"N={shape.N} is not divisible by world={world}")
         step = shape.N // world
-        local = Shape(step, shape.K, shape.C, shape.H, shape.W, shape.R, shape.S)
+        local = replace(shape, N=step)          # keeps the stride and input extents
     elif dim == "k":
         if shape.N != 1:
             raise ValueError("k-sharding is supported for N == 1 only (gathered buffer stays NCHW)")
         if shape.K % world:
             raise ValueError(f"K={shape.K} is not divisible by world={world}")
         step = shape.K // world
-        local = Shape(shape.N, step, shape.C, shape.H, shape.W, shape.R, shape.S)
+        local = replace(shape, K=step)
     else:
         raise ValueError(f"unknown shard dim {dim!r}")
     return ShardSpec(dim, world, rank, rank * step, (rank + 1) * step, local)

@@ -482,3 +482,22 @@ def test_fused_edge_shapes_and_graph_replay(path, shape):
         assert torch.equal(out, ref)
     ref64 = oracle.conv_eq1_strided(ROUND[path](inp2.numpy()), ROUND[path](ker2.numpy()), shape.U)
     assert rel_l2(out.cpu().numpy(), ref64) <= 1e-5
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_p10_k_shards_and_strided_shards_bit_identical(path):
+    """k-shards (N = 1, SURVEY Sec. 8(e) secondary split) and n-shards of a
+    strided layer equal the slices of the 1-GPU result bit for bit: each
+    rank's plan may re-tile, the k-order per output does not change (P10)."""
+    from paper_2101_09808_b200.shard import local_inputs, shard
+    for sh, dim, worlds in ((Shape(N=1, K=256, C=64, H=28, W=28, R=3, S=3), "k", (2, 4)),
+                            (Shape.strided(8, 64, 32, 29, 29, 3, 3, 2), "n", (2, 4))):
+        inp, ker = make_inputs(sh, seed=95)
+        full, _ = run(sh, inp, ker, path)
+        for world in worlds:
+            for r in range(world):
+                spec = shard(sh, world, r, dim=dim)
+                li, lk = local_inputs(spec, inp, ker)
+                got, _ = run(spec.local, li, lk, path)
+                ref = full[spec.start:spec.stop] if dim == "n" else full[:, spec.start:spec.stop]
+                assert np.array_equal(got, ref), (dim, world, r)

@@ -33,6 +33,13 @@ def test_shard_auto_picks_k_for_small_batch():
     assert s.dim == "k" and (s.start, s.stop) == (16, 32) and s.local.K == 16
 
 
+def test_shard_keeps_stride_and_input_extents():
+    sh = Shape.strided(8, 64, 32, 29, 29, 3, 3, 2)
+    for dim, world in (("n", 4), ("k", 2)):
+        loc = shard(sh if dim == "n" else Shape.strided(1, 64, 32, 29, 29, 3, 3, 2), world, 1, dim=dim).local
+        assert (loc.U, loc.Hin, loc.Win, loc.H, loc.W) == (2, 29, 29, 14, 14)
+
+
 def test_shard_errors():
     with pytest.raises(ValueError):
         shard(Shape(N=3, K=4, C=1, H=1, W=1, R=1, S=1), 2, 0, dim="n")
