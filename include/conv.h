@@ -18,6 +18,11 @@
  *     Out[n,k,h,w] = sum_{c,r,s} In[n,c,U*h+r,U*w+s] * Ker[k,c,r,s]
  *
  * with explicit INPUT extents Hin x Win and H = (Hin-R)/U + 1 (floor).
+ * conv_plan_create_dilated adds dilation D (the footnote's other case):
+ *
+ *     Out[n,k,h,w] = sum_{c,r,s} In[n,c,U*h+D*r,U*w+D*s] * Ker[k,c,r,s]
+ *
+ * with H = (Hin - D*(R-1) - 1)/U + 1 (floor), likewise W.
  * Internal layout
  * transforms are part of every conv_run, as the paper counts them
  * (PAPER.md:371).
@@ -90,6 +95,17 @@ CONV_API conv_plan* conv_plan_create(int N, int K, int C, int H, int W, int R, i
  * smaller than the kernel. */
 CONV_API conv_plan* conv_plan_create_strided(int N, int K, int C, int Hin, int Win, int R, int S, int U);
 
+/* Strided and dilated plan (PAPER.md:201 footnote 1): as
+ * conv_plan_create_strided plus dilation D >= 1 on both axes -- tap (r, s)
+ * reads input row U*h + D*r, column U*w + D*s; H = (Hin - D*(R-1) - 1)/U + 1,
+ * W = (Win - D*(S-1) - 1)/U + 1.  D = 1 is conv_plan_create_strided.
+ * Paths: the tensor-core paths (tap (r, s) is the TMA im2col offset
+ * (D*s, D*r); needs D*(R-1), D*(S-1) <= 128) and FP32 SIMT v1; SIMT v2
+ * needs U = D = 1.  Errors as conv_plan_create_strided, plus
+ * INVALID_ARGUMENT if D < 1 or the input is smaller than the dilated kernel
+ * (D*(R-1)+1) x (D*(S-1)+1). */
+CONV_API conv_plan* conv_plan_create_dilated(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D);
+
 /* A plan for a described (not present) device: `sms` SMs, `smem_optin` bytes
  * of opt-in shared memory per block, `l2_bytes` of L2.  Runs the same
  * selector; the plan can be described but not run (conv_run returns
@@ -100,6 +116,9 @@ CONV_API conv_plan* conv_plan_create_offline(int N, int K, int C, int H, int W, 
 /* Offline variant of conv_plan_create_strided (same arguments as above). */
 CONV_API conv_plan* conv_plan_create_strided_offline(int N, int K, int C, int Hin, int Win, int R, int S, int U,
                                                      int sms, size_t smem_optin, size_t l2_bytes);
+/* Offline variant of conv_plan_create_dilated (same arguments as above). */
+CONV_API conv_plan* conv_plan_create_dilated_offline(int N, int K, int C, int Hin, int Win, int R, int S, int U,
+                                                     int D, int sms, size_t smem_optin, size_t l2_bytes);
 
 /* Force a path (default AUTO) and re-run the selector for it.
  * INFEASIBLE if no candidate of that path fits (e.g. R or S > 128 on the
@@ -170,6 +189,11 @@ CONV_API conv_status conv_run_host(const conv_plan* plan, const float* in_host, 
 
 /* Thread-local message for the last failing call on this thread ("" if none). */
 CONV_API const char* conv_last_error(void);
+
+/* Thread-local status code of that failing call (CONV_OK if none) -- how a
+ * caller tells INVALID_ARGUMENT / INFEASIBLE / UNSUPPORTED_DEVICE apart when
+ * a conv_plan_create* call returns NULL. */
+CONV_API conv_status conv_last_status(void);
 
 /* Library version string, e.g. "0.1.0 sm_100a". */
 CONV_API const char* conv_version(void);

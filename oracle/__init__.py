@@ -19,6 +19,11 @@ Functions and the passage each follows:
                          stride-U output = stride-1 output subsampled (exact),
                          torch conv2d f64 with stride, a hand-worked golden,
                          brute-force points.
+* ``conv_eq1_dilated`` -- stride U and dilation D (PAPER.md:201 footnote):
+                         In[n,c,U*h+D*r,U*w+D*s]; plain C.  Pinned: D = 1 is
+                         conv_eq1_strided; = the strided oracle with a
+                         zero-inserted kernel, bit for bit; torch conv2d f64
+                         with dilation; brute-force points.
 * ``conv_eq1_point``  -- one output element of Eq. 1 as the correctly rounded
                          sum (``math.fsum``) of its C*R*S exact products; used
                          for sampled parity at full sizes.  Pinned against
@@ -69,6 +74,9 @@ def _load():
                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
             lib.oracle_conv_eq1_strided.restype = ctypes.c_int
             lib.oracle_conv_eq1_strided.argtypes = [ctypes.c_int] * 8 + [
+                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+            lib.oracle_conv_eq1_dilated.restype = ctypes.c_int
+            lib.oracle_conv_eq1_dilated.argtypes = [ctypes.c_int] * 9 + [
                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
             lib.oracle_num_threads.restype = ctypes.c_int
             lib.oracle_num_threads.argtypes = [ctypes.c_int]
@@ -131,11 +139,37 @@ def conv_eq1_strided(inp: np.ndarray, ker: np.ndarray, stride: int, nthreads: in
     return out
 
 
-def conv_eq1_point(inp: np.ndarray, ker: np.ndarray, n: int, k: int, h: int, w: int, stride: int = 1) -> float:
-    """Out[n,k,h,w] of Eq. 1 (stride U) as the correctly rounded sum of its
-    exact products (each fp32*fp32 product is exact in float64)."""
+def conv_eq1_dilated(inp: np.ndarray, ker: np.ndarray, stride: int, dilation: int, nthreads: int = 0) -> np.ndarray:
+    """Eq. 1 with stride U and dilation D, no padding.  ``inp``: fp32
+    [N,C,Hin,Win]; ``ker``: fp32 [K,C,R,S].  Returns float64 [N,K,H,W] with
+    H = (Hin - D*(R-1) - 1)//U + 1, likewise W."""
+    inp = np.ascontiguousarray(inp, dtype=np.float32)
+    ker = np.ascontiguousarray(ker, dtype=np.float32)
+    if inp.ndim != 4 or ker.ndim != 4 or inp.shape[1] != ker.shape[1]:
+        raise ValueError("expected In [N,C,Hin,Win] and Ker [K,C,R,S] with equal C")
+    N, C, Hin, Win = inp.shape
+    K, _, R, S = ker.shape
+    if stride < 1 or dilation < 1 or Hin < dilation * (R - 1) + 1 or Win < dilation * (S - 1) + 1:
+        raise ValueError("bad stride/dilation or input smaller than the dilated kernel")
+    H = (Hin - dilation * (R - 1) - 1) // stride + 1
+    W = (Win - dilation * (S - 1) - 1) // stride + 1
+    out = np.empty((N, K, H, W), dtype=np.float64)
+    rc = _load().oracle_conv_eq1_dilated(N, K, C, Hin, Win, R, S, stride, dilation,
+                                         inp.ctypes.data, ker.ctypes.data, out.ctypes.data,
+                                         nthreads or host_threads())
+    if rc != 0:
+        raise ValueError("oracle_conv_eq1_dilated rejected its arguments")
+    return out
+
+
+def conv_eq1_point(inp: np.ndarray, ker: np.ndarray, n: int, k: int, h: int, w: int, stride: int = 1,
+                   dilation: int = 1) -> float:
+    """Out[n,k,h,w] of Eq. 1 (stride U, dilation D) as the correctly rounded
+    sum of its exact products (each fp32*fp32 product is exact in float64)."""
     R, S = ker.shape[2], ker.shape[3]
-    window = inp[n, :, stride * h:stride * h + R, stride * w:stride * w + S].astype(np.float64)
+    d = dilation
+    window = inp[n, :, stride * h:stride * h + d * (R - 1) + 1:d,
+                 stride * w:stride * w + d * (S - 1) + 1:d].astype(np.float64)
     prods = window * ker[k].astype(np.float64)
     return math.fsum(prods.ravel().tolist())
 

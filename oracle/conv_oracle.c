@@ -112,6 +112,50 @@ int oracle_conv_eq1_strided(int N, int K, int C, int Hin, int Win, int R, int S,
     return 0;
 }
 
+/*
+ * Strided and dilated Eq. 1 (PAPER.md:201 footnote: "we do not show
+ * stride/dilation, but the methodology is applicable to the general case"):
+ *
+ *     Out[n,k,h,w] = sum_{c,r,s} In[n,c,U*h+D*r,U*w+D*s] * Ker[k,c,r,s]
+ *
+ * In [N][C][Hin][Win], H = (Hin - D*(R-1) - 1)/U + 1 (floor), likewise W.
+ * Same Listing-2 loop order, double accumulation and (n,k)-plane
+ * parallelism as oracle_conv_eq1.  Returns 0, or 1 on a bad extent / NULL.
+ */
+int oracle_conv_eq1_dilated(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D,
+                            const float* in, const float* ker, double* out, int nthreads)
+{
+    if (N < 1 || K < 1 || C < 1 || R < 1 || S < 1 || U < 1 || D < 1) return 1;
+    if ((int64_t)Hin < (int64_t)D * (R - 1) + 1 || (int64_t)Win < (int64_t)D * (S - 1) + 1) return 1;
+    if (!in || !ker || !out) return 1;
+    const int64_t H = ((int64_t)Hin - (int64_t)D * (R - 1) - 1) / U + 1;
+    const int64_t W = ((int64_t)Win - (int64_t)D * (S - 1) - 1) / U + 1;
+    const int64_t planes = (int64_t)N * K;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t nk = 0; nk < planes; ++nk) {
+        const int64_t n = nk / K;
+        const int64_t k = nk % K;
+        double* acc = out + nk * H * W;
+        for (int64_t i = 0; i < H * W; ++i) acc[i] = 0.0;
+        for (int64_t c = 0; c < C; ++c)
+            for (int64_t r = 0; r < R; ++r)
+                for (int64_t s = 0; s < S; ++s) {
+                    const double kv = (double)ker[((k * C + c) * R + r) * S + s];
+                    const float* in_rs = in + ((n * C + c) * (int64_t)Hin + D * r) * Win + D * s;
+                    for (int64_t h = 0; h < H; ++h)
+                        for (int64_t w = 0; w < W; ++w)
+                            acc[h * W + w] += (double)in_rs[(U * h) * (int64_t)Win + U * w] * kv;
+                }
+    }
+    return 0;
+}
+
 /* Number of OpenMP threads a parallel region would use (for reporting). */
 int oracle_num_threads(int nthreads)
 {

@@ -29,10 +29,11 @@ PATH_NAMES = {v: k for k, v in PATHS.items()}
 # Every symbol include/conv.h declares (tests check the library exports them).
 EXPORTED = (
     "conv_plan_create", "conv_plan_create_offline", "conv_plan_create_strided", "conv_plan_create_strided_offline",
+    "conv_plan_create_dilated", "conv_plan_create_dilated_offline",
     "conv_plan_set_path", "conv_plan_set_tile", "conv_plan_workspace_bytes",
     "conv_plan_num_kernels", "conv_plan_path", "conv_plan_describe", "conv_plan_destroy",
     "conv_run", "conv_run_events", "conv_plan_host_run_bytes", "conv_run_host",
-    "conv_last_error", "conv_version", "conv_model_dv", "conv_model_dv_matmul",
+    "conv_last_error", "conv_last_status", "conv_version", "conv_model_dv", "conv_model_dv_matmul",
     "conv_model_footprint",
 )
 
@@ -63,6 +64,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "conv_plan_create_offline": (vp, [i] * 8 + [sz, sz]),
             "conv_plan_create_strided": (vp, [i] * 8),
             "conv_plan_create_strided_offline": (vp, [i] * 9 + [sz, sz]),
+            "conv_plan_create_dilated": (vp, [i] * 9),
+            "conv_plan_create_dilated_offline": (vp, [i] * 10 + [sz, sz]),
             "conv_plan_set_path": (i, [vp, i]),
             "conv_plan_set_tile": (i, [vp, ctypes.c_char_p]),
             "conv_plan_workspace_bytes": (sz, [vp]),
@@ -75,6 +78,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "conv_plan_host_run_bytes": (sz, [vp]),
             "conv_run_host": (i, [vp, vp, vp, vp, vp, vp]),
             "conv_last_error": (ctypes.c_char_p, []),
+            "conv_last_status": (ctypes.c_int, []),
             "conv_version": (ctypes.c_char_p, []),
             "conv_model_dv": (d, [ctypes.POINTER(i), ctypes.POINTER(d), ctypes.POINTER(d), ctypes.POINTER(d)]),
             "conv_model_dv_matmul": (d, [ctypes.POINTER(i), ctypes.POINTER(d), ctypes.POINTER(d)]),
@@ -115,43 +119,43 @@ def _stream_handle(stream) -> Optional[int]:
 
 class ConvPlan:
     """A plan for Eq. 1 with OUTPUT extents H x W; with
-    ``stride`` U > 1 (or explicit ``in_hw``) the strided form
-    Out[n,k,h,w] = sum In[n,c,U*h+r,U*w+s] Ker[k,c,r,s] (conv_plan_create_strided)."""
+    ``stride`` U > 1, ``dilation`` D > 1 (or explicit ``in_hw``) the general form
+    Out[n,k,h,w] = sum In[n,c,U*h+D*r,U*w+D*s] Ker[k,c,r,s] (conv_plan_create_dilated)."""
 
     def __init__(self, N: int, K: int, C: int, H: int, W: int, R: int, S: int,
                  path: str = "auto", tile: Optional[str] = None, offline_device: Optional[dict] = None,
-                 stride: int = 1, in_hw: Optional[tuple] = None):
+                 stride: int = 1, in_hw: Optional[tuple] = None, dilation: int = 1):
         """``offline_device`` = dict(sms=, smem_optin=, l2_bytes=) plans for a
         described device without touching CUDA (describe-only plan).
         ``in_hw`` = (Hin, Win) input extents of a strided plan (default the
-        minimal ((H-1)*U+R, (W-1)*U+S)); H, W must equal the floor output
-        extents (Hin-R)//U+1, (Win-S)//U+1."""
+        minimal ((H-1)*U+D*(R-1)+1, (W-1)*U+D*(S-1)+1)); H, W must equal the
+        floor output extents (Hin-D*(R-1)-1)//U+1, likewise W."""
         lib = load_library()
         self._lib = lib
-        strided = stride != 1 or in_hw is not None
+        strided = stride != 1 or dilation != 1 or in_hw is not None
+        Re, Se = dilation * (R - 1) + 1, dilation * (S - 1) + 1     # dilated kernel extents
         if strided:
-            Hin, Win = in_hw if in_hw is not None else ((H - 1) * stride + R, (W - 1) * stride + S)
-            if stride >= 1 and Hin >= R and Win >= S and ((Hin - R) // stride + 1, (Win - S) // stride + 1) != (H, W):
-                raise ValueError(f"output {H}x{W} does not match input {Hin}x{Win}, kernel {R}x{S}, stride {stride}")
+            Hin, Win = in_hw if in_hw is not None else ((H - 1) * stride + Re, (W - 1) * stride + Se)
+            if (stride >= 1 and dilation >= 1 and Hin >= Re and Win >= Se
+                    and ((Hin - Re) // stride + 1, (Win - Se) // stride + 1) != (H, W)):
+                raise ValueError(f"output {H}x{W} does not match input {Hin}x{Win}, kernel {R}x{S}, "
+                                 f"stride {stride}, dilation {dilation}")
         else:
             Hin, Win = H + R - 1, W + S - 1
         self.shape = (N, K, C, H, W, R, S)
         self.stride = stride
+        self.dilation = dilation
         self.in_hw = (Hin, Win)
         if offline_device is not None:
             d = offline_device
             dev = (int(d["sms"]), int(d["smem_optin"]), int(d["l2_bytes"]))
-            h = (lib.conv_plan_create_strided_offline(N, K, C, Hin, Win, R, S, stride, *dev) if strided
+            h = (lib.conv_plan_create_dilated_offline(N, K, C, Hin, Win, R, S, stride, dilation, *dev) if strided
                  else lib.conv_plan_create_offline(N, K, C, H, W, R, S, *dev))
         else:
-            h = (lib.conv_plan_create_strided(N, K, C, Hin, Win, R, S, stride) if strided
+            h = (lib.conv_plan_create_dilated(N, K, C, Hin, Win, R, S, stride, dilation) if strided
                  else lib.conv_plan_create(N, K, C, H, W, R, S))
         if not h:
-            msg = last_error()
-            status = CONV_ERR_UNSUPPORTED_DEVICE if ("device" in msg and "extent" not in msg) else CONV_ERR_INVALID_ARGUMENT
-            if "no " in msg and "tile" in msg:
-                status = CONV_ERR_INFEASIBLE
-            raise ConvError(status, msg)
+            raise ConvError(lib.conv_last_status(), last_error())
         self._h = ctypes.c_void_p(h)
         self._shapes_cache = tuple(self._shapes_sizes())
         if path != "auto":

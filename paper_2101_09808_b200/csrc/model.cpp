@@ -265,7 +265,10 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
                int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, int force_pre_c,
                std::string& why) {
     const TcLayout L = tc_layout(pb, bf16);
-    if (pb.R > 128 || pb.S > 128) { why = "R, S > 128: TMA im2col offsets are limited to [-128, 127]"; return false; }
+    if ((int64_t)pb.D * (pb.R - 1) > 128 || (int64_t)pb.D * (pb.S - 1) > 128) {
+        why = "D*(R-1), D*(S-1) > 128: the TMA im2col bounding box of a 4-D map is limited to [-128, 127]";
+        return false;
+    }
     if (pb.U > 8) { why = "stride > 8: the TMA im2col traversal stride is limited to 8"; return false; }
     if (pb.M() + 256 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
     if (force_fuse == 1 && !L.coop_ok) {
@@ -373,11 +376,11 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // one chunk: every thread's FFMAs, plus the cp.async copies (one per 4-B
     // element in v1/v2 In rows, ~6 instructions each, spread over the CTA)
     const double fma_chunk_cta = (double)threads * t.tk * t.tw * t.bc * pb.R * pb.S * issue_factor;
-    const double in_elems_chunk = (double)t.bc * t.tn * ((t.th - 1) * pb.U + pb.R) * pb.Win();
+    const double in_elems_chunk = (double)t.bc * t.tn * pb.rows_span(t.th) * pb.Win();
     // v2 copies 16-B units from a per-thread plan when they fit 4 per thread;
     // beyond that a per-row loop of 4-B copies runs (~2.3x slower layer
     // measured r01b)
-    const double units_v2 = (double)t.bc * t.tn * ((t.th - 1) * pb.U + pb.R) * (pb.Win() % 4 == 0 ? pb.Win() / 4.0 : pb.Win());
+    const double units_v2 = (double)t.bc * t.tn * pb.rows_span(t.th) * (pb.Win() % 4 == 0 ? pb.Win() / 4.0 : pb.Win());
     const double copy_unit = (t.ver == 2 && units_v2 > 4.0 * threads) ? 6.0 * 4.0 : 6.0;
     const double copy_chunk_cta = in_elems_chunk * copy_unit + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak

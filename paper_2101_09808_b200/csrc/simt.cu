@@ -51,7 +51,8 @@ struct SimtParams {
     int Hin, Win, HW, RS;
     int tn, th, bc, kg;
     int bko;          // kg * TK
-    int rows_in;      // (th - 1) * U + R
+    int D;            // dilation (v1 only): tap (r, s) reads rows / columns D*r, D*s further
+    int rows_in;      // (th - 1) * U + D * (R - 1) + 1
     int plane;        // tn * rows_in * Win  (floats per channel in smem)
     int n_htiles;     // ceil(H / th)
     int nchunks;      // ceil(C / bc)
@@ -182,12 +183,12 @@ __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict_
         const int cc_end = p.C - chunk * p.bc < p.bc ? p.C - chunk * p.bc : p.bc;
         for (int cc = 0; cc < cc_end; ++cc) {
             for (int r = 0; r < p.R; ++r) {
-                const float* ip = in_s + cc * p.plane + r * p.Win;
+                const float* ip = in_s + cc * p.plane + r * p.D * p.Win;
                 const float* kp = ker_s + ((cc * p.R + r) * p.S) * p.bko + kgi * TK;
                 for (int s = 0; s < p.S; ++s) {
                     float iv[TW];
 #pragma unroll
-                    for (int j = 0; j < TW; ++j) iv[j] = ip[off[j] + s];
+                    for (int j = 0; j < TW; ++j) iv[j] = ip[off[j] + s * p.D];
                     float kv[TK];
 #pragma unroll
                     for (int i = 0; i < TK; i += 4) {
@@ -413,7 +414,7 @@ bool simt_tile_supported(const SimtTile& t) {
     return t.kg >= 1 && t.pw >= 1 && threads <= 512 && t.tn >= 1 && t.th >= 1 && t.bc >= 1;
 }
 
-bool simt_v2_ok(const Problem& pb) { return pb.U == 1 && (pb.S == 1 || pb.S == 3); }
+bool simt_v2_ok(const Problem& pb) { return pb.U == 1 && pb.D == 1 && (pb.S == 1 || pb.S == 3); }
 
 // Row mode (TW = 7 or 14): one thread per output row, allowed only when the
 // row is exactly that wide (its window then starts 16-B aligned at w = 0).
@@ -440,7 +441,7 @@ int simt2_pitch(const Problem& pb, const SimtTile& t) {
 
 size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
     const size_t row = t.ver == 2 ? (size_t)simt2_pitch(pb, t) : (size_t)pb.Win();
-    const size_t plane = (size_t)t.tn * ((t.th - 1) * pb.U + pb.R) * row;
+    const size_t plane = (size_t)t.tn * pb.rows_span(t.th) * row;
     const size_t in_stage = (size_t)t.bc * plane;
     const size_t ker_stage = (size_t)t.bc * pb.R * pb.S * t.kg * t.tk;
     return 2 * (in_stage + ker_stage) * sizeof(float);
@@ -514,18 +515,18 @@ size_t simt_ws_bytes(const Problem& pb, const SimtTile& t) {
 cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, const float* ker,
                      float* out, void* ws, cudaStream_t st, cudaEvent_t* ev, std::string& err) {
     SimtParams p;
-    p.N = pb.N; p.K = pb.K; p.C = pb.C; p.H = pb.H; p.W = pb.W; p.R = pb.R; p.S = pb.S; p.U = pb.U;
+    p.N = pb.N; p.K = pb.K; p.C = pb.C; p.H = pb.H; p.W = pb.W; p.R = pb.R; p.S = pb.S; p.U = pb.U; p.D = pb.D;
     p.Hin = (int)pb.Hin(); p.Win = (int)pb.Win(); p.HW = pb.H * pb.W; p.RS = pb.R * pb.S;
     p.tn = t.tn; p.th = t.th; p.bc = t.bc; p.kg = t.kg;
     p.bko = t.kg * t.tk;
-    p.rows_in = (t.th - 1) * pb.U + pb.R;
+    p.rows_in = (int)pb.rows_span(t.th);
     p.plane = t.tn * p.rows_in * p.Win;
     p.n_htiles = (pb.H + t.th - 1) / t.th;
     p.nchunks = (pb.C + t.bc - 1) / t.bc;
     p.bp = t.tn * t.th * pb.W;
     p.vec4_in = (p.Win % 4 == 0) ? 1 : 0;
     if (t.ver != 2 && p.bp > t.pw * 32 * t.tw) { err = "SIMT tile: pixel slots < tn*th*W"; return cudaErrorInvalidValue; }
-    if (t.ver == 2 && pb.U != 1) { err = "SIMT v2 needs stride 1"; return cudaErrorInvalidValue; }
+    if (t.ver == 2 && (pb.U != 1 || pb.D != 1)) { err = "SIMT v2 needs stride 1, dilation 1"; return cudaErrorInvalidValue; }
 
     float* kerp = static_cast<float*>(ws);
     const int64_t total = (int64_t)((pb.K + p.bko - 1) / p.bko) * p.bko * pb.C * p.RS;

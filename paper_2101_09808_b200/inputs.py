@@ -25,10 +25,10 @@ import torch
 
 @dataclass(frozen=True)
 class Shape:
-    """H, W are OUTPUT extents.  U is the stride (PAPER.md:201 footnote;
-    Table 1's * layers); hin/win are explicit input extents of a strided
-    layer (0: the minimal (H-1)*U + R).  Use ``Shape.strided`` to build one
-    from input extents as Table 1 lists them."""
+    """H, W are OUTPUT extents.  U is the stride and D the dilation
+    (PAPER.md:201 footnote; Table 1's * layers); hin/win are explicit input
+    extents of a strided layer (0: the minimal (H-1)*U + D*(R-1) + 1).  Use
+    ``Shape.strided`` to build one from input extents as Table 1 lists them."""
     N: int
     K: int
     C: int
@@ -39,24 +39,29 @@ class Shape:
     U: int = 1
     hin: int = 0
     win: int = 0
+    D: int = 1
 
     @classmethod
-    def strided(cls, N, K, C, Hin, Win, R, S, U) -> "Shape":
-        return cls(N, K, C, (Hin - R) // U + 1, (Win - S) // U + 1, R, S, U, Hin, Win)
+    def strided(cls, N, K, C, Hin, Win, R, S, U, D=1) -> "Shape":
+        Re, Se = D * (R - 1) + 1, D * (S - 1) + 1
+        return cls(N, K, C, (Hin - Re) // U + 1, (Win - Se) // U + 1, R, S, U, Hin, Win, D)
 
     @property
     def Hin(self) -> int:
-        return self.hin or (self.H - 1) * self.U + self.R
+        return self.hin or (self.H - 1) * self.U + self.D * (self.R - 1) + 1
 
     @property
     def Win(self) -> int:
-        return self.win or (self.W - 1) * self.U + self.S
+        return self.win or (self.W - 1) * self.U + self.D * (self.S - 1) + 1
 
     def plan_kwargs(self) -> dict:
-        """Keyword arguments of ConvPlan for this shape (stride, input extents)."""
-        if self.U == 1 and not self.hin and not self.win:
+        """Keyword arguments of ConvPlan for this shape (stride, dilation, input extents)."""
+        if self.U == 1 and self.D == 1 and not self.hin and not self.win:
             return {}
-        return {"stride": self.U, "in_hw": (self.Hin, self.Win)}
+        kw = {"stride": self.U, "in_hw": (self.Hin, self.Win)}
+        if self.D != 1:
+            kw["dilation"] = self.D
+        return kw
 
     @property
     def in_shape(self):

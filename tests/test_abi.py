@@ -231,3 +231,30 @@ def test_strided_plans_offline(lib):
     assert e.value.status == conv.CONV_ERR_INFEASIBLE
     with pytest.raises(ValueError):   # H, W inconsistent with the input extents
         conv.ConvPlan(1, 8, 8, 5, 5, 3, 3, stride=2, in_hw=(21, 21), offline_device=sh)
+
+
+def test_dilated_plans_offline(lib):
+    """conv_plan_create_dilated (PAPER.md:201 footnote: stride/dilation):
+    describe() reports D and the output extents (Hin - D(R-1) - 1)/U + 1;
+    SIMT falls back to v1 (v2 needs U = D = 1); D = 1 is the strided plan;
+    bad dilations, inputs smaller than the dilated kernel and dilated kernels
+    past the TMA im2col box (D(R-1) > 128) are rejected."""
+    sh = dict(sms=148, smem_optin=232448, l2_bytes=132120576)
+    for (Hin, R, U, D) in ((56, 3, 1, 2), (57, 3, 2, 2), (40, 5, 1, 3), (30, 1, 1, 4)):
+        H = (Hin - D * (R - 1) - 1) // U + 1
+        p = conv.ConvPlan(1, 64, 32, H, H, R, R, stride=U, dilation=D, in_hw=(Hin, Hin), offline_device=sh)
+        d = p.describe()["problem"]
+        assert (d["U"], d["D"], d["Hin"], d["Win"], d["H"], d["W"]) == (U, D, Hin, Hin, H, H)
+        ps = conv.ConvPlan(1, 64, 32, H, H, R, R, stride=U, dilation=D, in_hw=(Hin, Hin), offline_device=sh,
+                           path="fp32_simt")
+        assert ps.describe()["tile"]["ver"] == 1
+    a = conv.ConvPlan(2, 64, 32, 13, 13, 3, 3, stride=2, in_hw=(28, 28), offline_device=sh).describe()
+    b = conv.ConvPlan(2, 64, 32, 13, 13, 3, 3, stride=2, dilation=1, in_hw=(28, 28), offline_device=sh).describe()
+    assert a == b
+    assert not lib.conv_plan_create_dilated(1, 1, 1, 8, 8, 3, 3, 1, 0)
+    assert "extent must be >= 1" in conv.last_error()
+    assert not lib.conv_plan_create_dilated(1, 1, 1, 4, 8, 3, 3, 1, 2)   # dilated kernel is 5x5
+    assert "smaller than the kernel" in conv.last_error()
+    with pytest.raises(conv.ConvError) as e:   # D(R-1) = 129 > 128
+        conv.ConvPlan(1, 8, 8, 2, 2, 2, 2, dilation=129, in_hw=(131, 131), offline_device=sh, path="bf16")
+    assert e.value.status == conv.CONV_ERR_INFEASIBLE

@@ -282,3 +282,45 @@ def test_strided_points_brute_force():
     for _ in range(50):
         p = (rng.integers(2), rng.integers(6), rng.integers(out.shape[2]), rng.integers(out.shape[3]))
         assert abs(out[p] - oracle.conv_eq1_point(x, w, *p, stride=2)) <= 1e-13 * (1 + abs(out[p]))
+
+
+# ---- dilation (PAPER.md:201 footnote: "stride/dilation ... the general case")
+
+def test_dilated_unit_is_strided():
+    """D = 1 reduces to the (pinned) strided oracle, bit for bit."""
+    inp = torch.rand(2, 3, 13, 12, generator=torch.Generator().manual_seed(101)) * 2 - 1
+    ker = torch.rand(4, 3, 3, 2, generator=torch.Generator().manual_seed(102)) * 2 - 1
+    for U in (1, 2):
+        np.testing.assert_array_equal(oracle.conv_eq1_dilated(inp.numpy(), ker.numpy(), U, 1),
+                                      oracle.conv_eq1_strided(inp.numpy(), ker.numpy(), U))
+
+
+@pytest.mark.parametrize("U,D", [(1, 2), (2, 2), (1, 3), (2, 3)])
+def test_dilated_is_zero_inserted_kernel(U, D):
+    """Dilation D = the strided oracle with the kernel spread over a
+    (D(R-1)+1) x (D(S-1)+1) grid of zeros: the extra terms are exact zeros,
+    so the double sums are identical bit for bit (catches D*r vs r, a
+    dilation on one axis only, a wrong output extent)."""
+    inp = torch.rand(2, 3, 17, 15, generator=torch.Generator().manual_seed(103)) * 2 - 1
+    ker = torch.rand(4, 3, 3, 2, generator=torch.Generator().manual_seed(104)) * 2 - 1
+    k = ker.numpy()
+    big = np.zeros((4, 3, D * 2 + 1, D * 1 + 1), dtype=np.float32)
+    big[:, :, ::D, ::D] = k
+    got = oracle.conv_eq1_dilated(inp.numpy(), k, U, D)
+    np.testing.assert_array_equal(got, oracle.conv_eq1_strided(inp.numpy(), big, U))
+
+
+@pytest.mark.parametrize("U,D", [(1, 2), (2, 3)])
+def test_dilated_vs_torch_and_points(U, D):
+    """Library cross-check (torch conv2d f64 with stride and dilation) and
+    correctly rounded brute-force points."""
+    inp = torch.rand(2, 4, 19, 16, generator=torch.Generator().manual_seed(105)) * 2 - 1
+    ker = torch.rand(3, 4, 3, 3, generator=torch.Generator().manual_seed(106)) * 2 - 1
+    got = oracle.conv_eq1_dilated(inp.numpy(), ker.numpy(), U, D)
+    ref = torch.nn.functional.conv2d(inp.double(), ker.double(), stride=U, dilation=D).numpy()
+    np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13)
+    rng = np.random.default_rng(107)
+    for _ in range(30):
+        p = (rng.integers(2), rng.integers(3), rng.integers(got.shape[2]), rng.integers(got.shape[3]))
+        v = oracle.conv_eq1_point(inp.numpy(), ker.numpy(), *p, stride=U, dilation=D)
+        assert abs(got[p] - v) <= 1e-13 * (1 + abs(v))

@@ -401,6 +401,61 @@ def test_strided_fused_and_cta_groups_bit_identical(path):
     assert rel_l2(ref[:2].cpu().numpy(), ref64) <= 1e-5
 
 
+# ---- dilation (PAPER.md:201 footnote: "stride/dilation ... the general case")
+DILATED = [
+    Shape.strided(2, 128, 64, 60, 60, 3, 3, 1, 2),     # R4-like, D = 2
+    Shape.strided(1, 64, 96, 41, 41, 3, 3, 2, 2),      # stride 2 and dilation 2
+    Shape.strided(2, 40, 17, 23, 19, 3, 2, 1, 3),      # odd extents, R != S, D = 3
+    Shape.strided(1, 72, 32, 40, 40, 5, 5, 1, 4),      # wide dilated window (17 x 17)
+    Shape.strided(3, 24, 8, 21, 22, 1, 1, 2, 5),       # 1 x 1: dilation has no effect
+]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("shape", DILATED, ids=lambda s: f"{s.N}x{s.K}x{s.C}x{s.Hin}x{s.Win}x{s.R}x{s.S}s{s.U}d{s.D}")
+def test_dilated_parity(path, shape):
+    """Strided + dilated Eq. 1 on every path against the dilated oracle:
+    tolerance on real inputs (and 1e-5 against the oracle on the path's
+    rounded inputs), bit-exact on the integer twin."""
+    inp, ker = make_inputs(shape, seed=81)
+    got, plan = run(shape, inp, ker, path)
+    d = plan.describe()["problem"]
+    assert (d["U"], d["D"], d["Hin"], d["Win"], d["H"], d["W"]) == (shape.U, shape.D, shape.Hin, shape.Win,
+                                                                     shape.H, shape.W)
+    ref = oracle.conv_eq1_dilated(inp.numpy(), ker.numpy(), shape.U, shape.D)
+    assert got.shape == ref.shape
+    assert rel_l2(got, ref) <= TOL[path]
+    ref_r = oracle.conv_eq1_dilated(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), shape.U, shape.D)
+    assert rel_l2(got, ref_r) <= 1e-5
+    xi, wi = make_inputs(shape, seed=82, kind="int")
+    goti, _ = run(shape, xi, wi, path)
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1_dilated(xi.numpy(), wi.numpy(), shape.U, shape.D))
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_dilated_fused_and_cta_groups_bit_identical(path):
+    """A multi-wave dilated layer: the fused in-kernel transform (its chunk
+    ranges cover the D(R-1) halo rows) and both CTA-group sizes give the
+    same bits as the separate repack; sampled points against the oracle."""
+    sh = Shape.strided(96, 128, 64, 32, 32, 3, 3, 1, 2)
+    inp, ker = make_inputs(sh, seed=83)
+    i, k = inp.cuda(), ker.cuda()
+    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1", **sh.plan_kwargs()).run(i, k)
+    for spec in ("fuse=0,cg=2", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0", "fuse=1,cg=2,bn=64"):
+        out = conv.ConvPlan(*sh.as_tuple(), path=path, tile=spec, **sh.plan_kwargs()).run(i, k)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), spec
+    ref64 = oracle.conv_eq1_dilated(ROUND[path](inp.numpy()[:2]), ROUND[path](ker.numpy()), 1, 2)
+    assert rel_l2(ref[:2].cpu().numpy(), ref64) <= 1e-5
+    rng = np.random.default_rng(84)
+    x, w = ROUND[path](inp.numpy()), ROUND[path](ker.numpy())
+    got = ref.cpu().numpy()
+    for _ in range(64):
+        p = (rng.integers(sh.N), rng.integers(sh.K), rng.integers(sh.H), rng.integers(sh.W))
+        v = oracle.conv_eq1_point(x, w, *p, stride=1, dilation=2)
+        assert abs(got[p] - v) <= 1e-4 * (1 + abs(v)), p
+
+
 @pytest.mark.parametrize("path", PATHS)
 def test_table1_layers(path):
     """Every conv2d layer of PAPER.md:439 Table 1 (batch 1, stride 1/2, input
