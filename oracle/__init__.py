@@ -24,6 +24,12 @@ Functions and the passage each follows:
                          conv_eq1_strided; = the strided oracle with a
                          zero-inserted kernel, bit for bit; torch conv2d f64
                          with dilation; brute-force points.
+* ``conv_eq1_padded``  -- zero padding (ph, pw) with stride U and dilation D
+                         (SURVEY Sec. 8(f) NEXT-2): taps outside the input are
+                         skipped; plain C.  Pinned: pad 0 is conv_eq1_dilated;
+                         torch conv2d f64 with padding; the interior equals the
+                         unpadded output shifted by the pad; all-ones closed
+                         form (count of in-range taps); brute-force points.
 * ``conv_eq1_point``  -- one output element of Eq. 1 as the correctly rounded
                          sum (``math.fsum``) of its C*R*S exact products; used
                          for sampled parity at full sizes.  Pinned against
@@ -77,6 +83,9 @@ def _load():
                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
             lib.oracle_conv_eq1_dilated.restype = ctypes.c_int
             lib.oracle_conv_eq1_dilated.argtypes = [ctypes.c_int] * 9 + [
+                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+            lib.oracle_conv_eq1_padded.restype = ctypes.c_int
+            lib.oracle_conv_eq1_padded.argtypes = [ctypes.c_int] * 11 + [
                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
             lib.oracle_num_threads.restype = ctypes.c_int
             lib.oracle_num_threads.argtypes = [ctypes.c_int]
@@ -162,15 +171,45 @@ def conv_eq1_dilated(inp: np.ndarray, ker: np.ndarray, stride: int, dilation: in
     return out
 
 
+def conv_eq1_padded(inp: np.ndarray, ker: np.ndarray, stride: int = 1, dilation: int = 1, padding=0,
+                    nthreads: int = 0) -> np.ndarray:
+    """Eq. 1 with zero padding ``padding`` (int or (ph, pw)), stride U and
+    dilation D.  ``inp``: fp32 [N,C,Hin,Win]; ``ker``: fp32 [K,C,R,S].
+    Returns float64 [N,K,H,W], H = (Hin + 2ph - D(R-1) - 1)//U + 1."""
+    inp = np.ascontiguousarray(inp, dtype=np.float32)
+    ker = np.ascontiguousarray(ker, dtype=np.float32)
+    if inp.ndim != 4 or ker.ndim != 4 or inp.shape[1] != ker.shape[1]:
+        raise ValueError("expected In [N,C,Hin,Win] and Ker [K,C,R,S] with equal C")
+    ph, pw = (padding, padding) if np.isscalar(padding) else padding
+    N, C, Hin, Win = inp.shape
+    K, _, R, S = ker.shape
+    U, D = stride, dilation
+    if U < 1 or D < 1 or ph < 0 or pw < 0 or Hin + 2 * ph < D * (R - 1) + 1 or Win + 2 * pw < D * (S - 1) + 1:
+        raise ValueError("bad stride/dilation/padding or padded input smaller than the dilated kernel")
+    H = (Hin + 2 * ph - D * (R - 1) - 1) // U + 1
+    W = (Win + 2 * pw - D * (S - 1) - 1) // U + 1
+    out = np.empty((N, K, H, W), dtype=np.float64)
+    rc = _load().oracle_conv_eq1_padded(N, K, C, Hin, Win, R, S, U, D, ph, pw,
+                                        inp.ctypes.data, ker.ctypes.data, out.ctypes.data, nthreads or host_threads())
+    if rc != 0:
+        raise ValueError("oracle_conv_eq1_padded rejected its arguments")
+    return out
+
+
 def conv_eq1_point(inp: np.ndarray, ker: np.ndarray, n: int, k: int, h: int, w: int, stride: int = 1,
-                   dilation: int = 1) -> float:
-    """Out[n,k,h,w] of Eq. 1 (stride U, dilation D) as the correctly rounded
-    sum of its exact products (each fp32*fp32 product is exact in float64)."""
+                   dilation: int = 1, padding=0) -> float:
+    """Out[n,k,h,w] of Eq. 1 (stride U, dilation D, zero padding) as the
+    correctly rounded sum of its exact products (each fp32*fp32 product is
+    exact in float64); taps outside the input contribute nothing."""
     R, S = ker.shape[2], ker.shape[3]
+    ph, pw = (padding, padding) if np.isscalar(padding) else padding
     d = dilation
-    window = inp[n, :, stride * h:stride * h + d * (R - 1) + 1:d,
-                 stride * w:stride * w + d * (S - 1) + 1:d].astype(np.float64)
-    prods = window * ker[k].astype(np.float64)
+    rows = stride * h + d * np.arange(R) - ph        # input row of tap r
+    cols = stride * w + d * np.arange(S) - pw        # input column of tap s
+    rk, sk = np.nonzero((rows[:, None] >= 0) & (rows[:, None] < inp.shape[2])
+                        & (cols[None, :] >= 0) & (cols[None, :] < inp.shape[3]))
+    window = inp[n][:, rows[rk], cols[sk]].astype(np.float64)      # [C, taps in range]
+    prods = window * ker[k][:, rk, sk].astype(np.float64)
     return math.fsum(prods.ravel().tolist())
 
 

@@ -156,6 +156,60 @@ int oracle_conv_eq1_dilated(int N, int K, int C, int Hin, int Win, int R, int S,
     return 0;
 }
 
+/*
+ * Zero-padded ("same"-style) Eq. 1 with stride U and dilation D (SURVEY.md
+ * Sec. 8(f) NEXT-2; the paper's Eq. 1 has no padding, reading R3):
+ *
+ *     Out[n,k,h,w] = sum_{c,r,s} In[n,c,U*h+D*r-ph,U*w+D*s-pw] * Ker[k,c,r,s]
+ *
+ * where In[...] outside [0,Hin) x [0,Win) is zero (the term is skipped --
+ * written as the definition, with the bounds test, not by copying In into a
+ * padded buffer).  H = (Hin + 2*ph - D*(R-1) - 1)/U + 1 (floor), likewise W.
+ * Same loop order, double accumulation and (n,k)-plane parallelism as
+ * oracle_conv_eq1.  Returns 0, or 1 on a bad extent / NULL.
+ */
+int oracle_conv_eq1_padded(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D, int ph, int pw,
+                           const float* in, const float* ker, double* out, int nthreads)
+{
+    if (N < 1 || K < 1 || C < 1 || R < 1 || S < 1 || U < 1 || D < 1 || ph < 0 || pw < 0 || Hin < 1 || Win < 1)
+        return 1;
+    if ((int64_t)Hin + 2 * (int64_t)ph < (int64_t)D * (R - 1) + 1 ||
+        (int64_t)Win + 2 * (int64_t)pw < (int64_t)D * (S - 1) + 1) return 1;
+    if (!in || !ker || !out) return 1;
+    const int64_t H = ((int64_t)Hin + 2 * (int64_t)ph - (int64_t)D * (R - 1) - 1) / U + 1;
+    const int64_t W = ((int64_t)Win + 2 * (int64_t)pw - (int64_t)D * (S - 1) - 1) / U + 1;
+    const int64_t planes = (int64_t)N * K;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t nk = 0; nk < planes; ++nk) {
+        const int64_t n = nk / K;
+        const int64_t k = nk % K;
+        double* acc = out + nk * H * W;
+        for (int64_t i = 0; i < H * W; ++i) acc[i] = 0.0;
+        for (int64_t c = 0; c < C; ++c)
+            for (int64_t r = 0; r < R; ++r)
+                for (int64_t s = 0; s < S; ++s) {
+                    const double kv = (double)ker[((k * C + c) * R + r) * S + s];
+                    const float* plane = in + (n * C + c) * (int64_t)Hin * Win;
+                    for (int64_t h = 0; h < H; ++h) {
+                        const int64_t ih = U * h + D * r - ph;
+                        if (ih < 0 || ih >= Hin) continue;           /* zero padding */
+                        for (int64_t w = 0; w < W; ++w) {
+                            const int64_t iw = U * w + D * s - pw;
+                            if (iw < 0 || iw >= Win) continue;
+                            acc[h * W + w] += (double)plane[ih * Win + iw] * kv;
+                        }
+                    }
+                }
+    }
+    return 0;
+}
+
 /* Number of OpenMP threads a parallel region would use (for reporting). */
 int oracle_num_threads(int nthreads)
 {

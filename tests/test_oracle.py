@@ -324,3 +324,58 @@ def test_dilated_vs_torch_and_points(U, D):
         p = (rng.integers(2), rng.integers(3), rng.integers(got.shape[2]), rng.integers(got.shape[3]))
         v = oracle.conv_eq1_point(inp.numpy(), ker.numpy(), *p, stride=U, dilation=D)
         assert abs(got[p] - v) <= 1e-13 * (1 + abs(v))
+
+
+# ---- zero padding (DESIGN reading R3) --------------
+
+def test_padded_zero_pad_is_dilated():
+    """Padding 0 reduces to the (pinned) dilated oracle, bit for bit."""
+    inp = torch.rand(2, 3, 14, 13, generator=torch.Generator().manual_seed(111)) * 2 - 1
+    ker = torch.rand(4, 3, 3, 2, generator=torch.Generator().manual_seed(112)) * 2 - 1
+    for U, D in ((1, 1), (2, 1), (1, 2), (2, 3)):
+        np.testing.assert_array_equal(oracle.conv_eq1_padded(inp.numpy(), ker.numpy(), U, D, 0),
+                                      oracle.conv_eq1_dilated(inp.numpy(), ker.numpy(), U, D))
+
+
+@pytest.mark.parametrize("U,D,pad", [(1, 1, 1), (1, 1, (2, 0)), (2, 1, 3), (1, 2, 2), (2, 2, (1, 3))])
+def test_padded_vs_torch_and_points(U, D, pad):
+    """Library cross-check (torch conv2d f64 with padding, stride, dilation)
+    and correctly rounded brute-force points (with explicit tap bounds)."""
+    inp = torch.rand(2, 4, 15, 12, generator=torch.Generator().manual_seed(113)) * 2 - 1
+    ker = torch.rand(3, 4, 3, 5, generator=torch.Generator().manual_seed(114)) * 2 - 1
+    got = oracle.conv_eq1_padded(inp.numpy(), ker.numpy(), U, D, pad)
+    p2 = (pad, pad) if isinstance(pad, int) else pad
+    ref = torch.nn.functional.conv2d(inp.double(), ker.double(), stride=U, dilation=D, padding=p2).numpy()
+    assert got.shape == ref.shape
+    np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13)
+    rng = np.random.default_rng(115)
+    corners = [(0, 0, 0, 0), (1, 2, got.shape[2] - 1, got.shape[3] - 1), (0, 1, 0, got.shape[3] - 1)]
+    pts = corners + [(rng.integers(2), rng.integers(3), rng.integers(got.shape[2]), rng.integers(got.shape[3]))
+                     for _ in range(30)]
+    for p in pts:
+        v = oracle.conv_eq1_point(inp.numpy(), ker.numpy(), *p, stride=U, dilation=D, padding=pad)
+        assert abs(got[p] - v) <= 1e-13 * (1 + abs(v)), p
+
+
+def test_padded_interior_is_unpadded_output():
+    """Stride 1: Out_pad[n,k,h+ph,w+pw] = Out_valid[n,k,h,w] bit for bit
+    (same products, same order); the padded output is (Hin+2ph-R+1) wide."""
+    inp = torch.rand(2, 3, 11, 10, generator=torch.Generator().manual_seed(116)) * 2 - 1
+    ker = torch.rand(4, 3, 3, 3, generator=torch.Generator().manual_seed(117)) * 2 - 1
+    full = oracle.conv_eq1_padded(inp.numpy(), ker.numpy(), 1, 1, (2, 1))
+    valid = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert full.shape == (2, 4, 11 + 4 - 2, 10 + 2 - 2)
+    np.testing.assert_array_equal(full[:, :, 2:2 + valid.shape[2], 1:1 + valid.shape[3]], valid)
+
+
+def test_padded_all_ones_closed_form():
+    """In = 1, Ker = 1: Out[h,w] = C * (#taps r with 0 <= U h + D r - ph < Hin)
+    * (#taps s likewise) -- an independent count of the in-range taps."""
+    N, C, Hin, Win, R, S, U, D, ph, pw = 1, 5, 9, 8, 3, 4, 2, 2, 3, 2
+    got = oracle.conv_eq1_padded(np.ones((N, C, Hin, Win), np.float32), np.ones((2, C, R, S), np.float32),
+                                 U, D, (ph, pw))
+    for h in range(got.shape[2]):
+        for w in range(got.shape[3]):
+            nr = sum(1 for r in range(R) if 0 <= U * h + D * r - ph < Hin)
+            ns = sum(1 for s in range(S) if 0 <= U * w + D * s - pw < Win)
+            assert got[0, 1, h, w] == C * nr * ns, (h, w)
