@@ -23,6 +23,13 @@
  *     Out[n,k,h,w] = sum_{c,r,s} In[n,c,U*h+D*r,U*w+D*s] * Ker[k,c,r,s]
  *
  * with H = (Hin - D*(R-1) - 1)/U + 1 (floor), likewise W.
+ * conv_plan_create_padded adds zero padding ph (rows, top and bottom) and pw
+ * (columns, left and right) -- the "same"-padded layers of real networks
+ * (Eq. 1 itself has none, R3):
+ *
+ *     Out[n,k,h,w] = sum_{c,r,s} In[n,c,U*h+D*r-ph,U*w+D*s-pw] * Ker[k,c,r,s]
+ *
+ * with In = 0 outside [0,Hin) x [0,Win) and H = (Hin + 2ph - D*(R-1) - 1)/U + 1.
  * Internal layout
  * transforms are part of every conv_run, as the paper counts them
  * (PAPER.md:371).
@@ -106,6 +113,18 @@ CONV_API conv_plan* conv_plan_create_strided(int N, int K, int C, int Hin, int W
  * (D*(R-1)+1) x (D*(S-1)+1). */
 CONV_API conv_plan* conv_plan_create_dilated(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D);
 
+/* Padded, strided and dilated plan (the general form above): zero padding
+ * ph >= 0 rows above and below, pw >= 0 columns left and right; H = (Hin +
+ * 2ph - D*(R-1) - 1)/U + 1, W likewise.  ph = pw = 0 is
+ * conv_plan_create_dilated.  The padding is never materialised: the tensor
+ * paths' TMA im2col box starts at (-pw, -ph) and TMA zero-fills the
+ * out-of-bounds taps (needs ph, pw <= 128 and pad - D*(R-1) in [-128, 127]);
+ * FP32 SIMT v1 zero-fills its smem halo; SIMT v2 needs no padding.  Errors
+ * as conv_plan_create_dilated, plus INVALID_ARGUMENT if ph or pw < 0 or the
+ * padded input is smaller than the dilated kernel. */
+CONV_API conv_plan* conv_plan_create_padded(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D,
+                                            int ph, int pw);
+
 /* A plan for a described (not present) device: `sms` SMs, `smem_optin` bytes
  * of opt-in shared memory per block, `l2_bytes` of L2.  Runs the same
  * selector; the plan can be described but not run (conv_run returns
@@ -119,6 +138,10 @@ CONV_API conv_plan* conv_plan_create_strided_offline(int N, int K, int C, int Hi
 /* Offline variant of conv_plan_create_dilated (same arguments as above). */
 CONV_API conv_plan* conv_plan_create_dilated_offline(int N, int K, int C, int Hin, int Win, int R, int S, int U,
                                                      int D, int sms, size_t smem_optin, size_t l2_bytes);
+/* Offline variant of conv_plan_create_padded (same arguments as above). */
+CONV_API conv_plan* conv_plan_create_padded_offline(int N, int K, int C, int Hin, int Win, int R, int S, int U,
+                                                    int D, int ph, int pw, int sms, size_t smem_optin,
+                                                    size_t l2_bytes);
 
 /* Force a path (default AUTO) and re-run the selector for it.
  * INFEASIBLE if no candidate of that path fits (e.g. R or S > 128 on the

@@ -30,6 +30,7 @@ PATH_NAMES = {v: k for k, v in PATHS.items()}
 EXPORTED = (
     "conv_plan_create", "conv_plan_create_offline", "conv_plan_create_strided", "conv_plan_create_strided_offline",
     "conv_plan_create_dilated", "conv_plan_create_dilated_offline",
+    "conv_plan_create_padded", "conv_plan_create_padded_offline",
     "conv_plan_set_path", "conv_plan_set_tile", "conv_plan_workspace_bytes",
     "conv_plan_num_kernels", "conv_plan_path", "conv_plan_describe", "conv_plan_destroy",
     "conv_run", "conv_run_events", "conv_plan_host_run_bytes", "conv_run_host",
@@ -66,6 +67,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "conv_plan_create_strided_offline": (vp, [i] * 9 + [sz, sz]),
             "conv_plan_create_dilated": (vp, [i] * 9),
             "conv_plan_create_dilated_offline": (vp, [i] * 10 + [sz, sz]),
+            "conv_plan_create_padded": (vp, [i] * 11),
+            "conv_plan_create_padded_offline": (vp, [i] * 12 + [sz, sz]),
             "conv_plan_set_path": (i, [vp, i]),
             "conv_plan_set_tile": (i, [vp, ctypes.c_char_p]),
             "conv_plan_workspace_bytes": (sz, [vp]),
@@ -119,40 +122,44 @@ def _stream_handle(stream) -> Optional[int]:
 
 class ConvPlan:
     """A plan for Eq. 1 with OUTPUT extents H x W; with
-    ``stride`` U > 1, ``dilation`` D > 1 (or explicit ``in_hw``) the general form
-    Out[n,k,h,w] = sum In[n,c,U*h+D*r,U*w+D*s] Ker[k,c,r,s] (conv_plan_create_dilated)."""
+    ``stride`` U > 1, ``dilation`` D > 1, ``padding`` (ph, pw) (or explicit
+    ``in_hw``) the general form Out[n,k,h,w] = sum In[n,c,U*h+D*r-ph,U*w+D*s-pw]
+    Ker[k,c,r,s], In zero outside the input (conv_plan_create_padded)."""
 
     def __init__(self, N: int, K: int, C: int, H: int, W: int, R: int, S: int,
                  path: str = "auto", tile: Optional[str] = None, offline_device: Optional[dict] = None,
-                 stride: int = 1, in_hw: Optional[tuple] = None, dilation: int = 1):
+                 stride: int = 1, in_hw: Optional[tuple] = None, dilation: int = 1, padding=0):
         """``offline_device`` = dict(sms=, smem_optin=, l2_bytes=) plans for a
         described device without touching CUDA (describe-only plan).
         ``in_hw`` = (Hin, Win) input extents of a strided plan (default the
-        minimal ((H-1)*U+D*(R-1)+1, (W-1)*U+D*(S-1)+1)); H, W must equal the
-        floor output extents (Hin-D*(R-1)-1)//U+1, likewise W."""
+        minimal ((H-1)*U+D*(R-1)+1-2ph, (W-1)*U+D*(S-1)+1-2pw)); H, W must
+        equal the floor output extents (Hin+2ph-D*(R-1)-1)//U+1, likewise W.
+        ``padding`` is an int or (ph, pw)."""
         lib = load_library()
         self._lib = lib
-        strided = stride != 1 or dilation != 1 or in_hw is not None
+        ph, pw = (padding, padding) if isinstance(padding, int) else tuple(padding)
+        strided = stride != 1 or dilation != 1 or ph != 0 or pw != 0 or in_hw is not None
         Re, Se = dilation * (R - 1) + 1, dilation * (S - 1) + 1     # dilated kernel extents
         if strided:
-            Hin, Win = in_hw if in_hw is not None else ((H - 1) * stride + Re, (W - 1) * stride + Se)
-            if (stride >= 1 and dilation >= 1 and Hin >= Re and Win >= Se
-                    and ((Hin - Re) // stride + 1, (Win - Se) // stride + 1) != (H, W)):
+            Hin, Win = in_hw if in_hw is not None else ((H - 1) * stride + Re - 2 * ph, (W - 1) * stride + Se - 2 * pw)
+            if (stride >= 1 and dilation >= 1 and Hin + 2 * ph >= Re and Win + 2 * pw >= Se
+                    and ((Hin + 2 * ph - Re) // stride + 1, (Win + 2 * pw - Se) // stride + 1) != (H, W)):
                 raise ValueError(f"output {H}x{W} does not match input {Hin}x{Win}, kernel {R}x{S}, "
-                                 f"stride {stride}, dilation {dilation}")
+                                 f"stride {stride}, dilation {dilation}, padding {(ph, pw)}")
         else:
             Hin, Win = H + R - 1, W + S - 1
         self.shape = (N, K, C, H, W, R, S)
         self.stride = stride
         self.dilation = dilation
+        self.padding = (ph, pw)
         self.in_hw = (Hin, Win)
         if offline_device is not None:
             d = offline_device
             dev = (int(d["sms"]), int(d["smem_optin"]), int(d["l2_bytes"]))
-            h = (lib.conv_plan_create_dilated_offline(N, K, C, Hin, Win, R, S, stride, dilation, *dev) if strided
+            h = (lib.conv_plan_create_padded_offline(N, K, C, Hin, Win, R, S, stride, dilation, ph, pw, *dev) if strided
                  else lib.conv_plan_create_offline(N, K, C, H, W, R, S, *dev))
         else:
-            h = (lib.conv_plan_create_dilated(N, K, C, Hin, Win, R, S, stride, dilation) if strided
+            h = (lib.conv_plan_create_padded(N, K, C, Hin, Win, R, S, stride, dilation, ph, pw) if strided
                  else lib.conv_plan_create(N, K, C, H, W, R, S))
         if not h:
             raise ConvError(lib.conv_last_status(), last_error())

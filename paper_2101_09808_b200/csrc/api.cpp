@@ -194,20 +194,33 @@ static conv_plan* create_impl(const Problem& pb, const Device* offline) {
     return p;
 }
 
-static bool strided_problem(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D, Problem& pb) {
-    if (N < 1 || K < 1 || C < 1 || R < 1 || S < 1 || U < 1 || D < 1) {
-        fail(CONV_ERR_INVALID_ARGUMENT, "extent must be >= 1 (N=%d K=%d C=%d R=%d S=%d U=%d D=%d)", N, K, C, R, S, U, D);
+static bool strided_problem(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D, int ph, int pw,
+                            Problem& pb) {
+    if (N < 1 || K < 1 || C < 1 || R < 1 || S < 1 || U < 1 || D < 1 || Hin < 1 || Win < 1) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "extent must be >= 1 (N=%d K=%d C=%d Hin=%d Win=%d R=%d S=%d U=%d D=%d)", N, K,
+             C, Hin, Win, R, S, U, D);
+        return false;
+    }
+    if (ph < 0 || pw < 0) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "padding must be >= 0 (ph=%d pw=%d)", ph, pw);
         return false;
     }
     const int64_t Re = (int64_t)D * (R - 1) + 1, Se = (int64_t)D * (S - 1) + 1;   // dilated kernel extents
-    if (Hin < Re || Win < Se) {
-        fail(CONV_ERR_INVALID_ARGUMENT, "input %dx%d smaller than the kernel %lldx%lld (dilated extents)", Hin, Win,
-             (long long)Re, (long long)Se);
+    const int64_t Hp = (int64_t)Hin + 2 * (int64_t)ph, Wp = (int64_t)Win + 2 * (int64_t)pw;   // padded input
+    if (Hp < Re || Wp < Se) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "input %lldx%lld (padded) smaller than the kernel %lldx%lld (dilated extents)",
+             (long long)Hp, (long long)Wp, (long long)Re, (long long)Se);
         return false;
     }
-    pb = Problem{N, K, C, (int)((Hin - Re) / U + 1), (int)((Win - Se) / U + 1), R, S};
+    if ((Hp - Re) / U + 1 >= INT32_MAX || (Wp - Se) / U + 1 >= INT32_MAX) {
+        fail(CONV_ERR_INVALID_ARGUMENT, "output extent too large");
+        return false;
+    }
+    pb = Problem{N, K, C, (int)((Hp - Re) / U + 1), (int)((Wp - Se) / U + 1), R, S};
     pb.U = U;
     pb.D = D;
+    pb.ph = ph;
+    pb.pw = pw;
     pb.hin = Hin;
     pb.win = Win;
     return true;
@@ -226,8 +239,13 @@ extern "C" conv_plan* conv_plan_create_strided(int N, int K, int C, int Hin, int
 }
 
 extern "C" conv_plan* conv_plan_create_dilated(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D) {
+    return conv_plan_create_padded(N, K, C, Hin, Win, R, S, U, D, 0, 0);
+}
+
+extern "C" conv_plan* conv_plan_create_padded(int N, int K, int C, int Hin, int Win, int R, int S, int U, int D,
+                                              int ph, int pw) {
     Problem pb;
-    if (!strided_problem(N, K, C, Hin, Win, R, S, U, D, pb)) return nullptr;
+    if (!strided_problem(N, K, C, Hin, Win, R, S, U, D, ph, pw, pb)) return nullptr;
     return create_impl(pb, nullptr);
 }
 
@@ -260,8 +278,14 @@ extern "C" conv_plan* conv_plan_create_strided_offline(int N, int K, int C, int 
 
 extern "C" conv_plan* conv_plan_create_dilated_offline(int N, int K, int C, int Hin, int Win, int R, int S, int U,
                                                         int D, int sms, size_t smem_optin, size_t l2_bytes) {
+    return conv_plan_create_padded_offline(N, K, C, Hin, Win, R, S, U, D, 0, 0, sms, smem_optin, l2_bytes);
+}
+
+extern "C" conv_plan* conv_plan_create_padded_offline(int N, int K, int C, int Hin, int Win, int R, int S, int U,
+                                                       int D, int ph, int pw, int sms, size_t smem_optin,
+                                                       size_t l2_bytes) {
     Problem pb;
-    if (!strided_problem(N, K, C, Hin, Win, R, S, U, D, pb)) return nullptr;
+    if (!strided_problem(N, K, C, Hin, Win, R, S, U, D, ph, pw, pb)) return nullptr;
     Device d;
     if (!offline_device(sms, smem_optin, l2_bytes, d)) return nullptr;
     return create_impl(pb, &d);
@@ -381,7 +405,7 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     tile = t;
     char out[2048];
     int n = snprintf(out, sizeof out,
-        "{\"problem\":{\"N\":%d,\"K\":%d,\"C\":%d,\"H\":%d,\"W\":%d,\"R\":%d,\"S\":%d,\"U\":%d,\"D\":%d,\"Hin\":%lld,\"Win\":%lld},"
+        "{\"problem\":{\"N\":%d,\"K\":%d,\"C\":%d,\"H\":%d,\"W\":%d,\"R\":%d,\"S\":%d,\"U\":%d,\"D\":%d,\"ph\":%d,\"pw\":%d,\"Hin\":%lld,\"Win\":%lld},"
         "\"path\":\"%s\",\"tile\":%s,\"workspace_bytes\":%zu,\"kernels\":%d,"
         "\"model\":{\"tiles\":%ld,\"ctas\":%ld,\"wave_eff\":%.4f,\"smem_bytes\":%zu,"
         "\"levels\":{\"l2_smem\":{\"dv_bytes\":%.12g,\"bw\":%.6g,\"us\":%.4f},"
@@ -389,7 +413,7 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
         "\"compute\":{\"flops_issued_us\":%.4f,\"peak\":%.6g}},\"model_us\":%.4f},"
         "\"roofline\":{\"flops\":%.6g,\"compulsory_bytes\":%.6g,\"roofline_us\":%.4f},"
         "\"device\":{\"ordinal\":%d,\"sms\":%d,\"smem_optin\":%zu,\"l2_bytes\":%zu}}",
-        pb.N, pb.K, pb.C, pb.H, pb.W, pb.R, pb.S, pb.U, pb.D, (long long)pb.Hin(), (long long)pb.Win(), path_name(p->path), tile.c_str(), ws_bytes(p),
+        pb.N, pb.K, pb.C, pb.H, pb.W, pb.R, pb.S, pb.U, pb.D, pb.ph, pb.pw, (long long)pb.Hin(), (long long)pb.Win(), path_name(p->path), tile.c_str(), ws_bytes(p),
         conv_plan_num_kernels(p), m.tiles, m.ctas, m.wave_eff, m.smem,
         m.dv_l2_smem, p->dev.bw_l2, m.t_l2_us, m.dv_hbm, p->dev.bw_hbm, m.t_hbm_us, m.t_comp_us, peak,
         m.model_us, pb.flops(), comp_bytes, roof_us, p->dev.ordinal, p->dev.sms, p->dev.smem_optin,

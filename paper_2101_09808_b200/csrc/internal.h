@@ -10,18 +10,20 @@
 
 namespace conv {
 
-// Problem of Eq. 1: H, W are OUTPUT extents.  Stride U and
-// dilation D (PAPER.md:201 footnote; Table 1's * layers):
-// Out[n,k,h,w] sums In[n,c,U*h+D*r,U*w+D*s]; a strided / dilated plan stores
-// its explicit input extents (H = (hin - D*(R-1) - 1)/U + 1), a plain plan's
-// input is (H+R-1) x (W+S-1).
+// Problem of Eq. 1: H, W are OUTPUT extents.  Stride U,
+// dilation D (PAPER.md:201 footnote; Table 1's * layers) and
+// zero padding ph, pw: Out[n,k,h,w] sums
+// In[n,c,U*h+D*r-ph,U*w+D*s-pw] (zero outside the input); a general plan
+// stores its explicit input extents (H = (hin + 2ph - D*(R-1) - 1)/U + 1), a
+// plain plan's input is (H+R-1) x (W+S-1).
 struct Problem {
     int N, K, C, H, W, R, S;
     int U = 1;              // stride (both axes)
     int hin = 0, win = 0;   // explicit input extents (0: minimal, (H-1)*U + D*(R-1) + 1)
     int D = 1;              // dilation (both axes)
-    int64_t Hin() const { return hin ? (int64_t)hin : (int64_t)(H - 1) * U + (int64_t)D * (R - 1) + 1; }
-    int64_t Win() const { return win ? (int64_t)win : (int64_t)(W - 1) * U + (int64_t)D * (S - 1) + 1; }
+    int ph = 0, pw = 0;     // zero padding rows (top and bottom) / columns (left and right)
+    int64_t Hin() const { return hin ? (int64_t)hin : (int64_t)(H - 1) * U + (int64_t)D * (R - 1) + 1 - 2 * ph; }
+    int64_t Win() const { return win ? (int64_t)win : (int64_t)(W - 1) * U + (int64_t)D * (S - 1) + 1 - 2 * pw; }
     int64_t rows_span(int h_out) const { return (int64_t)(h_out - 1) * U + (int64_t)D * (R - 1) + 1; }  // input rows of h_out output rows
     int64_t M() const { return (int64_t)N * H * W; }  // implicit-GEMM M
     int64_t in_elems() const { return (int64_t)N * C * Hin() * Win(); }

@@ -265,9 +265,14 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
                int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, int force_pre_c,
                std::string& why) {
     const TcLayout L = tc_layout(pb, bf16);
-    if ((int64_t)pb.D * (pb.R - 1) > 128 || (int64_t)pb.D * (pb.S - 1) > 128) {
-        why = "D*(R-1), D*(S-1) > 128: the TMA im2col bounding box of a 4-D map is limited to [-128, 127]";
-        return false;
+    {
+        // the TMA im2col bounding-box corners of a 4-D map lie in [-128, 127]:
+        // lower = -pad, upper = pad - D*(R-1)
+        const int64_t uh = pb.ph - (int64_t)pb.D * (pb.R - 1), uw = pb.pw - (int64_t)pb.D * (pb.S - 1);
+        if (pb.ph > 128 || pb.pw > 128 || uh < -128 || uw < -128 || uh > 127 || uw > 127) {
+            why = "pad > 128 or pad - D*(R-1) outside [-128, 127]: the TMA im2col bounding box of a 4-D map is limited";
+            return false;
+        }
     }
     if (pb.U > 8) { why = "stride > 8: the TMA im2col traversal stride is limited to 8"; return false; }
     if (pb.M() + 256 > (int64_t)INT32_MAX) { why = "N*H*W too large for the tensor path"; return false; }
@@ -376,7 +381,7 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // one chunk: every thread's FFMAs, plus the cp.async copies (one per 4-B
     // element in v1/v2 In rows, ~6 instructions each, spread over the CTA)
     const double fma_chunk_cta = (double)threads * t.tk * t.tw * t.bc * pb.R * pb.S * issue_factor;
-    const double in_elems_chunk = (double)t.bc * t.tn * pb.rows_span(t.th) * pb.Win();
+    const double in_elems_chunk = (double)t.bc * t.tn * pb.rows_span(t.th) * (pb.Win() + 2 * pb.pw);
     // v2 copies 16-B units from a per-thread plan when they fit 4 per thread;
     // beyond that a per-row loop of 4-B copies runs (~2.3x slower layer
     // measured r01b)

@@ -53,7 +53,9 @@ struct SimtParams {
     int bko;          // kg * TK
     int D;            // dilation (v1 only): tap (r, s) reads rows / columns D*r, D*s further
     int rows_in;      // (th - 1) * U + D * (R - 1) + 1
-    int plane;        // tn * rows_in * Win  (floats per channel in smem)
+    int ph, pw;       // zero padding (v1 only): smem rows hold input rows h0*U - ph + i, columns c - pw
+    int pitch;        // smem row pitch: Win + 2 * pw
+    int plane;        // tn * rows_in * pitch  (floats per channel in smem)
     int n_htiles;     // ceil(H / th)
     int nchunks;      // ceil(C / bc)
     int bp;           // tn * th * W (real pixels per CTA tile)
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict_
         const int h = rem / p.W;
         const int w = rem - h * p.W;
         valid[j] = q < p.bp && (n0 + img) < p.N && (h0 + h) < p.H;
-        off[j] = valid[j] ? (img * p.rows_in + h * p.U) * p.Win + w * p.U : 0;
+        off[j] = valid[j] ? (img * p.rows_in + h * p.U) * p.pitch + w * p.U : 0;
         pix_img[j] = img;
         pix_h[j] = h;
         pix_w[j] = w;
@@ -139,17 +141,28 @@ __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict_
         float* in_s = sm + buf * stage_floats;
         float* ker_s = in_s + in_stage;
         const int c0 = chunk * p.bc;
-        // In: bc*tn segments of rows_in*Win contiguous floats.
-        const int seg_len = p.rows_in * p.Win;
+        // In: bc*tn segments of rows_in*pitch contiguous floats.
+        const int seg_len = p.rows_in * p.pitch;
         for (int seg = 0; seg < p.bc * p.tn; ++seg) {
             const int cc = seg / p.tn;
             const int img = seg - cc * p.tn;
             const int c = c0 + cc;
             const int n = n0 + img;
             const bool seg_ok = c < p.C && n < p.N;
-            const int hin0 = h0 * p.U;            // first input row of the tile
-            const float* g = in + (((int64_t)n * p.C + c) * p.Hin + hin0) * p.Win;
+            const int hin0 = h0 * p.U - p.ph;     // first input row of the tile (< 0: padding)
             float* s = in_s + cc * p.plane + img * seg_len;
+            if (p.ph | p.pw) {
+                // zero padding: element (i, col) of the segment is input row
+                // hin0 + i, column col - pw, or zero outside the input
+                const float* gp = in + ((int64_t)n * p.C + c) * p.Hin * p.Win;
+                for (int e = threadIdx.x; e < seg_len; e += blockDim.x) {
+                    const int i = e / p.pitch, col = e - i * p.pitch - p.pw, gr = hin0 + i;
+                    const bool ok = seg_ok && gr >= 0 && gr < p.Hin && col >= 0 && col < p.Win;
+                    cp_async4(s + e, ok ? gp + (int64_t)gr * p.Win + col : in, ok);
+                }
+                continue;
+            }
+            const float* g = in + (((int64_t)n * p.C + c) * p.Hin + hin0) * p.Win;
             // valid elements: rows < Hin - hin0
             const int rows_ok = p.Hin - hin0 < p.rows_in ? p.Hin - hin0 : p.rows_in;
             const int len_ok = seg_ok ? rows_ok * p.Win : 0;
@@ -183,7 +196,7 @@ __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict_
         const int cc_end = p.C - chunk * p.bc < p.bc ? p.C - chunk * p.bc : p.bc;
         for (int cc = 0; cc < cc_end; ++cc) {
             for (int r = 0; r < p.R; ++r) {
-                const float* ip = in_s + cc * p.plane + r * p.D * p.Win;
+                const float* ip = in_s + cc * p.plane + r * p.D * p.pitch;
                 const float* kp = ker_s + ((cc * p.R + r) * p.S) * p.bko + kgi * TK;
                 for (int s = 0; s < p.S; ++s) {
                     float iv[TW];
@@ -414,7 +427,7 @@ bool simt_tile_supported(const SimtTile& t) {
     return t.kg >= 1 && t.pw >= 1 && threads <= 512 && t.tn >= 1 && t.th >= 1 && t.bc >= 1;
 }
 
-bool simt_v2_ok(const Problem& pb) { return pb.U == 1 && pb.D == 1 && (pb.S == 1 || pb.S == 3); }
+bool simt_v2_ok(const Problem& pb) { return pb.U == 1 && pb.D == 1 && pb.ph == 0 && pb.pw == 0 && (pb.S == 1 || pb.S == 3); }
 
 // Row mode (TW = 7 or 14): one thread per output row, allowed only when the
 // row is exactly that wide (its window then starts 16-B aligned at w = 0).
@@ -440,7 +453,7 @@ int simt2_pitch(const Problem& pb, const SimtTile& t) {
 }
 
 size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
-    const size_t row = t.ver == 2 ? (size_t)simt2_pitch(pb, t) : (size_t)pb.Win();
+    const size_t row = t.ver == 2 ? (size_t)simt2_pitch(pb, t) : (size_t)(pb.Win() + 2 * pb.pw);
     const size_t plane = (size_t)t.tn * pb.rows_span(t.th) * row;
     const size_t in_stage = (size_t)t.bc * plane;
     const size_t ker_stage = (size_t)t.bc * pb.R * pb.S * t.kg * t.tk;
@@ -520,13 +533,16 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
     p.tn = t.tn; p.th = t.th; p.bc = t.bc; p.kg = t.kg;
     p.bko = t.kg * t.tk;
     p.rows_in = (int)pb.rows_span(t.th);
-    p.plane = t.tn * p.rows_in * p.Win;
+    p.ph = pb.ph;
+    p.pw = pb.pw;
+    p.pitch = p.Win + 2 * pb.pw;
+    p.plane = t.tn * p.rows_in * p.pitch;
     p.n_htiles = (pb.H + t.th - 1) / t.th;
     p.nchunks = (pb.C + t.bc - 1) / t.bc;
     p.bp = t.tn * t.th * pb.W;
     p.vec4_in = (p.Win % 4 == 0) ? 1 : 0;
     if (t.ver != 2 && p.bp > t.pw * 32 * t.tw) { err = "SIMT tile: pixel slots < tn*th*W"; return cudaErrorInvalidValue; }
-    if (t.ver == 2 && (pb.U != 1 || pb.D != 1)) { err = "SIMT v2 needs stride 1, dilation 1"; return cudaErrorInvalidValue; }
+    if (t.ver == 2 && !simt_v2_ok(pb)) { err = "SIMT v2 needs stride 1, dilation 1, no padding, S in {1, 3}"; return cudaErrorInvalidValue; }
 
     float* kerp = static_cast<float*>(ws);
     const int64_t total = (int64_t)((pb.K + p.bko - 1) / p.bko) * p.bko * pb.C * p.RS;

@@ -70,6 +70,7 @@ struct TcParams {
     int R, S;
     int U;            // stride: the im2col traversal visits input pixels U apart
     int D;            // dilation: tap (r, s) is the im2col offset (D*s, D*r)
+    int ph, pw;       // zero padding: output (h, w)'s window starts at input (U*h - ph, U*w - pw)
     int Cp, bkc, n_cblk;
     int k_iters;      // R*S*n_cblk
     int num_n_tiles;
@@ -88,7 +89,7 @@ struct TcParams {
     const float* in;          // In, NCHW fp32
     void* in_ws;              // NHWC workspace
     int C;                    // input channels
-    int P, Win;               // pixels per input image (Hin*Win), input width
+    int P, Win, Hin;          // pixels per input image (Hin*Win), input width, height
     int npch;                 // 64-pixel chunks per image plane: ceil(P / 64)
     int cc;                   // channels per chunk (min(32, bkc))
     int nch;                  // channel chunks: Cp / cc
@@ -424,11 +425,11 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                                 const int bx = (r1 * p.S + s1) * p.Cp + c1 * p.bkc;
                                 if (CG == 2) {
                                     tma_load_im2col_4d_pair(a_dst + kb * a_blk, &tmap_a, &full[stage], c1 * p.bkc,
-                                                            w0 * p.U, h0 * p.U, img, (uint16_t)(s1 * p.D), (uint16_t)(r1 * p.D), pol_a);
+                                                            w0 * p.U - p.pw, h0 * p.U - p.ph, img, (uint16_t)(s1 * p.D), (uint16_t)(r1 * p.D), pol_a);
                                     tma_load_2d_pair(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
                                 } else {
                                     tma_load_im2col_4d(a_dst + kb * a_blk, &tmap_a, &full[stage], c1 * p.bkc,
-                                                       w0 * p.U, h0 * p.U, img, (uint16_t)(s1 * p.D), (uint16_t)(r1 * p.D), pol_a);
+                                                       w0 * p.U - p.pw, h0 * p.U - p.ph, img, (uint16_t)(s1 * p.D), (uint16_t)(r1 * p.D), pol_a);
                                     tma_load_2d(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
                                 }
                                 if (p.tap_outer) {
@@ -550,8 +551,11 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     const int m1 = min(m0 + kBM, p.M) - 1;
                     const int na = m0 / p.HW, nb = m1 / p.HW;
                     const int ha = (m0 - na * p.HW) / p.W, hb = (m1 - nb * p.HW) / p.W;
-                    q_lo = na * p.npch + (ha * p.U * p.Win) / 64;
-                    q_hi = nb * p.npch + ((hb * p.U + p.D * (p.R - 1)) * p.Win + p.Win - 1) / 64;
+                    // input rows the tile's windows touch (padding rows clamped away)
+                    const int ra = min(max(ha * p.U - p.ph, 0), p.Hin - 1);
+                    const int rb = min(max(hb * p.U - p.ph + p.D * (p.R - 1), 0), p.Hin - 1);
+                    q_lo = na * p.npch + (ra * p.Win) / 64;
+                    q_hi = nb * p.npch + (rb * p.Win + p.Win - 1) / 64;
                 }
                 cnt = (q_hi - q_lo + 1) * p.hh;
             };
@@ -889,13 +893,14 @@ static cudaError_t encode_maps(const Problem& pb, const TcLayout& L, const TcTil
         cuuint64_t dims[4] = {(cuuint64_t)L.Cp, (cuuint64_t)pb.Win(), (cuuint64_t)pb.Hin(), (cuuint64_t)pb.N};
         cuuint64_t strides[3] = {(cuuint64_t)L.Cp * L.elem, (cuuint64_t)L.Cp * L.elem * pb.Win(),
                                  (cuuint64_t)L.Cp * L.elem * pb.Win() * pb.Hin()};
-        // Bounding box per image: w in [0, Win-1-D(S-1)], h in [0, Hin-1-D(R-1)]
-        // (the window origins of valid conv); the traversal steps U pixels
-        // (elementStrides), so it visits exactly the origins U*w, U*h of the
-        // output pixels, row by row, image by image; tap (r, s) is the
-        // per-load im2col offset (D*s, D*r).
-        int lower[2] = {0, 0};
-        int upper[2] = {-pb.D * (pb.S - 1), -pb.D * (pb.R - 1)};
+        // Bounding box per image: w in [-pw, Win-1+pw-D(S-1)], h likewise
+        // (the window origins; with padding they start outside the tensor,
+        // whose out-of-bounds elements TMA fills with zeros); the traversal
+        // steps U pixels (elementStrides), so it visits exactly the origins
+        // U*w - pw, U*h - ph of the output pixels, row by row, image by
+        // image; tap (r, s) is the per-load im2col offset (D*s, D*r).
+        int lower[2] = {-pb.pw, -pb.ph};
+        int upper[2] = {pb.pw - pb.D * (pb.S - 1), pb.ph - pb.D * (pb.R - 1)};
         cuuint32_t estr[4] = {1, (cuuint32_t)pb.U, (cuuint32_t)pb.U, 1};
         CUresult r = g_encode_im2col(&m.a, dt, 4, in_ws, dims, strides, lower, upper, (cuuint32_t)L.bkc,
                                      (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
@@ -999,6 +1004,8 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     prm.S = pb.S;
     prm.U = pb.U;
     prm.D = pb.D;
+    prm.ph = pb.ph;
+    prm.pw = pb.pw;
     prm.Cp = L.Cp;
     prm.bkc = L.bkc;
     prm.n_cblk = L.n_cblk;
@@ -1024,6 +1031,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         prm.C = pb.C;
         prm.P = (int)(pb.Hin() * pb.Win());
         prm.Win = (int)pb.Win();
+        prm.Hin = (int)pb.Hin();
         prm.npch = (int)L.npch;
         prm.cc = L.cc;
         prm.nch = L.nch;
@@ -1044,7 +1052,8 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
             const int m1 = (int)std::min<int64_t>((int64_t)(m_tile + 1) * tile_m, pb.M()) - 1;
             const int n = m1 / prm.HW;
             const int h = (m1 - n * prm.HW) / prm.W;
-            int e = n * (int)L.npch + (int)(((h * pb.U + pb.D * (pb.R - 1)) * pb.Win() + pb.Win() - 1) / 64) + 1;
+            const int64_t rb = std::min<int64_t>(std::max<int64_t>(h * pb.U - pb.ph + pb.D * (pb.R - 1), 0), pb.Hin() - 1);
+            int e = n * (int)L.npch + (int)((rb * pb.Win() + pb.Win() - 1) / 64) + 1;
             if (prm.n_groups > 0 && e < prm.gend[prm.n_groups - 1]) e = prm.gend[prm.n_groups - 1];
             prm.gend[prm.n_groups++] = e;
             if (wl == n_waves - 1) break;

@@ -25,10 +25,11 @@ import torch
 
 @dataclass(frozen=True)
 class Shape:
-    """H, W are OUTPUT extents.  U is the stride and D the dilation
-    (PAPER.md:201 footnote; Table 1's * layers); hin/win are explicit input
-    extents of a strided layer (0: the minimal (H-1)*U + D*(R-1) + 1).  Use
-    ``Shape.strided`` to build one from input extents as Table 1 lists them."""
+    """H, W are OUTPUT extents.  U is the stride, D the dilation
+    (PAPER.md:201 footnote; Table 1's * layers) and ph/pw the zero padding
+    (SURVEY NEXT-2); hin/win are explicit input extents of a general layer
+    (0: the minimal (H-1)*U + D*(R-1) + 1 - 2ph).  Use ``Shape.strided`` to
+    build one from input extents as Table 1 lists them."""
     N: int
     K: int
     C: int
@@ -40,27 +41,31 @@ class Shape:
     hin: int = 0
     win: int = 0
     D: int = 1
+    ph: int = 0
+    pw: int = 0
 
     @classmethod
-    def strided(cls, N, K, C, Hin, Win, R, S, U, D=1) -> "Shape":
+    def strided(cls, N, K, C, Hin, Win, R, S, U, D=1, ph=0, pw=0) -> "Shape":
         Re, Se = D * (R - 1) + 1, D * (S - 1) + 1
-        return cls(N, K, C, (Hin - Re) // U + 1, (Win - Se) // U + 1, R, S, U, Hin, Win, D)
+        return cls(N, K, C, (Hin + 2 * ph - Re) // U + 1, (Win + 2 * pw - Se) // U + 1, R, S, U, Hin, Win, D, ph, pw)
 
     @property
     def Hin(self) -> int:
-        return self.hin or (self.H - 1) * self.U + self.D * (self.R - 1) + 1
+        return self.hin or (self.H - 1) * self.U + self.D * (self.R - 1) + 1 - 2 * self.ph
 
     @property
     def Win(self) -> int:
-        return self.win or (self.W - 1) * self.U + self.D * (self.S - 1) + 1
+        return self.win or (self.W - 1) * self.U + self.D * (self.S - 1) + 1 - 2 * self.pw
 
     def plan_kwargs(self) -> dict:
-        """Keyword arguments of ConvPlan for this shape (stride, dilation, input extents)."""
-        if self.U == 1 and self.D == 1 and not self.hin and not self.win:
+        """Keyword arguments of ConvPlan for this shape (stride, dilation, padding, input extents)."""
+        if self.U == 1 and self.D == 1 and self.ph == 0 and self.pw == 0 and not self.hin and not self.win:
             return {}
         kw = {"stride": self.U, "in_hw": (self.Hin, self.Win)}
         if self.D != 1:
             kw["dilation"] = self.D
+        if self.ph or self.pw:
+            kw["padding"] = (self.ph, self.pw)
         return kw
 
     @property

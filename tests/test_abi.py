@@ -258,3 +258,34 @@ def test_dilated_plans_offline(lib):
     with pytest.raises(conv.ConvError) as e:   # D(R-1) = 129 > 128
         conv.ConvPlan(1, 8, 8, 2, 2, 2, 2, dilation=129, in_hw=(131, 131), offline_device=sh, path="bf16")
     assert e.value.status == conv.CONV_ERR_INFEASIBLE
+
+
+def test_padded_plans_offline(lib):
+    """conv_plan_create_padded ("same"-padded layers):
+    describe() reports ph/pw and H = (Hin + 2ph - D(R-1) - 1)/U + 1; SIMT
+    uses v1 (v2 has no padding); pad 0 is the dilated plan; negative pads,
+    padded inputs smaller than the dilated kernel and pads past the TMA box
+    are rejected with the right status."""
+    sh = dict(sms=148, smem_optin=232448, l2_bytes=132120576)
+    for (Hin, R, U, D, ph, pw) in ((56, 3, 1, 1, 1, 1), (224, 7, 2, 1, 3, 3), (14, 3, 2, 2, 2, 1), (5, 3, 1, 1, 4, 0)):
+        H = (Hin + 2 * ph - D * (R - 1) - 1) // U + 1
+        W = (Hin + 2 * pw - D * (R - 1) - 1) // U + 1
+        p = conv.ConvPlan(1, 64, 32, H, W, R, R, stride=U, dilation=D, padding=(ph, pw), in_hw=(Hin, Hin),
+                          offline_device=sh)
+        d = p.describe()["problem"]
+        assert (d["U"], d["D"], d["ph"], d["pw"], d["Hin"], d["H"], d["W"]) == (U, D, ph, pw, Hin, H, W)
+        ps = conv.ConvPlan(1, 64, 32, H, W, R, R, stride=U, dilation=D, padding=(ph, pw), in_hw=(Hin, Hin),
+                           offline_device=sh, path="fp32_simt")
+        assert ps.describe()["tile"]["ver"] == 1
+    a = conv.ConvPlan(2, 64, 32, 13, 13, 3, 3, stride=2, dilation=2, in_hw=(30, 30), offline_device=sh).describe()
+    b = conv.ConvPlan(2, 64, 32, 13, 13, 3, 3, stride=2, dilation=2, padding=0, in_hw=(30, 30),
+                      offline_device=sh).describe()
+    assert a == b
+    assert not lib.conv_plan_create_padded(1, 1, 1, 8, 8, 3, 3, 1, 1, -1, 0)
+    assert "padding must be >= 0" in conv.last_error()
+    assert lib.conv_last_status() == conv.CONV_ERR_INVALID_ARGUMENT
+    assert not lib.conv_plan_create_padded(1, 1, 1, 1, 1, 5, 5, 1, 1, 1, 1)   # 3x3 padded input, 5x5 kernel
+    assert "smaller than the kernel" in conv.last_error()
+    with pytest.raises(conv.ConvError) as e:   # lower corner -129
+        conv.ConvPlan(1, 8, 8, 3 + 258 - 2, 3, 3, 3, padding=(129, 0), in_hw=(3, 5), offline_device=sh, path="bf16")
+    assert e.value.status == conv.CONV_ERR_INFEASIBLE

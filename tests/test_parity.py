@@ -456,6 +456,89 @@ def test_dilated_fused_and_cta_groups_bit_identical(path):
         assert abs(got[p] - v) <= 1e-4 * (1 + abs(v)), p
 
 
+# ---- zero padding ("same"-padded layers) -----------
+PADDED = [
+    Shape.strided(2, 128, 64, 56, 56, 3, 3, 1, 1, 1, 1),      # R4 "same"
+    Shape.strided(1, 64, 3, 224, 224, 7, 7, 2, 1, 3, 3),      # R1* as in ResNet (pad 3)
+    Shape.strided(1, 128, 64, 56, 56, 3, 3, 2, 1, 1, 1),      # R4* as in ResNet (pad 1)
+    Shape.strided(2, 40, 17, 13, 11, 3, 2, 1, 1, 2, 0),       # asymmetric pads, R != S
+    Shape.strided(1, 24, 8, 9, 10, 3, 3, 2, 2, 3, 1),         # stride + dilation + padding
+    Shape.strided(2, 16, 5, 5, 6, 3, 3, 1, 1, 4, 3),          # pad > kernel: border outputs read only zeros
+    Shape.strided(3, 24, 8, 16, 15, 1, 1, 1, 1, 2, 2),        # 1x1 with padding: zero rim
+]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("shape", PADDED,
+                         ids=lambda s: f"{s.N}x{s.K}x{s.C}x{s.Hin}x{s.Win}x{s.R}x{s.S}s{s.U}d{s.D}p{s.ph}_{s.pw}")
+def test_padded_parity(path, shape):
+    """Zero-padded Eq. 1 on every path against the padded oracle: tolerance
+    on real inputs (1e-5 against the oracle on the path's rounded inputs),
+    bit-exact on the integer twin (the padding contributes exact zeros)."""
+    inp, ker = make_inputs(shape, seed=91)
+    got, plan = run(shape, inp, ker, path)
+    d = plan.describe()["problem"]
+    assert (d["ph"], d["pw"], d["Hin"], d["Win"], d["H"], d["W"]) == (shape.ph, shape.pw, shape.Hin, shape.Win,
+                                                                       shape.H, shape.W)
+    pad = (shape.ph, shape.pw)
+    ref = oracle.conv_eq1_padded(inp.numpy(), ker.numpy(), shape.U, shape.D, pad)
+    assert got.shape == ref.shape
+    assert rel_l2(got, ref) <= TOL[path]
+    ref_r = oracle.conv_eq1_padded(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), shape.U, shape.D, pad)
+    assert rel_l2(got, ref_r) <= 1e-5
+    xi, wi = make_inputs(shape, seed=92, kind="int")
+    goti, _ = run(shape, xi, wi, path)
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1_padded(xi.numpy(), wi.numpy(), shape.U, shape.D, pad))
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_padded_fused_and_cta_groups_bit_identical(path):
+    """A multi-wave "same"-padded layer: the fused in-kernel transform (its
+    chunk ranges clamp the padding rows), both CTA-group sizes and the
+    separate repack give the same bits; sampled points against the oracle."""
+    sh = Shape.strided(96, 128, 64, 32, 32, 3, 3, 1, 1, 1, 1)
+    inp, ker = make_inputs(sh, seed=93)
+    i, k = inp.cuda(), ker.cuda()
+    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1", **sh.plan_kwargs()).run(i, k)
+    for spec in ("fuse=0,cg=2", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0", "fuse=1,cg=2,bn=64"):
+        out = conv.ConvPlan(*sh.as_tuple(), path=path, tile=spec, **sh.plan_kwargs()).run(i, k)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), spec
+    ref64 = oracle.conv_eq1_padded(ROUND[path](inp.numpy()[:2]), ROUND[path](ker.numpy()), 1, 1, 1)
+    assert rel_l2(ref[:2].cpu().numpy(), ref64) <= 1e-5
+    rng = np.random.default_rng(94)
+    x, w = ROUND[path](inp.numpy()), ROUND[path](ker.numpy())
+    got = ref.cpu().numpy()
+    for _ in range(64):
+        p = (rng.integers(sh.N), rng.integers(sh.K), rng.choice([0, sh.H - 1, rng.integers(sh.H)]), rng.integers(sh.W))
+        v = oracle.conv_eq1_point(x, w, *p, padding=1)
+        assert abs(got[p] - v) <= 1e-4 * (1 + abs(v)), p
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_table1_layers_same_padded(path):
+    """Table 1's conv2d layers as the networks run them, with
+    "same" padding R//2 (stride 2 layers: ceil(Hin/2) outputs): whole output
+    vs the padded oracle for layers <= 0.3 GFLOP, 48 sampled points (border
+    rows included) for the larger ones."""
+    from paper_2101_09808_b200.inputs import TABLE1_ROWS
+    rng = np.random.default_rng(95)
+    for name, K, C, HW, R, U in TABLE1_ROWS:
+        sh = Shape.strided(1, K, C, HW, HW, R, R, U, 1, R // 2, R // 2)
+        inp, ker = make_inputs(sh, seed=96)
+        got, _ = run(sh, inp, ker, path)
+        x, w = inp.numpy(), ker.numpy()
+        if sh.flops <= 3e8:
+            ref = oracle.conv_eq1_padded(x, w, U, 1, R // 2)
+            assert rel_l2(got, ref) <= TOL[path], name
+        else:
+            pts = [(0, rng.integers(K), rng.choice([0, sh.H - 1, rng.integers(sh.H)]),
+                    rng.choice([0, sh.W - 1, rng.integers(sh.W)])) for _ in range(48)]
+            ref = np.array([oracle.conv_eq1_point(x, w, *p, stride=U, padding=R // 2) for p in pts])
+            val = np.array([got[p] for p in pts])
+            assert rel_l2(val, ref) <= 2 * TOL[path], name
+
+
 @pytest.mark.parametrize("path", PATHS)
 def test_table1_layers(path):
     """Every conv2d layer of PAPER.md:439 Table 1 (batch 1, stride 1/2, input
