@@ -432,7 +432,9 @@ def bench_table1(args):
     stride 1 or 2, Table 1's input extents), one JSON line per layer and
     path, timed like the headline (CUDA-graph replay of conv_run, L2 flushed
     before every step outside the event pair, CUDA events, after warm-up).
-    A NEXT-4 study, not the driver's bench line."""
+    A NEXT-4 study, not the driver's bench line.
+    ``--pad same`` runs the layers as the networks do, zero padding R//2
+    (NEXT-2)."""
     from paper_2101_09808_b200 import conv
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -446,10 +448,14 @@ def bench_table1(args):
     names = [n for n in TABLE1 if not args.layers or n in args.layers.split(",")]
     for name in names:
         sh = TABLE1[name]
+        if args.pad == "same":
+            sh = Shape.strided(sh.N, sh.K, sh.C, sh.Hin, sh.Win, sh.R, sh.S, sh.U, 1, sh.R // 2, sh.S // 2)
         inp, ker = make_inputs(sh, seed=0)
         d_in, d_ker = inp.to(dev), ker.to(dev)
         for path in paths:
             plan = conv.ConvPlan(*sh.as_tuple(), path=path, **sh.plan_kwargs())
+            if args.tile and path != "fp32_simt":
+                plan.set_tile(args.tile)
             out, ws = plan.new_output(dev), plan.new_workspace(dev)
             cap = torch.cuda.Stream(device=dev)
             cap.wait_stream(stream)
@@ -470,15 +476,25 @@ def bench_table1(args):
                 ev[i][1].record(stream)
             torch.cuda.synchronize(dev)
             ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+            # per-kernel attribution (events between the kernels, same flush)
+            nk = plan.num_kernels
+            kev = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
+            for i in range(args.steps):
+                flush.zero_()
+                torch.sum(flush_rd, dim=0, out=flush_out)
+                plan.run_events(d_in, d_ker, out, ws, kev[i])
+            torch.cuda.synchronize(dev)
+            kern_us = [round(float(np.mean([e[j].elapsed_time(e[j + 1]) for e in kev])) * 1e3, 2) for j in range(nk)]
             peak, bound, _ = path_peak(plan.path, peaks)
             roof_us = max(sh.flops / (peak * 1e12), 4.0 * (sh.N * sh.C * sh.Hin * sh.Win + sh.K * sh.C * sh.R * sh.S +
                                                            sh.N * sh.K * sh.H * sh.W) / (peaks["hbm_gbs"] * 1e9)) * 1e6
             d = plan.describe()
             print(json.dumps({
-                "layer": name, "path": plan.path, "K": sh.K, "C": sh.C, "Hin": sh.Hin, "R": sh.R, "U": sh.U,
+                "layer": name, "path": plan.path, "K": sh.K, "C": sh.C, "Hin": sh.Hin, "R": sh.R, "U": sh.U, "pad": sh.ph,
                 "out": [sh.H, sh.W], "gflop": round(sh.flops / 1e9, 4), "step_us": round(ms * 1e3, 2),
                 "tflops": round(sh.flops / (ms * 1e-3) / 1e12, 3), "roofline_us": round(roof_us, 3),
-                "frac": round(roof_us / (ms * 1e3), 4), "tile": d["tile"], "peak_source": peak_src}), flush=True)
+                "frac": round(roof_us / (ms * 1e3), 4), "kernels_us": kern_us, "tile": d["tile"],
+                "peak_source": peak_src}), flush=True)
 
 
 def main():
@@ -497,6 +513,8 @@ def main():
     ap.add_argument("--tile", default=None, help="force a tile (conv_plan_set_tile spec, e.g. 'fuse=0,bn=128'); experiments")
     ap.add_argument("--sweep", default=None, choices=["table1"], help="study mode: every Table-1 layer (one JSON line each)")
     ap.add_argument("--layers", default=None, help="--sweep: comma-separated layer names (default all)")
+    ap.add_argument("--pad", default="valid", choices=["valid", "same"],
+                    help="--sweep: Table 1 as listed (valid, Eq. 1) or with zero padding R//2 (same)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

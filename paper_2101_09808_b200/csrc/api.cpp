@@ -57,7 +57,7 @@ struct conv_plan {
     SimtTile simt;
     ModelResult model;
     // forced tile (conv_plan_set_tile)
-    int force_bn = 0, force_stages = 0, force_cg = 0, force_kbs = 0, force_fuse = -1, force_pre_c = -1;
+    TcForce force_tc;
     SimtTile force_simt;
     unsigned force_simt_mask = 0;
     // conv_run_host pipeline (created on first use, guarded by host_mu)
@@ -97,7 +97,9 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 static size_t ws_bytes(const conv_plan* p) {
     if (p->path == CONV_PATH_FP32_SIMT) return align256(simt_ws_bytes(p->pb, p->simt));
-    return align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes) + (p->tc.fuse ? align256(p->tcl.flag_bytes) : 0);
+    // aux region: the fused transform's flags, or split-K's counters + partials
+    const size_t aux = p->tc.fuse ? p->tcl.flag_bytes : tc_split_bytes(p->pb, p->tcl, p->tc);
+    return align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes) + align256(aux);
 }
 
 // Re-run the selector for the requested path (Alg. 1:
@@ -118,7 +120,7 @@ static conv_status select(conv_plan* p) {
         case CONV_PATH_TF32:
         case CONV_PATH_BF16: {
             const bool bf16 = p->requested == CONV_PATH_BF16;
-            if (!select_tc(pb, p->dev, bf16, tt, rt, p->force_bn, p->force_stages, p->force_cg, p->force_kbs, p->force_fuse, p->force_pre_c, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            if (!select_tc(pb, p->dev, bf16, tt, rt, p->force_tc, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             p->tc = tt; p->model = rt; p->path = p->requested; p->tcl = tc_layout(pb, bf16);
             break;
         }
@@ -127,7 +129,7 @@ static conv_status select(conv_plan* p) {
             // AUTO keeps fp32 inputs or TF32 products (the precision of the
             // paper's fp32 method); BF16 only when requested.
             const bool ok_s = select_simt(pb, p->dev, st, rs, fs, p->force_simt_mask, why);
-            const bool ok_t = select_tc(pb, p->dev, false, tt, rt, p->force_bn, p->force_stages, p->force_cg, p->force_kbs, p->force_fuse, p->force_pre_c, why);
+            const bool ok_t = select_tc(pb, p->dev, false, tt, rt, p->force_tc, why);
             if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             if (ok_t && (!ok_s || rt.model_us < rs.model_us)) {
                 p->tc = tt; p->model = rt; p->path = CONV_PATH_TF32; p->tcl = tc_layout(pb, false);
@@ -306,7 +308,7 @@ extern "C" conv_status conv_plan_set_path(conv_plan* p, conv_path path) {
 
 extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
     if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
-    int fbn = 0, fst = 0, fcg = 0, fkbs = 0, ffuse = -1, fpre = -1;
+    TcForce ft;
     SimtTile fs;
     unsigned mask = 0;
     if (spec && *spec) {
@@ -325,12 +327,13 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             long v = strtol(kv.c_str() + eq + 1, &end, 10);
             const long vmin = (key == "fuse" || key == "pre_c") ? 0 : 1;
             if (!end || *end || v < vmin || v > 4096) return fail(CONV_ERR_INVALID_ARGUMENT, "bad value in '%s'", kv.c_str());
-            if (key == "bn") fbn = (int)v;
-            else if (key == "stages") fst = (int)v;
-            else if (key == "cg") fcg = (int)v;
-            else if (key == "kbs") fkbs = (int)v;
-            else if (key == "fuse") ffuse = v ? 1 : 0;
-            else if (key == "pre_c") fpre = (int)v;
+            if (key == "bn") ft.bn = (int)v;
+            else if (key == "stages") ft.stages = (int)v;
+            else if (key == "cg") ft.cg = (int)v;
+            else if (key == "kbs") ft.kbs = (int)v;
+            else if (key == "splits") ft.splits = (int)v;
+            else if (key == "fuse") ft.fuse = v ? 1 : 0;
+            else if (key == "pre_c") ft.pre_c = (int)v;
             else if (key == "tk") { fs.tk = (int)v; mask |= 1; }
             else if (key == "tw") { fs.tw = (int)v; mask |= 2; }
             else if (key == "kg") { fs.kg = (int)v; mask |= 4; }
@@ -341,21 +344,22 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "ver") { fs.ver = (int)v; mask |= 128; }
             else return fail(CONV_ERR_INVALID_ARGUMENT, "unknown tile key '%s'", key.c_str());
         }
-        if (fbn && fbn != 32 && fbn != 64 && fbn != 128 && fbn != 192 && fbn != 256)
+        if (ft.bn && ft.bn != 32 && ft.bn != 64 && ft.bn != 128 && ft.bn != 192 && ft.bn != 256)
             return fail(CONV_ERR_INFEASIBLE, "bn must be one of 32, 64, 128, 192, 256");
-        if (fkbs && fkbs != 1 && fkbs != 2 && fkbs != 3 && fkbs != 4 && fkbs != 6)
+        if (ft.kbs && ft.kbs != 1 && ft.kbs != 2 && ft.kbs != 3 && ft.kbs != 4 && ft.kbs != 6)
             return fail(CONV_ERR_INFEASIBLE, "kbs must be 1, 2, 3, 4 or 6");
-        if (fcg && fcg != 1 && fcg != 2) return fail(CONV_ERR_INFEASIBLE, "cg must be 1 or 2");
+        if (ft.cg && ft.cg != 1 && ft.cg != 2) return fail(CONV_ERR_INFEASIBLE, "cg must be 1 or 2");
+        if (ft.splits > 16) return fail(CONV_ERR_INFEASIBLE, "splits must be <= 16");
+        if (ft.splits > 1 && ft.fuse == 1) return fail(CONV_ERR_INFEASIBLE, "split-K needs fuse=0");
     }
-    const int obn = p->force_bn, ost = p->force_stages, ocg = p->force_cg, okbs = p->force_kbs, ofuse = p->force_fuse,
-              opre = p->force_pre_c;
+    const TcForce oft = p->force_tc;
     const SimtTile ofs = p->force_simt;
     const unsigned omask = p->force_simt_mask;
-    p->force_bn = fbn; p->force_stages = fst; p->force_cg = fcg; p->force_kbs = fkbs; p->force_fuse = ffuse; p->force_pre_c = fpre;
+    p->force_tc = ft;
     p->force_simt = fs; p->force_simt_mask = mask;
     conv_status s = select(p);
     if (s != CONV_OK) {
-        p->force_bn = obn; p->force_stages = ost; p->force_cg = ocg; p->force_kbs = okbs; p->force_fuse = ofuse; p->force_pre_c = opre;
+        p->force_tc = oft;
         p->force_simt = ofs; p->force_simt_mask = omask;
         select(p);
     }
@@ -397,8 +401,8 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
                  32 * p->simt.kg * p->simt.pw);
     } else {
-        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
-                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
+        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
+                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
                  p->tc.fuse ? std::min(p->tc.pre_c, p->tcl.Cp) : 0,
                  p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
     }
@@ -448,7 +452,8 @@ static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0
         const size_t per_img = p->tcl.in_ws_bytes / (size_t)p->pb.N;
         void* in_ws = wsb + per_img * (size_t)n0;
         void* ker_ws = wsb + align256(p->tcl.in_ws_bytes);
-        void* flag_ws = p->tc.fuse ? wsb + align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes) : nullptr;
+        void* flag_ws = (p->tc.fuse || p->tc.splits > 1) ? wsb + align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes)
+                                                         : nullptr;
         e = tc_run(sub, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, in_ws, ker_ws, flag_ws, st, p->dev.sms,
                    evp, err);
     }

@@ -60,6 +60,8 @@ struct TcTile {
                          //    (cooperative chunk transform, warps 0-3 of every CTA)
     int tnb = 2;         // fuse: input staging buffers of the transform (2..6)
     int pre_c = 64;      // fuse: channels of wave 0's input converted by the repack launch (prologue)
+    int splits = 1;      // split-K (fuse = 0): each tile's k loop in `splits` stage-aligned ranges,
+                         //    fp32 partials summed in split order by the tile's last CTA
 };
 
 struct TcLayout {        // derived from Problem + element size
@@ -97,6 +99,17 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
                           const RepackFuse& fz);
 
 TcLayout tc_layout(const Problem& p, bool bf16);
+
+// Split-K geometry of a tile choice: k iterations per split (stage-aligned)
+// and the workspace the partial slabs + arrival counters take (0 if
+// t.splits == 1).  A split count whose last range would be empty is invalid
+// (tc_split_kper returns 0).
+int tc_split_kper(const Problem& pb, const TcLayout& L, const TcTile& t);
+size_t tc_split_bytes(const Problem& pb, const TcLayout& L, const TcTile& t);
+// Whether a split count is runnable for this tile: fuse = 0, cg = 1, BN <=
+// 128, non-empty stage-aligned ranges, the reduction shares fit the pipeline
+// smem (the one-wave condition depends on the device: the selector / tc_run).
+bool tc_split_ok(const Problem& pb, const TcLayout& L, const TcTile& t);
 size_t tc_smem_bytes(const TcLayout& L, const TcTile& t);
 
 // Launch the repack (K1 + K2, one launch) and K3 (tcgen05 implicit GEMM).

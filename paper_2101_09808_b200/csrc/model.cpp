@@ -173,6 +173,14 @@ static const double kEpiStoreBW = 5.0e12;  // bytes/s the whole chip's epilogues
 // fused transform (measured r01b, batched layer): 67 MB of fp32 In in ~35 us
 // per 148 CTAs while the MMAs run, 9% MMA slowdown, ~6 us startup chain
 static const double kTransformBW = 1.9e12;
+// Split-K epilogue: arrival fence + atomic + wait + the share's bulk copy
+// round trip, and one SM's L2 read rate for the reduction share.  Fitted to
+// the r01b Table-1 A/B (profiles/r01b/splitk_ab.jsonl): with 2.5 us the
+// modeled gain of every split layer matches the measured one within ~1 us,
+// and the shallow-k layers (R6, R7, M4: 18 k-blocks), where splitting
+// measured 1-2 us slower, stay unsplit.
+static const double kSplitSyncUs = 2.5;
+static const double kSplitReadBW = 150e9;
 static const double kTransformDrag = 1.09;
 static const double kTransformStartUs = 6.0;
 
@@ -182,9 +190,11 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     const long tm = 128L * t.cg;
     const long mt = (long)((pb.M() + tm - 1) / tm), nt = (pb.K + t.bn - 1) / t.bn;
     const long units = dev.sms / t.cg;
+    const int splits = std::max(1, t.splits);
     r.tiles = mt * nt;
-    r.ctas = std::min<long>(r.tiles, units) * t.cg;
-    r.wave_eff = wave_eff(r.tiles, units);
+    const long work = r.tiles * splits;                 // split-K work items
+    r.ctas = std::min<long>(work, units) * t.cg;
+    r.wave_eff = wave_eff(work, units);
     const double peak = bf16 ? dev.peak_bf16 : dev.peak_tf32;
     const double flops_issued = 2.0 * (double)mt * tm * (double)nt * t.bn * (double)pb.R * pb.S * L.Cp;
     r.t_comp_us = flops_issued / peak * 1e6;
@@ -192,8 +202,8 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     r.t_l2_us = r.dv_l2_smem / dev.bw_l2 * 1e6;
     // tensor pipe of the busiest unit: ceil(tiles/units) tiles, each
     // R*S*n_cblk/kbs stages of kbs*(sw/32) MMAs.
-    const double tiles_per_unit = ceil((double)r.tiles / units);
-    const double stages_per_tile = (double)pb.R * pb.S * L.n_cblk / t.kbs;   // k_iters / kbs
+    const double tiles_per_unit = ceil((double)work / units);
+    const double stages_per_tile = (double)tc_split_kper(pb, L, t) / t.kbs;   // per work item
     const double mma_clk = std::max(t.bn / 2.0, 48.0);
     // a stage also cannot turn over faster than the producer -> TMA -> MMA
     // -> commit round trip allows (kStageLatClk, r01b selector study: on
@@ -204,7 +214,14 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
     const double t_smem_us = kblocks_per_sm * 2.0 * (128.0 + (double)t.bn / t.cg) * L.sw /
                              kSmemBytesPerClk / kClockHz * 1e6;
     // last tile's epilogue is not overlapped: every CTA stores 128 x BN fp32
-    const double t_tail_us = std::min<double>(r.tiles * t.cg, dev.sms) * 128.0 * std::min(t.bn, pb.K) * 4.0 / kEpiStoreBW * 1e6;
+    double t_tail_us = std::min<double>(work * t.cg, dev.sms) * 128.0 * std::min(t.bn, pb.K) * 4.0 / kEpiStoreBW * 1e6;
+    if (splits > 1) {
+        // partial slab store + arrival (fence, atomic, wait for the tile's
+        // other splits) + each CTA's reduction share: the tile's `splits`
+        // slabs over 1/splits of the columns = one slab's bytes per CTA from
+        // L2 (~kSplitReadBW per SM)
+        t_tail_us = 2.0 * t_tail_us + kSplitSyncUs + 128.0 * t.bn * 4.0 / kSplitReadBW * 1e6;
+    }
     // HBM: repacks (read fp32 In/Ker, write workspace) + main kernel (read
     // workspace once -- the 9x im2col replay and the k-tile re-reads hit L2 --
     // and write fp32 Out once).
@@ -261,9 +278,10 @@ static int tc_max_stages(const Device& dev, const TcLayout& L, int bn, int cg, i
     return 0;
 }
 
-bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& best_r,
-               int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, int force_pre_c,
+bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& best_r, const TcForce& f,
                std::string& why) {
+    const int force_bn = f.bn, force_stages = f.stages, force_cg = f.cg, force_kbs = f.kbs, force_fuse = f.fuse,
+              force_pre_c = f.pre_c;
     const TcLayout L = tc_layout(pb, bf16);
     {
         // the TMA im2col bounding-box corners of a 4-D map lie in [-128, 127]:
@@ -320,8 +338,26 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
                             if (tc_smem_bytes(L, u) <= dev.smem_optin) { t.tnb = nb; break; }
                         }
                     }
-                    ModelResult r = model_tc(pb, dev, bf16, t);
-                    if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+                    // split-K (not fused): only while the tiles do not fill one
+                    // wave -- the k loop of a few long tiles then spreads over
+                    // the idle SMs (PAPER.md:375 parallelises over output
+                    // dimensions only: 8 CPU cores; 148 SMs at batch 1 need
+                    // the reduction split)
+                    const long tiles = ((pb.M() + 128L * cg - 1) / (128L * cg)) * ((pb.K + bn - 1) / bn);
+                    const long units = dev.sms / cg;
+                    static const int kFree[] = {1, 2, 3, 4, 6, 8, 12, 16};
+                    const int forced[] = {f.splits};
+                    const int* cand = f.splits ? forced : kFree;
+                    const int ncand = f.splits ? 1 : 8;
+                    for (int ci = 0; ci < ncand; ++ci) {
+                        const int sp = cand[ci];
+                        // (one wave: the split CTAs of a tile wait for each other)
+                        if (sp > 1 && (fuse || tiles * sp > units)) continue;
+                        t.splits = sp;
+                        if (!tc_split_ok(pb, L, t)) continue;
+                        ModelResult r = model_tc(pb, dev, bf16, t);
+                        if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+                    }
                 }
             }
         }

@@ -19,9 +19,14 @@ struct ModelResult {
     size_t smem = 0;         // dynamic shared memory per CTA
 };
 
+// Tensor-path tile keys forced through conv_plan_set_tile (0 / -1: free).
+struct TcForce {
+    int bn = 0, stages = 0, cg = 0, kbs = 0, splits = 0;
+    int fuse = -1, pre_c = -1;
+};
+
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t);
-bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& r,
-               int force_bn, int force_stages, int force_cg, int force_kbs, int force_fuse, int force_pre_c,
+bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& r, const TcForce& f,
                std::string& why);
 ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t);
 // forced_mask bits: 1 tk, 2 tw, 4 kg, 8 pw, 16 tn, 32 th, 64 bc, 128 ver

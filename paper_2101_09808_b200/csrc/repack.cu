@@ -77,6 +77,62 @@ struct RepackGeom {
     int cc_f;                        // fused: channels per chunk (flag column granularity)
 };
 
+// K1, one CTA (NT threads): Ker row k = blockIdx.x / ker_chunks, channels
+// [c0, c0 + cc): stage the contiguous KCRS slice (cload * RS fp32) in shared
+// memory, then write it as [RS][Cp] (channels >= C zero), converted.
+template <bool BF16, int NT>
+__device__ __forceinline__ void ker_repack_cta(const float* __restrict__ ker, typename Elem<BF16>::T* __restrict__ ker_ws,
+                                               const RepackGeom& g, float* sm) {
+    const int tid = threadIdx.x;
+    const int64_t k = blockIdx.x / g.ker_chunks;
+    const int c0 = (blockIdx.x % g.ker_chunks) * g.cc;
+    const int c1 = min(c0 + g.cc, g.Cp);
+    const int cload = max(0, min(c1, g.C) - c0);
+    const float* src = ker + (k * g.C + c0) * g.RS;
+    // the whole slice in flight at once: asynchronous global -> shared copies
+    // (register round trips, even eight deep, cap a weight-heavy repack at
+    // ~2.5 TB/s)
+    const int nld = cload * g.RS;
+    for (int i = tid; i < nld; i += NT) {
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sm + i));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + i) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    typename Elem<BF16>::T* dst = ker_ws + k * (int64_t)g.RS * g.Cp;
+    const int width = c1 - c0;
+    // Wide slices: one output row (tap rs) at a time, channels across the
+    // threads -- no per-element division (a division per element made the
+    // weight-heavy repacks issue-bound at ~2.5 TB/s); bf16 pairs are packed
+    // into one 4-B store (c0, width and Cp are even: the host keeps cc even).
+    // Narrow slices (few channels, e.g. 3-channel 7x7 stems): the flattened
+    // (tap, channel) loop keeps every thread busy.
+    if (width < NT / 2) {
+        for (int e = tid; e < g.RS * width; e += NT) {
+            const int rs = e / width;
+            const int c = e - rs * width;
+            dst[(int64_t)rs * g.Cp + c0 + c] = Elem<BF16>::cvt(c0 + c < g.C ? sm[c * g.RS + rs] : 0.0f);
+        }
+    } else if (BF16 && !((c0 | width) & 1)) {
+        const int hw = width >> 1;
+        for (int rs = 0; rs < g.RS; ++rs) {
+            uint32_t* d = reinterpret_cast<uint32_t*>(dst + (int64_t)rs * g.Cp + c0);
+            for (int c2 = tid; c2 < hw; c2 += NT) {
+                const int c = 2 * c2;
+                const float lo = c0 + c < g.C ? sm[c * g.RS + rs] : 0.0f;
+                const float hi = c0 + c + 1 < g.C ? sm[(c + 1) * g.RS + rs] : 0.0f;
+                d[c2] = pack2_bf16(lo, hi);
+            }
+        }
+    } else {
+        for (int rs = 0; rs < g.RS; ++rs) {
+            typename Elem<BF16>::T* d = dst + (int64_t)rs * g.Cp + c0;
+            for (int c = tid; c < width; c += NT)
+                d[c] = Elem<BF16>::cvt(c0 + c < g.C ? sm[c * g.RS + rs] : 0.0f);
+        }
+    }
+}
+
 template <bool BF16>
 __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, const float* __restrict__ ker,
                                                   typename Elem<BF16>::T* __restrict__ in_ws,
@@ -100,20 +156,7 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
                 if (!pre) g.zero_ptr[i] = 0;
             }
         }
-        const int64_t k = blockIdx.x / g.ker_chunks;
-        const int c0 = (blockIdx.x % g.ker_chunks) * g.cc;
-        const int c1 = min(c0 + g.cc, g.Cp);
-        const int cload = max(0, min(c1, g.C) - c0);
-        const float* src = ker + (k * g.C + c0) * g.RS;
-        for (int i = tid; i < cload * g.RS; i += 256) sm[i] = __ldg(src + i);
-        __syncthreads();
-        typename Elem<BF16>::T* dst = ker_ws + k * (int64_t)g.RS * g.Cp;
-        const int width = c1 - c0;
-        for (int i = tid; i < g.RS * width; i += 256) {
-            const int rs = i / width;
-            const int c = c0 + (i - rs * width);
-            dst[(int64_t)rs * g.Cp + c] = Elem<BF16>::cvt(c < g.C ? sm[(c - c0) * g.RS + rs] : 0.0f);
-        }
+        ker_repack_cta<BF16, 256>(ker, ker_ws, g, sm);
         return;
     }
     // ---- K2 ----
@@ -217,21 +260,7 @@ __global__ void __launch_bounds__(128) repack_tma(const float* __restrict__ ker,
     if ((int)blockIdx.x >= g.pdl_from) asm volatile("griddepcontrol.launch_dependents;");
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     if ((int)blockIdx.x < g.n_ker) {
-        float* filt = reinterpret_cast<float*>(sm);
-        const int64_t k = blockIdx.x / g.ker_chunks;
-        const int c0 = (blockIdx.x % g.ker_chunks) * g.cc;
-        const int c1 = min(c0 + g.cc, g.Cp);
-        const int cload = max(0, min(c1, g.C) - c0);
-        const float* src = ker + (k * g.C + c0) * g.RS;
-        for (int i = tid; i < cload * g.RS; i += 128) filt[i] = __ldg(src + i);
-        __syncthreads();
-        typename Elem<BF16>::T* dst = ker_ws + k * (int64_t)g.RS * g.Cp;
-        const int width = c1 - c0;
-        for (int i = tid; i < g.RS * width; i += 128) {
-            const int rs = i / width;
-            const int c = c0 + (i - rs * width);
-            dst[(int64_t)rs * g.Cp + c] = Elem<BF16>::cvt(c < g.C ? filt[(c - c0) * g.RS + rs] : 0.0f);
-        }
+        ker_repack_cta<BF16, 128>(ker, ker_ws, g, reinterpret_cast<float*>(sm));
         return;
     }
     float* in_buf[2] = {reinterpret_cast<float*>(sm), reinterpret_cast<float*>(sm + 16384)};
@@ -330,6 +359,7 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
     g.RS = pb.R * pb.S;
     // channels per K1 CTA so that the staged slice is <= 32 KB (at least 1)
     g.cc = std::max(1, std::min(Cp, (int)(32768 / (4 * g.RS))));
+    if (g.cc > 1) g.cc &= ~1;   // even: bf16 channel pairs share a 4-B store
     g.ker_chunks = (Cp + g.cc - 1) / g.cc;
     g.n_ker = pb.K * g.ker_chunks;
     g.P = pb.Hin() * pb.Win();

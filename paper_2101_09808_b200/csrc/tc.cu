@@ -75,6 +75,16 @@ struct TcParams {
     int k_iters;      // R*S*n_cblk
     int num_n_tiles;
     int num_tiles;
+    // split-K (fuse = 0, one wave): work item w = (tile w / splits, split
+    // w % splits) covers k iterations [split * kper, min(k_iters, (split + 1)
+    // * kper)) of the fixed k order; each writes an fp32 partial slab, waits
+    // for the tile's other splits, then sums a 1/splits column share of the
+    // slabs in split order into Out
+    int splits;
+    int kper;                 // k iterations per split (a multiple of kbs)
+    int num_work;             // num_tiles * splits
+    float* part;              // [num_work][CG][BN][128] partial slabs
+    int* tile_ctr;            // [num_tiles][CG] arrivals (zeroed by the repack launch)
     int stages;
     int kbs;                  // k-blocks per pipeline stage (1, 2 or 4)
     uint32_t sw;              // 32 / 64 / 128 (bytes per operand row per k-block)
@@ -264,6 +274,52 @@ __device__ __forceinline__ void store_accumulator(const TcParams& p, uint32_t tm
     }
 }
 
+// Split-K: this thread's accumulator row (TMEM lane q*32 + lane) of work
+// item w -> its partial slab, column-major (a warp writes 128 contiguous B
+// per column).
+template <int BN, int CG>
+__device__ __forceinline__ void store_partial(const TcParams& p, uint32_t tmem_base, int w, int acc, uint32_t rank,
+                                              int q, uint32_t lane) {
+    float* slab = p.part + ((size_t)w * CG + rank) * (kBM * BN) + q * 32 + lane;
+    const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+    for (int j0 = 0; j0 < BN; j0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t0 + (uint32_t)j0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) __stcg(slab + (size_t)(j0 + j) * kBM, __uint_as_float(v[j]));
+    }
+}
+
+// Split-K reduction share of split `sp` (CG = 1): columns [c_lo, c_hi) of
+// the tile, staged in shared memory as `splits` consecutive [ncols][128]
+// blocks (one per slab, bulk-copied from L2); this thread's row of each
+// column is the sum of the slabs in split order 0, 1, ..., splits-1 (fixed,
+// so the result is deterministic).
+template <int BN>
+__device__ __forceinline__ void reduce_share(const TcParams& p, int tile, const float* red, int c_lo, int c_hi,
+                                             int q, uint32_t lane) {
+    const int m_tile = tile / p.num_n_tiles;
+    const int n_tile = tile - m_tile * p.num_n_tiles;
+    const int row = q * 32 + (int)lane;
+    const int m = m_tile * kBM + row;
+    if (m >= p.M) return;
+    const int k0 = n_tile * BN;
+    const int img = m / p.HW, pix = m - img * p.HW;
+    float* obase = p.out + ((int64_t)img * p.K + k0) * p.HW + pix;
+    const int ncols = c_hi - c_lo, cend = min(c_hi, p.K - k0);
+    const float* r = red + row;
+#pragma unroll 1
+    for (int c = c_lo; c < cend; ++c) {
+        const float* rc = r + (c - c_lo) * kBM;
+        float acc = rc[0];
+#pragma unroll 4
+        for (int sp = 1; sp < p.splits; ++sp) acc += rc[(size_t)sp * ncols * kBM];
+        __stcs(obase + (int64_t)c * p.HW, acc);
+    }
+}
+
 // CG = 1: one CTA per 128-pixel tile (tcgen05 cta_group::1, M = 128).
 // CG = 2: a CTA pair (cluster of 2 on one TPC) per 256-pixel tile
 //   (cta_group::2, M = 256): each CTA loads its own 128 A rows and HALF of
@@ -271,7 +327,7 @@ __device__ __forceinline__ void store_accumulator(const TcParams& p, uint32_t tm
 //   shared memory, and each CTA's TMEM receives its own 128 accumulator rows.
 //   Per SM this halves the B operand traffic (L2 -> SMEM and SMEM -> tensor
 //   core), which is what bounds the 1-CTA kernel on wide tiles.
-template <int BN, bool BF16, int CG, int KSTEPS>
+template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b,
@@ -349,7 +405,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t wflavor = (p.debug >> 3) & 3;
-    const bool kSplitLast = CONV_SPLIT_LAST && BN >= 64 && !(p.debug & 32);
+    const bool kSplitLast = !SPLIT && CONV_SPLIT_LAST && BN >= 64 && !(p.debug & 32);
     // Programmatic dependent launch: everything above overlapped the tail of
     // the repack launch; from here on the repacked workspace (and, fused, the
     // zeroed chunk flags) is read and Out written, so wait for the preceding
@@ -370,7 +426,10 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             int tiles_done = 0;                           // fuse: tiles of this CTA so far
             int ready_seen = 0;                           // fuse: last value read from ready_ctr
             long long ready_wait = 0;
-            for (int tile = unit; tile < p.num_tiles; tile += nunits, ++tiles_done) {
+            for (int wi = unit; wi < p.num_work; wi += nunits, ++tiles_done) {
+                const int tile = SPLIT ? wi / p.splits : wi;
+                const int it_beg = SPLIT ? (wi - tile * p.splits) * p.kper : 0;
+                const int it_end = SPLIT ? min(p.k_iters, it_beg + p.kper) : p.k_iters;
                 const int m_tile = tile / p.num_n_tiles;
                 const int n_tile = tile - m_tile * p.num_n_tiles;
                 const int m0 = m_tile * (kBM * CG) + (int)rank * kBM;
@@ -384,7 +443,11 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 // tracked by counters (no divisions); a stage holds kbs
                 // consecutive iterations, so the order does not depend on kbs.
                 int cb = 0, r = 0, s = 0;
-                for (int it0 = 0; it0 < p.k_iters; it0 += p.kbs) {
+                if (SPLIT && it_beg) {                    // split-K: start mid-order
+                    if (p.tap_outer) { cb = it_beg % p.n_cblk; s = (it_beg / p.n_cblk) % p.S; r = it_beg / (p.n_cblk * p.S); }
+                    else { s = it_beg % p.S; r = (it_beg / p.S) % p.R; cb = it_beg / (p.S * p.R); }
+                }
+                for (int it0 = it_beg; it0 < it_end; it0 += p.kbs) {
                     const int cb_s = cb, r_s = r, s_s = s;
                     // advance the counters past this stage (all lanes, uniform)
                     int cb_last = cb;
@@ -469,11 +532,14 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             constexpr uint32_t a_blk = (kBM * kSw) >> 4, b_blk = ((BN / CG) * kSw) >> 4;
             const bool no_mma = (p.debug & 1) != 0;
             const int kbs = p.kbs;
-            const int iters = p.k_iters / kbs;
+
             unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
             int ti = 0;
             if (tr && lane == 0) tr[0] = globaltimer_ns();
-            for (int tile = unit; tile < p.num_tiles; tile += nunits, ++ti) {
+            for (int wi = unit; wi < p.num_work; wi += nunits, ++ti) {
+                const int tile = SPLIT ? wi / p.splits : wi;
+                const int it_beg = SPLIT ? (wi - tile * p.splits) * p.kper : 0;
+                const int iters = SPLIT ? (min(p.k_iters, it_beg + p.kper) - it_beg) / kbs : p.k_iters / kbs;
                 mbar_wait_flavor(&tmem_empty[acc], acc_phase ^ 1, wflavor);
                 tc_fence_after();
                 if (tr && lane == 0 && ti < 8) tr[1 + 4 * ti] = globaltimer_ns();
@@ -517,7 +583,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 if (elect_one_sync()) {
                     if (CG == 2) tc_commit_pair_mc(&tmem_full[acc], 0x3);
                     else tc_commit(&tmem_full[acc]);
-                    if (kSplitLast && tile + nunits >= p.num_tiles) {
+                    if (kSplitLast && wi + nunits >= p.num_work) {
                         if (CG == 2) tc_commit_pair_mc(last_full, 0x3);
                         else tc_commit(last_full);
                     }
@@ -727,13 +793,49 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         // ===== epilogue: TMEM -> registers -> NCHW Out =====
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = unit; tile < p.num_tiles; tile += nunits) {
+        for (int wi = unit; wi < p.num_work; wi += nunits) {
+            const int tile = SPLIT ? wi / p.splits : wi;
             mbar_wait_sleep(&tmem_full[acc], acc_phase, 256);
             tc_fence_after();
-            const int ti_e = (tile - unit) / nunits;
+            if constexpr (SPLIT) {
+                // (CG = 1, one wave: one work item per CTA, so the pipeline's
+                // smem is idle now and every split of the tile is resident)
+                store_partial<BN, 1>(p, tmem_base, wi, acc, 0, warp & 3, lane);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                const int sp = wi - tile * p.splits;
+                const int c_lo = BN * sp / p.splits, c_hi = BN * (sp + 1) / p.splits;
+                float* red = reinterpret_cast<float*>(smem);
+                __threadfence();                          // this thread's slab stores -> GPU scope
+                named_bar_sync(2, 128);
+                if (warp == 4 && lane == 0) {
+                    // arrive on the tile's counter, wait for its other splits,
+                    // then bulk-copy this split's column share of every slab
+                    int* ctr = p.tile_ctr + tile;
+                    atomicAdd(ctr, 1);
+                    const long long t0 = clock64();
+                    while (ld_acquire_gpu(ctr) < p.splits) {
+                        __nanosleep(32);
+                        if (clock64() - t0 > 8000000000ll) __trap();
+                    }
+                    fence_proxy_async_global();           // other CTAs' generic stores -> bulk-copy reads
+                    const uint32_t bytes = (uint32_t)(c_hi - c_lo) * kBM * 4;
+                    mbar_arrive_expect_tx(last_full, bytes * p.splits);
+                    const float* src = p.part + (size_t)tile * p.splits * (kBM * BN) + (size_t)c_lo * kBM;
+                    for (int s2 = 0; s2 < p.splits; ++s2)
+                        bulk_load_g2s(red + (size_t)s2 * (c_hi - c_lo) * kBM, src + (size_t)s2 * (kBM * BN), bytes,
+                                      last_full);
+                }
+                mbar_wait(last_full, 0);
+                reduce_share<BN>(p, tile, red, c_lo, c_hi, warp & 3, lane);
+                continue;
+            }
+            const int ti_e = (wi - unit) / nunits;
             if (p.trace && warp == 4 && lane == 0 && ti_e < 8) p.trace[(size_t)blockIdx.x * 64 + 40 + 2 * ti_e] = globaltimer_ns();
             // the CTA's last tile is split: warps 0-3 store columns [BN/2, BN)
-            const bool last = kSplitLast && tile + nunits >= p.num_tiles;
+            const bool last = kSplitLast && wi + nunits >= p.num_work;
             store_accumulator<BN, CG>(p, tmem_base, tile, acc, rank, warp & 3, lane, 0, last ? BN / 2 : BN);
             tc_fence_before();
             __syncwarp();
@@ -821,9 +923,9 @@ struct TcMaps {
     CUtensorMap a, b, src, dst;   // src/dst only with fuse (copies of a/b otherwise)
 };
 
-template <int BN, bool BF16, int CG, int KSTEPS>
+template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT>
 static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
-    auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS>;
+    auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS, SPLIT>;
     // Opt in to the largest dynamic smem once per instantiation (per process).
     static std::atomic<int> smem_set{0};
     if (smem_set.load(std::memory_order_acquire) < (int)smem) {
@@ -859,12 +961,23 @@ static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, 
 
 template <bool BF16, int CG, int KSTEPS>
 static cudaError_t launch_tc_bn(int bn, const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
+    if (prm.splits > 1) {          // split-K kernels: CG = 1, BN <= 128 only (tc_split_ok)
+        if constexpr (CG == 1) {
+            switch (bn) {
+                case 32: return launch_tc<32, BF16, 1, KSTEPS, true>(m, prm, smem, grid, st);
+                case 64: return launch_tc<64, BF16, 1, KSTEPS, true>(m, prm, smem, grid, st);
+                case 128: return launch_tc<128, BF16, 1, KSTEPS, true>(m, prm, smem, grid, st);
+                default: break;
+            }
+        }
+        return cudaErrorInvalidValue;
+    }
     switch (bn) {
-        case 32: return launch_tc<32, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
-        case 64: return launch_tc<64, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
-        case 128: return launch_tc<128, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
-        case 192: return launch_tc<192, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
-        case 256: return launch_tc<256, BF16, CG, KSTEPS>(m, prm, smem, grid, st);
+        case 32: return launch_tc<32, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
+        case 64: return launch_tc<64, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
+        case 128: return launch_tc<128, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
+        case 192: return launch_tc<192, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
+        case 256: return launch_tc<256, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -952,6 +1065,32 @@ static cudaError_t encode_maps(const Problem& pb, const TcLayout& L, const TcTil
     return cudaSuccess;
 }
 
+int tc_split_kper(const Problem& pb, const TcLayout& L, const TcTile& t) {
+    const int k_iters = pb.R * pb.S * L.n_cblk;
+    if (t.splits <= 1) return k_iters;
+    const int stages = k_iters / t.kbs;
+    const int per = (stages + t.splits - 1) / t.splits;       // stages per split
+    if ((t.splits - 1) * per >= stages) return 0;             // the last split would be empty
+    return per * t.kbs;
+}
+
+size_t tc_split_bytes(const Problem& pb, const TcLayout& L, const TcTile& t) {
+    (void)L;
+    if (t.splits <= 1) return 0;
+    const int64_t tiles = ((pb.M() + 127) / 128) * ((pb.K + t.bn - 1) / t.bn);
+    const size_t ctr = ((size_t)tiles * sizeof(int) + 255) / 256 * 256;
+    return ctr + (size_t)tiles * t.splits * 128 * t.bn * sizeof(float);
+}
+
+bool tc_split_ok(const Problem& pb, const TcLayout& L, const TcTile& t) {
+    if (t.splits <= 1) return true;
+    if (t.fuse || t.cg != 1 || t.bn > 128 || t.splits > 16 || tc_split_kper(pb, L, t) == 0) return false;
+    // the reduction stages `splits` column shares of <= ceil(BN/splits) columns
+    // x 128 rows fp32 in the (then idle) pipeline shared memory
+    const size_t share = (size_t)((t.bn + t.splits - 1) / t.splits) * 128 * 4;
+    return (size_t)t.splits * share <= tc_pipe_bytes(L, t);
+}
+
 cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool bf16,
                    const float* in, const float* ker, float* out, void* in_ws, void* ker_ws, void* flag_ws,
                    cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err) {
@@ -1014,6 +1153,18 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     const int tile_m = kBM * t.cg;
     const int num_m_tiles = (int)((pb.M() + tile_m - 1) / tile_m);
     prm.num_tiles = num_m_tiles * prm.num_n_tiles;
+    prm.splits = t.splits > 1 ? t.splits : 1;
+    prm.kper = tc_split_kper(pb, L, t);
+    prm.num_work = prm.num_tiles * prm.splits;
+    if (prm.splits > 1) {
+        if (!tc_split_ok(pb, L, t) || !flag_ws || prm.num_work > num_sms) {
+            err = "split-K needs fuse=0, cg=1, bn<=128, a split workspace, non-empty stage-aligned splits and one wave";
+            return cudaErrorInvalidValue;
+        }
+        prm.tile_ctr = static_cast<int*>(flag_ws);
+        prm.part = reinterpret_cast<float*>(static_cast<uint8_t*>(flag_ws) +
+                                            ((size_t)prm.num_tiles * sizeof(int) + 255) / 256 * 256);
+    }
 
     prm.stages = t.stages;
     prm.kbs = t.kbs;
@@ -1021,7 +1172,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     prm.a_stage_bytes = (uint32_t)(t.kbs * kBM * L.sw);
     prm.b_stage_bytes = (uint32_t)(t.kbs * (t.bn / t.cg) * L.sw);
     const int units = num_sms / t.cg;
-    const int grid = (prm.num_tiles < units ? prm.num_tiles : units) * t.cg;
+    const int grid = (prm.num_work < units ? prm.num_work : units) * t.cg;
     const size_t smem = tc_smem_bytes(L, t);
     prm.fuse = t.fuse;
     if (t.fuse) {
@@ -1076,6 +1227,9 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         fz.pre_q = pre_c > 0 ? prm.gend[0] : 0;
         fz.pre_ch = pre_c / L.cc;
         prm.seq0 = (pre_c / L.bkc) * prm.gend[0] * L.hh;
+    } else if (prm.splits > 1) {
+        fz.zero_ptr = prm.tile_ctr;               // the repack launch clears the arrival counters
+        fz.zero_n = prm.num_tiles;
     }
     e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse, fz);
     if (e != cudaSuccess) { err = "repack launch failed"; return e; }

@@ -134,7 +134,7 @@ def test_p10_tile_invariance_tensor(path):
     for cg in (1, 2):
         for bn, kbs, fuse in ((32, 1, 0), (64, 2, 1), (128, 4, 0), (192, 1, 1), (256, 2, 1), (64, 3, 0), (128, 6, 1)):
             try:
-                got, plan = run(sh, inp, ker, path, tile=f"bn={bn},cg={cg},kbs={kbs},fuse={fuse}")
+                got, plan = run(sh, inp, ker, path, tile=f"bn={bn},cg={cg},kbs={kbs},fuse={fuse},splits=1")
             except conv.ConvError as e:           # e.g. kbs=4 stages do not fit smem
                 assert e.status == conv.CONV_ERR_INFEASIBLE
                 continue
@@ -143,6 +143,69 @@ def test_p10_tile_invariance_tensor(path):
             outs.append(got)
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+# ---- split-K (small-M layers: the k loop of a few tiles over idle SMs) ------
+SPLITK = [
+    # (shape, splits): long k loops with few tiles, ragged K / M, uneven split ranges
+    (Shape(N=1, K=512, C=512, H=7, W=7, R=3, S=3), 8),        # Table-1 R12-like
+    (Shape(N=1, K=100, C=300, H=9, W=11, R=3, S=3), 5),       # ragged K and C; 45 stages over 5
+    (Shape(N=2, K=64, C=448, H=10, W=10, R=1, S=1), 3),       # 1x1; 7 (bf16) / 14 (tf32) stages over 3
+    (Shape(N=1, K=256, C=1024, H=5, W=5, R=3, S=3), 16),      # M9-like, 16 splits
+]
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+@pytest.mark.parametrize("case", range(len(SPLITK)))
+def test_splitk_parity(path, case):
+    """Split-K against the oracle (1e-5 on the path's rounded inputs, TOL on
+    real ones), bit-exact on the integer twin, deterministic run to run."""
+    sh, sp = SPLITK[case]
+    inp, ker = make_inputs(sh, seed=101 + case)
+    got, plan = run(sh, inp, ker, path, tile=f"splits={sp}")
+    assert plan.describe()["tile"]["splits"] == sp
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert rel_l2(got, ref) <= TOL[path]
+    assert rel_l2(got, oracle.conv_eq1(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()))) <= 1e-5
+    again, _ = run(sh, inp, ker, path, tile=f"splits={sp}")
+    assert np.array_equal(got, again)
+    xi, wi = make_inputs(sh, seed=111 + case, kind="int")
+    goti, _ = run(sh, xi, wi, path, tile=f"splits={sp}")
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_splitk_fixed_split_tile_invariance_and_graph_replay(path):
+    """P10 for a fixed split count: BN and kbs do not change the bits
+    (each split's k range and the split-order sum are tiling-independent
+    when the stage-aligned ranges coincide: kbs = 1 vs 3 with 72 = 8 x 9
+    k-blocks); and a captured graph replays correctly (the arrival counters
+    are re-zeroed by every launch)."""
+    sh = Shape(N=1, K=256, C=512, H=7, W=7, R=3, S=3)   # 9 taps x 8 c-blocks (bf16) = 72 k-iterations
+    inp, ker = make_inputs(sh, seed=121)
+    ref, _ = run(sh, inp, ker, path, tile="splits=8,bn=32,cg=1,kbs=1")
+    for spec in ("splits=8,bn=64,cg=1,kbs=3", "splits=8,bn=128,cg=1,kbs=1", "splits=8,bn=128,cg=1,kbs=3"):
+        got, _ = run(sh, inp, ker, path, tile=spec)
+        assert np.array_equal(got, ref), spec
+    plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile="splits=8")
+    i, k = inp.cuda(), ker.cuda()
+    out, ws = plan.new_output(), plan.new_workspace()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.run(i, k, out, ws)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.run(i, k, out, ws, stream=s)
+    for seed in (122, 123, 124):
+        inp2, ker2 = make_inputs(sh, seed=seed)
+        i.copy_(inp2)
+        k.copy_(ker2)
+        g.replay()
+        torch.cuda.synchronize()
+        r2 = oracle.conv_eq1(ROUND[path](inp2.numpy()), ROUND[path](ker2.numpy()))
+        assert rel_l2(out.cpu().numpy(), r2) <= 1e-5
 
 
 def test_p10_tile_invariance_simt():
@@ -158,15 +221,16 @@ def test_p10_tile_invariance_simt():
 
 @pytest.mark.parametrize("path", PATHS)
 def test_p10_batch_shards_bit_identical(path):
-    """Shards over n equal the slices of the full result."""
+    """Shards over n equal the slices of the full result
+    (plans without split-K: P10 holds for a fixed split count)."""
     sh = Shape(N=8, K=64, C=32, H=14, W=14, R=3, S=3)
     inp, ker = make_inputs(sh, seed=9)
-    full, _ = run(sh, inp, ker, path)
+    full, _ = run(sh, inp, ker, path, tile="splits=1")
     for p in (2, 4):
         step = sh.N // p
         for r in range(p):
             sub = Shape(N=step, K=sh.K, C=sh.C, H=sh.H, W=sh.W, R=sh.R, S=sh.S)
-            got, _ = run(sub, inp[r * step:(r + 1) * step].contiguous(), ker, path)
+            got, _ = run(sub, inp[r * step:(r + 1) * step].contiguous(), ker, path, tile="splits=1")
             assert np.array_equal(got, full[r * step:(r + 1) * step])
 
 
@@ -293,7 +357,7 @@ def test_fused_transform_bit_identical_to_separate(path, shape):
     for cg in (1, 2):
         fused = conv.ConvPlan(*shape.as_tuple(), path=path, tile=f"cg={cg},fuse=1")
         assert fused.describe()["tile"]["fuse"] == 1
-        sep = conv.ConvPlan(*shape.as_tuple(), path=path, tile=f"cg={cg},fuse=0")
+        sep = conv.ConvPlan(*shape.as_tuple(), path=path, tile=f"cg={cg},fuse=0,splits=1")
         out = fused.new_output()
         ws = fused.new_workspace()
         for seed in (21, 22, 23):
@@ -316,7 +380,7 @@ def test_fused_transform_prologue_depths(path, pre_c):
     sh = Shape(N=160, K=64, C=256, H=14, W=14, R=3, S=3)
     inp, ker = make_inputs(sh, seed=41)
     i, k = inp.cuda(), ker.cuda()
-    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1").run(i, k)
+    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1,splits=1").run(i, k)
     for cg in (1, 2):
         plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile=f"fuse=1,cg={cg},pre_c={pre_c}")
         d = plan.describe()["tile"]
@@ -392,8 +456,8 @@ def test_strided_fused_and_cta_groups_bit_identical(path):
     sh = Shape.strided(160, 128, 64, 28, 28, 3, 3, 2)
     inp, ker = make_inputs(sh, seed=63)
     i, k = inp.cuda(), ker.cuda()
-    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1", **sh.plan_kwargs()).run(i, k)
-    for spec in ("fuse=0,cg=2", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0"):
+    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1,splits=1", **sh.plan_kwargs()).run(i, k)
+    for spec in ("fuse=0,cg=2,splits=1", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0"):
         out = conv.ConvPlan(*sh.as_tuple(), path=path, tile=spec, **sh.plan_kwargs()).run(i, k)
         torch.cuda.synchronize()
         assert torch.equal(out, ref), spec
@@ -440,8 +504,8 @@ def test_dilated_fused_and_cta_groups_bit_identical(path):
     sh = Shape.strided(96, 128, 64, 32, 32, 3, 3, 1, 2)
     inp, ker = make_inputs(sh, seed=83)
     i, k = inp.cuda(), ker.cuda()
-    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1", **sh.plan_kwargs()).run(i, k)
-    for spec in ("fuse=0,cg=2", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0", "fuse=1,cg=2,bn=64"):
+    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1,splits=1", **sh.plan_kwargs()).run(i, k)
+    for spec in ("fuse=0,cg=2,splits=1", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0", "fuse=1,cg=2,bn=64"):
         out = conv.ConvPlan(*sh.as_tuple(), path=path, tile=spec, **sh.plan_kwargs()).run(i, k)
         torch.cuda.synchronize()
         assert torch.equal(out, ref), spec
@@ -499,8 +563,8 @@ def test_padded_fused_and_cta_groups_bit_identical(path):
     sh = Shape.strided(96, 128, 64, 32, 32, 3, 3, 1, 1, 1, 1)
     inp, ker = make_inputs(sh, seed=93)
     i, k = inp.cuda(), ker.cuda()
-    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1", **sh.plan_kwargs()).run(i, k)
-    for spec in ("fuse=0,cg=2", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0", "fuse=1,cg=2,bn=64"):
+    ref = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,cg=1,splits=1", **sh.plan_kwargs()).run(i, k)
+    for spec in ("fuse=0,cg=2,splits=1", "fuse=1,cg=1", "fuse=1,cg=2", "fuse=1,cg=2,pre_c=0", "fuse=1,cg=2,bn=64"):
         out = conv.ConvPlan(*sh.as_tuple(), path=path, tile=spec, **sh.plan_kwargs()).run(i, k)
         torch.cuda.synchronize()
         assert torch.equal(out, ref), spec
@@ -570,7 +634,7 @@ def test_run_host_fused_chunks_bit_identical(path):
     plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=1")
     assert plan.describe()["tile"]["fuse"] == 1
     dev_out = plan.run(inp.cuda(), ker.cuda())
-    sep = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0").run(inp.cuda(), ker.cuda())
+    sep = conv.ConvPlan(*sh.as_tuple(), path=path, tile="fuse=0,splits=1").run(inp.cuda(), ker.cuda())
     torch.cuda.synchronize()
     assert torch.equal(dev_out, sep)
     dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device="cuda")
@@ -598,7 +662,7 @@ def test_fused_edge_shapes_and_graph_replay(path, shape):
     assert coop_ok(Shape(shape.N, shape.K, shape.C, shape.Hin - shape.R + 1, shape.Win - shape.S + 1, shape.R, shape.S))
     kw = shape.plan_kwargs()
     plan = conv.ConvPlan(*shape.as_tuple(), path=path, tile="fuse=1", **kw)
-    sep = conv.ConvPlan(*shape.as_tuple(), path=path, tile="fuse=0", **kw)
+    sep = conv.ConvPlan(*shape.as_tuple(), path=path, tile="fuse=0,splits=1", **kw)
     inp, ker = make_inputs(shape, seed=82)
     i, k = inp.cuda(), ker.cuda()
     out, ws = plan.new_output(), plan.new_workspace()
@@ -631,11 +695,11 @@ def test_p10_k_shards_and_strided_shards_bit_identical(path):
     for sh, dim, worlds in ((Shape(N=1, K=256, C=64, H=28, W=28, R=3, S=3), "k", (2, 4)),
                             (Shape.strided(8, 64, 32, 29, 29, 3, 3, 2), "n", (2, 4))):
         inp, ker = make_inputs(sh, seed=95)
-        full, _ = run(sh, inp, ker, path)
+        full, _ = run(sh, inp, ker, path, tile="splits=1")
         for world in worlds:
             for r in range(world):
                 spec = shard(sh, world, r, dim=dim)
                 li, lk = local_inputs(spec, inp, ker)
-                got, _ = run(spec.local, li, lk, path)
+                got, _ = run(spec.local, li, lk, path, tile="splits=1")
                 ref = full[spec.start:spec.stop] if dim == "n" else full[:, spec.start:spec.stop]
                 assert np.array_equal(got, ref), (dim, world, r)
