@@ -63,6 +63,7 @@ struct Elem<true> {
 //                            stores of 8 bf16 / 4 fp32 consecutive channels.
 struct RepackGeom {
     int C, Cp, RS, cc, ker_chunks;   // K1
+    int K, krows;                    // K1: output channels; Ker rows per CTA (> 1 only if ker_chunks == 1)
     int64_t P;                       // K2: pixels per image
     int ptiles, ctiles;              // K2 tile grid per image
     int n_ker;                       // number of K1 CTAs
@@ -77,6 +78,45 @@ struct RepackGeom {
     int cc_f;                        // fused: channels per chunk (flag column granularity)
 };
 
+// K1 for many short rows (whole rows fit, K >= 4 CTAs per SM): Ker rows
+// [k0, k0 + krows) of one CTA are one contiguous KCRS slab of krows * C * RS
+// fp32, staged in shared memory and written row by row as [RS][Cp]
+// (channels >= C zero).  A separate function so that the common one-row
+// path stays the short code path it was (its instructions are fetched cold
+// after every L2 flush).
+template <bool BF16, int NT>
+__device__ __noinline__ void ker_repack_rows(const float* __restrict__ ker, typename Elem<BF16>::T* __restrict__ ker_ws,
+                                             const RepackGeom g, float* sm) {
+    const int tid = threadIdx.x;
+    const int64_t k0 = (int64_t)blockIdx.x * g.krows;
+    const int nrows = (int)min((int64_t)g.krows, g.K - k0);
+    const int row_f = g.C * g.RS;                       // staged floats per row
+    const float* src = ker + k0 * row_f;
+    const int nld = nrows * row_f;
+    for (int i = tid; i < nld; i += NT) {
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sm + i));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + i) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // (row, tap) output rows of Cp channels; bf16 pairs packed (Cp even)
+    const int width = g.Cp;
+    for (int rr = 0; rr < nrows * g.RS; ++rr) {
+        const int r = rr / g.RS, rs = rr - r * g.RS;
+        const float* sr = sm + r * row_f + rs;
+        typename Elem<BF16>::T* d = ker_ws + ((k0 + r) * g.RS + rs) * (int64_t)g.Cp;
+        if (BF16) {
+            uint32_t* d2 = reinterpret_cast<uint32_t*>(d);
+            for (int c2 = tid; c2 < (width >> 1); c2 += NT) {
+                const int c = 2 * c2;
+                d2[c2] = pack2_bf16(c < g.C ? sr[c * g.RS] : 0.0f, c + 1 < g.C ? sr[(c + 1) * g.RS] : 0.0f);
+            }
+        } else {
+            for (int c = tid; c < width; c += NT) d[c] = Elem<BF16>::cvt(c < g.C ? sr[c * g.RS] : 0.0f);
+        }
+    }
+}
+
 // K1, one CTA (NT threads): Ker row k = blockIdx.x / ker_chunks, channels
 // [c0, c0 + cc): stage the contiguous KCRS slice (cload * RS fp32) in shared
 // memory, then write it as [RS][Cp] (channels >= C zero), converted.
@@ -84,6 +124,10 @@ template <bool BF16, int NT>
 __device__ __forceinline__ void ker_repack_cta(const float* __restrict__ ker, typename Elem<BF16>::T* __restrict__ ker_ws,
                                                const RepackGeom& g, float* sm) {
     const int tid = threadIdx.x;
+    if (g.krows > 1) {
+        ker_repack_rows<BF16, NT>(ker, ker_ws, g, sm);
+        return;
+    }
     const int64_t k = blockIdx.x / g.ker_chunks;
     const int c0 = (blockIdx.x % g.ker_chunks) * g.cc;
     const int c1 = min(c0 + g.cc, g.Cp);
@@ -361,7 +405,22 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
     g.cc = std::max(1, std::min(Cp, (int)(32768 / (4 * g.RS))));
     if (g.cc > 1) g.cc &= ~1;   // even: bf16 channel pairs share a 4-B store
     g.ker_chunks = (Cp + g.cc - 1) / g.cc;
-    g.n_ker = pb.K * g.ker_chunks;
+    g.K = pb.K;
+    // whole rows fit and there are many of them: several consecutive
+    // (contiguous) rows per CTA, so that short rows (1x1 kernels: one 4-KB
+    // row of C = 1024, K = 28269) do not make tens of thousands of tiny CTAs
+    // -- but never fewer than ~4 CTAs per SM (a few long CTAs serialise:
+    // measured 9 -> 23-32 us on the 128-row and 3-channel Table-1 layers)
+    static int dev_sms = [] {
+        int n = 148, d = 0;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+        return n;
+    }();
+    g.krows = g.ker_chunks == 1
+                  ? std::max(1, std::min(8192 / std::max(1, pb.C * g.RS), pb.K / (4 * dev_sms)))
+                  : 1;
+    g.n_ker = ((pb.K + g.krows - 1) / g.krows) * g.ker_chunks;
     g.P = pb.Hin() * pb.Win();
     g.ptiles = (int)((g.P + 63) / 64);
     g.ctiles = (Cp + 63) / 64;
@@ -429,7 +488,8 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         g.pdl_from = (int)std::max<int64_t>(0, grid - (int64_t)sms * 8);   // ~ the last resident wave
     }
-    const size_t smem = std::max<size_t>(64 * 65 * sizeof(float), (size_t)g.cc * g.RS * sizeof(float));
+    const size_t smem = std::max<size_t>(64 * 65 * sizeof(float),
+                                         (g.krows > 1 ? (size_t)g.krows * g.C : (size_t)g.cc) * g.RS * sizeof(float));
     if (smem > 48 * 1024) {   // very large R*S: one channel per K1 CTA still needs > 48 KB
         cudaError_t e = bf16 ? cudaFuncSetAttribute(repack_all<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                              : cudaFuncSetAttribute(repack_all<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
