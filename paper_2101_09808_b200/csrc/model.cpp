@@ -245,15 +245,19 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
         // share the SM's shared-memory port, L2 and issue slots).  While the
         // transform has not caught up, wave 0 waits: the part of its input
         // beyond the prologue must be converted before its last channel
-        // block can run.  Single-wave layers also pay the chunk pipeline's
-        // startup chain (decode, load, convert, store, publish, watch).
+        // block can run.  Every fused plan also pays the chunk pipeline's
+        // startup chain (decode, load, convert, store, publish, watch):
+        // charged to single-wave layers only, the model picked the fused
+        // transform for the large-M batch-1 Table-1 layers Y0/Y2/Y5, where it
+        // measured 2-8 us slower than the separate repack (r01b
+        // profiles/r01b/selector_fuse.jsonl); only the batched layer gains.
         const double in_rd = 4.0 * pb.in_elems();
         const double waves = ceil((double)r.tiles / units);
         const double pre_frac = std::min(1.0, (double)t.pre_c / L.Cp) / std::max(1.0, waves);
         const double t_tr = in_rd * (1.0 - pre_frac) / kTransformBW * 1e6;
         const double wave0_in = in_rd / std::max(1.0, waves) * (1.0 - std::min(1.0, (double)t.pre_c / L.Cp));
         const double stall0 = std::max(0.0, wave0_in / kTransformBW * 1e6 - t_pipe_us / std::max(1.0, waves));
-        t_main_f = std::max(t_main * kTransformDrag, t_tr) + stall0 + (waves < 2 ? kTransformStartUs : 0.0);
+        t_main_f = std::max(t_main * kTransformDrag, t_tr) + stall0 + kTransformStartUs;
         const double pre_bytes = (4.0 + L.elem) * pb.in_elems() * pre_frac;
         t_rep = (4.0 * pb.ker_elems() + (double)L.ker_ws_bytes + pre_bytes) / (0.8 * dev.bw_hbm) * 1e6 + 2 * kLaunchUs;
         r.dv_hbm = in_rd + (double)L.in_ws_bytes + 4.0 * pb.ker_elems() + 2.0 * (double)L.ker_ws_bytes + 4.0 * pb.out_elems();
