@@ -316,6 +316,9 @@ def bench_ours(args):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": round(ms, 5),
+            # rank 0's K timed steps: the paper's statistic is the mean;
+            # median and a normal 95% CI of the mean beside it
+            "step_stats": step_stats(step_ms),
             "higher_is_better": True,
             "scaling": "weak" if (args.scaling == "weak" or world == 1) else "strong",
             "vs_baseline": None,
@@ -379,6 +382,26 @@ def oracle_sample_time(sh: Shape, n_img: int, threads: int):
     return time.perf_counter() - t0
 
 
+def step_stats(step_ms) -> dict:
+    x = np.asarray(step_ms, dtype=np.float64)
+    mean = float(x.mean())
+    half = float(1.96 * x.std(ddof=1) / np.sqrt(len(x))) if len(x) > 1 else 0.0
+    return {"mean_ms": round(mean, 5), "median_ms": round(float(np.median(x)), 5),
+            "ci95_ms": [round(mean - half, 5), round(mean + half, 5)],
+            "min_ms": round(float(x.min()), 5), "max_ms": round(float(x.max()), 5)}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(sh: Shape, args, target_s: float = 10.0):
     """The oracle as it stands, on the host cores, on a bounded sample of the
     workload (the first n images of the batch, sized for ~target_s)."""
@@ -390,6 +413,7 @@ def cpu_baseline(sh: Shape, args, target_s: float = 10.0):
     t = oracle_sample_time(sh, n, threads) if n > 1 else t1
     flops = 2.0 * n * sh.K * sh.H * sh.W * sh.C * sh.R * sh.S
     return {"value": round(flops / t / 1e12, 6), "unit": "TFLOP/s", "cores": used, "kind": "oracle",
+            "cpu": cpu_model(),
             "sample": f"first {n} of {sh.N} images of the {args.config} layer ({t:.1f} s, double accumulation, "
                       f"OpenMP over (n,k) planes)"}
 
@@ -421,7 +445,8 @@ def bench_reference(args):
                    "sample_images_per_step": n},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": used, "kind": "oracle",
-                         "sample": f"first {n} of {sh.N} images per step"},
+                         "cpu": cpu_model(), "sample": f"first {n} of {sh.N} images per step"},
+        "step_stats": step_stats(np.asarray(ts) * 1e3),
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
