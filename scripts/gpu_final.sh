@@ -13,3 +13,7 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 CMD="python bench.py --steps 2 --warmup 3 --soak 0 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_default.csv $CMD > gpurun_out/ncu_list.log 2>&1; echo "ncu list rc=$?"
 timeout 900 python bench.py --sweep table1 --path all --steps 20 --warmup 3 > gpurun_out/table1.jsonl 2> gpurun_out/table1.err; echo "sweep rc=$?"
+# one full ncu capture of the headline main kernel per tensor path (roofline traffic, profiles/)
+for p in bf16 tf32; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_igemm -c 1 -o gpurun_out/main_full_$p -f python scripts/run_layer.py batched $p > gpurun_out/ncu_full_$p.log 2>&1; echo "ncu full $p rc=$?"
+done
