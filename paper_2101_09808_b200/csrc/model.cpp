@@ -371,6 +371,12 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
 }
 
 // ---- SIMT -------------------------------------------------------------------
+// Issue cost per element of the v2 per-row 4-B copy loop (taken when the
+// 16-B copy plan does not fit 4 units per thread).  r01b: 24 from the batched
+// layer (~2.3x slower layer); the Table-1 study (simt_study2: Y18 bc 4 -> 8
+// crossed into it, 2.78 -> 8.07 us per chunk) measured ~3x more.
+static const double kSimtSlowCopy = 72.0;
+
 ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) {
     ModelResult r;
     const int bko = t.kg * t.tk;
@@ -426,7 +432,7 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // beyond that a per-row loop of 4-B copies runs (~2.3x slower layer
     // measured r01b)
     const double units_v2 = (double)t.bc * t.tn * pb.rows_span(t.th) * (pb.Win() % 4 == 0 ? pb.Win() / 4.0 : pb.Win());
-    const double copy_unit = (t.ver == 2 && units_v2 > 4.0 * threads) ? 6.0 * 4.0 : 6.0;
+    const double copy_unit = (t.ver == 2 && units_v2 > 4.0 * threads) ? kSimtSlowCopy : 6.0;
     const double copy_chunk_cta = in_elems_chunk * copy_unit + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
     // a chunk cannot take less than one L2 round trip + two barriers
@@ -453,6 +459,12 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     for (int ver = 1; ver <= 2; ++ver) {
     if (ver == 2 && !simt_v2_ok(pb)) continue;
     if (forced && (forced_mask & 128) && ver != forced->ver) continue;
+    // v1 only where v2 cannot run (S not in {1, 3}, stride, dilation,
+    // padding) unless forced: on every layer measured where both run, the
+    // best v2 tile beat the best v1 tile (r01b profiles/r01b/simt_study2.jsonl:
+    // Y19 139 vs 450 us, Y13 74 vs 256, Y18 356 vs 430), while the model
+    // ranked v1 first on the 1x1 layers (modeled 69 us, measured 471)
+    if (ver == 1 && simt_v2_ok(pb) && !(forced && (forced_mask & 128))) continue;
     for (int tk : tks)
     for (int tw = 1; tw <= 14; ++tw)
     for (int kg : kgs)

@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <atomic>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace conv {
@@ -38,8 +40,9 @@ static cudaError_t launch_pdl(Kern kfn, dim3 grid, int threads, size_t smem, cud
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
+    static const int no_pdl = getenv("CONV_NO_PDL") ? 1 : 0;   // experiments
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kfn, args...);
@@ -77,7 +80,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Packing kernel: Ker KCRS -> [ceil(K/bko)][C][R][S][bko], k >= K zero.
 __global__ void __launch_bounds__(256) pack_ker_simt(const float* __restrict__ ker, float* __restrict__ out,
                                                      int K, int C, int RS, int bko, int64_t total) {
-    asm volatile("griddepcontrol.launch_dependents;");   // small grid: one wave
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int kk = (int)(i % bko);
@@ -89,6 +91,11 @@ __global__ void __launch_bounds__(256) pack_ker_simt(const float* __restrict__ k
         const int64_t k = kb * bko + kk;
         out[i] = k < K ? __ldg(ker + (k * C + c) * RS + rs) : 0.0f;
     }
+    // Trigger the dependent SIMT launch only at the end of each CTA: triggered
+    // at the start, the (small) SIMT grid was placed while this grid still
+    // held most SMs and piled onto the few with room -- measured 2-3x slower
+    // on the small Table-1 layers (R2 92 vs 33 us, M6 612 vs 199 us).
+    asm volatile("griddepcontrol.launch_dependents;");
 }
 
 template <int TK, int TW>

@@ -1,5 +1,5 @@
 """SIMT tile study under the bench protocol (CUDA-graph replay, L2 flushed before every step):
-every v2 candidate tile (tk, tw, kg, tn, bc) of a layer, modeled vs measured (selector
+every v2 candidate tile (tk, tw, kg, tn, bc) and v1 candidate (tk, tw, kg, bc) of a layer, modeled vs measured (selector
 calibration for the latency-bound small layers).  Product code only."""
 import itertools, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -15,8 +15,12 @@ for name in sys.argv[1].split(","):
     inp, ker = make_inputs(sh); i, k = inp.cuda(), ker.cuda()
     auto = conv.ConvPlan(*sh.as_tuple(), path="fp32_simt", **sh.plan_kwargs()).describe()["tile"]
     rows = []
-    for tk, tw, kg, tn, bc in itertools.product((4, 8), (4, 8, sh.W), (1, 2, 4, 8), (1, 2, 4), (4, 8, 16)):
-        spec = f"ver=2,tk={tk},tw={tw},kg={kg},tn={tn},bc={bc}"
+    specs = [f"ver=2,tk={tk},tw={tw},kg={kg},tn={tn},bc={bc}"
+             for tk, tw, kg, tn, bc in itertools.product((4, 8), (4, 8, sh.W), (1, 2, 4, 8), (1, 2, 4), (4, 8, 16))]
+    # v1 (any R, S, stride): the selector fills th / pw / tn
+    specs += [f"ver=1,tk={tk},tw={tw},kg={kg},bc={bc}"
+              for tk, tw, kg, bc in itertools.product((4, 8), (1, 2, 4), (1, 2, 4, 8), (4, 8, 16, 32))]
+    for spec in specs:
         try:
             p = conv.ConvPlan(*sh.as_tuple(), path="fp32_simt", tile=spec, **sh.plan_kwargs())
         except conv.ConvError:
