@@ -603,6 +603,28 @@ def test_table1_layers_same_padded(path):
             assert rel_l2(val, ref) <= 2 * TOL[path], name
 
 
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+@pytest.mark.parametrize("splits", [1, 3, 8])
+def test_general_conv_with_split_k(path, splits):
+    """Stride, dilation, asymmetric zero padding and split-K together: a
+    deep-C, small-output layer (the split-K regime) against the padded
+    oracle; bit-exact on the integer twin; deterministic run to run."""
+    sh = Shape.strided(1, 96, 320, 19, 17, 3, 3, 2, 2, 2, 1)
+    spec = f"splits={splits}"
+    inp, ker = make_inputs(sh, seed=131)
+    got, plan = run(sh, inp, ker, path, tile=spec)
+    assert plan.describe()["tile"]["splits"] == splits
+    pad = (sh.ph, sh.pw)
+    ref = oracle.conv_eq1_padded(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), sh.U, sh.D, pad)
+    assert got.shape == ref.shape
+    assert rel_l2(got, ref) <= 1e-5
+    again, _ = run(sh, inp, ker, path, tile=spec)
+    assert np.array_equal(got, again)
+    xi, wi = make_inputs(sh, seed=132, kind="int")
+    goti, _ = run(sh, xi, wi, path, tile=spec)
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1_padded(xi.numpy(), wi.numpy(), sh.U, sh.D, pad))
+
+
 @pytest.mark.parametrize("path", PATHS)
 def test_table1_layers(path):
     """Every conv2d layer of PAPER.md:439 Table 1 (batch 1, stride 1/2, input
