@@ -456,7 +456,10 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     const int kgs[4] = {1, 2, 4, 8};
     const int bcs[3] = {4, 8, 16};
     const int tn_max = std::min(pb.N, 16);
-    for (int ver = 1; ver <= 2; ++ver) {
+    // v2 first when it can run and nothing is forced; v1 only if no v2 tile fits
+    const bool v2_first = simt_v2_ok(pb) && !(forced && forced_mask);
+    const int vers[2] = {v2_first ? 2 : 1, v2_first ? 1 : 2};
+    for (int ver : vers) {
     if (ver == 2 && !simt_v2_ok(pb)) continue;
     if (forced && (forced_mask & 128) && ver != forced->ver) continue;
     // v1 only where v2 cannot run (S not in {1, 3}, stride, dilation,
@@ -464,7 +467,8 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     // best v2 tile beat the best v1 tile (r01b profiles/r01b/simt_study2.jsonl:
     // Y19 139 vs 450 us, Y13 74 vs 256, Y18 356 vs 430), while the model
     // ranked v1 first on the 1x1 layers (modeled 69 us, measured 471)
-    if (ver == 1 && simt_v2_ok(pb) && !(forced && (forced_mask & 128))) continue;
+    // (automatic selection only: forced keys may name a v1-only tile)
+    if (ver == 1 && v2_first && found) continue;
     for (int tk : tks)
     for (int tw = 1; tw <= 14; ++tw)
     for (int kg : kgs)

@@ -90,9 +90,7 @@ struct TcParams {
     uint32_t sw;              // 32 / 64 / 128 (bytes per operand row per k-block)
     uint32_t a_stage_bytes;   // kbs * 128 * sw
     uint32_t b_stage_bytes;   // kbs * (bn / cg) * sw
-    uint32_t debug;           // experiments only (env CONV_DEBUG_MODE): 1 no MMA, 2 no TMA, 4 no stores
     unsigned long long* trace;  // experiments only (env CONV_TRACE): per-CTA timeline, 64 slots
-    int tap_outer;            // k order: 1 = (r, s, cb) [not with fuse], 0 = (cb, r, s)
     // ---- cooperative In transform (a-3 inside the main kernel, fuse = 1) ----
     int fuse;                 // 1: warps 0-3 of every CTA convert NCHW fp32 chunks into the NHWC workspace
     int* flags;               // [Q][nch] chunk-ready flags (zeroed by the Ker repack launch)
@@ -260,7 +258,7 @@ __device__ __forceinline__ void store_accumulator(const TcParams& p, uint32_t tm
         tmem_ld_32x32b_x32(t0 + (uint32_t)j0, v);
         tmem_ld_wait();
         const int kbase = k0 + j0;
-        if (valid_m && !(p.debug & 4)) {
+        if (valid_m) {
             if (kbase + 32 <= p.K) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
@@ -404,8 +402,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     if (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t wflavor = (p.debug >> 3) & 3;
-    const bool kSplitLast = !SPLIT && CONV_SPLIT_LAST && BN >= 64 && !(p.debug & 32);
+    const bool kSplitLast = !SPLIT && CONV_SPLIT_LAST && BN >= 64;
     // Programmatic dependent launch: everything above overlapped the tail of
     // the repack launch; from here on the repacked workspace (and, fused, the
     // zeroed chunk flags) is read and Out written, so wait for the preceding
@@ -439,13 +436,15 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 const int w0 = pix - h0 * p.W;
                 const int kb0 = n_tile * BN + (int)rank * (BN / CG);   // this CTA's B rows
                 const uint32_t a_blk = kBM * p.sw, b_blk = (BN / CG) * p.sw;
-                // k iterations in a fixed order -- (cb, r, s) or (r, s, cb) --
+                // k iterations in one fixed order -- (cb, r, s), s fastest --
                 // tracked by counters (no divisions); a stage holds kbs
-                // consecutive iterations, so the order does not depend on kbs.
+                // consecutive iterations, so the order does not depend on kbs
+                // (results bit-identical across tilings, P10).
                 int cb = 0, r = 0, s = 0;
                 if (SPLIT && it_beg) {                    // split-K: start mid-order
-                    if (p.tap_outer) { cb = it_beg % p.n_cblk; s = (it_beg / p.n_cblk) % p.S; r = it_beg / (p.n_cblk * p.S); }
-                    else { s = it_beg % p.S; r = (it_beg / p.S) % p.R; cb = it_beg / (p.S * p.R); }
+                    s = it_beg % p.S;
+                    r = (it_beg / p.S) % p.R;
+                    cb = it_beg / (p.S * p.R);
                 }
                 for (int it0 = it_beg; it0 < it_end; it0 += p.kbs) {
                     const int cb_s = cb, r_s = r, s_s = s;
@@ -453,11 +452,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     int cb_last = cb;
                     for (int kb = 0; kb < p.kbs; ++kb) {
                         cb_last = cb;
-                        if (p.tap_outer) {
-                            if (++cb == p.n_cblk) { cb = 0; if (++s == p.S) { s = 0; ++r; } }
-                        } else {
-                            if (++s == p.S) { s = 0; if (++r == p.R) { r = 0; ++cb; } }
-                        }
+                        if (++s == p.S) { s = 0; if (++r == p.R) { r = 0; ++cb; } }
                     }
                     if (p.fuse) {
                         // the watcher has confirmed (tile, channel block) units in
@@ -474,14 +469,12 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                         }
                     }
                     const long long pw0 = p.trace ? clock64() : 0;
-                    mbar_wait_flavor(&empty[stage], phase ^ 1, wflavor);
+                    mbar_wait(&empty[stage], phase ^ 1);
                     if (p.trace) prod_wait += clock64() - pw0;
                     uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
                     uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
                     if (elect_one_sync()) {
-                        if (p.debug & 2) {
-                            if (leader) mbar_arrive(&full[stage]);
-                        } else {
+                        {
                             if (leader) mbar_arrive_expect_tx(&full[stage], tx_bytes);
                             int c1 = cb_s, r1 = r_s, s1 = s_s;
                             for (int kb = 0; kb < p.kbs; ++kb) {
@@ -495,11 +488,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                                                        w0 * p.U - p.pw, h0 * p.U - p.ph, img, (uint16_t)(s1 * p.D), (uint16_t)(r1 * p.D), pol_a);
                                     tma_load_2d(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
                                 }
-                                if (p.tap_outer) {
-                                    if (++c1 == p.n_cblk) { c1 = 0; if (++s1 == p.S) { s1 = 0; ++r1; } }
-                                } else {
-                                    if (++s1 == p.S) { s1 = 0; if (++r1 == p.R) { r1 = 0; ++c1; } }
-                                }
+                                if (++s1 == p.S) { s1 = 0; if (++r1 == p.R) { r1 = 0; ++c1; } }
                             }
                         }
                     }
@@ -530,7 +519,6 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             const uint64_t b_desc0 = make_sdesc(smem_u32(smem_b), 8 * kSw, layout);
             const uint32_t a_step = p.a_stage_bytes >> 4, b_step = p.b_stage_bytes >> 4;
             constexpr uint32_t a_blk = (kBM * kSw) >> 4, b_blk = ((BN / CG) * kSw) >> 4;
-            const bool no_mma = (p.debug & 1) != 0;
             const int kbs = p.kbs;
 
             unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
@@ -540,7 +528,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 const int tile = SPLIT ? wi / p.splits : wi;
                 const int it_beg = SPLIT ? (wi - tile * p.splits) * p.kper : 0;
                 const int iters = SPLIT ? (min(p.k_iters, it_beg + p.kper) - it_beg) / kbs : p.k_iters / kbs;
-                mbar_wait_flavor(&tmem_empty[acc], acc_phase ^ 1, wflavor);
+                mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 if (tr && lane == 0 && ti < 8) tr[1 + 4 * ti] = globaltimer_ns();
                 long long wait_cyc = 0;
@@ -548,13 +536,13 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 uint32_t accum = 0;                      // first MMA of the tile overwrites D
                 for (int it = 0; it < iters; ++it) {
                     const long long w0 = tr ? clock64() : 0;
-                    mbar_wait_flavor(&full[stage], phase, wflavor);
+                    mbar_wait(&full[stage], phase);
                     if (tr) wait_cyc += clock64() - w0;
                     tc_fence_after();
                     if (elect_one_sync()) {
                         const uint64_t ad0 = a_desc0 + (uint64_t)(stage * a_step);
                         const uint64_t bd0 = b_desc0 + (uint64_t)(stage * b_step);
-                        if (!no_mma) {
+                        {
                             for (int kb = 0; kb < kbs; ++kb) {
 #pragma unroll
                                 for (int kk = 0; kk < KSTEPS; ++kk) {
@@ -1234,15 +1222,6 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse, fz);
     if (e != cudaSuccess) { err = "repack launch failed"; return e; }
 
-    static const uint32_t debug_mode = [] {
-        const char* e = getenv("CONV_DEBUG_MODE");
-        return e ? (uint32_t)atoi(e) : 0u;
-    }();
-    prm.debug = debug_mode;
-    static const int env_order = [] { const char* e = getenv("CONV_KORDER"); return e ? atoi(e) : -1; }();
-    // One order for every configuration (fused or not), so results are
-    // bit-identical across tilings (P10); env CONV_KORDER=1 is for experiments.
-    prm.tap_outer = t.fuse ? 0 : (env_order >= 0 ? env_order : 0);
     static const char* trace_path = getenv("CONV_TRACE");
     static unsigned long long* trace_buf = nullptr;
     prm.trace = nullptr;

@@ -35,5 +35,5 @@ for name in ("R6", "M7", "M9", "R12"):
         torch.cuda.synchronize()
         kern = [float(np.median([e[j].elapsed_time(e[j + 1]) for e in ev])) * 1e3 for j in range(nk)]
         print(json.dumps({"layer": name, "splits": sp, "tile": plan.describe()["tile"],
-                          "debug": os.environ.get("CONV_DEBUG_MODE", "0"), "kernels_us": [round(x, 2) for x in kern]}),
+                          "kernels_us": [round(x, 2) for x in kern]}),
               flush=True)
