@@ -38,7 +38,10 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
         nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-        cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *sources()]
+        # CONV_BUILD_TRACE=1: a trace build (kernel timeline instrumentation,
+        # env CONV_TRACE at run time; scripts/trace_tc.py) -- study only
+        extra = ["-DCONV_ENABLE_TRACE=1"] if os.environ.get("CONV_BUILD_TRACE") == "1" else []
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", *sources()]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

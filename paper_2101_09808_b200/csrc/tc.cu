@@ -57,6 +57,11 @@ static constexpr int kDecode = 16;          //   decoded per block, one block ah
 static constexpr int kMaxTnb = 6;           //   chunk buffers at most
 // The CTA's last tile is stored by 8 warps (4-7 and 0-3) when BN allows two
 // 32-column halves (CONV_DEBUG_MODE bit 32 disables it, experiments only).
+#ifndef CONV_ENABLE_TRACE
+#define CONV_ENABLE_TRACE 0   // build with CONV_BUILD_TRACE=1 (build.py) for scripts/trace_tc.py
+#endif
+static constexpr bool kTraceBuild = CONV_ENABLE_TRACE != 0;
+
 #ifndef CONV_SPLIT_LAST
 #define CONV_SPLIT_LAST 1
 #endif        // 12 warps: 4 In-transform, 4 epilogue, alloc, watcher, TMA, MMA
@@ -333,6 +338,10 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_dst,    // fuse: workspace NHWC {Cp, P, N}
                    const TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // timeline instrumentation (scripts/trace_tc.py) only in trace builds:
+    // in production builds it folds away (its clock reads and branches sat
+    // on the producer / MMA hot loops)
+    unsigned long long* const trace = kTraceBuild ? p.trace : nullptr;
     // 1024-B alignment for the 128-B swizzle atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;
@@ -465,12 +474,12 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                                 if (clock64() - t0 > 8000000000ll) __trap();
                             }
                             fence_proxy_async_global();   // flags observed -> TMA reads of the workspace
-                            if (p.trace) ready_wait += clock64() - t0;
+                            if (trace) ready_wait += clock64() - t0;
                         }
                     }
-                    const long long pw0 = p.trace ? clock64() : 0;
+                    const long long pw0 = trace ? clock64() : 0;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (p.trace) prod_wait += clock64() - pw0;
+                    if (trace) prod_wait += clock64() - pw0;
                     uint8_t* a_dst = smem_a + (size_t)stage * p.a_stage_bytes;
                     uint8_t* b_dst = smem_b + (size_t)stage * p.b_stage_bytes;
                     if (elect_one_sync()) {
@@ -496,10 +505,10 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
                 }
             }
-            if (p.trace && lane == 0) {
-                p.trace[(size_t)blockIdx.x * 64 + 60] = (unsigned long long)prod_wait;
-                p.trace[(size_t)blockIdx.x * 64 + 61] = globaltimer_ns();
-                p.trace[(size_t)blockIdx.x * 64 + 57] = (unsigned long long)ready_wait;
+            if (trace && lane == 0) {
+                trace[(size_t)blockIdx.x * 64 + 60] = (unsigned long long)prod_wait;
+                trace[(size_t)blockIdx.x * 64 + 61] = globaltimer_ns();
+                trace[(size_t)blockIdx.x * 64 + 57] = (unsigned long long)ready_wait;
             }
         }
     } else if (warp == 11) {
@@ -521,7 +530,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             constexpr uint32_t a_blk = (kBM * kSw) >> 4, b_blk = ((BN / CG) * kSw) >> 4;
             const int kbs = p.kbs;
 
-            unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
+            unsigned long long* tr = trace ? trace + (size_t)blockIdx.x * 64 : nullptr;
             int ti = 0;
             if (tr && lane == 0) tr[0] = globaltimer_ns();
             for (int wi = unit; wi < p.num_work; wi += nunits, ++ti) {
@@ -623,7 +632,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 if (pub < done) {
                     const int batch = min(32, done - pub);
                     if ((int)lane < batch) st_release_gpu(p.flags + cring[(pub + (int)lane) & (kRing - 1)].x, 1);
-                    if (p.trace && lane == 0 && pub == 0) p.trace[(size_t)(512 + blockIdx.x) * 64 + 2] = globaltimer_ns();
+                    if (trace && lane == 0 && pub == 0) trace[(size_t)(512 + blockIdx.x) * 64 + 2] = globaltimer_ns();
                     pub += batch;
                     __syncwarp();
                     if (lane == 0) st_release_cta_smem(pub_ctr, pub);
@@ -641,7 +650,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                         fence_proxy_async_global();       // -> the producer's TMA reads
                         ++u;
                         if (lane == 0) st_release_cta_smem(ready_ctr, u);
-                        if (p.trace && lane == 0 && u == 1) p.trace[(size_t)blockIdx.x * 64 + 56] = globaltimer_ns();
+                        if (trace && lane == 0 && u == 1) trace[(size_t)blockIdx.x * 64 + 56] = globaltimer_ns();
                         if (++cb == p.n_cblk) {
                             cb = 0;
                             tile += nunits;
@@ -651,12 +660,12 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     }
                 }
                 if (!progress) {
-                    const long long t0 = p.trace ? clock64() : 0;
+                    const long long t0 = trace ? clock64() : 0;
                     __nanosleep(128);
-                    if (p.trace) w_spin += clock64() - t0;
+                    if (trace) w_spin += clock64() - t0;
                 }
             }
-            if (p.trace && lane == 0) p.trace[(size_t)blockIdx.x * 64 + 39] = (unsigned long long)w_spin;
+            if (trace && lane == 0) trace[(size_t)blockIdx.x * 64 + 39] = (unsigned long long)w_spin;
         }
     } else if (warp == 8) {
         // ===== chunk loader / storer (fuse, lane 0): TMA-loads this CTA's
@@ -668,7 +677,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         if (p.fuse && lane == 0 && n_my > 0) {
             constexpr int kPubLag = 1, kReport = 2;   // completion checked + reported every kReport chunks
             const uint32_t buf_bytes = (uint32_t)p.cc * 256;
-            unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
+            unsigned long long* tr = trace ? trace + (size_t)blockIdx.x * 64 : nullptr;
             long long c_conv = 0, c_rd = 0, c_pub = 0, c_dec = 0;
             if (tr) tr[58] = globaltimer_ns();
             const long long t_start = clock64();
@@ -688,7 +697,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 mbar_arrive_expect_tx(&tfull[b], buf_bytes);
                 tma_load_3d(tbuf + (size_t)b * buf_bytes, &tmap_src, &tfull[b], e.z, e.w, e.y);
             };
-            unsigned long long* t2 = p.trace ? p.trace + (size_t)(512 + blockIdx.x) * 64 : nullptr;
+            unsigned long long* t2 = trace ? trace + (size_t)(512 + blockIdx.x) * 64 : nullptr;
             for (int k = 0; k < p.tnb && k < n_my; ++k) {
                 load(k);
                 if (t2 && k == 0) t2[4] = globaltimer_ns();
@@ -749,7 +758,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             };
             decode_block(0);
             if (kDecode < n_my) decode_block(kDecode);
-            if (p.trace && tid == 0) p.trace[(size_t)(512 + blockIdx.x) * 64 + 3] = globaltimer_ns();
+            if (trace && tid == 0) trace[(size_t)(512 + blockIdx.x) * 64 + 3] = globaltimer_ns();
             for (int k = 0; k < n_my; ++k) {
                 const int b = k % p.tnb;
                 // one block ahead: decode chunks [k + 2 kDecode, ...) once the
@@ -821,13 +830,13 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 continue;
             }
             const int ti_e = (wi - unit) / nunits;
-            if (p.trace && warp == 4 && lane == 0 && ti_e < 8) p.trace[(size_t)blockIdx.x * 64 + 40 + 2 * ti_e] = globaltimer_ns();
+            if (trace && warp == 4 && lane == 0 && ti_e < 8) trace[(size_t)blockIdx.x * 64 + 40 + 2 * ti_e] = globaltimer_ns();
             // the CTA's last tile is split: warps 0-3 store columns [BN/2, BN)
             const bool last = kSplitLast && wi + nunits >= p.num_work;
             store_accumulator<BN, CG>(p, tmem_base, tile, acc, rank, warp & 3, lane, 0, last ? BN / 2 : BN);
             tc_fence_before();
             __syncwarp();
-            if (p.trace && warp == 4 && lane == 0 && ti_e < 8) p.trace[(size_t)blockIdx.x * 64 + 41 + 2 * ti_e] = globaltimer_ns();
+            if (trace && warp == 4 && lane == 0 && ti_e < 8) trace[(size_t)blockIdx.x * 64 + 41 + 2 * ti_e] = globaltimer_ns();
             if (lane == 0) {
                 if (CG == 2) mbar_arrive_leader(&tmem_empty[acc]);
                 else mbar_arrive(&tmem_empty[acc]);
@@ -1222,7 +1231,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse, fz);
     if (e != cudaSuccess) { err = "repack launch failed"; return e; }
 
-    static const char* trace_path = getenv("CONV_TRACE");
+    static const char* trace_path = kTraceBuild ? getenv("CONV_TRACE") : nullptr;   // trace builds only
     static unsigned long long* trace_buf = nullptr;
     prm.trace = nullptr;
     if (trace_path) {

@@ -1,4 +1,6 @@
-"""Run the tensor kernel once with CONV_TRACE and summarise the per-CTA timeline."""
+"""Run the tensor kernel once with CONV_TRACE and summarise the per-CTA timeline.
+Needs a trace build of the library: CONV_BUILD_TRACE=1 python -c "import
+paper_2101_09808_b200.build as b; b.build(force=True)" (rebuild normally after)."""
 import os, sys, subprocess
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
