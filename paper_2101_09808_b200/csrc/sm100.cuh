@@ -39,20 +39,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
-    uint32_t ok;
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok) : "r"(bar), "r"(parity), "r"(ns) : "memory");
-    return ok != 0;
-}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -76,23 +62,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
-// Critical-path wait (TMA producer, MMA issuer).  flavor 0: try_wait
-// (hardware-suspended), 1: test_wait spin, 2: try_wait with a 20-ns suspend
-// hint.  Experiments only select the flavor; 0 is the default.
-__device__ __forceinline__ void mbar_wait_flavor(uint64_t* bar, uint32_t parity, uint32_t flavor) {
-    const uint32_t a = smem_u32(bar);
-    if (flavor == 0) { mbar_wait(bar, parity); return; }
-#ifndef CONV_NO_WATCHDOG
-    const long long t0 = clock64();
-#endif
-    for (;;) {
-        const bool ok = flavor == 1 ? mbar_test_wait(a, parity) : mbar_try_wait_hint(a, parity, 20);
-        if (ok) return;
-#ifndef CONV_NO_WATCHDOG
-        if (clock64() - t0 > 8000000000ll) __trap();
-#endif
-    }
-}
 
 // Waiters that are not on the critical issue path (the epilogue waiting for
 // a whole tile's accumulator) back off with nanosleep so that their polling
