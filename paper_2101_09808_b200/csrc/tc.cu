@@ -330,7 +330,7 @@ __device__ __forceinline__ void reduce_share(const TcParams& p, int tile, const 
 //   shared memory, and each CTA's TMEM receives its own 128 accumulator rows.
 //   Per SM this halves the B operand traffic (L2 -> SMEM and SMEM -> tensor
 //   core), which is what bounds the 1-CTA kernel on wide tiles.
-template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT>
+template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT, bool FUSE>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b,
@@ -366,7 +366,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     uint8_t* tbuf = smem + p.tr_off;
     int4* cring = reinterpret_cast<int4*>(tbuf + (size_t)p.tnb * p.cc * 256);
     // static chunk assignment: CTA w of W takes sequence indices seq0 + w, seq0 + w + W, ...
-    const int n_my = p.fuse ? max(0, (p.total_chunks - p.seq0 - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) : 0;
+    const int n_my = FUSE ? max(0, (p.total_chunks - p.seq0 - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) : 0;
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -380,7 +380,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
-        if (p.fuse) {
+        if (FUSE) {
             prefetch_tmap(&tmap_src);
             prefetch_tmap(&tmap_dst);
             for (int i = 0; i < p.tnb; ++i) {
@@ -463,7 +463,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                         cb_last = cb;
                         if (++s == p.S) { s = 0; if (++r == p.R) { r = 0; ++cb; } }
                     }
-                    if (p.fuse) {
+                    if (FUSE) {
                         // the watcher has confirmed (tile, channel block) units in
                         // order; this stage reads channel blocks up to cb_last
                         const int need = tiles_done * p.n_cblk + cb_last + 1;
@@ -601,7 +601,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         // the next (tile, channel block) unit of this CTA -- relaxed reads of
         // the flags of every chunk its im2col loads read -- and, once all are
         // set, acquire them and hand the unit count to the TMA producer. =====
-        if (p.fuse) {
+        if (FUSE) {
             int u = 0, pub = 0;
             const int n_units = ((p.num_tiles - unit + nunits - 1) / nunits) * p.n_cblk;
             int tile = unit, cb = 0, q_lo = 0, cnt = 0;
@@ -674,7 +674,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         // buffer once its store has read it, and reports landed stores
         // (kPubLag behind) to the publisher.  Chunk coordinates come
         // pre-decoded from the ring (no divisions on this thread). =====
-        if (p.fuse && lane == 0 && n_my > 0) {
+        if (FUSE && lane == 0 && n_my > 0) {
             constexpr int kPubLag = 1, kReport = 2;   // completion checked + reported every kReport chunks
             const uint32_t buf_bytes = (uint32_t)p.cc * 256;
             unsigned long long* tr = trace ? trace + (size_t)blockIdx.x * 64 : nullptr;
@@ -746,7 +746,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         // storer), then convert + transpose every loaded chunk in place
         // (RNE bf16 / RNA tf32) into the row-swizzled staging tile the
         // storer's TMA store expects. =====
-        if (p.fuse && n_my > 0) {
+        if (FUSE && n_my > 0) {
             const int tid = threadIdx.x;                  // 0..127
             const int w = (int)blockIdx.x, W = (int)gridDim.x;
             const uint32_t buf_bytes = (uint32_t)p.cc * 256;
@@ -920,9 +920,9 @@ struct TcMaps {
     CUtensorMap a, b, src, dst;   // src/dst only with fuse (copies of a/b otherwise)
 };
 
-template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT>
+template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT, bool FUSE>
 static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
-    auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS, SPLIT>;
+    auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS, SPLIT, FUSE>;
     // Opt in to the largest dynamic smem once per instantiation (per process).
     static std::atomic<int> smem_set{0};
     if (smem_set.load(std::memory_order_acquire) < (int)smem) {
@@ -958,23 +958,37 @@ static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, 
 
 template <bool BF16, int CG, int KSTEPS>
 static cudaError_t launch_tc_bn(int bn, const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
-    if (prm.splits > 1) {          // split-K kernels: CG = 1, BN <= 128 only (tc_split_ok)
+    if (prm.splits > 1) {          // split-K kernels: CG = 1, BN <= 128, not fused (tc_split_ok)
         if constexpr (CG == 1) {
             switch (bn) {
-                case 32: return launch_tc<32, BF16, 1, KSTEPS, true>(m, prm, smem, grid, st);
-                case 64: return launch_tc<64, BF16, 1, KSTEPS, true>(m, prm, smem, grid, st);
-                case 128: return launch_tc<128, BF16, 1, KSTEPS, true>(m, prm, smem, grid, st);
+                case 32: return launch_tc<32, BF16, 1, KSTEPS, true, false>(m, prm, smem, grid, st);
+                case 64: return launch_tc<64, BF16, 1, KSTEPS, true, false>(m, prm, smem, grid, st);
+                case 128: return launch_tc<128, BF16, 1, KSTEPS, true, false>(m, prm, smem, grid, st);
                 default: break;
             }
         }
         return cudaErrorInvalidValue;
     }
+    // The fused transform is a separate instance: compiled into the common
+    // kernel its (untaken) code cost every non-fused plan ~3 % (Table-1 sweep
+    // 660.6 vs 642.7 us on one box) -- instructions are fetched cold after
+    // each L2 flush.
+    if (prm.fuse) {
+        switch (bn) {
+            case 32: return launch_tc<32, BF16, CG, KSTEPS, false, true>(m, prm, smem, grid, st);
+            case 64: return launch_tc<64, BF16, CG, KSTEPS, false, true>(m, prm, smem, grid, st);
+            case 128: return launch_tc<128, BF16, CG, KSTEPS, false, true>(m, prm, smem, grid, st);
+            case 192: return launch_tc<192, BF16, CG, KSTEPS, false, true>(m, prm, smem, grid, st);
+            case 256: return launch_tc<256, BF16, CG, KSTEPS, false, true>(m, prm, smem, grid, st);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (bn) {
-        case 32: return launch_tc<32, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
-        case 64: return launch_tc<64, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
-        case 128: return launch_tc<128, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
-        case 192: return launch_tc<192, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
-        case 256: return launch_tc<256, BF16, CG, KSTEPS, false>(m, prm, smem, grid, st);
+        case 32: return launch_tc<32, BF16, CG, KSTEPS, false, false>(m, prm, smem, grid, st);
+        case 64: return launch_tc<64, BF16, CG, KSTEPS, false, false>(m, prm, smem, grid, st);
+        case 128: return launch_tc<128, BF16, CG, KSTEPS, false, false>(m, prm, smem, grid, st);
+        case 192: return launch_tc<192, BF16, CG, KSTEPS, false, false>(m, prm, smem, grid, st);
+        case 256: return launch_tc<256, BF16, CG, KSTEPS, false, false>(m, prm, smem, grid, st);
         default: return cudaErrorInvalidValue;
     }
 }
