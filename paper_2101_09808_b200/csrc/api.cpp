@@ -346,8 +346,8 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
         }
         if (ft.bn && ft.bn != 32 && ft.bn != 64 && ft.bn != 128 && ft.bn != 192 && ft.bn != 256)
             return fail(CONV_ERR_INFEASIBLE, "bn must be one of 32, 64, 128, 192, 256");
-        if (ft.kbs && ft.kbs != 1 && ft.kbs != 2 && ft.kbs != 3 && ft.kbs != 4 && ft.kbs != 6)
-            return fail(CONV_ERR_INFEASIBLE, "kbs must be 1, 2, 3, 4 or 6");
+        if (ft.kbs && (ft.kbs > 9 || ft.kbs == 5))
+            return fail(CONV_ERR_INFEASIBLE, "kbs must be 1, 2, 3, 4, 6, 7, 8 or 9");
         if (ft.cg && ft.cg != 1 && ft.cg != 2) return fail(CONV_ERR_INFEASIBLE, "cg must be 1 or 2");
         if (ft.splits > 16) return fail(CONV_ERR_INFEASIBLE, "splits must be <= 16");
         if (ft.splits > 1 && ft.fuse == 1) return fail(CONV_ERR_INFEASIBLE, "split-K needs fuse=0");

@@ -306,7 +306,11 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
     bool found = false;
     for (int cg = 1; cg <= 2; ++cg) {
         if (force_cg && cg != force_cg) continue;
-        for (int kbs : {1, 2, 3, 4, 6}) {               // k-blocks per stage; must divide the k loop
+        // k-blocks per stage; must divide the k loop.  7 and 9 are whole
+        // kernel rows / windows of 7x7 and 3x3 taps: tiny-C layers (C*elem
+        // <= 128 B: one k-block per tap) otherwise pay the per-stage latency
+        // floor once per tap (R1: 49 stages of 16 channels per tile).
+        for (int kbs : {1, 2, 3, 4, 6, 7, 8, 9}) {
             if (force_kbs && kbs != force_kbs) continue;
             if ((pb.R * pb.S * L.n_cblk) % kbs) continue;
             for (int bn : kBNs) {

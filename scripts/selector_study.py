@@ -79,7 +79,7 @@ def main():
         auto = conv.ConvPlan(*sh.as_tuple(), path=path, **sh.plan_kwargs())
         auto_tile = auto.describe()["tile"]
         rows = []
-        for bn, cg, kbs, fuse in itertools.product((32, 64, 128, 192, 256), (1, 2), (1, 2, 3, 4, 6), (0, 1)):
+        for bn, cg, kbs, fuse in itertools.product((32, 64, 128, 192, 256), (1, 2), (1, 2, 3, 4, 6, 7, 9), (0, 1)):
             spec = f"bn={bn},cg={cg},kbs={kbs},fuse={fuse}"
             try:
                 plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile=spec, **sh.plan_kwargs())

@@ -208,6 +208,21 @@ def test_splitk_fixed_split_tile_invariance_and_graph_replay(path):
         assert rel_l2(out.cpu().numpy(), r2) <= 1e-5
 
 
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_p10_whole_row_stages(path):
+    """kbs = 7 / 9 (one stage = a 7-tap kernel row / the whole 3x3 window of
+    a tiny-C layer) gives the same bits as one k-block per stage (P10), and
+    matches the oracle: a 7x7 stride-2 stem (R1-like) and a 3-channel 3x3."""
+    for sh, kbs in ((Shape.strided(2, 64, 3, 40, 38, 7, 7, 2), 7), (Shape(N=2, K=32, C=3, H=30, W=27, R=3, S=3), 9)):
+        inp, ker = make_inputs(sh, seed=141)
+        ref, _ = run(sh, inp, ker, path, tile="kbs=1,splits=1")
+        got, plan = run(sh, inp, ker, path, tile=f"kbs={kbs},splits=1")
+        assert plan.describe()["tile"]["kbs"] == kbs
+        assert np.array_equal(got, ref)
+        r64 = oracle.conv_eq1_strided(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), sh.U)
+        assert rel_l2(got, r64) <= 1e-5
+
+
 def test_p10_tile_invariance_simt():
     sh = Shape(N=2, K=32, C=24, H=12, W=12, R=3, S=3)
     inp, ker = make_inputs(sh, seed=8)
