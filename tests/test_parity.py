@@ -323,6 +323,29 @@ def test_run_host_end_to_end():
     assert rel_l2(out_h.numpy(), ref) <= TOL["tf32"]
 
 
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_run_host_split_k_plans(path):
+    """conv_run_host with split-K plans: a batch-1 deep-C layer (the AUTO plan
+    splits it) and a forced split count over a batch that the host pipeline
+    cuts into image chunks (each chunk a smaller sub-problem of the plan):
+    bit-identical to conv_run on device pointers, and within tolerance of
+    the oracle."""
+    from paper_2101_09808_b200.inputs import TABLE1
+    cases = ((TABLE1["M9"], None), (Shape(N=3, K=256, C=512, H=7, W=7, R=3, S=3), "splits=4"))
+    for sh, tile in cases:
+        inp, ker = make_inputs(sh, seed=151)
+        plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile=tile, **sh.plan_kwargs())
+        assert plan.describe()["tile"]["splits"] > 1
+        dev_out = plan.run(inp.cuda(), ker.cuda())
+        dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device="cuda")
+        out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+        plan.run_host(inp.pin_memory(), ker.pin_memory(), out_h, dbuf)
+        torch.cuda.synchronize()
+        assert torch.equal(out_h, dev_out.cpu())
+        ref = oracle.conv_eq1_strided(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), sh.U)
+        assert rel_l2(out_h.numpy(), ref) <= 1e-5
+
+
 def test_run_events_records_each_kernel():
     sh = CONFIGS["det"]
     inp, ker = make_inputs(sh, seed=0)
