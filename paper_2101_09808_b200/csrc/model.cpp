@@ -337,8 +337,10 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
                     t.stages = force_stages ? force_stages : smax;
                     if (t.stages < 2 || t.stages > smax) continue;
                     if (fuse) {   // as many transform chunk buffers as fit (2..6)
-                        // prologue depth measured best in r01b: 128 channels (bf16), 64 (tf32)
-                        t.pre_c = force_pre_c >= 0 ? force_pre_c : (bf16 ? 128 : 64);
+                        // prologue depth measured best in r01b (batched layer, after the
+                        // production-build cleanup): 192 channels bf16 (915-917 vs 905-906
+                        // TFLOP/s at 128), 64 tf32 (603.5 vs 589-597 at 96-192)
+                        t.pre_c = force_pre_c >= 0 ? force_pre_c : (bf16 ? 192 : 64);
                         t.tnb = 2;
                         for (int nb = 6; nb > 2; --nb) {
                             TcTile u = t;

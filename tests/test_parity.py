@@ -410,7 +410,7 @@ def test_fused_transform_bit_identical_to_separate(path, shape):
 
 
 @pytest.mark.parametrize("path", ["tf32", "bf16"])
-@pytest.mark.parametrize("pre_c", [0, 64, 128, 4096])
+@pytest.mark.parametrize("pre_c", [0, 64, 128, 192, 4096])
 def test_fused_transform_prologue_depths(path, pre_c):
     """The repack launch converts the first pre_c channels of wave 0's input
     (the prologue) and the kernel's chunk pipeline the rest: every split
