@@ -91,7 +91,10 @@ static conv_status fail(conv_status s, const char* fmt, ...) {
 
 extern "C" const char* conv_last_error(void) { return g_err.c_str(); }
 extern "C" conv_status conv_last_status(void) { return g_status; }
-extern "C" const char* conv_version(void) { return "0.1.0 sm_100a"; }
+#ifndef CONV_ENABLE_TRACE
+#define CONV_ENABLE_TRACE 0
+#endif
+extern "C" const char* conv_version(void) { return CONV_ENABLE_TRACE ? "0.1.0 sm_100a +trace" : "0.1.0 sm_100a"; }
 
 static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 

@@ -19,6 +19,10 @@ for _ in range(3): p.run(i, k, o, ws)
 torch.cuda.synchronize()
 print(p.describe()['tile'])
 """
+from paper_2101_09808_b200 import conv as _conv  # noqa: E402
+if "+trace" not in _conv.load_library().conv_version().decode():
+    raise SystemExit("not a trace build: CONV_BUILD_TRACE=1 python -c 'import paper_2101_09808_b200.build as b; "
+                     "b.build(force=True)'")
 subprocess.run([sys.executable, "-c", code], env=env, check=True)
 t = np.fromfile(out, dtype=np.uint64).reshape(-1, 64).astype(np.int64)
 t2all = t[512:]

@@ -289,3 +289,11 @@ def test_padded_plans_offline(lib):
     with pytest.raises(conv.ConvError) as e:   # lower corner -129
         conv.ConvPlan(1, 8, 8, 3 + 258 - 2, 3, 3, 3, padding=(129, 0), in_hw=(3, 5), offline_device=sh, path="bf16")
     assert e.value.status == conv.CONV_ERR_INFEASIBLE
+
+
+def test_production_build(lib):
+    """The in-tree library is a production build: the kernel timeline
+    instrumentation (CONV_BUILD_TRACE=1, scripts/trace_tc.py) is compiled
+    out -- it cost ~1.8 % on the headline."""
+    v = lib.conv_version().decode()
+    assert v.startswith("0.1.0 sm_100a") and "+trace" not in v
