@@ -18,6 +18,8 @@
 
 #include <algorithm>
 
+#include <type_traits>
+
 #include "internal.h"
 #include "sm100.cuh"
 
@@ -177,7 +179,12 @@ __device__ __forceinline__ void ker_repack_cta(const float* __restrict__ ker, ty
     }
 }
 
-template <bool BF16>
+// MODE 0: K1 + K2 (plain plans); 1: + clearing (split-K arrival counters);
+// 2: K1 + clearing + the fused prologue (fused plans).  Separate instances:
+// compiled into one kernel the untaken clearing / prologue code cost the
+// plain repack ~1 % of the Table-1 sweep (its instructions are fetched cold
+// after every L2 flush).
+template <bool BF16, int MODE>
 __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, const float* __restrict__ ker,
                                                   typename Elem<BF16>::T* __restrict__ in_ws,
                                                   typename Elem<BF16>::T* __restrict__ ker_ws, const RepackGeom g) {
@@ -191,7 +198,7 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
     if ((int)blockIdx.x >= g.pdl_from) asm volatile("griddepcontrol.launch_dependents;");
     if ((int)blockIdx.x < g.n_ker) {
         // ---- K1 ----
-        if (g.zero_n) {   // clear the fused transform's chunk flags (the prologue's are set below)
+        if (MODE >= 1 && g.zero_n) {   // clear the fused transform's chunk flags (the prologue's are set below)
             const int per = (g.zero_n + g.n_ker - 1) / g.n_ker;
             const int z0 = blockIdx.x * per, z1 = min(z0 + per, g.zero_n);
             for (int i = z0 + tid; i < z1; i += 256) {
@@ -209,7 +216,7 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
     int pt, ct;
     int64_t n;
     const int pre_ct = (g.pre_ch * g.cc_f + 63) / 64;   // 64-channel tiles in the prologue
-    if (g.n_pre) {                   // fused prologue: tile (q = b / pre_ct, channels 64 * (b % pre_ct) ...)
+    if (MODE == 2 && g.n_pre) {                   // fused prologue: tile (q = b / pre_ct, channels 64 * (b % pre_ct) ...)
         ct = b % pre_ct;
         const int q = b / pre_ct;
         n = q / g.ptiles;
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(256) repack_all(const float* __restrict__ in, 
     }
     // fused prologue: the main kernel reads these chunks only after this grid
     // has completed (griddepcontrol.wait), so plain stores suffice
-    if (g.n_pre) {
+    if (MODE == 2 && g.n_pre) {
         const int q = (blockIdx.x - g.n_ker) / pre_ct;
         const int ch0 = ct * 64 / g.cc_f, ch1 = min(ch0 + 64 / g.cc_f, g.pre_ch);
         if (tid < ch1 - ch0) g.zero_ptr[32 + (int64_t)q * g.nch + ch0 + tid] = 1;
@@ -490,16 +497,23 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
     }
     const size_t smem = std::max<size_t>(64 * 65 * sizeof(float),
                                          (g.krows > 1 ? (size_t)g.krows * g.C : (size_t)g.cc) * g.RS * sizeof(float));
+    const int mode = g.n_pre > 0 || (fz.zero_ptr && !with_in) ? 2 : (fz.zero_ptr ? 1 : 0);
+    auto kern = [&](auto bf) {
+        constexpr bool B = decltype(bf)::value;
+        return mode == 2 ? repack_all<B, 2> : mode == 1 ? repack_all<B, 1> : repack_all<B, 0>;
+    };
+    auto kfn16 = kern(std::true_type{});
+    auto kfn32 = kern(std::false_type{});
     if (smem > 48 * 1024) {   // very large R*S: one channel per K1 CTA still needs > 48 KB
-        cudaError_t e = bf16 ? cudaFuncSetAttribute(repack_all<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                             : cudaFuncSetAttribute(repack_all<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = bf16 ? cudaFuncSetAttribute(kfn16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                             : cudaFuncSetAttribute(kfn32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     if (ev) cudaEventRecord(ev[0], st);
     if (bf16)
-        repack_all<true><<<(unsigned)grid, 256, smem, st>>>(in, ker, (__nv_bfloat16*)in_ws, (__nv_bfloat16*)ker_ws, g);
+        kfn16<<<(unsigned)grid, 256, smem, st>>>(in, ker, (__nv_bfloat16*)in_ws, (__nv_bfloat16*)ker_ws, g);
     else
-        repack_all<false><<<(unsigned)grid, 256, smem, st>>>(in, ker, (float*)in_ws, (float*)ker_ws, g);
+        kfn32<<<(unsigned)grid, 256, smem, st>>>(in, ker, (float*)in_ws, (float*)ker_ws, g);
     if (ev) cudaEventRecord(ev[1], st);
     return cudaGetLastError();
 }
