@@ -49,6 +49,8 @@ using namespace conv;
 
 struct conv_plan {
     Problem pb;
+    bool expand = false;    // tensor paths: run expanded_problem(pb) after the tap expansion
+    Problem pe{};
     Device dev;
     conv_path requested = CONV_PATH_AUTO;
     conv_path path = CONV_PATH_AUTO;
@@ -101,8 +103,33 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 static size_t ws_bytes(const conv_plan* p) {
     if (p->path == CONV_PATH_FP32_SIMT) return align256(simt_ws_bytes(p->pb, p->simt));
     // aux region: the fused transform's flags, or split-K's counters + partials
-    const size_t aux = p->tc.fuse ? p->tcl.flag_bytes : tc_split_bytes(p->pb, p->tcl, p->tc);
+    const Problem& kp = p->expand ? p->pe : p->pb;          // the problem the tensor kernel runs
+    const size_t aux = p->tc.fuse ? p->tcl.flag_bytes : tc_split_bytes(kp, p->tcl, p->tc);
     return align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes) + align256(aux);
+}
+
+// Tensor-path selection on the problem the kernel will run: tiny-C layers
+// (expand_useful, or forced with the tile key expand) run their 1x1
+// tap-expanded equivalent, without the fused transform or split-K.
+static bool select_tensor(conv_plan* p, bool bf16, TcTile& tt, ModelResult& rt, bool& expand, Problem& pe,
+                          std::string& why) {
+    const Problem& pb = p->pb;
+    // automatic only when the fused transform / split-K are not forced
+    expand = p->force_tc.expand >= 0 ? p->force_tc.expand == 1
+                                     : expand_useful(pb, bf16) && p->force_tc.fuse != 1 && p->force_tc.splits <= 1;
+    if (expand && (p->force_tc.fuse == 1 || p->force_tc.splits > 1)) {
+        why = "the tap expansion runs without the fused transform and split-K";
+        return false;
+    }
+    if (!expand) return select_tc(pb, p->dev, bf16, tt, rt, p->force_tc, why);
+    pe = expanded_problem(pb);
+    TcForce f = p->force_tc;
+    f.fuse = 0;
+    f.splits = 1;
+    if (!select_tc(pe, p->dev, bf16, tt, rt, f, why)) return false;
+    // the expansion reads In (fp32) and Ker and writes the expanded workspace
+    // instead of the plain repack the model charged for pe
+    return true;
 }
 
 // Re-run the selector for the requested path (Alg. 1:
@@ -123,8 +150,11 @@ static conv_status select(conv_plan* p) {
         case CONV_PATH_TF32:
         case CONV_PATH_BF16: {
             const bool bf16 = p->requested == CONV_PATH_BF16;
-            if (!select_tc(pb, p->dev, bf16, tt, rt, p->force_tc, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
-            p->tc = tt; p->model = rt; p->path = p->requested; p->tcl = tc_layout(pb, bf16);
+            bool ex = false;
+            Problem pe{};
+            if (!select_tensor(p, bf16, tt, rt, ex, pe, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            p->tc = tt; p->model = rt; p->path = p->requested; p->expand = ex; p->pe = pe;
+            p->tcl = tc_layout(ex ? pe : pb, bf16);
             break;
         }
         case CONV_PATH_AUTO:
@@ -132,10 +162,13 @@ static conv_status select(conv_plan* p) {
             // AUTO keeps fp32 inputs or TF32 products (the precision of the
             // paper's fp32 method); BF16 only when requested.
             const bool ok_s = select_simt(pb, p->dev, st, rs, fs, p->force_simt_mask, why);
-            const bool ok_t = select_tc(pb, p->dev, false, tt, rt, p->force_tc, why);
+            bool ex = false;
+            Problem pe{};
+            const bool ok_t = select_tensor(p, false, tt, rt, ex, pe, why);
             if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             if (ok_t && (!ok_s || rt.model_us < rs.model_us)) {
-                p->tc = tt; p->model = rt; p->path = CONV_PATH_TF32; p->tcl = tc_layout(pb, false);
+                p->tc = tt; p->model = rt; p->path = CONV_PATH_TF32; p->expand = ex; p->pe = pe;
+                p->tcl = tc_layout(ex ? pe : pb, false);
             } else {
                 p->simt = st; p->model = rs; p->path = CONV_PATH_FP32_SIMT;
             }
@@ -328,7 +361,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             std::string key = kv.substr(0, eq);
             char* end = nullptr;
             long v = strtol(kv.c_str() + eq + 1, &end, 10);
-            const long vmin = (key == "fuse" || key == "pre_c") ? 0 : 1;
+            const long vmin = (key == "fuse" || key == "pre_c" || key == "expand") ? 0 : 1;
             if (!end || *end || v < vmin || v > 4096) return fail(CONV_ERR_INVALID_ARGUMENT, "bad value in '%s'", kv.c_str());
             if (key == "bn") ft.bn = (int)v;
             else if (key == "stages") ft.stages = (int)v;
@@ -337,6 +370,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "splits") ft.splits = (int)v;
             else if (key == "fuse") ft.fuse = v ? 1 : 0;
             else if (key == "pre_c") ft.pre_c = (int)v;
+            else if (key == "expand") ft.expand = v ? 1 : 0;
             else if (key == "tk") { fs.tk = (int)v; mask |= 1; }
             else if (key == "tw") { fs.tw = (int)v; mask |= 2; }
             else if (key == "kg") { fs.kg = (int)v; mask |= 4; }
@@ -404,8 +438,8 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
                  32 * p->simt.kg * p->simt.pw);
     } else {
-        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
-                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
+        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
+                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
                  p->tc.fuse ? std::min(p->tc.pre_c, p->tcl.Cp) : 0,
                  p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
     }
@@ -457,8 +491,14 @@ static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0
         void* ker_ws = wsb + align256(p->tcl.in_ws_bytes);
         void* flag_ws = (p->tc.fuse || p->tc.splits > 1) ? wsb + align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes)
                                                          : nullptr;
-        e = tc_run(sub, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, in_ws, ker_ws, flag_ws, st, p->dev.sms,
-                   evp, err);
+        if (p->expand) {
+            const Problem sub_e = expanded_problem(sub);
+            e = tc_run(sub_e, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, in_ws, ker_ws, flag_ws, st,
+                       p->dev.sms, evp, err, &sub);
+        } else {
+            e = tc_run(sub, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, in_ws, ker_ws, flag_ws, st,
+                       p->dev.sms, evp, err);
+        }
     }
     if (e != cudaSuccess) {
         cudaGetLastError();

@@ -98,6 +98,23 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
                           void* in_ws, void* ker_ws, cudaStream_t st, cudaEvent_t* ev, bool with_in,
                           const RepackFuse& fz);
 
+// Tiny-C tap expansion (repack.cu): In' = the R*S*C taps of every output
+// pixel as channels ([N][H][W][Cp]), Ker' = [K][Cp] in the same (r, s, c)
+// order; the equivalent 1x1 problem is expanded_problem(pb).
+cudaError_t launch_expand(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker, void* in_ws,
+                          void* ker_ws, cudaStream_t st, cudaEvent_t* ev);
+inline Problem expanded_problem(const Problem& pb) {
+    Problem pe{pb.N, pb.K, pb.R * pb.S * pb.C, pb.H, pb.W, 1, 1};
+    return pe;
+}
+// Layers for which the expansion pays (the TMA im2col rows would be <= 16 B
+// of channels and there are several taps): measured on Table 1's C = 3
+// stems (profiles/r01b/expand_ab.jsonl).
+inline bool expand_useful(const Problem& pb, bool bf16) {
+    const int elem = bf16 ? 2 : 4;
+    return pb.C * elem <= 16 && pb.R * pb.S >= 4 && (int64_t)pb.R * pb.S * pb.C <= 1024;
+}
+
 TcLayout tc_layout(const Problem& p, bool bf16);
 
 // Split-K geometry of a tile choice: k iterations per split (stage-aligned)
@@ -115,9 +132,12 @@ size_t tc_smem_bytes(const TcLayout& L, const TcTile& t);
 // Launch the repack (K1 + K2, one launch) and K3 (tcgen05 implicit GEMM).
 // events (optional, n_events == 3) are recorded around each kernel.
 // flag_ws: L.flag_bytes of workspace for the fused transform (unused if !t.fuse).
+// expand_src (tiny-C plans): p is expanded_problem(*expand_src) and the
+// layout transform is the tap expansion of *expand_src (launch_expand).
 cudaError_t tc_run(const Problem& p, const TcLayout& L, const TcTile& t, bool bf16,
                    const float* in, const float* ker, float* out, void* in_ws, void* ker_ws, void* flag_ws,
-                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err);
+                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err,
+                   const Problem* expand_src = nullptr);
 
 // ---- FP32 SIMT path (K4) ----------------------------------------------------
 struct SimtTile {

@@ -518,4 +518,120 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
     return cudaGetLastError();
 }
 
+
+// ---- tiny-C tap expansion (explicit im2col in the layout transform) --------
+// For layers with a handful of input channels (the C = 3 stems: Table 1 Y0,
+// R1) the tensor kernel's TMA im2col rows are 32 B each and there are R*S of
+// them per pixel: the layer is bound by TMA row throughput, not bytes.  The
+// expansion writes, per OUTPUT pixel, all R*S*C taps as channels --
+//   In'[n][h][w][(r*S + s)*C + c] = In[n][c][U*h + D*r - ph][U*w + D*s - pw]
+// (zero outside the input, zero for channels >= R*S*C) and
+//   Ker'[k][(r*S + s)*C + c]      = Ker[k][c][r][s]
+// -- so that the main kernel runs the equivalent 1x1 convolution with
+// C' = R*S*C over H x W (Eq. 1 regrouped: the same products, summed in the
+// k-block order of the 1x1 problem).  One launch: blocks [0, ker_blocks)
+// write Ker', the rest In' (8 channels = one 16-B bf16 / two 16-B tf32
+// stores per thread).  Triggers the dependent launch at the end of each
+// block, so the main kernel's large CTAs do not take SMs from it.
+struct ExpandGeom {
+    int N, K, C, H, W, R, S, U, D, ph, pw, Hin, Win;
+    int RSC, Cp, groups;              // groups = Cp / 8 (16-B bf16 / 32-B tf32 store units)
+    int ker_blocks, xblocks;          // Ker' blocks; In' blocks per output row
+    int64_t ker_elems;
+};
+
+// Per-channel (r, s, c) decode of the expanded layout, shared by a block:
+// input-plane offset of channel c and the tap's row / column shift.
+struct TapEntry {
+    int coff, dr, ds;                 // c*Hin*Win, D*r, D*s; coff < 0: padding channel (j >= R*S*C)
+};
+
+template <bool BF16>
+__global__ void __launch_bounds__(256) expand_taps(const float* __restrict__ in, const float* __restrict__ ker,
+                                                   typename Elem<BF16>::T* __restrict__ in_ws,
+                                                   typename Elem<BF16>::T* __restrict__ ker_ws, const ExpandGeom g) {
+    extern __shared__ TapEntry tab[];
+    if ((int)blockIdx.x < g.ker_blocks) {
+        for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < g.ker_elems; e += (int64_t)g.ker_blocks * 256) {
+            const int64_t k = e / g.Cp;
+            const int j = (int)(e - k * g.Cp);
+            float v = 0.0f;
+            if (j < g.RSC) {
+                const int rs = j / g.C, c = j - rs * g.C;
+                v = __ldg(ker + (k * g.C + c) * (g.R * g.S) + rs);
+            }
+            ker_ws[e] = Elem<BF16>::cvt(v);
+        }
+    } else {
+        // block b >= ker_blocks: output row (b - ker_blocks) / xblocks = n*H + h,
+        // its (pixel, channel-group) units [xb*256, xb*256 + 256)
+        for (int j = threadIdx.x; j < g.Cp; j += 256) {
+            TapEntry t{-1, 0, 0};
+            if (j < g.RSC) {
+                const int rs = j / g.C, c = j - rs * g.C, r = rs / g.S, sx = rs - (rs / g.S) * g.S;
+                t = TapEntry{c * g.Hin * g.Win, g.D * r, g.D * sx};
+            }
+            tab[j] = t;
+        }
+        __syncthreads();
+        const int b = (int)blockIdx.x - g.ker_blocks;
+        const int row = b / g.xblocks, xb = b - row * g.xblocks;
+        const int n = row / g.H, h = row - (row / g.H) * g.H;
+        const int e = xb * 256 + (int)threadIdx.x;
+        const int w = e / g.groups;
+        if (w < g.W) {
+            const int j0 = (e - w * g.groups) * 8;
+            const int ih0 = g.U * h - g.ph, iw0 = g.U * w - g.pw;
+            const float* src = in + (int64_t)n * g.C * g.Hin * g.Win;
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const TapEntry t = tab[j0 + i];
+                const int ih = ih0 + t.dr, iw = iw0 + t.ds;
+                v[i] = (t.coff >= 0 && (unsigned)ih < (unsigned)g.Hin && (unsigned)iw < (unsigned)g.Win)
+                           ? __ldg(src + t.coff + ih * g.Win + iw) : 0.0f;
+            }
+            typename Elem<BF16>::T* dst = in_ws + (((int64_t)row * g.W + w) * g.Cp + j0);
+            if (BF16) {
+                uint4 o;
+                o.x = pack2_bf16(v[0], v[1]);
+                o.y = pack2_bf16(v[2], v[3]);
+                o.z = pack2_bf16(v[4], v[5]);
+                o.w = pack2_bf16(v[6], v[7]);
+                *reinterpret_cast<uint4*>(dst) = o;
+            } else {
+                float4* d4 = reinterpret_cast<float4*>(dst);
+                d4[0] = make_float4(to_tf32_rna(v[0]), to_tf32_rna(v[1]), to_tf32_rna(v[2]), to_tf32_rna(v[3]));
+                d4[1] = make_float4(to_tf32_rna(v[4]), to_tf32_rna(v[5]), to_tf32_rna(v[6]), to_tf32_rna(v[7]));
+            }
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;");
+}
+
+cudaError_t launch_expand(const Problem& pb, int Cp, bool bf16, const float* in, const float* ker, void* in_ws,
+                          void* ker_ws, cudaStream_t st, cudaEvent_t* ev) {
+    ExpandGeom g;
+    g.N = pb.N; g.K = pb.K; g.C = pb.C; g.H = pb.H; g.W = pb.W; g.R = pb.R; g.S = pb.S;
+    g.U = pb.U; g.D = pb.D; g.ph = pb.ph; g.pw = pb.pw; g.Hin = (int)pb.Hin(); g.Win = (int)pb.Win();
+    g.RSC = pb.R * pb.S * pb.C;
+    g.Cp = Cp;
+    if (Cp % 8 || Cp < g.RSC || (int64_t)pb.C * pb.Hin() * pb.Win() >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;
+    g.groups = Cp / 8;
+    g.ker_elems = (int64_t)pb.K * Cp;
+    g.ker_blocks = (int)std::min<int64_t>((g.ker_elems + 255) / 256, 256);
+    g.xblocks = (int)(((int64_t)pb.W * g.groups + 255) / 256);
+    const int64_t blocks = g.ker_blocks + (int64_t)pb.N * pb.H * g.xblocks;
+    if (blocks >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;
+    const dim3 grid((unsigned)blocks);
+    const size_t smem = (size_t)Cp * sizeof(TapEntry);
+    if (ev) cudaEventRecord(ev[0], st);
+    if (bf16)
+        expand_taps<true><<<grid, 256, smem, st>>>(in, ker, (__nv_bfloat16*)in_ws, (__nv_bfloat16*)ker_ws, g);
+    else
+        expand_taps<false><<<grid, 256, smem, st>>>(in, ker, (float*)in_ws, (float*)ker_ws, g);
+    if (ev) cudaEventRecord(ev[1], st);
+    return cudaGetLastError();
+}
+
 }  // namespace conv

@@ -1104,7 +1104,8 @@ bool tc_split_ok(const Problem& pb, const TcLayout& L, const TcTile& t) {
 
 cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool bf16,
                    const float* in, const float* ker, float* out, void* in_ws, void* ker_ws, void* flag_ws,
-                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err) {
+                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err, const Problem* expand_src) {
+    if (expand_src && (t.fuse || t.splits > 1)) { err = "tap-expanded plans run without the fused transform and split-K"; return cudaErrorInvalidValue; }
     if (t.fuse && (!L.coop_ok || !flag_ws)) { err = "fused transform needs a TMA-legal NCHW plane and flag workspace"; return cudaErrorInvalidValue; }
     // Tensor maps depend on the workspace (and, fused, In) addresses, known
     // only here; they are encoded on first use and cached.
@@ -1242,7 +1243,8 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         fz.zero_ptr = prm.tile_ctr;               // the repack launch clears the arrival counters
         fz.zero_n = prm.num_tiles;
     }
-    e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse, fz);
+    e = expand_src ? launch_expand(*expand_src, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev)
+                   : launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse, fz);
     if (e != cudaSuccess) { err = "repack launch failed"; return e; }
 
     static const char* trace_path = kTraceBuild ? getenv("CONV_TRACE") : nullptr;   // trace builds only

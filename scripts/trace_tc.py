@@ -10,9 +10,9 @@ env = dict(os.environ, CONV_TRACE=out)
 code = f"""
 import torch
 from paper_2101_09808_b200 import conv
-from paper_2101_09808_b200.inputs import CONFIGS, make_inputs
-sh = CONFIGS['{cfg}']
-p = conv.ConvPlan(*sh.as_tuple(), path='{path}', tile='{tile}' or None)
+from paper_2101_09808_b200.inputs import CONFIGS, TABLE1, make_inputs
+sh = CONFIGS['{cfg}'] if '{cfg}' in CONFIGS else TABLE1['{cfg}']
+p = conv.ConvPlan(*sh.as_tuple(), path='{path}', tile='{tile}' or None, **sh.plan_kwargs())
 i, k = make_inputs(sh)
 i, k = i.cuda(), k.cuda(); o = p.new_output(); ws = p.new_workspace()
 for _ in range(3): p.run(i, k, o, ws)

@@ -226,9 +226,12 @@ def test_strided_plans_offline(lib):
     assert "extent must be >= 1" in conv.last_error()
     assert not lib.conv_plan_create_strided(1, 1, 1, 2, 8, 3, 3, 1)
     assert "smaller than the kernel" in conv.last_error()
-    with pytest.raises(conv.ConvError) as e:
-        conv.ConvPlan(1, 8, 8, 3, 3, 3, 3, stride=9, in_hw=(21, 21), offline_device=sh, path="bf16")
+    with pytest.raises(conv.ConvError) as e:   # TMA im2col traversal stride <= 8
+        conv.ConvPlan(1, 8, 64, 3, 3, 3, 3, stride=9, in_hw=(21, 21), offline_device=sh, path="bf16")
     assert e.value.status == conv.CONV_ERR_INFEASIBLE
+    # a tiny-C layer runs its tap-expanded 1x1 equivalent: any stride
+    d = conv.ConvPlan(1, 8, 8, 3, 3, 3, 3, stride=9, in_hw=(21, 21), offline_device=sh, path="bf16").describe()
+    assert d["tile"]["expand"] == 1
     with pytest.raises(ValueError):   # H, W inconsistent with the input extents
         conv.ConvPlan(1, 8, 8, 5, 5, 3, 3, stride=2, in_hw=(21, 21), offline_device=sh)
 
@@ -256,7 +259,7 @@ def test_dilated_plans_offline(lib):
     assert not lib.conv_plan_create_dilated(1, 1, 1, 4, 8, 3, 3, 1, 2)   # dilated kernel is 5x5
     assert "smaller than the kernel" in conv.last_error()
     with pytest.raises(conv.ConvError) as e:   # D(R-1) = 129 > 128
-        conv.ConvPlan(1, 8, 8, 2, 2, 2, 2, dilation=129, in_hw=(131, 131), offline_device=sh, path="bf16")
+        conv.ConvPlan(1, 8, 64, 2, 2, 2, 2, dilation=129, in_hw=(131, 131), offline_device=sh, path="bf16")
     assert e.value.status == conv.CONV_ERR_INFEASIBLE
 
 
@@ -287,8 +290,12 @@ def test_padded_plans_offline(lib):
     assert not lib.conv_plan_create_padded(1, 1, 1, 1, 1, 5, 5, 1, 1, 1, 1)   # 3x3 padded input, 5x5 kernel
     assert "smaller than the kernel" in conv.last_error()
     with pytest.raises(conv.ConvError) as e:   # lower corner -129
-        conv.ConvPlan(1, 8, 8, 3 + 258 - 2, 3, 3, 3, padding=(129, 0), in_hw=(3, 5), offline_device=sh, path="bf16")
+        conv.ConvPlan(1, 8, 64, 3 + 258 - 2, 3, 3, 3, padding=(129, 0), in_hw=(3, 5), offline_device=sh, path="bf16")
     assert e.value.status == conv.CONV_ERR_INFEASIBLE
+    # tiny C: the tap expansion computes the padded taps directly (no TMA box)
+    d = conv.ConvPlan(1, 8, 8, 3 + 258 - 2, 3, 3, 3, padding=(129, 0), in_hw=(3, 5), offline_device=sh,
+                      path="bf16").describe()
+    assert d["tile"]["expand"] == 1
 
 
 def test_production_build(lib):

@@ -215,8 +215,8 @@ def test_p10_whole_row_stages(path):
     matches the oracle: a 7x7 stride-2 stem (R1-like) and a 3-channel 3x3."""
     for sh, kbs in ((Shape.strided(2, 64, 3, 40, 38, 7, 7, 2), 7), (Shape(N=2, K=32, C=3, H=30, W=27, R=3, S=3), 9)):
         inp, ker = make_inputs(sh, seed=141)
-        ref, _ = run(sh, inp, ker, path, tile="kbs=1,splits=1")
-        got, plan = run(sh, inp, ker, path, tile=f"kbs={kbs},splits=1")
+        ref, _ = run(sh, inp, ker, path, tile="kbs=1,splits=1,expand=0")
+        got, plan = run(sh, inp, ker, path, tile=f"kbs={kbs},splits=1,expand=0")
         assert plan.describe()["tile"]["kbs"] == kbs
         assert np.array_equal(got, ref)
         r64 = oracle.conv_eq1_strided(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), sh.U)
@@ -307,7 +307,7 @@ def test_argument_errors():
     with pytest.raises(conv.ConvError):
         conv.ConvPlan(1, 1, 1, 0, 1, 1, 1)
     with pytest.raises(conv.ConvError) as e:
-        conv.ConvPlan(1, 4, 4, 4, 4, 130, 1, path="tf32")
+        conv.ConvPlan(1, 4, 64, 4, 4, 130, 1, path="tf32")   # R > 128: past the TMA im2col box
     assert e.value.status == conv.CONV_ERR_INFEASIBLE
 
 
@@ -661,6 +661,78 @@ def test_general_conv_with_split_k(path, splits):
     xi, wi = make_inputs(sh, seed=132, kind="int")
     goti, _ = run(sh, xi, wi, path, tile=spec)
     assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1_padded(xi.numpy(), wi.numpy(), sh.U, sh.D, pad))
+
+
+# ---- tiny-C tap expansion (explicit im2col in the layout transform) ---------
+EXPAND = [
+    Shape(N=2, K=32, C=3, H=40, W=38, R=3, S=3),                 # Y0-like 3x3 stem
+    Shape.strided(1, 64, 3, 45, 45, 7, 7, 2, 1, 3, 3),           # R1-like 7x7 stride-2 "same" stem
+    Shape.strided(2, 24, 1, 19, 17, 3, 3, 1, 2, 1, 2),           # C = 1, dilation, asymmetric padding
+    Shape(N=3, K=40, C=8, H=9, W=11, R=5, S=3),                  # C = 8 (16 B of bf16), R != S
+    Shape.strided(1, 16, 4, 30, 30, 3, 3, 9, 1),                 # stride 9 (past the TMA traversal limit)
+]
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", EXPAND, ids=lambda s: f"{s.N}x{s.K}x{s.C}x{s.Hin}x{s.Win}x{s.R}x{s.S}s{s.U}d{s.D}p{s.ph}")
+def test_tap_expansion_parity(path, shape):
+    """The tap-expanded 1x1 plan (forced, the AUTO choice for tiny C) against
+    the padded oracle: 1e-5 on the path's rounded inputs, bit-exact on the
+    integer twin; the plain plan (expand=0, where TMA allows it) agrees
+    within tolerance."""
+    inp, ker = make_inputs(shape, seed=161)
+    got, plan = run(shape, inp, ker, path, tile="expand=1")
+    assert plan.describe()["tile"]["expand"] == 1
+    pad = (shape.ph, shape.pw)
+    ref = oracle.conv_eq1_padded(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), shape.U, shape.D, pad)
+    assert got.shape == ref.shape
+    assert rel_l2(got, ref) <= 1e-5
+    xi, wi = make_inputs(shape, seed=162, kind="int")
+    goti, _ = run(shape, xi, wi, path, tile="expand=1")
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1_padded(xi.numpy(), wi.numpy(), shape.U, shape.D, pad))
+    if shape.U <= 8:
+        plain, p0 = run(shape, inp, ker, path, tile="expand=0")
+        assert p0.describe()["tile"]["expand"] == 0
+        assert rel_l2(plain, got) <= 1e-5
+
+
+@pytest.mark.parametrize("path", ["tf32", "bf16"])
+def test_tap_expansion_auto_graph_and_host(path):
+    """Table 1's C = 3 stems take the expansion automatically; a captured
+    graph replays it (new inputs each replay) and conv_run_host (image
+    chunks: each chunk expands its own images) is bit-identical."""
+    from paper_2101_09808_b200.inputs import TABLE1
+    sh = Shape.strided(4, 32, 3, 68, 68, 3, 3, 1)
+    plan = conv.ConvPlan(*sh.as_tuple(), path=path, **sh.plan_kwargs())
+    assert plan.describe()["tile"]["expand"] == 1
+    for name in ("Y0", "R1"):
+        t = TABLE1[name]
+        assert conv.ConvPlan(*t.as_tuple(), path=path, **t.plan_kwargs()).describe()["tile"]["expand"] == 1
+    inp, ker = make_inputs(sh, seed=163)
+    i, k = inp.cuda(), ker.cuda()
+    out, ws = plan.new_output(), plan.new_workspace()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.run(i, k, out, ws)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.run(i, k, out, ws, stream=s)
+    for seed in (164, 165):
+        inp2, ker2 = make_inputs(sh, seed=seed)
+        i.copy_(inp2)
+        k.copy_(ker2)
+        g.replay()
+        torch.cuda.synchronize()
+        r2 = oracle.conv_eq1(ROUND[path](inp2.numpy()), ROUND[path](ker2.numpy()))
+        assert rel_l2(out.cpu().numpy(), r2) <= 1e-5
+    dev_out = out.clone()
+    dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device="cuda")
+    out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+    plan.run_host(inp2.pin_memory(), ker2.pin_memory(), out_h, dbuf)
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, dev_out.cpu())
 
 
 @pytest.mark.parametrize("path", PATHS)
