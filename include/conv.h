@@ -149,8 +149,14 @@ CONV_API conv_plan* conv_plan_create_padded_offline(int N, int K, int C, int Hin
 CONV_API conv_status conv_plan_set_path(conv_plan* plan, conv_path path);
 
 /* Force a tiling (tests / the selector-validation study).  `spec` is a
- * comma-separated key=value list; keys for the tensor paths: bn, stages;
- * for the SIMT path: tk, tw, kg, pw, tn, th, bc.  Unspecified keys keep the
+ * comma-separated key=value list; keys for the tensor paths: bn (32, 64,
+ * 128, 192, 256), cg (1 or 2: CTA pair), kbs (k-blocks per stage: 1-4, 6-9),
+ * stages, splits (split-K count, 1-16), fuse (0/1: in-kernel In transform),
+ * pre_c (fused prologue channels), expand (0/1: tiny-C tap expansion -- the
+ * transform writes each output pixel's R*S*C taps as channels and the
+ * kernel runs the equivalent 1x1 problem; automatic when C*elem <= 16 B and
+ * R*S >= 4, and then free of the TMA limits stated above); for the SIMT
+ * path: ver, tk, tw, kg, pw, tn, th, bc.  Unspecified keys keep the
  * selector's choice.  NULL or "" restores the selector's choice.
  * INVALID_ARGUMENT on a malformed spec, INFEASIBLE if the tile exceeds
  * SMEM/TMEM/register capacity (Eq. 4, per level). */
