@@ -112,7 +112,10 @@ inline Problem expanded_problem(const Problem& pb) {
 // stems (profiles/r01b/expand_ab.jsonl).
 inline bool expand_useful(const Problem& pb, bool bf16) {
     const int elem = bf16 ? 2 : 4;
-    return pb.C * elem <= 16 && pb.R * pb.S >= 4 && (int64_t)pb.R * pb.S * pb.C <= 1024;
+    // the expanded workspace holds R*S*C channels per OUTPUT pixel: bounded
+    // at 2 GiB so that large-kernel layers keep the plain im2col path
+    return pb.C * elem <= 16 && pb.R * pb.S >= 4 && (int64_t)pb.R * pb.S * pb.C <= 1024 &&
+           pb.M() * pb.R * pb.S * pb.C * elem <= ((int64_t)1 << 31);
 }
 
 TcLayout tc_layout(const Problem& p, bool bf16);
