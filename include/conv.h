@@ -167,8 +167,9 @@ CONV_API conv_status conv_plan_set_tile(conv_plan* plan, const char* spec);
  * Caller allocates, 256-B aligned. */
 CONV_API size_t conv_plan_workspace_bytes(const conv_plan* plan);
 
-/* Number of kernels one conv_run launches: 2 on every path (one layout
- * transform launch + the main kernel). */
+/* Number of kernels one conv_run launches: 2 (one layout transform launch +
+ * the main kernel), 3 for FP32 SIMT plans with a split-C reduction (the
+ * splits' partial outputs summed in split order by a third kernel). */
 CONV_API int conv_plan_num_kernels(const conv_plan* plan);
 
 /* Path the plan will run (never AUTO after create). */

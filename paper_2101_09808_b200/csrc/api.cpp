@@ -367,7 +367,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "stages") ft.stages = (int)v;
             else if (key == "cg") ft.cg = (int)v;
             else if (key == "kbs") ft.kbs = (int)v;
-            else if (key == "splits") ft.splits = (int)v;
+            else if (key == "splits") { ft.splits = (int)v; fs.splits = (int)v; mask |= 256; }
             else if (key == "fuse") ft.fuse = v ? 1 : 0;
             else if (key == "pre_c") ft.pre_c = (int)v;
             else if (key == "expand") ft.expand = v ? 1 : 0;
@@ -407,7 +407,8 @@ extern "C" size_t conv_plan_workspace_bytes(const conv_plan* p) { return p ? ws_
 
 extern "C" int conv_plan_num_kernels(const conv_plan* p) {
     if (!p) return -1;
-    return 2;   // tensor paths: repack (K1+K2 in one launch) + main; SIMT: pack + main
+    // tensor paths: layout transform + main; SIMT: pack + main (+ the split-C reduce)
+    return p->path == CONV_PATH_FP32_SIMT ? simt_num_kernels(p->simt) : 2;
 }
 
 extern "C" conv_path conv_plan_path(const conv_plan* p) { return p ? p->path : CONV_PATH_AUTO; }
@@ -434,9 +435,9 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     std::string tile;
     char t[256];
     if (p->path == CONV_PATH_FP32_SIMT) {
-        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"threads\":%d}",
+        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"splits\":%d,\"threads\":%d}",
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
-                 32 * p->simt.kg * p->simt.pw);
+                 p->simt.splits, 32 * p->simt.kg * p->simt.pw);
     } else {
         snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
                  128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
@@ -532,7 +533,7 @@ static conv_status run_impl(const conv_plan* p, const float* in, const float* ke
     if (cudaGetDevice(&dev) != cudaSuccess || dev != p->dev.ordinal)
         return fail(CONV_ERR_INVALID_ARGUMENT, "current device %d is not the plan's device %d", dev, p->dev.ordinal);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaEvent_t ev[3];
+    cudaEvent_t ev[4];                     // up to 3 kernels (split-C SIMT plans) + 1
     cudaEvent_t* evp = nullptr;
     if (events) {
         for (int i = 0; i <= nk; ++i) {

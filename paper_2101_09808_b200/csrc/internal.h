@@ -153,9 +153,12 @@ struct SimtTile {
     int bc = 8;   // input channels per smem stage
     int ver = 1;  // 1: stride-32 pixel slots (any S); 2: consecutive-pixel windows (S in {1,3},
                   //    TW in {4,8}, or TW = W in {7,14}: one thread per output row)
+    int splits = 1;   // split-C: CTAs per output tile along C (grid z), partial outputs summed
+                      //    in split order by a third kernel (deterministic per split count)
 };
 size_t simt_smem_bytes(const Problem& p, const SimtTile& t);
-size_t simt_ws_bytes(const Problem& p, const SimtTile& t);   // packed Ker
+size_t simt_ws_bytes(const Problem& p, const SimtTile& t);   // packed Ker (+ split-C partials)
+inline int simt_num_kernels(const SimtTile& t) { return t.splits > 1 ? 3 : 2; }
 bool simt_v2_ok(const Problem& p);
 bool simt_v2_tw_ok(const Problem& p, int tw);
 int simt2_pitch(const Problem& p, const SimtTile& t);

@@ -387,7 +387,9 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     ModelResult r;
     const int bko = t.kg * t.tk;
     const long ntile = (pb.N + t.tn - 1) / t.tn, htile = (pb.H + t.th - 1) / t.th, ktile = (pb.K + bko - 1) / bko;
-    r.tiles = ntile * htile * ktile;
+    const double nchunks_all = ceil((double)pb.C / t.bc);
+    const int splits = std::max(1, std::min(t.splits, (int)nchunks_all));
+    r.tiles = ntile * htile * ktile * splits;       // CTAs (split-C: one per split of a tile)
     const int threads = 32 * t.kg * t.pw;
     const size_t smem = simt_smem_bytes(pb, t);
     r.smem = smem;
@@ -429,7 +431,7 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // us, r01b simt_sweep2): charged 4x so that it is picked only where v2
     // cannot run (S not in {1, 3})
     const double issue_factor = (1.0 + over_cr / fma_cr) * (t.ver == 2 ? (row_mode ? 1.0 : 1.25) : 4.0);
-    const double chunks = ceil((double)pb.C / t.bc);
+    const double chunks = ceil(nchunks_all / splits);    // per CTA
     // one chunk: every thread's FFMAs, plus the cp.async copies (one per 4-B
     // element in v1/v2 In rows, ~6 instructions each, spread over the CTA)
     const double fma_chunk_cta = (double)threads * t.tk * t.tw * t.bc * pb.R * pb.S * issue_factor;
@@ -452,6 +454,8 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     r.dv_hbm = 4.0 * (pb.in_elems() + 2.0 * pb.ker_elems() + pb.out_elems());
     r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
     r.model_us = std::max({r.t_comp_us, r.t_l2_us / r.wave_eff, r.t_hbm_us}) + 2 * kLaunchUs;
+    if (splits > 1)   // the reduce kernel: a launch + S partial outputs read, Out written
+        r.model_us += kLaunchUs + (splits + 1.0) * 4.0 * pb.out_elems() / dev.bw_hbm * 1e6;
     return r;
 }
 
@@ -463,7 +467,8 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     const int bcs[3] = {4, 8, 16};
     const int tn_max = std::min(pb.N, 16);
     // v2 first when it can run and nothing is forced; v1 only if no v2 tile fits
-    const bool v2_first = simt_v2_ok(pb) && !(forced && forced_mask);
+    const bool tile_forced = forced && (forced_mask & ~256u);   // a tile key other than splits
+    const bool v2_first = simt_v2_ok(pb) && !tile_forced;
     const int vers[2] = {v2_first ? 2 : 1, v2_first ? 1 : 2};
     for (int ver : vers) {
     if (ver == 2 && !simt_v2_ok(pb)) continue;
@@ -506,9 +511,23 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         if (2L * tn * th * per_row < cap && !whole && !(forced && (forced_mask & 32))) continue;
         t.th = th;
         if (simt_smem_bytes(pb, t) > dev.smem_optin) continue;
-        if (t.kg > 1 && t.kg * t.tk >= 2 * pb.K && !forced) continue;  // mostly-empty k tile
-        ModelResult r = model_simt(pb, dev, t);
-        if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+        if (t.kg > 1 && t.kg * t.tk >= 2 * pb.K && !tile_forced) continue;  // mostly-empty k tile
+        // split-C while the grid is small (each CTA would otherwise walk the
+        // whole C reduction alone): S partial outputs, summed in split order
+        const long ctas = (long)((pb.N + tn - 1) / tn) * ((pb.H + th - 1) / th) * ((pb.K + kg * tk - 1) / (kg * tk));
+        const int nchunks = (pb.C + bc - 1) / bc;
+        // forced tiles: the forced split count (tile key splits), else none
+        static const int kSimtSplits[] = {1, 2, 4, 8, 16};
+        const int forced_sp[] = {forced ? ((forced_mask & 256) ? forced->splits : 1) : 1};
+        const int* cand = forced ? forced_sp : kSimtSplits;
+        const int ncand = forced ? 1 : 5;
+        for (int ci = 0; ci < ncand; ++ci) {
+            const int sp = cand[ci];
+            if (!forced && sp > 1 && (ctas * sp > 2L * dev.sms || sp > nchunks)) continue;
+            t.splits = sp;
+            ModelResult r = model_simt(pb, dev, t);
+            if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+        }
     }
     }
     if (!found) why = "no SIMT tile fits shared memory for this request";

@@ -223,6 +223,32 @@ def test_p10_whole_row_stages(path):
         assert rel_l2(got, r64) <= 1e-5
 
 
+@pytest.mark.parametrize("splits", [2, 3, 8])
+def test_simt_split_c(splits):
+    """FP32 SIMT split-C (a deep-C, small-output layer; v2 and v1 kernels):
+    relL2 <= 1e-5 against the oracle, bit-exact on the integer twin,
+    deterministic run to run, one extra (reduce) kernel."""
+    for sh, ver in ((Shape(N=1, K=64, C=256, H=7, W=7, R=3, S=3), 2), (Shape.strided(1, 40, 96, 15, 13, 3, 3, 2), 1)):
+        inp, ker = make_inputs(sh, seed=171)
+        got, plan = run(sh, inp, ker, "fp32_simt", tile=f"splits={splits}")
+        d = plan.describe()
+        assert d["tile"]["splits"] == splits and d["tile"]["ver"] == ver and plan.num_kernels == 3
+        ref = oracle.conv_eq1_strided(inp.numpy(), ker.numpy(), sh.U)
+        assert rel_l2(got, ref) <= 1e-5
+        again, _ = run(sh, inp, ker, "fp32_simt", tile=f"splits={splits}")
+        assert np.array_equal(got, again)
+        xi, wi = make_inputs(sh, seed=172, kind="int")
+        goti, _ = run(sh, xi, wi, "fp32_simt", tile=f"splits={splits}")
+        assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1_strided(xi.numpy(), wi.numpy(), sh.U))
+        # conv_run_events brackets all three kernels
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(plan.num_kernels + 1)]
+        out = plan.new_output()
+        plan.run_events(inp.cuda(), ker.cuda(), out, plan.new_workspace(), ev)
+        torch.cuda.synchronize()
+        assert all(ev[j].elapsed_time(ev[j + 1]) >= 0 for j in range(plan.num_kernels))
+        assert np.array_equal(out.cpu().numpy(), got)
+
+
 def test_p10_tile_invariance_simt():
     sh = Shape(N=2, K=32, C=24, H=12, W=12, R=3, S=3)
     inp, ker = make_inputs(sh, seed=8)
