@@ -247,6 +247,12 @@ def test_simt_split_c(splits):
         torch.cuda.synchronize()
         assert all(ev[j].elapsed_time(ev[j + 1]) >= 0 for j in range(plan.num_kernels))
         assert np.array_equal(out.cpu().numpy(), got)
+        # conv_run_host (pinned host buffers, the plan's workspace layout)
+        dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device="cuda")
+        out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+        plan.run_host(inp.pin_memory(), ker.pin_memory(), out_h, dbuf)
+        torch.cuda.synchronize()
+        assert np.array_equal(out_h.numpy(), got)
 
 
 def test_p10_tile_invariance_simt():
