@@ -146,11 +146,14 @@ __device__ __forceinline__ void ker_repack_cta(const float* __restrict__ ker, ty
     const float* src = ker + (k * g.C + c0) * g.RS;
     // the whole slice in flight at once: asynchronous global -> shared copies
     // (register round trips, even eight deep, cap a weight-heavy repack at
-    // ~2.5 TB/s)
+    // ~2.5 TB/s); 16-B copies when the slice is 16-B aligned (cc is a
+    // multiple of 4 channels)
     const int nld = cload * g.RS;
-    for (int i = tid; i < nld; i += NT) {
+    const bool v16 = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)nld * 4) & 15) == 0;
+    for (int i = v16 ? tid * 4 : tid; i < nld; i += v16 ? NT * 4 : NT) {
         const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sm + i));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + i) : "memory");
+        if (v16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + i) : "memory");
+        else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + i) : "memory");
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
@@ -419,7 +422,8 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
     g.RS = pb.R * pb.S;
     // channels per K1 CTA so that the staged slice is <= 32 KB (at least 1)
     g.cc = std::max(1, std::min(Cp, (int)(32768 / (4 * g.RS))));
-    if (g.cc > 1) g.cc &= ~1;   // even: bf16 channel pairs share a 4-B store
+    if (g.cc > 4) g.cc &= ~3;          // multiple of 4: 16-B aligned slices (and even for bf16 pairs)
+    else if (g.cc > 1) g.cc &= ~1;     // even: bf16 channel pairs share a 4-B store
     g.ker_chunks = (Cp + g.cc - 1) / g.cc;
     g.K = pb.K;
     // whole rows fit and there are many of them: several consecutive
