@@ -304,3 +304,43 @@ def test_production_build(lib):
     out -- it cost ~1.8 % on the headline."""
     v = lib.conv_version().decode()
     assert v.startswith("0.1.0 sm_100a") and "+trace" not in v
+
+
+def test_tap_expansion_and_split_c_offline(lib):
+    """Selector features on a described B200 (no device): the C = 3 stems of
+    Table 1 take the tiny-C tap expansion (workspace = the expanded 1x1
+    problem's NHWC In' + Ker'), deep-C small-output layers take split-K
+    (tensor) / split-C (SIMT, one more kernel), forced fused / split-K plans
+    never expand, and the batched headline layer is neither expanded nor
+    split."""
+    from paper_2101_09808_b200.inputs import CONFIGS, TABLE1
+    y0 = TABLE1["Y0"]
+    d = conv.ConvPlan(*y0.as_tuple(), path="bf16", offline_device=conv.B200, **y0.plan_kwargs()).describe()
+    t = d["tile"]
+    assert t["expand"] == 1 and t["fuse"] == 0 and t["splits"] == 1
+    cp = t["cp"]
+    assert cp >= y0.R * y0.S * y0.C and cp % 8 == 0
+    in_ws = y0.N * y0.H * y0.W * cp * 2
+    ker_ws = y0.K * cp * 2
+    al = lambda x: (x + 255) // 256 * 256
+    assert d["workspace_bytes"] == al(in_ws) + al(ker_ws)
+    r1 = TABLE1["R1"]
+    assert conv.ConvPlan(*r1.as_tuple(), path="tf32", offline_device=conv.B200,
+                         **r1.plan_kwargs()).describe()["tile"]["expand"] == 1
+    # forcing the fused transform or split-K keeps the plain path (a small
+    # tiny-C layer: one wave, a TMA-legal NCHW plane)
+    from paper_2101_09808_b200.inputs import Shape
+    small = Shape(N=1, K=32, C=3, H=8, W=8, R=3, S=3)
+    assert conv.ConvPlan(*small.as_tuple(), path="bf16", offline_device=conv.B200).describe()["tile"]["expand"] == 1
+    for spec, key, val in (("fuse=1", "fuse", 1), ("splits=2", "splits", 2)):
+        dd = conv.ConvPlan(*small.as_tuple(), path="bf16", tile=spec, offline_device=conv.B200).describe()
+        assert dd["tile"]["expand"] == 0 and dd["tile"][key] == val
+    m9 = TABLE1["M9"]
+    assert conv.ConvPlan(*m9.as_tuple(), path="bf16", offline_device=conv.B200,
+                         **m9.plan_kwargs()).describe()["tile"]["splits"] > 1
+    ps = conv.ConvPlan(*m9.as_tuple(), path="fp32_simt", offline_device=conv.B200, **m9.plan_kwargs())
+    assert ps.describe()["tile"]["splits"] > 1 and ps.num_kernels == 3
+    b = CONFIGS["batched"]
+    for path in ("bf16", "tf32", "fp32_simt"):
+        tb = conv.ConvPlan(*b.as_tuple(), path=path, offline_device=conv.B200).describe()["tile"]
+        assert tb.get("splits", 1) == 1 and tb.get("expand", 0) == 0
