@@ -31,6 +31,9 @@ for name in sys.argv[1].split(","):
         rows.append({"tile": d["tile"], "model_us": d["model"]["model_us"], "us": time_plan(p, i, k, flush, flush_rd, fo)})
     m = np.array([r["model_us"] for r in rows]); t = np.array([r["us"] for r in rows])
     a = [r for r in rows if r["tile"] == auto]
+    if not a:   # the AUTO tile (e.g. split-C) is not among the forced, unsplit tiles: time it
+        ap = conv.ConvPlan(*sh.as_tuple(), path="fp32_simt", **sh.plan_kwargs())
+        a = [{"tile": auto, "model_us": ap.describe()["model"]["model_us"], "us": time_plan(ap, i, k, flush, flush_rd, fo)}]
     print(json.dumps({"layer": name, "n": len(rows), "best_us": round(float(t.min()), 1), "best": rows[int(t.argmin())]["tile"],
                       "auto_us": round(a[0]["us"], 1) if a else None, "auto": auto, "rho": round(spearman(m, t), 2),
                       "rows": [{"tile": r["tile"], "model": round(r["model_us"], 1), "us": round(r["us"], 1)} for r in rows]}), flush=True)
