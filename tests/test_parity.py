@@ -867,3 +867,55 @@ def test_p10_k_shards_and_strided_shards_bit_identical(path):
                 got, _ = run(spec.local, li, lk, path, tile="splits=1")
                 ref = full[spec.start:spec.stop] if dim == "n" else full[:, spec.start:spec.stop]
                 assert np.array_equal(got, ref), (dim, world, r)
+
+
+def _random_shapes(n, seed):
+    """Seeded random general problems (stride, dilation, asymmetric padding),
+    small enough for the oracle: the selector then picks whatever it picks
+    (plain / tap-expanded / split plans, SIMT v1 / v2)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        R, S = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+        U, D = int(rng.choice([1, 1, 2, 3])), int(rng.choice([1, 1, 2]))
+        ph, pw = int(rng.integers(0, 3)), int(rng.integers(0, 3))
+        C = int(rng.choice([1, 2, 3, 5, 8, 16, 33, 64, 130]))
+        K = int(rng.choice([1, 7, 16, 32, 40, 64, 100, 256]))
+        N = int(rng.integers(1, 4))
+        Hin, Win = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+        if Hin + 2 * ph < D * (R - 1) + 1 or Win + 2 * pw < D * (S - 1) + 1:
+            continue
+        sh = Shape.strided(N, K, C, Hin, Win, R, S, U, D, ph, pw)
+        if sh.flops > 2e8:
+            continue
+        out.append(sh)
+    return out
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_random_general_shapes(path):
+    """40 seeded random problems on every path: bit-exact on the integer
+    twin, relL2 <= 1e-5 against the padded oracle on the path's rounded
+    inputs.  Shapes the path cannot run must fail as INFEASIBLE, never with
+    a wrong result."""
+    ran = 0
+    for i, sh in enumerate(_random_shapes(40, 2026)):
+        pad = (sh.ph, sh.pw)
+        try:
+            plan = conv.ConvPlan(*sh.as_tuple(), path=path, **sh.plan_kwargs())
+        except conv.ConvError as e:
+            assert e.status == conv.CONV_ERR_INFEASIBLE, (sh, e)
+            continue
+        xi, wi = make_inputs(sh, seed=200 + i, kind="int")
+        goti = plan.run(xi.cuda(), wi.cuda())
+        torch.cuda.synchronize()
+        refi = oracle.conv_eq1_padded(xi.numpy(), wi.numpy(), sh.U, sh.D, pad)
+        assert np.array_equal(goti.cpu().numpy().astype(np.float64), refi), (sh, plan.describe()["tile"])
+        inp, ker = make_inputs(sh, seed=300 + i)
+        got = plan.run(inp.cuda(), ker.cuda())
+        torch.cuda.synchronize()
+        ref = oracle.conv_eq1_padded(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), sh.U, sh.D, pad)
+        if np.linalg.norm(ref) > 0:
+            assert rel_l2(got.cpu().numpy(), ref) <= 1e-5, (sh, plan.describe()["tile"])
+        ran += 1
+    assert ran >= 30
