@@ -377,7 +377,10 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
                 const bool ok = c < p.C && n < p.N && ir < rows_ok;
                 const float* src = in + (((int64_t)n * p.C + c) * p.Hin + h0 + ir) * p.Win;
                 float* dst = in_s + cc * p.plane + (im * p.rows_in + ir) * p.pitch;
-                for (int col = lane; col < p.Win; col += 32) cp_async4(dst + col, ok ? src + col : in, ok);
+                if (p.vec4)      // 16-B aligned rows (same addressing as the slotted plan)
+                    for (int col = lane * 4; col < p.Win; col += 128) cp_async16(dst + col, ok ? src + col : in, ok);
+                else
+                    for (int col = lane; col < p.Win; col += 32) cp_async4(dst + col, ok ? src + col : in, ok);
             }
         }
         // Ker: contiguous slab of the packed tensor, channels >= C zero.

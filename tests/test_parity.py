@@ -266,6 +266,31 @@ def test_p10_tile_invariance_simt():
         assert np.array_equal(o, outs[0])
 
 
+@pytest.mark.parametrize("W", [62, 61], ids=["vec4", "scalar"])
+def test_simt_v2_row_loop_copy(W):
+    """v2 tiles whose In tile has more copy units than 4 per thread take the
+    per-row copy loop (16-B copies when Win % 4 == 0, else 4-B).  Against the
+    oracle, and bit-identical to a tile whose copies fit the slotted plan (the
+    per-output accumulation order does not depend on the tile)."""
+    sh = Shape(N=2, K=8, C=20, H=30, W=W, R=3, S=3)
+    inp, ker = make_inputs(sh, seed=12)
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    row = "ver=2,tk=4,tw=4,kg=1,pw=2,tn=1,th=4,bc=16"        # 64 threads, 16*6*(Win/4 or Win) units
+    slot = "ver=2,tk=4,tw=4,kg=2,pw=1,tn=1,th=2,bc=4"        # 64 threads, 4*4*16 = 256 units (vec4)
+    win = W + 2
+    units = lambda bc, rows: bc * rows * (win // 4 if win % 4 == 0 else win)
+    assert units(16, 6) > 4 * 64
+    got, _ = run(sh, inp, ker, "fp32_simt", tile=row)
+    assert rel_l2(got, ref) <= TOL["fp32_simt"]
+    if win % 4 == 0:
+        assert units(4, 4) <= 4 * 64
+        got_s, _ = run(sh, inp, ker, "fp32_simt", tile=slot)
+        assert np.array_equal(got, got_s)
+    xi, wi = make_inputs(sh, seed=12, kind="int")
+    goti, _ = run(sh, xi, wi, "fp32_simt", tile=row)
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
 @pytest.mark.parametrize("path", PATHS)
 def test_p10_batch_shards_bit_identical(path):
     """Shards over n equal the slices of the full result
