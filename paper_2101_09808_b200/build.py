@@ -25,6 +25,7 @@ def sources():
 
 def deps():
     return sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) \
+        + glob.glob(os.path.join(CSRC, "*.inc")) \
         + glob.glob(os.path.join(INCLUDE, "*.h"))
 
 

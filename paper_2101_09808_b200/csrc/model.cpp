@@ -383,6 +383,28 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
 // crossed into it, 2.78 -> 8.07 us per chunk) measured ~3x more.
 static const double kSimtSlowCopy = 72.0;
 
+// Registers per thread of the kernel instance a tile launches (simt.cu
+// dispatch_simt2 / dispatch_simt), as ptxas allocated them in the built
+// library (simt_regs.inc, scripts/gen_simt_regs.py; tests/test_abi.py checks
+// it against libconv.so).  The former estimate (TK*TW + TK + window + 24 for
+// v2) said 72 for v2 TK=8 TW=4 S=3 where ptxas gives 104-128: 2 CTAs per SM
+// modeled where 1 fits (ncu r01b Y0: occupancy limited by registers to 1).
+struct SimtRegs { int ver, tk, tw, kr, ks, splitc, regs; };
+static const SimtRegs kSimtRegs[] = {
+#include "simt_regs.inc"
+};
+
+static int simt_regs(const Problem& pb, const SimtTile& t, int win) {
+    const int sc = t.splits > 1 ? 1 : 0;
+    const int kr = (t.ver == 2 && pb.R == pb.S && (pb.S == 1 || pb.S == 3)) ? pb.R : 0;
+    const int ks = t.ver == 2 ? pb.S : 0;
+    for (const SimtRegs& e : kSimtRegs)
+        if (e.ver == t.ver && e.tk == t.tk && e.tw == t.tw && e.kr == kr && e.ks == ks && e.splitc == sc)
+            return e.regs;
+    // an instance the table does not list (not built): the old estimate
+    return std::min(128, t.tk * t.tw + t.tk + win + (t.ver == 2 ? 24 : 2 * t.tw + 28));
+}
+
 ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) {
     ModelResult r;
     const int bko = t.kg * t.tk;
@@ -396,7 +418,7 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // Register level (Sec. 6 microkernel analog): TK*TW accumulators + the
     // input window + TK kernel values + addressing; ptxas caps at 128.
     const int win = t.ver == 2 ? (t.tw + pb.S - 1 + 3) / 4 * 4 : t.tw;
-    const int regs = std::min(128, t.tk * t.tw + t.tk + win + (t.ver == 2 ? 24 : 2 * t.tw + 28));
+    const int regs = simt_regs(pb, t, win);
     const int by_regs = 65536 / (((regs + 7) / 8 * 8) * threads);
     const int by_smem = (int)(228 * 1024 / (smem + 1024));
     const int by_thr = 2048 / threads;
@@ -444,7 +466,9 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const double copy_chunk_cta = in_elems_chunk * copy_unit + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
     // a chunk cannot take less than one L2 round trip + two barriers
-    const double chunk_cyc = std::max((double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff), 2000.0);
+    const double issue_cyc = (double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff);
+    const double chunk_cyc = std::max(issue_cyc, 2000.0);
+    r.issue_cyc = waves * chunks * issue_cyc;
     r.t_comp_us = waves * chunks * chunk_cyc / clk * 1e6;
     // L2 -> SMEM: per CTA, every c-chunk loads the In halo tile and Ker slab
     // (Eq. 4's In and Ker footprints).
@@ -526,7 +550,13 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
             if (!forced && sp > 1 && (ctas * sp > 2L * dev.sms || sp > nchunks)) continue;
             t.splits = sp;
             ModelResult r = model_simt(pb, dev, t);
-            if (!found || r.model_us < best_r.model_us) { best = t; best_r = r; found = true; }
+            // near-ties (e.g. tiles at the chunk-latency floor): the tile that
+            // issues less (r01b Y23: TK 8 vs 4 both modeled 656 us, measured
+            // 1129 vs 1316 us)
+            const bool tie = found && fabs(r.model_us - best_r.model_us) <= 0.005 * best_r.model_us;
+            if (!found || (tie ? r.issue_cyc < best_r.issue_cyc : r.model_us < best_r.model_us)) {
+                best = t; best_r = r; found = true;
+            }
         }
     }
     }

@@ -17,6 +17,7 @@ struct ModelResult {
     double t_hbm_us = 0;
     double model_us = 0;     // modeled conv_run time
     size_t smem = 0;         // dynamic shared memory per CTA
+    double issue_cyc = 0;    // SIMT: per-SM issue cycles before the chunk-latency floor (tie-break)
 };
 
 // Tensor-path tile keys forced through conv_plan_set_tile (0 / -1: free).

@@ -306,6 +306,28 @@ def test_production_build(lib):
     assert v.startswith("0.1.0 sm_100a") and "+trace" not in v
 
 
+def test_simt_register_table_matches_library(lib):
+    """The SIMT model's registers per thread (csrc/simt_regs.inc) are those
+    ptxas gave every kernel instance of the built library (cuobjdump), and
+    every instance the dispatch can launch is listed."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "gen_simt_regs", os.path.join(os.path.dirname(os.path.dirname(__file__)), "scripts", "gen_simt_regs.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    if not os.path.exists(gen.CUOBJDUMP):
+        pytest.skip("cuobjdump not available")
+    rows = gen.table()
+    assert open(gen.INC).read() == gen.render(rows), "run scripts/gen_simt_regs.py after changing simt.cu"
+    keys = {r[:6] for r in rows}
+    for tk, tw in itertools.product((4, 8), range(1, 9)):               # v1: dispatch_simt
+        for sc in (0, 1):
+            assert (1, tk, tw, 0, 0, sc) in keys
+    v2 = [(tk, tw) for tk in (4, 8) for tw in (4, 8)] + [(4, 14), (4, 7)]  # v2: dispatch_simt2
+    for (tk, tw), (kr, ks), sc in itertools.product(v2, ((1, 1), (3, 3), (0, 1), (0, 3)), (0, 1)):
+        assert (2, tk, tw, kr, ks, sc) in keys
+
+
 def test_tap_expansion_and_split_c_offline(lib):
     """Selector features on a described B200 (no device): the C = 3 stems of
     Table 1 take the tiny-C tap expansion (workspace = the expanded 1x1
