@@ -382,6 +382,11 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
 // layer (~2.3x slower layer); the Table-1 study (simt_study2: Y18 bc 4 -> 8
 // crossed into it, 2.78 -> 8.07 us per chunk) measured ~3x more.
 static const double kSimtSlowCopy = 72.0;
+// The same loop with 16-B copies (rows 16-B aligned, Win % 4 == 0; r01b):
+// the Table-1 AUTO sweep with 24 vs 72 (two runs each, profiles/r01b/
+// t1_simt_slowcopy16.jsonl) 2695 -> 2681 us (Y0 57.4 -> 47.1, Y2, Y4 -4 %;
+// R7 +8 %, Y5 +3 %).
+static const double kSimtSlowCopy16 = 24.0;
 
 // Registers per thread of the kernel instance a tile launches (simt.cu
 // dispatch_simt2 / dispatch_simt), as ptxas allocated them in the built
@@ -462,7 +467,8 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // beyond that a per-row loop of 4-B copies runs (~2.3x slower layer
     // measured r01b)
     const double units_v2 = (double)t.bc * t.tn * pb.rows_span(t.th) * (pb.Win() % 4 == 0 ? pb.Win() / 4.0 : pb.Win());
-    const double copy_unit = (t.ver == 2 && units_v2 > 4.0 * threads) ? kSimtSlowCopy : 6.0;
+    const double copy_unit = (t.ver == 2 && units_v2 > 4.0 * threads)
+                                 ? (pb.Win() % 4 == 0 ? kSimtSlowCopy16 : kSimtSlowCopy) : 6.0;
     const double copy_chunk_cta = in_elems_chunk * copy_unit + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
     // a chunk cannot take less than one L2 round trip + two barriers
