@@ -439,13 +439,17 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // FFMA issue: 128 lanes/clk/SM at >= 8 resident warps (2 per SMSP hide
     // the LDS latency), proportionally less below.  Per (c, r) the register
     // tile costs: v1 S*(TW + TK/4 + 1) loads/address ops, v2 WIN/4 + S*TK/4 + 3.
-    // ncu r01: 8 resident warps/SM issue on only ~54% of cycles; ~16 are
-    // needed to cover the LDS/FFMA dependency latencies.
+    // ncu r01: 8 resident warps/SM issue on only ~54% of cycles; more are
+    // needed to cover the LDS/FFMA dependency latencies (12, fitted below).
     const double warps = (double)conc * threads / 32.0;
     // one resident CTA per SM cannot hide its own chunk barriers / copy
     // waits behind another CTA's FFMAs (measured r01b: 512-thread row-mode
     // tiles 1501 us vs 2 x 256-thread tiles 1321 us, same warps per SM)
-    const double eff = std::min(1.0, warps / 16.0) * (conc == 1 ? 0.88 : 1.0);
+    // Re-fitted once the model had the real registers per instance (r01b,
+    // Table-1 AUTO sweep, profiles/r01b/t1_simt_occupancy.jsonl): 12 warps
+    // and 0.7 vs the former 16 and 0.88: 2675 -> 2649 us (R1 -12 %, M3 / M5 /
+    // M6 -9..-11 %; Y2 +4 %); the batched layer's tile is unchanged.
+    const double eff = std::min(1.0, warps / 12.0) * (conc == 1 ? 0.7 : 1.0);
     const double fma_cr = (double)pb.S * t.tk * t.tw;
     const double over_cr = t.ver == 2 ? win / 4.0 + pb.S * t.tk / 4.0 + 3.0
                                       : pb.S * (t.tw + t.tk / 4.0 + 1.0);
