@@ -39,6 +39,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+from paper_2101_09808_b200.clocks import ClockSampler  # noqa: E402
 from paper_2101_09808_b200.inputs import CONFIGS, TABLE1, Shape, make_inputs  # noqa: E402
 
 METRIC = "conv TFLOP/s (2*N*K*H*W*C*R*S / time)"
@@ -63,67 +64,6 @@ def path_peak(path, peaks):
     # FP32 SIMT: 148 SMs x 128 FFMA lanes x 2 flop x max SM clock
     return 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, "alu", \
         "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (derived)"
-
-
-class ClockSampler:
-    """SM clock + throttle reasons sampled through NVML every ~1 ms from a
-    background thread while the timed region runs (nvidia-smi's 100-ms floor
-    is longer than a 50-step timed region)."""
-
-    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
-               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
-
-    def __init__(self, device_index: int):
-        self.samples = []
-        self.reasons = 0
-        self.max_mhz = None
-        self._stop = threading.Event()
-        self._t = None
-        self._h = None
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self._nv = pynvml
-            props = torch.cuda.get_device_properties(device_index)
-            try:
-                bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
-                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
-            except Exception:
-                self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
-        except Exception as e:  # pragma: no cover - no NVML
-            self._err = repr(e)
-
-    def start(self):
-        if self._h is None:
-            return
-        self._stop.clear()
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-
-    def _run(self):
-        nv = self._nv
-        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            nv.nvmlDeviceGetCurrentClocksThrottleReasons
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                self.reasons |= int(get_reasons(self._h))
-            except Exception:
-                pass
-            time.sleep(0.001)
-
-    def stop(self):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=2)
-
-    def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
-        reasons = sorted(n for bit, n in self.REASONS.items() if self.reasons & bit)
-        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.samples), "sm_mhz_min": min(self.samples)}
 
 
 def dist_env():

@@ -366,3 +366,34 @@ def test_tap_expansion_and_split_c_offline(lib):
     for path in ("bf16", "tf32", "fp32_simt"):
         tb = conv.ConvPlan(*b.as_tuple(), path=path, offline_device=conv.B200).describe()["tile"]
         assert tb.get("splits", 1) == 1 and tb.get("expand", 0) == 0
+
+
+# ---- measured peaks (K5 probes) ------------------------------------------------
+
+def test_peaks_inc_matches_measured_json():
+    """csrc/peaks_measured.inc (the selector's constants) is the one
+    scripts/measure_peaks.py generated from profiles/peaks_measured.json."""
+    import json
+    doc = json.load(open(os.path.join(ROOT, "profiles", "peaks_measured.json")))
+    inc = open(os.path.join(ROOT, "paper_2101_09808_b200", "csrc", "peaks_measured.inc")).read()
+    vals = {m.group(1): float(m.group(2)) for m in re.finditer(r"#define (CONV_\w+) ([0-9.e]+)", inc)}
+    sel = doc["selected"]
+    assert vals["CONV_PEAK_FP32"] == sel["peak_fp32_tflops"] * 1e12
+    assert vals["CONV_PEAK_TF32"] == sel["peak_tf32_tflops"] * 1e12
+    assert vals["CONV_BW_L2_SMEM"] == sel["bw_l2_smem_tbs"] * 1e12
+    assert sel["peak_fp32_tflops"] == doc["probes"]["ffma_fp32"]["value"]
+    assert sel["peak_tf32_tflops"] == doc["probes"]["cublas_tf32"]["value"]
+    # each probe reached a plausible fraction of the B200's nominal rates
+    assert 50 < sel["peak_fp32_tflops"] < 80            # 148 SM x 128 lanes x 2 x <= 1.965 GHz = 74.4
+    assert 500 < sel["peak_tf32_tflops"] < 1200         # nominal dense tf32 1.1 PF
+    assert 5 < sel["bw_l2_smem_tbs"] < 40
+
+
+def test_probe_library_exports():
+    from paper_2101_09808_b200 import build
+    build.build()
+    src = open(os.path.join(ROOT, "include", "conv_probes.h")).read()
+    declared = set(re.findall(r"CONV_PROBE_API[^;(]*?\b(probe_\w+)\s*\(", src))
+    out = os.popen(f"nm -D --defined-only {build.PROBES_LIB}").read()
+    exported = set(re.findall(r" T (probe_\w+)", out))
+    assert declared and declared <= exported
