@@ -46,24 +46,38 @@ METRIC = "conv TFLOP/s (2*N*K*H*W*C*R*S / time)"
 
 
 def load_peaks():
+    """Roofline denominators: HBM and the bf16 burst from the driver's
+    MEASURED_PEAKS.json; the TF32 and FP32 peaks from this pool's probes
+    (profiles/peaks_measured.json, scripts/measure_peaks.py)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return d, "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+        src = "measured"
+    else:
+        d = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
+        src = "fallback (B200_PROFILING.md)"
+    q = os.path.join(ROOT, "profiles", "peaks_measured.json")
+    if os.path.exists(q):
+        with open(q) as f:
+            d["probes"] = json.load(f)
+    return d, src
 
 
 def path_peak(path, peaks):
-    """Peak for the dominant kernel's arithmetic (TFLOP/s) and its bound."""
+    """(peak TFLOP/s, bound, note, measured?) for a path's dominant kernel."""
+    sel = peaks.get("probes", {}).get("selected", {})
     if path == "bf16":
-        return peaks["bf16_tflops"], "tensor", "measured cuBLAS bf16 burst (MEASURED_PEAKS.json)"
+        return peaks["bf16_tflops"], "tensor", "cuBLAS bf16 GEMM burst (MEASURED_PEAKS.json, driver)", True
     if path == "tf32":
-        # kind::tf32 issues at half the kind::f16 rate (nominal 1.1 vs 2.25 PF dense)
-        return peaks["bf16_tflops"] * 0.5, "tensor", "measured bf16 burst x 0.5 (nominal tf32/bf16 ratio)"
-    # FP32 SIMT: 148 SMs x 128 FFMA lanes x 2 flop x max SM clock (DESIGN.md)
+        if "peak_tf32_tflops" in sel:
+            return sel["peak_tf32_tflops"], "tensor", \
+                "cuBLAS TF32 GEMM 8192^3 burst on this pool (profiles/peaks_measured.json)", True
+        return peaks["bf16_tflops"] * 0.5, "tensor", "bf16 burst x 0.5 (nominal tf32/bf16 ratio; derived)", False
+    if "peak_fp32_tflops" in sel:
+        return sel["peak_fp32_tflops"], "alu", "FFMA probe burst on this pool (profiles/peaks_measured.json)", True
     return 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, "alu", \
-        "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (derived)"
+        "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (derived)", False
 
 
 def dist_env():
@@ -73,244 +87,370 @@ def dist_env():
     return rank, world, local
 
 
-def workload(args, world):
-    base = CONFIGS[args.config]
-    if args.scaling == "strong" and world > 1:
-        if base.N % world:
-            raise SystemExit(f"N={base.N} not divisible by {world}")
-        return base, Shape(base.N // world, base.K, base.C, base.H, base.W, base.R, base.S)
-    return base, base
+PATH_DTYPE = {"bf16": "bf16", "tf32": "tf32", "fp32_simt": "f32"}
+L2_NOTE = ("flushed before every timed step, outside the event pair: write of a 2x-L2 buffer, then a read of "
+           "another 2x-L2 buffer (dirty lines written back before the step: cold, clean L2)")
+
+
+def shard_spec(args, world: int, rank: int):
+    """(full workload, this rank's ShardSpec).  Strong scaling (default): the
+    workload's units are split across ranks with shard.shard (n, or k for
+    N = 1 layers; PAPER.md:375 -- non-reduction dims only).  Weak (opt-in):
+    every rank runs the whole workload on its own seed."""
+    from paper_2101_09808_b200.shard import ShardSpec, shard
+    full = CONFIGS[args.config]
+    if world == 1 or args.scaling == "weak":
+        return full, ShardSpec("n", world, rank, 0, full.N, full)
+    return full, shard(full, world, rank, args.shard)
+
+
+def rank_inputs(args, full, spec, rank):
+    """This rank's (In, Ker) on the host, plus the full tensors (strong)."""
+    from paper_2101_09808_b200.shard import local_inputs
+    if spec.world == 1 or args.scaling == "weak":
+        inp, ker = make_inputs(full, seed=rank)
+        return inp, ker, inp, ker
+    inp, ker = make_inputs(full, seed=0)
+    li, lk = local_inputs(spec, inp, ker)
+    return li, lk, inp, ker
+
+
+class GpuEngine:
+    """Runs plans of libconv.so on this rank's GPU and times them on the
+    launching stream with CUDA events."""
+    timer = "cuda events on the launching stream"
+
+    def __init__(self, local: int):
+        from paper_2101_09808_b200 import conv
+        self.conv = conv
+        torch.cuda.set_device(local)
+        self.dev = torch.device("cuda", local)
+        self.local = local
+        self.stream = torch.cuda.current_stream(self.dev)
+        l2 = getattr(torch.cuda.get_device_properties(self.dev), "L2_cache_size", 126 << 20)
+        n = max(2 * l2, 256 << 20) // 4
+        self.flush_w = torch.empty(n, dtype=torch.float32, device=self.dev)
+        self.flush_r = torch.ones(n, dtype=torch.float32, device=self.dev)
+        self.flush_o = torch.empty((), dtype=torch.float32, device=self.dev)
+
+    def l2_flush(self):
+        # write a buffer > L2 (evicts every line), then read another one so
+        # the dirty lines of the first pass are written back here, outside
+        # the timed events: each step starts with a cold, clean L2
+        self.flush_w.zero_()
+        torch.sum(self.flush_r, dim=0, out=self.flush_o)
+
+    def sync(self):
+        torch.cuda.synchronize(self.dev)
+
+    def to_device(self, t):
+        return t.pin_memory().to(self.dev)
+
+    def measure(self, path, sh, d_in, d_ker, args, barrier):
+        """K timed steps of one path (CUDA-graph replay of conv_run, L2
+        flushed before each, an event pair around each), then K steps with
+        events between the kernels (attribution).  NVML clocks sampled over
+        the soak and both passes."""
+        conv = self.conv
+        plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile=args.tile, **sh.plan_kwargs())
+        d_out = plan.new_output(self.dev)
+        ws = plan.new_workspace(self.dev)
+        st = self.stream
+        for _ in range(args.warmup):
+            self.l2_flush()
+            plan.run(d_in, d_ker, d_out, ws)
+        self.sync()
+        clocks = ClockSampler(self.local)
+        clocks.start()
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < args.soak:
+            for _ in range(20):
+                self.l2_flush()
+                plan.run(d_in, d_ker, d_out, ws)
+            self.sync()
+        graph = None
+        if not args.no_graph:
+            try:
+                cap = torch.cuda.Stream(device=self.dev)
+                cap.wait_stream(st)
+                with torch.cuda.stream(cap):
+                    plan.run(d_in, d_ker, d_out, ws, stream=cap)
+                cap.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=cap):
+                    plan.run(d_in, d_ker, d_out, ws, stream=cap)
+                self.sync()
+                graph.replay()
+                self.sync()
+            except Exception as e:  # pragma: no cover - fall back to stream launches
+                print(f"warning: CUDA graph capture failed ({e}); timing stream launches", file=sys.stderr)
+                graph = None
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        self.sync()
+        for a, b in ev:
+            self.l2_flush()                                     # outside the event pair
+            a.record(st)
+            if graph is not None:
+                graph.replay()
+            else:
+                plan.run(d_in, d_ker, d_out, ws)
+            b.record(st)
+        self.sync()
+        barrier()
+        step_ms = np.array([a.elapsed_time(b) for a, b in ev])
+        nk = plan.num_kernels
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
+        barrier()
+        self.sync()
+        for e in evs:
+            self.l2_flush()
+            plan.run_events(d_in, d_ker, d_out, ws, e)
+        self.sync()
+        barrier()
+        clocks.stop()
+        per_kernel = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(nk)] for e in evs])
+        return {"plan": plan, "desc": plan.describe(), "path": plan.path, "step_ms": step_ms,
+                "per_kernel": per_kernel, "clocks": clocks.summary(), "out": d_out, "nk": nk,
+                "launch": "cuda_graph replay of conv_run" if graph is not None else "stream launches"}
+
+    def e2e(self, res, sh, in_h, ker_h, args, barrier):
+        """conv_run_host with pinned host buffers: H2D + conv + D2H inside the
+        event pair, every step."""
+        plan = res["plan"]
+        in_h, ker_h = in_h.pin_memory(), ker_h.pin_memory()
+        dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device=self.dev)
+        out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+        for _ in range(max(1, args.warmup)):
+            plan.run_host(in_h, ker_h, out_h, dbuf)
+        self.sync()
+        ms = []
+        barrier()
+        for _ in range(args.steps):
+            self.l2_flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(self.stream)
+            plan.run_host(in_h, ker_h, out_h, dbuf)
+            b.record(self.stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        self.sync()
+        return float(np.mean(ms))
+
+    def reference_slab(self, res, full, spec, inp_full, ker_full):
+        """P10: the 1-GPU result of the full workload
+        with the shard plan's tile forced (same k order, same split count),
+        sliced to this rank's slab.  Returns (slice, how)."""
+        conv = self.conv
+        d = res["desc"]["tile"]
+        keys = ("ver", "tk", "tw", "kg", "pw", "tn", "th", "bc", "splits") if res["path"] == "fp32_simt" else \
+            ("bn", "cg", "kbs", "stages", "splits", "fuse", "expand")
+        spec_s = ",".join(f"{k}={d[k]}" for k in keys if k in d)
+        how = f"full-workload plan, tile forced to the shard's ({spec_s})"
+        try:
+            plan = conv.ConvPlan(*full.as_tuple(), path=res["path"], tile=spec_s, **full.plan_kwargs())
+        except conv.ConvError:
+            plan = conv.ConvPlan(*full.as_tuple(), path=res["path"], **full.plan_kwargs())
+            how = "full-workload plan, AUTO tile (the shard's tile is infeasible on the full workload)"
+        out = plan.run(inp_full.to(self.dev), ker_full.to(self.dev))
+        self.sync()
+        sl = out[spec.start:spec.stop] if spec.dim == "n" else out[:, spec.start:spec.stop]
+        return sl.contiguous(), how
+
+    def timed_gather(self, out, spec, args, barrier):
+        from paper_2101_09808_b200.shard import gather
+        full = gather(out, spec)                                   # warm-up
+        self.sync()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(self.stream)
+        for _ in range(args.steps):
+            full = gather(out, spec)
+        b.record(self.stream)
+        self.sync()
+        return full, a.elapsed_time(b) / args.steps
+
+
+def harness(args, rank: int, world: int, engine, dist_mod=None):
+    """One rank of the bench: shard (strong n / k, or weak replicas), time
+    every requested path with the engine, check the slab against the 1-GPU
+    result (P10), optionally all-gather Out (timed separately), reduce the
+    timings as the MAX over ranks, and (rank 0) build the JSON line.
+    ``dist_mod`` is torch.distributed with an initialised process group when
+    world > 1 (NCCL on the GPU box; gloo in the CPU harness test)."""
+    def barrier():
+        if world > 1:
+            dist_mod.barrier()
+
+    def reduce(vals, op):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64)
+        if getattr(engine, "dev", None) is not None and dist_mod.get_backend() == "nccl":
+            t = t.to(engine.dev)
+        dist_mod.all_reduce(t, op=op)
+        return t.cpu().tolist()
+
+    full, spec = shard_spec(args, world, rank)
+    sh = spec.local
+    li, lk, inp_full, ker_full = rank_inputs(args, full, spec, rank)
+    d_in, d_ker = engine.to_device(li), engine.to_device(lk)
+    paths = [args.path] + [p for p in (args.paths.split(",") if args.paths else []) if p and p != args.path]
+    results = {p: engine.measure(p, sh, d_in, d_ker, args, barrier) for p in paths}
+    head = results[args.path]
+    e2e_ms = None if args.no_e2e else engine.e2e(head, sh, li, lk, args, barrier)
+
+    p10 = None
+    if world > 1 and args.scaling == "strong" and not args.no_check:
+        ref, how = engine.reference_slab(head, full, spec, inp_full, ker_full)
+        same = bool(torch.equal(head["out"].cpu(), ref.cpu()))
+        ok = reduce([1.0 if same else 0.0], dist_mod.ReduceOp.MIN)[0] if world > 1 else float(same)
+        p10 = {"bit_identical_all_ranks": ok == 1.0, "ranks": world, "reference": how}
+    gathered, g_ms = None, None
+    if args.gather and world > 1:
+        gathered, g_ms = engine.timed_gather(head["out"], spec, args, barrier)
+
+    # max over ranks of every time
+    vec = []
+    for p in paths:
+        vec += [float(results[p]["step_ms"].mean()), float(results[p]["per_kernel"][:, -1].mean())]
+    vec += [e2e_ms or 0.0, g_ms or 0.0]
+    red = reduce(vec, dist_mod.ReduceOp.MAX if world > 1 else None)
+    for i, p in enumerate(paths):
+        results[p]["ms_max"], results[p]["main_ms_max"] = red[2 * i], red[2 * i + 1]
+    e2e_ms = red[-2] if e2e_ms is not None else None
+    g_ms = red[-1] if g_ms is not None else None
+
+    line = None
+    if rank == 0:
+        line = build_line(args, world, full, spec, paths, results, e2e_ms, g_ms, p10, engine)
+    return {"line": line, "gathered": gathered, "results": results}
+
+
+def path_record(args, world, full, spec, res, engine, peaks, peak_src):
+    """value, roofline and clocks of one path (rank 0's view, max over ranks)."""
+    sh = spec.local
+    ms, main_ms = res["ms_max"], res["main_ms_max"]
+    total_flops = full.flops * (world if args.scaling == "weak" else 1)
+    peak, bound, peak_note, measured = path_peak(res["path"], peaks)
+    achieved = sh.flops / (main_ms * 1e-3) / 1e12
+    per_kernel = res["per_kernel"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath) and world == 1:
+        with open(tpath) as f:
+            tkey = f"{args.config}:{res['path']}" + (":fuse" if res["desc"]["tile"].get("fuse") else "")
+            traffic = json.load(f).get(tkey)
+    roof_us = max(sh.flops / (peak * 1e12), sh.compulsory_bytes / (peaks["hbm_gbs"] * 1e9)) * 1e6
+    return {
+        "value": round(total_flops / (ms * 1e-3) / 1e12, 3),
+        "ms_per_step": round(ms, 5),
+        "dtype": PATH_DTYPE[res["path"]],
+        "path": res["path"],
+        "tile": res["desc"]["tile"],
+        "step_stats": step_stats(res["step_ms"]),
+        "roofline": {
+            "bound": bound,
+            "achieved": round(achieved, 2),
+            "peak": round(peak, 2),
+            "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": traffic,
+            "kernel": "conv_igemm_tcgen05" if res["path"] != "fp32_simt" else "conv_direct_simt",
+            "kernel_ms": round(main_ms, 5),
+            "peak_source": f"{peak_note}; {peak_src}",
+            "peak_measured": measured,
+            "step_roofline_us": round(roof_us, 3),
+            "step_frac": round(roof_us / (ms * 1e3), 4),
+            "kernel_share_of_step": round(float(per_kernel[:, -1].mean()) / float(per_kernel.sum(axis=1).mean()), 4),
+            "kernel_ms_each": [round(float(x), 5) for x in per_kernel.mean(axis=0)],
+            "timing": "kernel durations from a second K-step pass with events between the kernels",
+        },
+        "clocks": res["clocks"],
+        "kernels_per_step": res["nk"],
+        "launch": res["launch"],
+    }
+
+
+def build_line(args, world, full, spec, paths, results, e2e_ms, g_ms, p10, engine):
+    peaks, peak_src = load_peaks()
+    sh = spec.local
+    head = path_record(args, world, full, spec, results[args.path], engine, peaks, peak_src)
+    total_flops = full.flops * (world if args.scaling == "weak" else 1)
+    strong = world > 1 and args.scaling == "strong"
+    wl = f"{args.config}: N={full.N} K={full.K} C={full.C} out {full.H}x{full.W} R={full.R} S={full.S} " \
+         f"(stride 1, no pad, fp32 NCHW/KCRS)"
+    line = {
+        "metric": METRIC,
+        "value": head["value"],
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": head["ms_per_step"],
+        # rank 0's K timed steps: the paper's statistic is the mean (P:515);
+        # median and a normal 95% CI of the mean beside it (SURVEY 8(d))
+        "step_stats": head["step_stats"],
+        "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
+        "vs_baseline": None,
+        "dtype": head["dtype"],
+        "data": "synthetic (seeded uniform[-1,1), BASELINE.json configs)",
+        "config": {
+            "workload": wl if world == 1 or strong else wl + f", x{world} replicas (weak)",
+            "path": head["path"],
+            "tile": head["tile"],
+            "l2": L2_NOTE,
+            "clocks_window": "NVML samples every ~1 ms over the >= 1 s warm-up soak and both timed passes",
+            "parallelism": ("single GPU" if world == 1 else
+                            f"{spec.dim}-shard x{world}" if strong else f"replicas x{world}"),
+            "shard": {"dim": spec.dim, "world": world, "per_rank": f"{spec.dim}={spec.size}",
+                      "per_rank_shape": list(sh.as_tuple())},
+            "kernels_per_step": head["kernels_per_step"],
+            "launch": head["launch"],
+            "timer": engine.timer,
+        },
+        "roofline": head["roofline"],
+        "gpu_launches": head["kernels_per_step"] * args.steps,
+        "clocks": head["clocks"],
+    }
+    if e2e_ms is not None:
+        line["e2e"] = {
+            "value": round(total_flops / (e2e_ms * 1e-3) / 1e12, 3),
+            "unit": "TFLOP/s",
+            "ms_per_step": round(e2e_ms, 4),
+            "h2d_bytes_per_step": 4 * (sh.N * sh.C * sh.Hin * sh.Win + sh.K * sh.C * sh.R * sh.S) * world,
+            "d2h_bytes_per_step": 4 * sh.N * sh.K * sh.H * sh.W * world,
+            "api": "conv_run_host (C ABI, pinned host buffers)" + (", every rank its slab" if world > 1 else ""),
+        }
+    others = [p for p in paths if p != args.path]
+    if others:
+        line["paths"] = {p: path_record(args, world, full, spec, results[p], engine, peaks, peak_src) for p in others}
+    if p10 is not None:
+        line["p10"] = p10
+    if g_ms is not None:
+        line["gather"] = {"ms": round(g_ms, 4), "collective": "all_gather_into_tensor (shard.gather)",
+                          "bytes_recv_per_gpu": (world - 1) * 4 * sh.N * sh.K * sh.H * sh.W,
+                          "note": "after the timed region, not in value"}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(full, args)
+    return line
 
 
 def bench_ours(args):
     import torch.distributed as dist
-
-    from paper_2101_09808_b200 import conv
-
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    engine = GpuEngine(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    full, sh = workload(args, world)
-
-    # inputs: seeded on the CPU; weak scaling gives every rank its own batch
-    if args.scaling == "strong" and world > 1:
-        inp_all, ker = make_inputs(full, seed=0)
-        inp = inp_all[rank * sh.N:(rank + 1) * sh.N].contiguous()
-    else:
-        inp, ker = make_inputs(sh, seed=rank)
-    inp_h, ker_h = inp.pin_memory(), ker.pin_memory()
-    d_in, d_ker = inp_h.to(dev), ker_h.to(dev)
-    plan = conv.ConvPlan(*sh.as_tuple(), path=args.path, tile=args.tile)
-    desc = plan.describe()
-    d_out = plan.new_output(dev)
-    ws = plan.new_workspace(dev)
-    props = torch.cuda.get_device_properties(dev)
-    l2 = getattr(props, "L2_cache_size", 126 << 20)
-    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
-    flush_rd = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
-    flush_out = torch.empty((), dtype=torch.float32, device=dev)
-
-    def l2_flush():
-        # write a buffer > L2 (evicts every line), then read another one so
-        # the dirty lines of the first pass are written back here, outside
-        # the timed events: each step starts with a cold, clean L2
-        flush.zero_()
-        torch.sum(flush_rd, dim=0, out=flush_out)
-    stream = torch.cuda.current_stream(dev)
-    nk = plan.num_kernels
-
-    def barrier():
+        dist.init_process_group("nccl", device_id=engine.dev)
+    try:
+        out = harness(args, rank, world, engine, dist)
+        if rank == 0:
+            print(json.dumps(out["line"]), flush=True)
+    finally:
         if world > 1:
             dist.barrier()
-
-    # warm-up: W steps, then the same step until >= 1 s has passed so that the
-    # clocks settle under this load (the clock sampler runs from here on)
-    for _ in range(args.warmup):
-        l2_flush()
-        plan.run(d_in, d_ker, d_out, ws)
-    torch.cuda.synchronize(dev)
-    clocks = ClockSampler(local)
-    clocks.start()
-    t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < args.soak:
-        for _ in range(20):
-            l2_flush()
-            plan.run(d_in, d_ker, d_out, ws)
-        torch.cuda.synchronize(dev)
-
-    # (1) headline: K steps, each conv_run bracketed by its own event pair.
-    #     conv_run is replayed from a CUDA graph (its kernels back to back on
-    #     the device, the main kernel's programmatic dependent launch kept),
-    #     so host launch latency never shows up in the device timing.
-    graph = None
-    if not args.no_graph:
-        try:
-            cap = torch.cuda.Stream(device=dev)
-            cap.wait_stream(stream)
-            with torch.cuda.stream(cap):
-                plan.run(d_in, d_ker, d_out, ws)
-            cap.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=cap):
-                plan.run(d_in, d_ker, d_out, ws, stream=cap)
-            torch.cuda.synchronize(dev)
-            graph.replay()
-            torch.cuda.synchronize(dev)
-        except Exception as e:  # pragma: no cover - fall back to stream launches
-            print(f"warning: CUDA graph capture failed ({e}); timing stream launches", file=sys.stderr)
-            graph = None
-    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize(dev)
-    for i in range(args.steps):
-        l2_flush()                                      # L2 flush, outside the event pair
-        step_ev[i][0].record(stream)
-        if graph is not None:
-            graph.replay()
-        else:
-            plan.run(d_in, d_ker, d_out, ws)
-        step_ev[i][1].record(stream)
-    torch.cuda.synchronize(dev)
-    barrier()
-    step_ms = np.array([a.elapsed_time(b) for a, b in step_ev])
-    ms = float(step_ms.mean())
-
-    # (2) attribution: K more steps with events between the kernels (this
-    #     serialises them), giving each kernel's duration on its stream
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize(dev)
-    for i in range(args.steps):
-        l2_flush()
-        plan.run_events(d_in, d_ker, d_out, ws, evs[i])
-    torch.cuda.synchronize(dev)
-    barrier()
-    clocks.stop()
-    per_kernel = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(nk)] for e in evs])  # ms
-    main_ms = float(per_kernel[:, -1].mean())
-    attributed_ms = float(per_kernel.sum(axis=1).mean())
-
-    # end-to-end through the C ABI with pinned host buffers (H2D + conv + D2H)
-    dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device=dev)
-    out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
-    for _ in range(max(1, args.warmup)):
-        plan.run_host(inp_h, ker_h, out_h, dbuf)
-    torch.cuda.synchronize(dev)
-    e2e_ms = []
-    barrier()
-    for _ in range(args.steps):
-        l2_flush()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        plan.run_host(inp_h, ker_h, out_h, dbuf)
-        b.record(stream)
-        b.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
-    torch.cuda.synchronize(dev)
-    e2e = float(np.mean(e2e_ms))
-
-    gather = None
-    if args.gather and world > 1:
-        full_out = torch.empty((world,) + tuple(d_out.shape), dtype=torch.float32, device=dev)
-        dist.all_gather_into_tensor(full_out, d_out)      # warm-up
-        torch.cuda.synchronize(dev)
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.steps):
-            dist.all_gather_into_tensor(full_out, d_out)
-        b.record(stream)
-        torch.cuda.synchronize(dev)
-        g_ms = a.elapsed_time(b) / args.steps
-        gather = {"ms": g_ms, "bytes_recv_per_gpu": (world - 1) * d_out.numel() * 4}
-
-    # max over ranks
-    vals = torch.tensor([ms, main_ms, e2e, gather["ms"] if gather else 0.0], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, main_ms, e2e, g_ms = vals.tolist()
-    if gather:
-        gather["ms"] = g_ms
-
-    if rank == 0:
-        peaks, peak_src = load_peaks()
-        peak, bound, peak_note = path_peak(plan.path, peaks)
-        flops_rank = sh.flops
-        total_flops = flops_rank * world
-        value = total_flops / (ms * 1e-3) / 1e12
-        achieved = flops_rank / (main_ms * 1e-3) / 1e12
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath):
-            with open(tpath) as f:
-                tkey = f"{args.config}:{plan.path}" + (":fuse" if desc["tile"].get("fuse") else "")
-                traffic = json.load(f).get(tkey)
-        roof_us = max(sh.flops / (peak * 1e12), sh.compulsory_bytes / (peaks["hbm_gbs"] * 1e9)) * 1e6
-        line = {
-            "metric": METRIC,
-            "value": round(value, 3),
-            "unit": "TFLOP/s",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": round(ms, 5),
-            # rank 0's K timed steps: the paper's statistic is the mean;
-            # median and a normal 95% CI of the mean beside it
-            "step_stats": step_stats(step_ms),
-            "higher_is_better": True,
-            "scaling": "weak" if (args.scaling == "weak" or world == 1) else "strong",
-            "vs_baseline": None,
-            "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32_simt": "f32"}[plan.path],
-            "data": "synthetic (seeded uniform[-1,1), BASELINE.json configs)",
-            "config": {
-                "workload": f"{args.config}: N={sh.N} K={sh.K} C={sh.C} out {sh.H}x{sh.W} R={sh.R} S={sh.S} "
-                            f"(stride 1, no pad, fp32 NCHW/KCRS){' per rank' if world > 1 else ''}",
-                "path": plan.path,
-                "tile": desc["tile"],
-                "l2": "flushed before every timed step, outside the event pair: write of a 2x-L2 buffer, then a read "
-                      "of another 2x-L2 buffer (dirty lines written back before the step: cold, clean L2)",
-                "clocks_window": "NVML samples every ~1 ms over the >= 1 s warm-up soak and both timed passes",
-                "parallelism": f"n-shard x{world}" if world > 1 else "single GPU",
-                "kernels_per_step": nk,
-                "launch": "cuda_graph replay of conv_run" if graph is not None else "stream launches",
-            },
-            "roofline": {
-                "bound": bound,
-                "achieved": round(achieved, 2),
-                "peak": round(peak, 1),
-                "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4),
-                "traffic": traffic,
-                "kernel": "conv_igemm_tcgen05" if plan.path != "fp32_simt" else "conv_direct_simt",
-                "kernel_ms": round(main_ms, 5),
-                "peak_source": f"{peak_note}; {peak_src}",
-                "step_roofline_us": round(roof_us, 3),
-                "step_frac": round(roof_us / (ms * 1e3), 4),
-                "kernel_share_of_step": round(main_ms / attributed_ms, 4),
-                "kernel_ms_each": [round(float(x), 5) for x in per_kernel.mean(axis=0)],
-                "timing": "kernel durations from a second K-step pass with events between the kernels",
-            },
-            "e2e": {
-                "value": round(total_flops / (e2e * 1e-3) / 1e12, 3),
-                "unit": "TFLOP/s",
-                "ms_per_step": round(e2e, 4),
-                "h2d_bytes_per_step": 4 * (sh.N * sh.C * sh.Hin * sh.Win + sh.K * sh.C * sh.R * sh.S),
-                "d2h_bytes_per_step": 4 * sh.N * sh.K * sh.H * sh.W,
-                "api": "conv_run_host (C ABI, pinned host buffers)",
-            },
-            "gpu_launches": nk * args.steps,
-            "clocks": clocks.summary(),
-        }
-        if gather:
-            line["gather"] = gather
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(full, args)
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+            dist.destroy_process_group()
 
 
 def oracle_sample_time(sh: Shape, n_img: int, threads: int):
@@ -450,7 +590,7 @@ def bench_table1(args):
                 plan.run_events(d_in, d_ker, out, ws, kev[i])
             torch.cuda.synchronize(dev)
             kern_us = [round(float(np.mean([e[j].elapsed_time(e[j + 1]) for e in kev])) * 1e3, 2) for j in range(nk)]
-            peak, bound, _ = path_peak(plan.path, peaks)
+            peak, bound, _, _ = path_peak(plan.path, peaks)
             roof_us = max(sh.flops / (peak * 1e12), 4.0 * (sh.N * sh.C * sh.Hin * sh.Win + sh.K * sh.C * sh.R * sh.S +
                                                            sh.N * sh.K * sh.H * sh.W) / (peaks["hbm_gbs"] * 1e9)) * 1e6
             d = plan.describe()
@@ -462,14 +602,44 @@ def bench_table1(args):
                 "peak_source": peak_src}), flush=True)
 
 
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args, argv) -> int:
+    """``--gpus N`` without torchrun: start N ranks (one process per GPU) with
+    torch.distributed.run on this node and return its exit code.  Fails
+    (rc 2) if fewer than N GPUs are visible."""
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        print(f"error: --gpus {args.gpus} but only {n} CUDA device(s) visible", file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--path", default="bf16", choices=["auto", "fp32_simt", "tf32", "bf16", "all"])
+    ap.add_argument("--path", default="fp32_simt", choices=["auto", "fp32_simt", "tf32", "bf16", "all"],
+                    help="the headline path (default: FP32, the paper's precision, PAPER.md:369)")
+    ap.add_argument("--paths", default="tf32,bf16",
+                    help="further paths measured in the same process, reported under 'paths' ('' for none)")
+    ap.add_argument("--shard", default="auto", choices=["auto", "n", "k"],
+                    help="strong scaling: shard the batch n (auto for N >= ranks) or output channels k (N = 1)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the multi-rank P10 slab check")
     ap.add_argument("--config", default="batched", choices=list(CONFIGS))
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): the workload's units split across ranks; weak: a replica per rank")
     ap.add_argument("--gather", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -483,6 +653,14 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus and args.impl == "ours":
+        print(f"error: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours" and not args.sweep:
+        sys.exit(launch_ranks(args, sys.argv[1:]))
     if args.sweep:
         bench_table1(args)
     elif args.impl == "reference":
