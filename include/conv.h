@@ -47,7 +47,13 @@
  *     device, conv_plan_create fails with CONV_ERR_UNSUPPORTED_DEVICE.
  *   - Thread safety: a plan is immutable after create / set_path / set_tile.
  *     conv_run may be called concurrently on one plan from several host
- *     threads / streams if each call has its own workspace.
+ *     threads / streams if each call has its own workspace.  Plans whose main
+ *     kernel needs all of its CTAs resident at once (describe: "fuse":1 or
+ *     "splits">1) are serialised per device by the library: such a conv_run
+ *     waits on the device for the previous one's main kernel (an internal
+ *     event), so two of them never share the SMs.  Inside CUDA-graph capture
+ *     that wait is not inserted; do not replay two graphs holding such plans
+ *     concurrently on one device.
  */
 #ifndef CONV_H_
 #define CONV_H_
@@ -75,10 +81,15 @@ typedef enum {
 } conv_status;
 
 typedef enum {
-    CONV_PATH_AUTO = 0,      /* selector picks among the three below */
+    CONV_PATH_AUTO = 0,      /* the faster (modeled) of the two FP32-precision paths: FP32_SIMT, FP32_TC */
     CONV_PATH_FP32_SIMT = 1, /* FP32 FFMA direct convolution on native NCHW In (Ker packed) */
     CONV_PATH_TF32 = 2,      /* tcgen05 implicit GEMM, inputs rounded to TF32 (RNA), fp32 accumulate */
-    CONV_PATH_BF16 = 3       /* tcgen05 implicit GEMM, inputs rounded to BF16 (RNE), fp32 accumulate */
+    CONV_PATH_BF16 = 3,      /* tcgen05 implicit GEMM, inputs rounded to BF16 (RNE), fp32 accumulate */
+    CONV_PATH_FP32_TC = 4    /* FP32-accurate on the tensor cores: every fp32 input split EXACTLY into three
+                                bf16 pieces x = x0 + x1 + x2 (RNE remainders); the products x_i * y_j with
+                                i + j <= 2 (6 pairs; dropped terms < 3 * 2^-24 |x*y|), or all 9 with the tile
+                                key split=9 (every product exact), accumulated in fp32 by the tcgen05 bf16
+                                kernel over npairs x the channels (reading R15) */
 } conv_path;
 
 /* ---- plans ------------------------------------------------------------- */

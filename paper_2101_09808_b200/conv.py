@@ -23,7 +23,7 @@ CONV_ERR_INFEASIBLE = 2
 CONV_ERR_CUDA = 3
 CONV_ERR_UNSUPPORTED_DEVICE = 4
 
-PATHS = {"auto": 0, "fp32_simt": 1, "tf32": 2, "bf16": 3}
+PATHS = {"auto": 0, "fp32_simt": 1, "tf32": 2, "bf16": 3, "fp32_tc": 4}
 PATH_NAMES = {v: k for k, v in PATHS.items()}
 
 # Every symbol include/conv.h declares (tests check the library exports them).
@@ -164,6 +164,12 @@ class ConvPlan:
         if not h:
             raise ConvError(lib.conv_last_status(), last_error())
         self._h = ctypes.c_void_p(h)
+        # the device the library bound the plan to (the current one); runs
+        # must pass tensors on it (checked in run / run_events)
+        self.device_index = None
+        if offline_device is None:
+            import torch
+            self.device_index = torch.cuda.current_device()
         self._shapes_cache = tuple(self._shapes_sizes())
         if path != "auto":
             self.set_path(path)
@@ -221,6 +227,8 @@ class ConvPlan:
             if not (t.is_cuda and t.dtype is _f32() and t.shape == s and t.is_contiguous()):
                 raise ValueError(f"{name} must be a contiguous float32 CUDA tensor of shape {tuple(s)}, "
                                  f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+            if t.device.index != self.device_index:
+                raise ValueError(f"{name} is on {t.device} but the plan was created on cuda:{self.device_index}")
 
     def new_workspace(self, device=None):
         import torch
@@ -233,15 +241,21 @@ class ConvPlan:
 
     def run(self, inp, ker, out=None, workspace=None, stream=None):
         """Out = Eq. 1 (In, Ker), asynchronous on ``stream`` (default: torch's
-        current stream).  Returns ``out``."""
-        if out is None:
-            out = self.new_output(inp.device)
-        self._check_tensors(inp, ker, out)
-        if workspace is None and self.workspace_bytes:
-            workspace = self.new_workspace(inp.device)
-        ws = workspace.data_ptr() if workspace is not None and self.workspace_bytes else None
-        _check(self._lib.conv_run(self._h, inp.data_ptr(), ker.data_ptr(), out.data_ptr(), ws,
-                                  _stream_handle(stream)))
+        current stream).  Returns ``out``.  Buffers this call allocates (out,
+        workspace) are allocated on ``stream`` (torch's caching allocator
+        then never hands them to other work while the kernels run)."""
+        import torch
+        with torch.cuda.device(inp.device):
+            alloc = torch.cuda.stream(stream) if stream is not None else _nullcontext()
+            with alloc:
+                if out is None:
+                    out = self.new_output(inp.device)
+                if workspace is None and self.workspace_bytes:
+                    workspace = self.new_workspace(inp.device)
+            self._check_tensors(inp, ker, out)
+            ws = workspace.data_ptr() if workspace is not None and self.workspace_bytes else None
+            _check(self._lib.conv_run(self._h, inp.data_ptr(), ker.data_ptr(), out.data_ptr(), ws,
+                                      _stream_handle(stream)))
         return out
 
     def run_events(self, inp, ker, out, workspace, events: Sequence, stream=None):
@@ -273,6 +287,14 @@ class ConvPlan:
                                        _stream_handle(stream)))
 
 
+class _nullcontext:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
+
 def _f32():
     import torch
     return torch.float32
@@ -291,7 +313,9 @@ def conv2d(inp, ker, path: str = "auto", out=None, stream=None):
     key = (N, K, C, Hin - R + 1, Win - S + 1, R, S, path, inp.device.index)
     plan = _plan_cache.get(key)
     if plan is None:
-        plan = ConvPlan(*key[:7], path=path)
+        import torch
+        with torch.cuda.device(inp.device):          # the plan binds the current device
+            plan = ConvPlan(*key[:7], path=path)
         _plan_cache[key] = plan
     return plan.run(inp, ker, out=out, stream=stream)
 

@@ -51,6 +51,8 @@ struct conv_plan {
     Problem pb;
     bool expand = false;    // tensor paths: run expanded_problem(pb) after the tap expansion
     Problem pe{};
+    int split = 0;          // FP32_TC: piece pairs (6 or 9); the kernel runs split_problem(pb, split)
+    Problem ps{};
     Device dev;
     conv_path requested = CONV_PATH_AUTO;
     conv_path path = CONV_PATH_AUTO;
@@ -103,7 +105,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 static size_t ws_bytes(const conv_plan* p) {
     if (p->path == CONV_PATH_FP32_SIMT) return align256(simt_ws_bytes(p->pb, p->simt));
     // aux region: the fused transform's flags, or split-K's counters + partials
-    const Problem& kp = p->expand ? p->pe : p->pb;          // the problem the tensor kernel runs
+    const Problem& kp = p->split ? p->ps : (p->expand ? p->pe : p->pb);   // the problem the tensor kernel runs
     const size_t aux = p->tc.fuse ? p->tcl.flag_bytes : tc_split_bytes(kp, p->tcl, p->tc);
     return align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes) + align256(aux);
 }
@@ -132,6 +134,26 @@ static bool select_tensor(conv_plan* p, bool bf16, TcTile& tt, ModelResult& rt, 
     return true;
 }
 
+// FP32_TC selection: the bf16 kernel's tiles on split_problem(pb, npairs)
+// (no fused transform, no tap expansion).  The model charged the layout
+// transform the fp32 read of npairs*Cq input channels; the split launch reads
+// the C real ones once.
+static bool select_split(conv_plan* p, TcTile& tt, ModelResult& rt, Problem& ps, int& np, std::string& why) {
+    np = p->force_tc.split ? p->force_tc.split : 6;
+    ps = split_problem(p->pb, np);
+    TcForce f = p->force_tc;
+    if (f.fuse == 1) { why = "FP32_TC plans run without the fused transform"; return false; }
+    f.fuse = 0;
+    f.expand = 0;
+    if (!select_tc(ps, p->dev, true, tt, rt, f, why)) return false;
+    const double over = 4.0 * ((double)ps.in_elems() - (double)p->pb.in_elems()) +
+                        4.0 * ((double)ps.ker_elems() - (double)p->pb.ker_elems());
+    rt.dv_hbm -= over;
+    rt.t_hbm_us = rt.dv_hbm / p->dev.bw_hbm * 1e6;
+    rt.model_us -= over / (0.8 * p->dev.bw_hbm) * 1e6;
+    return true;
+}
+
 // Re-run the selector for the requested path (Alg. 1:
 // every candidate evaluated, minimum modeled cost wins).
 static conv_status select(conv_plan* p) {
@@ -142,11 +164,20 @@ static conv_status select(conv_plan* p) {
     SimtTile st;
     ModelResult rs;
     const SimtTile* fs = p->force_simt_mask ? &p->force_simt : nullptr;
+    p->split = 0;
     switch (p->requested) {
         case CONV_PATH_FP32_SIMT:
             if (!select_simt(pb, p->dev, st, rs, fs, p->force_simt_mask, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             p->simt = st; p->model = rs; p->path = CONV_PATH_FP32_SIMT;
             break;
+        case CONV_PATH_FP32_TC: {
+            Problem ps{};
+            int np = 0;
+            if (!select_split(p, tt, rt, ps, np, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            p->tc = tt; p->model = rt; p->path = CONV_PATH_FP32_TC; p->expand = false; p->split = np; p->ps = ps;
+            p->tcl = tc_layout(ps, true);
+            break;
+        }
         case CONV_PATH_TF32:
         case CONV_PATH_BF16: {
             const bool bf16 = p->requested == CONV_PATH_BF16;
@@ -159,16 +190,19 @@ static conv_status select(conv_plan* p) {
         }
         case CONV_PATH_AUTO:
         default: {
-            // AUTO keeps fp32 inputs or TF32 products (the precision of the
-            // paper's fp32 method); BF16 only when requested.
+            // AUTO returns results at the paper's precision (fp32, PAPER.md:369;
+            // DESIGN.md reading R6): the faster of the FP32 SIMT path and the
+            // FP32-accurate tensor path by modeled time.  TF32 / BF16 inputs
+            // (relL2 ~3e-4 / ~2e-3) only when requested.
             const bool ok_s = select_simt(pb, p->dev, st, rs, fs, p->force_simt_mask, why);
-            bool ex = false;
-            Problem pe{};
-            const bool ok_t = select_tensor(p, false, tt, rt, ex, pe, why);
-            if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
+            Problem ps{};
+            int np = 0;
+            std::string why_t;
+            const bool ok_t = select_split(p, tt, rt, ps, np, why_t);
+            if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s; %s", why.c_str(), why_t.c_str());
             if (ok_t && (!ok_s || rt.model_us < rs.model_us)) {
-                p->tc = tt; p->model = rt; p->path = CONV_PATH_TF32; p->expand = ex; p->pe = pe;
-                p->tcl = tc_layout(ex ? pe : pb, false);
+                p->tc = tt; p->model = rt; p->path = CONV_PATH_FP32_TC; p->expand = false; p->split = np; p->ps = ps;
+                p->tcl = tc_layout(ps, true);
             } else {
                 p->simt = st; p->model = rs; p->path = CONV_PATH_FP32_SIMT;
             }
@@ -331,7 +365,7 @@ extern "C" conv_plan* conv_plan_create_padded_offline(int N, int K, int C, int H
 
 extern "C" conv_status conv_plan_set_path(conv_plan* p, conv_path path) {
     if (!p) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
-    if (path < CONV_PATH_AUTO || path > CONV_PATH_BF16) return fail(CONV_ERR_INVALID_ARGUMENT, "unknown path %d", (int)path);
+    if (path < CONV_PATH_AUTO || path > CONV_PATH_FP32_TC) return fail(CONV_ERR_INVALID_ARGUMENT, "unknown path %d", (int)path);
     const conv_path old = p->requested;
     p->requested = path;
     conv_status s = select(p);
@@ -371,6 +405,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "fuse") ft.fuse = v ? 1 : 0;
             else if (key == "pre_c") ft.pre_c = (int)v;
             else if (key == "expand") ft.expand = v ? 1 : 0;
+            else if (key == "split") ft.split = (int)v;
             else if (key == "tk") { fs.tk = (int)v; mask |= 1; }
             else if (key == "tw") { fs.tw = (int)v; mask |= 2; }
             else if (key == "kg") { fs.kg = (int)v; mask |= 4; }
@@ -386,6 +421,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
         if (ft.kbs && (ft.kbs > 9 || ft.kbs == 5))
             return fail(CONV_ERR_INFEASIBLE, "kbs must be 1, 2, 3, 4, 6, 7, 8 or 9");
         if (ft.cg && ft.cg != 1 && ft.cg != 2) return fail(CONV_ERR_INFEASIBLE, "cg must be 1 or 2");
+        if (ft.split && ft.split != 6 && ft.split != 9) return fail(CONV_ERR_INFEASIBLE, "split must be 6 or 9");
         if (ft.splits > 16) return fail(CONV_ERR_INFEASIBLE, "splits must be <= 16");
         if (ft.splits > 1 && ft.fuse == 1) return fail(CONV_ERR_INFEASIBLE, "split-K needs fuse=0");
     }
@@ -420,6 +456,7 @@ static const char* path_name(conv_path p) {
         case CONV_PATH_FP32_SIMT: return "fp32_simt";
         case CONV_PATH_TF32: return "tf32";
         case CONV_PATH_BF16: return "bf16";
+        case CONV_PATH_FP32_TC: return "fp32_tc";
         default: return "auto";
     }
 }
@@ -428,8 +465,11 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     if (!p) return -1;
     const Problem& pb = p->pb;
     const ModelResult& m = p->model;
+    // FP32_TC: the bf16 tensor peak shared by the split's piece pairs
     const double peak = p->path == CONV_PATH_FP32_SIMT ? p->dev.peak_fp32
-                        : (p->path == CONV_PATH_BF16 ? p->dev.peak_bf16 : p->dev.peak_tf32);
+                        : p->path == CONV_PATH_BF16  ? p->dev.peak_bf16
+                        : p->path == CONV_PATH_FP32_TC ? p->dev.peak_bf16 / p->split
+                                                       : p->dev.peak_tf32;
     const double comp_bytes = 4.0 * (pb.in_elems() + pb.ker_elems() + pb.out_elems());
     const double roof_us = std::max(pb.flops() / peak, comp_bytes / p->dev.bw_hbm) * 1e6;
     std::string tile;
@@ -439,8 +479,8 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
                  p->simt.splits, 32 * p->simt.kg * p->simt.pw);
     } else {
-        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
-                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
+        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"split\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
+                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->split, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
                  p->tc.fuse ? std::min(p->tc.pre_c, p->tcl.Cp) : 0,
                  p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
     }
@@ -492,7 +532,10 @@ static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0
         void* ker_ws = wsb + align256(p->tcl.in_ws_bytes);
         void* flag_ws = (p->tc.fuse || p->tc.splits > 1) ? wsb + align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes)
                                                          : nullptr;
-        if (p->expand) {
+        if (p->split) {
+            e = tc_run(split_problem(sub, p->split), p->tcl, p->tc, true, in, ker, out, in_ws, ker_ws, flag_ws, st,
+                       p->dev.sms, evp, err, &sub, p->split);
+        } else if (p->expand) {
             const Problem sub_e = expanded_problem(sub);
             e = tc_run(sub_e, p->tcl, p->tc, p->path == CONV_PATH_BF16, in, ker, out, in_ws, ker_ws, flag_ws, st,
                        p->dev.sms, evp, err, &sub);

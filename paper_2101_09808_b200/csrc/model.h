@@ -25,6 +25,7 @@ struct TcForce {
     int bn = 0, stages = 0, cg = 0, kbs = 0, splits = 0;
     int fuse = -1, pre_c = -1;
     int expand = -1;        // tiny-C tap expansion: -1 auto (expand_useful), 0 off, 1 on
+    int split = 0;          // FP32_TC piece pairs: 0 default (6), 6 or 9
 };
 
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t);

@@ -482,13 +482,9 @@ cudaError_t launch_repack(const Problem& pb, int Cp, bool bf16, const float* in,
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t persist = std::min<int64_t>(g.n_tiles, (int64_t)sms * 3);
         const size_t smem = 1024 + 65536 + 64;
-        static bool attr_set[2] = {false, false};
-        if (!attr_set[bf16]) {
-            cudaError_t e = bf16 ? cudaFuncSetAttribute(repack_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                                 : cudaFuncSetAttribute(repack_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            attr_set[bf16] = true;
-        }
+        static SmemOptIn attr_set[2];
+        cudaError_t e = bf16 ? attr_set[1].ensure(repack_tma<true>, smem) : attr_set[0].ensure(repack_tma<false>, smem);
+        if (e != cudaSuccess) return e;
         if (ev) cudaEventRecord(ev[0], st);
         const unsigned grid = (unsigned)(g.n_ker + persist);
         g.pdl_from = (int)std::max<int64_t>(0, (int64_t)grid - (int64_t)sms * 3);
@@ -643,6 +639,174 @@ cudaError_t launch_expand(const Problem& pb, int Cp, bool bf16, const float* in,
         expand_taps<true><<<grid, 256, smem, st>>>(in, ker, (__nv_bfloat16*)in_ws, (__nv_bfloat16*)ker_ws, g);
     else
         expand_taps<false><<<grid, 256, smem, st>>>(in, ker, (float*)in_ws, (float*)ker_ws, g);
+    if (ev) cudaEventRecord(ev[1], st);
+    return cudaGetLastError();
+}
+
+// ---- FP32-accurate tensor path: exact bf16 splitting (CONV_PATH_FP32_TC) ----
+// Every fp32 value x splits EXACTLY into three bf16 pieces, each the
+// round-to-nearest-even bf16 of the remainder so far:
+//   x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1) = x - x0 - x1
+// (each subtraction is exact: a value and its nearest bf16 are within a
+// factor 2; a binary32 significand is 24 bits, each piece takes 8 of them,
+// so the third remainder fits a bf16 exactly).  x*y = sum_{i,j} x_i*y_j, and
+// every x_i*y_j is exact in fp32 (8 x 8 significant bits).  The path computes
+// the pairs (i, j) of split_pairs() -- i + j <= 2 (6 pairs; the three dropped
+// are below 3 * 2^-24 |x*y|) or all 9 (exact products) -- as ONE bf16
+// convolution with C' = npairs * Cq channels: In' channel p*Cq + c holds
+// piece ip[p] of In channel c, Ker' channel p*Cq + c piece kp[p] of Ker
+// channel c, so the tensor kernel's fp32 accumulation sums exactly those
+// products (channels c >= C and the tail up to Cp are zero).
+struct SplitGeom {
+    int C, Cq, Cp, RS, npairs;
+    int ip[kSplitMaxPairs], kp[kSplitMaxPairs];
+    int K;
+    int64_t P;                       // pixels per input image
+    int ptiles, ctiles;              // K2 tile grid per image (64 px x 64 channels of In)
+    int ker_blocks;
+    int64_t ker_groups;              // K * RS * Cp / 8 (8 channels = one 16-B store)
+    int* zero_ptr;                   // split-K arrival counters to clear
+    int zero_n;
+};
+
+__device__ __forceinline__ void split3_bf16(float x, float (&v)[3]) {
+    v[0] = __bfloat162float(__float2bfloat16_rn(x));
+    const float r1 = __fsub_rn(x, v[0]);
+    v[1] = __bfloat162float(__float2bfloat16_rn(r1));
+    v[2] = __fsub_rn(r1, v[1]);               // exactly representable in bf16
+}
+
+__global__ void __launch_bounds__(256) split_repack(const float* __restrict__ in, const float* __restrict__ ker,
+                                                    __nv_bfloat16* __restrict__ in_ws,
+                                                    __nv_bfloat16* __restrict__ ker_ws, const SplitGeom g) {
+    __shared__ float tile[64][65];
+    const int tid = threadIdx.x;
+    if ((int)blockIdx.x < g.ker_blocks) {
+        // ---- Ker' [K][R][S][Cp]: one 8-channel group per thread ----
+        for (int i = blockIdx.x * 256 + tid; i < g.zero_n; i += g.ker_blocks * 256) g.zero_ptr[i] = 0;
+        const int gpr = g.Cp / 8;                  // groups per (k, rs) row
+        for (int64_t e = (int64_t)blockIdx.x * 256 + tid; e < g.ker_groups; e += (int64_t)g.ker_blocks * 256) {
+            const int64_t row = e / gpr;           // k * RS + rs
+            const int j0 = (int)(e - row * gpr) * 8;
+            const int64_t k = row / g.RS;
+            const int rs = (int)(row - k * g.RS);
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int j = j0 + i, p = j / g.Cq, c = j - p * g.Cq;
+                float x = 0.0f;
+                if (p < g.npairs && c < g.C) {
+                    float pc[3];
+                    split3_bf16(__ldg(ker + (k * g.C + c) * g.RS + rs), pc);
+                    const int kp = g.kp[p];
+                    x = kp == 0 ? pc[0] : (kp == 1 ? pc[1] : pc[2]);
+                }
+                v[i] = x;
+            }
+            uint4 o;
+            o.x = pack2_bf16(v[0], v[1]);
+            o.y = pack2_bf16(v[2], v[3]);
+            o.z = pack2_bf16(v[4], v[5]);
+            o.w = pack2_bf16(v[6], v[7]);
+            *reinterpret_cast<uint4*>(ker_ws + row * g.Cp + j0) = o;
+        }
+    } else {
+        // ---- In' [N][Hin][Win][Cp]: one (image, 64-channel, 64-pixel) tile ----
+        int b = (int)blockIdx.x - g.ker_blocks;
+        const int pt = b % g.ptiles;
+        b /= g.ptiles;
+        const int ct = b % g.ctiles;
+        const int64_t n = b / g.ctiles;
+        const int64_t P = g.P, p0 = (int64_t)pt * 64;
+        const int c0 = ct * 64;
+        const float* src = in + n * g.C * P;
+        if ((P & 3) == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int idx = tid + i * 256;
+                const int cl = idx >> 4, pq = (idx & 15) * 4;
+                const int c = c0 + cl;
+                const int64_t p = p0 + pq;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (c < g.C && p < P) v = __ldg(reinterpret_cast<const float4*>(src + (int64_t)c * P + p));
+                tile[cl][pq] = v.x; tile[cl][pq + 1] = v.y; tile[cl][pq + 2] = v.z; tile[cl][pq + 3] = v.w;
+            }
+        } else {
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+                const int idx = tid + i * 256;
+                const int cl = idx >> 6, pl = idx & 63;
+                const int c = c0 + cl;
+                const int64_t p = p0 + pl;
+                tile[cl][pl] = (c < g.C && p < P) ? __ldg(src + (int64_t)c * P + p) : 0.0f;
+            }
+        }
+        __syncthreads();
+        __nv_bfloat16* dst = in_ws + n * P * g.Cp;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {              // 64 px x 8 groups of 8 channels / 256 threads
+            const int idx = tid + i * 256;
+            const int pl = idx >> 3, cq = (idx & 7) * 8;
+            const int64_t p = p0 + pl;
+            const int c = c0 + cq;
+            if (p < P && c < g.Cq) {
+                float pc[8][3];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) split3_bf16(tile[cq + j][pl], pc[j]);
+                uint4 piece[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    piece[q] = make_uint4(pack2_bf16(pc[0][q], pc[1][q]), pack2_bf16(pc[2][q], pc[3][q]),
+                                          pack2_bf16(pc[4][q], pc[5][q]), pack2_bf16(pc[6][q], pc[7][q]));
+                __nv_bfloat16* d = dst + p * g.Cp + c;
+                for (int pr = 0; pr < g.npairs; ++pr) {
+                    const int q = g.ip[pr];
+                    *reinterpret_cast<uint4*>(d + pr * g.Cq) = q == 0 ? piece[0] : (q == 1 ? piece[1] : piece[2]);
+                }
+            }
+        }
+        // the channel tail [npairs * Cq, Cp) is zero (written once, by the
+        // first channel tile of each pixel block)
+        const int tail0 = g.npairs * g.Cq, tail_groups = (g.Cp - tail0) / 8;
+        if (ct == 0 && tail_groups > 0) {
+            for (int idx = tid; idx < 64 * tail_groups; idx += 256) {
+                const int pl = idx / tail_groups, gq = idx - pl * tail_groups;
+                const int64_t p = p0 + pl;
+                if (p < P) *reinterpret_cast<uint4*>(dst + p * g.Cp + tail0 + gq * 8) = make_uint4(0, 0, 0, 0);
+            }
+        }
+    }
+    // the main kernel waits for this grid's completion (griddepcontrol.wait)
+    asm volatile("griddepcontrol.launch_dependents;");
+}
+
+cudaError_t launch_split(const Problem& pb, int Cp, int npairs, const float* in, const float* ker, void* in_ws,
+                         void* ker_ws, cudaStream_t st, cudaEvent_t* ev, int* zero_ptr, int zero_n) {
+    SplitGeom g;
+    const SplitPairs sp = split_pairs(npairs);
+    if (sp.n == 0) return cudaErrorInvalidValue;
+    g.C = pb.C;
+    g.Cq = split_cq(pb.C);
+    g.Cp = Cp;
+    g.RS = pb.R * pb.S;
+    g.npairs = sp.n;
+    for (int i = 0; i < kSplitMaxPairs; ++i) {
+        g.ip[i] = sp.ip[i];
+        g.kp[i] = sp.kp[i];
+    }
+    if (Cp % 8 || Cp < g.npairs * g.Cq) return cudaErrorInvalidValue;
+    g.K = pb.K;
+    g.P = pb.Hin() * pb.Win();
+    g.ptiles = (int)((g.P + 63) / 64);
+    g.ctiles = (pb.C + 63) / 64;
+    g.ker_groups = (int64_t)pb.K * g.RS * Cp / 8;
+    g.ker_blocks = (int)std::min<int64_t>((g.ker_groups + 255) / 256, 1184);
+    g.zero_ptr = zero_ptr;
+    g.zero_n = zero_ptr ? zero_n : 0;
+    const int64_t blocks = g.ker_blocks + (int64_t)g.ptiles * g.ctiles * pb.N;
+    if (blocks >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;
+    if (ev) cudaEventRecord(ev[0], st);
+    split_repack<<<(unsigned)blocks, 256, 0, st>>>(in, ker, (__nv_bfloat16*)in_ws, (__nv_bfloat16*)ker_ws, g);
     if (ev) cudaEventRecord(ev[1], st);
     return cudaGetLastError();
 }

@@ -499,25 +499,18 @@ size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
 }
 
 // Launch one SIMT kernel instance, opting it in to the largest dynamic smem
-// once (`smem_set` is that instance's own flag).
+// per device (`smem_set` is that instance's own flags).
 template <typename K, typename P>
-static cudaError_t launch_simt_inst(K kfn, std::atomic<int>& smem_set, const float* in, const float* kerp, float* out,
+static cudaError_t launch_simt_inst(K kfn, SmemOptIn& smem_set, const float* in, const float* kerp, float* out,
                                     const P& p, dim3 grid, int threads, size_t smem, cudaStream_t st) {
-    if (smem_set.load(std::memory_order_acquire) < (int)smem) {
-        int optin = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-        if (e != cudaSuccess) return e;
-        smem_set.store(optin, std::memory_order_release);
-    }
+    if (cudaError_t e = smem_set.ensure(kfn, smem); e != cudaSuccess) return e;
     return launch_pdl(kfn, grid, threads, smem, st, in, kerp, out, p);
 }
 
 template <int TK, int TW, int KR, int KS>
 static cudaError_t launch_simt2_t(const float* in, const float* kerp, float* out, const Simt2Params& p,
                                   dim3 grid, int threads, size_t smem, cudaStream_t st) {
-    static std::atomic<int> set_plain{0}, set_split{0};
+    static SmemOptIn set_plain, set_split;
     if (grid.z > 1)
         return launch_simt_inst(conv_direct_simt2<TK, TW, KR, KS, true>, set_split, in, kerp, out, p, grid, threads, smem, st);
     return launch_simt_inst(conv_direct_simt2<TK, TW, KR, KS, false>, set_plain, in, kerp, out, p, grid, threads, smem, st);
@@ -542,7 +535,7 @@ static cudaError_t dispatch_simt2(const SimtTile& t, int R, int S, const float* 
 template <int TK, int TW>
 static cudaError_t launch_simt_t(const float* in, const float* kerp, float* out, const SimtParams& p,
                                  dim3 grid, int threads, size_t smem, cudaStream_t st) {
-    static std::atomic<int> set_plain{0}, set_split{0};
+    static SmemOptIn set_plain, set_split;
     if (grid.z > 1)
         return launch_simt_inst(conv_direct_simt<TK, TW, true>, set_split, in, kerp, out, p, grid, threads, smem, st);
     return launch_simt_inst(conv_direct_simt<TK, TW, false>, set_plain, in, kerp, out, p, grid, threads, smem, st);

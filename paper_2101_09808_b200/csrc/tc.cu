@@ -624,9 +624,8 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             };
             if (n_units > 0) tile_range();
             long long w_spin = 0;
-            const long long t_start = clock64();
+            long long t_last = clock64();                 // watchdog: time of the last progress
             while (u < n_units || pub < n_my) {
-                if (clock64() - t_start > 8000000000ll) __trap();
                 bool progress = false;
                 const int done = ld_acquire_cta_smem(done_ctr);
                 if (pub < done) {
@@ -660,9 +659,12 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     }
                 }
                 if (!progress) {
-                    const long long t0 = trace ? clock64() : 0;
+                    const long long t0 = clock64();
                     __nanosleep(128);
                     if (trace) w_spin += clock64() - t0;
+                    if (t0 - t_last > 8000000000ll) __trap();   // ~4 s without progress
+                } else {
+                    t_last = clock64();
                 }
             }
             if (trace && lane == 0) trace[(size_t)blockIdx.x * 64 + 39] = (unsigned long long)w_spin;
@@ -680,12 +682,11 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             unsigned long long* tr = trace ? trace + (size_t)blockIdx.x * 64 : nullptr;
             long long c_conv = 0, c_rd = 0, c_pub = 0, c_dec = 0;
             if (tr) tr[58] = globaltimer_ns();
-            const long long t_start = clock64();
             auto entry = [&](int k) -> int4 {          // waits until the converters decoded chunk k
                 if (ld_acquire_cta_smem(dec_ctr) <= k) {
                     const long long t0 = clock64();
                     while (ld_acquire_cta_smem(dec_ctr) <= k) {
-                        if (clock64() - t_start > 8000000000ll) __trap();
+                        if (clock64() - t0 > 8000000000ll) __trap();   // this wait, ~4 s
                     }
                     if (tr) c_dec += clock64() - t0;
                 }
@@ -923,16 +924,9 @@ struct TcMaps {
 template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT, bool FUSE>
 static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
     auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS, SPLIT, FUSE>;
-    // Opt in to the largest dynamic smem once per instantiation (per process).
-    static std::atomic<int> smem_set{0};
-    if (smem_set.load(std::memory_order_acquire) < (int)smem) {
-        int optin = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-        if (e != cudaSuccess) return e;
-        smem_set.store(optin, std::memory_order_release);
-    }
+    // Opt in to the largest dynamic smem once per instantiation and device.
+    static SmemOptIn opt;
+    if (cudaError_t e = opt.ensure(kfn, smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
@@ -946,11 +940,13 @@ static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, 
     static const int no_pdl = getenv("CONV_NO_PDL") ? 1 : 0;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL after the repack
     attr[1].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
-    // The fused transform's CTAs wait on chunks other CTAs convert: all of
-    // them must be resident at once.  They are -- one CTA per SM (smem and
-    // registers), grid <= SM count -- so no cooperative launch is requested
-    // (ncu cannot replay cooperative cluster launches); a starved wait traps
-    // after ~4 s (watchdog) instead of hanging.
+    // The fused transform's and split-K's CTAs wait on work other CTAs of
+    // the grid do: all of them must be resident at once.  They are -- one CTA
+    // per SM (smem and registers), grid <= SM count -- as long as no other
+    // such grid holds part of the GPU: tc_run serialises these launches per
+    // device (ResidentChain).  No cooperative launch is requested (ncu
+    // cannot replay cooperative cluster launches); a starved wait traps
+    // after ~4 s without progress (watchdog) instead of hanging.
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kfn, m.a, m.b, m.src, m.dst, prm);
@@ -1102,10 +1098,27 @@ bool tc_split_ok(const Problem& pb, const TcLayout& L, const TcTile& t) {
     return (size_t)t.splits * share <= tc_pipe_bytes(L, t);
 }
 
+// Plans whose main kernel needs all of its CTAs resident at once (the fused
+// transform waits on chunks other CTAs convert, split-K on the tile's other
+// splits) are serialised per device across streams and host threads: each
+// such conv_run waits (on the device) for the previous one's main kernel and
+// records the device's chain event after its own.  Two such grids sharing
+// the GPU could otherwise each hold part of the SMs and wait on CTAs that can
+// never be scheduled.  Inside CUDA-graph capture the chain is not used (a
+// captured stream cannot wait on an event recorded outside the capture): the
+// graph's own order serialises its launches (include/conv.h).
+struct ResidentChain {
+    std::mutex mu;
+    cudaEvent_t ev[kMaxDevices] = {};
+};
+static ResidentChain g_chain;
+
 cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool bf16,
                    const float* in, const float* ker, float* out, void* in_ws, void* ker_ws, void* flag_ws,
-                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err, const Problem* expand_src) {
-    if (expand_src && (t.fuse || t.splits > 1)) { err = "tap-expanded plans run without the fused transform and split-K"; return cudaErrorInvalidValue; }
+                   cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err, const Problem* expand_src,
+                   int split_pairs) {
+    if (expand_src && !split_pairs && (t.fuse || t.splits > 1)) { err = "tap-expanded plans run without the fused transform and split-K"; return cudaErrorInvalidValue; }
+    if (split_pairs && (!expand_src || !bf16 || t.fuse)) { err = "FP32_TC plans run the bf16 kernel without the fused transform"; return cudaErrorInvalidValue; }
     if (t.fuse && (!L.coop_ok || !flag_ws)) { err = "fused transform needs a TMA-legal NCHW plane and flag workspace"; return cudaErrorInvalidValue; }
     // Tensor maps depend on the workspace (and, fused, In) addresses, known
     // only here; they are encoded on first use and cached.
@@ -1225,6 +1238,22 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         prm.tr_off = (uint32_t)((tc_pipe_bytes(L, t) + 1023) / 1024 * 1024);
     }
 
+    // all-resident plans: serialise with the device's previous one (above)
+    std::unique_lock<std::mutex> chain_lock;
+    if (t.fuse || prm.splits > 1) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) { cudaGetLastError(); cs = cudaStreamCaptureStatusNone; }
+        if (cs == cudaStreamCaptureStatusNone && dev >= 0 && dev < kMaxDevices) {
+            chain_lock = std::unique_lock<std::mutex>(g_chain.mu);
+            if (!g_chain.ev[dev] && cudaEventCreateWithFlags(&g_chain.ev[dev], cudaEventDisableTiming) != cudaSuccess) {
+                err = "cannot create the all-resident chain event";
+                return cudaErrorUnknown;
+            }
+            e = cudaStreamWaitEvent(st, g_chain.ev[dev], 0);
+            if (e != cudaSuccess) { err = "cudaStreamWaitEvent (all-resident chain) failed"; return e; }
+        }
+    }
+
     RepackFuse fz;
     if (t.fuse) {
         fz.zero_ptr = static_cast<int*>(flag_ws);
@@ -1243,8 +1272,12 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         fz.zero_ptr = prm.tile_ctr;               // the repack launch clears the arrival counters
         fz.zero_n = prm.num_tiles;
     }
-    e = expand_src ? launch_expand(*expand_src, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev)
-                   : launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse, fz);
+    if (split_pairs)
+        e = launch_split(*expand_src, L.Cp, split_pairs, in, ker, in_ws, ker_ws, st, ev, fz.zero_ptr, fz.zero_n);
+    else if (expand_src)
+        e = launch_expand(*expand_src, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev);
+    else
+        e = launch_repack(pb, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev, /*with_in=*/!t.fuse, fz);
     if (e != cudaSuccess) { err = "repack launch failed"; return e; }
 
     static const char* trace_path = kTraceBuild ? getenv("CONV_TRACE") : nullptr;   // trace builds only
@@ -1263,6 +1296,7 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         e = bf16 ? launch_tc_sw<true, 1>(L.sw, t.bn, maps, prm, smem, grid, st)
                  : launch_tc_sw<false, 1>(L.sw, t.bn, maps, prm, smem, grid, st);
     if (e != cudaSuccess) { err = std::string("tcgen05 kernel launch failed: ") + cudaGetErrorString(e); return e; }
+    if (chain_lock.owns_lock()) cudaEventRecord(g_chain.ev[dev], st);
     if (ev) cudaEventRecord(ev[2], st);
     if (prm.trace) {
         static unsigned long long host[1024 * 64];
