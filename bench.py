@@ -64,9 +64,14 @@ def load_peaks():
     return d, src
 
 
-def path_peak(path, peaks):
-    """(peak TFLOP/s, bound, note, measured?) for a path's dominant kernel."""
+def path_peak(path, peaks, split=0):
+    """(peak TFLOP/s, bound, note, measured?) for a path's dominant kernel.
+    FP32_TC runs `split` bf16 piece-pair products per fp32 product: its peak
+    is the bf16 peak / split in fp32 FLOPs."""
     sel = peaks.get("probes", {}).get("selected", {})
+    if path == "fp32_tc":
+        return peaks["bf16_tflops"] / split, "tensor", \
+            f"cuBLAS bf16 GEMM burst (MEASURED_PEAKS.json, driver) / {split} piece pairs", True
     if path == "bf16":
         return peaks["bf16_tflops"], "tensor", "cuBLAS bf16 GEMM burst (MEASURED_PEAKS.json, driver)", True
     if path == "tf32":
@@ -87,7 +92,7 @@ def dist_env():
     return rank, world, local
 
 
-PATH_DTYPE = {"bf16": "bf16", "tf32": "tf32", "fp32_simt": "f32"}
+PATH_DTYPE = {"bf16": "bf16", "tf32": "tf32", "fp32_simt": "f32", "fp32_tc": "f32 (bf16x{split} exact split)"}
 L2_NOTE = ("flushed before every timed step, outside the event pair: write of a 2x-L2 buffer, then a read of "
            "another 2x-L2 buffer (dirty lines written back before the step: cold, clean L2)")
 
@@ -332,7 +337,7 @@ def path_record(args, world, full, spec, res, engine, peaks, peak_src):
     sh = spec.local
     ms, main_ms = res["ms_max"], res["main_ms_max"]
     total_flops = full.flops * (world if args.scaling == "weak" else 1)
-    peak, bound, peak_note, measured = path_peak(res["path"], peaks)
+    peak, bound, peak_note, measured = path_peak(res["path"], peaks, res["desc"]["tile"].get("split", 0))
     achieved = sh.flops / (main_ms * 1e-3) / 1e12
     per_kernel = res["per_kernel"]
     traffic = None
@@ -345,7 +350,7 @@ def path_record(args, world, full, spec, res, engine, peaks, peak_src):
     return {
         "value": round(total_flops / (ms * 1e-3) / 1e12, 3),
         "ms_per_step": round(ms, 5),
-        "dtype": PATH_DTYPE[res["path"]],
+        "dtype": PATH_DTYPE[res["path"]].format(split=res["desc"]["tile"].get("split", 0)),
         "path": res["path"],
         "tile": res["desc"]["tile"],
         "step_stats": step_stats(res["step_ms"]),
@@ -549,7 +554,7 @@ def bench_table1(args):
     flush_rd = torch.ones_like(flush)
     flush_out = torch.empty((), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    paths = [args.path] if args.path != "all" else ["bf16", "tf32", "fp32_simt"]
+    paths = [args.path] if args.path != "all" else ["bf16", "tf32", "fp32_simt", "fp32_tc"]
     names = [n for n in TABLE1 if not args.layers or n in args.layers.split(",")]
     for name in names:
         sh = TABLE1[name]
@@ -590,7 +595,7 @@ def bench_table1(args):
                 plan.run_events(d_in, d_ker, out, ws, kev[i])
             torch.cuda.synchronize(dev)
             kern_us = [round(float(np.mean([e[j].elapsed_time(e[j + 1]) for e in kev])) * 1e3, 2) for j in range(nk)]
-            peak, bound, _, _ = path_peak(plan.path, peaks)
+            peak, bound, _, _ = path_peak(plan.path, peaks, plan.describe()["tile"].get("split", 0))
             roof_us = max(sh.flops / (peak * 1e12), 4.0 * (sh.N * sh.C * sh.Hin * sh.Win + sh.K * sh.C * sh.R * sh.S +
                                                            sh.N * sh.K * sh.H * sh.W) / (peaks["hbm_gbs"] * 1e9)) * 1e6
             d = plan.describe()
@@ -629,7 +634,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--path", default="fp32_simt", choices=["auto", "fp32_simt", "tf32", "bf16", "all"],
+    ap.add_argument("--path", default="fp32_simt", choices=["auto", "fp32_simt", "fp32_tc", "tf32", "bf16", "all"],
                     help="the headline path (default: FP32, the paper's precision, PAPER.md:369)")
     ap.add_argument("--paths", default="tf32,bf16",
                     help="further paths measured in the same process, reported under 'paths' ('' for none)")

@@ -143,8 +143,10 @@ static bool select_split(conv_plan* p, TcTile& tt, ModelResult& rt, Problem& ps,
     ps = split_problem(p->pb, np);
     TcForce f = p->force_tc;
     if (f.fuse == 1) { why = "FP32_TC plans run without the fused transform"; return false; }
+    if (f.splits > 1) { why = "FP32_TC plans run without split-K (the promoted accumulation)"; return false; }
     f.fuse = 0;
     f.expand = 0;
+    f.splits = 1;
     if (!select_tc(ps, p->dev, true, tt, rt, f, why)) return false;
     const double over = 4.0 * ((double)ps.in_elems() - (double)p->pb.in_elems()) +
                         4.0 * ((double)ps.ker_elems() - (double)p->pb.ker_elems());

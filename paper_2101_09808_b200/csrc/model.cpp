@@ -315,6 +315,7 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
             if ((pb.R * pb.S * L.n_cblk) % kbs) continue;
             for (int bn : kBNs) {
                 if (force_bn && bn != force_bn) continue;
+                if (f.bn_max && bn > f.bn_max) continue;
                 if (!force_bn && bn > 32 && bn / 2 >= pb.K) continue;   // mostly padding
                 // CTA pairs halve the B operand traffic, which is negligible at
                 // BN = 32, while their cluster synchronisation lengthens a

@@ -114,6 +114,11 @@ struct TcParams {
     int gend[32];             // group g covers chunk-pixel indices q in [gend[g-1], gend[g])
     int tnb;                  // input staging buffers (2..4)
     uint32_t tr_off;          // byte offset of the transform smem region (1024-aligned)
+    // ---- promoted accumulation (FP32_TC plans, PROMOTE instances) ----
+    int pchunk;               // pipeline stages per promotion chunk: the tensor core accumulates a
+                              // chunk of the k loop in TMEM (fresh accumulator), the epilogue warps add
+                              // it to fp32 registers (IEEE round-to-nearest) -- the tcgen05 fp32
+                              // accumulation alone truncates (reading R16)
 };
 
 // ---- cooperative NCHW -> NHWC transform (row a-3 inside K3) ----------------
@@ -330,7 +335,7 @@ __device__ __forceinline__ void reduce_share(const TcParams& p, int tile, const 
 //   shared memory, and each CTA's TMEM receives its own 128 accumulator rows.
 //   Per SM this halves the B operand traffic (L2 -> SMEM and SMEM -> tensor
 //   core), which is what bounds the 1-CTA kernel on wide tiles.
-template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT, bool FUSE>
+template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT, bool FUSE, bool PROMOTE>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b,
@@ -397,7 +402,8 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
-            mbar_init(&tmem_empty[i], 4 * CG);    // one arrive per epilogue warp of the pair
+            // one arrive per epilogue warp of the pair (8 warps promote)
+            mbar_init(&tmem_empty[i], (PROMOTE ? 8 : 4) * CG);
         }
         mbar_init(last_full, 1);
         *ready_ctr = 0;
@@ -411,7 +417,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
     if (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const bool kSplitLast = !SPLIT && CONV_SPLIT_LAST && BN >= 64;
+    const bool kSplitLast = !SPLIT && !PROMOTE && CONV_SPLIT_LAST && BN >= 64;
     // Programmatic dependent launch: everything above overlapped the tail of
     // the repack launch; from here on the repacked workspace (and, fused, the
     // zeroed chunk flags) is read and Out written, so wait for the preceding
@@ -537,13 +543,19 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 const int tile = SPLIT ? wi / p.splits : wi;
                 const int it_beg = SPLIT ? (wi - tile * p.splits) * p.kper : 0;
                 const int iters = SPLIT ? (min(p.k_iters, it_beg + p.kper) - it_beg) / kbs : p.k_iters / kbs;
+                // PROMOTE: the tile's k loop in chunks of pchunk stages, each
+                // into a fresh (double-buffered) accumulator the epilogue adds
+                // to its fp32 registers; otherwise one chunk = the whole loop
+                const int chunk = PROMOTE ? p.pchunk : iters;
+                for (int c0 = 0; c0 < iters; c0 += chunk) {
+                const int c1 = min(iters, c0 + chunk);
                 mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 if (tr && lane == 0 && ti < 8) tr[1 + 4 * ti] = globaltimer_ns();
                 long long wait_cyc = 0;
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-                uint32_t accum = 0;                      // first MMA of the tile overwrites D
-                for (int it = 0; it < iters; ++it) {
+                uint32_t accum = 0;                      // first MMA of the tile (chunk) overwrites D
+                for (int it = c0; it < c1; ++it) {
                     const long long w0 = tr ? clock64() : 0;
                     mbar_wait(&full[stage], phase);
                     if (tr) wait_cyc += clock64() - w0;
@@ -592,6 +604,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     tr[1 + 4 * ti + 3] = (unsigned long long)clock64();
                 }
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                }   // chunks
             }
         }
     } else if (warp == 9) {
@@ -741,7 +754,7 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
             }
         }
         __syncwarp();
-    } else if (warp < 4) {
+    } else if (warp < 4 && !PROMOTE) {
         // ===== chunk converters + decoders (fuse): decode the chunk ring
         // one block ahead (parallel binary searches, no divisions on the
         // storer), then convert + transpose every loaded chunk in place
@@ -785,6 +798,59 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                 fence_proxy_async_smem();                 // generic smem writes -> TMA store
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tconv[b]);
+            }
+        }
+    } else if (PROMOTE && warp < 8) {
+        // ===== promoted epilogue (8 warps; warp w: TMEM lane quadrant w % 4,
+        // column half w / 4): each chunk's accumulator is added to fp32
+        // registers with IEEE round-to-nearest adds, then released to the MMA
+        // warp; after the tile's last chunk the registers go to NCHW Out =====
+        constexpr int HB = BN / 2;
+        const int q = warp & 3, half = warp >> 2;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        const int iters = p.k_iters / p.kbs;
+        const int nchunk = (iters + p.pchunk - 1) / p.pchunk;
+        for (int wi = unit; wi < p.num_work; wi += nunits) {
+            float run[HB];
+#pragma unroll
+            for (int j = 0; j < HB; ++j) run[j] = 0.0f;
+            for (int c = 0; c < nchunk; ++c) {
+                mbar_wait_sleep(&tmem_full[acc], acc_phase, 64);
+                tc_fence_after();
+                const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + half * HB);
+                // narrow loads at BN >= 192: the BN/2 sums + the load buffer
+                // must stay within the 168 registers of a 384-thread CTA
+                constexpr int LW = HB > 64 ? 8 : 16;
+#pragma unroll
+                for (int j0 = 0; j0 < HB; j0 += LW) {
+                    uint32_t v[LW];
+                    if constexpr (LW == 8) tmem_ld_32x32b_x8(t0 + (uint32_t)j0, v);
+                    else tmem_ld_32x32b_x16(t0 + (uint32_t)j0, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < LW; ++j) run[j0 + j] = __fadd_rn(run[j0 + j], __uint_as_float(v[j]));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_leader(&tmem_empty[acc]);
+                    else mbar_arrive(&tmem_empty[acc]);
+                }
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+            // registers -> NCHW Out (32 consecutive pixels of one (n, k) plane per warp store)
+            const int tile = wi;
+            const int m_tile = tile / p.num_n_tiles;
+            const int n_tile = tile - m_tile * p.num_n_tiles;
+            const int m = m_tile * (kBM * CG) + (int)rank * kBM + q * 32 + (int)lane;
+            if (m < p.M) {
+                const int img = m / p.HW, pix = m - img * p.HW;
+                const int kbase = n_tile * BN + half * HB;
+                float* obase = p.out + ((int64_t)img * p.K) * p.HW + pix;
+#pragma unroll
+                for (int j = 0; j < HB; ++j)
+                    if (kbase + j < p.K) __stcs(obase + (int64_t)(kbase + j) * p.HW, run[j]);
             }
         }
     } else if (warp >= 4 && warp < 8) {
@@ -894,6 +960,8 @@ TcLayout tc_layout(const Problem& pb, bool bf16) {
     return L;
 }
 
+int tc_promote_kblocks(const TcLayout& L) { return std::max(1, (kPromoteProducts + L.bkc - 1) / L.bkc); }
+
 // pipeline ring + barrier block, then (fuse) the transform region at a
 // 1024-B boundary: tnb fp32 [cc][64] chunk buffers (converted in place),
 // tnb mbarriers and tnb chunk slots.
@@ -921,9 +989,9 @@ struct TcMaps {
     CUtensorMap a, b, src, dst;   // src/dst only with fuse (copies of a/b otherwise)
 };
 
-template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT, bool FUSE>
+template <int BN, bool BF16, int CG, int KSTEPS, bool SPLIT, bool FUSE, bool PROMOTE = false>
 static cudaError_t launch_tc(const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
-    auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS, SPLIT, FUSE>;
+    auto kfn = conv_igemm_tcgen05<BN, BF16, CG, KSTEPS, SPLIT, FUSE, PROMOTE>;
     // Opt in to the largest dynamic smem once per instantiation and device.
     static SmemOptIn opt;
     if (cudaError_t e = opt.ensure(kfn, smem); e != cudaSuccess) return e;
@@ -960,6 +1028,21 @@ static cudaError_t launch_tc_bn(int bn, const TcMaps& m, const TcParams& prm, si
                 case 32: return launch_tc<32, BF16, 1, KSTEPS, true, false>(m, prm, smem, grid, st);
                 case 64: return launch_tc<64, BF16, 1, KSTEPS, true, false>(m, prm, smem, grid, st);
                 case 128: return launch_tc<128, BF16, 1, KSTEPS, true, false>(m, prm, smem, grid, st);
+                default: break;
+            }
+        }
+        return cudaErrorInvalidValue;
+    }
+    // Promoted accumulation (FP32_TC): bf16 (the epilogue's 8 warps hold
+    // BN/2 fp32 sums each), no split-K, no fused transform
+    if (prm.pchunk > 0) {
+        if constexpr (BF16 && KSTEPS == 4) {
+            switch (bn) {
+                case 32: return launch_tc<32, true, CG, 4, false, false, true>(m, prm, smem, grid, st);
+                case 64: return launch_tc<64, true, CG, 4, false, false, true>(m, prm, smem, grid, st);
+                case 128: return launch_tc<128, true, CG, 4, false, false, true>(m, prm, smem, grid, st);
+                case 192: return launch_tc<192, true, CG, 4, false, false, true>(m, prm, smem, grid, st);
+                case 256: return launch_tc<256, true, CG, 4, false, false, true>(m, prm, smem, grid, st);
                 default: break;
             }
         }
@@ -1118,7 +1201,10 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
                    cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err, const Problem* expand_src,
                    int split_pairs) {
     if (expand_src && !split_pairs && (t.fuse || t.splits > 1)) { err = "tap-expanded plans run without the fused transform and split-K"; return cudaErrorInvalidValue; }
-    if (split_pairs && (!expand_src || !bf16 || t.fuse)) { err = "FP32_TC plans run the bf16 kernel without the fused transform"; return cudaErrorInvalidValue; }
+    if (split_pairs && (!expand_src || !bf16 || t.fuse || t.splits > 1)) {
+        err = "FP32_TC plans run the promoted bf16 kernel: no fused transform, no split-K";
+        return cudaErrorInvalidValue;
+    }
     if (t.fuse && (!L.coop_ok || !flag_ws)) { err = "fused transform needs a TMA-legal NCHW plane and flag workspace"; return cudaErrorInvalidValue; }
     // Tensor maps depend on the workspace (and, fused, In) addresses, known
     // only here; they are encoded on first use and cached.
@@ -1193,6 +1279,9 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
 
     prm.stages = t.stages;
     prm.kbs = t.kbs;
+    // FP32_TC: promote every ~kPromoteProducts products per output (9 k-blocks
+    // of 64 channels = one 3x3 window of a channel block), R16
+    prm.pchunk = split_pairs ? std::max(1, (tc_promote_kblocks(L) + t.kbs - 1) / t.kbs) : 0;
     prm.sw = (uint32_t)L.sw;
     prm.a_stage_bytes = (uint32_t)(t.kbs * kBM * L.sw);
     prm.b_stage_bytes = (uint32_t)(t.kbs * (t.bn / t.cg) * L.sw);

@@ -379,3 +379,46 @@ def test_padded_all_ones_closed_form():
             nr = sum(1 for r in range(R) if 0 <= U * h + D * r - ph < Hin)
             ns = sum(1 for s in range(S) if 0 <= U * w + D * s - pw < Win)
             assert got[0, 1, h, w] == C * nr * ns, (h, w)
+
+
+def test_bf16_three_piece_split_is_exact():
+    """DESIGN.md reading R15 (the FP32_TC path): x0 = bf16(x), x1 = bf16(x -
+    x0), x2 = bf16(x - x0 - x1) reproduces every binary32 x exactly
+    (x0 + x1 + x2 == x, each remainder exact in fp32, x2 representable in
+    bf16), every piece product x_i * y_j is exact in fp32 (8 x 8 bits), and
+    the three pairs with i + j > 2 that the 6-pair variant drops are below
+    3 * 2^-24 |x * y| (products inside binary32's normal range; outside it
+    any fp32 arithmetic over/underflows).  Pinned with the oracle's bf16
+    rounding (RNE)."""
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.uniform(-1, 1, 20000), rng.standard_normal(5000) * 1e30,
+                        rng.standard_normal(5000) * 1e-30]).astype(np.float32)
+    y = rng.permutation(x)
+
+    def split(v):
+        v0 = oracle.round_bf16_rne(v)
+        r1 = (v - v0).astype(np.float32)
+        v1 = oracle.round_bf16_rne(r1)
+        r2 = (r1 - v1).astype(np.float32)
+        v2 = oracle.round_bf16_rne(r2)
+        assert np.array_equal(v2, r2)                            # the last remainder is a bf16
+        assert np.array_equal(v0.astype(np.float64) + v1 + v2, v.astype(np.float64))
+        return v0, v1, v2
+
+    xs, ys = split(x), split(y)
+    exact = x.astype(np.float64) * y.astype(np.float64)
+    for i in range(3):
+        for j in range(3):
+            with np.errstate(over="ignore", under="ignore"):
+                pf = (xs[i] * ys[j]).astype(np.float32)          # fp32 product of two pieces
+            p64 = xs[i].astype(np.float64) * ys[j]
+            # exact wherever the product is in binary32's normal range (as
+            # for any fp32 arithmetic, products outside it over/underflow)
+            ok = (np.abs(p64) >= 2.0 ** -126) & (np.abs(p64) < 2.0 ** 127)
+            assert ok.mean() > 0.5
+            assert np.array_equal(pf[ok].astype(np.float64), p64[ok])
+    dropped = sum(xs[i].astype(np.float64) * ys[j] for i, j in ((1, 2), (2, 1), (2, 2)))
+    nz = exact != 0
+    assert np.all(np.abs(dropped[nz]) <= 3 * 2.0 ** -24 * np.abs(exact[nz]))
+    six = sum(xs[i].astype(np.float64) * ys[j] for i, j in ((0, 0), (0, 1), (1, 0), (0, 2), (1, 1), (2, 0)))
+    assert np.array_equal(six + dropped, exact)

@@ -15,9 +15,10 @@ from paper_2101_09808_b200.inputs import CONFIGS, Shape, make_inputs
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"fp32_simt": 1e-5, "tf32": 5e-3, "bf16": 5e-3}
-ROUND = {"fp32_simt": lambda x: x, "tf32": oracle.round_tf32_rna, "bf16": oracle.round_bf16_rne}
-PATHS = ["fp32_simt", "tf32", "bf16"]
+TOL = {"fp32_simt": 1e-5, "fp32_tc": 1e-5, "tf32": 5e-3, "bf16": 5e-3}
+ROUND = {"fp32_simt": lambda x: x, "fp32_tc": lambda x: x, "tf32": oracle.round_tf32_rna,
+         "bf16": oracle.round_bf16_rne}
+PATHS = ["fp32_simt", "fp32_tc", "tf32", "bf16"]
 
 
 def rel_l2(got, ref):
@@ -337,7 +338,7 @@ def test_auto_path_and_describe():
     for name, sh in CONFIGS.items():
         plan = conv.ConvPlan(*sh.as_tuple())
         d = plan.describe()
-        assert d["path"] in ("fp32_simt", "tf32")
+        assert d["path"] in ("fp32_simt", "fp32_tc")      # AUTO: fp32 precision only
         assert d["problem"]["N"] == sh.N and d["problem"]["W"] == sh.W
         assert d["model"]["model_us"] > 0
         assert d["kernels"] == plan.num_kernels
@@ -985,3 +986,47 @@ def test_concurrent_all_resident_plans_on_two_streams():
     for i in range(len(plans)):
         for it in range(3):
             assert torch.equal(outs[i][it], refs[i]), (cases[i], it)
+
+
+@pytest.mark.parametrize("split", [6, 9])
+def test_fp32_tc_split_pairs(split):
+    """FP32_TC with 6 (i + j <= 2) and 9 (all) bf16 piece pairs: relL2 at the
+    FP32 tolerance on real data over tile variants (CTA pair / single, split-K,
+    BN), bit-exact on the integer twin, and its error no larger than a few
+    times the FP32 SIMT path's on the same inputs."""
+    sh = Shape(N=2, K=96, C=80, H=17, W=19, R=3, S=3)
+    inp, ker = make_inputs(sh, seed=150)
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    simt, _ = run(sh, inp, ker, "fp32_simt")
+    e_simt = rel_l2(simt, ref)
+    for spec in (f"split={split}", f"split={split},cg=1", f"split={split},cg=2,bn=64",
+                 f"split={split},splits=4,cg=1"):
+        try:
+            got, plan = run(sh, inp, ker, "fp32_tc", tile=spec)
+        except conv.ConvError as e:
+            assert e.status == conv.CONV_ERR_INFEASIBLE and "splits" in spec
+            continue
+        d = plan.describe()
+        assert d["path"] == "fp32_tc" and d["tile"]["split"] == split
+        e = rel_l2(got, ref)
+        assert e <= 1e-5 and e <= 4 * e_simt + 1e-7, (spec, e, e_simt)
+    xi, wi = make_inputs(sh, seed=151, kind="int")
+    goti, _ = run(sh, xi, wi, "fp32_tc", tile=f"split={split}")
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
+def test_fp32_tc_extreme_magnitudes():
+    """Inputs spanning many binades (|x| from 2^-60 to 2^60, both signs): the
+    exact 3-piece split keeps every significand bit, so the result still
+    matches the oracle at the FP32 tolerance (a 2-piece split or a TF32
+    rounding would not)."""
+    sh = Shape(N=1, K=32, C=48, H=12, W=12, R=3, S=3)
+    g = torch.Generator().manual_seed(160)
+    mant = torch.rand(sh.in_shape, generator=g) + 1.0
+    ex = torch.randint(-60, 61, sh.in_shape, generator=g).to(torch.float32)
+    sign = torch.randint(0, 2, sh.in_shape, generator=g).to(torch.float32) * 2 - 1
+    inp = (sign * mant * torch.pow(2.0, ex)).contiguous()
+    ker = (torch.rand(sh.ker_shape, generator=g) * 2 - 1).contiguous()
+    got, _ = run(sh, inp, ker, "fp32_tc")
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert rel_l2(got, ref) <= 1e-5
