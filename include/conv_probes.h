@@ -35,6 +35,12 @@ extern "C" {
 CONV_PROBE_API int probe_ffma(float* out, int blocks, int threads, int iters, void* stream);
 CONV_PROBE_API double probe_ffma_flops(int blocks, int threads, int iters);
 
+/* FFMA2 (fma.rn.f32x2: two fp32 FMAs per lane and instruction, sm_100):
+ * 8 register-pair chains x 8 * iters steps, pair x broadcast-scalar
+ * operands (the SIMT kernel's form); same FLOPs per launch as probe_ffma
+ * with the same arguments. */
+CONV_PROBE_API int probe_ffma2(float* out, int blocks, int threads, int iters, void* stream);
+
 /* tcgen05.mma issue rate from shared-memory operands (no loads): `grid` CTAs
  * (a multiple of cg; cluster of cg), each CTA group issuing 4 * iters MMAs of
  * M = 128*cg, N = 256, K = 16 (bf16 != 0, kind::f16 with bf16 inputs) or

@@ -283,6 +283,11 @@ struct Simt2Params {
     int vec4;         // Win % 4 == 0: 16-B copies of input rows
 };
 
+static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth
+#ifndef CONV_SIMT_FFMA2
+#define CONV_SIMT_FFMA2 1                  // v2 inner product on FFMA2 (0: scalar FFMA, A/B builds)
+#endif
+
 template <int TK, int TW, int KR, int KS, bool SPLITC>   // KR = 0: runtime R
 __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict__ in,
                                                           const float* __restrict__ kerp,
@@ -315,11 +320,24 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
     const bool valid = q < p.slots && (n0 + img) < p.N && (h0 + row) < p.H;
     const int off = valid ? (img * p.rows_in + row) * p.pitch + w0 : 0;
 
+#if CONV_SIMT_FFMA2
+    // FFMA2 (fma.rn.f32x2, sm_100): output channels in pairs, acc2[i][j] =
+    // (acc[2i][j], acc[2i+1][j]) in one 64-bit register pair; each
+    // instruction does two FMAs (kernel pair x broadcast input value), so the
+    // FMA pipe stays busy with half the issue slots (ncu r02: the FFMA form
+    // was issue-bound -- 85 % FFMA, 15 % addressing/LDS, 83 % issue slots busy)
+    unsigned long long acc2[TK / 2][TW];
+#pragma unroll
+    for (int i = 0; i < TK / 2; ++i)
+#pragma unroll
+        for (int j = 0; j < TW; ++j) acc2[i][j] = 0ull;
+#else
     float acc[TK][TW];
 #pragma unroll
     for (int i = 0; i < TK; ++i)
 #pragma unroll
         for (int j = 0; j < TW; ++j) acc[i][j] = 0.0f;
+#endif
 
     // Copy plan of the In tile, computed once: a unit is 16 B (4 floats) of
     // one input row when Win % 4 == 0 (rows are then 16-B aligned in NCHW and
@@ -400,14 +418,21 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
     const int c_beg = SPLITC ? (int)blockIdx.z * p.cper : 0;
     const int c_end = SPLITC ? min(p.nchunks, c_beg + p.cper) : p.nchunks;
     if (SPLITC) out += (int64_t)blockIdx.z * p.zstride;
+    // three-stage ring, one barrier per chunk: the copies of chunk i+2 are
+    // issued after the barrier that ends every thread's use of chunk i-1's
+    // buffer (ncu r02: with two stages and two barriers per chunk a third of
+    // the stall samples sat outside the FFMA loop, in the waits)
     load_stage(0, c_beg);
     cp_async_commit();
+    if (c_beg + 1 < c_end) load_stage(1, c_beg + 1);
+    cp_async_commit();
     for (int chunk = c_beg; chunk < c_end; ++chunk) {
-        const int buf = (chunk - c_beg) & 1;
-        if (chunk + 1 < c_end) load_stage(buf ^ 1, chunk + 1);
-        cp_async_commit();
-        cp_async_wait<1>();
+        const int ci = chunk - c_beg;
+        const int buf = ci % kSimt2Stages;
+        cp_async_wait<1>();                       // chunk i has landed (i+1 may be in flight)
         __syncthreads();
+        if (chunk + 2 < c_end) load_stage((ci + 2) % kSimt2Stages, chunk + 2);
+        cp_async_commit();
         const float* in_s = sm + buf * stage_floats;
         const float* ker_s = in_s + in_stage;
         const int cc_end = p.C - chunk * p.bc < p.bc ? p.C - chunk * p.bc : p.bc;
@@ -425,6 +450,23 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
                 }
 #pragma unroll
                 for (int s = 0; s < KS; ++s) {
+#if CONV_SIMT_FFMA2
+                    unsigned long long kv2[TK / 2];
+#pragma unroll
+                    for (int i = 0; i < TK; i += 4) {
+                        const float4 k4 = *reinterpret_cast<const float4*>(kp + (r * KS + s) * p.bko + i);
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(kv2[i / 2]) : "f"(k4.x), "f"(k4.y));
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(kv2[i / 2 + 1]) : "f"(k4.z), "f"(k4.w));
+                    }
+#pragma unroll
+                    for (int j = 0; j < TW; ++j) {
+                        unsigned long long w2;
+                        asm("mov.b64 %0, {%1, %1};" : "=l"(w2) : "f"(win[j + s]));   // folds into a .F32 operand
+#pragma unroll
+                        for (int i = 0; i < TK / 2; ++i)
+                            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[i][j]) : "l"(kv2[i]), "l"(w2));
+                    }
+#else
                     float kv[TK];
 #pragma unroll
                     for (int i = 0; i < TK; i += 4) {
@@ -435,14 +477,24 @@ __global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict
                     for (int i = 0; i < TK; ++i)
 #pragma unroll
                         for (int j = 0; j < TW; ++j) acc[i][j] = fmaf(kv[i], win[j + s], acc[i][j]);
+#endif
                 }
             }
         }
-        __syncthreads();
     }
 
     if (!valid) return;
     const int h = h0 + row;
+#if CONV_SIMT_FFMA2
+    float acc[TK][TW];
+#pragma unroll
+    for (int i = 0; i < TK / 2; ++i)
+#pragma unroll
+        for (int j = 0; j < TW; ++j) {
+            acc[2 * i][j] = __uint_as_float((uint32_t)acc2[i][j]);
+            acc[2 * i + 1][j] = __uint_as_float((uint32_t)(acc2[i][j] >> 32));
+        }
+#endif
 #pragma unroll
     for (int i = 0; i < TK; ++i) {
         const int k = k0 + kgi * TK + i;
@@ -495,7 +547,7 @@ size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
     const size_t plane = (size_t)t.tn * pb.rows_span(t.th) * row;
     const size_t in_stage = (size_t)t.bc * plane;
     const size_t ker_stage = (size_t)t.bc * pb.R * pb.S * t.kg * t.tk;
-    return 2 * (in_stage + ker_stage) * sizeof(float);
+    return (size_t)(t.ver == 2 ? kSimt2Stages : 2) * (in_stage + ker_stage) * sizeof(float);
 }
 
 // Launch one SIMT kernel instance, opting it in to the largest dynamic smem

@@ -49,6 +49,37 @@ __global__ void __launch_bounds__(256) ffma_kernel(float* out, int iters, float 
     if (s == 1234.5678f) out[blockIdx.x * blockDim.x + threadIdx.x] = s;   // never true in practice; keeps the chains live
 }
 
+// FFMA2 (sm_100: two fp32 FMAs per lane in one instruction on a 64-bit
+// register pair; fma.rn.f32x2): 8 pair chains, the multiplier pair and the
+// broadcast scalar addend-free form the SIMT kernel uses (pair x scalar).
+__global__ void __launch_bounds__(256) ffma2_kernel(float* out, int iters, float a0, float b0) {
+    const float a = a0 + 1e-7f * (float)(threadIdx.x & 7);
+    const float b = b0 - 1e-7f * (float)(threadIdx.x & 3);
+    unsigned long long ap, x[8];
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ap) : "f"(a), "f"(b));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float lo = (float)(threadIdx.x + 2 * j) * 1e-3f, hi = (float)(threadIdx.x + 2 * j + 1) * 1e-3f;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(x[j]) : "f"(lo), "f"(hi));
+    }
+#pragma unroll 1
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                unsigned long long bb;
+                asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(b));
+                asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(x[j]) : "l"(ap), "l"(bb));
+            }
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += __int_as_float((int)x[j]) + __int_as_float((int)(x[j] >> 32));
+    if (s == 1234.5678f) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // ---- tcgen05.mma ------------------------------------------------------------
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
     x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
@@ -195,6 +226,12 @@ int set_smem(F kfn, size_t bytes) {
 API int probe_ffma(float* out, int blocks, int threads, int iters, void* stream) {
     if (!out || blocks < 1 || threads < 32 || threads > 256 || threads % 32 || iters < 1) return -1;
     ffma_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(out, iters, 0.999f, 1e-3f);
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+API int probe_ffma2(float* out, int blocks, int threads, int iters, void* stream) {
+    if (!out || blocks < 1 || threads < 32 || threads > 256 || threads % 32 || iters < 1) return -1;
+    ffma2_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(out, iters, 0.999f, 1e-3f);
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

@@ -48,6 +48,7 @@ def load_probes():
     vp, i, d, sz, u = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t, ctypes.c_uint
     for name, res, args in (
         ("probe_ffma", i, [vp, i, i, i, vp]), ("probe_ffma_flops", d, [i, i, i]),
+        ("probe_ffma2", i, [vp, i, i, i, vp]),
         ("probe_mma", i, [i, i, i, i, vp, vp]), ("probe_mma_flops", d, [i, i, i, i]),
         ("probe_l2_bulk", i, [vp, sz, i, u, i, vp]), ("probe_l2_tiled", i, [vp, sz, i, i, vp]),
         ("probe_l2_tiled_bytes", d, [i, i]),
@@ -102,6 +103,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--sustain", type=float, default=2.0)
     ap.add_argument("--no-write", action="store_true")
+    ap.add_argument("--only", default=None, help="comma-separated probe keys to run (study; implies --no-write)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -109,6 +111,10 @@ def main():
     sms = props.multi_processor_count
     lib = load_probes()
     res = {}
+    only = set(args.only.split(",")) if args.only else None
+
+    def want(k):
+        return only is None or k in only
 
     def chk(rc, what):
         if rc != 0:
@@ -116,6 +122,22 @@ def main():
 
     # ---- FFMA: 4 CTAs x 256 threads per SM (32 warps, 16 chains each)
     out = torch.empty(sms * 4 * 256, device=dev)
+    if want("ffma"):
+        ffma_probes(lib, res, out, sms, args, dev, chk)
+    if want("mma"):
+        mma_probes(lib, res, sms, args, dev, chk)
+    if want("l2"):
+        l2_probes(lib, res, sms, args, dev, chk)
+    if want("lib"):
+        lib_probes(res, args, dev)
+    if only is not None:
+        print(json.dumps({k: {"value": v["value"], "unit": v["unit"], "clocks": v["clocks"].get("sm_mhz")}
+                          for k, v in res.items()}))
+        return
+    finish(res, sms, args, dev)
+
+
+def ffma_probes(lib, res, out, sms, args, dev, chk):
     blocks, threads, iters = sms * 4, 256, 4000
     fl = lib.probe_ffma_flops(blocks, threads, iters)
     b, s, c = timed(lambda st: chk(lib.probe_ffma(out.data_ptr(), blocks, threads, iters, st.cuda_stream), "ffma"),
@@ -125,7 +147,15 @@ def main():
     sm_clk = c.get("sm_mhz") or 1965.0
     res["ffma_fp32"]["flop_per_clk_per_sm"] = round(fl / b / (sm_clk * 1e6) / sms, 1)
 
-    # ---- tcgen05.mma issue rate
+    b, s, c = timed(lambda st: chk(lib.probe_ffma2(out.data_ptr(), blocks, threads, iters, st.cuda_stream), "ffma2"),
+                    args.reps, args.sustain, dev)
+    res["ffma2_fp32"] = rec("ffma2", "TFLOP/s", fl, b, s, c,
+                            f"{blocks}x{threads} threads, 8 register-pair FFMA2 (fma.rn.f32x2) chains each, "
+                            f"pair x broadcast scalar, 8*{iters} steps")
+
+
+
+def mma_probes(lib, res, sms, args, dev, chk):
     for bf16 in (1, 0):
         for cg in (1, 2):
             iters = 6000 if bf16 else 3000
@@ -140,7 +170,9 @@ def main():
             clk = c.get("sm_mhz") or 1965.0
             res[key]["flop_per_clk_per_sm"] = round(fl / b / (clk * 1e6) / grid, 1)
 
-    # ---- L2 -> SMEM
+
+
+def l2_probes(lib, res, sms, args, dev, chk):
     buf = torch.randint(0, 255, (32 << 20,), dtype=torch.uint8, device=dev)
     buf.sum()                                   # resident in L2
     chunk, iters = 32768, 3000
@@ -157,7 +189,10 @@ def main():
                                f"2-D tiled TMA 128x128 B boxes, 128-B swizzle, 2 boxes x 6 stages in flight, {sms} CTAs")
     del buf
 
-    # ---- library cross-checks (the driver's method for MEASURED_PEAKS.json)
+
+
+def lib_probes(res, args, dev):
+    """library cross-checks (the driver's method for MEASURED_PEAKS.json)"""
     n = 8192
     for name, dt, tf32 in (("cublas_bf16", torch.bfloat16, False), ("cublas_tf32", torch.float32, True),
                            ("cublas_fp32", torch.float32, False)):
@@ -176,6 +211,8 @@ def main():
                           scale=1e9)
     del a, a2
 
+
+def finish(res, sms, args, dev):
     doc = {
         "gpu": torch.cuda.get_device_name(dev), "sms": sms, "when": datetime.datetime.now(datetime.timezone.utc).isoformat(),
         "torch": torch.__version__, "probes": res,

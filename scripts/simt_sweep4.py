@@ -45,32 +45,37 @@ def timeit(plan, i, k, o, ws, n=10):
     return float(np.mean([a.elapsed_time(b) for a, b in ev])) * 1e3
 
 
-name = sys.argv[1] if len(sys.argv) > 1 else "batched"
-sh = CONFIGS[name]
-xi, wi = make_inputs(sh, seed=0)
-i, k = xi.cuda(), wi.cuda()
-ref = oracle.conv_eq1(xi.numpy()[:2], wi.numpy())
-specs = [None]
-for tk, tw in ((4, 14), (4, 7), (8, 7)):
-    groups = (sh.W + tw - 1) // tw
-    for th, tn, kg, bc in itertools.product((1, 2, 7, 14), (1, 2, 4, 8, 16, 32), (2, 4, 8, 16), (2, 4, 8)):
-        slots = tn * th * groups
-        if slots % 32 or slots > 128 or sh.H % th:
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "batched"
+    sh = CONFIGS[name]
+    xi, wi = make_inputs(sh, seed=0)
+    i, k = xi.cuda(), wi.cuda()
+    ref = oracle.conv_eq1(xi.numpy()[:2], wi.numpy())
+    specs = [None]
+    for tk, tw in ((4, 14), (4, 7), (8, 7)):
+        groups = (sh.W + tw - 1) // tw
+        for th, tn, kg, bc in itertools.product((1, 2, 7, 14), (1, 2, 4, 8, 16, 32), (2, 4, 8, 16), (2, 4, 8)):
+            slots = tn * th * groups
+            if slots % 32 or slots > 128 or sh.H % th:
+                continue
+            pw = slots // 32
+            if 32 * kg * pw > 512:
+                continue
+            specs.append(f"ver=2,tk={tk},tw={tw},kg={kg},pw={pw},tn={tn},th={th},bc={bc}")
+    for spec in specs:
+        try:
+            plan = conv.ConvPlan(*sh.as_tuple(), path="fp32_simt", tile=spec)
+        except conv.ConvError as e:
+            print(json.dumps({"spec": spec, "error": str(e)[:100]}), flush=True)
             continue
-        pw = slots // 32
-        if 32 * kg * pw > 512:
-            continue
-        specs.append(f"ver=2,tk={tk},tw={tw},kg={kg},pw={pw},tn={tn},th={th},bc={bc}")
-for spec in specs:
-    try:
-        plan = conv.ConvPlan(*sh.as_tuple(), path="fp32_simt", tile=spec)
-    except conv.ConvError as e:
-        print(json.dumps({"spec": spec, "error": str(e)[:100]}), flush=True)
-        continue
-    o, ws = plan.new_output(), plan.new_workspace()
-    us = timeit(plan, i, k, o, ws)
-    got = o[:2].cpu().numpy().astype(np.float64)
-    rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
-    d = plan.describe()
-    print(json.dumps({"spec": spec, "tile": d["tile"], "us": round(us, 1), "tflops": round(sh.flops / us / 1e6, 2),
-                      "model_us": round(d["model"]["model_us"], 1), "rel": rel}), flush=True)
+        o, ws = plan.new_output(), plan.new_workspace()
+        us = timeit(plan, i, k, o, ws)
+        got = o[:2].cpu().numpy().astype(np.float64)
+        rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        d = plan.describe()
+        print(json.dumps({"spec": spec, "tile": d["tile"], "us": round(us, 1), "tflops": round(sh.flops / us / 1e6, 2),
+                          "model_us": round(d["model"]["model_us"], 1), "rel": rel}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
