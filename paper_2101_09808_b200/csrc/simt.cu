@@ -285,7 +285,7 @@ struct Simt2Params {
 
 static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth
 #ifndef CONV_SIMT_FFMA2
-#define CONV_SIMT_FFMA2 1                  // v2 inner product on FFMA2 (0: scalar FFMA, A/B builds)
+#define CONV_SIMT_FFMA2 0                  // 1: v2 inner product on FFMA2 (A/B: r02 measured 4 % slower)
 #endif
 
 template <int TK, int TW, int KR, int KS, bool SPLITC>   // KR = 0: runtime R
