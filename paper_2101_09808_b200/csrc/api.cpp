@@ -104,6 +104,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 static size_t ws_bytes(const conv_plan* p) {
     if (p->path == CONV_PATH_FP32_SIMT) return align256(simt_ws_bytes(p->pb, p->simt));
+    if (p->tc.halo) return align256(halo_ws_bytes(p->pb, p->path == CONV_PATH_BF16));   // the B image only
     // aux region: the fused transform's flags, or split-K's counters + partials
     const Problem& kp = p->split ? p->ps : (p->expand ? p->pe : p->pb);   // the problem the tensor kernel runs
     const size_t aux = p->tc.fuse ? p->tcl.flag_bytes : tc_split_bytes(kp, p->tcl, p->tc);
@@ -118,7 +119,8 @@ static bool select_tensor(conv_plan* p, bool bf16, TcTile& tt, ModelResult& rt, 
     const Problem& pb = p->pb;
     // automatic only when the fused transform / split-K are not forced
     expand = p->force_tc.expand >= 0 ? p->force_tc.expand == 1
-                                     : expand_useful(pb, bf16) && p->force_tc.fuse != 1 && p->force_tc.splits <= 1;
+                                     : expand_useful(pb, bf16) && p->force_tc.fuse != 1 && p->force_tc.splits <= 1 &&
+                                           p->force_tc.halo != 1;
     if (expand && (p->force_tc.fuse == 1 || p->force_tc.splits > 1)) {
         why = "the tap expansion runs without the fused transform and split-K";
         return false;
@@ -128,7 +130,22 @@ static bool select_tensor(conv_plan* p, bool bf16, TcTile& tt, ModelResult& rt, 
     TcForce f = p->force_tc;
     f.fuse = 0;
     f.splits = 1;
+    f.halo = 0;                                   // the halo kernel reads the real NCHW input
     if (!select_tc(pe, p->dev, bf16, tt, rt, f, why)) return false;
+    // tiny-C layers the halo kernel can run in one launch: the faster (modeled)
+    if (p->force_tc.expand < 0 && p->force_tc.halo != 0) {
+        TcTile th;
+        ModelResult rh;
+        std::string w2;
+        TcForce fh = p->force_tc;
+        fh.halo = 1;
+        if (halo_ok(pb, bf16, p->dev.smem_optin) && select_tc(pb, p->dev, bf16, th, rh, fh, w2) &&
+            rh.model_us < rt.model_us) {
+            tt = th;
+            rt = rh;
+            expand = false;
+        }
+    }
     // the expansion reads In (fp32) and Ker and writes the expanded workspace
     // instead of the plain repack the model charged for pe
     return true;
@@ -147,6 +164,7 @@ static bool select_split(conv_plan* p, TcTile& tt, ModelResult& rt, Problem& ps,
     f.fuse = 0;
     f.expand = 0;
     f.splits = 1;
+    f.halo = 0;                                   // the halo kernel reads the real NCHW input
     if (!select_tc(ps, p->dev, true, tt, rt, f, why)) return false;
     const double over = 4.0 * ((double)ps.in_elems() - (double)p->pb.in_elems()) +
                         4.0 * ((double)ps.ker_elems() - (double)p->pb.ker_elems());
@@ -397,7 +415,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             std::string key = kv.substr(0, eq);
             char* end = nullptr;
             long v = strtol(kv.c_str() + eq + 1, &end, 10);
-            const long vmin = (key == "fuse" || key == "pre_c" || key == "expand") ? 0 : 1;
+            const long vmin = (key == "fuse" || key == "pre_c" || key == "expand" || key == "halo") ? 0 : 1;
             if (!end || *end || v < vmin || v > 4096) return fail(CONV_ERR_INVALID_ARGUMENT, "bad value in '%s'", kv.c_str());
             if (key == "bn") ft.bn = (int)v;
             else if (key == "stages") ft.stages = (int)v;
@@ -408,6 +426,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "pre_c") ft.pre_c = (int)v;
             else if (key == "expand") ft.expand = v ? 1 : 0;
             else if (key == "split") ft.split = (int)v;
+            else if (key == "halo") ft.halo = v ? 1 : 0;
             else if (key == "tk") { fs.tk = (int)v; mask |= 1; }
             else if (key == "tw") { fs.tw = (int)v; mask |= 2; }
             else if (key == "kg") { fs.kg = (int)v; mask |= 4; }
@@ -445,7 +464,7 @@ extern "C" size_t conv_plan_workspace_bytes(const conv_plan* p) { return p ? ws_
 
 extern "C" int conv_plan_num_kernels(const conv_plan* p) {
     if (!p) return -1;
-    // tensor paths: layout transform + main; SIMT: pack + main (+ the split-C reduce)
+    // tensor paths: layout transform (halo plans: the Ker pack) + main; SIMT: pack + main (+ the split-C reduce)
     return p->path == CONV_PATH_FP32_SIMT ? simt_num_kernels(p->simt) : 2;
 }
 
@@ -481,8 +500,8 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
                  p->simt.splits, 32 * p->simt.kg * p->simt.pw);
     } else {
-        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"split\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
-                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->split, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
+        snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"split\":%d,\"halo\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
+                 128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->split, p->tc.halo, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
                  p->tc.fuse ? std::min(p->tc.pre_c, p->tcl.Cp) : 0,
                  p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
     }
@@ -531,7 +550,7 @@ static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0
         uint8_t* wsb = static_cast<uint8_t*>(ws);
         const size_t per_img = p->tcl.in_ws_bytes / (size_t)p->pb.N;
         void* in_ws = wsb + per_img * (size_t)n0;
-        void* ker_ws = wsb + align256(p->tcl.in_ws_bytes);
+        void* ker_ws = p->tc.halo ? ws : wsb + align256(p->tcl.in_ws_bytes);   // halo: the B image
         void* flag_ws = (p->tc.fuse || p->tc.splits > 1) ? wsb + align256(p->tcl.in_ws_bytes) + align256(p->tcl.ker_ws_bytes)
                                                          : nullptr;
         if (p->split) {

@@ -133,6 +133,12 @@ extern "C" double conv_model_dv_matmul(const int perm[3], const double Nx[3], co
 namespace conv {
 
 static const double kLaunchUs = 2.0;      // per-kernel launch + ramp
+// halo kernel (single launch): fixed per-CTA chain (barrier init, TMEM
+// alloc, Ker conversion, MMA issue), staged-input bandwidth per SM and the
+// epilogue's store bandwidth per SM -- first estimates, r02
+static const double kHaloFixedUs = 1.5;
+static const double kHaloBW = 60e9;
+static const double kHaloEpiBW = 40e9;
 static const double kTileOverheadUs = 0.25;  // per wave: pipeline fill + epilogue drain
 
 static double wave_eff(long tiles, long slots) {
@@ -372,6 +378,43 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
                 }
             }
         }
+    }
+    // the single-launch halo kernel (halo.cu): one CTA per 128-pixel tile of
+    // the padded grid, the whole layer in one launch -- modeled as launch +
+    // the per-CTA chain (staged input at ~kHaloBW per SM, the R*S*rowb/32
+    // MMAs, the 128 x K fp32 epilogue) per wave
+    const bool halo_forced = f.halo == 1;
+    if (f.halo != 0 && halo_ok(pb, bf16, dev.smem_optin) && !f.bn && !f.cg && !f.kbs && f.splits <= 1 &&
+        f.fuse != 1) {
+        ModelResult r;
+        const int64_t ctas = halo_ctas(pb);
+        const double waves = ceil((double)ctas / dev.sms);
+        const double stage_bytes = 4.0 * pb.C * (128.0 + (pb.R - 1) * (double)pb.Win() + pb.S - 1);
+        const double epi_bytes = 128.0 * pb.K * 4.0;
+        const double per_cta_us = kHaloFixedUs + stage_bytes / kHaloBW * 1e6 + epi_bytes / kHaloEpiBW * 1e6;
+        r.tiles = (long)ctas;
+        r.ctas = (long)std::min<int64_t>(ctas, dev.sms);
+        r.wave_eff = (double)ctas / (waves * dev.sms);
+        const double flops_issued = 2.0 * (double)ctas * 128.0 * pb.K * pb.R * pb.S * pb.C;
+        r.t_comp_us = flops_issued / (bf16 ? dev.peak_bf16 : dev.peak_tf32) * 1e6;
+        r.dv_l2_smem = (double)ctas * (stage_bytes + 4.0 * pb.ker_elems());
+        r.t_l2_us = r.dv_l2_smem / dev.bw_l2 * 1e6;
+        r.dv_hbm = 4.0 * (pb.in_elems() + pb.ker_elems() + pb.out_elems());
+        r.t_hbm_us = r.dv_hbm / dev.bw_hbm * 1e6;
+        r.model_us = kLaunchUs + std::max({waves * per_cta_us, r.t_hbm_us, r.t_l2_us});
+        r.smem = 0;
+        if (halo_forced || !found || r.model_us < best_r.model_us) {
+            best = TcTile();
+            best.halo = 1;
+            best.bn = pb.K;
+            best.stages = 1;
+            best_r = r;
+            found = true;
+        }
+    } else if (halo_forced) {
+        why = "layer not eligible for the halo kernel (stride/dilation/padding 1/1/0, C*elem <= 128 B, K <= 256, "
+              "smem) or other tile keys forced";
+        return false;
     }
     if (!found) why = "no tensor-path tile fits shared memory / TMEM for this request";
     return found;

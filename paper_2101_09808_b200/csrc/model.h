@@ -26,7 +26,8 @@ struct TcForce {
     int fuse = -1, pre_c = -1;
     int expand = -1;        // tiny-C tap expansion: -1 auto (expand_useful), 0 off, 1 on
     int split = 0;          // FP32_TC piece pairs: 0 default (6), 6 or 9
-    int bn_max = 0;         // largest BN considered (0: any; FP32_TC's promoted epilogue: 128)
+    int bn_max = 0;         // largest BN considered (0: any)
+    int halo = -1;          // halo kernel: -1 auto, 0 off, 1 forced
 };
 
 ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTile& t);

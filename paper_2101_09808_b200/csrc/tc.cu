@@ -1200,6 +1200,10 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
                    const float* in, const float* ker, float* out, void* in_ws, void* ker_ws, void* flag_ws,
                    cudaStream_t st, int num_sms, cudaEvent_t* ev, std::string& err, const Problem* expand_src,
                    int split_pairs) {
+    if (t.halo) {                          // the single-launch halo kernel (halo.cu)
+        if (expand_src || split_pairs) { err = "the halo kernel runs plain problems only"; return cudaErrorInvalidValue; }
+        return halo_run(pb, bf16, in, ker, out, ker_ws, st, ev, err);
+    }
     if (expand_src && !split_pairs && (t.fuse || t.splits > 1)) { err = "tap-expanded plans run without the fused transform and split-K"; return cudaErrorInvalidValue; }
     if (split_pairs && (!expand_src || !bf16 || t.fuse || t.splits > 1)) {
         err = "FP32_TC plans run the promoted bf16 kernel: no fused transform, no split-K";

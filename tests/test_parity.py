@@ -346,7 +346,7 @@ def test_auto_path_and_describe():
 
 def test_argument_errors():
     sh = CONFIGS["tiny"]
-    plan = conv.ConvPlan(*sh.as_tuple(), path="tf32")
+    plan = conv.ConvPlan(*sh.as_tuple(), path="tf32", tile="halo=0")
     inp, ker = make_inputs(sh, seed=0)
     i, k = inp.cuda(), ker.cuda()
     out = plan.new_output()
@@ -767,7 +767,7 @@ def test_tap_expansion_auto_graph_and_host(path):
     chunks: each chunk expands its own images) is bit-identical."""
     from paper_2101_09808_b200.inputs import TABLE1
     sh = Shape.strided(4, 32, 3, 68, 68, 3, 3, 1)
-    plan = conv.ConvPlan(*sh.as_tuple(), path=path, **sh.plan_kwargs())
+    plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile="halo=0", **sh.plan_kwargs())
     assert plan.describe()["tile"]["expand"] == 1
     for name in ("Y0", "R1"):
         t = TABLE1[name]
@@ -1030,3 +1030,37 @@ def test_fp32_tc_extreme_magnitudes():
     got, _ = run(sh, inp, ker, "fp32_tc")
     ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
     assert rel_l2(got, ref) <= 1e-5
+
+
+HALO = [CONFIGS["tiny"], CONFIGS["r2"], CONFIGS["pw"], CONFIGS["det"],
+        Shape(N=3, K=40, C=5, H=9, W=14, R=3, S=3),           # tiny C, several images, ragged K
+        Shape(N=2, K=256, C=64, H=13, W=11, R=3, S=3),        # BN 256, odd extents
+        Shape(N=1, K=7, C=17, H=30, W=29, R=2, S=3),          # R != S, ragged everything
+        Shape(N=1, K=96, C=24, H=20, W=40, R=5, S=5)]         # 5x5 taps, halo 4 rows
+
+
+@pytest.mark.parametrize("path", ["bf16", "tf32"])
+@pytest.mark.parametrize("shape", HALO, ids=lambda s: "x".join(map(str, s.as_tuple())))
+def test_halo_kernel_parity(path, shape):
+    """The single-launch halo kernel (halo.cu: the input tile staged once per
+    CTA, filter taps as shifted tcgen05 descriptors over the padded output
+    grid): oracle parity on real inputs (path tolerance; 1e-5 against the
+    rounded-input oracle), bit-exact on the integer twin, and bit-identical
+    to the two-launch im2col kernel (same k order: taps, then channels)."""
+    inp, ker = make_inputs(shape, seed=170)
+    try:
+        got, plan = run(shape, inp, ker, path, tile="halo=1")
+    except conv.ConvError as e:
+        assert e.status == conv.CONV_ERR_INFEASIBLE
+        pytest.skip(f"not eligible: {e}")
+    d = plan.describe()
+    assert d["tile"]["halo"] == 1 and d["kernels"] == 2 and 0 < d["workspace_bytes"] <= 9 * 256 * 128 * 4
+    ref = oracle.conv_eq1(inp.numpy(), ker.numpy())
+    assert rel_l2(got, ref) <= TOL[path]
+    ref_r = oracle.conv_eq1(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()))
+    assert rel_l2(got, ref_r) <= 1e-5
+    plain, _ = run(shape, inp, ker, path, tile="fuse=0,cg=1,splits=1,expand=0")
+    assert np.array_equal(got, plain)
+    xi, wi = make_inputs(shape, seed=171, kind="int")
+    goti, _ = run(shape, xi, wi, path, tile="halo=1")
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
