@@ -132,20 +132,6 @@ static bool select_tensor(conv_plan* p, bool bf16, TcTile& tt, ModelResult& rt, 
     f.splits = 1;
     f.halo = 0;                                   // the halo kernel reads the real NCHW input
     if (!select_tc(pe, p->dev, bf16, tt, rt, f, why)) return false;
-    // tiny-C layers the halo kernel can run in one launch: the faster (modeled)
-    if (p->force_tc.expand < 0 && p->force_tc.halo != 0) {
-        TcTile th;
-        ModelResult rh;
-        std::string w2;
-        TcForce fh = p->force_tc;
-        fh.halo = 1;
-        if (halo_ok(pb, bf16, p->dev.smem_optin) && select_tc(pb, p->dev, bf16, th, rh, fh, w2) &&
-            rh.model_us < rt.model_us) {
-            tt = th;
-            rt = rh;
-            expand = false;
-        }
-    }
     // the expansion reads In (fp32) and Ker and writes the expanded workspace
     // instead of the plain repack the model charged for pe
     return true;

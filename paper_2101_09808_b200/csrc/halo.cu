@@ -18,14 +18,15 @@
 //      bf16 / RNA tf32; rows k >= K, channels >= C zero) -- converted once,
 //      not once per CTA (a per-CTA conversion was measured 2x slower: its
 //      strided L2 loads serialise on latency);
-//   conv_halo_tcgen05, one CTA (4 warps) per 128-pixel tile of one image, all
+//   conv_halo_tcgen05, one CTA (8 warps) per 128-pixel tile of one image, all
 //   K output channels (BN = K rounded up to 32..256):
 //   1. thread 0: cp.async.bulk of the tile's input pixel range (plus halo,
 //      (R-1)*Win + S-1 pixels) from every NCHW fp32 channel plane into an
 //      fp32 staging area; warp 0 allocates TMEM;
 //   2. all threads: staging -> the swizzled K-major A tile (one row per
 //      input pixel, channels C..Cp-1 zero) -- all of this overlaps the pack;
-//   3. thread 0: griddepcontrol.wait, then ONE bulk copy of the B image;
+//   3. thread 0, right after the input copies: griddepcontrol.wait, then
+//      ONE bulk copy of the B image (its latency overlaps step 2);
 //   4. thread 0: R*S*(row bytes / 32) tcgen05.mma (M = 128, N = BN) into TMEM,
 //      tap (r, s) = A descriptor start + (r*Win + s) rows;
 //   5. all warps: TMEM -> registers -> NCHW Out (valid pixels only).
@@ -111,8 +112,10 @@ __global__ void __launch_bounds__(256) halo_ker_pack(const HaloParams p, uint8_t
     }
 }
 
+static constexpr int kThreadsH = 256;   // 8 warps: two per TMEM lane quadrant
+
 template <int BN, bool BF16>
-__global__ void __launch_bounds__(128, 1) conv_halo_tcgen05(const HaloParams p) {
+__global__ void __launch_bounds__(kThreadsH, 1) conv_halo_tcgen05(const HaloParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* A = smem + p.a_off;
@@ -138,32 +141,42 @@ __global__ void __launch_bounds__(128, 1) conv_halo_tcgen05(const HaloParams p) 
         const float* src = p.in + ((int64_t)n * p.C) * p.P + p0;
         for (int c = 0; c < p.C; ++c)
             bulk_load_g2s(stage + (size_t)c * p.stage_px, src + (int64_t)c * p.P, bytes, &bar_in);
+        // the B image, written by the pack grid (programmatic dependency):
+        // requested now, so that its latency overlaps the input conversion
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        const uint32_t bbytes = (uint32_t)(p.R * p.S) * p.b_tap_bytes;
+        mbar_arrive_expect_tx(&bar_b, bbytes);
+        for (uint32_t o = 0; o < bbytes; o += 32768)
+            bulk_load_g2s(B + o, p.bimg + o, min(32768u, bbytes - o), &bar_b);
     }
     if (warp == 0) tmem_alloc(&tmem_slot, kCols);
     __syncthreads();                                    // barrier inits visible to every waiter
 
     const int chunks = p.rowb / 16;
 
-    // 3. staged input -> A rows (pixel r of the tile's range), once landed
+    // 2. staged input -> A rows (pixel r of the tile's range), once landed;
+    // a unit = 4 consecutive pixels x one 16-B channel chunk: kEpc LDS.128
+    // (one per channel, 4 pixels each), 4 STS.128 (one per pixel row)
     mbar_wait(&bar_in, 0);
-    for (int r = tid; r < p.rows_a; r += 128) {
-        for (int q = 0; q < chunks; ++q) {
-            float v[8];
+    {
+        const int groups = p.rows_a / 4;               // rows_a is a multiple of 8
+        for (int u = tid; u < groups * chunks; u += kThreadsH) {
+            const int q = u / groups, r0 = (u - q * groups) * 4;
+            float4 x[8];
 #pragma unroll
             for (int e = 0; e < kEpc; ++e) {
                 const int c = q * kEpc + e;
-                v[e] = (c < p.C && r < npx) ? stage[(size_t)c * p.stage_px + r] : 0.0f;
+                x[e] = c < p.C ? *reinterpret_cast<const float4*>(stage + (size_t)c * p.stage_px + r0)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            *reinterpret_cast<uint4*>(A + halo_swz(r, q, p.rowb)) = halo_pack<BF16>(v);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < kEpc; ++e) v[e] = i == 0 ? x[e].x : i == 1 ? x[e].y : i == 2 ? x[e].z : x[e].w;
+                *reinterpret_cast<uint4*>(A + halo_swz(r0 + i, q, p.rowb)) = halo_pack<BF16>(v);
+            }
         }
-    }
-    // the B image: written by the pack grid (programmatic dependency)
-    if (tid == 0) {
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        const uint32_t bbytes = (uint32_t)(p.R * p.S) * p.b_tap_bytes;
-        mbar_arrive_expect_tx(&bar_b, bbytes);
-        for (uint32_t o = 0; o < bbytes; o += 32768)
-            bulk_load_g2s(B + o, p.bimg + o, min(32768u, bbytes - o), &bar_b);
     }
     fence_proxy_async_smem();                           // generic smem writes -> tensor core reads
     tc_fence_before();
@@ -171,39 +184,49 @@ __global__ void __launch_bounds__(128, 1) conv_halo_tcgen05(const HaloParams p) 
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
 
-    // 4. the MMAs: tap (r, s) reads the A tile from row r*Win + s
-    if (tid == 0) {
+    // 4. the MMAs: tap (r, s) reads the A tile from row r*Win + s; the
+    // whole warp runs the loop (descriptors in uniform registers), one
+    // elected lane issues.  (Traced r02 on det: the 18 dependent N = 64 MMAs
+    // into one accumulator take ~1.6 us -- ~180 cycles each, the MMA
+    // latency, not its 50-cycle issue interval.)
+    if (warp == 0) {
         mbar_wait(&bar_b, 0);
         const uint32_t layout = umma_layout_for_swizzle((uint32_t)p.rowb);
         const uint32_t idesc = make_idesc(BF16 ? 1u : 2u, 128, BN);
         const uint32_t a0 = smem_u32(A), b0 = smem_u32(B);
+        const int ksteps = p.rowb / 32;
         uint32_t accum = 0;
         for (int r = 0; r < p.R; ++r)
             for (int s = 0; s < p.S; ++s) {
                 const uint64_t ad = make_sdesc(a0 + (uint32_t)(r * p.Win + s) * p.rowb, 8 * p.rowb, layout);
                 const uint64_t bd = make_sdesc(b0 + (uint32_t)(r * p.S + s) * p.b_tap_bytes, 8 * p.rowb, layout);
-                for (int kk = 0; kk < p.rowb / 32; ++kk) {
-                    if (BF16) mma_bf16(tmem, ad + 2 * kk, bd + 2 * kk, idesc, accum);
-                    else mma_tf32(tmem, ad + 2 * kk, bd + 2 * kk, idesc, accum);
-                    accum = 1;
+                if (elect_one_sync()) {
+                    for (int kk = 0; kk < ksteps; ++kk) {
+                        if (BF16) mma_bf16(tmem, ad + 2 * kk, bd + 2 * kk, idesc, accum | (uint32_t)kk);
+                        else mma_tf32(tmem, ad + 2 * kk, bd + 2 * kk, idesc, accum | (uint32_t)kk);
+                    }
                 }
+                __syncwarp();
+                accum = 1;
             }
-        tc_commit(&bar_mma);
+        if (elect_one_sync()) tc_commit(&bar_mma);
+        __syncwarp();
     }
-    __syncwarp();
 
-    // 5. epilogue: warp w owns TMEM lanes 32w.. = tile pixels p0 + 32w + lane
+    // 5. epilogue: warp w owns TMEM lanes 32(w%4).. = tile pixels
+    // p0 + 32(w%4) + lane and the column half w/4 (32-column steps)
     mbar_wait_sleep(&bar_mma, 0, 64);
     tc_fence_after();
-    const int pix = p0 + warp * 32 + lane;
+    const int qd = warp & 3;
+    const int pix = p0 + qd * 32 + lane;
     const int h = pix / p.Win, w = pix - h * p.Win;
     const bool valid = h < p.H && w < p.W;
     float* obase = p.out + ((int64_t)n * p.K) * p.H * p.W + (int64_t)h * p.W + w;
     const int64_t HW = (int64_t)p.H * p.W;
 #pragma unroll 1
-    for (int j0 = 0; j0 < BN; j0 += 32) {
+    for (int j0 = (warp >> 2) * 32; j0 < BN; j0 += 64) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)j0, v);
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)j0, v);
         tmem_ld_wait();
         if (valid) {
 #pragma unroll
@@ -270,7 +293,7 @@ static cudaError_t launch_halo_t(const HaloParams& p, int grid, size_t smem, cud
     if (cudaError_t e = opt.ensure(kfn, smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(kThreadsH);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

@@ -383,8 +383,14 @@ bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, Mo
     // the padded grid, the whole layer in one launch -- modeled as launch +
     // the per-CTA chain (staged input at ~kHaloBW per SM, the R*S*rowb/32
     // MMAs, the 128 x K fp32 epilogue) per wave
+    // Only on request (tile key halo=1): measured r02 (profiles/r02/
+    // bench_small_halo_*.jsonl) it does not beat the two-launch im2col plans
+    // on the BASELINE layers (det 14.4 vs 13.8 us, r2 14.4 vs 12.0, pw 18.4 vs
+    // 10.3, tiny 10.4 vs 10.4): the per-CTA chain -- cold input copy 2.3 us,
+    // conversion 0.9, dependent MMAs 1.7, epilogue 1.7 -- is not shorter
+    // than the im2col kernel's, and the protocol floor of one launch is 6 us.
     const bool halo_forced = f.halo == 1;
-    if (f.halo != 0 && halo_ok(pb, bf16, dev.smem_optin) && !f.bn && !f.cg && !f.kbs && f.splits <= 1 &&
+    if (halo_forced && halo_ok(pb, bf16, dev.smem_optin) && !f.bn && !f.cg && !f.kbs && f.splits <= 1 &&
         f.fuse != 1) {
         ModelResult r;
         const int64_t ctas = halo_ctas(pb);

@@ -86,6 +86,62 @@ __global__ void __launch_bounds__(128) probe(float* out) {
     if (warp == 0) tmem_dealloc(tmem, 32);
 }
 
+// timing: 256 back-to-back MMAs (M=128, N=64 / 256) from a descriptor
+// starting `t` rows into the tile; clock64 span, one CTA
+template <int ROWB, int NN>
+__global__ void __launch_bounds__(128) probe_time(long long* cyc) {
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    for (int i = threadIdx.x; i < (kRowsA + NN) * ROWB / 4; i += 128) reinterpret_cast<uint32_t*>(sm)[i] = 0x3f803f80u;
+    __shared__ uint32_t tslot;
+    __shared__ __align__(8) uint64_t bar;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (warp == 0) tmem_alloc(&tslot, NN < 32 ? 32 : NN);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    constexpr uint32_t layout = ROWB == 128 ? 2u : 4u;
+    constexpr uint32_t idesc = make_idesc(1u, 128, NN);
+    uint32_t phase = 0;
+    for (int t = 0; t < 10; ++t) {
+        if (threadIdx.x == 0) {
+            const uint64_t bd = make_sdesc(smem_u32(sm + kRowsA * ROWB), 8 * ROWB, layout);
+            const long long c0 = clock64();
+            for (int i = 0; i < 256; ++i) {
+                const int sh = (t < 8 ? t : (t == 8 ? 8 : 16)) + (i & 1) * 8;     // shifts t, t+8 alternate
+                const uint64_t ad = make_sdesc(smem_u32(sm) + sh * ROWB, 8 * ROWB, layout);
+                mma_bf16(tslot, ad, bd, idesc, 1);
+            }
+            tc_commit(&bar);
+            mbar_wait(&bar, phase);
+            cyc[t] = clock64() - c0;
+        }
+        phase ^= 1;
+        __syncthreads();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc(tslot, NN < 32 ? 32 : NN); }
+}
+
+template <int ROWB, int NN>
+void run_time() {
+    long long* d;
+    cudaMalloc(&d, 16 * sizeof(long long));
+    const size_t smem = 1024 + (kRowsA + NN) * ROWB;
+    cudaFuncSetAttribute(probe_time<ROWB, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int rep = 0; rep < 2; ++rep) probe_time<ROWB, NN><<<1, 128, smem>>>(d);
+    cudaDeviceSynchronize();
+    long long h[16];
+    cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("swizzle %3dB N=%3d: cycles per MMA by start-row shift:", ROWB, NN);
+    for (int t = 0; t < 10; ++t) printf(" %d:%.1f", t < 8 ? t : (t == 8 ? 8 : 16), h[t] / 256.0);
+    printf("\n");
+    cudaFree(d);
+}
+
 template <int ROWB>
 void run() {
     constexpr int K = ROWB / 2;
@@ -119,5 +175,9 @@ void run() {
 int main() {
     run<64>();
     run<128>();
+    run_time<64, 64>();
+    run_time<64, 256>();
+    run_time<128, 64>();
+    run_time<128, 256>();
     return 0;
 }
