@@ -288,8 +288,13 @@ static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth
 #define CONV_SIMT_FFMA2 0                  // 1: v2 inner product on FFMA2 (A/B: r02 measured 4 % slower)
 #endif
 
+// Row-mode TK = 8 instances hold 112 accumulators: at most 256 threads, so
+// that ptxas may give a thread up to 255 registers.
+template <int TK, int TW>
+struct Simt2Threads { static constexpr int value = TK * TW > 64 ? 256 : 512; };
+
 template <int TK, int TW, int KR, int KS, bool SPLITC>   // KR = 0: runtime R
-__global__ void __launch_bounds__(512) conv_direct_simt2(const float* __restrict__ in,
+__global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2(const float* __restrict__ in,
                                                           const float* __restrict__ kerp,
                                                           float* __restrict__ out, const Simt2Params p) {
     extern __shared__ __align__(16) float sm[];
@@ -512,9 +517,13 @@ bool simt_tile_supported(const SimtTile& t) {
     if (t.ver != 2 && t.tw > 8) return false;
     // v2: 4 / 8 pixels per thread (16-B aligned windows), or a whole output
     // row of 7 or 14 pixels (row mode, TK = 4: 56 accumulators)
+    // (row mode with TK = 8 -- 112 accumulators, 254 registers, one 256-thread
+    // CTA per SM -- measured 13 % slower on the batched layer, r02
+    // profiles/r02/simt_sweep_tk8.jsonl; not instantiated)
     if (t.ver == 2 && t.tw != 4 && t.tw != 8 && !((t.tw == 7 || t.tw == 14) && t.tk == 4)) return false;
     const int threads = 32 * t.kg * t.pw;
-    return t.kg >= 1 && t.pw >= 1 && threads <= 512 && t.tn >= 1 && t.th >= 1 && t.bc >= 1;
+    const int max_threads = (t.ver == 2 && t.tk * t.tw > 64) ? 256 : 512;   // Simt2Threads
+    return t.kg >= 1 && t.pw >= 1 && threads <= max_threads && t.tn >= 1 && t.th >= 1 && t.bc >= 1;
 }
 
 bool simt_v2_ok(const Problem& pb) { return pb.U == 1 && pb.D == 1 && pb.ph == 0 && pb.pw == 0 && (pb.S == 1 || pb.S == 3); }

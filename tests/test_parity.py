@@ -1064,3 +1064,64 @@ def test_halo_kernel_parity(path, shape):
     xi, wi = make_inputs(shape, seed=171, kind="int")
     goti, _ = run(shape, xi, wi, path, tile="halo=1")
     assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
+def _guarded(t, pad, fill):
+    """A copy of t placed in the middle of a larger buffer whose `pad`
+    elements on each side hold `fill` (canaries)."""
+    n = t.numel()
+    buf = torch.full((n + 2 * pad,), fill, dtype=torch.float32, device="cuda")
+    buf[pad:pad + n] = t.reshape(-1).cuda()
+    return buf, buf[pad:pad + n].view(t.shape)
+
+
+GUARD_CASES = [
+    ("tiny", CONFIGS["tiny"], "fp32_simt", None), ("tiny", CONFIGS["tiny"], "fp32_tc", None),
+    ("tiny", CONFIGS["tiny"], "tf32", None), ("tiny", CONFIGS["tiny"], "bf16", "halo=1"),
+    ("r2", CONFIGS["r2"], "fp32_simt", None), ("r2", CONFIGS["r2"], "bf16", None),
+    ("fused-2wave", Shape(N=160, K=256, C=256, H=14, W=14, R=3, S=3), "bf16", "fuse=1,cg=2"),
+    ("fused-cg1", Shape(N=24, K=128, C=64, H=14, W=14, R=3, S=3), "tf32", "fuse=1,cg=1"),
+    ("splitk-8", Shape.strided(1, 96, 320, 19, 17, 3, 3, 2, 2, 2, 1), "bf16", "splits=8"),
+    ("splitk-3", Shape(N=1, K=128, C=256, H=7, W=7, R=3, S=3), "tf32", "splits=3"),
+    ("simt-splitc", Shape(N=1, K=64, C=256, H=7, W=7, R=3, S=3), "fp32_simt", "splits=4"),
+    ("fp32tc-promote", Shape(N=2, K=256, C=128, H=14, W=14, R=3, S=3), "fp32_tc", None),
+    ("expand", Shape.strided(2, 32, 3, 34, 34, 3, 3, 1), "bf16", "expand=1"),
+]
+
+
+@pytest.mark.parametrize("case", GUARD_CASES, ids=lambda c: f"{c[0]}-{c[2]}")
+def test_guard_bands_no_out_of_bounds_access(case):
+    """compute-sanitizer is closed on this pool (profiles/r02/sanitizer_closed.log),
+    so out-of-bounds accesses are checked with guard bands instead: Out and
+    the workspace sit between canary regions that must be untouched after the
+    run (no stray writes), In and Ker between NaN regions (a stray read that
+    reached a valid output would make it NaN: the oracle comparison catches
+    it), and two runs are bit-identical (no races on the cross-CTA flags /
+    counters).  The multi-wave fused plan and the split-K plans are the ones
+    whose CTAs wait on each other."""
+    name, sh, path, tile = case
+    pad = 4096
+    inp, ker = make_inputs(sh, seed=180)
+    _, gin = _guarded(inp, pad, float("nan"))
+    _, gker = _guarded(ker, pad, float("nan"))
+    plan = conv.ConvPlan(*sh.as_tuple(), path=path, tile=tile, **sh.plan_kwargs())
+    canary = 1234.5
+    obuf, gout = _guarded(torch.zeros(sh.out_shape), pad, canary)
+    wsn = max(plan.workspace_bytes, 4)
+    wbuf = torch.full(((wsn + 255) // 4 + 2 * pad + 64,), canary, dtype=torch.float32, device="cuda")
+    off = pad + 64 - (pad + 64) % 64                               # 256-B aligned workspace start
+    ws_view = wbuf[off:off + (wsn + 3) // 4]
+    outs = []
+    for _ in range(2):
+        plan.run(gin, gker, gout, ws_view.view(torch.uint8)[:wsn] if plan.workspace_bytes else None)
+        torch.cuda.synchronize()
+        outs.append(gout.clone())
+    assert torch.all(obuf[:pad] == canary) and torch.all(obuf[-pad:] == canary), "write before/after Out"
+    assert torch.all(wbuf[:off] == canary) and torch.all(wbuf[off + (wsn + 3) // 4:] == canary), \
+        "write outside the workspace"
+    assert torch.equal(outs[0], outs[1]), "two runs differ"
+    got = outs[0].cpu().numpy()
+    assert np.all(np.isfinite(got)), "a NaN from outside In / Ker reached an output"
+    pad_hw = (sh.ph, sh.pw)
+    ref = oracle.conv_eq1_padded(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), sh.U, sh.D, pad_hw)
+    assert rel_l2(got, ref) <= 1e-5          # vs the oracle on the path's rounded inputs
