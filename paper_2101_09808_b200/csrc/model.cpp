@@ -16,6 +16,7 @@
 // tile-loop order, wave_eff = tiles / (ceil(tiles / slots) * slots) is Sec. 7's
 // "prod T/PT == num_cores" load-balance term and DV_HBM counts
 // the compulsory traffic plus the layout transforms.
+#include <cstdlib>
 #include <math.h>
 #include <stdio.h>
 #include <string.h>
@@ -437,6 +438,11 @@ static const double kSimtSlowCopy = 72.0;
 // t1_simt_slowcopy16.jsonl) 2695 -> 2681 us (Y0 57.4 -> 47.1, Y2, Y4 -4 %;
 // R7 +8 %, Y5 +3 %).
 static const double kSimtSlowCopy16 = 24.0;
+// (env CONV_SIMT_CHUNK_SYNC overrides it: the selector study of this term)
+static const double kSimtChunkSyncClk = [] {
+    const char* e = getenv("CONV_SIMT_CHUNK_SYNC");
+    return e ? atof(e) : 0.0;
+}();
 
 // Registers per thread of the kernel instance a tile launches (simt.cu
 // dispatch_simt2 / dispatch_simt), as ptxas allocated them in the built
@@ -527,7 +533,9 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
     // a chunk cannot take less than one L2 round trip + two barriers
     const double issue_cyc = (double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff);
-    const double chunk_cyc = std::max(issue_cyc, 2000.0);
+    // (+ a per-chunk synchronisation charge: a study knob, default 0 --
+    // see the bc tie-break in select_simt)
+    const double chunk_cyc = std::max(issue_cyc, 2000.0) + kSimtChunkSyncClk;
     r.issue_cyc = waves * chunks * issue_cyc;
     r.t_comp_us = waves * chunks * chunk_cyc / clk * 1e6;
     // L2 -> SMEM: per CTA, every c-chunk loads the In halo tile and Ker slab
@@ -614,7 +622,13 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
             // issues less (r01b Y23: TK 8 vs 4 both modeled 656 us, measured
             // 1129 vs 1316 us)
             const bool tie = found && fabs(r.model_us - best_r.model_us) <= 0.005 * best_r.model_us;
-            if (!found || (tie ? r.issue_cyc < best_r.issue_cyc : r.model_us < best_r.model_us)) {
+            // and on equal issue as well, the deeper channel chunk (fewer
+            // ring waits / barriers: r02 batched layer bc 8 vs 4, 1303 vs
+            // 1348 us; charging every chunk instead -- CONV_SIMT_CHUNK_SYNC --
+            // lost 2.6 % on the Table-1 total, profiles/r02/t1_simt_sync*.jsonl)
+            const bool issue_tie = tie && fabs(r.issue_cyc - best_r.issue_cyc) <= 0.001 * best_r.issue_cyc;
+            if (!found || (issue_tie ? t.bc > best.bc
+                                     : tie ? r.issue_cyc < best_r.issue_cyc : r.model_us < best_r.model_us)) {
                 best = t; best_r = r; found = true;
             }
         }
