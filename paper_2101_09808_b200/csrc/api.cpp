@@ -137,6 +137,24 @@ static bool select_tensor(conv_plan* p, bool bf16, TcTile& tt, ModelResult& rt, 
     return true;
 }
 
+// FP32_TC layout: the bf16 layout of the split problem; when each piece
+// block is whole k-blocks the NHWC workspace holds the 3 pieces once (3*Cq
+// channels, half of the 6-pair layout) and the kernel maps pair blocks to
+// pieces (tc_run)
+static TcLayout split_layout(const Problem& real, const Problem& ps) {
+    TcLayout L = tc_layout(ps, true);
+    // opt-in (env CONV_SPLIT_COMPACT=1): measured r02 on the batched layer the
+    // compact layout's transform is 16 us shorter (36 vs 52 us) but its main
+    // kernel 7-12 % longer (264-273 vs 244-247 us), a wash (186-200 vs
+    // 194-200 TFLOP/s, same box, alternating) -- default off
+    static const bool compact = getenv("CONV_SPLIT_COMPACT") && atoi(getenv("CONV_SPLIT_COMPACT")) == 1;
+    if (compact && split_compact_ok(real, L.bkc)) {
+        L.a_chan = 3 * split_cq(real.C);
+        L.in_ws_bytes = (size_t)real.N * real.Hin() * real.Win() * L.a_chan * L.elem;
+    }
+    return L;
+}
+
 // FP32_TC selection: the bf16 kernel's tiles on split_problem(pb, npairs)
 // (no fused transform, no tap expansion).  The model charged the layout
 // transform the fp32 read of npairs*Cq input channels; the split launch reads
@@ -181,7 +199,7 @@ static conv_status select(conv_plan* p) {
             int np = 0;
             if (!select_split(p, tt, rt, ps, np, why)) return fail(CONV_ERR_INFEASIBLE, "%s", why.c_str());
             p->tc = tt; p->model = rt; p->path = CONV_PATH_FP32_TC; p->expand = false; p->split = np; p->ps = ps;
-            p->tcl = tc_layout(ps, true);
+            p->tcl = split_layout(pb, ps);
             break;
         }
         case CONV_PATH_TF32:
@@ -208,7 +226,7 @@ static conv_status select(conv_plan* p) {
             if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s; %s", why.c_str(), why_t.c_str());
             if (ok_t && (!ok_s || rt.model_us < rs.model_us)) {
                 p->tc = tt; p->model = rt; p->path = CONV_PATH_FP32_TC; p->expand = false; p->split = np; p->ps = ps;
-                p->tcl = tc_layout(ps, true);
+                p->tcl = split_layout(pb, ps);
             } else {
                 p->simt = st; p->model = rs; p->path = CONV_PATH_FP32_SIMT;
             }

@@ -667,6 +667,8 @@ struct SplitGeom {
     int64_t ker_groups;              // K * RS * Cp / 8 (8 channels = one 16-B store)
     int* zero_ptr;                   // split-K arrival counters to clear
     int zero_n;
+    int in_pairs;                    // In' piece blocks: npairs (pair layout) or 3 (compact: piece q at q*Cq)
+    int in_cp;                       // In' channels per pixel
 };
 
 __device__ __forceinline__ void split3_bf16(float x, float (&v)[3]) {
@@ -742,7 +744,7 @@ __global__ void __launch_bounds__(256) split_repack(const float* __restrict__ in
             }
         }
         __syncthreads();
-        __nv_bfloat16* dst = in_ws + n * P * g.Cp;
+        __nv_bfloat16* dst = in_ws + n * P * g.in_cp;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {              // 64 px x 8 groups of 8 channels / 256 threads
             const int idx = tid + i * 256;
@@ -758,21 +760,21 @@ __global__ void __launch_bounds__(256) split_repack(const float* __restrict__ in
                 for (int q = 0; q < 3; ++q)
                     piece[q] = make_uint4(pack2_bf16(pc[0][q], pc[1][q]), pack2_bf16(pc[2][q], pc[3][q]),
                                           pack2_bf16(pc[4][q], pc[5][q]), pack2_bf16(pc[6][q], pc[7][q]));
-                __nv_bfloat16* d = dst + p * g.Cp + c;
-                for (int pr = 0; pr < g.npairs; ++pr) {
-                    const int q = g.ip[pr];
+                __nv_bfloat16* d = dst + p * g.in_cp + c;
+                for (int pr = 0; pr < g.in_pairs; ++pr) {
+                    const int q = g.in_pairs == 3 ? pr : g.ip[pr];
                     *reinterpret_cast<uint4*>(d + pr * g.Cq) = q == 0 ? piece[0] : (q == 1 ? piece[1] : piece[2]);
                 }
             }
         }
         // the channel tail [npairs * Cq, Cp) is zero (written once, by the
         // first channel tile of each pixel block)
-        const int tail0 = g.npairs * g.Cq, tail_groups = (g.Cp - tail0) / 8;
+        const int tail0 = g.in_pairs * g.Cq, tail_groups = (g.in_cp - tail0) / 8;
         if (ct == 0 && tail_groups > 0) {
             for (int idx = tid; idx < 64 * tail_groups; idx += 256) {
                 const int pl = idx / tail_groups, gq = idx - pl * tail_groups;
                 const int64_t p = p0 + pl;
-                if (p < P) *reinterpret_cast<uint4*>(dst + p * g.Cp + tail0 + gq * 8) = make_uint4(0, 0, 0, 0);
+                if (p < P) *reinterpret_cast<uint4*>(dst + p * g.in_cp + tail0 + gq * 8) = make_uint4(0, 0, 0, 0);
             }
         }
     }
@@ -781,7 +783,7 @@ __global__ void __launch_bounds__(256) split_repack(const float* __restrict__ in
 }
 
 cudaError_t launch_split(const Problem& pb, int Cp, int npairs, const float* in, const float* ker, void* in_ws,
-                         void* ker_ws, cudaStream_t st, cudaEvent_t* ev, int* zero_ptr, int zero_n) {
+                         void* ker_ws, cudaStream_t st, cudaEvent_t* ev, int* zero_ptr, int zero_n, bool compact) {
     SplitGeom g;
     const SplitPairs sp = split_pairs(npairs);
     if (sp.n == 0) return cudaErrorInvalidValue;
@@ -795,6 +797,8 @@ cudaError_t launch_split(const Problem& pb, int Cp, int npairs, const float* in,
         g.kp[i] = sp.kp[i];
     }
     if (Cp % 8 || Cp < g.npairs * g.Cq) return cudaErrorInvalidValue;
+    g.in_pairs = compact ? 3 : g.npairs;
+    g.in_cp = compact ? 3 * g.Cq : Cp;
     g.K = pb.K;
     g.P = pb.Hin() * pb.Win();
     g.ptiles = (int)((g.P + 63) / 64);

@@ -115,6 +115,8 @@ struct TcParams {
     int tnb;                  // input staging buffers (2..4)
     uint32_t tr_off;          // byte offset of the transform smem region (1024-aligned)
     // ---- promoted accumulation (FP32_TC plans, PROMOTE instances) ----
+    int pnb;                  // compact FP32_TC In' (PROMOTE only): k-blocks per piece block (0: off);
+    int pip[kSplitMaxPairs];  //   pair block p of the k loop reads In' piece pip[p]
     int pchunk;               // pipeline stages per promotion chunk: the tensor core accumulates a
                               // chunk of the k loop in TMEM (fresh accumulator), the epilogue warps add
                               // it to fp32 registers (IEEE round-to-nearest) -- the tcgen05 fp32
@@ -494,12 +496,20 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                             int c1 = cb_s, r1 = r_s, s1 = s_s;
                             for (int kb = 0; kb < p.kbs; ++kb) {
                                 const int bx = (r1 * p.S + s1) * p.Cp + c1 * p.bkc;
+                                // compact FP32_TC In': pair block -> its piece's channels
+                                int ca = c1 * p.bkc;
+                                if constexpr (PROMOTE) {
+                                    if (p.pnb) {
+                                        const int pb_ = c1 / p.pnb;
+                                        ca = (p.pip[pb_] * p.pnb + (c1 - pb_ * p.pnb)) * p.bkc;
+                                    }
+                                }
                                 if (CG == 2) {
-                                    tma_load_im2col_4d_pair(a_dst + kb * a_blk, &tmap_a, &full[stage], c1 * p.bkc,
+                                    tma_load_im2col_4d_pair(a_dst + kb * a_blk, &tmap_a, &full[stage], ca,
                                                             w0 * p.U - p.pw, h0 * p.U - p.ph, img, (uint16_t)(s1 * p.D), (uint16_t)(r1 * p.D), pol_a);
                                     tma_load_2d_pair(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
                                 } else {
-                                    tma_load_im2col_4d(a_dst + kb * a_blk, &tmap_a, &full[stage], c1 * p.bkc,
+                                    tma_load_im2col_4d(a_dst + kb * a_blk, &tmap_a, &full[stage], ca,
                                                        w0 * p.U - p.pw, h0 * p.U - p.ph, img, (uint16_t)(s1 * p.D), (uint16_t)(r1 * p.D), pol_a);
                                     tma_load_2d(b_dst + kb * b_blk, &tmap_b, &full[stage], bx, kb0, pol_b);
                                 }
@@ -1093,9 +1103,10 @@ static cudaError_t encode_maps(const Problem& pb, const TcLayout& L, const TcTil
     const CUtensorMapSwizzle swz = swizzle_for(L.sw);
     {
         // In NHWC: dims (C, W, H, N) innermost first.
-        cuuint64_t dims[4] = {(cuuint64_t)L.Cp, (cuuint64_t)pb.Win(), (cuuint64_t)pb.Hin(), (cuuint64_t)pb.N};
-        cuuint64_t strides[3] = {(cuuint64_t)L.Cp * L.elem, (cuuint64_t)L.Cp * L.elem * pb.Win(),
-                                 (cuuint64_t)L.Cp * L.elem * pb.Win() * pb.Hin()};
+        const int ac = L.a_chan ? L.a_chan : L.Cp;          // channels per pixel of the workspace
+        cuuint64_t dims[4] = {(cuuint64_t)ac, (cuuint64_t)pb.Win(), (cuuint64_t)pb.Hin(), (cuuint64_t)pb.N};
+        cuuint64_t strides[3] = {(cuuint64_t)ac * L.elem, (cuuint64_t)ac * L.elem * pb.Win(),
+                                 (cuuint64_t)ac * L.elem * pb.Win() * pb.Hin()};
         // Bounding box per image: w in [-pw, Win-1+pw-D(S-1)], h likewise
         // (the window origins; with padding they start outside the tensor,
         // whose out-of-bounds elements TMA fills with zeros); the traversal
@@ -1286,6 +1297,12 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
     // FP32_TC: promote every ~kPromoteProducts products per output (9 k-blocks
     // of 64 channels = one 3x3 window of a channel block), R16
     prm.pchunk = split_pairs ? std::max(1, (tc_promote_kblocks(L) + t.kbs - 1) / t.kbs) : 0;
+    const bool compact = split_pairs && L.a_chan && L.a_chan != L.Cp;
+    if (compact) {
+        const SplitPairs sp = conv::split_pairs(split_pairs);
+        prm.pnb = split_cq(expand_src->C) / L.bkc;
+        for (int i = 0; i < kSplitMaxPairs; ++i) prm.pip[i] = sp.ip[i];
+    }
     prm.sw = (uint32_t)L.sw;
     prm.a_stage_bytes = (uint32_t)(t.kbs * kBM * L.sw);
     prm.b_stage_bytes = (uint32_t)(t.kbs * (t.bn / t.cg) * L.sw);
@@ -1366,7 +1383,8 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         fz.zero_n = prm.num_tiles;
     }
     if (split_pairs)
-        e = launch_split(*expand_src, L.Cp, split_pairs, in, ker, in_ws, ker_ws, st, ev, fz.zero_ptr, fz.zero_n);
+        e = launch_split(*expand_src, L.Cp, split_pairs, in, ker, in_ws, ker_ws, st, ev, fz.zero_ptr, fz.zero_n,
+                         compact);
     else if (expand_src)
         e = launch_expand(*expand_src, L.Cp, bf16, in, ker, in_ws, ker_ws, st, ev);
     else
