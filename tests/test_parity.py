@@ -1125,3 +1125,36 @@ def test_guard_bands_no_out_of_bounds_access(case):
     pad_hw = (sh.ph, sh.pw)
     ref = oracle.conv_eq1_padded(ROUND[path](inp.numpy()), ROUND[path](ker.numpy()), sh.U, sh.D, pad_hw)
     assert rel_l2(got, ref) <= 1e-5          # vs the oracle on the path's rounded inputs
+
+
+def test_fp32_tc_compact_layout_subprocess():
+    """The opt-in compact FP32_TC workspace (CONV_SPLIT_COMPACT=1: the 3 bf16
+    pieces once, pair blocks mapped to pieces in the producer) gives the same
+    result bit for bit as the default 6-pair layout (same products, same
+    k order), in a fresh process (the knob is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = """
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2101_09808_b200 import conv
+from paper_2101_09808_b200.inputs import Shape, make_inputs
+sh = Shape(N=3, K=96, C=128, H=10, W=12, R=3, S=3)
+inp, ker = make_inputs(sh, seed=190)
+p = conv.ConvPlan(*sh.as_tuple(), path="fp32_tc")
+out = p.run(inp.cuda(), ker.cuda()).cpu().numpy()
+np.save(sys.argv[1], out)
+print(p.workspace_bytes)
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        for v in ("0", "1"):
+            f = os.path.join(d, f"o{v}.npy")
+            r = subprocess.run([sys.executable, "-c", code, f], capture_output=True, text=True, timeout=300,
+                               env={**os.environ, "CONV_SPLIT_COMPACT": v})
+            assert r.returncode == 0, r.stderr[-2000:]
+            res[v] = (np.load(f), int(r.stdout.strip().splitlines()[-1]))
+    assert res["1"][1] < res["0"][1]                      # the compact workspace is smaller
+    assert np.array_equal(res["0"][0], res["1"][0])
