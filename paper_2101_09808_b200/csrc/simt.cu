@@ -273,7 +273,8 @@ struct Simt2Params {
     int bko;          // kg * TK
     int rows_in;      // th + R - 1
     int pitch;        // floats per smem row (>= groups*TW + S - 1, multiple of 4)
-    int plane;        // tn * rows_in * pitch (floats per channel in smem)
+    int istride;      // floats between the images of a channel in smem (>= rows_in * pitch; simt2_istride)
+    int plane;        // tn * istride (floats per channel in smem)
     int groups;       // ceil(W / TW): pixel groups per output row
     int n_htiles;
     int nchunks;
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     const int g = rem - row * p.groups;
     const int w0 = g * TW;
     const bool valid = q < p.slots && (n0 + img) < p.N && (h0 + row) < p.H;
-    const int off = valid ? (img * p.rows_in + row) * p.pitch + w0 : 0;
+    const int off = valid ? img * p.istride + row * p.pitch + w0 : 0;
 
 #if CONV_SIMT_FFMA2
     // FFMA2 (fma.rn.f32x2, sm_100): output channels in pairs, acc2[i][j] =
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
             const int ir = rr % p.rows_in, t2 = rr / p.rows_in;
             const int im = t2 % p.tn, cc = t2 / p.tn;
             const int n = n0 + im;
-            s_dst[k] = cc * p.plane + (im * p.rows_in + ir) * p.pitch + col;
+            s_dst[k] = cc * p.plane + im * p.istride + ir * p.pitch + col;
             if (n < p.N && ir < rows_ok) {
                 s_cc[k] = cc;
                 s_src[k] = (((int64_t)n * p.C + cc) * p.Hin + h0 + ir) * p.Win + col;
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
                 const int c = c0 + cc, n = n0 + im;
                 const bool ok = c < p.C && n < p.N && ir < rows_ok;
                 const float* src = in + (((int64_t)n * p.C + c) * p.Hin + h0 + ir) * p.Win;
-                float* dst = in_s + cc * p.plane + (im * p.rows_in + ir) * p.pitch;
+                float* dst = in_s + cc * p.plane + im * p.istride + ir * p.pitch;
                 if (p.vec4)      // 16-B aligned rows (same addressing as the slotted plan)
                     for (int col = lane * 4; col < p.Win; col += 128) cp_async16(dst + col, ok ? src + col : in, ok);
                 else
@@ -551,9 +552,23 @@ int simt2_pitch(const Problem& pb, const SimtTile& t) {
     return pitch;
 }
 
+// v2 image stride in smem: row mode with few rows per image (th < 8) puts
+// several images in one quarter-warp; their windows are then 16-B units
+// i*istride/4 + r*pitch/4 apart, and an image stride of 2 or 6 (mod 8) units
+// with the odd pitch keeps the 8 loads on distinct bank groups (without it
+// the lane-filling tn = 16, th = 2 tile ran 2-way conflicted, r02)
+int simt2_istride(const Problem& pb, const SimtTile& t) {
+    const int pitch = simt2_pitch(pb, t);
+    int units = (int)pb.rows_span(t.th) * pitch / 4;
+    const bool row_mode = (pb.W + t.tw - 1) / t.tw == 1;
+    if (row_mode && t.th < 8)
+        while (units % 8 != 2 && units % 8 != 6) ++units;
+    return units * 4;
+}
+
 size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
     const size_t row = t.ver == 2 ? (size_t)simt2_pitch(pb, t) : (size_t)(pb.Win() + 2 * pb.pw);
-    const size_t plane = (size_t)t.tn * pb.rows_span(t.th) * row;
+    const size_t plane = t.ver == 2 ? (size_t)t.tn * simt2_istride(pb, t) : (size_t)t.tn * pb.rows_span(t.th) * row;
     const size_t in_stage = (size_t)t.bc * plane;
     const size_t ker_stage = (size_t)t.bc * pb.R * pb.S * t.kg * t.tk;
     return (size_t)(t.ver == 2 ? kSimt2Stages : 2) * (in_stage + ker_stage) * sizeof(float);
@@ -669,7 +684,8 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
         q.tn = t.tn; q.th = t.th; q.bc = t.bc; q.kg = t.kg; q.bko = p.bko;
         q.rows_in = p.rows_in;
         q.pitch = simt2_pitch(pb, t);
-        q.plane = t.tn * q.rows_in * q.pitch;
+        q.istride = simt2_istride(pb, t);
+        q.plane = t.tn * q.istride;
         q.groups = (pb.W + t.tw - 1) / t.tw;
         q.n_htiles = p.n_htiles;
         q.nchunks = p.nchunks;
