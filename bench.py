@@ -636,7 +636,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--path", default="fp32_simt", choices=["auto", "fp32_simt", "fp32_tc", "tf32", "bf16", "all"],
                     help="the headline path (default: FP32, the paper's precision, PAPER.md:369)")
-    ap.add_argument("--paths", default="tf32,bf16",
+    ap.add_argument("--paths", default="fp32_tc,tf32,bf16",
                     help="further paths measured in the same process, reported under 'paths' ('' for none)")
     ap.add_argument("--shard", default="auto", choices=["auto", "n", "k"],
                     help="strong scaling: shard the batch n (auto for N >= ranks) or output channels k (N = 1)")

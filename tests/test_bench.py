@@ -53,9 +53,10 @@ def test_bench_line_contract():
     assert j["config"]["workload"].startswith("batched")
     # headline at the paper's precision (fp32) against measured peaks
     assert j["dtype"] == "f32" and j["roofline"]["peak_measured"] is True
-    for p in ("tf32", "bf16"):
+    for p in ("fp32_tc", "tf32", "bf16"):
         sub = j["paths"][p]
-        assert sub["dtype"] == p and sub["value"] > j["value"] and sub["roofline"]["peak_measured"] is True
+        assert sub["dtype"].startswith({"fp32_tc": "f32"}.get(p, p)) and sub["value"] > j["value"]
+        assert sub["roofline"]["peak_measured"] is True
         assert 0 < sub["roofline"]["frac"] <= 1.0 and sub["clocks"]["sm_mhz"]
     rf = j["roofline"]
     assert rf["bound"] in ("tensor", "hbm", "alu") and 0 < rf["frac"] <= 1.0
