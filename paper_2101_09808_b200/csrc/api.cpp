@@ -164,10 +164,8 @@ static bool select_split(conv_plan* p, TcTile& tt, ModelResult& rt, Problem& ps,
     ps = split_problem(p->pb, np);
     TcForce f = p->force_tc;
     if (f.fuse == 1) { why = "FP32_TC plans run without the fused transform"; return false; }
-    if (f.splits > 1) { why = "FP32_TC plans run without split-K (the promoted accumulation)"; return false; }
     f.fuse = 0;
     f.expand = 0;
-    f.splits = 1;
     f.halo = 0;                                   // the halo kernel reads the real NCHW input
     if (!select_tc(ps, p->dev, true, tt, rt, f, why)) return false;
     const double over = 4.0 * ((double)ps.in_elems() - (double)p->pb.in_elems()) +
@@ -224,7 +222,13 @@ static conv_status select(conv_plan* p) {
             std::string why_t;
             const bool ok_t = select_split(p, tt, rt, ps, np, why_t);
             if (!ok_s && !ok_t) return fail(CONV_ERR_INFEASIBLE, "%s; %s", why.c_str(), why_t.c_str());
-            if (ok_t && (!ok_s || rt.model_us < rs.model_us)) {
+            // The two models are calibrated separately; against the measured
+            // Table-1 steps the FP32_TC model reads ~1.2x optimistic relative
+            // to the SIMT one (r02, profiles/r02/t1_*_sk.jsonl: AUTO total
+            // 1742 us with factor 1.0, 1651 with 1.2, 1688 with 1.4; the
+            // per-layer best of the two 1613)
+            constexpr double kTcVsSimt = 1.2;
+            if (ok_t && (!ok_s || rt.model_us * kTcVsSimt < rs.model_us)) {
                 p->tc = tt; p->model = rt; p->path = CONV_PATH_FP32_TC; p->expand = false; p->split = np; p->ps = ps;
                 p->tcl = split_layout(pb, ps);
             } else {

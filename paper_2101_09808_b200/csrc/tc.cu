@@ -819,9 +819,12 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
         const int q = warp & 3, half = warp >> 2;
         int acc = 0;
         uint32_t acc_phase = 0;
-        const int iters = p.k_iters / p.kbs;
-        const int nchunk = (iters + p.pchunk - 1) / p.pchunk;
         for (int wi = unit; wi < p.num_work; wi += nunits) {
+            // this work item's stages (split-K: its k range) in promotion chunks
+            const int tile_w = SPLIT ? wi / p.splits : wi;
+            const int it_beg = SPLIT ? (wi - tile_w * p.splits) * p.kper : 0;
+            const int iters = SPLIT ? (min(p.k_iters, it_beg + p.kper) - it_beg) / p.kbs : p.k_iters / p.kbs;
+            const int nchunk = (iters + p.pchunk - 1) / p.pchunk;
             float run[HB];
 #pragma unroll
             for (int j = 0; j < HB; ++j) run[j] = 0.0f;
@@ -848,6 +851,40 @@ conv_igemm_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                     else mbar_arrive(&tmem_empty[acc]);
                 }
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+            if constexpr (SPLIT) {
+                // split-K (CG = 1, one wave): the promoted partial of this
+                // k range -> its slab ([BN][128] column-major, as
+                // store_partial), then warps 4-7 run the common arrival /
+                // split-order reduction below
+                float* slab = p.part + (size_t)wi * (kBM * BN) + q * 32 + lane;
+#pragma unroll
+                for (int j = 0; j < HB; ++j) __stcg(slab + (size_t)(half * HB + j) * kBM, run[j]);
+                __threadfence();
+                named_bar_sync(2, 256);
+                if (warp < 4) continue;
+                const int sp = wi - tile_w * p.splits;
+                const int c_lo = BN * sp / p.splits, c_hi = BN * (sp + 1) / p.splits;
+                float* red = reinterpret_cast<float*>(smem);
+                if (warp == 4 && lane == 0) {
+                    int* ctr = p.tile_ctr + tile_w;
+                    atomicAdd(ctr, 1);
+                    const long long t0 = clock64();
+                    while (ld_acquire_gpu(ctr) < p.splits) {
+                        __nanosleep(32);
+                        if (clock64() - t0 > 8000000000ll) __trap();
+                    }
+                    fence_proxy_async_global();
+                    const uint32_t bytes = (uint32_t)(c_hi - c_lo) * kBM * 4;
+                    mbar_arrive_expect_tx(last_full, bytes * p.splits);
+                    const float* src = p.part + (size_t)tile_w * p.splits * (kBM * BN) + (size_t)c_lo * kBM;
+                    for (int s2 = 0; s2 < p.splits; ++s2)
+                        bulk_load_g2s(red + (size_t)s2 * (c_hi - c_lo) * kBM, src + (size_t)s2 * (kBM * BN), bytes,
+                                      last_full);
+                }
+                mbar_wait(last_full, 0);
+                reduce_share<BN>(p, tile_w, red, c_lo, c_hi, warp & 3, lane);
+                continue;
             }
             // registers -> NCHW Out (32 consecutive pixels of one (n, k) plane per warp store)
             const int tile = wi;
@@ -1034,6 +1071,17 @@ template <bool BF16, int CG, int KSTEPS>
 static cudaError_t launch_tc_bn(int bn, const TcMaps& m, const TcParams& prm, size_t smem, int grid, cudaStream_t st) {
     if (prm.splits > 1) {          // split-K kernels: CG = 1, BN <= 128, not fused (tc_split_ok)
         if constexpr (CG == 1) {
+            if (prm.pchunk > 0) {      // FP32_TC: promoted partials
+                if constexpr (BF16 && KSTEPS == 4) {
+                    switch (bn) {
+                        case 32: return launch_tc<32, true, 1, 4, true, false, true>(m, prm, smem, grid, st);
+                        case 64: return launch_tc<64, true, 1, 4, true, false, true>(m, prm, smem, grid, st);
+                        case 128: return launch_tc<128, true, 1, 4, true, false, true>(m, prm, smem, grid, st);
+                        default: break;
+                    }
+                }
+                return cudaErrorInvalidValue;
+            }
             switch (bn) {
                 case 32: return launch_tc<32, BF16, 1, KSTEPS, true, false>(m, prm, smem, grid, st);
                 case 64: return launch_tc<64, BF16, 1, KSTEPS, true, false>(m, prm, smem, grid, st);
@@ -1216,8 +1264,8 @@ cudaError_t tc_run(const Problem& pb, const TcLayout& L, const TcTile& t, bool b
         return halo_run(pb, bf16, in, ker, out, ker_ws, st, ev, err);
     }
     if (expand_src && !split_pairs && (t.fuse || t.splits > 1)) { err = "tap-expanded plans run without the fused transform and split-K"; return cudaErrorInvalidValue; }
-    if (split_pairs && (!expand_src || !bf16 || t.fuse || t.splits > 1)) {
-        err = "FP32_TC plans run the promoted bf16 kernel: no fused transform, no split-K";
+    if (split_pairs && (!expand_src || !bf16 || t.fuse)) {
+        err = "FP32_TC plans run the promoted bf16 kernel: no fused transform";
         return cudaErrorInvalidValue;
     }
     if (t.fuse && (!L.coop_ok || !flag_ws)) { err = "fused transform needs a TMA-legal NCHW plane and flag workspace"; return cudaErrorInvalidValue; }
