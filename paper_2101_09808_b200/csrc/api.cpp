@@ -662,7 +662,25 @@ extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, 
     // 1-2-4-6-6-6-6-4-2-1 taper 1.583 ms; H2D + D2H alone 1.38 ms).
     // One chunk for small inputs; env CONV_HOST_CHUNKS for experiments.
     static const int env_chunks = [] { const char* e = getenv("CONV_HOST_CHUNKS"); return e ? atoi(e) : 0; }();
-    const int nch = (bi < (8u << 20)) ? 1 : std::min({pb.N, (int)conv_plan::kMaxChunks, env_chunks > 0 ? env_chunks : 6});
+    int nch = (bi < (8u << 20)) ? 1 : std::min({pb.N, (int)conv_plan::kMaxChunks, env_chunks > 0 ? env_chunks : 6});
+    if (nch > 1 && env_chunks <= 0 && p->path == CONV_PATH_FP32_SIMT) {
+        // FP32 SIMT chunks are compute-heavy and run whole waves of CTAs: the
+        // chunk count (2..8) with the fewest summed waves, the most chunks
+        // among those (batched layer: 4 chunks of 64 images = 4 waves, as
+        // unchunked; 6 chunks ran 6 partial waves, e2e 2.71 ms, r02)
+        const int64_t slots = std::max<int64_t>(1, p->model.ctas);
+        int best = nch;
+        int64_t best_w = INT64_MAX;
+        for (int c = 2; c <= std::min(8, pb.N); ++c) {
+            int64_t w = 0;
+            for (int j = 0; j < c; ++j) {
+                const int64_t nimg = (int64_t)pb.N * (j + 1) / c - (int64_t)pb.N * j / c;
+                w += (simt_ctas(pb, p->simt, (int)nimg) + slots - 1) / slots;
+            }
+            if (w <= best_w) { best_w = w; best = c; }
+        }
+        nch = best;
+    }
     int bounds[conv_plan::kMaxChunks + 1];
     bounds[0] = 0;
     for (int j = 0; j < nch; ++j) bounds[j + 1] = (int)((int64_t)pb.N * (j + 1) / nch);
