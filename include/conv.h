@@ -166,7 +166,11 @@ CONV_API conv_status conv_plan_set_path(conv_plan* plan, conv_path path);
  * pre_c (fused prologue channels), expand (0/1: tiny-C tap expansion -- the
  * transform writes each output pixel's R*S*C taps as channels and the
  * kernel runs the equivalent 1x1 problem; automatic when C*elem <= 16 B and
- * R*S >= 4, and then free of the TMA limits stated above); for the SIMT
+ * R*S >= 4, and then free of the TMA limits stated above), split (FP32_TC:
+ * 6 or 9 bf16 piece pairs, default 6), halo (0/1: the halo kernel -- the
+ * input tile staged once per CTA in shared memory, the filter taps as
+ * shifted tcgen05 descriptors; stride 1, dilation 1, no padding,
+ * C*elem <= 128 B, K <= 256; only on request); for the SIMT
  * path: ver, tk, tw, kg, pw, tn, th, bc.  Unspecified keys keep the
  * selector's choice.  NULL or "" restores the selector's choice.
  * INVALID_ARGUMENT on a malformed spec, INFEASIBLE if the tile exceeds
@@ -174,7 +178,10 @@ CONV_API conv_status conv_plan_set_path(conv_plan* plan, conv_path path);
 CONV_API conv_status conv_plan_set_tile(conv_plan* plan, const char* spec);
 
 /* Bytes of device workspace conv_run needs: the NHWC In / KRSC Ker buffers of
- * the tensor paths, the packed [K/BKo][C][R][S][BKo] Ker of the SIMT path.
+ * the tensor paths (FP32_TC: of the bf16 pieces, 6 pair blocks of the
+ * channels; halo plans: only the per-tap Ker image), the packed
+ * [K/BKo][C][R][S][BKo] Ker of the SIMT path, plus the fused transform's
+ * chunk flags / split-K partial slabs when the plan uses them.
  * Caller allocates, 256-B aligned. */
 CONV_API size_t conv_plan_workspace_bytes(const conv_plan* plan);
 
