@@ -497,10 +497,15 @@ def cpu_baseline(sh: Shape, args, target_s: float = 10.0):
     n = int(max(1, min(sh.N, target_s / max(t1, 1e-6))))
     t = oracle_sample_time(sh, n, threads) if n > 1 else t1
     flops = 2.0 * n * sh.K * sh.H * sh.W * sh.C * sh.R * sh.S
+    # single-thread oracle beside it: one image
+    t_1 = oracle_sample_time(sh, 1, 1)
+    flops_1 = 2.0 * sh.K * sh.H * sh.W * sh.C * sh.R * sh.S
     return {"value": round(flops / t / 1e12, 6), "unit": "TFLOP/s", "cores": used, "kind": "oracle",
             "cpu": cpu_model(),
             "sample": f"first {n} of {sh.N} images of the {args.config} layer ({t:.1f} s, double accumulation, "
-                      f"OpenMP over (n,k) planes)"}
+                      f"OpenMP over (n,k) planes)",
+            "single_thread": {"value": round(flops_1 / t_1 / 1e12, 6), "unit": "TFLOP/s", "cores": 1,
+                              "sample": f"1 image ({t_1:.2f} s)"}}
 
 
 def bench_reference(args):
