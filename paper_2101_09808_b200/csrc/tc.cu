@@ -1007,7 +1007,14 @@ TcLayout tc_layout(const Problem& pb, bool bf16) {
     return L;
 }
 
-int tc_promote_kblocks(const TcLayout& L) { return std::max(1, (kPromoteProducts + L.bkc - 1) / L.bkc); }
+int tc_promote_kblocks(const TcLayout& L) {
+    // env CONV_PROMOTE_PRODUCTS: the promotion interval (study knob)
+    static const int products = [] {
+        const char* e = getenv("CONV_PROMOTE_PRODUCTS");
+        return e && atoi(e) > 0 ? atoi(e) : kPromoteProducts;
+    }();
+    return std::max(1, (products + L.bkc - 1) / L.bkc);
+}
 
 // pipeline ring + barrier block, then (fuse) the transform region at a
 // 1024-B boundary: tnb fp32 [cc][64] chunk buffers (converted in place),
