@@ -450,7 +450,7 @@ static const double kSimtChunkSyncClk = [] {
 // it against libconv.so).  The former estimate (TK*TW + TK + window + 24 for
 // v2) said 72 for v2 TK=8 TW=4 S=3 where ptxas gives 104-128: 2 CTAs per SM
 // modeled where 1 fits (ncu r01b Y0: occupancy limited by registers to 1).
-struct SimtRegs { int ver, tk, tw, kr, ks, splitc, regs; };
+struct SimtRegs { int ver, tk, tw, kr, ks, splitc, tma, regs; };
 static const SimtRegs kSimtRegs[] = {
 #include "simt_regs.inc"
 };
@@ -459,8 +459,10 @@ static int simt_regs(const Problem& pb, const SimtTile& t, int win) {
     const int sc = t.splits > 1 ? 1 : 0;
     const int kr = (t.ver == 2 && pb.R == pb.S && (pb.S == 1 || pb.S == 3)) ? pb.R : 0;
     const int ks = t.ver == 2 ? pb.S : 0;
+    const int tma = t.ver == 2 && simt2_layout(pb, t).tma ? 1 : 0;
     for (const SimtRegs& e : kSimtRegs)
-        if (e.ver == t.ver && e.tk == t.tk && e.tw == t.tw && e.kr == kr && e.ks == ks && e.splitc == sc)
+        if (e.ver == t.ver && e.tk == t.tk && e.tw == t.tw && e.kr == kr && e.ks == ks && e.splitc == sc &&
+            e.tma == tma)
             return e.regs;
     // an instance the table does not list (not built): the old estimate
     return std::min(128, t.tk * t.tw + t.tk + win + (t.ver == 2 ? 24 : 2 * t.tw + 28));
@@ -529,7 +531,12 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const double units_v2 = (double)t.bc * t.tn * pb.rows_span(t.th) * (pb.Win() % 4 == 0 ? pb.Win() / 4.0 : pb.Win());
     const double copy_unit = (t.ver == 2 && units_v2 > 4.0 * threads)
                                  ? (pb.Win() % 4 == 0 ? kSimtSlowCopy16 : kSimtSlowCopy) : 6.0;
-    const double copy_chunk_cta = in_elems_chunk * copy_unit + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
+    // TMA layout (simt2_layout): one thread issues the In box and the Ker
+    // bulk copy; the other threads only pass the barrier and the mbarrier
+    // wait (~20 issue slots per warp per chunk; lane-instructions here)
+    const bool tma = t.ver == 2 && simt2_layout(pb, t).tma;
+    const double copy_chunk_cta = tma ? 20.0 * threads + 100.0 * 32.0
+                                      : in_elems_chunk * copy_unit + (double)t.bc * pb.R * pb.S * bko / 4.0 * 6.0;
     const double clk = dev.peak_fp32 / (dev.sms * 256.0);      // Hz implied by the FP32 peak
     // a chunk cannot take less than one L2 round trip + two barriers
     const double issue_cyc = (double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff);

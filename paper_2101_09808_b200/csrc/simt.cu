@@ -24,8 +24,11 @@
 #include <atomic>
 
 #include <cstdlib>
+#include <cstring>
+#include <string>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace conv {
 
@@ -116,7 +119,7 @@ template <int TK, int TW, bool SPLITC>
 __global__ void __launch_bounds__(512) conv_direct_simt(const float* __restrict__ in,
                                                          const float* __restrict__ kerp,
                                                          float* __restrict__ out, const SimtParams p) {
-    extern __shared__ __align__(16) float sm[];
+    extern __shared__ __align__(128) float sm[];
     const int in_stage = p.bc * p.plane;
     const int ker_stage = p.bc * p.RS * p.bko;
     const int stage_floats = in_stage + ker_stage;
@@ -273,15 +276,21 @@ struct Simt2Params {
     int bko;          // kg * TK
     int rows_in;      // th + R - 1
     int pitch;        // floats per smem row (>= groups*TW + S - 1, multiple of 4)
-    int istride;      // floats between the images of a channel in smem (>= rows_in * pitch; simt2_istride)
-    int plane;        // tn * istride (floats per channel in smem)
+    int istride;      // floats between the images in smem (cp.async layout: of one channel, >= rows_in * pitch;
+                      //    TMA layout: an image's bc channels, 128-B aligned; simt2_istride)
+    int cstride;      // floats between the channels of an image in smem (cp.async: tn * istride; TMA: rows_in * pitch)
+    int plane;        // cp.async layout: tn * istride (floats per channel in smem)
+    int in_stage;     // floats of one stage's In tile
+    int lpi;          // lanes (pixel-group slots) per image: per_img, or rounded up to 8 in the TMA layout
+                      //    so that no quarter-warp straddles two images (conflict-free window loads)
     int groups;       // ceil(W / TW): pixel groups per output row
     int n_htiles;
     int nchunks;
     int cper;         // split-C: chunks per split (blockIdx.z)
     int64_t zstride;  // split-C: floats between partial outputs
-    int slots;        // tn * th * groups (valid pixel-group slots per CTA)
+    int slots;        // tn * lpi (pixel-group slots per CTA)
     int vec4;         // Win % 4 == 0: 16-B copies of input rows
+    uint32_t tx_in;   // TMA layout: bytes of one In box (tn * bc * rows_in * pitch * 4)
 };
 
 static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth
@@ -294,14 +303,17 @@ static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth
 template <int TK, int TW>
 struct Simt2Threads { static constexpr int value = TK * TW > 64 ? 256 : 512; };
 
-template <int TK, int TW, int KR, int KS, bool SPLITC>   // KR = 0: runtime R
+template <int TK, int TW, int KR, int KS, bool SPLITC, bool TMA>   // KR = 0: runtime R
 __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2(const float* __restrict__ in,
                                                           const float* __restrict__ kerp,
-                                                          float* __restrict__ out, const Simt2Params p) {
-    extern __shared__ __align__(16) float sm[];
-    const int in_stage = p.bc * p.plane;
+                                                          float* __restrict__ out, const Simt2Params p,
+                                                          const __grid_constant__ CUtensorMap tmap_in) {
+    // TMA layout: stage buffers 128-B aligned (cp.async.bulk.tensor destination)
+    extern __shared__ __align__(128) float sm[];
+    __shared__ __align__(8) uint64_t full_bar[kSimt2Stages];   // TMA layout: stage landed (tx bytes)
+    const int in_stage = p.in_stage;
     const int ker_stage = p.bc * p.R * KS * p.bko;
-    const int stage_floats = in_stage + ker_stage;
+    const int stage_floats = TMA ? (in_stage + ker_stage + 31) / 32 * 32 : in_stage + ker_stage;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -318,12 +330,12 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     // this thread's pixel group: (img, row, g) -> pixels w0 .. w0+TW-1 of one row
     const int q = pwi * 32 + lane;
     const int per_img = p.th * p.groups;
-    const int img = q / per_img;
-    const int rem = q - img * per_img;
+    const int img = q / p.lpi;
+    const int rem = q - img * p.lpi;
     const int row = rem / p.groups;
     const int g = rem - row * p.groups;
     const int w0 = g * TW;
-    const bool valid = q < p.slots && (n0 + img) < p.N && (h0 + row) < p.H;
+    const bool valid = q < p.slots && rem < per_img && (n0 + img) < p.N && (h0 + row) < p.H;
     const int off = valid ? img * p.istride + row * p.pitch + w0 : 0;
 
 #if CONV_SIMT_FFMA2
@@ -354,7 +366,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     const int nrows = p.bc * p.tn * p.rows_in;
     const int upr = p.vec4 ? p.Win / 4 : p.Win;           // units per row
     const int units = nrows * upr;
-    const bool slotted = units <= kSlots * (int)blockDim.x;
+    const bool slotted = !TMA && units <= kSlots * (int)blockDim.x;
     const int rows_ok = p.Hin - h0 < p.rows_in ? p.Hin - h0 : p.rows_in;
     int64_t s_src[kSlots];
     int s_dst[kSlots], s_cc[kSlots];
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
             const int ir = rr % p.rows_in, t2 = rr / p.rows_in;
             const int im = t2 % p.tn, cc = t2 / p.tn;
             const int n = n0 + im;
-            s_dst[k] = cc * p.plane + im * p.istride + ir * p.pitch + col;
+            s_dst[k] = cc * p.cstride + im * p.istride + ir * p.pitch + col;
             if (n < p.N && ir < rows_ok) {
                 s_cc[k] = cc;
                 s_src[k] = (((int64_t)n * p.C + cc) * p.Hin + h0 + ir) * p.Win + col;
@@ -400,7 +412,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
                 const int c = c0 + cc, n = n0 + im;
                 const bool ok = c < p.C && n < p.N && ir < rows_ok;
                 const float* src = in + (((int64_t)n * p.C + c) * p.Hin + h0 + ir) * p.Win;
-                float* dst = in_s + cc * p.plane + im * p.istride + ir * p.pitch;
+                float* dst = in_s + cc * p.cstride + im * p.istride + ir * p.pitch;
                 if (p.vec4)      // 16-B aligned rows (same addressing as the slotted plan)
                     for (int col = lane * 4; col < p.Win; col += 128) cp_async16(dst + col, ok ? src + col : in, ok);
                 else
@@ -413,6 +425,23 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
         const float* gk = kerp + (((int64_t)kb * p.C + c0) * p.R * KS) * p.bko;
         for (int e = threadIdx.x * 4; e < ker_stage; e += blockDim.x * 4)
             cp_async16(ker_s + e, e < len_ok ? gk + e : kerp, e < len_ok);
+    };
+
+    // TMA layout: one 4-D box {pitch columns, rows_in rows, bc channels, tn
+    // images} of In (columns >= Win, rows >= Hin, channels >= C and images
+    // >= N zero-filled) plus one bulk copy of the packed Ker slab, issued by
+    // one thread and completing on the stage's mbarrier (ncu r02: the
+    // per-thread cp.async plan cost ~300 issue slots per warp per chunk,
+    // ~8 % of the kernel's instructions)
+    auto issue_stage = [&](int buf, int chunk) {
+        float* in_s = sm + buf * stage_floats;
+        float* ker_s = in_s + in_stage;
+        const int c0 = chunk * p.bc;
+        const int cvalid = p.C - c0 < p.bc ? p.C - c0 : p.bc;
+        const uint32_t kbytes = (uint32_t)cvalid * p.R * KS * p.bko * 4u;
+        sm100::mbar_arrive_expect_tx(&full_bar[buf], p.tx_in + kbytes);
+        sm100::tma_load_4d(in_s, &tmap_in, &full_bar[buf], 0, h0, c0, n0);
+        sm100::bulk_load_g2s(ker_s, kerp + (((int64_t)kb * p.C + c0) * p.R * KS) * p.bko, kbytes, &full_bar[buf]);
     };
 
     constexpr int WIN = TW + KS - 1;
@@ -428,23 +457,38 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     // issued after the barrier that ends every thread's use of chunk i-1's
     // buffer (ncu r02: with two stages and two barriers per chunk a third of
     // the stall samples sat outside the FFMA loop, in the waits)
-    load_stage(0, c_beg);
-    cp_async_commit();
-    if (c_beg + 1 < c_end) load_stage(1, c_beg + 1);
-    cp_async_commit();
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < kSimt2Stages; ++i) sm100::mbar_init(&full_bar[i], 1);
+            sm100::fence_barrier_init();
+            issue_stage(0, c_beg);
+            if (c_beg + 1 < c_end) issue_stage(1, c_beg + 1);
+        }
+    } else {
+        load_stage(0, c_beg);
+        cp_async_commit();
+        if (c_beg + 1 < c_end) load_stage(1, c_beg + 1);
+        cp_async_commit();
+    }
     for (int chunk = c_beg; chunk < c_end; ++chunk) {
         const int ci = chunk - c_beg;
         const int buf = ci % kSimt2Stages;
-        cp_async_wait<1>();                       // chunk i has landed (i+1 may be in flight)
-        __syncthreads();
-        if (chunk + 2 < c_end) load_stage((ci + 2) % kSimt2Stages, chunk + 2);
-        cp_async_commit();
+        if (TMA) {
+            __syncthreads();                      // every thread is done with chunk i-1's buffer
+            if (threadIdx.x == 0 && chunk + 2 < c_end) issue_stage((ci + 2) % kSimt2Stages, chunk + 2);
+            sm100::mbar_wait(&full_bar[buf], (uint32_t)(ci / kSimt2Stages) & 1u);
+        } else {
+            cp_async_wait<1>();                   // chunk i has landed (i+1 may be in flight)
+            __syncthreads();
+            if (chunk + 2 < c_end) load_stage((ci + 2) % kSimt2Stages, chunk + 2);
+            cp_async_commit();
+        }
         const float* in_s = sm + buf * stage_floats;
         const float* ker_s = in_s + in_stage;
         const int cc_end = p.C - chunk * p.bc < p.bc ? p.C - chunk * p.bc : p.bc;
         const int R = KR ? KR : p.R;
         for (int cc = 0; cc < cc_end; ++cc) {
-            const float* ip = in_s + cc * p.plane + off;
+            const float* ip = in_s + cc * p.cstride + off;
             const float* kp = ker_s + cc * R * KS * p.bko + kgi * TK;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -566,12 +610,50 @@ int simt2_istride(const Problem& pb, const SimtTile& t) {
     return units * 4;
 }
 
+// v2 shared-memory layout of one stage.  The TMA layout is taken when In
+// rows are 16-B multiples (Win % 4 == 0, the TMA stride rule), the box fits
+// TMA's 256-element dims, R is a compiled tap count, and each image's slots
+// can be padded to whole quarter-warps (the image stride is then a 128-B
+// multiple, so a quarter-warp that straddled two images would conflict).
+// CONV_SIMT_NO_TMA=1 keeps the per-thread cp.async layout (A/B).
+Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
+    Simt2Layout L;
+    L.pitch = simt2_pitch(pb, t);
+    const int rows_in = (int)pb.rows_span(t.th);
+    const int groups = (pb.W + t.tw - 1) / t.tw;
+    const int per_img = t.th * groups;
+    const int lpi8 = (per_img + 7) / 8 * 8;
+    static const bool no_tma = getenv("CONV_SIMT_NO_TMA") != nullptr;
+    L.tma = !no_tma && t.ver == 2 && simt_v2_ok(pb) && pb.Win() % 4 == 0 && L.pitch <= 256 && rows_in <= 256 &&
+            t.bc <= 256 && t.tn <= 256 && (pb.R == 1 || pb.R == 3) && t.tn * lpi8 <= 32 * t.pw;
+    const int ker_stage = t.bc * pb.R * pb.S * t.kg * t.tk;
+    if (L.tma) {
+        L.cstride = rows_in * L.pitch;
+        L.istride = (t.bc * L.cstride + 31) / 32 * 32;
+        L.in_stage = t.tn * L.istride;
+        L.lpi = lpi8;
+        L.stage_floats = (L.in_stage + ker_stage + 31) / 32 * 32;
+    } else {
+        L.istride = simt2_istride(pb, t);
+        L.cstride = t.tn * L.istride;
+        L.in_stage = t.bc * L.cstride;
+        L.lpi = per_img;
+        L.stage_floats = L.in_stage + ker_stage;
+    }
+    return L;
+}
+
 size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
-    const size_t row = t.ver == 2 ? (size_t)simt2_pitch(pb, t) : (size_t)(pb.Win() + 2 * pb.pw);
-    const size_t plane = t.ver == 2 ? (size_t)t.tn * simt2_istride(pb, t) : (size_t)t.tn * pb.rows_span(t.th) * row;
+    if (t.ver == 2) {
+        const Simt2Layout L = simt2_layout(pb, t);
+        // TMA layout: + the mbarriers' 128-B aligned static slot
+        return (size_t)kSimt2Stages * L.stage_floats * sizeof(float) + (L.tma ? 128 : 0);
+    }
+    const size_t row = (size_t)(pb.Win() + 2 * pb.pw);
+    const size_t plane = (size_t)t.tn * pb.rows_span(t.th) * row;
     const size_t in_stage = (size_t)t.bc * plane;
     const size_t ker_stage = (size_t)t.bc * pb.R * pb.S * t.kg * t.tk;
-    return (size_t)(t.ver == 2 ? kSimt2Stages : 2) * (in_stage + ker_stage) * sizeof(float);
+    return 2 * (in_stage + ker_stage) * sizeof(float);
 }
 
 // Launch one SIMT kernel instance, opting it in to the largest dynamic smem
@@ -583,21 +665,31 @@ static cudaError_t launch_simt_inst(K kfn, SmemOptIn& smem_set, const float* in,
     return launch_pdl(kfn, grid, threads, smem, st, in, kerp, out, p);
 }
 
-template <int TK, int TW, int KR, int KS>
+template <int TK, int TW, int KR, int KS, bool TMA>
 static cudaError_t launch_simt2_t(const float* in, const float* kerp, float* out, const Simt2Params& p,
-                                  dim3 grid, int threads, size_t smem, cudaStream_t st) {
+                                  const CUtensorMap& tmap, dim3 grid, int threads, size_t smem, cudaStream_t st) {
     static SmemOptIn set_plain, set_split;
-    if (grid.z > 1)
-        return launch_simt_inst(conv_direct_simt2<TK, TW, KR, KS, true>, set_split, in, kerp, out, p, grid, threads, smem, st);
-    return launch_simt_inst(conv_direct_simt2<TK, TW, KR, KS, false>, set_plain, in, kerp, out, p, grid, threads, smem, st);
+    const size_t dyn = TMA ? smem - 128 : smem;
+    if (grid.z > 1) {
+        auto kfn = conv_direct_simt2<TK, TW, KR, KS, true, TMA>;
+        if (cudaError_t e = set_split.ensure(kfn, dyn); e != cudaSuccess) return e;
+        return launch_pdl(kfn, grid, threads, dyn, st, in, kerp, out, p, tmap);
+    }
+    auto kfn = conv_direct_simt2<TK, TW, KR, KS, false, TMA>;
+    if (cudaError_t e = set_plain.ensure(kfn, dyn); e != cudaSuccess) return e;
+    return launch_pdl(kfn, grid, threads, dyn, st, in, kerp, out, p, tmap);
 }
 
 
-static cudaError_t dispatch_simt2(const SimtTile& t, int R, int S, const float* in, const float* kerp, float* out,
-                                  const Simt2Params& p, dim3 grid, int threads, size_t smem, cudaStream_t st) {
+static cudaError_t dispatch_simt2(const SimtTile& t, int R, int S, bool tma, const float* in, const float* kerp,
+                                  float* out, const Simt2Params& p, const CUtensorMap& tmap, dim3 grid, int threads,
+                                  size_t smem, cudaStream_t st) {
+    // TMA instances only for the compiled tap counts (R = S in {1, 3})
 #define SIMT2_CASE(TK_, TW_, R_, S_) \
-    if (t.tk == TK_ && t.tw == TW_ && (R_ == 0 || R == R_) && S == S_) \
-        return launch_simt2_t<TK_, TW_, R_, S_>(in, kerp, out, p, grid, threads, smem, st);
+    if (t.tk == TK_ && t.tw == TW_ && (R_ == 0 || R == R_) && S == S_) { \
+        if (R_ != 0 && tma) return launch_simt2_t<TK_, TW_, R_, S_, (R_ != 0)>(in, kerp, out, p, tmap, grid, threads, smem, st); \
+        if (!tma) return launch_simt2_t<TK_, TW_, R_, S_, false>(in, kerp, out, p, tmap, grid, threads, smem, st); \
+    }
     SIMT2_CASE(4, 4, 1, 1) SIMT2_CASE(4, 8, 1, 1) SIMT2_CASE(8, 4, 1, 1) SIMT2_CASE(8, 8, 1, 1)
     SIMT2_CASE(4, 4, 3, 3) SIMT2_CASE(4, 8, 3, 3) SIMT2_CASE(8, 4, 3, 3) SIMT2_CASE(8, 8, 3, 3)
     SIMT2_CASE(4, 4, 0, 1) SIMT2_CASE(4, 8, 0, 1) SIMT2_CASE(8, 4, 0, 1) SIMT2_CASE(8, 8, 0, 1)
@@ -683,18 +775,40 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
         q.Hin = (int)pb.Hin(); q.Win = (int)pb.Win();
         q.tn = t.tn; q.th = t.th; q.bc = t.bc; q.kg = t.kg; q.bko = p.bko;
         q.rows_in = p.rows_in;
-        q.pitch = simt2_pitch(pb, t);
-        q.istride = simt2_istride(pb, t);
-        q.plane = t.tn * q.istride;
+        const Simt2Layout L = simt2_layout(pb, t);
+        q.pitch = L.pitch;
+        q.istride = L.istride;
+        q.cstride = L.cstride;
+        q.plane = L.cstride;
+        q.in_stage = L.in_stage;
+        q.lpi = L.lpi;
         q.groups = (pb.W + t.tw - 1) / t.tw;
         q.n_htiles = p.n_htiles;
         q.nchunks = p.nchunks;
         q.cper = p.cper;
         q.zstride = p.zstride;
-        q.slots = t.tn * t.th * q.groups;
+        q.slots = t.tn * L.lpi;
         if (q.slots > t.pw * 32) { err = "SIMT v2 tile: pixel-group slots > pw*32"; return cudaErrorInvalidValue; }
         q.vec4 = (q.Win % 4 == 0) ? 1 : 0;
-        e = dispatch_simt2(t, pb.R, pb.S, in, kerp, kout, q, grid, threads, smem, st);
+        q.tx_in = (uint32_t)((size_t)t.tn * t.bc * q.rows_in * q.pitch * sizeof(float));
+        CUtensorMap tmap;
+        memset(&tmap, 0, sizeof(tmap));
+        if (L.tma) {
+            // In NCHW as {Win, Hin, C, N}; box {pitch, rows_in, bc, tn}: columns
+            // >= Win (the pitch padding), rows >= Hin, channels >= C and
+            // images >= N are zero-filled
+            if (!driver_init(err)) return cudaErrorInvalidValue;
+            cuuint64_t dims[4] = {(cuuint64_t)q.Win, (cuuint64_t)q.Hin, (cuuint64_t)pb.C, (cuuint64_t)pb.N};
+            cuuint64_t strides[3] = {(cuuint64_t)q.Win * 4, (cuuint64_t)q.Hin * q.Win * 4,
+                                     (cuuint64_t)pb.C * q.Hin * q.Win * 4};
+            cuuint32_t box[4] = {(cuuint32_t)q.pitch, (cuuint32_t)q.rows_in, (cuuint32_t)t.bc, (cuuint32_t)t.tn};
+            cuuint32_t estr[4] = {1, 1, 1, 1};
+            CUresult r = g_encode_tiled(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in), dims, strides,
+                                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeTiled (SIMT In) failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
+        }
+        e = dispatch_simt2(t, pb.R, pb.S, L.tma, in, kerp, kout, q, tmap, grid, threads, smem, st);
     } else {
         e = dispatch_simt(t, in, kerp, kout, p, grid, threads, smem, st);
     }
