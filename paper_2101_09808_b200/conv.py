@@ -15,7 +15,9 @@ import threading
 from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libconv.so")
+# CONV_LIB: an A/B build of the same sources with study flags
+# (scripts/build_ab.py, e.g. _ab_ffma2/libconv.so); experiments only
+LIB_PATH = os.environ.get("CONV_LIB") or os.path.join(_HERE, "libconv.so")
 
 CONV_OK = 0
 CONV_ERR_INVALID_ARGUMENT = 1

@@ -289,13 +289,16 @@ struct Simt2Params {
     int cper;         // split-C: chunks per split (blockIdx.z)
     int64_t zstride;  // split-C: floats between partial outputs
     int slots;        // tn * lpi (pixel-group slots per CTA)
+    int stages;       // TMA layout: ring depth (<= kSimt2MaxStages)
     int vec4;         // Win % 4 == 0: 16-B copies of input rows
     uint32_t tx_in;   // TMA layout: bytes of one In box (tn * bc * rows_in * pitch * 4)
 };
 
-static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth
+static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth (cp.async layout; TMA default)
+static constexpr int kSimt2MaxStages = 4;  // TMA layout: ring depth p.stages <= this
 #ifndef CONV_SIMT_FFMA2
-#define CONV_SIMT_FFMA2 0                  // 1: v2 inner product on FFMA2 (A/B: r02 measured 4 % slower)
+#define CONV_SIMT_FFMA2 1                  // v2 inner product on FFMA2 (r02: 4 % slower with the cp.async
+                                           // copies; r02b TMA layout: 1184-1194 vs 1207 us, 100 vs 114 registers)
 #endif
 
 // Row-mode TK = 8 instances hold 112 accumulators: at most 256 threads, so
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
                                                           const __grid_constant__ CUtensorMap tmap_in) {
     // TMA layout: stage buffers 128-B aligned (cp.async.bulk.tensor destination)
     extern __shared__ __align__(128) float sm[];
-    __shared__ __align__(8) uint64_t full_bar[kSimt2Stages];   // TMA layout: stage landed (tx bytes)
+    __shared__ __align__(8) uint64_t full_bar[kSimt2MaxStages];   // TMA layout: stage landed (tx bytes)
     const int in_stage = p.in_stage;
     const int ker_stage = p.bc * p.R * KS * p.bko;
     const int stage_floats = TMA ? (in_stage + ker_stage + 31) / 32 * 32 : in_stage + ker_stage;
@@ -332,11 +335,16 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     const int per_img = p.th * p.groups;
     const int img = q / p.lpi;
     const int rem = q - img * p.lpi;
-    const int row = rem / p.groups;
-    const int g = rem - row * p.groups;
+    // a padding slot (TMA layout: rem >= per_img) reads the last real slot's
+    // window -- the same addresses, a broadcast -- instead of row 0's, which
+    // shared 16-B bank groups with the quarter-warp's real rows (ncu r02b:
+    // 6 wavefronts per window LDS.128 instead of 4)
+    const int remc = rem < per_img ? rem : per_img - 1;
+    const int row = remc / p.groups;
+    const int g = remc - row * p.groups;
     const int w0 = g * TW;
     const bool valid = q < p.slots && rem < per_img && (n0 + img) < p.N && (h0 + row) < p.H;
-    const int off = valid ? img * p.istride + row * p.pitch + w0 : 0;
+    const int off = q < p.slots ? img * p.istride + row * p.pitch + w0 : 0;
 
 #if CONV_SIMT_FFMA2
     // FFMA2 (fma.rn.f32x2, sm_100): output channels in pairs, acc2[i][j] =
@@ -457,12 +465,14 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     // issued after the barrier that ends every thread's use of chunk i-1's
     // buffer (ncu r02: with two stages and two barriers per chunk a third of
     // the stall samples sat outside the FFMA loop, in the waits)
+    // (TMA layout: p.stages deep, chunk i + stages - 1 issued into chunk
+    // i-1's buffer after the barrier)
+    const int S = TMA ? p.stages : kSimt2Stages;
     if (TMA) {
         if (threadIdx.x == 0) {
-            for (int i = 0; i < kSimt2Stages; ++i) sm100::mbar_init(&full_bar[i], 1);
+            for (int i = 0; i < S; ++i) sm100::mbar_init(&full_bar[i], 1);
             sm100::fence_barrier_init();
-            issue_stage(0, c_beg);
-            if (c_beg + 1 < c_end) issue_stage(1, c_beg + 1);
+            for (int i = 0; i < S - 1 && c_beg + i < c_end; ++i) issue_stage(i, c_beg + i);
         }
     } else {
         load_stage(0, c_beg);
@@ -470,13 +480,14 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
         if (c_beg + 1 < c_end) load_stage(1, c_beg + 1);
         cp_async_commit();
     }
+    int buf = 0;
+    uint32_t phase = 0;
     for (int chunk = c_beg; chunk < c_end; ++chunk) {
         const int ci = chunk - c_beg;
-        const int buf = ci % kSimt2Stages;
         if (TMA) {
             __syncthreads();                      // every thread is done with chunk i-1's buffer
-            if (threadIdx.x == 0 && chunk + 2 < c_end) issue_stage((ci + 2) % kSimt2Stages, chunk + 2);
-            sm100::mbar_wait(&full_bar[buf], (uint32_t)(ci / kSimt2Stages) & 1u);
+            if (threadIdx.x == 0 && chunk + S - 1 < c_end) issue_stage(buf == 0 ? S - 1 : buf - 1, chunk + S - 1);
+            sm100::mbar_wait(&full_bar[buf], phase);
         } else {
             cp_async_wait<1>();                   // chunk i has landed (i+1 may be in flight)
             __syncthreads();
@@ -523,6 +534,9 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
                         const float4 k4 = *reinterpret_cast<const float4*>(kp + (r * KS + s) * p.bko + i);
                         kv[i] = k4.x; kv[i + 1] = k4.y; kv[i + 2] = k4.z; kv[i + 3] = k4.w;
                     }
+                    // (pixel-outer order, to pair accumulators and kernel
+                    // values in opposite register banks: ptxas reorders it
+                    // anyway and the layer ran 3.6 % slower, r02b)
 #pragma unroll
                     for (int i = 0; i < TK; ++i)
 #pragma unroll
@@ -531,6 +545,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
                 }
             }
         }
+        if (++buf == S) { buf = 0; phase ^= 1u; }
     }
 
     if (!valid) return;
@@ -615,7 +630,8 @@ int simt2_istride(const Problem& pb, const SimtTile& t) {
 // TMA's 256-element dims, R is a compiled tap count, and each image's slots
 // can be padded to whole quarter-warps (the image stride is then a 128-B
 // multiple, so a quarter-warp that straddled two images would conflict).
-// CONV_SIMT_NO_TMA=1 keeps the per-thread cp.async layout (A/B).
+// CONV_SIMT_NO_TMA=1 keeps the per-thread cp.async layout, CONV_SIMT_STAGES=n
+// sets the TMA ring depth (2..4; A/B).
 Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
     Simt2Layout L;
     L.pitch = simt2_pitch(pb, t);
@@ -624,8 +640,10 @@ Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
     const int per_img = t.th * groups;
     const int lpi8 = (per_img + 7) / 8 * 8;
     static const bool no_tma = getenv("CONV_SIMT_NO_TMA") != nullptr;
+    static const int env_stages = getenv("CONV_SIMT_STAGES") ? atoi(getenv("CONV_SIMT_STAGES")) : 0;
     L.tma = !no_tma && t.ver == 2 && simt_v2_ok(pb) && pb.Win() % 4 == 0 && L.pitch <= 256 && rows_in <= 256 &&
             t.bc <= 256 && t.tn <= 256 && (pb.R == 1 || pb.R == 3) && t.tn * lpi8 <= 32 * t.pw;
+    L.stages = L.tma && env_stages >= 2 && env_stages <= kSimt2MaxStages ? env_stages : kSimt2Stages;
     const int ker_stage = t.bc * pb.R * pb.S * t.kg * t.tk;
     if (L.tma) {
         L.cstride = rows_in * L.pitch;
@@ -647,7 +665,7 @@ size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
     if (t.ver == 2) {
         const Simt2Layout L = simt2_layout(pb, t);
         // TMA layout: + the mbarriers' 128-B aligned static slot
-        return (size_t)kSimt2Stages * L.stage_floats * sizeof(float) + (L.tma ? 128 : 0);
+        return (size_t)L.stages * L.stage_floats * sizeof(float) + (L.tma ? 128 : 0);
     }
     const size_t row = (size_t)(pb.Win() + 2 * pb.pw);
     const size_t plane = (size_t)t.tn * pb.rows_span(t.th) * row;
@@ -791,6 +809,7 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
         if (q.slots > t.pw * 32) { err = "SIMT v2 tile: pixel-group slots > pw*32"; return cudaErrorInvalidValue; }
         q.vec4 = (q.Win % 4 == 0) ? 1 : 0;
         q.tx_in = (uint32_t)((size_t)t.tn * t.bc * q.rows_in * q.pitch * sizeof(float));
+        q.stages = L.stages;
         CUtensorMap tmap;
         memset(&tmap, 0, sizeof(tmap));
         if (L.tma) {
