@@ -69,6 +69,8 @@ struct conv_plan {
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
     static constexpr int kMaxChunks = 32;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {};
+    int host_nch = 0;                           // image chunks of the pipeline (0: not planned yet)
+    int host_bounds[kMaxChunks + 1] = {};       // chunk j = images [host_bounds[j], host_bounds[j+1])
     ~conv_plan() {
         for (cudaStream_t s : {h2d, comp, d2h}) if (s) cudaStreamDestroy(s);
         for (cudaEvent_t e : {ev_start, ev_end}) if (e) cudaEventDestroy(e);
@@ -180,6 +182,7 @@ static bool select_split(conv_plan* p, TcTile& tt, ModelResult& rt, Problem& ps,
 // every candidate evaluated, minimum modeled cost wins).
 static conv_status select(conv_plan* p) {
     std::string why;
+    p->host_nch = 0;                              // the host pipeline is re-planned for the new tile
     const Problem& pb = p->pb;
     TcTile tt;
     ModelResult rt;
@@ -490,6 +493,7 @@ static const char* path_name(conv_path p) {
     }
 }
 
+static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_us);
 extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     if (!p) return -1;
     const Problem& pb = p->pb;
@@ -514,7 +518,14 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
                  p->tcl.bkc, p->tcl.Cp, p->tcl.sw);
     }
     tile = t;
-    char out[2048];
+    // conv_run_host's image chunks (plan_host_chunks) and their modeled time
+    int hb[conv_plan::kMaxChunks + 1];
+    double host_us = 0;
+    const int hn = compute_host_chunks(p, hb, &host_us);
+    std::string chunks = "[";
+    for (int j = 0; j < hn; ++j) chunks += (j ? "," : "") + std::to_string(hb[j + 1] - hb[j]);
+    chunks += "]";
+    char out[2560];
     int n = snprintf(out, sizeof out,
         "{\"problem\":{\"N\":%d,\"K\":%d,\"C\":%d,\"H\":%d,\"W\":%d,\"R\":%d,\"S\":%d,\"U\":%d,\"D\":%d,\"ph\":%d,\"pw\":%d,\"Hin\":%lld,\"Win\":%lld},"
         "\"path\":\"%s\",\"tile\":%s,\"workspace_bytes\":%zu,\"kernels\":%d,"
@@ -523,11 +534,12 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
         "\"hbm\":{\"dv_bytes\":%.12g,\"bw\":%.6g,\"us\":%.4f},"
         "\"compute\":{\"flops_issued_us\":%.4f,\"peak\":%.6g}},\"model_us\":%.4f},"
         "\"roofline\":{\"flops\":%.6g,\"compulsory_bytes\":%.6g,\"roofline_us\":%.4f},"
+        "\"host_pipeline\":{\"chunks\":%s,\"model_us\":%.4f},"
         "\"device\":{\"ordinal\":%d,\"sms\":%d,\"smem_optin\":%zu,\"l2_bytes\":%zu}}",
         pb.N, pb.K, pb.C, pb.H, pb.W, pb.R, pb.S, pb.U, pb.D, pb.ph, pb.pw, (long long)pb.Hin(), (long long)pb.Win(), path_name(p->path), tile.c_str(), ws_bytes(p),
         conv_plan_num_kernels(p), m.tiles, m.ctas, m.wave_eff, m.smem,
         m.dv_l2_smem, p->dev.bw_l2, m.t_l2_us, m.dv_hbm, p->dev.bw_hbm, m.t_hbm_us, m.t_comp_us, peak,
-        m.model_us, pb.flops(), comp_bytes, roof_us, p->dev.ordinal, p->dev.sms, p->dev.smem_optin,
+        m.model_us, pb.flops(), comp_bytes, roof_us, chunks.c_str(), host_us, p->dev.ordinal, p->dev.sms, p->dev.smem_optin,
         p->dev.l2_bytes);
     if (n < 0) return -1;
     if (buf && cap) {
@@ -638,6 +650,93 @@ extern "C" size_t conv_plan_host_run_bytes(const conv_plan* p) {
            ws_bytes(p);
 }
 
+// ---- conv_run_host chunk plan -----------------------------------------
+// The pipeline overlaps the upload of chunk j+1, the convolution of chunk j
+// and the download of chunk j-1 on three streams.  Its length is
+//   t_h2d(first chunk) + the compute chain + t_d2h(last chunk)
+// when compute-bound, or all uploads + the last chunk's compute and download
+// when transfer-bound; small chunks at the ends shorten both, but chunks
+// that leave SM waves partly empty lengthen the compute chain.  The plan is
+// chosen like a tile (Alg. 1: every candidate evaluated
+// on the model, the minimum wins): equal partitions into c = 1..32 chunks,
+// and the same with a small head and tail chunk, each simulated with the
+// selector's model time of every chunk's sub-problem (same tile) and the
+// host link measured on the box (r02b profiles/r02b/e2e/: pinned
+// H2D 55.2 GB/s, D2H 56.9 GB/s alone; both at once 67 + 51 MB in 1.31 ms,
+// i.e. the upload at ~0.92 and the download at ~0.70 of its solo rate --
+// the rates below, as the two overlap for most of the pipeline).
+static const double kH2dBps = 55.2e9 * 0.92, kD2hBps = 56.9e9 * 0.70;
+static const double kChunkOverheadUs = 6.0;     // per chunk: copy + event + launch issue
+
+static double model_run_us(const conv_plan* p, const Problem& sub) {
+    if (p->path == CONV_PATH_FP32_SIMT) return model_simt(sub, p->dev, p->simt).model_us;
+    if (p->split) return model_tc(split_problem(sub, p->split), p->dev, true, p->tc).model_us;
+    if (p->expand) return model_tc(expanded_problem(sub), p->dev, p->path == CONV_PATH_BF16, p->tc).model_us;
+    return model_tc(sub, p->dev, p->path == CONV_PATH_BF16, p->tc).model_us;
+}
+
+static double simulate_host_pipeline(const conv_plan* p, const int* bounds, int nch) {
+    const Problem& pb = p->pb;
+    const double img_in = 4.0 * pb.C * pb.Hin() * pb.Win(), img_out = 4.0 * pb.K * pb.H * pb.W;
+    double th = 4.0 * pb.ker_elems() / kH2dBps * 1e6, tc = 0, td = 0;
+    for (int j = 0; j < nch; ++j) {
+        const int n = bounds[j + 1] - bounds[j];
+        if (n <= 0) continue;
+        Problem sub = pb;
+        sub.N = n;
+        th += n * img_in / kH2dBps * 1e6 + kChunkOverheadUs;
+        tc = std::max(tc, th) + model_run_us(p, sub);
+        td = std::max(td, tc) + n * img_out / kD2hBps * 1e6;
+    }
+    return td;
+}
+
+static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_us) {
+    const int N = p->pb.N;
+    static const int env_chunks = [] { const char* e = getenv("CONV_HOST_CHUNKS"); return e ? atoi(e) : 0; }();
+    auto equal = [&](int c, int* b) {
+        for (int j = 0; j <= c; ++j) b[j] = (int)((int64_t)N * j / c);
+    };
+    if (env_chunks > 0) {                       // experiments: equal chunks
+        const int c = std::min({env_chunks, N, (int)conv_plan::kMaxChunks});
+        equal(c, out_bounds);
+        if (out_us) *out_us = simulate_host_pipeline(p, out_bounds, c);
+        return c;
+    }
+    int best[conv_plan::kMaxChunks + 1], cand[conv_plan::kMaxChunks + 1];
+    int best_n = 1;
+    equal(1, best);
+    double best_t = simulate_host_pipeline(p, best, 1);
+    const int cmax = std::min(N, (int)conv_plan::kMaxChunks);
+    for (int c = 2; c <= cmax; ++c) {
+        for (int taper = 0; taper < 2; ++taper) {
+            if (taper) {
+                // head and tail of about half an equal chunk, c - 2 equal chunks between
+                if (c < 3) continue;
+                const int ht = std::max(1, N / (2 * (c - 1)));
+                if (N - 2 * ht < c - 2) continue;
+                cand[0] = 0;
+                cand[1] = ht;
+                for (int j = 1; j <= c - 2; ++j) cand[j + 1] = ht + (int)((int64_t)(N - 2 * ht) * j / (c - 2));
+                cand[c] = N;
+            } else {
+                equal(c, cand);
+            }
+            const double t = simulate_host_pipeline(p, cand, c);
+            if (t < 0.995 * best_t) {           // a clear win only: fewer chunks on near-ties
+                best_t = t;
+                best_n = c;
+                std::copy(cand, cand + c + 1, best);
+            }
+        }
+    }
+    std::copy(best, best + best_n + 1, out_bounds);
+    if (out_us) *out_us = best_t;
+    return best_n;
+}
+
+static void plan_host_chunks(conv_plan* p) { p->host_nch = compute_host_chunks(p, p->host_bounds, nullptr); }
+
 extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, const float* ker_host,
                                      float* out_host, void* dbuf, void* stream) {
     if (!cp) return fail(CONV_ERR_INVALID_ARGUMENT, "plan is NULL");
@@ -656,35 +755,12 @@ extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // Pipeline over image chunks on three internal streams: the upload of
     // chunk j+1, the convolution of chunk j and the download of chunk j-1
-    // overlap (PCIe is full duplex).  One chunk for small inputs.
-    // Equal image chunks; 6 measured best for the batched layer (r01b:
-    // 4 / 6 / 8 / 16 chunks = 1.598 / 1.574 / 1.624 / 1.821 ms per step; a
-    // 1-2-4-6-6-6-6-4-2-1 taper 1.583 ms; H2D + D2H alone 1.38 ms).
-    // One chunk for small inputs; env CONV_HOST_CHUNKS for experiments.
-    static const int env_chunks = [] { const char* e = getenv("CONV_HOST_CHUNKS"); return e ? atoi(e) : 0; }();
-    int nch = (bi < (8u << 20)) ? 1 : std::min({pb.N, (int)conv_plan::kMaxChunks, env_chunks > 0 ? env_chunks : 6});
-    if (nch > 1 && env_chunks <= 0 && p->path == CONV_PATH_FP32_SIMT) {
-        // FP32 SIMT chunks are compute-heavy and run whole waves of CTAs: the
-        // chunk count (2..8) with the fewest summed waves, the most chunks
-        // among those (batched layer: 4 chunks of 64 images = 4 waves, as
-        // unchunked; 6 chunks ran 6 partial waves, e2e 2.71 ms, r02)
-        const int64_t slots = std::max<int64_t>(1, p->model.ctas);
-        int best = nch;
-        int64_t best_w = INT64_MAX;
-        for (int c = 2; c <= std::min(8, pb.N); ++c) {
-            int64_t w = 0;
-            for (int j = 0; j < c; ++j) {
-                const int64_t nimg = (int64_t)pb.N * (j + 1) / c - (int64_t)pb.N * j / c;
-                w += (simt_ctas(pb, p->simt, (int)nimg) + slots - 1) / slots;
-            }
-            if (w <= best_w) { best_w = w; best = c; }
-        }
-        nch = best;
-    }
-    int bounds[conv_plan::kMaxChunks + 1];
-    bounds[0] = 0;
-    for (int j = 0; j < nch; ++j) bounds[j + 1] = (int)((int64_t)pb.N * (j + 1) / nch);
+    // overlap (PCIe is full duplex); the chunks are planned once per plan on
+    // the model (plan_host_chunks).
     std::lock_guard<std::mutex> g(p->host_mu);
+    if (p->host_nch == 0) plan_host_chunks(p);
+    const int nch = p->host_nch;
+    const int* bounds = p->host_bounds;
     cudaError_t e = cudaSuccess;
     auto ok = [&](cudaError_t r) { if (r != cudaSuccess && e == cudaSuccess) e = r; };
     if (!p->h2d) {
