@@ -290,6 +290,8 @@ struct Simt2Params {
     int64_t zstride;  // split-C: floats between partial outputs
     int slots;        // tn * lpi (pixel-group slots per CTA)
     int stages;       // TMA layout: ring depth (<= kSimt2MaxStages)
+    int ktiles;       // ceil(K / bko): grid x = (image tile, row tile) * ktiles + k tile -- the k
+                      //    tiles of an image tile run together, so its In tile is read from HBM once
     int vec4;         // Win % 4 == 0: 16-B copies of input rows
     uint32_t tx_in;   // TMA layout: bytes of one In box (tn * bc * rows_in * pitch * 4)
 };
@@ -323,11 +325,12 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     const int kgi = warp % p.kg;
     const int pwi = warp / p.kg;
 
-    const int nt = blockIdx.x / p.n_htiles;
-    const int ht = blockIdx.x - nt * p.n_htiles;
+    const int bx = gridDim.y > 1 ? (int)blockIdx.x : (int)blockIdx.x / p.ktiles;
+    const int kb = gridDim.y > 1 ? (int)blockIdx.y : (int)blockIdx.x - bx * p.ktiles;
+    const int nt = bx / p.n_htiles;
+    const int ht = bx - nt * p.n_htiles;
     const int n0 = nt * p.tn;
     const int h0 = ht * p.th;
-    const int kb = blockIdx.y;
     const int k0 = kb * p.bko;
 
     // this thread's pixel group: (img, row, g) -> pixels w0 .. w0+TW-1 of one row
@@ -810,6 +813,10 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
         q.vec4 = (q.Win % 4 == 0) ? 1 : 0;
         q.tx_in = (uint32_t)((size_t)t.tn * t.bc * q.rows_in * q.pitch * sizeof(float));
         q.stages = L.stages;
+        q.ktiles = (pb.K + p.bko - 1) / p.bko;
+        static const bool grid2d = getenv("CONV_SIMT_GRID2D") != nullptr;   // A/B: the r02 2-D grid (k tile = y)
+        if (!grid2d) grid = dim3(grid.x * grid.y, 1, grid.z);
+        else q.ktiles = 1;
         CUtensorMap tmap;
         memset(&tmap, 0, sizeof(tmap));
         if (L.tma) {
