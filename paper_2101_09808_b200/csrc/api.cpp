@@ -508,9 +508,12 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     std::string tile;
     char t[256];
     if (p->path == CONV_PATH_FP32_SIMT) {
-        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"splits\":%d,\"threads\":%d}",
+        // staging: "tma" (one 4-D TMA box + a bulk Ker copy per chunk) or
+        // "cp.async" (per-thread copies; v1, and v2 where Win % 4 != 0)
+        const bool tma = p->simt.ver == 2 && simt2_layout(pb, p->simt).tma;
+        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"splits\":%d,\"threads\":%d,\"staging\":\"%s\"}",
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
-                 p->simt.splits, 32 * p->simt.kg * p->simt.pw);
+                 p->simt.splits, 32 * p->simt.kg * p->simt.pw, tma ? "tma" : "cp.async");
     } else {
         snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"split\":%d,\"halo\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
                  128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->split, p->tc.halo, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,

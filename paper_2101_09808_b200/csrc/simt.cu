@@ -277,7 +277,7 @@ struct Simt2Params {
     int rows_in;      // th + R - 1
     int pitch;        // floats per smem row (>= groups*TW + S - 1, multiple of 4)
     int istride;      // floats between the images in smem (cp.async layout: of one channel, >= rows_in * pitch;
-                      //    TMA layout: an image's bc channels, 128-B aligned; simt2_istride)
+                      //    TMA layout: an image's bc channels, bc * rows_in * pitch; simt2_layout)
     int cstride;      // floats between the channels of an image in smem (cp.async: tn * istride; TMA: rows_in * pitch)
     int plane;        // cp.async layout: tn * istride (floats per channel in smem)
     int in_stage;     // floats of one stage's In tile
@@ -631,8 +631,9 @@ int simt2_istride(const Problem& pb, const SimtTile& t) {
 // v2 shared-memory layout of one stage.  The TMA layout is taken when In
 // rows are 16-B multiples (Win % 4 == 0, the TMA stride rule), the box fits
 // TMA's 256-element dims, R is a compiled tap count, and each image's slots
-// can be padded to whole quarter-warps (the image stride is then a 128-B
-// multiple, so a quarter-warp that straddled two images would conflict).
+// can be padded to whole quarter-warps: the box lands dense as
+// [img][c][row][pitch], so the image stride (bc * rows * pitch) is not free
+// to choose, and a quarter-warp that straddled two images could conflict.
 // CONV_SIMT_NO_TMA=1 keeps the per-thread cp.async layout, CONV_SIMT_STAGES=n
 // sets the TMA ring depth (2..4; A/B).
 Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
@@ -650,7 +651,7 @@ Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
     const int ker_stage = t.bc * pb.R * pb.S * t.kg * t.tk;
     if (L.tma) {
         L.cstride = rows_in * L.pitch;
-        L.istride = (t.bc * L.cstride + 31) / 32 * 32;
+        L.istride = t.bc * L.cstride;            // the box is dense: [img][c][row][pitch]
         L.in_stage = t.tn * L.istride;
         L.lpi = lpi8;
         L.stage_floats = (L.in_stage + ker_stage + 31) / 32 * 32;

@@ -437,6 +437,32 @@ def test_run_host_pipelined_chunks_bit_identical(path):
     assert rel_l2(out_h.numpy()[:2], ref) <= TOL[path]
 
 
+# FP32 SIMT v2 TMA staging (Win % 4 == 0): ragged image, row, channel-chunk
+# and k tiles, row mode and pixel-group mode, 3x3 and 1x1, split-C
+SIMT_TMA_CASES = [
+    (Shape(N=5, K=44, C=13, H=9, W=14, R=3, S=3), "ver=2,tk=4,tw=14,kg=4,pw=1,tn=2,th=9,bc=8"),
+    (Shape(N=3, K=20, C=9, H=10, W=30, R=3, S=3), "ver=2,tk=4,tw=8,kg=2,pw=2,tn=1,th=10,bc=4"),
+    (Shape(N=2, K=36, C=21, H=13, W=22, R=3, S=3), "ver=2,tk=8,tw=4,kg=2,pw=2,tn=1,th=7,bc=8"),
+    (Shape(N=3, K=24, C=10, H=7, W=12, R=1, S=1), "ver=2,tk=4,tw=4,kg=2,pw=2,tn=2,th=7,bc=4"),
+    (Shape(N=1, K=32, C=40, H=14, W=14, R=3, S=3), "ver=2,tk=4,tw=14,kg=4,pw=1,tn=1,th=14,bc=4,splits=4"),
+]
+
+
+@pytest.mark.parametrize("shape,tile", SIMT_TMA_CASES, ids=lambda x: x if isinstance(x, str) else "x".join(map(str, x.as_tuple())))
+def test_simt_tma_staging_ragged(shape, tile):
+    """The v2 TMA staging (one 4-D box of In per chunk, OOB zero-fill for
+    columns >= Win, rows >= Hin, channels >= C, images >= N, plus one bulk
+    copy of the packed Ker slab) on tiles that are ragged in every dimension:
+    1e-5 against the double oracle and bit-exact on the integer twin."""
+    inp, ker = make_inputs(shape, seed=31)
+    got, plan = run(shape, inp, ker, "fp32_simt", tile=tile)
+    assert plan.describe()["tile"]["staging"] == "tma"
+    assert rel_l2(got, oracle.conv_eq1(inp.numpy(), ker.numpy())) <= TOL["fp32_simt"]
+    xi, wi = make_inputs(shape, seed=32, kind="int")
+    goti, _ = run(shape, xi, wi, "fp32_simt", tile=tile)
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
 FUSE_SHAPES = [CONFIGS["tiny"], CONFIGS["r2"], CONFIGS["pw"], CONFIGS["det"],
                Shape(N=5, K=64, C=40, H=6, W=2, R=3, S=3), Shape(N=2, K=40, C=70, H=8, W=10, R=1, S=1),
                Shape(N=7, K=96, C=200, H=10, W=14, R=3, S=3), Shape(N=3, K=32, C=16, H=62, W=30, R=3, S=3)]
