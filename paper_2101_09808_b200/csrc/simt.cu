@@ -298,6 +298,9 @@ struct Simt2Params {
 
 static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth (cp.async layout; TMA default)
 static constexpr int kSimt2MaxStages = 4;  // TMA layout: ring depth p.stages <= this
+#ifndef CONV_SIMT_SHFL
+#define CONV_SIMT_SHFL 2                   // TW = 4 halo by warp shuffle: 2 for TK = 8 tiles (default),
+#endif                                     // 1 for every TW = 4 tile, 0 never (A/B builds)
 #ifndef CONV_SIMT_FFMA2
 #define CONV_SIMT_FFMA2 1                  // v2 inner product on FFMA2 (r02: 4 % slower with the cp.async
                                            // copies; r02b TMA layout: 1184-1194 vs 1207 us, 100 vs 114 registers)
@@ -457,6 +460,14 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
 
     constexpr int WIN = TW + KS - 1;
     constexpr int WIN4 = (WIN + 3) / 4 * 4;
+    // warp-shuffle halo (north_star's wording): pixel-group mode TW = 4,
+    // S = 3 only -- in row mode a lane's window is its whole input row and
+    // no neighbour holds any of it.  r02b A/B over the 19 Table-1 layers
+    // that take TW = 4 (profiles/r02b/simt_shfl_ab/): TK = 8 tiles 0.77-1.00x
+    // (Y0 -23 %, M5 -4 %, none slower than +0.4 %), TK = 4 tiles up to 6 %
+    // slower (Y2, Y8) -- so the shuffle halo is compiled for TK = 8 only
+    constexpr bool kShflHalo = TW == 4 && KS == 3 && (CONV_SIMT_SHFL == 1 || (CONV_SIMT_SHFL == 2 && TK == 8));
+    const bool own_halo = g == p.groups - 1 || lane == 31;
     asm volatile("griddepcontrol.wait;" ::: "memory");   // packed Ker written by the previous grid
     // split-C (separate instances, so the plain loop keeps its exact code --
     // the runtime range measured 3.5 % slower on the batched layer): this
@@ -507,10 +518,26 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 float win[WIN4];
+                if (kShflHalo) {
+                    // north_star's warp-shuffle reuse (A/B build): the lane's
+                    // own 4 inputs by one LDS.128, the 2-float halo from the
+                    // next lane (the next pixel group of the row), or by an
+                    // LDS.64 where that lane is in another row or warp
+                    const float4 v = *reinterpret_cast<const float4*>(ip + r * p.pitch);
+                    win[0] = v.x; win[1] = v.y; win[2] = v.z; win[3] = v.w;
+                    float h0 = __shfl_down_sync(0xffffffffu, v.x, 1);
+                    float h1 = __shfl_down_sync(0xffffffffu, v.y, 1);
+                    if (own_halo) {
+                        const float2 t = *reinterpret_cast<const float2*>(ip + r * p.pitch + 4);
+                        h0 = t.x; h1 = t.y;
+                    }
+                    win[4] = h0; win[5] = h1;
+                } else {
 #pragma unroll
-                for (int j = 0; j < WIN4; j += 4) {
-                    const float4 v = *reinterpret_cast<const float4*>(ip + r * p.pitch + j);
-                    win[j] = v.x; win[j + 1] = v.y; win[j + 2] = v.z; win[j + 3] = v.w;
+                    for (int j = 0; j < WIN4; j += 4) {
+                        const float4 v = *reinterpret_cast<const float4*>(ip + r * p.pitch + j);
+                        win[j] = v.x; win[j + 1] = v.y; win[j + 2] = v.z; win[j + 3] = v.w;
+                    }
                 }
 #pragma unroll
                 for (int s = 0; s < KS; ++s) {
