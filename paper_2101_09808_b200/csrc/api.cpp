@@ -668,11 +668,29 @@ extern "C" size_t conv_plan_host_run_bytes(const conv_plan* p) {
 // H2D 55.2 GB/s, D2H 56.9 GB/s alone; both at once 67 + 51 MB in 1.31 ms,
 // i.e. the upload at ~0.92 and the download at ~0.70 of its solo rate --
 // the rates below, as the two overlap for most of the pipeline).
-static const double kH2dBps = 55.2e9 * 0.92, kD2hBps = 56.9e9 * 0.70;
-static const double kChunkOverheadUs = 6.0;     // per chunk: copy + event + launch issue
+static const double kH2dBps = 55.2e9 * 0.92, kD2hBps = 56.9e9 * 0.70, kD2hSoloBps = 56.9e9;
+// per chunk beyond the model: copy + event + launch issue; the tensor
+// paths' chunks also pay their layout launch and main-kernel prologue again
+// (measured r02b, profiles/r02b/e2e/e2e_check.txt: bf16 16 vs 6 equal
+// chunks +0.25 ms, i.e. ~25 us per extra chunk)
+static const double kChunkOverheadUs = 6.0, kTcChunkOverheadUs = 30.0;
 
+// FP32 SIMT chunk time: measured r02b on the batched layer's tile
+// (profiles/r02b/e2e/simt_time_vs_batch.txt, N = 6..256 images) the time is
+// T(k) = 35 + 85 k us with k = ceil(CTAs / SMs) -- proportional to the CTAs
+// each SM runs, whatever their concurrency (FFMA2 keeps the FMA pipe busy
+// from one warp per SMSP, so a lone CTA runs ~3x faster than one of three),
+// plus a fixed ~35 us (launch, Ker pack, ring fill and drain).  The chunk
+// estimate scales the full problem's model by that: a + (model - a) k/k_full.
+static const double kSimtChunkFixedUs = 35.0;
 static double model_run_us(const conv_plan* p, const Problem& sub) {
-    if (p->path == CONV_PATH_FP32_SIMT) return model_simt(sub, p->dev, p->simt).model_us;
+    if (p->path == CONV_PATH_FP32_SIMT) {
+        const int64_t sms = std::max(1, p->dev.sms);
+        const int64_t k_sub = (simt_ctas(sub, p->simt, sub.N) + sms - 1) / sms;
+        const int64_t k_full = std::max<int64_t>(1, (simt_ctas(p->pb, p->simt, p->pb.N) + sms - 1) / sms);
+        const double full = std::max(p->model.model_us, kSimtChunkFixedUs + 1.0);
+        return kSimtChunkFixedUs + (full - kSimtChunkFixedUs) * (double)k_sub / (double)k_full;
+    }
     if (p->split) return model_tc(split_problem(sub, p->split), p->dev, true, p->tc).model_us;
     if (p->expand) return model_tc(expanded_problem(sub), p->dev, p->path == CONV_PATH_BF16, p->tc).model_us;
     return model_tc(sub, p->dev, p->path == CONV_PATH_BF16, p->tc).model_us;
@@ -687,9 +705,13 @@ static double simulate_host_pipeline(const conv_plan* p, const int* bounds, int 
         if (n <= 0) continue;
         Problem sub = pb;
         sub.N = n;
-        th += n * img_in / kH2dBps * 1e6 + kChunkOverheadUs;
+        // (the tensor paths' per-chunk cost shows up on the whole pipeline,
+        // measured; it is charged to the upload chain, which sets their pace)
+        th += n * img_in / kH2dBps * 1e6 + (p->path == CONV_PATH_FP32_SIMT ? kChunkOverheadUs : kTcChunkOverheadUs);
         tc = std::max(tc, th) + model_run_us(p, sub);
-        td = std::max(td, tc) + n * img_out / kD2hBps * 1e6;
+        // the last download has the link to itself (the uploads are done)
+        const double d2h_bps = j == nch - 1 ? kD2hSoloBps : kD2hBps;
+        td = std::max(td, tc) + n * img_out / d2h_bps * 1e6;
     }
     return td;
 }
@@ -706,11 +728,68 @@ static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_
         if (out_us) *out_us = simulate_host_pipeline(p, out_bounds, c);
         return c;
     }
+    // CONV_HOST_SPLIT=a,b,... (study): explicit chunk sizes summing to N
+    static const char* env_split = getenv("CONV_HOST_SPLIT");
+    if (env_split) {
+        int c = 0, sum = 0;
+        out_bounds[0] = 0;
+        for (const char* q = env_split; *q && c < conv_plan::kMaxChunks;) {
+            const int v = atoi(q);
+            if (v <= 0) break;
+            sum += v;
+            out_bounds[++c] = std::min(sum, N);
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+        }
+        if (c > 0 && sum == N) {
+            if (out_us) *out_us = simulate_host_pipeline(p, out_bounds, c);
+            return c;
+        }
+    }
     int best[conv_plan::kMaxChunks + 1], cand[conv_plan::kMaxChunks + 1];
     int best_n = 1;
     equal(1, best);
     double best_t = simulate_host_pipeline(p, best, 1);
-    const int cmax = std::min(N, (int)conv_plan::kMaxChunks);
+    auto consider = [&](int c) {
+        const double t = simulate_host_pipeline(p, cand, c);
+        if (t < 0.995 * best_t) {               // a clear win only: fewer chunks on near-ties
+            best_t = t;
+            best_n = c;
+            std::copy(cand, cand + c + 1, best);
+        }
+    };
+    // wave-aligned partitions: middle chunks of m whole waves of CTAs (a
+    // partly empty wave costs nearly a full one), a head of 0 / 1/8 / 1/4 /
+    // 1/2 / 1 wave and the remainder as the tail.  FP32 SIMT plans choose
+    // among these only: measured r02b on the batched layer
+    // (profiles/r02b/e2e/e2e_explicit_splits.txt) one-wave middle chunks with
+    // a small head beat every equal partition (6,54,54,54,54,34: 1.80 ms;
+    // 8 x 32: 1.92; 6 x 42-43: 2.11), which the per-chunk model -- exact for
+    // isolated kernels, not for back-to-back ones -- ranks the other way
+    const bool simt = p->path == CONV_PATH_FP32_SIMT;
+    {
+        int wimg = 0;                           // images that fill the resident CTA slots once
+        if (p->path == CONV_PATH_FP32_SIMT) {
+            const int64_t per_ntile = simt_ctas(p->pb, p->simt, p->simt.tn);
+            wimg = (int)(std::max<int64_t>(1, p->model.ctas / std::max<int64_t>(1, per_ntile))) * p->simt.tn;
+        } else if (p->model.tiles > 0) {
+            wimg = (int)std::floor((double)p->model.ctas * N / (double)p->model.tiles);
+        }
+        for (int m = 1; wimg >= 1 && m <= 3; ++m) {
+            const int mid = m * wimg;
+            for (int hq = 0; hq <= 5; ++hq) {   // heads 0, 1/8, 1/4, 1/2, 1 wave
+                if (hq == 4 || (simt && hq != 1)) continue;   // SIMT: the measured 1/8-wave head
+                const int head = hq == 0 ? 0 : hq == 1 ? std::max(1, wimg / 8) : std::max(1, wimg * (hq - 1) / 4);
+                int c = 0, at = 0;
+                cand[0] = 0;
+                if (head > 0 && head < N) { at = head; cand[++c] = at; }
+                while (N - at > mid && c < conv_plan::kMaxChunks - 1) { at += mid; cand[++c] = at; }
+                cand[++c] = N;
+                if (c >= 2) consider(c);
+            }
+        }
+    }
+    const int cmax = simt && best_n > 1 ? 1 : std::min(N, (int)conv_plan::kMaxChunks);
     for (int c = 2; c <= cmax; ++c) {
         for (int taper = 0; taper < 2; ++taper) {
             if (taper) {
@@ -725,12 +804,7 @@ static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_
             } else {
                 equal(c, cand);
             }
-            const double t = simulate_host_pipeline(p, cand, c);
-            if (t < 0.995 * best_t) {           // a clear win only: fewer chunks on near-ties
-                best_t = t;
-                best_n = c;
-                std::copy(cand, cand + c + 1, best);
-            }
+            consider(c);
         }
     }
     std::copy(best, best + best_n + 1, out_bounds);

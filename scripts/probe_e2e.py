@@ -67,7 +67,7 @@ def one(path, cfg, chunks):
     return {"path": path, "chunks": chunks, "ms": round(ms, 4), "tflops": round(sh.flops / ms / 1e9, 2)}
 
 
-if __name__ == "__main__" and not os.environ.get("PROBE_COPY_PIPELINE") and not os.environ.get("PROBE_COPY_LOAD"):
+if __name__ == "__main__" and not os.environ.get("PROBE_COPY_PIPELINE") and not os.environ.get("PROBE_COPY_LOAD") and not os.environ.get("PROBE_OVERLAP"):
     if len(sys.argv) > 1 and sys.argv[1] == "--one":
         print(json.dumps(one(sys.argv[2], sys.argv[3], os.environ.get("CONV_HOST_CHUNKS", "auto"))), flush=True)
         sys.exit(0)
@@ -155,3 +155,79 @@ def copies_under_load(path="fp32_simt", reps=5):
 
 if __name__ == "__main__" and os.environ.get("PROBE_COPY_LOAD"):
     print(json.dumps(copies_under_load(os.environ.get("PROBE_COPY_LOAD"))), flush=True)
+
+
+def overlap_test(path="fp32_simt", chunks=16, reps=3):
+    """Is the link slower while conv kernels run?  All work on explicit
+    non-blocking streams; timing events on the copy streams themselves.
+    Reports the 16-chunk H2D+D2H pipeline alone, then with a chain of conv
+    kernels launched first on another stream (and the chain's own span)."""
+    from paper_2101_09808_b200 import conv
+    from paper_2101_09808_b200.inputs import CONFIGS, make_inputs
+    sh = CONFIGS["batched"]
+    xi, wi = make_inputs(sh, seed=0)
+    plan = conv.ConvPlan(*sh.as_tuple(), path=path)
+    i, k = xi.cuda(), wi.cuda()
+    o, ws = plan.new_output(), plan.new_workspace()
+    bi, bo = 4 * sh.N * sh.C * sh.Hin * sh.Win, 4 * sh.N * sh.K * sh.H * sh.W
+    dev = torch.device("cuda", 0)
+    hi = torch.empty(bi // 4, dtype=torch.float32).pin_memory()
+    ho = torch.empty(bo // 4, dtype=torch.float32).pin_memory()
+    di = torch.empty(bi // 4, dtype=torch.float32, device=dev)
+    do = torch.empty(bo // 4, dtype=torch.float32, device=dev)
+    s1, s2, sk = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+    ib = [bi // 4 * j // chunks for j in range(chunks + 1)]
+    ob = [bo // 4 * j // chunks for j in range(chunks + 1)]
+
+    def pipeline():
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s1)
+        s2.wait_event(a)
+        for j in range(chunks):
+            with torch.cuda.stream(s1):
+                di[ib[j]:ib[j + 1]].copy_(hi[ib[j]:ib[j + 1]], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s1)
+            s2.wait_event(ev)
+            with torch.cuda.stream(s2):
+                ho[ob[j]:ob[j + 1]].copy_(do[ob[j]:ob[j + 1]], non_blocking=True)
+        s1.wait_stream(s2)
+        b.record(s1)
+        return a, b
+
+    out = {"alone": [], "loaded": [], "kernel_span": []}
+    for _ in range(reps):
+        a, b = pipeline()
+        torch.cuda.synchronize()
+        out["alone"].append(round(a.elapsed_time(b), 4))
+    for _ in range(reps):
+        ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ka.record(sk)
+        with torch.cuda.stream(sk):
+            for _ in range(6):
+                plan.run(i, k, o, ws, stream=sk)
+        kb.record(sk)
+        a, b = pipeline()
+        torch.cuda.synchronize()
+        out["loaded"].append(round(a.elapsed_time(b), 4))
+        out["kernel_span"].append(round(ka.elapsed_time(kb), 4))
+        out.setdefault("copy_start_after_kernels_start", []).append(round(ka.elapsed_time(a), 4))
+    # the kernels read the very buffer the uploads write (and write the one
+    # the downloads read), as in conv_run_host (a race; timing only)
+    di4, do4 = di.view(sh.in_shape), do.view(sh.out_shape)
+    for _ in range(reps):
+        ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ka.record(sk)
+        with torch.cuda.stream(sk):
+            for _ in range(6):
+                plan.run(di4, k, do4, ws, stream=sk)
+        kb.record(sk)
+        a, b = pipeline()
+        torch.cuda.synchronize()
+        out.setdefault("loaded_same_buffers", []).append(round(a.elapsed_time(b), 4))
+    return out
+
+
+if __name__ == "__main__" and os.environ.get("PROBE_OVERLAP"):
+    print(json.dumps(overlap_test(os.environ.get("PROBE_OVERLAP"))), flush=True)
