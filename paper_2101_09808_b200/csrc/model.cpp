@@ -507,7 +507,13 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // Table-1 AUTO sweep, profiles/r01b/t1_simt_occupancy.jsonl): 12 warps
     // and 0.7 vs the former 16 and 0.88: 2675 -> 2649 us (R1 -12 %, M3 / M5 /
     // M6 -9..-11 %; Y2 +4 %); the batched layer's tile is unchanged.
-    const double eff = std::min(1.0, warps / 12.0) * (conc == 1 ? 0.7 : 1.0);
+    // (v2 runs FFMA2 since r02b, which occupies the FMA pipe two cycles per
+    // instruction, so fewer warps keep it busy; env CONV_SIMT_EFF_WARPS /
+    // CONV_SIMT_EFF_LONE: the v2 occupancy study, defaults = the r01b fit)
+    static const double eff_warps = getenv("CONV_SIMT_EFF_WARPS") ? atof(getenv("CONV_SIMT_EFF_WARPS")) : 12.0;
+    static const double eff_lone = getenv("CONV_SIMT_EFF_LONE") ? atof(getenv("CONV_SIMT_EFF_LONE")) : 0.7;
+    const double eff = t.ver == 2 ? std::min(1.0, warps / eff_warps) * (conc == 1 ? eff_lone : 1.0)
+                                  : std::min(1.0, warps / 12.0) * (conc == 1 ? 0.7 : 1.0);
     const double fma_cr = (double)pb.S * t.tk * t.tw;
     const double over_cr = t.ver == 2 ? win / 4.0 + pb.S * t.tk / 4.0 + 3.0
                                       : pb.S * (t.tw + t.tk / 4.0 + 1.0);
