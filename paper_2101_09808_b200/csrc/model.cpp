@@ -549,8 +549,17 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // (+ a per-chunk synchronisation charge: a study knob, default 0 --
     // see the bc tie-break in select_simt)
     const double chunk_cyc = std::max(issue_cyc, 2000.0) + kSimtChunkSyncClk;
-    r.issue_cyc = waves * chunks * issue_cyc;
-    r.t_comp_us = waves * chunks * chunk_cyc / clk * 1e6;
+    // v2 (FFMA2): the time goes with the CTAs each SM runs, not with whole
+    // waves -- measured r02b (profiles/r02b/e2e/simt_time_vs_batch.txt,
+    // shard_tiles.txt): the batched tile at N = 6..256 takes 35 + 85 k us for
+    // k = ceil(CTAs / SMs), and at N = 128 the 7-CTA-per-SM kg = 4 tile beat
+    // the 3.5-wave kg = 8 one that whole-wave counting preferred (621 vs
+    // 698 us); a finished CTA's slot is refilled at once, so the last wave
+    // costs its share.  (CONV_SIMT_WHOLE_WAVES=1: the r01b whole-wave count.)
+    static const bool whole_waves = getenv("CONV_SIMT_WHOLE_WAVES") != nullptr;
+    const double wv = (t.ver == 2 && !whole_waves) ? (double)per_sm_total / (double)conc : (double)waves;
+    r.issue_cyc = wv * chunks * issue_cyc;
+    r.t_comp_us = wv * chunks * chunk_cyc / clk * 1e6;
     // L2 -> SMEM: per CTA, every c-chunk loads the In halo tile and Ker slab
     // (Eq. 4's In and Ker footprints).
     const double ker_stage = (double)t.bc * pb.R * pb.S * bko;
