@@ -649,8 +649,15 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
             // 1348 us; charging every chunk instead -- CONV_SIMT_CHUNK_SYNC --
             // lost 2.6 % on the Table-1 total, profiles/r02/t1_simt_sync*.jsonl)
             const bool issue_tie = tie && fabs(r.issue_cyc - best_r.issue_cyc) <= 0.001 * best_r.issue_cyc;
-            if (!found || (issue_tie ? t.bc > best.bc
-                                     : tie ? r.issue_cyc < best_r.issue_cyc : r.model_us < best_r.model_us)) {
+            // v2 near-ties within 1 % of issue: the finer tile (more resident
+            // CTA slots) -- its last CTAs and conv_run_host's chunks balance
+            // better (r02b batched: kg 4 vs kg 8 equal on the device, 1.79 vs
+            // 1.91 ms end to end, profiles/r02b/e2e_kg8.txt)
+            const bool fine_tie = tie && t.ver == 2 && best.ver == 2 && r.ctas != best_r.ctas &&
+                                  fabs(r.issue_cyc - best_r.issue_cyc) <= 0.01 * best_r.issue_cyc;
+            if (!found || (fine_tie ? r.ctas > best_r.ctas
+                           : issue_tie ? t.bc > best.bc
+                                       : tie ? r.issue_cyc < best_r.issue_cyc : r.model_us < best_r.model_us)) {
                 best = t; best_r = r; found = true;
             }
         }
