@@ -298,6 +298,9 @@ struct Simt2Params {
 
 static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth (cp.async layout; TMA default)
 static constexpr int kSimt2MaxStages = 4;  // TMA layout: ring depth p.stages <= this
+#ifndef CONV_SIMT_CC_UNROLL
+#define CONV_SIMT_CC_UNROLL 0              // v2 channel-loop unroll for every instance (A/B builds; 0: the default below)
+#endif
 #ifndef CONV_SIMT_SHFL
 #define CONV_SIMT_SHFL 2                   // TW = 4 halo by warp shuffle: 2 for TK = 8 tiles (default),
 #endif                                     // 1 for every TW = 4 tile, 0 never (A/B builds)
@@ -512,6 +515,12 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
         const float* ker_s = in_s + in_stage;
         const int cc_end = p.C - chunk * p.bc < p.bc ? p.C - chunk * p.bc : p.bc;
         const int R = KR ? KR : p.R;
+        // row mode unrolls the channel loop by 2 so that the next channel's
+        // window and kernel loads overlap this one's FFMA2s (r02b: batched
+        // 1199 -> 1190 us; for the TW = 4 / 8 instances it lost 3 % on
+        // Table 1, Y0 +35 %: profiles/r02b/simt_cc_unroll_ab/)
+        constexpr int kCcUnroll = CONV_SIMT_CC_UNROLL > 0 ? CONV_SIMT_CC_UNROLL : (TW >= 7 ? 2 : 1);
+#pragma unroll kCcUnroll
         for (int cc = 0; cc < cc_end; ++cc) {
             const float* ip = in_s + cc * p.cstride + off;
             const float* kp = ker_s + cc * R * KS * p.bko + kgi * TK;
