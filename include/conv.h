@@ -229,9 +229,16 @@ CONV_API size_t conv_plan_host_run_bytes(const conv_plan* plan);
 
 /* End-to-end call with HOST buffers (pinned for overlap; pageable works but
  * synchronises): copies in/ker host->device into `device_buffer`
- * (>= conv_plan_host_run_bytes, 256-B aligned), runs conv_run, copies Out
- * device->host, all on `stream` with one cudaMemcpyAsync per tensor.  The
- * call is asynchronous: out_host is valid after the stream synchronises. */
+ * (>= conv_plan_host_run_bytes, 256-B aligned), runs the plan's kernels,
+ * copies Out device->host.  Large batches are pipelined over image chunks
+ * (upload of chunk j+1, kernels of chunk j and download of chunk j-1 overlap
+ * on three streams the plan owns; one cudaMemcpyAsync per tensor chunk); the
+ * chunks are chosen once per plan by simulating the pipeline on the
+ * selector's model (conv_plan_describe "host_pipeline").  Everything starts
+ * after the work already queued on `stream`, and `stream` waits for all of
+ * it: the call is asynchronous, out_host is valid after `stream`
+ * synchronises.  Results are bit-identical to conv_run.  Concurrent calls on
+ * one plan are serialised (the pipeline resources are per plan). */
 CONV_API conv_status conv_run_host(const conv_plan* plan, const float* in_host, const float* ker_host,
                           float* out_host, void* device_buffer, void* stream);
 
