@@ -400,3 +400,20 @@ def test_probe_library_exports():
     out = os.popen(f"nm -D --defined-only {build.PROBES_LIB}").read()
     exported = set(re.findall(r" T (probe_\w+)", out))
     assert declared and declared <= exported
+
+
+def test_simt_staging_choice_offline(lib):
+    """FP32 SIMT v2 staging (simt2_layout): the TMA box + bulk Ker copy
+    wherever In rows are 16-B multiples (Win % 4 == 0) and the box fits TMA's
+    256-element dims; the per-thread cp.async layout otherwise, and always for
+    v1 (strided) tiles.  The batched layer's plan is the r02b headline tile."""
+    from paper_2101_09808_b200.inputs import CONFIGS, TABLE1
+    d = _offline(CONFIGS["batched"], "fp32_simt").describe()["tile"]
+    assert (d["ver"], d["tk"], d["tw"], d["tn"], d["th"], d["staging"]) == (2, 4, 14, 2, 14, "tma")
+    for name in ("r2", "det", "tiny"):                       # Win = 58, 138, 10
+        assert _offline(CONFIGS[name], "fp32_simt").describe()["tile"]["staging"] == "cp.async"
+    sh = TABLE1["Y2"]                                        # Win = 272: a row wider than a TMA box
+    assert _offline(sh, "fp32_simt").describe()["tile"]["staging"] == "cp.async"
+    sh = TABLE1["M2"]                                        # stride 2: v1
+    t = conv.ConvPlan(*sh.as_tuple(), path="fp32_simt", offline_device=conv.B200, **sh.plan_kwargs()).describe()["tile"]
+    assert t["ver"] == 1 and t["staging"] == "cp.async"
