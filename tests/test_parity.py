@@ -463,6 +463,27 @@ def test_simt_tma_staging_ragged(shape, tile):
     assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
 
 
+@pytest.mark.parametrize("path", ["fp32_simt", "bf16"])
+def test_run_host_batched_planned_chunks(path):
+    """The bench's e2e call: conv_run_host on the batched layer with the
+    modeled chunk plan (FP32 SIMT: a 1/8-wave head and one-wave chunks;
+    tensor paths: equal chunks) -- bit-identical to conv_run, twice."""
+    sh = CONFIGS["batched"]
+    inp, ker = make_inputs(sh, seed=41)
+    plan = conv.ConvPlan(*sh.as_tuple(), path=path)
+    chunks = plan.describe()["host_pipeline"]["chunks"]
+    assert len(chunks) >= 4 and sum(chunks) == sh.N
+    dev_out = plan.run(inp.cuda(), ker.cuda()).cpu().numpy()
+    dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device="cuda")
+    ih, kh = inp.pin_memory(), ker.pin_memory()
+    out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        out_h.fill_(float("nan"))
+        plan.run_host(ih, kh, out_h, dbuf)
+        torch.cuda.synchronize()
+        assert np.array_equal(out_h.numpy(), dev_out)
+
+
 FUSE_SHAPES = [CONFIGS["tiny"], CONFIGS["r2"], CONFIGS["pw"], CONFIGS["det"],
                Shape(N=5, K=64, C=40, H=6, W=2, R=3, S=3), Shape(N=2, K=40, C=70, H=8, W=10, R=1, S=1),
                Shape(N=7, K=96, C=200, H=10, W=14, R=3, S=3), Shape(N=3, K=32, C=16, H=62, W=30, R=3, S=3)]
