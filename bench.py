@@ -397,7 +397,9 @@ def build_line(args, world, full, spec, paths, results, e2e_ms, g_ms, p10, engin
         # median and a normal 95% CI of the mean beside it
         "step_stats": head["step_stats"],
         "higher_is_better": True,
-        "scaling": "strong" if strong else "weak",
+        # the requested mode (default strong: BASELINE configs[4]'s n-sharded
+        # batch); at N = 1 both modes run the same whole workload
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": head["dtype"],
         "data": "synthetic (seeded uniform[-1,1), BASELINE.json configs)",
@@ -529,9 +531,11 @@ def bench_reference(args):
     line = {
         "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded uniform[-1,1), BASELINE.json configs)",
-        "config": {"workload": f"{args.config}: N={sh.N} K={sh.K} C={sh.C} out {sh.H}x{sh.W} R={sh.R} S={sh.S}",
+        # the same workload string as our arm's line (the driver compares them)
+        "config": {"workload": f"{args.config}: N={sh.N} K={sh.K} C={sh.C} out {sh.H}x{sh.W} R={sh.R} S={sh.S} "
+                               f"(stride 1, no pad, fp32 NCHW/KCRS)",
                    "sample_images_per_step": n},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": used, "kind": "oracle",

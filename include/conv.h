@@ -171,7 +171,11 @@ CONV_API conv_status conv_plan_set_path(conv_plan* plan, conv_path path);
  * input tile staged once per CTA in shared memory, the filter taps as
  * shifted tcgen05 descriptors; stride 1, dilation 1, no padding,
  * C*elem <= 128 B, K <= 256; only on request); for the SIMT
- * path: ver, tk, tw, kg, pw, tn, th, bc.  Unspecified keys keep the
+ * path: ver, tk, tw, kg, pw, tn, th, bc, splits (split-C), flat (0/1: v2
+ * row mode over whole images, TW = W in {7, 14}, Win % 4 == 0: each CTA's
+ * 32*pw lanes take consecutive (image, row) slots of the flattened batch,
+ * so no lane is padding; tn is then the images one In box spans and th = H).
+ * Unspecified keys keep the
  * selector's choice.  NULL or "" restores the selector's choice.
  * INVALID_ARGUMENT on a malformed spec, INFEASIBLE if the tile exceeds
  * SMEM/TMEM/register capacity (Eq. 4, per level). */

@@ -426,7 +426,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             std::string key = kv.substr(0, eq);
             char* end = nullptr;
             long v = strtol(kv.c_str() + eq + 1, &end, 10);
-            const long vmin = (key == "fuse" || key == "pre_c" || key == "expand" || key == "halo") ? 0 : 1;
+            const long vmin = (key == "fuse" || key == "pre_c" || key == "expand" || key == "halo" || key == "flat") ? 0 : 1;
             if (!end || *end || v < vmin || v > 4096) return fail(CONV_ERR_INVALID_ARGUMENT, "bad value in '%s'", kv.c_str());
             if (key == "bn") ft.bn = (int)v;
             else if (key == "stages") ft.stages = (int)v;
@@ -446,6 +446,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "th") { fs.th = (int)v; mask |= 32; }
             else if (key == "bc") { fs.bc = (int)v; mask |= 64; }
             else if (key == "ver") { fs.ver = (int)v; mask |= 128; }
+            else if (key == "flat") { fs.flat = v ? 1 : 0; mask |= 512; }
             else return fail(CONV_ERR_INVALID_ARGUMENT, "unknown tile key '%s'", key.c_str());
         }
         if (ft.bn && ft.bn != 32 && ft.bn != 64 && ft.bn != 128 && ft.bn != 192 && ft.bn != 256)
@@ -511,9 +512,9 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
         // staging: "tma" (one 4-D TMA box + a bulk Ker copy per chunk) or
         // "cp.async" (per-thread copies; v1, and v2 where Win % 4 != 0)
         const bool tma = p->simt.ver == 2 && simt2_layout(pb, p->simt).tma;
-        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"splits\":%d,\"threads\":%d,\"staging\":\"%s\"}",
+        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"splits\":%d,\"flat\":%d,\"threads\":%d,\"staging\":\"%s\"}",
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
-                 p->simt.splits, 32 * p->simt.kg * p->simt.pw, tma ? "tma" : "cp.async");
+                 p->simt.splits, p->simt.flat, 32 * p->simt.kg * p->simt.pw, tma ? "tma" : "cp.async");
     } else {
         snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"split\":%d,\"halo\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
                  128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->split, p->tc.halo, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,

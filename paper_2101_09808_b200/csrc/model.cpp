@@ -474,10 +474,12 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const long ntile = (pb.N + t.tn - 1) / t.tn, htile = (pb.H + t.th - 1) / t.th, ktile = (pb.K + bko - 1) / bko;
     const double nchunks_all = ceil((double)pb.C / t.bc);
     const int splits = std::max(1, std::min(t.splits, (int)nchunks_all));
-    r.tiles = ntile * htile * ktile * splits;       // CTAs (split-C: one per split of a tile)
+    r.tiles = t.flat ? (long)simt_ctas(pb, t, pb.N)   // flat: 32*pw (image, row) slots per CTA
+                     : ntile * htile * ktile * splits;  // CTAs (split-C: one per split of a tile)
     const int threads = 32 * t.kg * t.pw;
     const size_t smem = simt_smem_bytes(pb, t);
     r.smem = smem;
+    if (smem == SIZE_MAX) { r.model_us = 1e30; return r; }
     // Register level (Sec. 6 microkernel analog): TK*TW accumulators + the
     // input window + TK kernel values + addressing; ptxas caps at 128.
     const int win = t.ver == 2 ? (t.tw + pb.S - 1 + 3) / 4 * 4 : t.tw;
@@ -525,7 +527,14 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // v1 (strided scalar loads) measured 3.5x its model on r2 (62.5 vs 17.8
     // us, r01b simt_sweep2): charged 4x so that it is picked only where v2
     // cannot run (S not in {1, 3})
-    const double issue_factor = (1.0 + over_cr / fma_cr) * (t.ver == 2 ? (row_mode ? 1.0 : 1.25) : 4.0);
+    // Flat row-mode tiles (every lane an output row) measured ~4 % slower per
+    // CTA than per-image row tiles of the same register tile (r02c,
+    // profiles/r02c/flat_ab.txt: (T - 35 us) / (CTAs per SM) = 86.8-87.6 vs
+    // 83.5-84.3 us on the batched layer at N = 256 / 128 -- the box's zero
+    // rows up to rows_box and the 4-channel chunks their smem allows)
+    static const double kSimtFlatCost = 1.04;
+    const double issue_factor = (1.0 + over_cr / fma_cr) * (t.ver == 2 ? (row_mode ? 1.0 : 1.25) : 4.0) *
+                                (t.flat ? kSimtFlatCost : 1.0);
     const double chunks = ceil(nchunks_all / splits);    // per CTA
     // one chunk: every thread's FFMAs, plus the cp.async copies (one per 4-B
     // element in v1/v2 In rows, ~6 instructions each, spread over the CTA)
@@ -577,8 +586,8 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
                  const SimtTile* forced, unsigned forced_mask, std::string& why) {
     bool found = false;
     const int tks[2] = {4, 8};
-    const int kgs[4] = {1, 2, 4, 8};
-    const int bcs[3] = {4, 8, 16};
+    const int kgs[4] = {1, 2, 4, 8};   // (3, 5, 6: CTAs of 3-6 warps load the 4 SMSPs unevenly; flat r02c 1.2-1.3x slower)
+    const int bcs[4] = {2, 4, 8, 16};   // 2: flat tiles (or forced) only
     const int tn_max = std::min(pb.N, 16);
     // v2 first when it can run and nothing is forced; v1 only if no v2 tile fits
     const bool tile_forced = forced && (forced_mask & ~256u);   // a tile key other than splits
@@ -599,10 +608,26 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     for (int kg : kgs)
     for (int pw = 1; pw * kg <= 16; ++pw)
     for (int tn = 1; tn <= tn_max; tn = (tn < 4 ? tn + 1 : tn * 2))
-    for (int bc : bcs) {
+    for (int bc : bcs)
+    for (int fl = 0; fl < 2; ++fl) {
         SimtTile t;
         t.tk = tk; t.tw = tw; t.kg = kg; t.pw = pw; t.tn = tn; t.bc = bc; t.ver = ver;
+        if (fl) {
+            // flat row mode (whole images, every lane an output row): once
+            // per register tile, where the row-mode TMA layout applies
+            if (ver != 2 || tn != 1 || tw != pb.W || !simt_v2_tw_ok(pb, tw)) continue;
+            t.flat = 1;
+            t.th = pb.H;
+            t.tn = simt_flat_images(pb, t);
+            if (!simt2_layout(pb, t).tma) continue;
+        }
+        // 2-channel chunks and CTAs under 4 warps: forced only (flat r02c:
+        // kg 2 / bc 2 1181 us vs kg 4 / bc 4 1163 on the batched layer, which
+        // the model, blind to the per-chunk waits, ranked the other way)
+        if (bc == 2 && !(forced && (forced_mask & 64))) continue;
+        if (t.flat && t.kg * t.pw < 4 && !tile_forced) continue;
         if (forced) {
+            if ((forced_mask & 512) && t.flat != forced->flat) continue;
             if ((forced_mask & 1) && t.tk != forced->tk) continue;
             if ((forced_mask & 2) && t.tw != forced->tw) continue;
             if ((forced_mask & 4) && t.kg != forced->kg) continue;
@@ -612,6 +637,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         }
         if (!simt_tile_supported(t)) continue;
         if (ver == 2 && !simt_v2_tw_ok(pb, tw)) continue;
+        if (!t.flat) {
         // rows per tile: as many as the pixel slots allow
         const long slots = 32L * pw;                                   // lanes per k-group
         const long per_row = ver == 2 ? (pb.W + tw - 1) / tw : pb.W;   // slots one output row needs
@@ -624,11 +650,14 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         const bool whole = th >= pb.H && tn >= pb.N;
         if (2L * tn * th * per_row < cap && !whole && !(forced && (forced_mask & 32))) continue;
         t.th = th;
+        } else if (forced && (forced_mask & 32) && forced->th != pb.H) {
+            continue;
+        }
         if (simt_smem_bytes(pb, t) > dev.smem_optin) continue;
         if (t.kg > 1 && t.kg * t.tk >= 2 * pb.K && !tile_forced) continue;  // mostly-empty k tile
         // split-C while the grid is small (each CTA would otherwise walk the
         // whole C reduction alone): S partial outputs, summed in split order
-        const long ctas = (long)((pb.N + tn - 1) / tn) * ((pb.H + th - 1) / th) * ((pb.K + kg * tk - 1) / (kg * tk));
+        const long ctas = simt_ctas(pb, t, pb.N);
         const int nchunks = (pb.C + bc - 1) / bc;
         // forced tiles: the forced split count (tile key splits), else none
         static const int kSimtSplits[] = {1, 2, 4, 8, 16};

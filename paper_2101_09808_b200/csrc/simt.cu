@@ -293,7 +293,10 @@ struct Simt2Params {
     int ktiles;       // ceil(K / bko): grid x = (image tile, row tile) * ktiles + k tile -- the k
                       //    tiles of an image tile run together, so its In tile is read from HBM once
     int vec4;         // Win % 4 == 0: 16-B copies of input rows
-    uint32_t tx_in;   // TMA layout: bytes of one In box (tn * bc * rows_in * pitch * 4)
+    uint32_t tx_in;   // TMA layout: bytes of one In box (tn * bc * rows_box * pitch * 4)
+    int flat;         // flat row mode (SimtTile::flat): grid x = slot tile * ktiles + k tile, slot tile
+                      //    = 32*pw consecutive (image, row) slots; the box starts at the slot tile's
+                      //    first image, smem [c][img][rows_box][pitch] (istride = rows_box * pitch)
 };
 
 static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth (cp.async layout; TMA default)
@@ -333,27 +336,45 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
 
     const int bx = gridDim.y > 1 ? (int)blockIdx.x : (int)blockIdx.x / p.ktiles;
     const int kb = gridDim.y > 1 ? (int)blockIdx.y : (int)blockIdx.x - bx * p.ktiles;
-    const int nt = bx / p.n_htiles;
-    const int ht = bx - nt * p.n_htiles;
-    const int n0 = nt * p.tn;
-    const int h0 = ht * p.th;
     const int k0 = kb * p.bko;
-
-    // this thread's pixel group: (img, row, g) -> pixels w0 .. w0+TW-1 of one row
     const int q = pwi * 32 + lane;
-    const int per_img = p.th * p.groups;
-    const int img = q / p.lpi;
-    const int rem = q - img * p.lpi;
-    // a padding slot (TMA layout: rem >= per_img) reads the last real slot's
-    // window -- the same addresses, a broadcast -- instead of row 0's, which
-    // shared 16-B bank groups with the quarter-warp's real rows (ncu r02b:
-    // 6 wavefronts per window LDS.128 instead of 4)
-    const int remc = rem < per_img ? rem : per_img - 1;
-    const int row = remc / p.groups;
-    const int g = remc - row * p.groups;
+    // n0 / h0: the In box origin (image, row); n_out / h_out: this thread's output row
+    int n0, h0, n_out, h_out, g, off;
+    bool valid;
+    if (p.flat) {
+        // flat row mode: slot s0 + q of the flattened (image, row) batch;
+        // the box holds the images from the slot tile's first one on
+        const int s0 = bx * p.slots;
+        n0 = s0 / p.H;
+        h0 = 0;
+        const int slot = s0 + q;
+        n_out = slot / p.H;
+        h_out = slot - n_out * p.H;
+        g = 0;
+        valid = n_out < p.N;
+        off = valid ? (n_out - n0) * p.istride + h_out * p.pitch : 0;
+    } else {
+        const int nt = bx / p.n_htiles;
+        const int ht = bx - nt * p.n_htiles;
+        n0 = nt * p.tn;
+        h0 = ht * p.th;
+        // this thread's pixel group: (img, row, g) -> pixels w0 .. w0+TW-1 of one row
+        const int per_img = p.th * p.groups;
+        const int img = q / p.lpi;
+        const int rem = q - img * p.lpi;
+        // a padding slot (TMA layout: rem >= per_img) reads the last real slot's
+        // window -- the same addresses, a broadcast -- instead of row 0's, which
+        // shared 16-B bank groups with the quarter-warp's real rows (ncu r02b:
+        // 6 wavefronts per window LDS.128 instead of 4)
+        const int remc = rem < per_img ? rem : per_img - 1;
+        const int row = remc / p.groups;
+        g = remc - row * p.groups;
+        valid = q < p.slots && rem < per_img && (n0 + img) < p.N && (h0 + row) < p.H;
+        off = q < p.slots ? img * p.istride + row * p.pitch + g * TW : 0;
+        n_out = n0 + img;
+        h_out = h0 + row;
+    }
     const int w0 = g * TW;
-    const bool valid = q < p.slots && rem < per_img && (n0 + img) < p.N && (h0 + row) < p.H;
-    const int off = q < p.slots ? img * p.istride + row * p.pitch + w0 : 0;
 
 #if CONV_SIMT_FFMA2
     // FFMA2 (fma.rn.f32x2, sm_100): output channels in pairs, acc2[i][j] =
@@ -457,7 +478,8 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
         const int cvalid = p.C - c0 < p.bc ? p.C - c0 : p.bc;
         const uint32_t kbytes = (uint32_t)cvalid * p.R * KS * p.bko * 4u;
         sm100::mbar_arrive_expect_tx(&full_bar[buf], p.tx_in + kbytes);
-        sm100::tma_load_4d(in_s, &tmap_in, &full_bar[buf], 0, h0, c0, n0);
+        if (p.flat) sm100::tma_load_4d(in_s, &tmap_in, &full_bar[buf], 0, 0, n0, c0);   // dims {Win, Hin, N, C}
+        else sm100::tma_load_4d(in_s, &tmap_in, &full_bar[buf], 0, h0, c0, n0);
         sm100::bulk_load_g2s(ker_s, kerp + (((int64_t)kb * p.C + c0) * p.R * KS) * p.bko, kbytes, &full_bar[buf]);
     };
 
@@ -588,7 +610,6 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     }
 
     if (!valid) return;
-    const int h = h0 + row;
 #if CONV_SIMT_FFMA2
     float acc[TK][TW];
 #pragma unroll
@@ -603,7 +624,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     for (int i = 0; i < TK; ++i) {
         const int k = k0 + kgi * TK + i;
         if (k >= p.K) break;
-        float* o = out + (((int64_t)(n0 + img) * p.K + k) * p.H + h) * p.W + w0;
+        float* o = out + (((int64_t)n_out * p.K + k) * p.H + h_out) * p.W + w0;
 #pragma unroll
         for (int j = 0; j < TW; ++j)
             if (w0 + j < p.W) o[j] = acc[i][j];
@@ -682,10 +703,33 @@ Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
     static const bool no_tma = getenv("CONV_SIMT_NO_TMA") != nullptr;
     static const int env_stages = getenv("CONV_SIMT_STAGES") ? atoi(getenv("CONV_SIMT_STAGES")) : 0;
     L.tma = !no_tma && t.ver == 2 && simt_v2_ok(pb) && pb.Win() % 4 == 0 && L.pitch <= 256 && rows_in <= 256 &&
-            t.bc <= 256 && t.tn <= 256 && (pb.R == 1 || pb.R == 3) && t.tn * lpi8 <= 32 * t.pw;
-    L.stages = L.tma && env_stages >= 2 && env_stages <= kSimt2MaxStages ? env_stages : kSimt2Stages;
+            t.bc <= 256 && t.tn <= 256 && (pb.R == 1 || pb.R == 3) && (t.flat || t.tn * lpi8 <= 32 * t.pw);
+    // (flat tiles: a 2-deep ring by default -- their boxes carry the zero
+    // rows up to rows_box, and 3 stages would cost a resident CTA per SM)
+    L.stages = L.tma && env_stages >= 2 && env_stages <= kSimt2MaxStages ? env_stages : t.flat ? 2 : kSimt2Stages;
     const int ker_stage = t.bc * pb.R * pb.S * t.kg * t.tk;
-    if (L.tma) {
+    if (t.flat) {
+        // flat row mode: smem [c][img][rows_box][pitch] (the tensor map's
+        // image and channel dims swapped), rows_box = rows_in rounded up to
+        // = H (mod 8).  Slot q of the CTA sits at (img*rows_box + row)*pitch;
+        // with an odd number of 16-B units per row, 8 consecutive slots then
+        // fall on 8 distinct bank groups even where they cross an image
+        // (img*rows_box + row = q + img*(rows_box - H)).
+        const bool ok = L.tma && groups == 1 && t.th == pb.H;
+        L.tma = ok;
+        if (!ok) { L.in_stage = -1; return L; }
+        int rb = rows_in;
+        while ((rb - pb.H) % 8 != 0) ++rb;
+        L.rows_box = rb;
+        const int nb = simt_flat_images(pb, t);
+        if (rb > 256 || nb > 256) { L.tma = false; L.in_stage = -1; return L; }
+        L.istride = rb * L.pitch;
+        L.cstride = nb * L.istride;
+        L.in_stage = t.bc * L.cstride;
+        L.lpi = pb.H;
+        L.stage_floats = (L.in_stage + ker_stage + 31) / 32 * 32;
+    } else if (L.tma) {
+        L.rows_box = rows_in;
         L.cstride = rows_in * L.pitch;
         L.istride = t.bc * L.cstride;            // the box is dense: [img][c][row][pitch]
         L.in_stage = t.tn * L.istride;
@@ -704,6 +748,7 @@ Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
 size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
     if (t.ver == 2) {
         const Simt2Layout L = simt2_layout(pb, t);
+        if (L.in_stage < 0) return SIZE_MAX;      // infeasible (flat without the TMA layout)
         // TMA layout: + the mbarriers' 128-B aligned static slot
         return (size_t)L.stages * L.stage_floats * sizeof(float) + (L.tma ? 128 : 0);
     }
@@ -845,10 +890,14 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
         q.nchunks = p.nchunks;
         q.cper = p.cper;
         q.zstride = p.zstride;
-        q.slots = t.tn * L.lpi;
+        q.flat = t.flat ? 1 : 0;
+        if (t.flat && !L.tma) { err = "SIMT flat tile needs the TMA row-mode layout (th = H, TW = W, Win % 4 == 0)"; return cudaErrorInvalidValue; }
+        const int box_imgs = t.flat ? simt_flat_images(pb, t) : t.tn;
+        q.slots = t.flat ? 32 * t.pw : t.tn * L.lpi;
         if (q.slots > t.pw * 32) { err = "SIMT v2 tile: pixel-group slots > pw*32"; return cudaErrorInvalidValue; }
         q.vec4 = (q.Win % 4 == 0) ? 1 : 0;
-        q.tx_in = (uint32_t)((size_t)t.tn * t.bc * q.rows_in * q.pitch * sizeof(float));
+        q.tx_in = (uint32_t)((size_t)box_imgs * t.bc * L.rows_box * q.pitch * sizeof(float));
+        if (t.flat) grid.x = (unsigned)(((int64_t)pb.N * pb.H + q.slots - 1) / q.slots);
         q.stages = L.stages;
         q.ktiles = (pb.K + p.bko - 1) / p.bko;
         static const bool grid2d = getenv("CONV_SIMT_GRID2D") != nullptr;   // A/B: the r02 2-D grid (k tile = y)
@@ -861,10 +910,15 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
             // >= Win (the pitch padding), rows >= Hin, channels >= C and
             // images >= N are zero-filled
             if (!driver_init(err)) return cudaErrorInvalidValue;
-            cuuint64_t dims[4] = {(cuuint64_t)q.Win, (cuuint64_t)q.Hin, (cuuint64_t)pb.C, (cuuint64_t)pb.N};
-            cuuint64_t strides[3] = {(cuuint64_t)q.Win * 4, (cuuint64_t)q.Hin * q.Win * 4,
-                                     (cuuint64_t)pb.C * q.Hin * q.Win * 4};
-            cuuint32_t box[4] = {(cuuint32_t)q.pitch, (cuuint32_t)q.rows_in, (cuuint32_t)t.bc, (cuuint32_t)t.tn};
+            // (flat: {Win, Hin, N, C}, box {pitch, rows_box, images, bc} -- the
+            // image dim inside the channel dim, so a channel's images are
+            // consecutive row blocks in smem)
+            const cuuint64_t plane_b = (cuuint64_t)q.Hin * q.Win * 4, image_b = (cuuint64_t)pb.C * plane_b;
+            cuuint64_t dims[4] = {(cuuint64_t)q.Win, (cuuint64_t)q.Hin, (cuuint64_t)(t.flat ? pb.N : pb.C),
+                                  (cuuint64_t)(t.flat ? pb.C : pb.N)};
+            cuuint64_t strides[3] = {(cuuint64_t)q.Win * 4, t.flat ? image_b : plane_b, t.flat ? plane_b : image_b};
+            cuuint32_t box[4] = {(cuuint32_t)q.pitch, (cuuint32_t)L.rows_box, (cuuint32_t)(t.flat ? box_imgs : t.bc),
+                                 (cuuint32_t)(t.flat ? t.bc : t.tn)};
             cuuint32_t estr[4] = {1, 1, 1, 1};
             CUresult r = g_encode_tiled(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in), dims, strides,
                                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -1,11 +1,13 @@
 #!/bin/bash
-# r02b SIMT A/B: TMA padded vs flat lane-filling tiles, FFMA vs FFMA2, ring depth
+# r02c: flat row-mode SIMT tiles (every lane an output row) vs the per-image
+# row-mode tile on the batched layer, parity tests first
 cd "$(dirname "$0")/.."
-P="ver=2,tk=4,tw=14,kg=8,pw=1,tn=2,th=14,bc=8;ver=2,tk=4,tw=14,kg=4,pw=1,tn=2,th=14,bc=8"
-F="ver=2,tk=4,tw=14,kg=1,pw=7,tn=16,th=14,bc=1;ver=2,tk=4,tw=14,kg=1,pw=7,tn=16,th=14,bc=2;ver=2,tk=4,tw=14,kg=2,pw=7,tn=16,th=14,bc=1;ver=2,tk=4,tw=14,kg=2,pw=7,tn=16,th=14,bc=2"
-out=gpurun_out/sw7_flat.txt
-: > $out
-python scripts/simt_sweep7.py batched 256 ";$P;$F" | sed "s/^/ffma2 s3 /" >> $out 2>&1
-CONV_SIMT_STAGES=4 python scripts/simt_sweep7.py batched 256 "$P;$F" | sed "s/^/ffma2 s4 /" >> $out 2>&1
-CONV_SIMT_STAGES=2 python scripts/simt_sweep7.py batched 256 "$F" | sed "s/^/ffma2 s2 /" >> $out 2>&1
-CONV_LIB=_ab_fma1/libconv.so python scripts/simt_sweep7.py batched 256 "$P;$F" | sed "s/^/ffma s3 /" >> $out 2>&1
+O=gpurun_out/r02c_flat
+mkdir -p $O
+timeout 600 python -m pytest tests/test_parity.py -m gpu -q -x -k "flat or tma_staging" > $O/pytest_flat.log 2>&1; tail -3 $O/pytest_flat.log
+T="ver=2,tk=4,tw=14,kg=4,pw=1,tn=2,th=14,bc=8;flat=1,tk=4,kg=4,pw=1,bc=4;flat=1,tk=4,kg=4,pw=2,bc=4;flat=1,tk=4,kg=8,pw=1,bc=4;flat=1,tk=4,kg=2,pw=1,bc=4;flat=1,tk=4,kg=2,pw=2,bc=4;flat=1,tk=4,kg=4,pw=1,bc=8"
+for st in 2 3; do
+  CONV_SIMT_STAGES=$st timeout 600 python scripts/simt_sweep7.py batched 256,128 "$T" 2>&1 | sed "s/^/s$st /" >> $O/flat_ab.txt
+done
+timeout 300 python scripts/simt_sweep7.py batched 256 "" 2>&1 | sed "s/^/auto /" >> $O/flat_ab.txt
+grep -o '"spec": "[^"]*".*"us": [0-9.]*' $O/flat_ab.txt | sed 's/"tile".*"us"/us/' | head -40

@@ -160,7 +160,15 @@ def test_selector_respects_capacity(lib, path):
             assert d["tile"]["cp"] >= sh.C and (d["tile"]["cp"] * (2 if path == "bf16" else 4)) % 32 == 0
         else:
             t = d["tile"]
-            assert t["threads"] <= 512 and t["tn"] * t["th"] * sh.W <= t["threads"] // 32 // t["kg"] * 32 * t["tw"]
+            lanes = t["threads"] // 32 // t["kg"] * 32           # output-row slots per k group
+            assert t["threads"] <= 512
+            if t["flat"]:
+                # flat row mode: whole images (th = H, TW = W), 32*pw consecutive
+                # (image, row) slots per CTA, tn = the images such a run can span
+                assert t["th"] == sh.H and t["tw"] == sh.W and t["staging"] == "tma"
+                assert t["tn"] == min(sh.N, (lanes + sh.H - 2) // sh.H + 1)
+            else:
+                assert t["tn"] * t["th"] * sh.W <= lanes * t["tw"]
 
 
 def test_selector_forced_tiles(lib):
@@ -406,10 +414,16 @@ def test_simt_staging_choice_offline(lib):
     """FP32 SIMT v2 staging (simt2_layout): the TMA box + bulk Ker copy
     wherever In rows are 16-B multiples (Win % 4 == 0) and the box fits TMA's
     256-element dims; the per-thread cp.async layout otherwise, and always for
-    v1 (strided) tiles.  The batched layer's plan is the r02b headline tile."""
+    v1 (strided) tiles.  The batched layer's plan is the r02c headline tile
+    (flat row mode: 32 consecutive (image, row) slots per CTA, boxes of 4
+    images); its 128-image shard keeps the per-image r02b tile."""
+    import dataclasses
     from paper_2101_09808_b200.inputs import CONFIGS, TABLE1
     d = _offline(CONFIGS["batched"], "fp32_simt").describe()["tile"]
-    assert (d["ver"], d["tk"], d["tw"], d["tn"], d["th"], d["staging"]) == (2, 4, 14, 2, 14, "tma")
+    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["tn"], d["th"], d["bc"], d["flat"], d["staging"]) == \
+        (2, 4, 14, 4, 4, 14, 4, 1, "tma")
+    d = _offline(dataclasses.replace(CONFIGS["batched"], N=128), "fp32_simt").describe()["tile"]
+    assert (d["ver"], d["tk"], d["tw"], d["tn"], d["th"], d["flat"], d["staging"]) == (2, 4, 14, 2, 14, 0, "tma")
     for name in ("r2", "det", "tiny"):                       # Win = 58, 138, 10
         assert _offline(CONFIGS[name], "fp32_simt").describe()["tile"]["staging"] == "cp.async"
     sh = TABLE1["Y2"]                                        # Win = 272: a row wider than a TMA box

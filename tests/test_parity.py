@@ -463,6 +463,44 @@ def test_simt_tma_staging_ragged(shape, tile):
     assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
 
 
+# FP32 SIMT flat row mode (tile key flat=1): a CTA's 32*pw lanes take
+# consecutive (image, row) slots across image boundaries; ragged batches
+# (slot tiles past N), ragged k and channel chunks, H not a multiple of
+# anything, one image (half the lanes idle), split-C
+SIMT_FLAT_CASES = [
+    (Shape(N=9, K=40, C=20, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4"),
+    (Shape(N=9, K=40, C=20, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=2,pw=2,bc=8"),
+    (Shape(N=5, K=44, C=13, H=9, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=8"),
+    (Shape(N=3, K=24, C=11, H=5, W=14, R=3, S=3), "flat=1,tk=4,kg=2,pw=1,bc=4"),
+    (Shape(N=1, K=16, C=8, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4"),
+    (Shape(N=4, K=32, C=40, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4,splits=3"),
+    (Shape(N=11, K=44, C=12, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=8,pw=1,bc=4"),
+    (Shape(N=6, K=36, C=9, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=1,pw=2,bc=8"),
+]
+
+
+@pytest.mark.parametrize("shape,tile", SIMT_FLAT_CASES, ids=lambda x: x if isinstance(x, str) else "x".join(map(str, x.as_tuple())))
+def test_simt_flat_row_mode(shape, tile):
+    """Flat row-mode tiles: 1e-5 against the double oracle, bit-exact on the
+    integer twin, and bit-identical to the per-image row-mode tile (every
+    output row is the same thread-level FFMA2 sequence, only the lane that
+    runs it differs)."""
+    inp, ker = make_inputs(shape, seed=33)
+    got, plan = run(shape, inp, ker, "fp32_simt", tile=tile)
+    t = plan.describe()["tile"]
+    assert t["flat"] == 1 and t["staging"] == "tma" and t["th"] == shape.H
+    assert rel_l2(got, oracle.conv_eq1(inp.numpy(), ker.numpy())) <= TOL["fp32_simt"]
+    per_image = f"ver=2,tk=4,tw=14,kg={t['kg']},pw=1,tn=1,th={shape.H},bc={t['bc']},flat=0"
+    if t["splits"] > 1:
+        per_image += f",splits={t['splits']}"
+    ref_tile, p2 = run(shape, inp, ker, "fp32_simt", tile=per_image)
+    assert p2.describe()["tile"]["flat"] == 0
+    assert np.array_equal(got, ref_tile)
+    xi, wi = make_inputs(shape, seed=34, kind="int")
+    goti, _ = run(shape, xi, wi, "fp32_simt", tile=tile)
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
 @pytest.mark.parametrize("path", ["fp32_simt", "bf16"])
 def test_run_host_batched_planned_chunks(path):
     """The bench's e2e call: conv_run_host on the batched layer with the
