@@ -145,11 +145,13 @@ static bool select_tensor(conv_plan* p, bool bf16, TcTile& tt, ModelResult& rt, 
 // pieces (tc_run)
 static TcLayout split_layout(const Problem& real, const Problem& ps) {
     TcLayout L = tc_layout(ps, true);
-    // opt-in (env CONV_SPLIT_COMPACT=1): measured r02 on the batched layer the
-    // compact layout's transform is 16 us shorter (36 vs 52 us) but its main
-    // kernel 7-12 % longer (264-273 vs 244-247 us), a wash (186-200 vs
-    // 194-200 TFLOP/s, same box, alternating) -- default off
-    static const bool compact = getenv("CONV_SPLIT_COMPACT") && atoi(getenv("CONV_SPLIT_COMPACT")) == 1;
+    // default since r02c (env CONV_SPLIT_COMPACT=0: the 6-pair layout): on
+    // the batched layer the compact layout's transform is 16-18 us shorter
+    // (35 vs 52-55 us) and its main kernel ~5 % longer (262-264 vs 249-263
+    // us); r02 measured that a wash (186-200 vs 194-200 TFLOP/s), r02c
+    // 200.8-202.5 vs 190.0-197.9 TFLOP/s over three alternations on one box
+    // (profiles/r02c/ab/)
+    static const bool compact = !(getenv("CONV_SPLIT_COMPACT") && atoi(getenv("CONV_SPLIT_COMPACT")) == 0);
     if (compact && split_compact_ok(real, L.bkc)) {
         L.a_chan = 3 * split_cq(real.C);
         L.in_ws_bytes = (size_t)real.N * real.Hin() * real.Win() * L.a_chan * L.elem;
@@ -770,7 +772,13 @@ static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_
     const bool simt = p->path == CONV_PATH_FP32_SIMT;
     {
         int wimg = 0;                           // images that fill the resident CTA slots once
-        if (p->path == CONV_PATH_FP32_SIMT) {
+        if (p->path == CONV_PATH_FP32_SIMT && p->simt.flat) {
+            // flat tiles: whole slot tiles (32*pw image rows) x k tiles per wave
+            const int64_t per_slot_tile = std::max<int64_t>(1, simt_ctas(p->pb, p->simt, 1) /
+                                                                   ((p->pb.H + 32 * p->simt.pw - 1) / (32 * p->simt.pw)));
+            const int64_t slot_tiles = std::max<int64_t>(1, p->model.ctas / per_slot_tile);
+            wimg = (int)std::max<int64_t>(1, slot_tiles * 32 * p->simt.pw / p->pb.H);
+        } else if (p->path == CONV_PATH_FP32_SIMT) {
             const int64_t per_ntile = simt_ctas(p->pb, p->simt, p->simt.tn);
             wimg = (int)(std::max<int64_t>(1, p->model.ctas / std::max<int64_t>(1, per_ntile))) * p->simt.tn;
         } else if (p->model.tiles > 0) {
