@@ -95,6 +95,58 @@ __global__ void __launch_bounds__(256) reduce_splits(const float* __restrict__ p
 }
 
 // Packing kernel: Ker KCRS -> [ceil(K/bko)][C][R][S][bko], k >= K zero.
+// k tile kb's source is ONE contiguous [bko][C*R*S] block of KCRS and its
+// destination the contiguous [C*R*S][bko] block, so the pack is a transpose
+// per k tile: a CTA stages a bko x cw slice (cw = 1024 / bko columns) in
+// shared memory with coalesced row reads and writes it back with coalesced
+// column-major stores.  (r02c: the per-element gather below it read each
+// element from its own 32-B sector -- 1.1-1.3 TB/s on the large Table-1
+// layers, 25 % of the Table-1 SIMT step time; tiled 16-B: Table-1 SIMT
+// total 2329 -> 2042 us.)
+__global__ void __launch_bounds__(256) pack_ker_simt_tiled(const float* __restrict__ ker, float* __restrict__ out,
+                                                           int K, int CRS, int bko, int cw, int nchunk) {
+    __shared__ float tile[1024 + 64];            // bko x (cw + 1), bko * cw = 1024
+    const int kb = (int)blockIdx.x / nchunk;
+    const int c0 = ((int)blockIdx.x - kb * nchunk) * cw;
+    const int ncol = CRS - c0 < cw ? CRS - c0 : cw;
+    const int pitch = cw + 1;                    // odd: the column reads hit distinct banks
+    if ((CRS & 3) == 0) {
+        // 16-B units both ways (CRS % 4 == 0: rows, c0 and the output block
+        // are 16-B aligned; bko is a multiple of 4)
+        const int cw4 = cw >> 2;
+        for (int e = threadIdx.x; e < bko * cw4; e += blockDim.x) {
+            const int r = e / cw4, j = (e - r * cw4) * 4;
+            const int k = kb * bko + r;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (k < K && j < ncol) v = __ldg(reinterpret_cast<const float4*>(ker + (int64_t)k * CRS + c0 + j));
+            float* t = tile + r * pitch + j;
+            t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+        }
+        __syncthreads();
+        float4* o = reinterpret_cast<float4*>(out + ((int64_t)kb * CRS + c0) * bko);
+        const int b4 = bko >> 2;
+        for (int e = threadIdx.x; e < ncol * b4; e += blockDim.x) {
+            const int j = e / b4, r = (e - j * b4) * 4;
+            const float* t = tile + r * pitch + j;
+            o[e] = make_float4(t[0], t[pitch], t[2 * pitch], t[3 * pitch]);
+        }
+    } else {
+        for (int e = threadIdx.x; e < bko * cw; e += blockDim.x) {
+            const int r = e / cw, j = e - r * cw;
+            const int k = kb * bko + r;
+            tile[r * pitch + j] = (k < K && j < ncol) ? __ldg(ker + (int64_t)k * CRS + c0 + j) : 0.0f;
+        }
+        __syncthreads();
+        float* o = out + ((int64_t)kb * CRS + c0) * bko;
+        for (int e = threadIdx.x; e < ncol * bko; e += blockDim.x) {
+            const int j = e / bko, r = e - j * bko;
+            o[e] = tile[r * pitch + j];
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;");   // at the end of each CTA (see pack_ker_simt)
+}
+
+// (the r01-r02b per-element form, kept for the A/B: CONV_SIMT_PACK_GATHER=1)
 __global__ void __launch_bounds__(256) pack_ker_simt(const float* __restrict__ ker, float* __restrict__ out,
                                                      int K, int C, int RS, int bko, int64_t total) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -864,7 +916,23 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
     const int64_t total = (int64_t)((pb.K + p.bko - 1) / p.bko) * p.bko * pb.C * p.RS;
     const int pblocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
     if (ev) cudaEventRecord(ev[0], st);
-    pack_ker_simt<<<pblocks, 256, 0, st>>>(ker, kerp, pb.K, pb.C, p.RS, p.bko, total);
+    // the tiled transpose, except for small packs with C*R*S % 4 != 0 (its
+    // scalar form measured r02c, profiles/r02c/pack/: Y0 8.4 vs 7.1 us, R1
+    // 8.7 vs 6.9 for the gather; with 16-B units it is at least as fast on
+    // every Table-1 layer, M9 66.8 -> 21.2 us, Y23 183 -> 55, batched 12.3 ->
+    // 8.0)
+    static const int gather_env = getenv("CONV_SIMT_PACK_GATHER") ? atoi(getenv("CONV_SIMT_PACK_GATHER")) : -1;
+    const bool gather = gather_env == 1 ||
+                        (gather_env != 0 && (pb.C * p.RS) % 4 != 0 && total < (int64_t)1 << 18);
+    if (gather || p.bko > 1024) {
+        pack_ker_simt<<<pblocks, 256, 0, st>>>(ker, kerp, pb.K, pb.C, p.RS, p.bko, total);
+    } else {
+        const int crs = pb.C * p.RS;
+        const int cw = 1024 / p.bko;                         // bko is a multiple of 4 up to 64
+        const int nchunk = (crs + cw - 1) / cw;
+        const int64_t nblk = (int64_t)((pb.K + p.bko - 1) / p.bko) * nchunk;
+        pack_ker_simt_tiled<<<(unsigned)nblk, 256, 0, st>>>(ker, kerp, pb.K, crs, p.bko, cw, nchunk);
+    }
     if (ev) cudaEventRecord(ev[1], st);
 
     const int n_ntiles = (pb.N + t.tn - 1) / t.tn;

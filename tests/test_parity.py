@@ -1213,10 +1213,10 @@ def test_guard_bands_no_out_of_bounds_access(case):
 
 
 def test_fp32_tc_compact_layout_subprocess():
-    """The opt-in compact FP32_TC workspace (CONV_SPLIT_COMPACT=1: the 3 bf16
+    """The compact FP32_TC workspace (default; CONV_SPLIT_COMPACT=1: the 3 bf16
     pieces once, pair blocks mapped to pieces in the producer) gives the same
     result bit for bit as the default 6-pair layout (same products, same
-    k order), in a fresh process (the knob is read once)."""
+    k order) as the 6-pair layout (=0), in fresh processes (the knob is read once)."""
     import os
     import subprocess
     import sys
@@ -1243,3 +1243,39 @@ print(p.workspace_bytes)
             res[v] = (np.load(f), int(r.stdout.strip().splitlines()[-1]))
     assert res["1"][1] < res["0"][1]                      # the compact workspace is smaller
     assert np.array_equal(res["0"][0], res["1"][0])
+
+
+def test_simt_ker_pack_forms_subprocess():
+    """The FP32 SIMT Ker pack (KCRS -> [K/bko][C][R][S][bko], a permutation):
+    the tiled transpose (CONV_SIMT_PACK_GATHER=0, 16-B units when C*R*S % 4
+    == 0, scalar otherwise) and the per-element gather (=1) give bit-identical
+    convolutions, on ragged k tiles and odd C*R*S, in fresh processes (the
+    knob is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = """
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2101_09808_b200 import conv
+from paper_2101_09808_b200.inputs import Shape, make_inputs
+outs = []
+for sh in (Shape(N=2, K=44, C=13, H=9, W=14, R=3, S=3), Shape(N=1, K=70, C=12, H=6, W=7, R=3, S=3),
+           Shape(N=1, K=36, C=40, H=5, W=9, R=1, S=1)):
+    inp, ker = make_inputs(sh, seed=77)
+    p = conv.ConvPlan(*sh.as_tuple(), path="fp32_simt")
+    outs.append(p.run(inp.cuda(), ker.cuda()).cpu().numpy())
+np.savez(sys.argv[1], *outs)
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+    res = {}
+    with tempfile.TemporaryDirectory() as d:
+        for v in ("0", "1"):
+            f = os.path.join(d, f"o{v}.npz")
+            r = subprocess.run([sys.executable, "-c", code, f], capture_output=True, text=True, timeout=300,
+                               env={**os.environ, "CONV_SIMT_PACK_GATHER": v})
+            assert r.returncode == 0, r.stderr[-2000:]
+            z = np.load(f)
+            res[v] = [z[k] for k in sorted(z.files)]
+    for a, b in zip(res["0"], res["1"]):
+        assert np.array_equal(a, b)
