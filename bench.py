@@ -373,6 +373,9 @@ def path_record(args, world, full, spec, res, engine, peaks, peak_src):
         },
         "clocks": res["clocks"],
         "kernels_per_step": res["nk"],
+        # FP32 SIMT flat tiles: the remainder grid is a launch of its own, timed together with
+        # the main grid it runs beside (no event between the two)
+        "launches_per_step": res["nk"] + (1 if res["desc"]["tile"].get("rem") else 0),
         "launch": res["launch"],
     }
 
@@ -414,11 +417,12 @@ def build_line(args, world, full, spec, paths, results, e2e_ms, g_ms, p10, engin
             "shard": {"dim": spec.dim, "world": world, "per_rank": f"{spec.dim}={spec.size}",
                       "per_rank_shape": list(sh.as_tuple())},
             "kernels_per_step": head["kernels_per_step"],
+            "launches_per_step": head["launches_per_step"],
             "launch": head["launch"],
             "timer": engine.timer,
         },
         "roofline": head["roofline"],
-        "gpu_launches": head["kernels_per_step"] * args.steps,
+        "gpu_launches": head["launches_per_step"] * args.steps,
         "clocks": head["clocks"],
     }
     if e2e_ms is not None:

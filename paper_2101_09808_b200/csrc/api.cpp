@@ -428,7 +428,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             std::string key = kv.substr(0, eq);
             char* end = nullptr;
             long v = strtol(kv.c_str() + eq + 1, &end, 10);
-            const long vmin = (key == "fuse" || key == "pre_c" || key == "expand" || key == "halo" || key == "flat") ? 0 : 1;
+            const long vmin = (key == "fuse" || key == "pre_c" || key == "expand" || key == "halo" || key == "flat" || key == "rem") ? 0 : 1;
             if (!end || *end || v < vmin || v > 4096) return fail(CONV_ERR_INVALID_ARGUMENT, "bad value in '%s'", kv.c_str());
             if (key == "bn") ft.bn = (int)v;
             else if (key == "stages") ft.stages = (int)v;
@@ -449,6 +449,7 @@ extern "C" conv_status conv_plan_set_tile(conv_plan* p, const char* spec) {
             else if (key == "bc") { fs.bc = (int)v; mask |= 64; }
             else if (key == "ver") { fs.ver = (int)v; mask |= 128; }
             else if (key == "flat") { fs.flat = v ? 1 : 0; mask |= 512; }
+            else if (key == "rem") { fs.rem = v ? 1 : 0; mask |= 1024; }
             else return fail(CONV_ERR_INVALID_ARGUMENT, "unknown tile key '%s'", key.c_str());
         }
         if (ft.bn && ft.bn != 32 && ft.bn != 64 && ft.bn != 128 && ft.bn != 192 && ft.bn != 256)
@@ -514,9 +515,10 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
         // staging: "tma" (one 4-D TMA box + a bulk Ker copy per chunk) or
         // "cp.async" (per-thread copies; v1, and v2 where Win % 4 != 0)
         const bool tma = p->simt.ver == 2 && simt2_layout(pb, p->simt).tma;
-        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"splits\":%d,\"flat\":%d,\"threads\":%d,\"staging\":\"%s\"}",
+        snprintf(t, sizeof t, "{\"ver\":%d,\"tk\":%d,\"tw\":%d,\"kg\":%d,\"pw\":%d,\"tn\":%d,\"th\":%d,\"bc\":%d,\"splits\":%d,\"flat\":%d,\"rem\":%d,\"threads\":%d,\"staging\":\"%s\"}",
                  p->simt.ver, p->simt.tk, p->simt.tw, p->simt.kg, p->simt.pw, p->simt.tn, p->simt.th, p->simt.bc,
-                 p->simt.splits, p->simt.flat, 32 * p->simt.kg * p->simt.pw, tma ? "tma" : "cp.async");
+                 p->simt.splits, p->simt.flat, tma ? simt_rem_tiles(pb, p->simt, p->dev.sms) : 0,
+                 32 * p->simt.kg * p->simt.pw, tma ? "tma" : "cp.async");
     } else {
         snprintf(t, sizeof t, "{\"bm\":%d,\"bn\":%d,\"cg\":%d,\"kbs\":%d,\"stages\":%d,\"splits\":%d,\"expand\":%d,\"split\":%d,\"halo\":%d,\"fuse\":%d,\"tnb\":%d,\"pre_c\":%d,\"bkc\":%d,\"cp\":%d,\"swizzle\":%d}",
                  128 * p->tc.cg, p->tc.bn, p->tc.cg, p->tc.kbs, p->tc.stages, p->tc.splits, p->expand ? 1 : 0, p->split, p->tc.halo, p->tc.fuse, p->tc.fuse ? p->tc.tnb : 0,
@@ -571,7 +573,7 @@ static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0
     std::string err;
     cudaError_t e;
     if (p->path == CONV_PATH_FP32_SIMT) {
-        e = simt_run(sub, p->simt, in, ker, out, ws, st, evp, err);
+        e = simt_run(sub, p->simt, in, ker, out, ws, st, evp, err, p->dev.sms);
     } else {
         uint8_t* wsb = static_cast<uint8_t*>(ws);
         const size_t per_img = p->tcl.in_ws_bytes / (size_t)p->pb.N;

@@ -491,7 +491,10 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     if (per_sm < 1) { r.model_us = 1e30; return r; }
     // CTAs land round-robin on the SMs: the busiest SM runs ceil(tiles/SMs)
     // of them, `conc` at a time.
-    const long per_sm_total = (r.tiles + dev.sms - 1) / dev.sms;
+    // (remainder launch, simt_rem_tiles: the busiest SM runs one CTA less and
+    // one remainder warp, 1 / kg of a CTA's issue, beside its resident CTAs)
+    const int rem = simt_rem_tiles(pb, t, dev.sms);
+    const long per_sm_total = (r.tiles + dev.sms - 1) / dev.sms - (rem > 0 ? 1 : 0);
     const long conc = std::min<long>(per_sm, per_sm_total);
     const long waves = (per_sm_total + conc - 1) / conc;
     r.ctas = std::min<long>(r.tiles, (long)per_sm * dev.sms);
@@ -566,7 +569,8 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     // 698 us); a finished CTA's slot is refilled at once, so the last wave
     // costs its share.  (CONV_SIMT_WHOLE_WAVES=1: the r01b whole-wave count.)
     static const bool whole_waves = getenv("CONV_SIMT_WHOLE_WAVES") != nullptr;
-    const double wv = (t.ver == 2 && !whole_waves) ? (double)per_sm_total / (double)conc : (double)waves;
+    const double wv = ((t.ver == 2 && !whole_waves) ? (double)per_sm_total / (double)conc : (double)waves) +
+                      (rem > 0 ? 1.0 / (t.kg * (double)conc) : 0.0);
     r.issue_cyc = wv * chunks * issue_cyc;
     r.t_comp_us = wv * chunks * chunk_cyc / clk * 1e6;
     // L2 -> SMEM: per CTA, every c-chunk loads the In halo tile and Ker slab
@@ -590,7 +594,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     const int bcs[4] = {2, 4, 8, 16};   // 2: flat tiles (or forced) only
     const int tn_max = std::min(pb.N, 16);
     // v2 first when it can run and nothing is forced; v1 only if no v2 tile fits
-    const bool tile_forced = forced && (forced_mask & ~256u);   // a tile key other than splits
+    const bool tile_forced = forced && (forced_mask & ~(256u | 1024u));   // a tile key other than splits / rem
     const bool v2_first = simt_v2_ok(pb) && !tile_forced;
     const int vers[2] = {v2_first ? 2 : 1, v2_first ? 1 : 2};
     for (int ver : vers) {
@@ -626,6 +630,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         // the model, blind to the per-chunk waits, ranked the other way)
         if (bc == 2 && !(forced && (forced_mask & 64))) continue;
         if (t.flat && t.kg * t.pw < 4 && !tile_forced) continue;
+        if (forced && (forced_mask & 1024)) t.rem = forced->rem;
         if (forced) {
             if ((forced_mask & 512) && t.flat != forced->flat) continue;
             if ((forced_mask & 1) && t.tk != forced->tk) continue;

@@ -34,7 +34,7 @@ ModelResult model_tc(const Problem& pb, const Device& dev, bool bf16, const TcTi
 bool select_tc(const Problem& pb, const Device& dev, bool bf16, TcTile& best, ModelResult& r, const TcForce& f,
                std::string& why);
 ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t);
-// forced_mask bits: 1 tk, 2 tw, 4 kg, 8 pw, 16 tn, 32 th, 64 bc, 128 ver, 256 splits
+// forced_mask bits: 1 tk, 2 tw, 4 kg, 8 pw, 16 tn, 32 th, 64 bc, 128 ver, 256 splits, 512 flat, 1024 rem
 bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResult& r,
                  const SimtTile* forced, unsigned forced_mask, std::string& why);
 

@@ -349,6 +349,15 @@ struct Simt2Params {
     int flat;         // flat row mode (SimtTile::flat): grid x = slot tile * ktiles + k tile, slot tile
                       //    = 32*pw consecutive (image, row) slots; the box starts at the slot tile's
                       //    first image, smem [c][img][rows_box][pitch] (istride = rows_box * pitch)
+    int solo;         // remainder launch (simt_rem_tiles; flat TMA tiles, TK = 1 instance): > 0 = CTAs per
+                      //    (slot tile, k tile); CTA blockIdx is channels 4 * (blockIdx % solo) + warp of k tile
+                      //    (blockIdx / solo) % ktiles of slot tile tile0 + blockIdx / (solo * ktiles)
+    int tile0;        // remainder launch: first slot tile
+    int trigger;      // griddepcontrol.launch_dependents once the packed Ker is complete
+    int endwait;      // griddepcontrol.wait at the CTA's end (so that this grid's end implies the previous one's)
+    int nowait;       // main grid launched behind the remainder grid: no griddepcontrol.wait (that would
+                      //    wait for the remainder grid's end; the packed Ker was complete before the
+                      //    remainder CTAs triggered this launch)
 };
 
 static constexpr int kSimt2Stages = 3;     // v2 shared-memory ring depth (cp.async layout; TMA default)
@@ -383,11 +392,19 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int kgi = warp % p.kg;
+    int kgi = warp % p.kg;
     const int pwi = warp / p.kg;
 
-    const int bx = gridDim.y > 1 ? (int)blockIdx.x : (int)blockIdx.x / p.ktiles;
-    const int kb = gridDim.y > 1 ? (int)blockIdx.y : (int)blockIdx.x - bx * p.ktiles;
+    int bx = gridDim.y > 1 ? (int)blockIdx.x : (int)blockIdx.x / p.ktiles;
+    int kb = gridDim.y > 1 ? (int)blockIdx.y : (int)blockIdx.x - bx * p.ktiles;
+    if (TMA && p.solo) {
+        // remainder launch (Simt2Params::solo): 4 warps = 4 of the k tile's channels
+        const int b = (int)blockIdx.x / p.solo;
+        kgi = ((int)blockIdx.x - b * p.solo) * 4 + warp;
+        bx = b / p.ktiles;
+        kb = b - bx * p.ktiles;
+        bx += p.tile0;
+    }
     const int k0 = kb * p.bko;
     const int q = pwi * 32 + lane;
     // n0 / h0: the In box origin (image, row); n_out / h_out: this thread's output row
@@ -434,11 +451,15 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     // instruction does two FMAs (kernel pair x broadcast input value), so the
     // FMA pipe stays busy with half the issue slots (ncu r02: the FFMA form
     // was issue-bound -- 85 % FFMA, 15 % addressing/LDS, 83 % issue slots busy)
-    unsigned long long acc2[TK / 2][TW];
+    // (TK = 1, the remainder launch's instance: plain fmaf on acc1)
+    unsigned long long acc2[TK / 2 > 0 ? TK / 2 : 1][TW];
+    float acc1[TW];
 #pragma unroll
     for (int i = 0; i < TK / 2; ++i)
 #pragma unroll
         for (int j = 0; j < TW; ++j) acc2[i][j] = 0ull;
+#pragma unroll
+    for (int j = 0; j < TW; ++j) acc1[j] = 0.0f;
 #else
     float acc[TK][TW];
 #pragma unroll
@@ -545,7 +566,8 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
     // slower (Y2, Y8) -- so the shuffle halo is compiled for TK = 8 only
     constexpr bool kShflHalo = TW == 4 && KS == 3 && (CONV_SIMT_SHFL == 1 || (CONV_SIMT_SHFL == 2 && TK == 8));
     const bool own_halo = g == p.groups - 1 || lane == 31;
-    asm volatile("griddepcontrol.wait;" ::: "memory");   // packed Ker written by the previous grid
+    if (!(TMA && p.nowait)) asm volatile("griddepcontrol.wait;" ::: "memory");   // packed Ker written by the previous grid
+    if (TMA && p.trigger) asm volatile("griddepcontrol.launch_dependents;");     // the other grid may start (Ker complete)
     // split-C (separate instances, so the plain loop keeps its exact code --
     // the runtime range measured 3.5 % slower on the batched layer): this
     // CTA's channel chunks [c_beg, c_end) and its partial-output slab
@@ -625,9 +647,14 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
 #pragma unroll
                 for (int s = 0; s < KS; ++s) {
 #if CONV_SIMT_FFMA2
-                    unsigned long long kv2[TK / 2];
+                    if constexpr (TK == 1) {
+                        const float kv1 = kp[(r * KS + s) * p.bko];
 #pragma unroll
-                    for (int i = 0; i < TK; i += 4) {
+                        for (int j = 0; j < TW; ++j) acc1[j] = fmaf(kv1, win[j + s], acc1[j]);
+                    } else {
+                    unsigned long long kv2[TK / 2 > 0 ? TK / 2 : 1];
+#pragma unroll
+                    for (int i = 0; i + 3 < TK; i += 4) {
                         const float4 k4 = *reinterpret_cast<const float4*>(kp + (r * KS + s) * p.bko + i);
                         asm("mov.b64 %0, {%1, %2};" : "=l"(kv2[i / 2]) : "f"(k4.x), "f"(k4.y));
                         asm("mov.b64 %0, {%1, %2};" : "=l"(kv2[i / 2 + 1]) : "f"(k4.z), "f"(k4.w));
@@ -640,10 +667,12 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
                         for (int i = 0; i < TK / 2; ++i)
                             asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[i][j]) : "l"(kv2[i]), "l"(w2));
                     }
+                    }
 #else
                     float kv[TK];
+                    if constexpr (TK == 1) kv[0] = kp[(r * KS + s) * p.bko];
 #pragma unroll
-                    for (int i = 0; i < TK; i += 4) {
+                    for (int i = 0; i + 3 < TK; i += 4) {
                         const float4 k4 = *reinterpret_cast<const float4*>(kp + (r * KS + s) * p.bko + i);
                         kv[i] = k4.x; kv[i + 1] = k4.y; kv[i + 2] = k4.z; kv[i + 3] = k4.w;
                     }
@@ -661,6 +690,7 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
         if (++buf == S) { buf = 0; phase ^= 1u; }
     }
 
+    if (TMA && p.endwait) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (!valid) return;
 #if CONV_SIMT_FFMA2
     float acc[TK][TW];
@@ -671,6 +701,10 @@ __global__ void __launch_bounds__(Simt2Threads<TK, TW>::value) conv_direct_simt2
             acc[2 * i][j] = __uint_as_float((uint32_t)acc2[i][j]);
             acc[2 * i + 1][j] = __uint_as_float((uint32_t)(acc2[i][j] >> 32));
         }
+    if constexpr (TK == 1) {
+#pragma unroll
+        for (int j = 0; j < TW; ++j) acc[0][j] = acc1[j];
+    }
 #endif
 #pragma unroll
     for (int i = 0; i < TK; ++i) {
@@ -797,6 +831,43 @@ Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
     return L;
 }
 
+// Remainder launch of a flat tile (internal.h).  The kernel's time goes with
+// the CTAs per SM, k = ceil(CTAs / SMs) (T = 35 + 87 k us on the batched
+// layer); when (k - 1) * SMs CTAs hold all but `rem` slot tiles, those run
+// as rem * ktiles * kg one-warp CTAs -- at most one per SM, and small enough
+// (2-channel chunks) to fit beside the main grid's resident CTAs -- so the
+// busiest SM carries k - 1 CTAs and one warp instead of k CTAs (r02d,
+// batched layer: 1792 CTAs = 12.1 per SM -> 1776 + 64 warps).
+SimtTile simt_rem_tile(const SimtTile& t) {
+    SimtTile ts = t;
+    ts.bc = std::min(t.bc, 2);
+    ts.kg = t.kg * t.tk;      // same k tile (bko channels) and packed Ker, one channel per k group
+    ts.tk = 1;
+    return ts;
+}
+
+int simt_rem_tiles(const Problem& pb, const SimtTile& t, int sms) {
+    static const bool off = getenv("CONV_SIMT_NO_REM") != nullptr;   // A/B
+    if (off || !t.flat || !t.rem || t.ver != 2 || t.splits > 1 || t.pw != 1 || t.kg < 2 || sms < 1) return 0;
+    const int64_t ktiles = (pb.K + (int64_t)t.kg * t.tk - 1) / ((int64_t)t.kg * t.tk);
+    const int64_t tiles = ((int64_t)pb.N * pb.H + 31) / 32;           // slot tiles (pw = 1)
+    const int64_t ctas = tiles * ktiles;
+    const int64_t k = (ctas + sms - 1) / sms;
+    if (k < 2) return 0;
+    const int64_t main_tiles = (k - 1) * sms / ktiles;
+    const int64_t rem = tiles - main_tiles;
+    if (rem < 1 || main_tiles < 1 || rem * ktiles * (t.kg * t.tk / 4) > sms) return 0;
+    // shared memory: the main grid's resident CTAs + one remainder CTA per SM
+    const SimtTile ts = simt_rem_tile(t);
+    const size_t sm_main = simt_smem_bytes(pb, t), sm_rem = simt_smem_bytes(pb, ts);
+    if (sm_main == SIZE_MAX || sm_rem == SIZE_MAX || !simt2_layout(pb, ts).tma) return 0;
+    const int64_t threads = 32 * t.kg;
+    const int64_t per_sm = std::min<int64_t>({(int64_t)(228 * 1024 / (sm_main + 1024)), (2048 - 128) / threads,
+                                              (65536 - 64 * 128) / (128 * threads), k - 1});
+    if (per_sm < 1 || per_sm * (sm_main + 1024) + (sm_rem + 1024) > (size_t)228 * 1024) return 0;
+    return (int)rem;
+}
+
 size_t simt_smem_bytes(const Problem& pb, const SimtTile& t) {
     if (t.ver == 2) {
         const Simt2Layout L = simt2_layout(pb, t);
@@ -851,6 +922,9 @@ static cudaError_t dispatch_simt2(const SimtTile& t, int R, int S, bool tma, con
     SIMT2_CASE(4, 4, 0, 3) SIMT2_CASE(4, 8, 0, 3) SIMT2_CASE(8, 4, 0, 3) SIMT2_CASE(8, 8, 0, 3)
     SIMT2_CASE(4, 14, 3, 3) SIMT2_CASE(4, 7, 3, 3) SIMT2_CASE(4, 14, 1, 1) SIMT2_CASE(4, 7, 1, 1)
     SIMT2_CASE(4, 14, 0, 3) SIMT2_CASE(4, 7, 0, 3) SIMT2_CASE(4, 14, 0, 1) SIMT2_CASE(4, 7, 0, 1)
+    // the remainder launch's instance (simt_rem_tile: flat tiles exist for W = 14, R = S = 3 only)
+    if (t.tk == 1 && t.tw == 14 && R == 3 && S == 3 && tma)
+        return launch_simt2_t<1, 14, 3, 3, true>(in, kerp, out, p, tmap, grid, threads, smem, st);
 #undef SIMT2_CASE
     return cudaErrorInvalidValue;
 }
@@ -889,7 +963,7 @@ size_t simt_ws_bytes(const Problem& pb, const SimtTile& t) {
 }
 
 cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, const float* ker,
-                     float* out, void* ws, cudaStream_t st, cudaEvent_t* ev, std::string& err) {
+                     float* out, void* ws, cudaStream_t st, cudaEvent_t* ev, std::string& err, int sms) {
     SimtParams p;
     p.N = pb.N; p.K = pb.K; p.C = pb.C; p.H = pb.H; p.W = pb.W; p.R = pb.R; p.S = pb.S; p.U = pb.U; p.D = pb.D;
     p.Hin = (int)pb.Hin(); p.Win = (int)pb.Win(); p.HW = pb.H * pb.W; p.RS = pb.R * pb.S;
@@ -973,25 +1047,61 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
         else q.ktiles = 1;
         CUtensorMap tmap;
         memset(&tmap, 0, sizeof(tmap));
-        if (L.tma) {
-            // In NCHW as {Win, Hin, C, N}; box {pitch, rows_in, bc, tn}: columns
-            // >= Win (the pitch padding), rows >= Hin, channels >= C and
-            // images >= N are zero-filled
-            if (!driver_init(err)) return cudaErrorInvalidValue;
-            // (flat: {Win, Hin, N, C}, box {pitch, rows_box, images, bc} -- the
-            // image dim inside the channel dim, so a channel's images are
-            // consecutive row blocks in smem)
+        // In NCHW as {Win, Hin, C, N}; box {pitch, rows_in, bc, tn}: columns
+        // >= Win (the pitch padding), rows >= Hin, channels >= C and
+        // images >= N are zero-filled
+        // (flat: {Win, Hin, N, C}, box {pitch, rows_box, images, bc} -- the
+        // image dim inside the channel dim, so a channel's images are
+        // consecutive row blocks in smem)
+        auto encode = [&](CUtensorMap* tm, const Simt2Layout& Lx, int bc) -> bool {
+            if (!driver_init(err)) return false;
             const cuuint64_t plane_b = (cuuint64_t)q.Hin * q.Win * 4, image_b = (cuuint64_t)pb.C * plane_b;
             cuuint64_t dims[4] = {(cuuint64_t)q.Win, (cuuint64_t)q.Hin, (cuuint64_t)(t.flat ? pb.N : pb.C),
                                   (cuuint64_t)(t.flat ? pb.C : pb.N)};
             cuuint64_t strides[3] = {(cuuint64_t)q.Win * 4, t.flat ? image_b : plane_b, t.flat ? plane_b : image_b};
-            cuuint32_t box[4] = {(cuuint32_t)q.pitch, (cuuint32_t)L.rows_box, (cuuint32_t)(t.flat ? box_imgs : t.bc),
-                                 (cuuint32_t)(t.flat ? t.bc : t.tn)};
+            cuuint32_t box[4] = {(cuuint32_t)Lx.pitch, (cuuint32_t)Lx.rows_box, (cuuint32_t)(t.flat ? box_imgs : bc),
+                                 (cuuint32_t)(t.flat ? bc : t.tn)};
             cuuint32_t estr[4] = {1, 1, 1, 1};
-            CUresult r = g_encode_tiled(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in), dims, strides,
+            CUresult r = g_encode_tiled(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in), dims, strides,
                                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeTiled (SIMT In) failed (" + std::to_string((int)r) + ")"; return cudaErrorInvalidValue; }
+            if (r != CUDA_SUCCESS) { err = "cuTensorMapEncodeTiled (SIMT In) failed (" + std::to_string((int)r) + ")"; return false; }
+            return true;
+        };
+        if (L.tma && !encode(&tmap, L, t.bc)) return cudaErrorInvalidValue;
+        q.solo = 0; q.tile0 = 0; q.nowait = 0; q.trigger = 0; q.endwait = 0;
+        // Remainder launch (simt_rem_tiles): the last `rem` slot tiles run as
+        // 4-warp CTAs of the TK = 1 instance with 2-channel chunks -- each
+        // warp one output channel of the CTA's 4, so the four SMSPs of the SM
+        // get a quarter of a main warp's FMAs each -- small enough to sit
+        // beside the main grid's resident CTAs.  Launched first; the main
+        // grid follows as their programmatic dependent (released once they
+        // have seen the packed Ker complete), does not wait for their end
+        // before it starts, and waits for it at the end of each CTA, so that
+        // the main grid's end implies the remainder grid's.  Per output the
+        // arithmetic is the main tile's (same c, r, s order of fmaf).
+        const int rem = (L.tma && !grid2d && zsplits == 1) ? simt_rem_tiles(pb, t, sms) : 0;
+        if (rem > 0) {
+            const SimtTile ts = simt_rem_tile(t);
+            const Simt2Layout Ls = simt2_layout(pb, ts);
+            Simt2Params qs = q;
+            qs.bc = ts.bc; qs.kg = ts.kg;
+            qs.pitch = Ls.pitch; qs.istride = Ls.istride; qs.cstride = Ls.cstride; qs.plane = Ls.cstride;
+            qs.in_stage = Ls.in_stage; qs.lpi = Ls.lpi; qs.stages = Ls.stages;
+            qs.nchunks = (pb.C + ts.bc - 1) / ts.bc;
+            qs.cper = qs.nchunks;
+            qs.tx_in = (uint32_t)((size_t)box_imgs * ts.bc * Ls.rows_box * qs.pitch * sizeof(float));
+            qs.solo = t.kg * t.tk / 4;                 // remainder CTAs per (slot tile, k tile): 4 channels each
+            qs.tile0 = (int)grid.x / q.ktiles - rem;
+            qs.trigger = 1;
+            CUtensorMap tmap_s;
+            memset(&tmap_s, 0, sizeof(tmap_s));
+            if (!encode(&tmap_s, Ls, ts.bc)) return cudaErrorInvalidValue;
+            e = dispatch_simt2(ts, pb.R, pb.S, true, in, kerp, kout, qs, tmap_s, dim3((unsigned)(rem * q.ktiles * qs.solo)),
+                               128, simt_smem_bytes(pb, ts), st);
+            if (e != cudaSuccess) { err = std::string("SIMT remainder launch failed: ") + cudaGetErrorString(e); return e; }
+            grid.x -= (unsigned)(rem * q.ktiles);
+            q.nowait = 1; q.endwait = 1;
         }
         e = dispatch_simt2(t, pb.R, pb.S, L.tma, in, kerp, kout, q, tmap, grid, threads, smem, st);
     } else {

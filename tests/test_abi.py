@@ -144,10 +144,38 @@ def _offline(shape, path, tile=None):
     return conv.ConvPlan(*shape.as_tuple(), path=path, tile=tile, offline_device=conv.B200)
 
 
+def test_simt_remainder_launch_plan(lib):
+    """Host logic of the flat tile's remainder launch (simt_rem_tiles): on 148
+    SMs the batched layer's 112 slot tiles x 16 k tiles = 1792 CTAs are 12.1
+    per SM, so 111 tiles (1776 CTAs = 12 per SM) stay in the main grid and one
+    runs as 64 one-warp CTAs; 253 images (111 slot tiles) need none; the tile
+    key rem=0 turns it off; a remainder that would need more than one warp
+    per SM is not taken."""
+    import dataclasses
+    from paper_2101_09808_b200.inputs import CONFIGS, Shape
+    flat = "flat=1,tk=4,kg=4,pw=1,bc=4"
+    sh = CONFIGS["batched"]
+    d = _offline(sh, "fp32_simt").describe()
+    assert d["tile"]["flat"] == 1 and d["tile"]["rem"] == 1, d["tile"]
+    assert _offline(sh, "fp32_simt", flat + ",rem=0").describe()["tile"]["rem"] == 0
+    assert _offline(dataclasses.replace(sh, N=253), "fp32_simt", flat).describe()["tile"]["rem"] == 0
+    # 128 images: 56 slot tiles x 16 = 896 CTAs, k = 7, 55 main tiles (880 <= 888), 1 remainder tile
+    assert _offline(dataclasses.replace(sh, N=128), "fp32_simt", flat).describe()["tile"]["rem"] == 1
+    # 240 images: 105 tiles, k = 12, 101 main tiles -> 4 remainder tiles = 256 warps > 148: not taken
+    assert _offline(dataclasses.replace(sh, N=240), "fp32_simt", flat).describe()["tile"]["rem"] == 0
+    # fewer CTAs than SMs: nothing to take off
+    assert _offline(Shape(N=8, K=32, C=8, H=14, W=14, R=3, S=3), "fp32_simt", flat).describe()["tile"]["rem"] == 0
+    # the modeled time with the remainder launch is below the one without
+    with_rem = _offline(sh, "fp32_simt", flat).describe()["model"]["model_us"]
+    without = _offline(sh, "fp32_simt", flat + ",rem=0").describe()["model"]["model_us"]
+    assert with_rem < without
+
+
 @pytest.mark.parametrize("path", ["fp32_simt", "tf32", "bf16"])
 def test_selector_respects_capacity(lib, path):
     """Every emitted tile satisfies the per-level capacity constraints (Eq. 4
     per level): shared memory per CTA <= opt-in, TMEM 2*BN <= 512."""
+    import dataclasses
     from paper_2101_09808_b200.inputs import CONFIGS, Shape
     shapes = list(CONFIGS.values()) + [Shape(1, 5, 3, 7, 9, 3, 3), Shape(2, 300, 700, 9, 10, 1, 1),
                                        Shape(1, 64, 4096, 3, 3, 3, 3), Shape(1, 8, 8, 2, 3000, 1, 5)]
@@ -414,16 +442,19 @@ def test_simt_staging_choice_offline(lib):
     """FP32 SIMT v2 staging (simt2_layout): the TMA box + bulk Ker copy
     wherever In rows are 16-B multiples (Win % 4 == 0) and the box fits TMA's
     256-element dims; the per-thread cp.async layout otherwise, and always for
-    v1 (strided) tiles.  The batched layer's plan is the r02c headline tile
+    v1 (strided) tiles.  The batched layer's plan is the r02d headline tile
     (flat row mode: 32 consecutive (image, row) slots per CTA, boxes of 4
-    images); its 128-image shard keeps the per-image r02b tile."""
+    images, 8 k groups, the last slot tile as the remainder launch); its
+    128- and 64-image shards take flat tiles with a remainder launch too."""
     import dataclasses
     from paper_2101_09808_b200.inputs import CONFIGS, TABLE1
     d = _offline(CONFIGS["batched"], "fp32_simt").describe()["tile"]
-    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["tn"], d["th"], d["bc"], d["flat"], d["staging"]) == \
-        (2, 4, 14, 4, 4, 14, 4, 1, "tma")
+    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["tn"], d["th"], d["bc"], d["flat"], d["rem"], d["staging"]) == \
+        (2, 4, 14, 8, 4, 14, 4, 1, 1, "tma")
     d = _offline(dataclasses.replace(CONFIGS["batched"], N=128), "fp32_simt").describe()["tile"]
-    assert (d["ver"], d["tk"], d["tw"], d["tn"], d["th"], d["flat"], d["staging"]) == (2, 4, 14, 2, 14, 0, "tma")
+    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["flat"], d["rem"], d["staging"]) == (2, 4, 14, 8, 14, 1, 1, "tma")
+    d = _offline(dataclasses.replace(CONFIGS["batched"], N=64), "fp32_simt").describe()["tile"]
+    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["flat"], d["rem"], d["staging"]) == (2, 4, 14, 4, 14, 1, 1, "tma")
     for name in ("r2", "det", "tiny"):                       # Win = 58, 138, 10
         assert _offline(CONFIGS[name], "fp32_simt").describe()["tile"]["staging"] == "cp.async"
     sh = TABLE1["Y2"]                                        # Win = 272: a row wider than a TMA box

@@ -501,6 +501,47 @@ def test_simt_flat_row_mode(shape, tile):
     assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
 
 
+# flat tiles whose last slot tiles run as the remainder launch (simt_rem_tiles):
+# ceil(CTAs / 148) = k with (k - 1) * 148 CTAs holding all but `rem` slot tiles
+SIMT_REM_CASES = [
+    # 75 slot tiles x 2 k tiles = 150 CTAs: 74 main tiles + 1 remainder tile (8 one-warp CTAs), ragged last slot tile
+    (Shape(N=171, K=32, C=8, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4", 1),
+    # 2 k tiles of 8 channels (kg = 2), ragged K and C: 76 tiles -> 74 + 2 remainder tiles, odd channel count in 2-channel chunks
+    (Shape(N=173, K=14, C=7, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=2,pw=1,bc=4", 2),
+    # H = 9 rows per image (slot tiles cross image boundaries at other places)
+    (Shape(N=267, K=32, C=6, H=9, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4", 2),
+    # 3 rounds: 223 tiles x 2 = 446 CTAs, k = 4 -> 222 main tiles
+    (Shape(N=509, K=32, C=4, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=2", 1),
+]
+
+
+@pytest.mark.parametrize("shape,tile,rem", SIMT_REM_CASES, ids=lambda x: x if isinstance(x, str) else str(x) if isinstance(x, int) else "x".join(map(str, x.as_tuple())))
+def test_simt_remainder_launch(shape, tile, rem):
+    """The remainder launch of a flat tile (the last slot tiles as one-warp
+    CTAs beside the main grid): bit-identical to the same tile without it
+    (rem=0: every output is the same thread-level FMA sequence), 1e-5 against
+    the double oracle, integer twin exact, twice (the second run re-packs Ker
+    while nothing of the first is in flight)."""
+    inp, ker = make_inputs(shape, seed=51)
+    plan = conv.ConvPlan(*shape.as_tuple(), path="fp32_simt", tile=tile)
+    t = plan.describe()["tile"]
+    assert t["flat"] == 1 and t["rem"] == rem, t
+    plain = conv.ConvPlan(*shape.as_tuple(), path="fp32_simt", tile=tile + ",rem=0")
+    assert plain.describe()["tile"]["rem"] == 0
+    di, dk = inp.cuda(), ker.cuda()
+    ref = plain.run(di, dk).cpu().numpy()
+    out = plan.new_output()
+    for _ in range(2):
+        out.fill_(float("nan"))
+        plan.run(di, dk, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref)
+    assert rel_l2(ref, oracle.conv_eq1(inp.numpy(), ker.numpy())) <= TOL["fp32_simt"]
+    xi, wi = make_inputs(shape, seed=52, kind="int")
+    goti = plan.run(xi.cuda(), wi.cuda()).cpu().numpy()
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
 @pytest.mark.parametrize("path", ["fp32_simt", "bf16"])
 def test_run_host_batched_planned_chunks(path):
     """The bench's e2e call: conv_run_host on the batched layer with the
