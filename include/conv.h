@@ -174,7 +174,11 @@ CONV_API conv_status conv_plan_set_path(conv_plan* plan, conv_path path);
  * path: ver, tk, tw, kg, pw, tn, th, bc, splits (split-C), flat (0/1: v2
  * row mode over whole images, TW = W in {7, 14}, Win % 4 == 0: each CTA's
  * 32*pw lanes take consecutive (image, row) slots of the flattened batch,
- * so no lane is padding; tn is then the images one In box spans and th = H).
+ * so no lane is padding; tn is then the images one In box spans and th = H),
+ * rem (0/1, flat tiles, default 1: the slot tiles that would start a mostly
+ * empty extra CTA per SM run as a second, small grid of 4-warp CTAs beside
+ * the main grid -- same arithmetic per output, bit-identical results;
+ * describe() reports the slot tiles it takes as tile.rem).
  * Unspecified keys keep the
  * selector's choice.  NULL or "" restores the selector's choice.
  * INVALID_ARGUMENT on a malformed spec, INFEASIBLE if the tile exceeds
@@ -189,9 +193,12 @@ CONV_API conv_status conv_plan_set_tile(conv_plan* plan, const char* spec);
  * Caller allocates, 256-B aligned. */
 CONV_API size_t conv_plan_workspace_bytes(const conv_plan* plan);
 
-/* Number of kernels one conv_run launches: 2 (one layout transform launch +
- * the main kernel), 3 for FP32 SIMT plans with a split-C reduction (the
- * splits' partial outputs summed in split order by a third kernel). */
+/* Number of timed stages of one conv_run (conv_run_events records one event
+ * around each): 2 (one layout transform launch + the main kernel), 3 for
+ * FP32 SIMT plans with a split-C reduction (the splits' partial outputs
+ * summed in split order by a third kernel).  An FP32 SIMT flat plan with a
+ * remainder grid (tile.rem > 0 in describe()) launches that grid and the main
+ * grid as one stage: two launches that run side by side. */
 CONV_API int conv_plan_num_kernels(const conv_plan* plan);
 
 /* Path the plan will run (never AUTO after create). */

@@ -70,6 +70,7 @@ struct conv_plan {
     static constexpr int kMaxChunks = 32;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {};
     int host_nch = 0;                           // image chunks of the pipeline (0: not planned yet)
+    SimtTile simt_host;                         // FP32 SIMT: the tile the pipeline's chunks run with (compute_host_chunks)
     int host_bounds[kMaxChunks + 1] = {};       // chunk j = images [host_bounds[j], host_bounds[j+1])
     ~conv_plan() {
         for (cudaStream_t s : {h2d, comp, d2h}) if (s) cudaStreamDestroy(s);
@@ -497,7 +498,7 @@ static const char* path_name(conv_path p) {
     }
 }
 
-static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_us);
+static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_us, SimtTile* host_tile);
 extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     if (!p) return -1;
     const Problem& pb = p->pb;
@@ -529,7 +530,8 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
     // conv_run_host's image chunks (plan_host_chunks) and their modeled time
     int hb[conv_plan::kMaxChunks + 1];
     double host_us = 0;
-    const int hn = compute_host_chunks(p, hb, &host_us);
+    SimtTile host_tile;
+    const int hn = compute_host_chunks(p, hb, &host_us, &host_tile);
     std::string chunks = "[";
     for (int j = 0; j < hn; ++j) chunks += (j ? "," : "") + std::to_string(hb[j + 1] - hb[j]);
     chunks += "]";
@@ -542,12 +544,12 @@ extern "C" int conv_plan_describe(const conv_plan* p, char* buf, size_t cap) {
         "\"hbm\":{\"dv_bytes\":%.12g,\"bw\":%.6g,\"us\":%.4f},"
         "\"compute\":{\"flops_issued_us\":%.4f,\"peak\":%.6g}},\"model_us\":%.4f},"
         "\"roofline\":{\"flops\":%.6g,\"compulsory_bytes\":%.6g,\"roofline_us\":%.4f},"
-        "\"host_pipeline\":{\"chunks\":%s,\"model_us\":%.4f},"
+        "\"host_pipeline\":{\"chunks\":%s,\"model_us\":%.4f,\"simt_kg\":%d},"
         "\"device\":{\"ordinal\":%d,\"sms\":%d,\"smem_optin\":%zu,\"l2_bytes\":%zu}}",
         pb.N, pb.K, pb.C, pb.H, pb.W, pb.R, pb.S, pb.U, pb.D, pb.ph, pb.pw, (long long)pb.Hin(), (long long)pb.Win(), path_name(p->path), tile.c_str(), ws_bytes(p),
         conv_plan_num_kernels(p), m.tiles, m.ctas, m.wave_eff, m.smem,
         m.dv_l2_smem, p->dev.bw_l2, m.t_l2_us, m.dv_hbm, p->dev.bw_hbm, m.t_hbm_us, m.t_comp_us, peak,
-        m.model_us, pb.flops(), comp_bytes, roof_us, chunks.c_str(), host_us, p->dev.ordinal, p->dev.sms, p->dev.smem_optin,
+        m.model_us, pb.flops(), comp_bytes, roof_us, chunks.c_str(), host_us, p->path == CONV_PATH_FP32_SIMT ? host_tile.kg : 0, p->dev.ordinal, p->dev.sms, p->dev.smem_optin,
         p->dev.l2_bytes);
     if (n < 0) return -1;
     if (buf && cap) {
@@ -569,11 +571,12 @@ static conv_status check_ptr(const void* ptr, const char* name, size_t align) {
 // workspace slice of those images and the shared Ker workspace are addressed
 // inside the plan's full workspace, so chunks never overlap.
 static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0, const float* in, const float* ker,
-                                  float* out, void* ws, cudaStream_t st, cudaEvent_t* evp) {
+                                  float* out, void* ws, cudaStream_t st, cudaEvent_t* evp,
+                                  const SimtTile* simt_tile = nullptr) {
     std::string err;
     cudaError_t e;
     if (p->path == CONV_PATH_FP32_SIMT) {
-        e = simt_run(sub, p->simt, in, ker, out, ws, st, evp, err, p->dev.sms);
+        e = simt_run(sub, simt_tile ? *simt_tile : p->simt, in, ker, out, ws, st, evp, err, p->dev.sms);
     } else {
         uint8_t* wsb = static_cast<uint8_t*>(ws);
         const size_t per_img = p->tcl.in_ws_bytes / (size_t)p->pb.N;
@@ -688,12 +691,12 @@ static const double kChunkOverheadUs = 6.0, kTcChunkOverheadUs = 30.0;
 // plus a fixed ~35 us (launch, Ker pack, ring fill and drain).  The chunk
 // estimate scales the full problem's model by that: a + (model - a) k/k_full.
 static const double kSimtChunkFixedUs = 35.0;
-static double model_run_us(const conv_plan* p, const Problem& sub) {
+static double model_run_us(const conv_plan* p, const SimtTile& st, const ModelResult& sm, const Problem& sub) {
     if (p->path == CONV_PATH_FP32_SIMT) {
         const int64_t sms = std::max(1, p->dev.sms);
-        const int64_t k_sub = (simt_ctas(sub, p->simt, sub.N) + sms - 1) / sms;
-        const int64_t k_full = std::max<int64_t>(1, (simt_ctas(p->pb, p->simt, p->pb.N) + sms - 1) / sms);
-        const double full = std::max(p->model.model_us, kSimtChunkFixedUs + 1.0);
+        const int64_t k_sub = (simt_ctas(sub, st, sub.N) + sms - 1) / sms;
+        const int64_t k_full = std::max<int64_t>(1, (simt_ctas(p->pb, st, p->pb.N) + sms - 1) / sms);
+        const double full = std::max(sm.model_us, kSimtChunkFixedUs + 1.0);
         return kSimtChunkFixedUs + (full - kSimtChunkFixedUs) * (double)k_sub / (double)k_full;
     }
     if (p->split) return model_tc(split_problem(sub, p->split), p->dev, true, p->tc).model_us;
@@ -701,7 +704,7 @@ static double model_run_us(const conv_plan* p, const Problem& sub) {
     return model_tc(sub, p->dev, p->path == CONV_PATH_BF16, p->tc).model_us;
 }
 
-static double simulate_host_pipeline(const conv_plan* p, const int* bounds, int nch) {
+static double simulate_host_pipeline(const conv_plan* p, const SimtTile& st, const ModelResult& sm, const int* bounds, int nch) {
     const Problem& pb = p->pb;
     const double img_in = 4.0 * pb.C * pb.Hin() * pb.Win(), img_out = 4.0 * pb.K * pb.H * pb.W;
     double th = 4.0 * pb.ker_elems() / kH2dBps * 1e6, tc = 0, td = 0;
@@ -713,7 +716,7 @@ static double simulate_host_pipeline(const conv_plan* p, const int* bounds, int 
         // (the tensor paths' per-chunk cost shows up on the whole pipeline,
         // measured; it is charged to the upload chain, which sets their pace)
         th += n * img_in / kH2dBps * 1e6 + (p->path == CONV_PATH_FP32_SIMT ? kChunkOverheadUs : kTcChunkOverheadUs);
-        tc = std::max(tc, th) + model_run_us(p, sub);
+        tc = std::max(tc, th) + model_run_us(p, st, sm, sub);
         // the last download has the link to itself (the uploads are done)
         const double d2h_bps = j == nch - 1 ? kD2hSoloBps : kD2hBps;
         td = std::max(td, tc) + n * img_out / d2h_bps * 1e6;
@@ -721,7 +724,7 @@ static double simulate_host_pipeline(const conv_plan* p, const int* bounds, int 
     return td;
 }
 
-static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_us) {
+static int compute_host_chunks_for(const conv_plan* p, const SimtTile& st, const ModelResult& sm, int* out_bounds, double* out_us) {
     const int N = p->pb.N;
     static const int env_chunks = [] { const char* e = getenv("CONV_HOST_CHUNKS"); return e ? atoi(e) : 0; }();
     auto equal = [&](int c, int* b) {
@@ -730,7 +733,7 @@ static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_
     if (env_chunks > 0) {                       // experiments: equal chunks
         const int c = std::min({env_chunks, N, (int)conv_plan::kMaxChunks});
         equal(c, out_bounds);
-        if (out_us) *out_us = simulate_host_pipeline(p, out_bounds, c);
+        if (out_us) *out_us = simulate_host_pipeline(p, st, sm, out_bounds, c);
         return c;
     }
     // CONV_HOST_SPLIT=a,b,... (study): explicit chunk sizes summing to N
@@ -747,16 +750,16 @@ static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_
             if (*q == ',') ++q;
         }
         if (c > 0 && sum == N) {
-            if (out_us) *out_us = simulate_host_pipeline(p, out_bounds, c);
+            if (out_us) *out_us = simulate_host_pipeline(p, st, sm, out_bounds, c);
             return c;
         }
     }
     int best[conv_plan::kMaxChunks + 1], cand[conv_plan::kMaxChunks + 1];
     int best_n = 1;
     equal(1, best);
-    double best_t = simulate_host_pipeline(p, best, 1);
+    double best_t = simulate_host_pipeline(p, st, sm, best, 1);
     auto consider = [&](int c) {
-        const double t = simulate_host_pipeline(p, cand, c);
+        const double t = simulate_host_pipeline(p, st, sm, cand, c);
         if (t < 0.995 * best_t) {               // a clear win only: fewer chunks on near-ties
             best_t = t;
             best_n = c;
@@ -774,17 +777,17 @@ static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_
     const bool simt = p->path == CONV_PATH_FP32_SIMT;
     {
         int wimg = 0;                           // images that fill the resident CTA slots once
-        if (p->path == CONV_PATH_FP32_SIMT && p->simt.flat) {
+        if (p->path == CONV_PATH_FP32_SIMT && st.flat) {
             // flat tiles: whole slot tiles (32*pw image rows) x k tiles per wave
-            const int64_t per_slot_tile = std::max<int64_t>(1, simt_ctas(p->pb, p->simt, 1) /
-                                                                   ((p->pb.H + 32 * p->simt.pw - 1) / (32 * p->simt.pw)));
-            const int64_t slot_tiles = std::max<int64_t>(1, p->model.ctas / per_slot_tile);
-            wimg = (int)std::max<int64_t>(1, slot_tiles * 32 * p->simt.pw / p->pb.H);
+            const int64_t per_slot_tile = std::max<int64_t>(1, simt_ctas(p->pb, st, 1) /
+                                                                   ((p->pb.H + 32 * st.pw - 1) / (32 * st.pw)));
+            const int64_t slot_tiles = std::max<int64_t>(1, sm.ctas / per_slot_tile);
+            wimg = (int)std::max<int64_t>(1, slot_tiles * 32 * st.pw / p->pb.H);
         } else if (p->path == CONV_PATH_FP32_SIMT) {
-            const int64_t per_ntile = simt_ctas(p->pb, p->simt, p->simt.tn);
-            wimg = (int)(std::max<int64_t>(1, p->model.ctas / std::max<int64_t>(1, per_ntile))) * p->simt.tn;
-        } else if (p->model.tiles > 0) {
-            wimg = (int)std::floor((double)p->model.ctas * N / (double)p->model.tiles);
+            const int64_t per_ntile = simt_ctas(p->pb, st, st.tn);
+            wimg = (int)(std::max<int64_t>(1, sm.ctas / std::max<int64_t>(1, per_ntile))) * st.tn;
+        } else if (sm.tiles > 0) {
+            wimg = (int)std::floor((double)sm.ctas * N / (double)sm.tiles);
         }
         for (int m = 1; wimg >= 1 && m <= 3; ++m) {
             const int mid = m * wimg;
@@ -823,7 +826,40 @@ static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_
     return best_n;
 }
 
-static void plan_host_chunks(conv_plan* p) { p->host_nch = compute_host_chunks(p, p->host_bounds, nullptr); }
+// The FP32 SIMT tile conv_run_host's chunks run with: the plan's tile, or --
+// for a flat tile of more than 4 k groups whose kg was not forced -- the
+// same tile with half the k groups when the modeled pipeline is shorter
+// with it (finer CTA waves give finer one-wave chunks; every unsplit tile
+// accumulates each output in the same order, so the results are the same
+// bits).  r02d, batched layer: the kg = 8 tile is faster on the device (1091
+// vs 1110 us) but its one-wave chunks are 84 images (e2e 2.00 ms) against 61
+// for kg = 4 (1.84 ms).
+static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_us, SimtTile* host_tile) {
+    double t0 = 0;
+    int n0 = compute_host_chunks_for(p, p->simt, p->model, out_bounds, &t0);
+    SimtTile use = p->simt;
+    if (p->path == CONV_PATH_FP32_SIMT && p->simt.flat && p->simt.kg > 4 && p->simt.kg % 2 == 0 &&
+        !(p->force_simt_mask & 4)) {
+        SimtTile h = p->simt;
+        h.kg /= 2;
+        if (simt_tile_supported(h) && simt_smem_bytes(p->pb, h) <= p->dev.smem_optin &&
+            simt_ws_bytes(p->pb, h) <= simt_ws_bytes(p->pb, p->simt)) {
+            const ModelResult mh = model_simt(p->pb, p->dev, h);
+            int b2[conv_plan::kMaxChunks + 1];
+            double t1 = 0;
+            const int n1 = compute_host_chunks_for(p, h, mh, b2, &t1);
+            if (t1 < t0) {
+                std::copy(b2, b2 + n1 + 1, out_bounds);
+                n0 = n1; t0 = t1; use = h;
+            }
+        }
+    }
+    if (out_us) *out_us = t0;
+    if (host_tile) *host_tile = use;
+    return n0;
+}
+
+static void plan_host_chunks(conv_plan* p) { p->host_nch = compute_host_chunks(p, p->host_bounds, nullptr, &p->simt_host); }
 
 extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, const float* ker_host,
                                      float* out_host, void* dbuf, void* stream) {
@@ -880,7 +916,8 @@ extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, 
         ok(cudaEventRecord(p->ev_h2d[j], p->h2d));
         ok(cudaStreamWaitEvent(p->comp, p->ev_h2d[j], 0));
         if (e != cudaSuccess) break;
-        s = launch_kernels(p, sub, n0, din + n0 * img_in, dker, dout + n0 * img_out, dws, p->comp, nullptr);
+        s = launch_kernels(p, sub, n0, din + n0 * img_in, dker, dout + n0 * img_out, dws, p->comp, nullptr,
+                           p->path == CONV_PATH_FP32_SIMT ? &p->simt_host : nullptr);
         if (s != CONV_OK) return s;
         ok(cudaEventRecord(p->ev_comp[j], p->comp));
         ok(cudaStreamWaitEvent(p->d2h, p->ev_comp[j], 0));

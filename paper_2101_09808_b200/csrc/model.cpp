@@ -591,7 +591,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     bool found = false;
     const int tks[2] = {4, 8};
     const int kgs[4] = {1, 2, 4, 8};   // (3, 5, 6: CTAs of 3-6 warps load the 4 SMSPs unevenly; flat r02c 1.2-1.3x slower)
-    const int bcs[4] = {2, 4, 8, 16};   // 2: flat tiles (or forced) only
+    const int bcs[6] = {2, 4, 8, 16, 6, 12};   // 2, 6, 12: forced only
     const int tn_max = std::min(pb.N, 16);
     // v2 first when it can run and nothing is forced; v1 only if no v2 tile fits
     const bool tile_forced = forced && (forced_mask & ~(256u | 1024u));   // a tile key other than splits / rem
@@ -628,7 +628,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         // 2-channel chunks and CTAs under 4 warps: forced only (flat r02c:
         // kg 2 / bc 2 1181 us vs kg 4 / bc 4 1163 on the batched layer, which
         // the model, blind to the per-chunk waits, ranked the other way)
-        if (bc == 2 && !(forced && (forced_mask & 64))) continue;
+        if ((bc == 2 || bc == 6 || bc == 12) && !(forced && (forced_mask & 64))) continue;
         if (t.flat && t.kg * t.pw < 4 && !tile_forced) continue;
         if (forced && (forced_mask & 1024)) t.rem = forced->rem;
         if (forced) {

@@ -165,6 +165,12 @@ def test_simt_remainder_launch_plan(lib):
     assert _offline(dataclasses.replace(sh, N=240), "fp32_simt", flat).describe()["tile"]["rem"] == 0
     # fewer CTAs than SMs: nothing to take off
     assert _offline(Shape(N=8, K=32, C=8, H=14, W=14, R=3, S=3), "fp32_simt", flat).describe()["tile"]["rem"] == 0
+    # conv_run_host runs its chunks with the finer kg = 4 flat tile (61-image one-wave chunks) while
+    # the device plan is the kg = 8 tile; a forced kg keeps the plan's tile
+    hp = d["host_pipeline"]
+    assert d["tile"]["kg"] == 8 and hp["simt_kg"] == 4 and sum(hp["chunks"]) == sh.N and max(hp["chunks"]) == 61, hp
+    hp8 = _offline(sh, "fp32_simt", "flat=1,tk=4,kg=8,pw=1,bc=4").describe()["host_pipeline"]
+    assert hp8["simt_kg"] == 8 and max(hp8["chunks"]) == 84, hp8
     # the modeled time with the remainder launch is below the one without
     with_rem = _offline(sh, "fp32_simt", flat).describe()["model"]["model_us"]
     without = _offline(sh, "fp32_simt", flat + ",rem=0").describe()["model"]["model_us"]
