@@ -177,7 +177,8 @@ CONV_API conv_status conv_plan_set_path(conv_plan* plan, conv_path path);
  * so no lane is padding; tn is then the images one In box spans and th = H),
  * rem (0/1, flat tiles, default 1: the slot tiles that would start a mostly
  * empty extra CTA per SM run as a second, small grid of 4-warp CTAs beside
- * the main grid -- same arithmetic per output, bit-identical results;
+ * the main grid -- same arithmetic per output, bit-identical results; with
+ * split-C it takes the same per-split channel ranges and partial slabs;
  * describe() reports the slot tiles it takes as tile.rem).
  * Unspecified keys keep the
  * selector's choice.  NULL or "" restores the selector's choice.

@@ -671,8 +671,12 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         const int ncand = forced ? 1 : 5;
         for (int ci = 0; ci < ncand; ++ci) {
             const int sp = cand[ci];
-            if (!forced && sp > 1 && (ctas * sp > 2L * dev.sms || sp > nchunks)) continue;
             t.splits = sp;
+            // (r02e: also a 2-way split of a larger flat grid when it brings the remainder launch --
+            // finer CTAs whose last round then runs beside the main grid; batched shards N = 32 / 64:
+            // 181 / 319 us vs 202 / 333 for the unsplit picks, profiles/r02e/remsplit/)
+            const bool flat_rem2 = t.flat && sp == 2 && ctas * sp <= 8L * dev.sms && simt_rem_tiles(pb, t, dev.sms) > 0;
+            if (!forced && sp > 1 && ((ctas * sp > 2L * dev.sms && !flat_rem2) || sp > nchunks)) continue;
             ModelResult r = model_simt(pb, dev, t);
             // near-ties (e.g. tiles at the chunk-latency floor): the tile that
             // issues less (r01b Y23: TK 8 vs 4 both modeled 656 us, measured

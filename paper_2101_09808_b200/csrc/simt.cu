@@ -848,8 +848,16 @@ SimtTile simt_rem_tile(const SimtTile& t) {
 
 int simt_rem_tiles(const Problem& pb, const SimtTile& t, int sms) {
     static const bool off = getenv("CONV_SIMT_NO_REM") != nullptr;   // A/B
-    if (off || !t.flat || !t.rem || t.ver != 2 || t.splits > 1 || t.pw != 1 || t.kg < 2 || sms < 1) return 0;
-    const int64_t ktiles = (pb.K + (int64_t)t.kg * t.tk - 1) / ((int64_t)t.kg * t.tk);
+    if (off || !t.flat || !t.rem || t.ver != 2 || t.pw != 1 || t.kg < 2 || sms < 1) return 0;
+    // split-C (r02e): a slot tile is k tiles x splits CTAs; the remainder grid takes the same
+    // channel ranges in its own 2-channel chunks (needs an even chunk depth) and writes the
+    // same partial slabs
+    const int64_t nchunks = (pb.C + t.bc - 1) / t.bc;
+    const int64_t splits = std::max<int64_t>(1, std::min<int64_t>(t.splits, nchunks));
+    const int64_t cper = (nchunks + splits - 1) / splits;
+    const int64_t zsplits = (nchunks + cper - 1) / cper;
+    if (zsplits > 1 && t.bc % 2 != 0) return 0;
+    const int64_t ktiles = (pb.K + (int64_t)t.kg * t.tk - 1) / ((int64_t)t.kg * t.tk) * zsplits;
     const int64_t tiles = ((int64_t)pb.N * pb.H + 31) / 32;           // slot tiles (pw = 1)
     const int64_t ctas = tiles * ktiles;
     const int64_t k = (ctas + sms - 1) / sms;
@@ -1080,7 +1088,7 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
         // before it starts, and waits for it at the end of each CTA, so that
         // the main grid's end implies the remainder grid's.  Per output the
         // arithmetic is the main tile's (same c, r, s order of fmaf).
-        const int rem = (L.tma && !grid2d && zsplits == 1) ? simt_rem_tiles(pb, t, sms) : 0;
+        const int rem = (L.tma && !grid2d) ? simt_rem_tiles(pb, t, sms) : 0;
         if (rem > 0) {
             const SimtTile ts = simt_rem_tile(t);
             const Simt2Layout Ls = simt2_layout(pb, ts);
@@ -1089,7 +1097,8 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
             qs.pitch = Ls.pitch; qs.istride = Ls.istride; qs.cstride = Ls.cstride; qs.plane = Ls.cstride;
             qs.in_stage = Ls.in_stage; qs.lpi = Ls.lpi; qs.stages = Ls.stages;
             qs.nchunks = (pb.C + ts.bc - 1) / ts.bc;
-            qs.cper = qs.nchunks;
+            // split-C: the main tile's channel range per split, in the remainder tile's chunks
+            qs.cper = zsplits > 1 ? q.cper * (t.bc / ts.bc) : qs.nchunks;
             qs.tx_in = (uint32_t)((size_t)box_imgs * ts.bc * Ls.rows_box * qs.pitch * sizeof(float));
             qs.solo = t.kg * t.tk / 4;                 // remainder CTAs per (slot tile, k tile): 4 channels each
             qs.tile0 = (int)grid.x / q.ktiles - rem;
@@ -1097,8 +1106,9 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
             CUtensorMap tmap_s;
             memset(&tmap_s, 0, sizeof(tmap_s));
             if (!encode(&tmap_s, Ls, ts.bc)) return cudaErrorInvalidValue;
-            e = dispatch_simt2(ts, pb.R, pb.S, true, in, kerp, kout, qs, tmap_s, dim3((unsigned)(rem * q.ktiles * qs.solo)),
-                               128, simt_smem_bytes(pb, ts), st);
+            e = dispatch_simt2(ts, pb.R, pb.S, true, in, kerp, kout, qs, tmap_s,
+                               dim3((unsigned)(rem * q.ktiles * qs.solo), 1, (unsigned)zsplits), 128,
+                               simt_smem_bytes(pb, ts), st);
             if (e != cudaSuccess) { err = std::string("SIMT remainder launch failed: ") + cudaGetErrorString(e); return e; }
             grid.x -= (unsigned)(rem * q.ktiles);
             q.nowait = 1; q.endwait = 1;

@@ -165,6 +165,10 @@ def test_simt_remainder_launch_plan(lib):
     assert _offline(dataclasses.replace(sh, N=240), "fp32_simt", flat).describe()["tile"]["rem"] == 0
     # fewer CTAs than SMs: nothing to take off
     assert _offline(Shape(N=8, K=32, C=8, H=14, W=14, R=3, S=3), "fp32_simt", flat).describe()["tile"]["rem"] == 0
+    # split-C: a slot tile is k tiles x splits CTAs (N = 32: 14 x 16 x 2 = 448, k = 4, 13 main tiles, 128 remainder CTAs);
+    # 4 splits would need 256 remainder CTAs: not taken
+    assert _offline(dataclasses.replace(sh, N=32), "fp32_simt", flat + ",splits=2").describe()["tile"]["rem"] == 1
+    assert _offline(dataclasses.replace(sh, N=32), "fp32_simt", flat + ",splits=4").describe()["tile"]["rem"] == 0
     # conv_run_host runs its chunks with the finer kg = 4 flat tile (61-image one-wave chunks) while
     # the device plan is the kg = 8 tile; a forced kg keeps the plan's tile
     hp = d["host_pipeline"]
@@ -460,7 +464,12 @@ def test_simt_staging_choice_offline(lib):
     d = _offline(dataclasses.replace(CONFIGS["batched"], N=128), "fp32_simt").describe()["tile"]
     assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["flat"], d["rem"], d["staging"]) == (2, 4, 14, 8, 14, 1, 1, "tma")
     d = _offline(dataclasses.replace(CONFIGS["batched"], N=64), "fp32_simt").describe()["tile"]
-    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["flat"], d["rem"], d["staging"]) == (2, 4, 14, 4, 14, 1, 1, "tma")
+    # r02e: the 64- and 32-image shards take a 2-way split-C flat tile with the remainder launch
+    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["splits"], d["flat"], d["rem"], d["staging"]) == \
+        (2, 4, 14, 8, 14, 2, 1, 1, "tma")
+    d = _offline(dataclasses.replace(CONFIGS["batched"], N=32), "fp32_simt").describe()["tile"]
+    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["splits"], d["flat"], d["rem"], d["staging"]) == \
+        (2, 4, 14, 4, 14, 2, 1, 1, "tma")
     for name in ("r2", "det", "tiny"):                       # Win = 58, 138, 10
         assert _offline(CONFIGS[name], "fp32_simt").describe()["tile"]["staging"] == "cp.async"
     sh = TABLE1["Y2"]                                        # Win = 272: a row wider than a TMA box

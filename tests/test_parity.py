@@ -512,6 +512,13 @@ SIMT_REM_CASES = [
     (Shape(N=267, K=32, C=6, H=9, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4", 2),
     # 3 rounds: 223 tiles x 2 = 446 CTAs, k = 4 -> 222 main tiles
     (Shape(N=509, K=32, C=4, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=2", 1),
+    # split-C (r02e): 38 slot tiles x 2 k tiles x 2 splits = 152 CTAs -> 37 main tiles + 1 remainder tile whose CTAs
+    # take the same channel ranges (12 + 10 of C = 22: ragged last chunk) in 2-channel chunks, into the same partial slabs
+    (Shape(N=86, K=32, C=22, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4,splits=2", 1),
+    # 3 splits of 2 + 2 + 1 chunks, 26 slot tiles x 2 x 3 = 156 CTAs -> 24 main + 2 remainder tiles
+    (Shape(N=58, K=32, C=20, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4,splits=3", 2),
+    # the batched layer's 8-GPU shard: 14 x 16 x 2 = 448 CTAs, k = 4 -> 13 main tiles (2.8 CTAs per SM) + 128 remainder CTAs
+    (Shape(N=32, K=256, C=256, H=14, W=14, R=3, S=3), "flat=1,tk=4,kg=4,pw=1,bc=4,splits=2", 1),
 ]
 
 
@@ -540,6 +547,31 @@ def test_simt_remainder_launch(shape, tile, rem):
     xi, wi = make_inputs(shape, seed=52, kind="int")
     goti = plan.run(xi.cuda(), wi.cuda()).cpu().numpy()
     assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_run_host_simt_split_remainder_shards(n):
+    """The batched layer's 8- and 4-GPU shards (r02e: 2-way split-C flat tiles
+    with the remainder launch): conv_run_host's chunks (each a sub-batch with
+    its own main / remainder grids and partial slabs) give the bits of
+    conv_run, which match the oracle on sampled images at 1e-5."""
+    import dataclasses
+    sh = dataclasses.replace(CONFIGS["batched"], N=n)
+    inp, ker = make_inputs(sh, seed=43)
+    plan = conv.ConvPlan(*sh.as_tuple(), path="fp32_simt")
+    t = plan.describe()["tile"]
+    assert t["flat"] == 1 and t["splits"] == 2 and t["rem"] == 1, t
+    dev_out = plan.run(inp.cuda(), ker.cuda()).cpu().numpy()
+    for i in (0, n // 2 + 1, n - 1):
+        assert rel_l2(dev_out[i:i + 1], oracle.conv_eq1(inp.numpy()[i:i + 1], ker.numpy())) <= TOL["fp32_simt"]
+    dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device="cuda")
+    ih, kh = inp.pin_memory(), ker.pin_memory()
+    out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        out_h.fill_(float("nan"))
+        plan.run_host(ih, kh, out_h, dbuf)
+        torch.cuda.synchronize()
+        assert np.array_equal(out_h.numpy(), dev_out)
 
 
 @pytest.mark.parametrize("path", ["fp32_simt", "bf16"])
