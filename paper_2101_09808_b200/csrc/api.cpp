@@ -842,6 +842,7 @@ static int compute_host_chunks(const conv_plan* p, int* out_bounds, double* out_
         !(p->force_simt_mask & 4)) {
         SimtTile h = p->simt;
         h.kg /= 2;
+        if (h.bc == 6) h.bc = 4;                // 6-channel chunks would cost the kg = 4 tile a resident CTA (r02e)
         if (simt_tile_supported(h) && simt_smem_bytes(p->pb, h) <= p->dev.smem_optin &&
             simt_ws_bytes(p->pb, h) <= simt_ws_bytes(p->pb, p->simt)) {
             const ModelResult mh = model_simt(p->pb, p->dev, h);

@@ -560,7 +560,11 @@ ModelResult model_simt(const Problem& pb, const Device& dev, const SimtTile& t) 
     const double issue_cyc = (double)conc * (fma_chunk_cta + copy_chunk_cta) / (128.0 * eff);
     // (+ a per-chunk synchronisation charge: a study knob, default 0 --
     // see the bc tie-break in select_simt)
-    const double chunk_cyc = std::max(issue_cyc, 2000.0) + kSimtChunkSyncClk;
+    // Flat tiles are charged ~400 clk per chunk round (r02e, profiles/r02e/bc6/: on the kg = 8 flat
+    // tile 6-channel chunks -- 43 ring waits / barriers per CTA instead of 64 -- run 1074 vs 1088 us at
+    // N = 256, 567 vs 574 at N = 128, 319 vs 321 at N = 64: 14 us / (3 CTA rounds x 21 chunks) ~ 440 clk)
+    static const double kSimtFlatChunkSyncClk = getenv("CONV_SIMT_FLAT_SYNC") ? atof(getenv("CONV_SIMT_FLAT_SYNC")) : 400.0;
+    const double chunk_cyc = std::max(issue_cyc, 2000.0) + kSimtChunkSyncClk + (t.flat ? kSimtFlatChunkSyncClk : 0.0);
     // v2 (FFMA2): the time goes with the CTAs each SM runs, not with whole
     // waves -- measured r02b (profiles/r02b/e2e/simt_time_vs_batch.txt,
     // shard_tiles.txt): the batched tile at N = 6..256 takes 35 + 85 k us for
@@ -591,7 +595,7 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
     bool found = false;
     const int tks[2] = {4, 8};
     const int kgs[4] = {1, 2, 4, 8};   // (3, 5, 6: CTAs of 3-6 warps load the 4 SMSPs unevenly; flat r02c 1.2-1.3x slower)
-    const int bcs[6] = {2, 4, 8, 16, 6, 12};   // 2, 6, 12: forced only
+    const int bcs[6] = {2, 4, 8, 16, 6, 12};   // 2, 12 (and 6 on other than flat tiles): forced only
     const int tn_max = std::min(pb.N, 16);
     // v2 first when it can run and nothing is forced; v1 only if no v2 tile fits
     const bool tile_forced = forced && (forced_mask & ~(256u | 1024u));   // a tile key other than splits / rem
@@ -628,7 +632,8 @@ bool select_simt(const Problem& pb, const Device& dev, SimtTile& best, ModelResu
         // 2-channel chunks and CTAs under 4 warps: forced only (flat r02c:
         // kg 2 / bc 2 1181 us vs kg 4 / bc 4 1163 on the batched layer, which
         // the model, blind to the per-chunk waits, ranked the other way)
-        if ((bc == 2 || bc == 6 || bc == 12) && !(forced && (forced_mask & 64))) continue;
+        // (6-channel chunks: flat tiles only, r02e)
+        if ((bc == 2 || bc == 12 || (bc == 6 && !t.flat)) && !(forced && (forced_mask & 64))) continue;
         if (t.flat && t.kg * t.pw < 4 && !tile_forced) continue;
         if (forced && (forced_mask & 1024)) t.rem = forced->rem;
         if (forced) {

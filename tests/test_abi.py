@@ -460,9 +460,10 @@ def test_simt_staging_choice_offline(lib):
     from paper_2101_09808_b200.inputs import CONFIGS, TABLE1
     d = _offline(CONFIGS["batched"], "fp32_simt").describe()["tile"]
     assert (d["ver"], d["tk"], d["tw"], d["kg"], d["tn"], d["th"], d["bc"], d["flat"], d["rem"], d["staging"]) == \
-        (2, 4, 14, 8, 4, 14, 4, 1, 1, "tma")
+        (2, 4, 14, 8, 4, 14, 6, 1, 1, "tma")       # r02e: 6-channel chunks on the kg = 8 flat tile
     d = _offline(dataclasses.replace(CONFIGS["batched"], N=128), "fp32_simt").describe()["tile"]
-    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["flat"], d["rem"], d["staging"]) == (2, 4, 14, 8, 14, 1, 1, "tma")
+    assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["bc"], d["flat"], d["rem"], d["staging"]) == \
+        (2, 4, 14, 8, 14, 6, 1, 1, "tma")
     d = _offline(dataclasses.replace(CONFIGS["batched"], N=64), "fp32_simt").describe()["tile"]
     # r02e: the 64- and 32-image shards take a 2-way split-C flat tile with the remainder launch
     assert (d["ver"], d["tk"], d["tw"], d["kg"], d["th"], d["splits"], d["flat"], d["rem"], d["staging"]) == \
