@@ -789,7 +789,10 @@ Simt2Layout simt2_layout(const Problem& pb, const SimtTile& t) {
     static const bool no_tma = getenv("CONV_SIMT_NO_TMA") != nullptr;
     static const int env_stages = getenv("CONV_SIMT_STAGES") ? atoi(getenv("CONV_SIMT_STAGES")) : 0;
     L.tma = !no_tma && t.ver == 2 && simt_v2_ok(pb) && pb.Win() % 4 == 0 && L.pitch <= 256 && rows_in <= 256 &&
-            t.bc <= 256 && t.tn <= 256 && (pb.R == 1 || pb.R == 3) && (t.flat || t.tn * lpi8 <= 32 * t.pw);
+            t.bc <= 256 && t.tn <= 256 && pb.R == pb.S && (pb.S == 1 || pb.S == 3) &&   // the compiled TMA instances
+            (t.flat || t.tn * lpi8 <= 32 * t.pw);                                       // (dispatch_simt2): 1x1 and 3x3 taps
+    // (r02e fuzz: the test was R in {1, 3}, which let 1x3 problems with Win % 4 == 0 plan a TMA tile that no
+    // instance runs -- the launch failed with invalid argument; they take the cp.async layout now)
     // (flat tiles: a 2-deep ring by default -- their boxes carry the zero
     // rows up to rows_box, and 3 stages would cost a resident CTA per SM)
     L.stages = L.tma && env_stages >= 2 && env_stages <= kSimt2MaxStages ? env_stages : t.flat ? 2 : kSimt2Stages;
@@ -849,6 +852,9 @@ SimtTile simt_rem_tile(const SimtTile& t) {
 int simt_rem_tiles(const Problem& pb, const SimtTile& t, int sms) {
     static const bool off = getenv("CONV_SIMT_NO_REM") != nullptr;   // A/B
     if (off || !t.flat || !t.rem || t.ver != 2 || t.pw != 1 || t.kg < 2 || sms < 1) return 0;
+    // the remainder instance is compiled for 3x3 taps and 14-pixel rows only (dispatch_simt2); other flat
+    // problems (W = 14, S = 3, R != 3) run the main grid alone (r02e fuzz: the launch failed with R = 1, 2, 5)
+    if (pb.R != 3 || pb.S != 3 || t.tw != 14 || t.tk != 4) return 0;
     // split-C (r02e): a slot tile is k tiles x splits CTAs; the remainder grid takes the same
     // channel ranges in its own 2-channel chunks (needs an even chunk depth) and writes the
     // same partial slabs

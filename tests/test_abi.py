@@ -165,6 +165,12 @@ def test_simt_remainder_launch_plan(lib):
     assert _offline(dataclasses.replace(sh, N=240), "fp32_simt", flat).describe()["tile"]["rem"] == 0
     # fewer CTAs than SMs: nothing to take off
     assert _offline(Shape(N=8, K=32, C=8, H=14, W=14, R=3, S=3), "fp32_simt", flat).describe()["tile"]["rem"] == 0
+    # 1x3 taps: the TMA staging (and with it flat tiles and the remainder launch) has 1x1 / 3x3 instances only
+    sh13 = Shape(N=171, K=32, C=8, H=14, W=14, R=1, S=3)
+    assert _offline(sh13, "fp32_simt").describe()["tile"]["staging"] == "cp.async"
+    with pytest.raises(conv.ConvError):
+        _offline(sh13, "fp32_simt", flat)
+    assert _offline(Shape(N=171, K=32, C=8, H=14, W=14, R=3, S=3), "fp32_simt", flat).describe()["tile"]["rem"] == 1
     # split-C: a slot tile is k tiles x splits CTAs (N = 32: 14 x 16 x 2 = 448, k = 4, 13 main tiles, 128 remainder CTAs);
     # 4 splits would need 256 remainder CTAs: not taken
     assert _offline(dataclasses.replace(sh, N=32), "fp32_simt", flat + ",splits=2").describe()["tile"]["rem"] == 1

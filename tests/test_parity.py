@@ -549,6 +549,24 @@ def test_simt_remainder_launch(shape, tile, rem):
     assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
 
 
+@pytest.mark.parametrize("shape", [Shape(N=171, K=32, C=8, H=14, W=14, R=1, S=3), Shape(N=3, K=30, C=5, H=16, W=14, R=1, S=3),
+                                   Shape(N=2, K=16, C=8, H=9, W=10, R=1, S=3), Shape(N=2, K=16, C=8, H=9, W=12, R=3, S=1)],
+                         ids=lambda sh: "x".join(map(str, sh.as_tuple())))
+def test_simt_non_square_taps_with_tma_aligned_rows(shape):
+    """R != S with Win % 4 == 0 (r02e fuzz regression): the TMA staging has
+    instances for 1x1 and 3x3 taps only; such problems planned a TMA tile whose
+    launch failed with invalid argument.  They take the cp.async layout (or
+    v1), and match the oracle -- 1e-5, integer twin exact."""
+    plan = conv.ConvPlan(*shape.as_tuple(), path="fp32_simt")
+    assert plan.describe()["tile"]["staging"] == "cp.async"
+    inp, ker = make_inputs(shape, seed=61)
+    got = plan.run(inp.cuda(), ker.cuda()).cpu().numpy()
+    assert rel_l2(got, oracle.conv_eq1(inp.numpy(), ker.numpy())) <= TOL["fp32_simt"]
+    xi, wi = make_inputs(shape, seed=62, kind="int")
+    goti = plan.run(xi.cuda(), wi.cuda()).cpu().numpy()
+    assert np.array_equal(goti.astype(np.float64), oracle.conv_eq1(xi.numpy(), wi.numpy()))
+
+
 @pytest.mark.parametrize("n", [32, 64])
 def test_run_host_simt_split_remainder_shards(n):
     """The batched layer's 8- and 4-GPU shards (r02e: 2-way split-C flat tiles
