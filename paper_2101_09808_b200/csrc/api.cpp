@@ -66,14 +66,14 @@ struct conv_plan {
     unsigned force_simt_mask = 0;
     // conv_run_host pipeline (created on first use, guarded by host_mu)
     std::mutex host_mu;
-    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    cudaStream_t h2d = nullptr, comp = nullptr, comp2 = nullptr, d2h = nullptr;   // comp2: FP32 SIMT chunks alternate
     static constexpr int kMaxChunks = 32;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {};
     int host_nch = 0;                           // image chunks of the pipeline (0: not planned yet)
     SimtTile simt_host;                         // FP32 SIMT: the tile the pipeline's chunks run with (compute_host_chunks)
     int host_bounds[kMaxChunks + 1] = {};       // chunk j = images [host_bounds[j], host_bounds[j+1])
     ~conv_plan() {
-        for (cudaStream_t s : {h2d, comp, d2h}) if (s) cudaStreamDestroy(s);
+        for (cudaStream_t s : {h2d, comp, comp2, d2h}) if (s) cudaStreamDestroy(s);
         for (cudaEvent_t e : {ev_start, ev_end}) if (e) cudaEventDestroy(e);
         for (int i = 0; i < kMaxChunks; ++i) {
             if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
@@ -572,11 +572,11 @@ static conv_status check_ptr(const void* ptr, const char* name, size_t align) {
 // inside the plan's full workspace, so chunks never overlap.
 static conv_status launch_kernels(const conv_plan* p, const Problem& sub, int n0, const float* in, const float* ker,
                                   float* out, void* ws, cudaStream_t st, cudaEvent_t* evp,
-                                  const SimtTile* simt_tile = nullptr) {
+                                  const SimtTile* simt_tile = nullptr, bool simt_skip_pack = false) {
     std::string err;
     cudaError_t e;
     if (p->path == CONV_PATH_FP32_SIMT) {
-        e = simt_run(sub, simt_tile ? *simt_tile : p->simt, in, ker, out, ws, st, evp, err, p->dev.sms);
+        e = simt_run(sub, simt_tile ? *simt_tile : p->simt, in, ker, out, ws, st, evp, err, p->dev.sms, simt_skip_pack);
     } else {
         uint8_t* wsb = static_cast<uint8_t*>(ws);
         const size_t per_img = p->tcl.in_ws_bytes / (size_t)p->pb.N;
@@ -891,6 +891,7 @@ extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, 
     if (!p->h2d) {
         ok(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
         ok(cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking));
+        ok(cudaStreamCreateWithFlags(&p->comp2, cudaStreamNonBlocking));
         ok(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
         ok(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
         ok(cudaEventCreateWithFlags(&p->ev_end, cudaEventDisableTiming));
@@ -904,23 +905,38 @@ extern "C" conv_status conv_run_host(const conv_plan* cp, const float* in_host, 
     ok(cudaEventRecord(p->ev_start, st));
     ok(cudaStreamWaitEvent(p->h2d, p->ev_start, 0));
     ok(cudaStreamWaitEvent(p->comp, p->ev_start, 0));
+    ok(cudaStreamWaitEvent(p->comp2, p->ev_start, 0));
     ok(cudaStreamWaitEvent(p->d2h, p->ev_start, 0));
     ok(cudaMemcpyAsync(dker, ker_host, bk, cudaMemcpyHostToDevice, p->h2d));
     const int64_t img_in = (int64_t)pb.C * pb.Hin() * pb.Win(), img_out = (int64_t)pb.K * pb.H * pb.W;
-    int n0 = 0;
+    // Study knob CONV_HOST_TWO_COMP=1 (r02e, FP32 SIMT without split-C): the chunks' kernels alternate
+    // between two compute streams, so that a chunk's CTAs fill the SMs while the previous chunk's last
+    // ones drain.  Ker is packed once, by the first chunk -- the later chunks skip the pack and read the
+    // same packed copy, the second stream starts behind the first chunk -- and nothing else in the
+    // workspace is shared (split-C partial slabs would be: those plans keep one compute stream); each
+    // output is still one CTA's own sequence of FMAs: the same bits (fuzz_run_host.py, 480 runs).
+    // Measured on the batched layer (profiles/r02e/e2e/two_comp_ab.txt, three passes): 1.87 vs 1.85 ms
+    // with the planned chunks, 1.79 vs 1.82 with a tapered tail, 1.99 vs 2.07 with 30-image chunks --
+    // no gain for the plan, so the single compute stream stays the default.
+    static const bool two_env = getenv("CONV_HOST_TWO_COMP") != nullptr;
+    const bool two_comp = two_env && p->path == CONV_PATH_FP32_SIMT && p->simt_host.splits <= 1 && nch >= 3;
+    int n0 = 0, launched = 0;
     for (int j = 0; j < nch && e == cudaSuccess; ++j) {
         const int n1 = bounds[j + 1];
         if (n1 == n0) continue;
         Problem sub = pb;
         sub.N = n1 - n0;
+        cudaStream_t cs = (two_comp && (launched & 1)) ? p->comp2 : p->comp;
         ok(cudaMemcpyAsync(din + n0 * img_in, in_host + n0 * img_in, 4 * sub.N * img_in, cudaMemcpyHostToDevice, p->h2d));
         ok(cudaEventRecord(p->ev_h2d[j], p->h2d));
-        ok(cudaStreamWaitEvent(p->comp, p->ev_h2d[j], 0));
+        ok(cudaStreamWaitEvent(cs, p->ev_h2d[j], 0));
         if (e != cudaSuccess) break;
-        s = launch_kernels(p, sub, n0, din + n0 * img_in, dker, dout + n0 * img_out, dws, p->comp, nullptr,
-                           p->path == CONV_PATH_FP32_SIMT ? &p->simt_host : nullptr);
+        s = launch_kernels(p, sub, n0, din + n0 * img_in, dker, dout + n0 * img_out, dws, cs, nullptr,
+                           p->path == CONV_PATH_FP32_SIMT ? &p->simt_host : nullptr, two_comp && launched > 0);
         if (s != CONV_OK) return s;
-        ok(cudaEventRecord(p->ev_comp[j], p->comp));
+        ok(cudaEventRecord(p->ev_comp[j], cs));
+        if (two_comp && launched == 0) ok(cudaStreamWaitEvent(p->comp2, p->ev_comp[j], 0));   // packed Ker complete
+        ++launched;
         ok(cudaStreamWaitEvent(p->d2h, p->ev_comp[j], 0));
         ok(cudaMemcpyAsync(out_host + n0 * img_out, dout + n0 * img_out, 4 * sub.N * img_out, cudaMemcpyDeviceToHost, p->d2h));
         n0 = n1;

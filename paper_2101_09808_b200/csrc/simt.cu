@@ -977,7 +977,7 @@ size_t simt_ws_bytes(const Problem& pb, const SimtTile& t) {
 }
 
 cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, const float* ker,
-                     float* out, void* ws, cudaStream_t st, cudaEvent_t* ev, std::string& err, int sms) {
+                     float* out, void* ws, cudaStream_t st, cudaEvent_t* ev, std::string& err, int sms, bool skip_pack) {
     SimtParams p;
     p.N = pb.N; p.K = pb.K; p.C = pb.C; p.H = pb.H; p.W = pb.W; p.R = pb.R; p.S = pb.S; p.U = pb.U; p.D = pb.D;
     p.Hin = (int)pb.Hin(); p.Win = (int)pb.Win(); p.HW = pb.H * pb.W; p.RS = pb.R * pb.S;
@@ -1012,7 +1012,9 @@ cudaError_t simt_run(const Problem& pb, const SimtTile& t, const float* in, cons
     static const int gather_env = getenv("CONV_SIMT_PACK_GATHER") ? atoi(getenv("CONV_SIMT_PACK_GATHER")) : -1;
     const bool gather = gather_env == 1 ||
                         (gather_env != 0 && (pb.C * p.RS) % 4 != 0 && total < (int64_t)1 << 18);
-    if (gather || p.bko > 1024) {
+    // skip_pack (conv_run_host's later chunks): the workspace already holds this tile's packed Ker
+    if (skip_pack) {
+    } else if (gather || p.bko > 1024) {
         pack_ker_simt<<<pblocks, 256, 0, st>>>(ker, kerp, pb.K, pb.C, p.RS, p.bko, total);
     } else {
         const int crs = pb.C * p.RS;
