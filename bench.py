@@ -219,13 +219,45 @@ class GpuEngine:
                 "per_kernel": per_kernel, "clocks": clocks.summary(), "out": d_out, "nk": nk,
                 "launch": "cuda_graph replay of conv_run" if graph is not None else "stream launches"}
 
+    def gpu_local_cpus(self):
+        """CPUs NVML names as local to this GPU (its NUMA node), within the
+        process's allowed set; None if unknown."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            props = torch.cuda.get_device_properties(self.dev)
+            try:
+                bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.dev.index or 0)
+            words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+            cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+            cpus &= os.sched_getaffinity(0)
+            return cpus or None
+        except Exception:
+            return None
+
     def e2e(self, res, sh, in_h, ker_h, args, barrier):
         """conv_run_host with pinned host buffers: H2D + conv + D2H inside the
-        event pair, every step."""
+        event pair, every step.  The pinned buffers are allocated (first
+        touched) with the thread on the GPU's local CPUs (--cpu-affinity gpu,
+        the default: host pages on the GPU's NUMA node), then the affinity is
+        restored for the other legs."""
         plan = res["plan"]
-        in_h, ker_h = in_h.pin_memory(), ker_h.pin_memory()
+        prev = os.sched_getaffinity(0)
+        local = self.gpu_local_cpus() if args.cpu_affinity == "gpu" else None
+        if local:
+            os.sched_setaffinity(0, local)
+        self.e2e_affinity = f"gpu-local ({len(local)} of {len(prev)} cpus)" if local else "process default"
+        try:
+            in_h, ker_h = in_h.clone().pin_memory(), ker_h.clone().pin_memory()
+            out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
+            out_h.zero_()
+        finally:
+            if local:
+                os.sched_setaffinity(0, prev)
         dbuf = torch.empty(plan.host_run_bytes, dtype=torch.uint8, device=self.dev)
-        out_h = torch.empty(sh.out_shape, dtype=torch.float32).pin_memory()
         for _ in range(max(1, args.warmup)):
             plan.run_host(in_h, ker_h, out_h, dbuf)
         self.sync()
@@ -433,6 +465,7 @@ def build_line(args, world, full, spec, paths, results, e2e_ms, g_ms, p10, engin
             "h2d_bytes_per_step": 4 * (sh.N * sh.C * sh.Hin * sh.Win + sh.K * sh.C * sh.R * sh.S) * world,
             "d2h_bytes_per_step": 4 * sh.N * sh.K * sh.H * sh.W * world,
             "api": "conv_run_host (C ABI, pinned host buffers)" + (", every rank its slab" if world > 1 else ""),
+            "host_buffers": getattr(engine, "e2e_affinity", None),
         }
     others = [p for p in paths if p != args.path]
     if others:
@@ -654,6 +687,8 @@ def main():
     ap.add_argument("--shard", default="auto", choices=["auto", "n", "k"],
                     help="strong scaling: shard the batch n (auto for N >= ranks) or output channels k (N = 1)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-affinity", choices=["gpu", "none"], default="gpu",
+                    help="e2e leg: allocate the pinned host buffers from the GPU's local CPUs (NUMA node)")
     ap.add_argument("--no-check", action="store_true", help="skip the multi-rank P10 slab check")
     ap.add_argument("--config", default="batched", choices=list(CONFIGS))
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
